@@ -1,0 +1,183 @@
+/* hbgpu.h — C ABI of the B200-native HB-GLS hot path (libhbgpu.so).
+ *
+ * Drop-in boundary for the reference solver's hot-path calls
+ * (reference = /root/reference/proj, C++20 CPU code).  Each entry point names
+ * the reference interface it replaces.  A C++ adapter with the reference's
+ * exact signatures forwards to these functions, so
+ * solve_harmonic (src/hb_solver.cpp:113-221) is the only call-site change.
+ *
+ * Conventions
+ *  - Plain pointers and sizes; no C++ or torch types.  Host buffers unless a
+ *    function name ends in _dev (device pointers, ordered on the context's
+ *    CUDA stream, see hbgpu_stream()).
+ *  - Layouts are the reference's:
+ *      state / residual   (node*4 + comp)*N + n, comp 3 = pressure  (assembly.hpp:25-47)
+ *      dirichlet_g        (node*3 + i)*N + n                         (assembly.hpp:52-54)
+ *      geometry           22 doubles per element = ElementGeometry  (mesh.hpp:26-34)
+ *      BSR values         (blk*8 + slot)*N + n, slots K|G1..3|D1..3|L (linalg.hpp:30-51)
+ *      pattern            CSR row_ptr[nn+1], col_idx[nnz], sorted    (linalg.hpp:14-23)
+ *  - Every function returns an hbgpu_status; the adapter rethrows the
+ *    matching reference exception (errors.hpp, std::invalid_argument,
+ *    std::domain_error).  hbgpu_last_error() gives the message.
+ *  - A context is not thread-safe (one solve owns it); the
+ *    reference's `threads` arguments have no GPU meaning and are not taken.
+ *  - No CPU fallback: creating a context without a usable sm_100 device fails
+ *    with HBGPU_ERR_CUDA.
+ */
+#ifndef HBGPU_H
+#define HBGPU_H
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    HBGPU_OK = 0,
+    HBGPU_ERR_INVALID = 1,     /* std::invalid_argument (linalg.cpp:45-46,81-82) */
+    HBGPU_ERR_DOMAIN = 2,      /* std::domain_error, singular tau (assembly.cpp:51-53) */
+    HBGPU_ERR_GEOMETRY = 3,    /* GeometryError (mesh.cpp:173-174) */
+    HBGPU_ERR_PARSE = 4,       /* ParseError (spectral.cpp:19-22) */
+    HBGPU_ERR_STAGNATION = 5,  /* StagnationError (hb_solver.cpp:200-203) */
+    HBGPU_ERR_DIVERGENCE = 6,  /* DivergenceError (hb_solver.cpp:165-186) */
+    HBGPU_ERR_CUDA = 7,
+    HBGPU_ERR_OOM = 8
+} hbgpu_status;
+
+typedef struct hbgpu_ctx hbgpu_ctx;
+
+/* Mesh after Mesh::finalize (mesh.cpp:60-157): oriented elements and facets,
+ * outward unit normals and facet areas, Dirichlet node mask.  `geometry` may
+ * be the reference's std::vector<ElementGeometry>::data() (zero-copy); when
+ * NULL it is computed on the device from xyz (element_geometry, mesh.cpp:159-203). */
+typedef struct {
+    int num_nodes;
+    int num_elements;
+    const double* xyz;                /* nn*3; may be NULL when geometry is given */
+    const int* conn;                  /* ne*4 */
+    const double* geometry;           /* ne*22 or NULL */
+    const unsigned char* dirichlet;   /* nn, Mesh::is_dirichlet_node */
+    int num_patches;
+    const int* patch_kind;            /* 0 = Dirichlet, 1 = Neumann */
+    const int* patch_num_facets;
+    const int* facets;                /* sum(patch_num_facets)*3, patch-major */
+    const double* normals;            /* same count * 3 */
+    const double* areas;              /* same count */
+} hbgpu_mesh_desc;
+
+/* Uploads the mesh, builds NodePattern (linalg.cpp:10-30) and the device
+ * incidence structures.  Returns NULL on failure (*status says why). */
+hbgpu_ctx* hbgpu_create(const hbgpu_mesh_desc* mesh, int* status);
+void hbgpu_destroy(hbgpu_ctx* ctx);
+const char* hbgpu_last_error(const hbgpu_ctx* ctx);
+/* Message of the last failed hbgpu_create on this thread. */
+const char* hbgpu_create_error(void);
+/* cudaStream_t of the context, as void*. */
+void* hbgpu_stream(hbgpu_ctx* ctx);
+int hbgpu_synchronize(hbgpu_ctx* ctx);
+
+/* SpectralBasis(M, T) (spectral.cpp:18-27) + SpectralOperators (H = E^-1 Omega E,
+ * spectral.cpp:146-164,236-256), applied as a dense N x N matrix on device. */
+int hbgpu_set_basis(hbgpu_ctx* ctx, int modes, double period);
+/* FluidProperties (assembly.hpp:17-23); validate() semantics (assembly.cpp:38-41). */
+int hbgpu_set_fluid(hbgpu_ctx* ctx, double rho, double mu);
+/* BoundaryConditionSet (assembly.hpp:50-60): dirichlet_g nn*3*N (may be NULL =
+ * zeros), Neumann list (patch index, h[N] each, h is n_neumann*N), backflow beta. */
+int hbgpu_set_bcs(hbgpu_ctx* ctx, const double* dirichlet_g, int n_neumann,
+                  const int* neumann_patch, const double* neumann_h, double backflow_beta);
+/* AssemblyConfig (assembly.hpp:64-70): tau_mode 0 = QuadraturePoint, 1 = ElementMean;
+ * pseudo_dt <= 0 or non-finite = infinity (no pseudo-time term). */
+int hbgpu_set_assembly_config(hbgpu_ctx* ctx, int tau_mode, double pseudo_dt, double pseudo_c1,
+                              int backflow_in_tangent);
+
+/* Sizes: nodes, elements, time points N, pattern nnz, state length nn*4*N. */
+int hbgpu_sizes(const hbgpu_ctx* ctx, int* num_nodes, int* num_elements, int* time_points,
+                long long* nnz, long long* state_len);
+/* NodePattern export (bit-exact target vs linalg.cpp:10-30). */
+int hbgpu_get_pattern(hbgpu_ctx* ctx, int* row_ptr, int* col_idx);
+/* Device-computed ElementGeometry (22 doubles per element). */
+int hbgpu_get_geometry(hbgpu_ctx* ctx, double* geometry);
+
+/* ---- drop-ins (host buffers) ------------------------------------------ */
+
+/* assemble_residual (assembly.hpp:129-134, assembly.cpp:443-548). */
+int hbgpu_assemble_residual(hbgpu_ctx* ctx, const double* state, double* residual);
+/* assemble_tangent (assembly.hpp:138-141, assembly.cpp:550-666).  P stays on
+ * the device for hbgpu_matvec / hbgpu_jacobi / hbgpu_gmres; pvals may be NULL. */
+int hbgpu_assemble_tangent(hbgpu_ctx* ctx, const double* state, double* pvals);
+/* assemble_mass (assembly.hpp:145-146, assembly.cpp:668-681).  Kept on device; mass may be NULL. */
+int hbgpu_assemble_mass(hbgpu_ctx* ctx, double* mass);
+/* Replace the device P values (e.g. a P assembled elsewhere), nnz*8*N doubles. */
+int hbgpu_set_pvals(hbgpu_ctx* ctx, const double* pvals);
+/* TangentOperator::matvec (linalg.hpp:75, linalg.cpp:78-128): out = (P + H (x) mass) y. */
+int hbgpu_matvec(hbgpu_ctx* ctx, const double* y, double* out);
+/* BlockSparseMatrix::matvec, accumulate = false (linalg.hpp:55-57, linalg.cpp:41-76). */
+int hbgpu_bsr_matvec(hbgpu_ctx* ctx, const double* y, double* out);
+/* jacobi_preconditioner (linalg.hpp:84, linalg.cpp:130-154).  Stored on device;
+ * inv_diag may be NULL. */
+int hbgpu_jacobi(hbgpu_ctx* ctx, double* inv_diag, int* degenerate_entries);
+
+typedef struct {
+    int restart;       /* KrylovConfig (linalg.hpp:86-90): 200 */
+    int max_iters;     /* 1000 */
+    double tolerance;  /* 0.03, relative, of the split-scaled system */
+} hbgpu_krylov_cfg;
+
+typedef struct {
+    int iterations;
+    double relative_residual;
+    int status;        /* KrylovStatus: 0 Converged, 1 MaxIterations, 2 Stagnated */
+    int history_len;   /* entries written to `history` (<= capacity) */
+} hbgpu_krylov_result;
+
+/* gmres_solve(TangentOperator, rhs, JacobiPreconditioner, cfg)
+ * (linalg.hpp:102-115, linalg.cpp:167-293) with the device operator.
+ * inv_diag NULL = the context's current Jacobi vector. */
+int hbgpu_gmres(hbgpu_ctx* ctx, const double* rhs, const double* inv_diag,
+                const hbgpu_krylov_cfg* cfg, double* x, hbgpu_krylov_result* result,
+                double* history, int history_capacity);
+
+/* ---- device-resident fast path (device pointers, ctx stream) ----------- */
+int hbgpu_assemble_residual_dev(hbgpu_ctx* ctx, const double* d_state, double* d_residual);
+int hbgpu_assemble_tangent_dev(hbgpu_ctx* ctx, const double* d_state);
+int hbgpu_matvec_dev(hbgpu_ctx* ctx, const double* d_y, double* d_out);
+int hbgpu_bsr_matvec_dev(hbgpu_ctx* ctx, const double* d_y, double* d_out);
+int hbgpu_jacobi_dev(hbgpu_ctx* ctx, int* degenerate_entries);
+int hbgpu_gmres_dev(hbgpu_ctx* ctx, const double* d_rhs, const hbgpu_krylov_cfg* cfg,
+                    double* d_x, hbgpu_krylov_result* result, double* history,
+                    int history_capacity);
+/* Device pointers of the context's P values / mass / inverse diagonal. */
+double* hbgpu_pvals_dev(hbgpu_ctx* ctx);
+
+/* ---- Newton driver ------------------------------------------------------- */
+
+typedef struct {
+    double pseudo_dt;          /* SolverConfig (hb_solver.hpp:12-23): 0 = auto h_c/u_c */
+    double newton_tol_orders;  /* 3 */
+    int max_newton_iters;      /* 60 */
+    hbgpu_krylov_cfg krylov;
+    int tau_mode;
+    int backflow_in_tangent;
+    double divergence_ratio;   /* 1e3 */
+} hbgpu_solver_cfg;
+
+typedef struct {
+    int entries;               /* ConvergenceLog entries written (<= capacity) */
+    int converged;
+    double pseudo_dt, cfl;
+    double assembly_seconds, linear_seconds, total_seconds;
+} hbgpu_solve_info;
+
+/* solve_harmonic (hb_solver.hpp:70-72, hb_solver.cpp:113-221): rest + Dirichlet
+ * + outlet pressure start, pseudo-time Newton, device GMRES.  Log arrays have
+ * `capacity` entries (iter, res, res_rel, linear_iters, seconds).  state_out
+ * receives the final HarmonicState data.  Returns HBGPU_ERR_DIVERGENCE /
+ * HBGPU_ERR_STAGNATION exactly where the reference throws. */
+int hbgpu_solve_harmonic(hbgpu_ctx* ctx, const hbgpu_solver_cfg* cfg, double* state_out,
+                         hbgpu_solve_info* info, int capacity, int* log_iter, double* log_res,
+                         double* log_rel, int* log_linear, double* log_seconds);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif

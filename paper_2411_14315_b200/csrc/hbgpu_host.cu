@@ -1,0 +1,1227 @@
+// Host runtime and C ABI of libhbgpu.so (see include/hbgpu.h).
+//
+// Owns the device copies of mesh, geometry, NodePattern, element incidence
+// lists, colour classes and solver work buffers; orchestrates the kernels in
+// hbgpu_kernels.cu on one CUDA stream.  The Newton driver mirrors
+// solve_harmonic (/root/reference/proj/src/hb_solver.cpp:113-221) and the
+// Krylov driver mirrors gmres_solve (src/linalg.cpp:167-293) with the
+// Hessenberg / Givens bookkeeping on the host and all vector work on device.
+#include "../../include/hbgpu.h"
+#include "hbgpu_internal.h"
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <complex>
+#include <cstdio>
+#include <cstring>
+#include <limits>
+#include <numeric>
+#include <string>
+#include <vector>
+
+using namespace hbgpu;
+
+namespace {
+
+thread_local std::string g_create_error;
+
+struct Timer {
+    std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+    double seconds() const {
+        return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    }
+};
+
+template <class T>
+struct DBuf {
+    T* p = nullptr;
+    size_t n = 0;
+    cudaError_t alloc(size_t count) {
+        release();
+        n = count;
+        if (count == 0)
+            return cudaSuccess;
+        return cudaMalloc(reinterpret_cast<void**>(&p), sizeof(T) * count);
+    }
+    void release() {
+        if (p)
+            cudaFree(p);
+        p = nullptr;
+        n = 0;
+    }
+};
+
+struct HostPatch {
+    int kind = 0;
+    std::vector<int> facets;      // 3 per facet
+    std::vector<double> normals;  // 3 per facet
+    std::vector<double> areas;
+    double area = 0.0;
+};
+
+}  // namespace
+
+struct hbgpu_ctx {
+    int nn = 0, ne = 0;
+    int M = 0, N = 0;
+    double period = 1.0, omega = 0.0;
+    double rho = 1.06, mu = 0.04;
+    int tau_mode = 0;
+    double pseudo_dt = std::numeric_limits<double>::infinity();
+    double pseudo_c1 = 1.5;
+    int backflow_tangent = 0;
+    double h_c = 0.0;
+
+    std::vector<int> conn_h;
+    std::vector<uint8_t> dir_h;
+    std::vector<HostPatch> patches;
+    std::vector<int> row_ptr_h, col_idx_h;
+    long long nnz = 0;
+
+    // device mesh structures
+    DBuf<int4> conn;
+    DBuf<double> geom;
+    DBuf<uint8_t> dir, edmask;
+    DBuf<int> row_ptr, col_idx, diag_blk, inc_ptr;
+    DBuf<uint32_t> inc_elem, inc_cols;
+    std::vector<int> color_ptr;
+    DBuf<int> color_elems;
+
+    // tangent CTA plan (depends on N)
+    std::vector<int> tcta_h;
+    DBuf<int> tcta;
+    size_t tsmem = 0;
+    int tthreads = 0;
+
+    // spectral + BCs
+    DBuf<double> H;
+    DBuf<double> g;
+    std::vector<double> g_h;
+    DBuf<double> hN;
+    std::vector<double> h_h;
+    std::vector<int> bc_patch;
+    double beta = 0.2;
+    DBuf<int> bnode, bptr, binc, fac, fbc;
+    DBuf<double> fnormal, farea;
+    int nbnodes = 0;
+
+    // work buffers
+    DBuf<double> state, r, hu, s, pvals, mass, inv, y, out, x, w, scale, b, tmp;
+    DBuf<double> V;
+    size_t V_vecs = 0;
+    DBuf<double> partial, red;
+    double* h_red = nullptr;  // pinned
+    DBuf<int> flag, ideg;
+    int* h_int = nullptr;  // pinned
+
+    bool mass_valid = false, p_valid = false, inv_valid = false;
+    cudaStream_t stream = nullptr;
+    std::string err;
+
+    long long state_len() const { return (long long)nn * 4 * N; }
+};
+
+#define CK(ctx, expr)                                                              \
+    do {                                                                           \
+        cudaError_t e_ = (expr);                                                   \
+        if (e_ != cudaSuccess) {                                                   \
+            (ctx)->err = std::string(#expr) + ": " + cudaGetErrorString(e_);       \
+            return e_ == cudaErrorMemoryAllocation ? HBGPU_ERR_OOM : HBGPU_ERR_CUDA; \
+        }                                                                          \
+    } while (0)
+
+#define TRY(expr)            \
+    do {                     \
+        int s_ = (expr);     \
+        if (s_ != HBGPU_OK)  \
+            return s_;       \
+    } while (0)
+
+static int fail(hbgpu_ctx* c, int code, const std::string& msg) {
+    c->err = msg;
+    return code;
+}
+
+static int check_launch(hbgpu_ctx* c) {
+    CK(c, cudaGetLastError());
+    return HBGPU_OK;
+}
+
+// Singular-tau flag raised inside the element kernels -> std::domain_error.
+static int check_flag(hbgpu_ctx* c) {
+    CK(c, cudaMemcpyAsync(c->h_int, c->flag.p, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    CK(c, cudaStreamSynchronize(c->stream));
+    const int f = c->h_int[0];
+    if (f) {
+        CK(c, cudaMemsetAsync(c->flag.p, 0, sizeof(int), c->stream));
+        if (f & 2)
+            return fail(c, HBGPU_ERR_GEOMETRY, "element has non-positive volume");
+        return fail(c, HBGPU_ERR_DOMAIN,
+                    "singular stabilization parameter: zero velocity with zero viscosity");
+    }
+    return HBGPU_OK;
+}
+
+// ---------------------------------------------------------------- host builders
+
+// NodePattern::build semantics (linalg.cpp:10-30): element adjacency plus the
+// diagonal, sorted unique columns per row.
+static void build_pattern(int nn, int ne, const int* conn, std::vector<int>& row_ptr,
+                          std::vector<int>& col_idx) {
+    std::vector<int> cnt(size_t(nn) + 1, 0);
+    for (long e = 0; e < ne; ++e)
+        for (int a = 0; a < 4; ++a)
+            cnt[size_t(conn[4 * e + a]) + 1] += 4;
+    for (int a = 0; a < nn; ++a)
+        cnt[size_t(a) + 1] += cnt[size_t(a)] + 1;
+    std::vector<int> buf(static_cast<size_t>(cnt[size_t(nn)]));
+    std::vector<int> fill(cnt.begin(), cnt.end() - 1);
+    for (int a = 0; a < nn; ++a)
+        buf[size_t(fill[size_t(a)]++)] = a;
+    for (long e = 0; e < ne; ++e)
+        for (int a = 0; a < 4; ++a) {
+            const int A = conn[4 * e + a];
+            for (int b = 0; b < 4; ++b)
+                buf[size_t(fill[size_t(A)]++)] = conn[4 * e + b];
+        }
+    row_ptr.assign(size_t(nn) + 1, 0);
+    col_idx.clear();
+    col_idx.reserve(buf.size() / 3);
+    for (int a = 0; a < nn; ++a) {
+        auto b0 = buf.begin() + cnt[size_t(a)], b1 = buf.begin() + cnt[size_t(a) + 1];
+        std::sort(b0, b1);
+        auto last = std::unique(b0, b1);
+        col_idx.insert(col_idx.end(), b0, last);
+        row_ptr[size_t(a) + 1] = int(col_idx.size());
+    }
+}
+
+static int upload_all(hbgpu_ctx* c, const hbgpu_mesh_desc* d) {
+    const int nn = c->nn, ne = c->ne;
+    cudaStream_t st = c->stream;
+    CK(c, c->conn.alloc(size_t(ne)));
+    CK(c, cudaMemcpyAsync(c->conn.p, d->conn, sizeof(int4) * size_t(ne), cudaMemcpyHostToDevice, st));
+    CK(c, c->dir.alloc(size_t(nn)));
+    CK(c, cudaMemcpyAsync(c->dir.p, c->dir_h.data(), size_t(nn), cudaMemcpyHostToDevice, st));
+    CK(c, c->flag.alloc(1));
+    CK(c, c->ideg.alloc(1));
+    CK(c, cudaMemsetAsync(c->flag.p, 0, sizeof(int), st));
+    CK(c, c->geom.alloc(size_t(ne) * 22));
+    if (d->geometry) {
+        CK(c, cudaMemcpyAsync(c->geom.p, d->geometry, sizeof(double) * 22 * size_t(ne),
+                              cudaMemcpyHostToDevice, st));
+    } else {
+        DBuf<double> xyz;
+        CK(c, xyz.alloc(size_t(nn) * 3));
+        CK(c, cudaMemcpyAsync(xyz.p, d->xyz, sizeof(double) * 3 * size_t(nn),
+                              cudaMemcpyHostToDevice, st));
+        launch_geometry(xyz.p, c->conn.p, ne, c->geom.p, c->flag.p, st);
+        TRY(check_launch(c));
+        CK(c, cudaStreamSynchronize(st));
+        xyz.release();
+        TRY(check_flag(c));
+    }
+
+    // pattern + per-row diagonal
+    build_pattern(nn, ne, d->conn, c->row_ptr_h, c->col_idx_h);
+    c->nnz = (long long)c->col_idx_h.size();
+    std::vector<int> diag(static_cast<size_t>(nn));
+    for (int A = 0; A < nn; ++A) {
+        const int* b0 = c->col_idx_h.data() + c->row_ptr_h[size_t(A)];
+        const int* b1 = c->col_idx_h.data() + c->row_ptr_h[size_t(A) + 1];
+        diag[size_t(A)] = int(std::lower_bound(b0, b1, A) - c->col_idx_h.data());
+    }
+    CK(c, c->row_ptr.alloc(size_t(nn) + 1));
+    CK(c, c->col_idx.alloc(size_t(c->nnz)));
+    CK(c, c->diag_blk.alloc(size_t(nn)));
+    CK(c, cudaMemcpyAsync(c->row_ptr.p, c->row_ptr_h.data(), sizeof(int) * (size_t(nn) + 1),
+                          cudaMemcpyHostToDevice, st));
+    CK(c, cudaMemcpyAsync(c->col_idx.p, c->col_idx_h.data(), sizeof(int) * size_t(c->nnz),
+                          cudaMemcpyHostToDevice, st));
+    CK(c, cudaMemcpyAsync(c->diag_blk.p, diag.data(), sizeof(int) * size_t(nn),
+                          cudaMemcpyHostToDevice, st));
+
+    // element incidences per row, element order; local block offsets
+    std::vector<int> iptr(size_t(nn) + 1, 0);
+    for (long e = 0; e < ne; ++e)
+        for (int a = 0; a < 4; ++a)
+            iptr[size_t(d->conn[4 * e + a]) + 1] += 1;
+    for (int A = 0; A < nn; ++A)
+        iptr[size_t(A) + 1] += iptr[size_t(A)];
+    std::vector<uint32_t> ielem(size_t(4) * size_t(ne)), icols(size_t(4) * size_t(ne));
+    std::vector<int> fill(iptr.begin(), iptr.end() - 1);
+    std::vector<uint8_t> edm(static_cast<size_t>(ne));
+    for (long e = 0; e < ne; ++e) {
+        uint8_t m = 0;
+        for (int b = 0; b < 4; ++b)
+            m |= uint8_t((c->dir_h[size_t(d->conn[4 * e + b])] ? 1 : 0) << b);
+        edm[size_t(e)] = m;
+        for (int a = 0; a < 4; ++a) {
+            const int A = d->conn[4 * e + a];
+            const int* r0 = c->col_idx_h.data() + c->row_ptr_h[size_t(A)];
+            const int* r1 = c->col_idx_h.data() + c->row_ptr_h[size_t(A) + 1];
+            uint32_t cols = 0;
+            for (int b = 0; b < 4; ++b) {
+                const long off = std::lower_bound(r0, r1, d->conn[4 * e + b]) - r0;
+                if (off > 255)
+                    return fail(c, HBGPU_ERR_INVALID, "node degree above 255 blocks per row");
+                cols |= uint32_t(off) << (8 * b);
+            }
+            const int slot = fill[size_t(A)]++;
+            ielem[size_t(slot)] = uint32_t(e) | (uint32_t(a) << 30);
+            icols[size_t(slot)] = cols;
+        }
+    }
+    CK(c, c->inc_ptr.alloc(size_t(nn) + 1));
+    CK(c, c->inc_elem.alloc(ielem.size()));
+    CK(c, c->inc_cols.alloc(icols.size()));
+    CK(c, c->edmask.alloc(size_t(ne)));
+    CK(c, cudaMemcpyAsync(c->inc_ptr.p, iptr.data(), sizeof(int) * iptr.size(),
+                          cudaMemcpyHostToDevice, st));
+    CK(c, cudaMemcpyAsync(c->inc_elem.p, ielem.data(), sizeof(uint32_t) * ielem.size(),
+                          cudaMemcpyHostToDevice, st));
+    CK(c, cudaMemcpyAsync(c->inc_cols.p, icols.data(), sizeof(uint32_t) * icols.size(),
+                          cudaMemcpyHostToDevice, st));
+    CK(c, cudaMemcpyAsync(c->edmask.p, edm.data(), edm.size(), cudaMemcpyHostToDevice, st));
+
+    // greedy element colouring (element order, smallest free colour):
+    // elements of one class share no node
+    std::vector<uint64_t> used(size_t(nn) * 2, 0);
+    std::vector<int> color(static_cast<size_t>(ne));
+    int ncol = 0;
+    for (long e = 0; e < ne; ++e) {
+        uint64_t f0 = 0, f1 = 0;
+        for (int a = 0; a < 4; ++a) {
+            f0 |= used[2 * size_t(d->conn[4 * e + a])];
+            f1 |= used[2 * size_t(d->conn[4 * e + a]) + 1];
+        }
+        int col;
+        if (~f0)
+            col = __builtin_ctzll(~f0);
+        else if (~f1)
+            col = 64 + __builtin_ctzll(~f1);
+        else
+            return fail(c, HBGPU_ERR_INVALID, "element colouring needs more than 128 colours");
+        color[size_t(e)] = col;
+        ncol = std::max(ncol, col + 1);
+        for (int a = 0; a < 4; ++a)
+            used[2 * size_t(d->conn[4 * e + a]) + (col >> 6)] |= uint64_t(1) << (col & 63);
+    }
+    c->color_ptr.assign(size_t(ncol) + 1, 0);
+    for (long e = 0; e < ne; ++e)
+        c->color_ptr[size_t(color[size_t(e)]) + 1] += 1;
+    for (int k = 0; k < ncol; ++k)
+        c->color_ptr[size_t(k) + 1] += c->color_ptr[size_t(k)];
+    std::vector<int> celem(static_cast<size_t>(ne));
+    std::vector<int> cf(c->color_ptr.begin(), c->color_ptr.end() - 1);
+    for (long e = 0; e < ne; ++e)
+        celem[size_t(cf[size_t(color[size_t(e)])]++)] = int(e);
+    CK(c, c->color_elems.alloc(size_t(ne)));
+    CK(c, cudaMemcpyAsync(c->color_elems.p, celem.data(), sizeof(int) * size_t(ne),
+                          cudaMemcpyHostToDevice, st));
+
+    CK(c, cudaMallocHost(reinterpret_cast<void**>(&c->h_red), sizeof(double) * 1024));
+    CK(c, cudaMallocHost(reinterpret_cast<void**>(&c->h_int), sizeof(int) * 16));
+    CK(c, c->partial.alloc(size_t(kRedBlocks) * 1024));
+    CK(c, c->red.alloc(1024));
+    CK(c, cudaStreamSynchronize(st));
+    return HBGPU_OK;
+}
+
+// Tangent CTA plan: consecutive block rows per CTA such that the rows' P
+// segment fits the shared-memory budget and rows*N <= 256 threads.
+static int plan_tangent(hbgpu_ctx* c) {
+    const int N = c->N;
+    const size_t row_bytes_per_blk = sizeof(double) * 8 * size_t(N);
+    const size_t budget = 100 * 1024;
+    const int max_rows = std::max(1, 256 / N);
+    c->tcta_h.clear();
+    c->tcta_h.push_back(0);
+    size_t maxsmem = 0;
+    int A = 0;
+    while (A < c->nn) {
+        int B = A;
+        size_t bytes = 0;
+        while (B < c->nn && B - A < max_rows) {
+            const size_t rb = size_t(c->row_ptr_h[size_t(B) + 1] - c->row_ptr_h[size_t(B)]) *
+                              row_bytes_per_blk;
+            if (B > A && bytes + rb > budget)
+                break;
+            bytes += rb;
+            ++B;
+        }
+        maxsmem = std::max(maxsmem, bytes);
+        c->tcta_h.push_back(B);
+        A = B;
+    }
+    if (maxsmem > 227 * 1024)
+        return fail(c, HBGPU_ERR_INVALID, "a block row exceeds the shared-memory budget");
+    c->tsmem = maxsmem;
+    c->tthreads = ((max_rows * N + 31) / 32) * 32;
+    CK(c, c->tcta.alloc(c->tcta_h.size()));
+    CK(c, cudaMemcpyAsync(c->tcta.p, c->tcta_h.data(), sizeof(int) * c->tcta_h.size(),
+                          cudaMemcpyHostToDevice, c->stream));
+    return HBGPU_OK;
+}
+
+static int rows_per_matvec_cta(int N) { return std::max(1, 256 / N); }
+
+// ---------------------------------------------------------------- operations
+
+static int residual_dev(hbgpu_ctx* c, const double* d_state, double* d_r) {
+    const int N = c->N;
+    cudaStream_t st = c->stream;
+    const size_t tot = size_t(c->nn) * 4 * size_t(N);
+    CK(c, cudaMemsetAsync(d_r, 0, sizeof(double) * tot, st));
+    CK(c, cudaMemsetAsync(c->s.p, 0, sizeof(double) * size_t(c->nn) * 3 * size_t(N), st));
+    if (N > 1)
+        launch_apply_h_series(c->H.p, N, d_state, 4 * N, c->hu.p, 3 * N, c->nn, st);
+    else
+        CK(c, cudaMemsetAsync(c->hu.p, 0, sizeof(double) * size_t(c->nn) * 3, st));
+    ResidualArgs a;
+    a.conn = c->conn.p;
+    a.geom = c->geom.p;
+    a.state = d_state;
+    a.hu = c->hu.p;
+    a.r = d_r;
+    a.s = c->s.p;
+    a.N = N;
+    a.rho = c->rho;
+    a.mu = c->mu;
+    a.nu = c->mu / c->rho;
+    a.tau_mode = c->tau_mode;
+    a.flag = c->flag.p;
+    for (size_t k = 0; k + 1 < c->color_ptr.size(); ++k)
+        launch_residual_color(a, c->color_elems.p + c->color_ptr[k],
+                              c->color_ptr[k + 1] - c->color_ptr[k], st);
+    launch_residual_finalize(c->H.p, N, c->s.p, c->dir.p, d_r, c->nn, st);
+    if (c->nbnodes > 0) {
+        BoundaryArgs b;
+        b.bnode = c->bnode.p;
+        b.bptr = c->bptr.p;
+        b.binc = c->binc.p;
+        b.fac = c->fac.p;
+        b.fnormal = c->fnormal.p;
+        b.farea = c->farea.p;
+        b.fbc = c->fbc.p;
+        b.h = c->hN.p;
+        b.dir = c->dir.p;
+        b.state = d_state;
+        b.r = d_r;
+        b.nbnodes = c->nbnodes;
+        b.N = N;
+        b.rho = c->rho;
+        b.beta = c->beta;
+        launch_boundary(b, st);
+    }
+    return check_launch(c);
+}
+
+static int tangent_dev(hbgpu_ctx* c, const double* d_state) {
+    if (c->backflow_tangent)
+        return fail(c, HBGPU_ERR_INVALID, "backflow_in_tangent is not supported on the GPU path yet");
+    TangentArgs a;
+    a.conn = c->conn.p;
+    a.geom = c->geom.p;
+    a.state = d_state;
+    a.edmask = c->edmask.p;
+    a.dir = c->dir.p;
+    a.row_ptr = c->row_ptr.p;
+    a.inc_ptr = c->inc_ptr.p;
+    a.inc_elem = c->inc_elem.p;
+    a.inc_cols = c->inc_cols.p;
+    a.cta_rows = c->tcta.p;
+    a.pvals = c->pvals.p;
+    a.N = c->N;
+    a.rho = c->rho;
+    a.mu = c->mu;
+    a.nu = c->mu / c->rho;
+    const bool pseudo = std::isfinite(c->pseudo_dt);
+    a.pseudo_c = pseudo ? c->pseudo_c1 * c->rho / c->pseudo_dt : 0.0;
+    a.tau_mode = c->tau_mode;
+    a.flag = c->flag.p;
+    launch_tangent_rows(a, int(c->tcta_h.size()) - 1, c->tthreads, c->tsmem, c->stream);
+    c->p_valid = true;
+    c->inv_valid = false;
+    return check_launch(c);
+}
+
+static int mass_dev(hbgpu_ctx* c) {
+    launch_mass_rows(c->conn.p, c->geom.p, c->row_ptr.p, c->inc_ptr.p, c->inc_elem.p,
+                     c->inc_cols.p, c->rho, c->mass.p, c->nn, c->stream);
+    c->mass_valid = true;
+    return check_launch(c);
+}
+
+static int matvec_dev(hbgpu_ctx* c, const double* d_y, double* d_out, const double* d_scale,
+                      bool with_c) {
+    if (!c->p_valid)
+        return fail(c, HBGPU_ERR_INVALID, "matvec before assemble_tangent / set_pvals");
+    if (with_c && c->N > 1 && !c->mass_valid)
+        TRY(mass_dev(c));
+    MatvecArgs a;
+    a.row_ptr = c->row_ptr.p;
+    a.col_idx = c->col_idx.p;
+    a.vals = c->pvals.p;
+    a.mass = c->mass.p;
+    a.dir = c->dir.p;
+    a.H = c->H.p;
+    a.y = d_y;
+    a.out = d_out;
+    a.scale = d_scale;
+    a.nn = c->nn;
+    a.N = c->N;
+    a.rows_per_cta = rows_per_matvec_cta(c->N);
+    a.with_c = (with_c && c->N > 1) ? 1 : 0;
+    launch_matvec(a, c->stream);
+    return check_launch(c);
+}
+
+static int jacobi_dev(hbgpu_ctx* c, int* degenerate) {
+    if (!c->p_valid)
+        return fail(c, HBGPU_ERR_INVALID, "jacobi before assemble_tangent / set_pvals");
+    CK(c, cudaMemsetAsync(c->ideg.p, 0, sizeof(int), c->stream));
+    launch_jacobi(c->pvals.p, c->diag_blk.p, c->nn, c->N, c->inv.p, c->ideg.p, c->stream);
+    TRY(check_launch(c));
+    CK(c, cudaMemcpyAsync(c->h_int + 1, c->ideg.p, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    CK(c, cudaStreamSynchronize(c->stream));
+    if (degenerate)
+        *degenerate = c->h_int[1];
+    c->inv_valid = true;
+    return HBGPU_OK;
+}
+
+// <a,b> for vectors already on device; deterministic.  Result on host.
+static int dot_dev(hbgpu_ctx* c, const double* a, const double* b, long n, double* out,
+                   bool take_sqrt) {
+    launch_multidot(a, 0, 1, b, n, c->partial.p, c->stream);
+    launch_reduce_partials(c->partial.p, 1, c->red.p, take_sqrt ? 1 : 0, c->stream);
+    TRY(check_launch(c));
+    CK(c, cudaMemcpyAsync(c->h_red, c->red.p, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    CK(c, cudaStreamSynchronize(c->stream));
+    *out = c->h_red[0];
+    return HBGPU_OK;
+}
+
+static int ensure_basis(hbgpu_ctx* c) {
+    if (c->N <= 0)
+        return fail(c, HBGPU_ERR_INVALID, "spectral basis not set (hbgpu_set_basis)");
+    return HBGPU_OK;
+}
+
+// gmres_solve (linalg.cpp:167-293): split Jacobi scaling, restarted Arnoldi
+// with classical Gram-Schmidt + one DGKS re-orthogonalisation when the
+// projection removed more than half of the norm, Givens rotations, true
+// residual recompute per cycle, stagnation when a cycle does not decrease it.
+static int gmres_dev(hbgpu_ctx* c, const double* d_rhs, const double* d_inv,
+                     const hbgpu_krylov_cfg* kc, double* d_x, hbgpu_krylov_result* res,
+                     double* history, int hcap) {
+    cudaStream_t st = c->stream;
+    const long n = long(c->state_len());
+    const int m = std::max(1, kc->restart);
+    res->iterations = 0;
+    res->relative_residual = 1.0;
+    res->status = 0;
+    res->history_len = 0;
+    auto push_hist = [&](double v) {
+        if (history && res->history_len < hcap)
+            history[res->history_len] = v;
+        res->history_len += (history && res->history_len < hcap) ? 1 : 0;
+    };
+    if (c->V_vecs < size_t(m) + 1) {
+        CK(c, c->V.alloc((size_t(m) + 1) * size_t(n)));
+        c->V_vecs = size_t(m) + 1;
+    }
+    if (size_t(m) + 2 > 1024)
+        return fail(c, HBGPU_ERR_INVALID, "restart above 1022 not supported");
+    double* V = c->V.p;
+    launch_sqrt_abs(d_inv, c->scale.p, n, st);
+    launch_mul(c->scale.p, d_rhs, c->b.p, n, st);
+    CK(c, cudaMemsetAsync(d_x, 0, sizeof(double) * size_t(n), st));
+    double bnorm = 0.0;
+    TRY(dot_dev(c, c->b.p, c->b.p, n, &bnorm, true));
+    if (bnorm == 0.0) {
+        res->relative_residual = 0.0;
+        return HBGPU_OK;
+    }
+    std::vector<double> Hm(static_cast<size_t>((m + 1) * m)), cs(static_cast<size_t>(m)),
+        sn(static_cast<size_t>(m)), gv(static_cast<size_t>(m + 1)), yv(static_cast<size_t>(m));
+
+    auto HH = [&](int i, int j) -> double& { return Hm[size_t(j) * size_t(m + 1) + size_t(i)]; };
+    double rnorm = bnorm;
+    const double* rsrc = c->b.p;  // current residual vector (scaled)
+    push_hist(1.0);
+    while (res->iterations < kc->max_iters) {
+        const double cycle_start = rnorm;
+        std::fill(Hm.begin(), Hm.end(), 0.0);
+        std::fill(gv.begin(), gv.end(), 0.0);
+        gv[0] = rnorm;
+        c->h_red[0] = rnorm;
+        CK(c, cudaMemcpyAsync(c->red.p, c->h_red, sizeof(double), cudaMemcpyHostToDevice, st));
+        launch_scale_copy(rsrc, c->red.p, 1, V, n, st);
+        int j = 0;
+        for (; j < m && res->iterations < kc->max_iters; ++j) {
+            double* vj = V + size_t(j) * size_t(n);
+            TRY(matvec_dev(c, vj, c->w.p, c->scale.p, true));
+            // h_i = <w, V_i>, i <= j, and <w,w>
+            launch_multidot(V, n, j + 1, c->w.p, n, c->partial.p, st);
+            launch_multidot(c->w.p, 0, 1, c->w.p, n, c->partial.p + size_t(j + 1) * kRedBlocks, st);
+            launch_reduce_partials(c->partial.p, j + 2, c->red.p, 0, st);
+            launch_gemv_sub(V, n, j + 1, c->red.p, c->w.p, n, st);
+            TRY(check_launch(c));
+            CK(c, cudaMemcpyAsync(c->h_red, c->red.p, sizeof(double) * size_t(j + 2),
+                                  cudaMemcpyDeviceToHost, st));
+            CK(c, cudaStreamSynchronize(st));
+            double proj2 = 0.0;
+            for (int i = 0; i <= j; ++i) {
+                HH(i, j) = c->h_red[i];
+                proj2 += c->h_red[i] * c->h_red[i];
+            }
+            const double w2 = c->h_red[j + 1];
+            if (w2 - proj2 < 0.5 * w2) {
+                // re-orthogonalise once (twice is enough)
+                launch_multidot(V, n, j + 1, c->w.p, n, c->partial.p, st);
+                launch_reduce_partials(c->partial.p, j + 1, c->red.p, 0, st);
+                launch_gemv_sub(V, n, j + 1, c->red.p, c->w.p, n, st);
+                TRY(check_launch(c));
+                CK(c, cudaMemcpyAsync(c->h_red, c->red.p, sizeof(double) * size_t(j + 1),
+                                      cudaMemcpyDeviceToHost, st));
+                CK(c, cudaStreamSynchronize(st));
+                for (int i = 0; i <= j; ++i)
+                    HH(i, j) += c->h_red[i];
+            }
+            double hj1 = 0.0;
+            TRY(dot_dev(c, c->w.p, c->w.p, n, &hj1, true));
+            HH(j + 1, j) = hj1;
+            if (hj1 > 0.0) {
+                c->h_red[0] = hj1;
+                CK(c, cudaMemcpyAsync(c->red.p, c->h_red, sizeof(double), cudaMemcpyHostToDevice, st));
+                launch_scale_copy(c->w.p, c->red.p, 1, V + size_t(j + 1) * size_t(n), n, st);
+            }
+            for (int i = 0; i < j; ++i) {
+                const double t = cs[size_t(i)] * HH(i, j) + sn[size_t(i)] * HH(i + 1, j);
+                HH(i + 1, j) = -sn[size_t(i)] * HH(i, j) + cs[size_t(i)] * HH(i + 1, j);
+                HH(i, j) = t;
+            }
+            const double den = std::hypot(HH(j, j), HH(j + 1, j));
+            cs[size_t(j)] = den == 0.0 ? 1.0 : HH(j, j) / den;
+            sn[size_t(j)] = den == 0.0 ? 0.0 : HH(j + 1, j) / den;
+            HH(j, j) = den;
+            HH(j + 1, j) = 0.0;
+            gv[size_t(j) + 1] = -sn[size_t(j)] * gv[size_t(j)];
+            gv[size_t(j)] = cs[size_t(j)] * gv[size_t(j)];
+            res->iterations += 1;
+            const double est = std::fabs(gv[size_t(j) + 1]);
+            push_hist(est / bnorm);
+            if (est / bnorm <= kc->tolerance || hj1 == 0.0) {
+                ++j;
+                break;
+            }
+        }
+        while (j > 0 && HH(j - 1, j - 1) == 0.0)
+            --j;
+        for (int i = j - 1; i >= 0; --i) {
+            double sacc = gv[size_t(i)];
+            for (int k = i + 1; k < j; ++k)
+                sacc -= HH(i, k) * yv[size_t(k)];
+            yv[size_t(i)] = sacc / HH(i, i);
+        }
+        if (j > 0) {
+            std::copy(yv.begin(), yv.begin() + j, c->h_red);
+            CK(c, cudaMemcpyAsync(c->red.p, c->h_red, sizeof(double) * size_t(j),
+                                  cudaMemcpyHostToDevice, st));
+            launch_gemv_add_scaled(V, n, j, c->red.p, c->scale.p, d_x, n, st);
+        }
+        // recomputed scaled residual r = S (rhs - L x)
+        TRY(matvec_dev(c, d_x, c->w.p, nullptr, true));
+        launch_scaled_diff(c->scale.p, d_rhs, c->w.p, c->tmp.p, n, st);
+        rsrc = c->tmp.p;
+        TRY(dot_dev(c, c->tmp.p, c->tmp.p, n, &rnorm, true));
+        res->relative_residual = rnorm / bnorm;
+        if (res->relative_residual <= kc->tolerance) {
+            res->status = 0;
+            return HBGPU_OK;
+        }
+        if (rnorm >= cycle_start) {
+            res->status = 2;
+            return HBGPU_OK;
+        }
+    }
+    res->status = 1;
+    return HBGPU_OK;
+}
+
+// ---------------------------------------------------------------- C ABI
+
+extern "C" {
+
+const char* hbgpu_create_error(void) { return g_create_error.c_str(); }
+
+hbgpu_ctx* hbgpu_create(const hbgpu_mesh_desc* d, int* status) {
+    auto set = [&](int s, const std::string& m) {
+        if (status)
+            *status = s;
+        g_create_error = m;
+    };
+    if (!d || d->num_nodes <= 0 || d->num_elements < 0 || !d->conn || !d->dirichlet ||
+        (!d->geometry && !d->xyz)) {
+        set(HBGPU_ERR_INVALID, "invalid mesh descriptor");
+        return nullptr;
+    }
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+        set(HBGPU_ERR_CUDA, "no CUDA device: the HB-GLS GPU path has no CPU fallback");
+        return nullptr;
+    }
+    int dev = 0, major = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
+    if (major < 10) {
+        set(HBGPU_ERR_CUDA, "libhbgpu is built for sm_100a (B200); device is older");
+        return nullptr;
+    }
+    auto* c = new hbgpu_ctx;
+    c->nn = d->num_nodes;
+    c->ne = d->num_elements;
+    c->conn_h.assign(d->conn, d->conn + 4 * size_t(c->ne));
+    c->dir_h.assign(d->dirichlet, d->dirichlet + size_t(c->nn));
+    for (int k = 0; k < 4 * c->ne; ++k)
+        if (d->conn[k] < 0 || d->conn[k] >= c->nn) {
+            set(HBGPU_ERR_PARSE, "element references a node out of range");
+            delete c;
+            return nullptr;
+        }
+    size_t off = 0;
+    for (int p = 0; p < d->num_patches; ++p) {
+        HostPatch hp;
+        hp.kind = d->patch_kind[p];
+        const int nf = d->patch_num_facets[p];
+        hp.facets.assign(d->facets + 3 * off, d->facets + 3 * (off + size_t(nf)));
+        hp.normals.assign(d->normals + 3 * off, d->normals + 3 * (off + size_t(nf)));
+        hp.areas.assign(d->areas + off, d->areas + off + size_t(nf));
+        for (double a : hp.areas)
+            hp.area += a;
+        c->patches.push_back(std::move(hp));
+        off += size_t(nf);
+    }
+    // characteristic length (mesh.cpp:213-224), from signed volumes
+    if (c->ne > 0) {
+        double total = 0.0;
+        if (d->xyz) {
+            for (int e = 0; e < c->ne; ++e) {
+                const double* x[4];
+                for (int a = 0; a < 4; ++a)
+                    x[a] = d->xyz + 3 * size_t(d->conn[4 * e + a]);
+                const double b0[3] = {x[1][0] - x[0][0], x[1][1] - x[0][1], x[1][2] - x[0][2]};
+                const double b1[3] = {x[2][0] - x[0][0], x[2][1] - x[0][1], x[2][2] - x[0][2]};
+                const double b2[3] = {x[3][0] - x[0][0], x[3][1] - x[0][1], x[3][2] - x[0][2]};
+                const double cr[3] = {b1[1] * b2[2] - b1[2] * b2[1], b1[2] * b2[0] - b1[0] * b2[2],
+                                      b1[0] * b2[1] - b1[1] * b2[0]};
+                total += (b0[0] * cr[0] + b0[1] * cr[1] + b0[2] * cr[2]) / 6.0;
+            }
+        } else {
+            for (int e = 0; e < c->ne; ++e)
+                total += d->geometry[22 * size_t(e) + 12];
+        }
+        c->h_c = std::cbrt(6.0 * std::sqrt(2.0) * (total / double(c->ne)));
+    }
+    if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess) {
+        set(HBGPU_ERR_CUDA, "cudaStreamCreate failed");
+        delete c;
+        return nullptr;
+    }
+    const int st = upload_all(c, d);
+    if (st != HBGPU_OK) {
+        set(st, c->err);
+        hbgpu_destroy(c);
+        return nullptr;
+    }
+    if (status)
+        *status = HBGPU_OK;
+    return c;
+}
+
+void hbgpu_destroy(hbgpu_ctx* c) {
+    if (!c)
+        return;
+    if (c->stream)
+        cudaStreamSynchronize(c->stream);
+    if (c->h_red)
+        cudaFreeHost(c->h_red);
+    if (c->h_int)
+        cudaFreeHost(c->h_int);
+    for (DBuf<double>* b : {&c->geom, &c->H, &c->g, &c->hN, &c->fnormal, &c->farea, &c->state,
+                            &c->r, &c->hu, &c->s, &c->pvals, &c->mass, &c->inv, &c->y, &c->out,
+                            &c->x, &c->w, &c->scale, &c->b, &c->tmp, &c->V, &c->partial, &c->red})
+        b->release();
+    for (DBuf<int>* b : {&c->row_ptr, &c->col_idx, &c->diag_blk, &c->inc_ptr, &c->color_elems,
+                         &c->tcta, &c->bnode, &c->bptr, &c->binc, &c->fac, &c->fbc, &c->flag,
+                         &c->ideg})
+        b->release();
+    c->conn.release();
+    c->dir.release();
+    c->edmask.release();
+    c->inc_elem.release();
+    c->inc_cols.release();
+    if (c->stream)
+        cudaStreamDestroy(c->stream);
+    delete c;
+}
+
+const char* hbgpu_last_error(const hbgpu_ctx* c) { return c ? c->err.c_str() : ""; }
+
+void* hbgpu_stream(hbgpu_ctx* c) { return c->stream; }
+
+int hbgpu_synchronize(hbgpu_ctx* c) {
+    CK(c, cudaStreamSynchronize(c->stream));
+    return check_flag(c);
+}
+
+int hbgpu_set_basis(hbgpu_ctx* c, int modes, double period) {
+    if (modes < 1)
+        return fail(c, HBGPU_ERR_PARSE, "spectral basis requires at least one mode (M >= 1)");
+    if (!(period > 0.0))
+        return fail(c, HBGPU_ERR_PARSE, "spectral basis requires a positive period");
+    c->M = modes;
+    c->N = 2 * modes - 1;
+    c->period = period;
+    c->omega = 2.0 * M_PI / period;
+    const int N = c->N;
+    // H = E^-1 Omega E, E(j,k) = e^{-2 pi i j k/N}/N, Omega_kk = i omega m(k) (spectral.cpp:236-256)
+    std::vector<double> H(size_t(N) * size_t(N));
+    for (int j = 0; j < N; ++j)
+        for (int k = 0; k < N; ++k) {
+            std::complex<double> acc(0.0, 0.0);
+            for (int l = 0; l < N; ++l) {
+                const double ph1 = 2.0 * M_PI * double(j) * double(l) / double(N);
+                const double ph2 = -2.0 * M_PI * double(l) * double(k) / double(N);
+                const std::complex<double> einv(std::cos(ph1), std::sin(ph1));
+                const std::complex<double> e(std::cos(ph2) / N, std::sin(ph2) / N);
+                const int mm = l < modes ? l : l - N;
+                const std::complex<double> om(0.0, c->omega * double(mm));
+                acc += einv * om * e;
+            }
+            H[size_t(j) * size_t(N) + size_t(k)] = acc.real();
+        }
+    CK(c, c->H.alloc(H.size()));
+    CK(c, cudaMemcpyAsync(c->H.p, H.data(), sizeof(double) * H.size(), cudaMemcpyHostToDevice,
+                          c->stream));
+    const size_t n = size_t(c->state_len());
+    for (DBuf<double>* b : {&c->state, &c->r, &c->inv, &c->y, &c->out, &c->x, &c->w, &c->scale,
+                            &c->b, &c->tmp})
+        CK(c, b->alloc(n));
+    CK(c, c->hu.alloc(size_t(c->nn) * 3 * size_t(N)));
+    CK(c, c->s.alloc(size_t(c->nn) * 3 * size_t(N)));
+    CK(c, c->pvals.alloc(size_t(c->nnz) * 8 * size_t(N)));
+    CK(c, c->mass.alloc(size_t(c->nnz)));
+    CK(c, c->g.alloc(size_t(c->nn) * 3 * size_t(N)));
+    CK(c, cudaMemsetAsync(c->g.p, 0, sizeof(double) * size_t(c->nn) * 3 * size_t(N), c->stream));
+    c->g_h.assign(size_t(c->nn) * 3 * size_t(N), 0.0);
+    c->V.release();
+    c->V_vecs = 0;
+    c->p_valid = c->inv_valid = false;
+    c->mass_valid = false;
+    TRY(plan_tangent(c));
+    CK(c, configure_tangent_smem(c->tsmem));
+    // clear previous Neumann data sized for another N
+    c->hN.release();
+    c->h_h.clear();
+    c->bc_patch.clear();
+    c->nbnodes = 0;
+    CK(c, cudaStreamSynchronize(c->stream));
+    return HBGPU_OK;
+}
+
+int hbgpu_set_fluid(hbgpu_ctx* c, double rho, double mu) {
+    if (!(rho > 0.0) || !(mu > 0.0))
+        return fail(c, HBGPU_ERR_PARSE, "fluid density and viscosity must be strictly positive");
+    c->rho = rho;
+    c->mu = mu;
+    c->mass_valid = false;
+    return HBGPU_OK;
+}
+
+int hbgpu_set_assembly_config(hbgpu_ctx* c, int tau_mode, double pseudo_dt, double pseudo_c1,
+                              int backflow_in_tangent) {
+    c->tau_mode = tau_mode == 1 ? 1 : 0;
+    c->pseudo_dt = (pseudo_dt > 0.0 && std::isfinite(pseudo_dt))
+                       ? pseudo_dt
+                       : std::numeric_limits<double>::infinity();
+    c->pseudo_c1 = pseudo_c1;
+    c->backflow_tangent = backflow_in_tangent;
+    return HBGPU_OK;
+}
+
+int hbgpu_set_bcs(hbgpu_ctx* c, const double* dirichlet_g, int n_neumann, const int* neumann_patch,
+                  const double* neumann_h, double backflow_beta) {
+    TRY(ensure_basis(c));
+    const int N = c->N;
+    const size_t gl = size_t(c->nn) * 3 * size_t(N);
+    if (dirichlet_g)
+        c->g_h.assign(dirichlet_g, dirichlet_g + gl);
+    else
+        c->g_h.assign(gl, 0.0);
+    CK(c, cudaMemcpyAsync(c->g.p, c->g_h.data(), sizeof(double) * gl, cudaMemcpyHostToDevice,
+                          c->stream));
+    c->beta = backflow_beta;
+    c->bc_patch.assign(neumann_patch, neumann_patch + n_neumann);
+    c->h_h.assign(neumann_h, neumann_h + size_t(n_neumann) * size_t(N));
+    for (int k = 0; k < n_neumann; ++k)
+        if (neumann_patch[k] < 0 || neumann_patch[k] >= int(c->patches.size()))
+            return fail(c, HBGPU_ERR_INVALID, "Neumann entry references an unknown patch");
+    // facet arrays over the Neumann list (assembly.cpp:537-539 order) and
+    // per-node incidence lists in that order
+    std::vector<int> fac, fbc;
+    std::vector<double> fnorm, farea;
+    for (int k = 0; k < n_neumann; ++k) {
+        const HostPatch& p = c->patches[size_t(neumann_patch[k])];
+        for (size_t f = 0; f < p.areas.size(); ++f) {
+            for (int v = 0; v < 3; ++v) {
+                fac.push_back(p.facets[3 * f + size_t(v)]);
+                fnorm.push_back(p.normals[3 * f + size_t(v)]);
+            }
+            farea.push_back(p.areas[f]);
+            fbc.push_back(k);
+        }
+    }
+    const int nf = int(farea.size());
+    std::vector<int> cnt(size_t(c->nn) + 1, 0);
+    for (int f = 0; f < nf; ++f)
+        for (int v = 0; v < 3; ++v)
+            cnt[size_t(fac[3 * size_t(f) + size_t(v)]) + 1] += 1;
+    std::vector<int> bnode, bptr{0}, binc;
+    std::vector<int> start(size_t(c->nn), -1);
+    for (int A = 0; A < c->nn; ++A)
+        if (cnt[size_t(A) + 1] > 0) {
+            start[size_t(A)] = bptr.back();
+            bnode.push_back(A);
+            bptr.push_back(bptr.back() + cnt[size_t(A) + 1]);
+        }
+    binc.assign(size_t(bptr.back()), 0);
+    std::vector<int> fillp(start);
+    for (int f = 0; f < nf; ++f)
+        for (int v = 0; v < 3; ++v) {
+            const int A = fac[3 * size_t(f) + size_t(v)];
+            binc[size_t(fillp[size_t(A)]++)] = f * 4 + v;
+        }
+    c->nbnodes = int(bnode.size());
+    if (nf > 0) {
+        CK(c, c->fac.alloc(fac.size()));
+        CK(c, c->fbc.alloc(fbc.size()));
+        CK(c, c->fnormal.alloc(fnorm.size()));
+        CK(c, c->farea.alloc(farea.size()));
+        CK(c, c->bnode.alloc(bnode.size()));
+        CK(c, c->bptr.alloc(bptr.size()));
+        CK(c, c->binc.alloc(binc.size()));
+        CK(c, c->hN.alloc(c->h_h.size()));
+        cudaStream_t st = c->stream;
+        CK(c, cudaMemcpyAsync(c->fac.p, fac.data(), sizeof(int) * fac.size(), cudaMemcpyHostToDevice, st));
+        CK(c, cudaMemcpyAsync(c->fbc.p, fbc.data(), sizeof(int) * fbc.size(), cudaMemcpyHostToDevice, st));
+        CK(c, cudaMemcpyAsync(c->fnormal.p, fnorm.data(), sizeof(double) * fnorm.size(), cudaMemcpyHostToDevice, st));
+        CK(c, cudaMemcpyAsync(c->farea.p, farea.data(), sizeof(double) * farea.size(), cudaMemcpyHostToDevice, st));
+        CK(c, cudaMemcpyAsync(c->bnode.p, bnode.data(), sizeof(int) * bnode.size(), cudaMemcpyHostToDevice, st));
+        CK(c, cudaMemcpyAsync(c->bptr.p, bptr.data(), sizeof(int) * bptr.size(), cudaMemcpyHostToDevice, st));
+        CK(c, cudaMemcpyAsync(c->binc.p, binc.data(), sizeof(int) * binc.size(), cudaMemcpyHostToDevice, st));
+        CK(c, cudaMemcpyAsync(c->hN.p, c->h_h.data(), sizeof(double) * c->h_h.size(), cudaMemcpyHostToDevice, st));
+    }
+    CK(c, cudaStreamSynchronize(c->stream));
+    return HBGPU_OK;
+}
+
+int hbgpu_sizes(const hbgpu_ctx* c, int* nn, int* ne, int* N, long long* nnz, long long* slen) {
+    if (nn) *nn = c->nn;
+    if (ne) *ne = c->ne;
+    if (N) *N = c->N;
+    if (nnz) *nnz = c->nnz;
+    if (slen) *slen = c->state_len();
+    return HBGPU_OK;
+}
+
+int hbgpu_get_pattern(hbgpu_ctx* c, int* row_ptr, int* col_idx) {
+    if (row_ptr)
+        CK(c, cudaMemcpy(row_ptr, c->row_ptr.p, sizeof(int) * (size_t(c->nn) + 1), cudaMemcpyDeviceToHost));
+    if (col_idx)
+        CK(c, cudaMemcpy(col_idx, c->col_idx.p, sizeof(int) * size_t(c->nnz), cudaMemcpyDeviceToHost));
+    return HBGPU_OK;
+}
+
+int hbgpu_get_geometry(hbgpu_ctx* c, double* geometry) {
+    CK(c, cudaMemcpy(geometry, c->geom.p, sizeof(double) * 22 * size_t(c->ne), cudaMemcpyDeviceToHost));
+    return HBGPU_OK;
+}
+
+int hbgpu_assemble_residual_dev(hbgpu_ctx* c, const double* d_state, double* d_r) {
+    TRY(ensure_basis(c));
+    return residual_dev(c, d_state, d_r);
+}
+
+int hbgpu_assemble_residual(hbgpu_ctx* c, const double* state, double* residual) {
+    TRY(ensure_basis(c));
+    const size_t n = size_t(c->state_len());
+    CK(c, cudaMemcpyAsync(c->state.p, state, sizeof(double) * n, cudaMemcpyHostToDevice, c->stream));
+    TRY(residual_dev(c, c->state.p, c->r.p));
+    CK(c, cudaMemcpyAsync(residual, c->r.p, sizeof(double) * n, cudaMemcpyDeviceToHost, c->stream));
+    CK(c, cudaStreamSynchronize(c->stream));
+    return check_flag(c);
+}
+
+int hbgpu_assemble_tangent_dev(hbgpu_ctx* c, const double* d_state) {
+    TRY(ensure_basis(c));
+    return tangent_dev(c, d_state);
+}
+
+int hbgpu_assemble_tangent(hbgpu_ctx* c, const double* state, double* pvals) {
+    TRY(ensure_basis(c));
+    const size_t n = size_t(c->state_len());
+    CK(c, cudaMemcpyAsync(c->state.p, state, sizeof(double) * n, cudaMemcpyHostToDevice, c->stream));
+    TRY(tangent_dev(c, c->state.p));
+    if (pvals)
+        CK(c, cudaMemcpyAsync(pvals, c->pvals.p, sizeof(double) * size_t(c->nnz) * 8 * size_t(c->N),
+                              cudaMemcpyDeviceToHost, c->stream));
+    CK(c, cudaStreamSynchronize(c->stream));
+    return check_flag(c);
+}
+
+int hbgpu_assemble_mass(hbgpu_ctx* c, double* mass) {
+    TRY(ensure_basis(c));
+    TRY(mass_dev(c));
+    if (mass)
+        CK(c, cudaMemcpyAsync(mass, c->mass.p, sizeof(double) * size_t(c->nnz), cudaMemcpyDeviceToHost, c->stream));
+    CK(c, cudaStreamSynchronize(c->stream));
+    return HBGPU_OK;
+}
+
+int hbgpu_set_pvals(hbgpu_ctx* c, const double* pvals) {
+    TRY(ensure_basis(c));
+    CK(c, cudaMemcpyAsync(c->pvals.p, pvals, sizeof(double) * size_t(c->nnz) * 8 * size_t(c->N),
+                          cudaMemcpyHostToDevice, c->stream));
+    CK(c, cudaStreamSynchronize(c->stream));
+    c->p_valid = true;
+    c->inv_valid = false;
+    return HBGPU_OK;
+}
+
+double* hbgpu_pvals_dev(hbgpu_ctx* c) { return c->pvals.p; }
+
+int hbgpu_matvec_dev(hbgpu_ctx* c, const double* d_y, double* d_out) {
+    TRY(ensure_basis(c));
+    return matvec_dev(c, d_y, d_out, nullptr, true);
+}
+
+int hbgpu_bsr_matvec_dev(hbgpu_ctx* c, const double* d_y, double* d_out) {
+    TRY(ensure_basis(c));
+    return matvec_dev(c, d_y, d_out, nullptr, false);
+}
+
+static int host_matvec(hbgpu_ctx* c, const double* y, double* out, bool with_c) {
+    TRY(ensure_basis(c));
+    const size_t n = size_t(c->state_len());
+    CK(c, cudaMemcpyAsync(c->y.p, y, sizeof(double) * n, cudaMemcpyHostToDevice, c->stream));
+    TRY(matvec_dev(c, c->y.p, c->out.p, nullptr, with_c));
+    CK(c, cudaMemcpyAsync(out, c->out.p, sizeof(double) * n, cudaMemcpyDeviceToHost, c->stream));
+    CK(c, cudaStreamSynchronize(c->stream));
+    return HBGPU_OK;
+}
+
+int hbgpu_matvec(hbgpu_ctx* c, const double* y, double* out) { return host_matvec(c, y, out, true); }
+int hbgpu_bsr_matvec(hbgpu_ctx* c, const double* y, double* out) { return host_matvec(c, y, out, false); }
+
+int hbgpu_jacobi_dev(hbgpu_ctx* c, int* degenerate) {
+    TRY(ensure_basis(c));
+    return jacobi_dev(c, degenerate);
+}
+
+int hbgpu_jacobi(hbgpu_ctx* c, double* inv_diag, int* degenerate) {
+    TRY(ensure_basis(c));
+    TRY(jacobi_dev(c, degenerate));
+    if (inv_diag) {
+        CK(c, cudaMemcpyAsync(inv_diag, c->inv.p, sizeof(double) * size_t(c->state_len()),
+                              cudaMemcpyDeviceToHost, c->stream));
+        CK(c, cudaStreamSynchronize(c->stream));
+    }
+    return HBGPU_OK;
+}
+
+int hbgpu_gmres_dev(hbgpu_ctx* c, const double* d_rhs, const hbgpu_krylov_cfg* cfg, double* d_x,
+                    hbgpu_krylov_result* result, double* history, int hcap) {
+    TRY(ensure_basis(c));
+    if (!c->inv_valid)
+        TRY(jacobi_dev(c, nullptr));
+    return gmres_dev(c, d_rhs, c->inv.p, cfg, d_x, result, history, hcap);
+}
+
+int hbgpu_gmres(hbgpu_ctx* c, const double* rhs, const double* inv_diag, const hbgpu_krylov_cfg* cfg,
+                double* x, hbgpu_krylov_result* result, double* history, int hcap) {
+    TRY(ensure_basis(c));
+    const size_t n = size_t(c->state_len());
+    if (inv_diag) {
+        CK(c, cudaMemcpyAsync(c->inv.p, inv_diag, sizeof(double) * n, cudaMemcpyHostToDevice, c->stream));
+        c->inv_valid = true;
+    } else if (!c->inv_valid) {
+        TRY(jacobi_dev(c, nullptr));
+    }
+    CK(c, cudaMemcpyAsync(c->y.p, rhs, sizeof(double) * n, cudaMemcpyHostToDevice, c->stream));
+    TRY(gmres_dev(c, c->y.p, c->inv.p, cfg, c->x.p, result, history, hcap));
+    CK(c, cudaMemcpyAsync(x, c->x.p, sizeof(double) * n, cudaMemcpyDeviceToHost, c->stream));
+    CK(c, cudaStreamSynchronize(c->stream));
+    return HBGPU_OK;
+}
+
+// solve_harmonic (hb_solver.cpp:113-221)
+int hbgpu_solve_harmonic(hbgpu_ctx* c, const hbgpu_solver_cfg* cfg, double* state_out,
+                         hbgpu_solve_info* info, int cap, int* log_iter, double* log_res,
+                         double* log_rel, int* log_lin, double* log_sec) {
+    TRY(ensure_basis(c));
+    Timer total;
+    const int N = c->N;
+    const long n = long(c->state_len());
+    cudaStream_t st = c->stream;
+    hbgpu_solve_info inf{};
+    auto log = [&](int iter, double res, double rel, int lin, double sec) {
+        if (inf.entries < cap) {
+            if (log_iter) log_iter[inf.entries] = iter;
+            if (log_res) log_res[inf.entries] = res;
+            if (log_rel) log_rel[inf.entries] = rel;
+            if (log_lin) log_lin[inf.entries] = lin;
+            if (log_sec) log_sec[inf.entries] = sec;
+            inf.entries += 1;
+        }
+    };
+    auto finish = [&](int code) {
+        inf.total_seconds = total.seconds();
+        if (info) *info = inf;
+        if (state_out)
+            cudaMemcpy(state_out, c->state.p, sizeof(double) * size_t(n), cudaMemcpyDeviceToHost);
+        return code;
+    };
+
+    // rest + Dirichlet data + outlet pressure level (hb_solver.cpp:119-132,
+    // assembly.cpp:415-441)
+    CK(c, cudaMemsetAsync(c->state.p, 0, sizeof(double) * size_t(n), st));
+    launch_install_dirichlet(c->g.p, c->dir.p, c->nn, N, c->state.p, st);
+    double wsum = 0.0, acc = 0.0;
+    for (size_t k = 0; k < c->bc_patch.size(); ++k) {
+        double hbar = 0.0;
+        for (int m = 0; m < N; ++m)
+            hbar += c->h_h[k * size_t(N) + size_t(m)];
+        hbar /= double(N);
+        const double area = c->patches[size_t(c->bc_patch[k])].area;
+        acc += area * (-hbar);
+        wsum += area;
+    }
+    const double p0 = wsum > 0.0 ? acc / wsum : 0.0;
+    if (p0 != 0.0)
+        launch_fill_pressure(p0, c->nn, N, c->state.p, st);
+    TRY(check_launch(c));
+
+    // pseudo-time step (hb_solver.cpp:28-56,86-111)
+    double u_c = 0.0;
+    bool has_inlet = false;
+    for (const HostPatch& p : c->patches) {
+        if (p.kind != 0 || !(p.area > 0.0))
+            continue;
+        has_inlet = true;
+        for (int m = 0; m < N; ++m) {
+            double q = 0.0;
+            for (size_t f = 0; f < p.areas.size(); ++f) {
+                const double w = p.areas[f] / 3.0;
+                for (int qp = 0; qp < 3; ++qp) {
+                    double un = 0.0;
+                    for (int a = 0; a < 3; ++a) {
+                        const double sa = qp == a ? 2.0 / 3.0 : 1.0 / 6.0;
+                        const int A = p.facets[3 * f + size_t(a)];
+                        for (int i = 0; i < 3; ++i)
+                            un += sa * c->g_h[(size_t(A) * 3 + size_t(i)) * size_t(N) + size_t(m)] *
+                                  p.normals[3 * f + size_t(i)];
+                    }
+                    q += w * un;
+                }
+            }
+            u_c = std::max(u_c, std::fabs(q) / p.area);
+        }
+    }
+    double dt = cfg->pseudo_dt;
+    if (!(dt > 0.0))
+        dt = u_c <= 0.0 ? c->period / double(N) : c->h_c / u_c;
+    if (!has_inlet)
+        return finish(fail(c, HBGPU_ERR_GEOMETRY, "CFL number needs a Dirichlet inlet patch with positive area"));
+    inf.pseudo_dt = dt;
+    inf.cfl = u_c * dt / c->h_c;
+    c->tau_mode = cfg->tau_mode;
+    c->pseudo_dt = dt;
+    c->backflow_tangent = cfg->backflow_in_tangent;
+
+    {
+        Timer t;
+        TRY(mass_dev(c));
+        CK(c, cudaStreamSynchronize(st));
+        inf.assembly_seconds += t.seconds();
+    }
+    const double target = std::pow(10.0, -cfg->newton_tol_orders);
+    double r0 = 0.0;
+    std::vector<double> hist;
+    for (int iter = 0; iter <= cfg->max_newton_iters; ++iter) {
+        Timer t_iter;
+        Timer t0;
+        int s = residual_dev(c, c->state.p, c->r.p);
+        if (s != HBGPU_OK)
+            return finish(s);
+        double res = 0.0;
+        s = dot_dev(c, c->r.p, c->r.p, n, &res, true);
+        if (s != HBGPU_OK)
+            return finish(s);
+        s = check_flag(c);
+        if (s != HBGPU_OK)
+            return finish(s);
+        inf.assembly_seconds += t0.seconds();
+        if (!std::isfinite(res)) {
+            log(iter, res, res / (r0 > 0 ? r0 : 1.0), 0, t_iter.seconds());
+            return finish(fail(c, HBGPU_ERR_DIVERGENCE, "residual is not finite at iteration " + std::to_string(iter)));
+        }
+        if (iter == 0)
+            r0 = res;
+        const double rel = iter == 0 ? 1.0 : (r0 > 0.0 ? res / r0 : 0.0);
+        if (r0 <= 1e-30 || rel <= target) {
+            log(iter, res, rel, 0, t_iter.seconds());
+            inf.converged = 1;
+            break;
+        }
+        if (rel > cfg->divergence_ratio) {
+            log(iter, res, rel, 0, t_iter.seconds());
+            return finish(fail(c, HBGPU_ERR_DIVERGENCE, "nonlinear solve diverged: residual ratio " +
+                                                             std::to_string(rel) + " at iteration " +
+                                                             std::to_string(iter)));
+        }
+        if (iter == cfg->max_newton_iters) {
+            log(iter, res, rel, 0, t_iter.seconds());
+            break;
+        }
+        Timer t1;
+        s = tangent_dev(c, c->state.p);
+        if (s == HBGPU_OK)
+            s = check_flag(c);
+        if (s != HBGPU_OK)
+            return finish(s);
+        inf.assembly_seconds += t1.seconds();
+        Timer t2;
+        s = jacobi_dev(c, nullptr);
+        hbgpu_krylov_result kr{};
+        if (s == HBGPU_OK)
+            s = gmres_dev(c, c->r.p, c->inv.p, &cfg->krylov, c->x.p, &kr, nullptr, 0);
+        if (s != HBGPU_OK)
+            return finish(s);
+        inf.linear_seconds += t2.seconds();
+        if (kr.status == 2)
+            return finish(fail(c, HBGPU_ERR_STAGNATION,
+                               "GMRES stagnated at Newton iteration " + std::to_string(iter) +
+                                   " (relative residual " + std::to_string(kr.relative_residual) + ")"));
+        launch_newton_update(c->x.p, c->dir.p, c->nn, N, c->state.p, st);
+        TRY(check_launch(c));
+        CK(c, cudaStreamSynchronize(st));
+        log(iter, res, rel, kr.iterations, t_iter.seconds());
+    }
+    return finish(HBGPU_OK);
+}
+
+}  // extern "C"

@@ -1,0 +1,129 @@
+// Internal definitions shared by the kernels (hbgpu_kernels.cu) and the host
+// runtime / C ABI (hbgpu_host.cu).  Not part of the public interface.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+namespace hbgpu {
+
+// 4-point tet Gauss rule (reference assembly.cpp:15-20).
+constexpr double kQA = 0.5854101966249684544613761;
+constexpr double kQB = 0.1381966011250105151795414;
+// Gauss-Seidel block: number of partial sums of the deterministic reductions.
+constexpr int kRedBlocks = 592;  // 4 x 148 SMs
+constexpr int kRedThreads = 256;
+
+// ---------------------------------------------------------------- kernel args
+
+struct ResidualArgs {
+    const int4* conn;
+    const double* geom;   // 22 doubles / element
+    const double* state;  // (A*4+c)*N+n
+    const double* hu;     // (A*3+i)*N+n
+    double* r;            // (A*4+c)*N+n, accumulated
+    double* s;            // (A*3+i)*N+n, accumulated
+    int N;
+    double rho, mu, nu;
+    int tau_mode;
+    int* flag;  // bit0: singular tau
+};
+
+struct TangentArgs {
+    const int4* conn;
+    const double* geom;
+    const double* state;
+    const uint8_t* edmask;   // per element: bit b = node b Dirichlet
+    const uint8_t* dir;      // per node
+    const int* row_ptr;
+    const int* inc_ptr;      // per node, into inc_elem / inc_cols
+    const uint32_t* inc_elem;  // e | a<<30
+    const uint32_t* inc_cols;  // 4 x uint8 block offset within the row
+    const int* cta_rows;     // row range per CTA
+    double* pvals;
+    int N;
+    double rho, mu, nu, pseudo_c;
+    int tau_mode;
+    int* flag;
+};
+
+struct MatvecArgs {
+    const int* row_ptr;
+    const int* col_idx;
+    const double* vals;
+    const double* mass;
+    const uint8_t* dir;
+    const double* H;
+    const double* y;
+    double* out;
+    const double* scale;  // optional split scaling: out = S L (S y)
+    int nn, N, rows_per_cta;
+    int with_c;
+};
+
+struct BoundaryArgs {
+    const int* bnode;       // boundary node ids
+    const int* bptr;        // per boundary node, into binc
+    const int* binc;        // facet*4 + v
+    const int* fac;         // facet nodes (3)
+    const double* fnormal;  // 3
+    const double* farea;
+    const int* fbc;         // Neumann entry of the facet
+    const double* h;        // nbc*N
+    const uint8_t* dir;
+    const double* state;
+    double* r;
+    int nbnodes, N;
+    double rho, beta;
+};
+
+// ---------------------------------------------------------------- launchers
+// (defined in hbgpu_kernels.cu; all asynchronous on `st`)
+
+void launch_geometry(const double* xyz, const int4* conn, int ne, double* geom, int* flag,
+                     cudaStream_t st);
+void launch_apply_h_series(const double* H, int N, const double* in, int in_node_stride,
+                           double* out, int out_node_stride, int nnodes, cudaStream_t st);
+void launch_residual_color(const ResidualArgs& a, const int* elems, int count, cudaStream_t st);
+void launch_residual_finalize(const double* H, int N, const double* s, const uint8_t* dir,
+                              double* r, int nn, cudaStream_t st);
+void launch_boundary(const BoundaryArgs& a, cudaStream_t st);
+cudaError_t configure_tangent_smem(size_t bytes);
+void launch_tangent_rows(const TangentArgs& a, int nctas, int threads, size_t smem,
+                         cudaStream_t st);
+void launch_mass_rows(const int4* conn, const double* geom, const int* row_ptr,
+                      const int* inc_ptr, const uint32_t* inc_elem, const uint32_t* inc_cols,
+                      double rho, double* mass, int nn, cudaStream_t st);
+void launch_matvec(const MatvecArgs& a, cudaStream_t st);
+void launch_jacobi(const double* vals, const int* diag_blk, int nn, int N, double* inv_diag,
+                   int* degenerate, cudaStream_t st);
+void launch_install_dirichlet(const double* g, const uint8_t* dir, int nn, int N, double* state,
+                              cudaStream_t st);
+void launch_fill_pressure(double p0, int nn, int N, double* state, cudaStream_t st);
+void launch_newton_update(const double* dx, const uint8_t* dir, int nn, int N, double* state,
+                          cudaStream_t st);
+
+// vectors (length n), deterministic reductions
+void launch_sqrt_abs(const double* in, double* out, long n, cudaStream_t st);
+void launch_mul(const double* a, const double* b, double* out, long n, cudaStream_t st);
+void launch_scaled_diff(const double* s, const double* a, const double* b, double* out, long n,
+                        cudaStream_t st);  // out = s*(a-b)
+void launch_scale_copy(const double* in, const double* alpha_dev, int inv, double* out, long n,
+                       cudaStream_t st);  // out = in * alpha or in / alpha
+// partial[i*kRedBlocks + b] = block b's share of <V_i, w>, i < nv.
+void launch_multidot(const double* V, long ld, int nv, const double* w, long n, double* partial,
+                     cudaStream_t st);
+// out[i] = sum_b partial[i*kRedBlocks+b] (fixed order); optional sqrt of out[0]
+void launch_reduce_partials(const double* partial, int nv, double* out, int take_sqrt,
+                            cudaStream_t st);
+// w -= sum_i h[i] V_i
+void launch_gemv_sub(const double* V, long ld, int nv, const double* h, double* w, long n,
+                     cudaStream_t st);
+// x += s * sum_i y[i] V_i
+void launch_gemv_add_scaled(const double* V, long ld, int nv, const double* y, const double* s,
+                            double* x, long n, cudaStream_t st);
+
+}  // namespace hbgpu

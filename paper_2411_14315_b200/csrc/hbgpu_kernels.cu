@@ -1,0 +1,880 @@
+// CUDA kernels of the B200-native HB-GLS hot path (sm_100a, FP64).
+//
+// Reference (CPU C++, /root/reference/proj) loops being replaced:
+//   element_residual + scatter   src/assembly.cpp:141-263, 465-521
+//   nodal H passes               src/assembly.cpp:453-463, 523-535 (FFTW there, dense N x N here)
+//   boundary terms               src/assembly.cpp:376-413
+//   element_tangent_p + scatter  src/assembly.cpp:265-374, 550-666
+//   assemble_mass                src/assembly.cpp:668-681
+//   TangentOperator::matvec      src/linalg.cpp:41-128
+//   jacobi_preconditioner        src/linalg.cpp:130-154
+//   gmres_solve vector work      src/linalg.cpp:167-293
+//
+// Every kernel is deterministic: no floating-point atomics, fixed reduction
+// trees, fixed summation order per output (element order for the tangent /
+// mass, colour order for the residual).
+#include "hbgpu_internal.h"
+
+namespace hbgpu {
+
+namespace {
+
+__device__ __forceinline__ double ldg(const double* p) { return __ldg(p); }
+
+struct Geo {
+    double gN[4][3];
+    double V;
+    double xi[9];
+};
+
+__device__ __forceinline__ void load_geo(const double* __restrict__ g, Geo& G) {
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int j = 0; j < 3; ++j)
+            G.gN[a][j] = ldg(g + 3 * a + j);
+    G.V = ldg(g + 12);
+#pragma unroll
+    for (int k = 0; k < 9; ++k)
+        G.xi[k] = ldg(g + 13 + k);
+}
+
+// tau = (u.xi.u + 3 nu^2 xi:xi)^(-1/2)   (assembly.cpp:43-56).  A non-positive
+// argument is the reference's std::domain_error; flagged, tau set to 0.
+__device__ __forceinline__ double tau_of(const Geo& G, const double u[3], double diff,
+                                         int* flag) {
+    double conv = 0.0;
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+        const double xu = G.xi[3 * i + 0] * u[0] + G.xi[3 * i + 1] * u[1] + G.xi[3 * i + 2] * u[2];
+        conv += u[i] * xu;
+    }
+    const double arg = conv + diff;
+    if (!(arg > 0.0)) {
+        atomicOr(flag, 1);
+        return 0.0;
+    }
+    return rsqrt(arg);
+}
+
+__device__ __forceinline__ double xi_dd(const Geo& G) {
+    double s = 0.0;
+#pragma unroll
+    for (int k = 0; k < 9; ++k)
+        s += G.xi[k] * G.xi[k];
+    return s;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------- geometry
+
+// element_geometry (mesh.cpp:159-203), one thread per element.
+__global__ void geometry_kernel(const double* __restrict__ xyz, const int4* __restrict__ conn,
+                                int ne, double* __restrict__ geom, int* flag) {
+    const int e = blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= ne)
+        return;
+    const int4 c = conn[e];
+    const int nd[4] = {c.x, c.y, c.z, c.w};
+    double x[4][3];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int i = 0; i < 3; ++i)
+            x[a][i] = xyz[3 * (long)nd[a] + i];
+    double c0[3], c1[3], c2[3];
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+        c0[i] = x[1][i] - x[0][i];
+        c1[i] = x[2][i] - x[0][i];
+        c2[i] = x[3][i] - x[0][i];
+    }
+    const double det = c0[0] * (c1[1] * c2[2] - c1[2] * c2[1]) -
+                       c1[0] * (c0[1] * c2[2] - c0[2] * c2[1]) +
+                       c2[0] * (c0[1] * c1[2] - c0[2] * c1[1]);
+    double* g = geom + 22 * (long)e;
+    g[12] = det / 6.0;
+    if (!(det / 6.0 > 0.0))
+        atomicOr(flag, 2);
+    const double r0[3] = {c1[1] * c2[2] - c1[2] * c2[1], c1[2] * c2[0] - c1[0] * c2[2],
+                          c1[0] * c2[1] - c1[1] * c2[0]};
+    const double r1[3] = {c2[1] * c0[2] - c2[2] * c0[1], c2[2] * c0[0] - c2[0] * c0[2],
+                          c2[0] * c0[1] - c2[1] * c0[0]};
+    const double r2[3] = {c0[1] * c1[2] - c0[2] * c1[1], c0[2] * c1[0] - c0[0] * c1[2],
+                          c0[0] * c1[1] - c0[1] * c1[0]};
+    double j[3][3];
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+        j[0][i] = r0[i] / det;
+        j[1][i] = r1[i] / det;
+        j[2][i] = r2[i] / det;
+    }
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+        g[3 * 1 + i] = j[0][i];
+        g[3 * 2 + i] = j[1][i];
+        g[3 * 3 + i] = j[2][i];
+        g[i] = -(j[0][i] + j[1][i] + j[2][i]);
+    }
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+        for (int b = 0; b < 3; ++b)
+            g[13 + 3 * a + b] = j[0][a] * j[0][b] + j[1][a] * j[1][b] + j[2][a] * j[2][b];
+}
+
+void launch_geometry(const double* xyz, const int4* conn, int ne, double* geom, int* flag,
+                     cudaStream_t st) {
+    if (ne <= 0)
+        return;
+    geometry_kernel<<<(ne + 255) / 256, 256, 0, st>>>(xyz, conn, ne, geom, flag);
+}
+
+// ---------------------------------------------------------------- nodal H
+
+// out[(A*os + i*N) + n] = sum_m H[n][m] in[(A*is + i*N) + m], i < 3: the
+// batched pseudo-spectral derivative of every velocity series
+// (assembly.cpp:453-463; SpectralOperators::apply_many, spectral.cpp:185-227).
+__global__ void apply_h_series_kernel(const double* __restrict__ H, int N,
+                                      const double* __restrict__ in, int is,
+                                      double* __restrict__ out, int os, int nnodes) {
+    extern __shared__ double sh[];
+    double* sH = sh;
+    for (int k = threadIdx.x; k < N * N; k += blockDim.x)
+        sH[k] = H[k];
+    __syncthreads();
+    const int per = blockDim.x / N;
+    const int ls = threadIdx.x / N, n = threadIdx.x - ls * N;
+    const long s = (long)blockIdx.x * per + ls;
+    if (ls >= per || s >= 3L * nnodes)
+        return;
+    const long A = s / 3;
+    const int i = (int)(s - 3 * A);
+    const double* src = in + A * is + (long)i * N;
+    double acc = 0.0;
+    for (int m = 0; m < N; ++m)
+        acc += sH[n * N + m] * src[m];
+    out[A * os + (long)i * N + n] = acc;
+}
+
+void launch_apply_h_series(const double* H, int N, const double* in, int in_node_stride,
+                           double* out, int out_node_stride, int nnodes, cudaStream_t st) {
+    const int per = (N >= 256) ? 1 : 256 / N;
+    const long nser = 3L * nnodes;
+    const int blocks = (int)((nser + per - 1) / per);
+    apply_h_series_kernel<<<blocks, per * N, sizeof(double) * N * N, st>>>(
+        H, N, in, in_node_stride, out, out_node_stride, nnodes);
+}
+
+// ---------------------------------------------------------------- residual
+
+// One (element, time sample) per thread, all elements of one colour class:
+// no two elements of a class share a node, so the scatter is a plain
+// read-modify-write (deterministic: each node sums its elements in colour
+// order).  Element residual of assembly.cpp:141-263 with the per-node sums
+// hoisted: u_q = B*sum_a u_a + (A-B)*u_q (same for Hu).
+__global__ void __launch_bounds__(256) residual_color_kernel(ResidualArgs a,
+                                                             const int* __restrict__ elems,
+                                                             int count) {
+    const int N = a.N;
+    const long t = (long)blockIdx.x * blockDim.x + threadIdx.x;
+    const int k = (int)(t / N);
+    const int n = (int)(t - (long)k * N);
+    if (k >= count)
+        return;
+    const int e = elems[k];
+    const int4 c = __ldg(&a.conn[e]);
+    const int nd[4] = {c.x, c.y, c.z, c.w};
+    Geo G;
+    load_geo(a.geom + 22 * (long)e, G);
+
+    double u[4][3], hu[4][3], p[4];
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+        const double* sb = a.state + (long)nd[b] * 4 * N + n;
+        const double* hb = a.hu + (long)nd[b] * 3 * N + n;
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {
+            u[b][i] = ldg(sb + i * N);
+            hu[b][i] = ldg(hb + i * N);
+        }
+        p[b] = ldg(sb + 3 * N);
+    }
+    const double rho = a.rho, V = G.V, w = 0.25 * V;
+
+    // element_fields (assembly.cpp:92-118)
+    double gu[3][3], gp[3];
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+#pragma unroll
+        for (int j = 0; j < 3; ++j)
+            gu[i][j] = G.gN[0][j] * u[0][i] + G.gN[1][j] * u[1][i] + G.gN[2][j] * u[2][i] +
+                       G.gN[3][j] * u[3][i];
+        gp[i] = G.gN[0][i] * p[0] + G.gN[1][i] * p[1] + G.gN[2][i] * p[2] + G.gN[3][i] * p[3];
+    }
+    const double div = gu[0][0] + gu[1][1] + gu[2][2];
+    const double psum = p[0] + p[1] + p[2] + p[3];
+    double usum[3], hsum[3];
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+        usum[i] = u[0][i] + u[1][i] + u[2][i] + u[3][i];
+        hsum[i] = hu[0][i] + hu[1][i] + hu[2][i] + hu[3][i];
+    }
+
+    // constant-gradient Galerkin rows (assembly.cpp:156-192):
+    // mu V gradN_a.grad u_i - dN_a/dx_i (V/4) sum p + rho sum_b M_ab Hu_b,i
+    double rm[4][3], sv[4][3], rc[4];
+    const double muV = a.mu * V, moff = rho * V / 20.0;
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {
+            rm[b][i] = muV * (G.gN[b][0] * gu[i][0] + G.gN[b][1] * gu[i][1] +
+                              G.gN[b][2] * gu[i][2]) -
+                       G.gN[b][i] * w * psum + moff * (hsum[i] + hu[b][i]);
+            sv[b][i] = 0.0;
+        }
+        rc[b] = w * div;
+    }
+
+    const double diff = 3.0 * a.nu * a.nu * xi_dd(G);
+    double tau_mean = 0.0;
+    if (a.tau_mode == 1) {
+        const double um[3] = {0.25 * usum[0], 0.25 * usum[1], 0.25 * usum[2]};
+        tau_mean = tau_of(G, um, diff, a.flag);
+    }
+    const double dAB = kQA - kQB, wr = w / rho;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        double uq[3], huq[3];
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {
+            uq[i] = kQB * usum[i] + dAB * u[q][i];
+            huq[i] = kQB * hsum[i] + dAB * hu[q][i];
+        }
+        const double tau = a.tau_mode == 0 ? tau_of(G, uq, diff, a.flag) : tau_mean;
+        double conv[3], tl[3];
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {
+            conv[i] = uq[0] * gu[i][0] + uq[1] * gu[i][1] + uq[2] * gu[i][2];
+            tl[i] = tau * (rho * huq[i] + rho * conv[i] + gp[i]);  // tau * strong residual
+        }
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+            const double sa = (b == q) ? kQA : kQB;
+            const double adv = uq[0] * G.gN[b][0] + uq[1] * G.gN[b][1] + uq[2] * G.gN[b][2];
+#pragma unroll
+            for (int i = 0; i < 3; ++i) {
+                rm[b][i] += w * (rho * sa * conv[i] + adv * tl[i]);
+                sv[b][i] += w * sa * tl[i];
+            }
+            rc[b] += wr * (G.gN[b][0] * tl[0] + G.gN[b][1] * tl[1] + G.gN[b][2] * tl[2]);
+        }
+    }
+
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+        double* rb = a.r + (long)nd[b] * 4 * N + n;
+        double* sb = a.s + (long)nd[b] * 3 * N + n;
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {
+            rb[i * N] += rm[b][i];
+            sb[i * N] += sv[b][i];
+        }
+        rb[3 * N] += rc[b];
+    }
+}
+
+void launch_residual_color(const ResidualArgs& a, const int* elems, int count, cudaStream_t st) {
+    if (count <= 0)
+        return;
+    const long threads = (long)count * a.N;
+    residual_color_kernel<<<(int)((threads + 255) / 256), 256, 0, st>>>(a, elems, count);
+}
+
+// r_u -= H s, then zero the Dirichlet velocity rows (assembly.cpp:523-535,541-544).
+__global__ void residual_finalize_kernel(const double* __restrict__ H, int N,
+                                         const double* __restrict__ s,
+                                         const uint8_t* __restrict__ dir, double* __restrict__ r,
+                                         int nn) {
+    extern __shared__ double sh[];
+    for (int k = threadIdx.x; k < N * N; k += blockDim.x)
+        sh[k] = H[k];
+    __syncthreads();
+    const int per = blockDim.x / N;
+    const int ls = threadIdx.x / N, n = threadIdx.x - ls * N;
+    const long sr = (long)blockIdx.x * per + ls;
+    if (ls >= per || sr >= 3L * nn)
+        return;
+    const long A = sr / 3;
+    const int i = (int)(sr - 3 * A);
+    double* out = r + A * 4 * N + (long)i * N + n;
+    if (dir[A]) {
+        *out = 0.0;
+        return;
+    }
+    const double* src = s + sr * N;
+    double acc = 0.0;
+    for (int m = 0; m < N; ++m)
+        acc += sh[n * N + m] * src[m];
+    *out -= acc;
+}
+
+void launch_residual_finalize(const double* H, int N, const double* s, const uint8_t* dir,
+                              double* r, int nn, cudaStream_t st) {
+    const int per = (N >= 256) ? 1 : 256 / N;
+    const long nser = 3L * nn;
+    residual_finalize_kernel<<<(int)((nser + per - 1) / per), per * N,
+                               sizeof(double) * N * N, st>>>(H, N, s, dir, r, nn);
+}
+
+// Neumann traction + backflow (assembly.cpp:376-413), node-centric: one
+// thread per (boundary node, n) sums its incident facets in the reference's
+// order (Neumann entry, then facet).  Dirichlet nodes are skipped because
+// their velocity rows end at zero (assembly.cpp:541-544).
+__global__ void boundary_kernel(BoundaryArgs a) {
+    const int N = a.N;
+    const long t = (long)blockIdx.x * blockDim.x + threadIdx.x;
+    const int bn = (int)(t / N);
+    const int n = (int)(t - (long)bn * N);
+    if (bn >= a.nbnodes)
+        return;
+    const int A = a.bnode[bn];
+    if (a.dir[A])
+        return;
+    double acc[3] = {0.0, 0.0, 0.0};
+    for (int k = a.bptr[bn]; k < a.bptr[bn + 1]; ++k) {
+        const int f = a.binc[k] >> 2, v = a.binc[k] & 3;
+        const int f0 = a.fac[3 * f], f1 = a.fac[3 * f + 1], f2 = a.fac[3 * f + 2];
+        const double nv[3] = {a.fnormal[3 * f], a.fnormal[3 * f + 1], a.fnormal[3 * f + 2]};
+        const double w = a.farea[f] / 3.0;
+        const double hn = a.h[(long)a.fbc[f] * N + n];
+        double uf[3][3];
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {
+            uf[0][i] = a.state[((long)f0 * 4 + i) * N + n];
+            uf[1][i] = a.state[((long)f1 * 4 + i) * N + n];
+            uf[2][i] = a.state[((long)f2 * 4 + i) * N + n];
+        }
+        for (int q = 0; q < 3; ++q) {
+            double uq[3];
+#pragma unroll
+            for (int i = 0; i < 3; ++i)
+                uq[i] = (q == 0 ? 2.0 / 3.0 : 1.0 / 6.0) * uf[0][i] +
+                        (q == 1 ? 2.0 / 3.0 : 1.0 / 6.0) * uf[1][i] +
+                        (q == 2 ? 2.0 / 3.0 : 1.0 / 6.0) * uf[2][i];
+            const double un = uq[0] * nv[0] + uq[1] * nv[1] + uq[2] * nv[2];
+            const double neg = un < 0.0 ? un : 0.0;
+            const double sa = (q == v) ? 2.0 / 3.0 : 1.0 / 6.0;
+#pragma unroll
+            for (int i = 0; i < 3; ++i)
+                acc[i] += w * sa * (-hn * nv[i] - 0.5 * a.rho * a.beta * neg * uq[i]);
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+        a.r[((long)A * 4 + i) * N + n] += acc[i];
+}
+
+void launch_boundary(const BoundaryArgs& a, cudaStream_t st) {
+    if (a.nbnodes <= 0)
+        return;
+    const long threads = (long)a.nbnodes * a.N;
+    boundary_kernel<<<(int)((threads + 255) / 256), 256, 0, st>>>(a);
+}
+
+// ---------------------------------------------------------------- tangent
+
+// Row-owned assembly of the pointwise tangent P (assembly.cpp:265-374,
+// 550-666).  A CTA owns a contiguous range of block rows; its shared memory
+// holds exactly the P.vals segment of those rows ([blk][slot][n], the global
+// layout), so the block values are accumulated on chip and written once,
+// coalesced.  Thread (row A, sample n) walks the elements containing A in
+// element order (the reference's summation order per block) and adds that
+// element's contribution to the 4 blocks (A, conn[e][b]).
+//
+// Per element and sample the q-sums factor through 8 scalars:
+//   K_ab = kc_ab + kappa_a . gradN_b,  kappa_a = w rho sum_q (N_a(q) + tau_q adv_a(q)) u_q
+//   G_ab = -dN_a V/4 + alpha_a gradN_b, alpha_a = w sum_q tau_q adv_a(q)
+//   D_ab = dN_b V/4 + dN_a (w z . gradN_b), z = sum_q tau_q u_q
+//   L_ab = gradN_a.gradN_b * (w/rho) sum_q tau_q
+__global__ void __launch_bounds__(256) tangent_rows_kernel(TangentArgs a) {
+    extern __shared__ double sm[];
+    const int N = a.N;
+    const int row_lo = a.cta_rows[blockIdx.x], row_hi = a.cta_rows[blockIdx.x + 1];
+    const long blk_lo = a.row_ptr[row_lo];
+    const long nvals = ((long)a.row_ptr[row_hi] - blk_lo) * 8 * N;
+    for (long k = threadIdx.x; k < nvals; k += blockDim.x)
+        sm[k] = 0.0;
+    __syncthreads();
+
+    const int r = threadIdx.x / N, n = threadIdx.x - r * N;
+    const int A = row_lo + r;
+    if (A < row_hi) {
+        const long rowoff = (long)a.row_ptr[A] - blk_lo;
+        const double rho = a.rho;
+        long diag_local = -1;
+        for (int ii = a.inc_ptr[A]; ii < a.inc_ptr[A + 1]; ++ii) {
+            const uint32_t ie = __ldg(&a.inc_elem[ii]);
+            const int e = (int)(ie & 0x3FFFFFFFu);
+            const int la = (int)(ie >> 30);
+            const uint32_t cols = __ldg(&a.inc_cols[ii]);
+            const int em = a.edmask[e];
+            const int4 c = __ldg(&a.conn[e]);
+            const int nd[4] = {c.x, c.y, c.z, c.w};
+            Geo G;
+            load_geo(a.geom + 22 * (long)e, G);
+            double u[4][3];
+#pragma unroll
+            for (int b = 0; b < 4; ++b) {
+                const double* sb = a.state + (long)nd[b] * 4 * N + n;
+#pragma unroll
+                for (int i = 0; i < 3; ++i)
+                    u[b][i] = ldg(sb + i * N);
+            }
+            const double V = G.V, w = 0.25 * V;
+            double usum[3];
+#pragma unroll
+            for (int i = 0; i < 3; ++i)
+                usum[i] = u[0][i] + u[1][i] + u[2][i] + u[3][i];
+            const double diff = 3.0 * a.nu * a.nu * xi_dd(G);
+            double tau_mean = 0.0;
+            if (a.tau_mode == 1) {
+                const double um[3] = {0.25 * usum[0], 0.25 * usum[1], 0.25 * usum[2]};
+                tau_mean = tau_of(G, um, diff, a.flag);
+            }
+            double ga[3];
+#pragma unroll
+            for (int i = 0; i < 3; ++i)
+                ga[i] = (la == 0) ? G.gN[0][i] : (la == 1) ? G.gN[1][i] : (la == 2) ? G.gN[2][i] : G.gN[3][i];
+            double asum = 0.0, tsum = 0.0, z[3] = {0.0, 0.0, 0.0}, kap[3] = {0.0, 0.0, 0.0};
+            const double dAB = kQA - kQB;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                double uq[3];
+#pragma unroll
+                for (int i = 0; i < 3; ++i)
+                    uq[i] = kQB * usum[i] + dAB * u[q][i];
+                const double tq = a.tau_mode == 0 ? tau_of(G, uq, diff, a.flag) : tau_mean;
+                const double adv = uq[0] * ga[0] + uq[1] * ga[1] + uq[2] * ga[2];
+                const double tadv = tq * adv;
+                const double na = (q == la) ? kQA : kQB;
+                asum += tadv;
+                tsum += tq;
+#pragma unroll
+                for (int i = 0; i < 3; ++i) {
+                    z[i] += tq * uq[i];
+                    kap[i] += (na + tadv) * uq[i];
+                }
+            }
+            const double alpha_a = w * asum, beta = (w / rho) * tsum, wr = w * rho;
+            const bool afix = (em >> la) & 1;
+#pragma unroll
+            for (int b = 0; b < 4; ++b) {
+                const int j = (cols >> (8 * b)) & 0xFF;
+                double* acc = sm + (rowoff + j) * 8 * N + n;
+                const bool bfix = (em >> b) & 1;
+                const double* gb = G.gN[b];
+                const double gg = ga[0] * gb[0] + ga[1] * gb[1] + ga[2] * gb[2];
+                if (!afix && !bfix) {
+                    const double kc = a.mu * V * gg + a.pseudo_c * (b == la ? V / 10.0 : V / 20.0);
+                    acc[0] += kc + wr * (kap[0] * gb[0] + kap[1] * gb[1] + kap[2] * gb[2]);
+                }
+                if (!afix) {
+#pragma unroll
+                    for (int i = 0; i < 3; ++i)
+                        acc[(1 + i) * N] += -ga[i] * w + alpha_a * gb[i];
+                }
+                if (!bfix) {
+                    const double alpha_b = w * (z[0] * gb[0] + z[1] * gb[1] + z[2] * gb[2]);
+#pragma unroll
+                    for (int i = 0; i < 3; ++i)
+                        acc[(4 + i) * N] += gb[i] * w + ga[i] * alpha_b;
+                }
+                acc[7 * N] += gg * beta;
+                if (b == la)
+                    diag_local = rowoff + j;
+            }
+        }
+        // identity on constrained velocity diagonals (assembly.cpp:659-665)
+        if (a.dir[A] && diag_local >= 0)
+            sm[diag_local * 8 * N + n] = 1.0;
+    }
+    __syncthreads();
+    double* dst = a.pvals + blk_lo * 8 * N;
+    const double2* s2 = reinterpret_cast<const double2*>(sm);
+    double2* d2 = reinterpret_cast<double2*>(dst);
+    for (long k = threadIdx.x; k < nvals / 2; k += blockDim.x)
+        d2[k] = s2[k];
+}
+
+cudaError_t configure_tangent_smem(size_t bytes) {
+    return cudaFuncSetAttribute(tangent_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                int(bytes < 48 * 1024 ? 48 * 1024 : bytes));
+}
+
+void launch_tangent_rows(const TangentArgs& a, int nctas, int threads, size_t smem,
+                         cudaStream_t st) {
+    if (nctas <= 0)
+        return;
+    tangent_rows_kernel<<<nctas, threads, smem, st>>>(a);
+}
+
+// assemble_mass (assembly.cpp:668-681), row-owned: each block row sums its
+// elements in element order — the reference's order, hence bit-identical.
+__global__ void mass_rows_kernel(const int4* __restrict__ conn, const double* __restrict__ geom,
+                                 const int* __restrict__ row_ptr, const int* __restrict__ inc_ptr,
+                                 const uint32_t* __restrict__ inc_elem,
+                                 const uint32_t* __restrict__ inc_cols, double rho,
+                                 double* __restrict__ mass, int nn) {
+    const int A = blockIdx.x * blockDim.x + threadIdx.x;
+    if (A >= nn)
+        return;
+    double* m = mass + row_ptr[A];
+    for (int k = row_ptr[A]; k < row_ptr[A + 1]; ++k)
+        mass[k] = 0.0;
+    for (int ii = inc_ptr[A]; ii < inc_ptr[A + 1]; ++ii) {
+        const uint32_t ie = inc_elem[ii];
+        const int e = (int)(ie & 0x3FFFFFFFu), la = (int)(ie >> 30);
+        const uint32_t cols = inc_cols[ii];
+        const double V = geom[22 * (long)e + 12];
+        const double diag = rho * V / 10.0, off = rho * V / 20.0;
+        for (int b = 0; b < 4; ++b)
+            m[(cols >> (8 * b)) & 0xFF] += (b == la) ? diag : off;
+    }
+}
+
+void launch_mass_rows(const int4* conn, const double* geom, const int* row_ptr,
+                      const int* inc_ptr, const uint32_t* inc_elem, const uint32_t* inc_cols,
+                      double rho, double* mass, int nn, cudaStream_t st) {
+    if (nn <= 0)
+        return;
+    mass_rows_kernel<<<(nn + 127) / 128, 128, 0, st>>>(conn, geom, row_ptr, inc_ptr, inc_elem,
+                                                       inc_cols, rho, mass, nn);
+}
+
+// ---------------------------------------------------------------- operator
+
+// Fused L-matvec (linalg.cpp:78-128): out_A = sum_k P_k y_col(k)
+//   + [A free] H * sum_{k: col free} m_k y_col(k)[velocity].
+// Thread (row, n); the N threads of a row exchange the mass-gathered series
+// through shared memory for the dense H product.  Optional split scaling
+// (gmres_solve's S A S, linalg.cpp:214-219) is fused on load and store.
+__global__ void __launch_bounds__(256) matvec_kernel(MatvecArgs a) {
+    extern __shared__ double sh[];
+    const int N = a.N;
+    double* sH = sh;
+    double* st = sh + (a.with_c ? N * N : 0);
+    if (a.with_c)
+        for (int k = threadIdx.x; k < N * N; k += blockDim.x)
+            sH[k] = a.H[k];
+    const int r = threadIdx.x / N, n = threadIdx.x - r * N;
+    const int A = blockIdx.x * a.rows_per_cta + r;
+    const bool valid = (r < a.rows_per_cta) && (A < a.nn);
+    double ou0 = 0.0, ou1 = 0.0, ou2 = 0.0, op = 0.0, t0 = 0.0, t1 = 0.0, t2 = 0.0;
+    bool afree = false;
+    if (valid) {
+        afree = !a.dir[A];
+        const int kb = a.row_ptr[A], ke = a.row_ptr[A + 1];
+        for (int k = kb; k < ke; ++k) {
+            const int B = __ldg(&a.col_idx[k]);
+            const double* v = a.vals + (long)k * 8 * N + n;
+            const long yb = (long)B * 4 * N + n;
+            double y0 = ldg(a.y + yb), y1 = ldg(a.y + yb + N), y2 = ldg(a.y + yb + 2 * N),
+                   y3 = ldg(a.y + yb + 3 * N);
+            if (a.scale) {
+                y0 *= ldg(a.scale + yb);
+                y1 *= ldg(a.scale + yb + N);
+                y2 *= ldg(a.scale + yb + 2 * N);
+                y3 *= ldg(a.scale + yb + 3 * N);
+            }
+            const double kd = ldg(v);
+            ou0 += kd * y0 + ldg(v + 1 * N) * y3;
+            ou1 += kd * y1 + ldg(v + 2 * N) * y3;
+            ou2 += kd * y2 + ldg(v + 3 * N) * y3;
+            op += ldg(v + 4 * N) * y0;
+            op += ldg(v + 5 * N) * y1;
+            op += ldg(v + 6 * N) * y2;
+            op += ldg(v + 7 * N) * y3;
+            if (a.with_c && afree && !a.dir[B]) {
+                const double m = ldg(a.mass + k);
+                t0 += m * y0;
+                t1 += m * y1;
+                t2 += m * y2;
+            }
+        }
+    }
+    if (a.with_c) {
+        if (valid) {
+            st[(r * 3 + 0) * N + n] = t0;
+            st[(r * 3 + 1) * N + n] = t1;
+            st[(r * 3 + 2) * N + n] = t2;
+        }
+        __syncthreads();
+        if (valid && afree) {
+            const double* h = sH + n * N;
+            const double* s0 = st + (r * 3) * N;
+            double h0 = 0.0, h1 = 0.0, h2 = 0.0;
+            for (int m = 0; m < N; ++m) {
+                const double hm = h[m];
+                h0 += hm * s0[m];
+                h1 += hm * s0[N + m];
+                h2 += hm * s0[2 * N + m];
+            }
+            ou0 += h0;
+            ou1 += h1;
+            ou2 += h2;
+        }
+    }
+    if (valid) {
+        const long o = (long)A * 4 * N + n;
+        if (a.scale) {
+            ou0 *= ldg(a.scale + o);
+            ou1 *= ldg(a.scale + o + N);
+            ou2 *= ldg(a.scale + o + 2 * N);
+            op *= ldg(a.scale + o + 3 * N);
+        }
+        a.out[o] = ou0;
+        a.out[o + N] = ou1;
+        a.out[o + 2 * N] = ou2;
+        a.out[o + 3 * N] = op;
+    }
+}
+
+void launch_matvec(const MatvecArgs& a, cudaStream_t st) {
+    if (a.nn <= 0)
+        return;
+    const int blocks = (a.nn + a.rows_per_cta - 1) / a.rows_per_cta;
+    const size_t smem = a.with_c ? sizeof(double) * ((size_t)a.N * a.N + 3 * (size_t)a.N * a.rows_per_cta) : 0;
+    matvec_kernel<<<blocks, a.rows_per_cta * a.N, smem, st>>>(a);
+}
+
+// jacobi_preconditioner (linalg.cpp:130-154)
+__global__ void jacobi_kernel(const double* __restrict__ vals, const int* __restrict__ diag_blk,
+                              int nn, int N, double* __restrict__ inv, int* degenerate) {
+    const long t = (long)blockIdx.x * blockDim.x + threadIdx.x;
+    const long total = (long)nn * 4 * N;
+    if (t >= total)
+        return;
+    const long A = t / (4L * N);
+    const int rem = (int)(t - A * 4 * N);
+    const int c = rem / N, n = rem - c * N;
+    const double d = vals[((long)diag_blk[A] * 8 + (c < 3 ? 0 : 7)) * N + n];
+    if (fabs(d) < 1e-30) {
+        inv[t] = 1.0;
+        atomicAdd(degenerate, 1);
+    } else {
+        inv[t] = 1.0 / d;
+    }
+}
+
+void launch_jacobi(const double* vals, const int* diag_blk, int nn, int N, double* inv_diag,
+                   int* degenerate, cudaStream_t st) {
+    const long total = (long)nn * 4 * N;
+    if (total <= 0)
+        return;
+    jacobi_kernel<<<(int)((total + 255) / 256), 256, 0, st>>>(vals, diag_blk, nn, N, inv_diag,
+                                                              degenerate);
+}
+
+// ---------------------------------------------------------------- state ops
+
+__global__ void install_dirichlet_kernel(const double* __restrict__ g, const uint8_t* dir, int nn,
+                                         int N, double* state) {
+    const long t = (long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= 3L * nn * N)
+        return;
+    const long A = t / (3L * N);
+    if (!dir[A])
+        return;
+    const int rem = (int)(t - A * 3 * N);
+    state[A * 4 * N + rem] = g[t];
+}
+
+void launch_install_dirichlet(const double* g, const uint8_t* dir, int nn, int N, double* state,
+                              cudaStream_t st) {
+    const long tot = 3L * nn * N;
+    if (tot <= 0)
+        return;
+    install_dirichlet_kernel<<<(int)((tot + 255) / 256), 256, 0, st>>>(g, dir, nn, N, state);
+}
+
+__global__ void fill_pressure_kernel(double p0, int nn, int N, double* state) {
+    const long t = (long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= (long)nn * N)
+        return;
+    const long A = t / N;
+    state[A * 4 * N + 3 * N + (t - A * N)] = p0;
+}
+
+void launch_fill_pressure(double p0, int nn, int N, double* state, cudaStream_t st) {
+    const long tot = (long)nn * N;
+    if (tot <= 0)
+        return;
+    fill_pressure_kernel<<<(int)((tot + 255) / 256), 256, 0, st>>>(p0, nn, N, state);
+}
+
+// y -= x except constrained velocity (hb_solver.cpp:205-215)
+__global__ void newton_update_kernel(const double* __restrict__ dx, const uint8_t* dir, int nn,
+                                     int N, double* state) {
+    const long t = (long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= 4L * nn * N)
+        return;
+    const long A = t / (4L * N);
+    const int c = (int)((t - A * 4 * N) / N);
+    if (dir[A] && c < 3)
+        return;
+    state[t] -= dx[t];
+}
+
+void launch_newton_update(const double* dx, const uint8_t* dir, int nn, int N, double* state,
+                          cudaStream_t st) {
+    const long tot = 4L * nn * N;
+    if (tot <= 0)
+        return;
+    newton_update_kernel<<<(int)((tot + 255) / 256), 256, 0, st>>>(dx, dir, nn, N, state);
+}
+
+// ---------------------------------------------------------------- vectors
+
+__global__ void sqrt_abs_kernel(const double* in, double* out, long n) {
+    for (long k = (long)blockIdx.x * blockDim.x + threadIdx.x; k < n;
+         k += (long)gridDim.x * blockDim.x)
+        out[k] = sqrt(fabs(in[k]));
+}
+void launch_sqrt_abs(const double* in, double* out, long n, cudaStream_t st) {
+    sqrt_abs_kernel<<<4 * 148, 256, 0, st>>>(in, out, n);
+}
+
+__global__ void mul_kernel(const double* a, const double* b, double* out, long n) {
+    for (long k = (long)blockIdx.x * blockDim.x + threadIdx.x; k < n;
+         k += (long)gridDim.x * blockDim.x)
+        out[k] = a[k] * b[k];
+}
+void launch_mul(const double* a, const double* b, double* out, long n, cudaStream_t st) {
+    mul_kernel<<<4 * 148, 256, 0, st>>>(a, b, out, n);
+}
+
+__global__ void scaled_diff_kernel(const double* s, const double* a, const double* b, double* out,
+                                   long n) {
+    for (long k = (long)blockIdx.x * blockDim.x + threadIdx.x; k < n;
+         k += (long)gridDim.x * blockDim.x)
+        out[k] = s[k] * (a[k] - b[k]);
+}
+void launch_scaled_diff(const double* s, const double* a, const double* b, double* out, long n,
+                        cudaStream_t st) {
+    scaled_diff_kernel<<<4 * 148, 256, 0, st>>>(s, a, b, out, n);
+}
+
+__global__ void scale_copy_kernel(const double* in, const double* alpha, int inv, double* out,
+                                  long n) {
+    const double al = *alpha;
+    for (long k = (long)blockIdx.x * blockDim.x + threadIdx.x; k < n;
+         k += (long)gridDim.x * blockDim.x)
+        out[k] = inv ? in[k] / al : in[k] * al;
+}
+void launch_scale_copy(const double* in, const double* alpha_dev, int inv, double* out, long n,
+                       cudaStream_t st) {
+    scale_copy_kernel<<<4 * 148, 256, 0, st>>>(in, alpha_dev, inv, out, n);
+}
+
+__device__ __forceinline__ double block_sum(double v, double* red) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1)
+        v += __shfl_down_sync(0xffffffffu, v, o);
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    __syncthreads();
+    if (lane == 0)
+        red[wid] = v;
+    __syncthreads();
+    double s = 0.0;
+    if (threadIdx.x == 0)
+        for (int k = 0; k < (int)(blockDim.x >> 5); ++k)
+            s += red[k];
+    return s;  // valid in thread 0
+}
+
+// Fixed partition of [0,n) into kRedBlocks contiguous chunks.
+__global__ void __launch_bounds__(kRedThreads) multidot_kernel(const double* __restrict__ V,
+                                                               long ld, int nv,
+                                                               const double* __restrict__ w,
+                                                               long n, double* partial) {
+    __shared__ double red[kRedThreads / 32];
+    const long chunk = (n + kRedBlocks - 1) / kRedBlocks;
+    const long lo = (long)blockIdx.x * chunk;
+    const long hi = lo + chunk < n ? lo + chunk : n;
+    for (int i = 0; i < nv; ++i) {
+        const double* vi = V + (long)i * ld;
+        double acc = 0.0;
+        for (long k = lo + threadIdx.x; k < hi; k += blockDim.x)
+            acc += vi[k] * w[k];
+        const double s = block_sum(acc, red);
+        if (threadIdx.x == 0)
+            partial[(long)i * kRedBlocks + blockIdx.x] = s;
+    }
+}
+void launch_multidot(const double* V, long ld, int nv, const double* w, long n, double* partial,
+                     cudaStream_t st) {
+    multidot_kernel<<<kRedBlocks, kRedThreads, 0, st>>>(V, ld, nv, w, n, partial);
+}
+
+__global__ void reduce_partials_kernel(const double* __restrict__ partial, double* out,
+                                       int take_sqrt) {
+    __shared__ double red[kRedThreads / 32];
+    const double* p = partial + (long)blockIdx.x * kRedBlocks;
+    double acc = 0.0;
+    for (int k = threadIdx.x; k < kRedBlocks; k += blockDim.x)
+        acc += p[k];
+    const double s = block_sum(acc, red);
+    if (threadIdx.x == 0)
+        out[blockIdx.x] = (take_sqrt && blockIdx.x == 0) ? sqrt(s) : s;
+}
+void launch_reduce_partials(const double* partial, int nv, double* out, int take_sqrt,
+                            cudaStream_t st) {
+    if (nv <= 0)
+        return;
+    reduce_partials_kernel<<<nv, kRedThreads, 0, st>>>(partial, out, take_sqrt);
+}
+
+__global__ void gemv_sub_kernel(const double* __restrict__ V, long ld, int nv,
+                                const double* __restrict__ h, double* __restrict__ w, long n) {
+    extern __shared__ double sh[];
+    for (int i = threadIdx.x; i < nv; i += blockDim.x)
+        sh[i] = h[i];
+    __syncthreads();
+    for (long k = (long)blockIdx.x * blockDim.x + threadIdx.x; k < n;
+         k += (long)gridDim.x * blockDim.x) {
+        double acc = 0.0;
+        for (int i = 0; i < nv; ++i)
+            acc += sh[i] * V[(long)i * ld + k];
+        w[k] -= acc;
+    }
+}
+void launch_gemv_sub(const double* V, long ld, int nv, const double* h, double* w, long n,
+                     cudaStream_t st) {
+    gemv_sub_kernel<<<8 * 148, 256, sizeof(double) * (nv > 0 ? nv : 1), st>>>(V, ld, nv, h, w, n);
+}
+
+__global__ void gemv_add_scaled_kernel(const double* __restrict__ V, long ld, int nv,
+                                       const double* __restrict__ y, const double* __restrict__ s,
+                                       double* __restrict__ x, long n) {
+    extern __shared__ double sh[];
+    for (int i = threadIdx.x; i < nv; i += blockDim.x)
+        sh[i] = y[i];
+    __syncthreads();
+    for (long k = (long)blockIdx.x * blockDim.x + threadIdx.x; k < n;
+         k += (long)gridDim.x * blockDim.x) {
+        double acc = 0.0;
+        for (int i = 0; i < nv; ++i)
+            acc += sh[i] * V[(long)i * ld + k];
+        x[k] += s[k] * acc;
+    }
+}
+void launch_gemv_add_scaled(const double* V, long ld, int nv, const double* y, const double* s,
+                            double* x, long n, cudaStream_t st) {
+    gemv_add_scaled_kernel<<<8 * 148, 256, sizeof(double) * (nv > 0 ? nv : 1), st>>>(V, ld, nv, y,
+                                                                                   s, x, n);
+}
+
+}  // namespace hbgpu
