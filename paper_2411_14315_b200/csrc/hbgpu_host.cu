@@ -200,6 +200,8 @@ static void build_pattern(int nn, int ne, const int* conn, std::vector<int>& row
 static int upload_all(hbgpu_ctx* c, const hbgpu_mesh_desc* d) {
     const int nn = c->nn, ne = c->ne;
     cudaStream_t st = c->stream;
+    CK(c, cudaMallocHost(reinterpret_cast<void**>(&c->h_red), sizeof(double) * 1024));
+    CK(c, cudaMallocHost(reinterpret_cast<void**>(&c->h_int), sizeof(int) * 16));
     CK(c, c->conn.alloc(size_t(ne)));
     CK(c, cudaMemcpyAsync(c->conn.p, d->conn, sizeof(int4) * size_t(ne), cudaMemcpyHostToDevice, st));
     CK(c, c->dir.alloc(size_t(nn)));
@@ -321,8 +323,6 @@ static int upload_all(hbgpu_ctx* c, const hbgpu_mesh_desc* d) {
     CK(c, cudaMemcpyAsync(c->color_elems.p, celem.data(), sizeof(int) * size_t(ne),
                           cudaMemcpyHostToDevice, st));
 
-    CK(c, cudaMallocHost(reinterpret_cast<void**>(&c->h_red), sizeof(double) * 1024));
-    CK(c, cudaMallocHost(reinterpret_cast<void**>(&c->h_int), sizeof(int) * 16));
     CK(c, c->partial.alloc(size_t(kRedBlocks) * 1024));
     CK(c, c->red.alloc(1024));
     CK(c, cudaStreamSynchronize(st));
