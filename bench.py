@@ -1,0 +1,439 @@
+#!/usr/bin/env python
+"""B200 HB-GLS hot-path benchmark (BASELINE.json metric, config 1).
+
+Step = one pass of the hot path's assembly over the config-1 workload:
+element residual + scatter (assemble_residual) and element Jacobian + BSR
+scatter (assemble_tangent), inputs resident in HBM.  value = elements*Nm/s
+(Nm = modes = 10).  The same JSON line carries the other two BASELINE
+metric items — L-matvec (BSR SpMV + H(x)mass) GB/s vs HBM over 100
+back-to-back calls, and a converged solve time (config 0) — plus the
+roofline of the dominant kernel, the reference CPU baseline, e2e through the
+C ABI with host buffers, clocks and the launch count.
+
+  python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+
+Multi-GPU: the path is single-GPU (north_star); N ranks run N independent
+replicas ("replicas only", weak scaling), max time over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "HB-GLS assembly elements*modes/s; BSR SpMV GB/s vs HBM; converged solve time"
+UNIT = "elements*modes/s"
+CANON_RES_FLOP = 1198  # per (element, time sample), SURVEY.md §8(d) / Appendix A2
+CANON_TAN_FLOP = 1532
+WORKLOAD = ("config1: rigid pipe r=0.3 cm L=6 cm, 20x20x120 hex grid mapped to the disk, "
+            "6 Kuhn tets/hex -> 288000 tets / 53361 nodes; Nm=10 (N=19 samples); "
+            "step = assemble_residual + assemble_tangent")
+
+
+def env_rank():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("LOCAL_RANK", 0)),
+            int(os.environ.get("WORLD_SIZE", 1)))
+
+
+class ClockSampler:
+    """nvidia-smi-equivalent clocks + throttle reasons sampled during the timed region."""
+
+    REASONS = {
+        0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+        0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+        0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+    }
+
+    def __init__(self, index):
+        self.samples, self.reasons, self.stop = [], 0, threading.Event()
+        self.max_mhz = None
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+
+    def _run(self):
+        while not self.stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                self.reasons |= self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+            except Exception:
+                pass
+            time.sleep(0.02)
+
+    def __enter__(self):
+        if self.nv:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.nv:
+            self.stop.set()
+            self.t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unavailable"]}
+        names = [n for b, n in self.REASONS.items() if self.reasons & b and b != 0x1]
+        return {"sm_mhz": float(np.median(self.samples)), "sm_max_mhz": self.max_mhz,
+                "reasons": names, "samples": len(self.samples)}
+
+
+def spmv_bytes(nnz, nn, N):
+    """Compulsory bytes of one L-matvec: P.vals, mass, col_idx,
+    row_ptr, y in, out, Dirichlet mask."""
+    return 64 * N * nnz + 8 * nnz + 4 * nnz + 4 * (nn + 1) + 32 * N * nn + 32 * N * nn + nn
+
+
+def problem_and_state(cfg):
+    from paper_2411_14315_b200 import cases
+
+    prob = cases.config_problem(cfg)
+    state = cases.random_state(prob.mesh.num_nodes, prob.N, 1000 + cfg)
+    return prob, state
+
+
+def auto_pseudo_dt(prob):
+    """suggest_pseudo_dt (hb_solver.cpp:86-98) on the host data."""
+    mesh, N = prob.mesh, prob.N
+    g = prob.dirichlet_g.reshape(mesh.num_nodes, 3, N)
+    tri = np.array([[2 / 3, 1 / 6, 1 / 6], [1 / 6, 2 / 3, 1 / 6], [1 / 6, 1 / 6, 2 / 3]])
+    best = 0.0
+    for p in mesh.patches:
+        if p.kind != 0 or not p.area > 0:
+            continue
+        gq = np.einsum("qa,faik->fqik", tri, g[p.facets])  # (F,3q,3i,N)
+        un = np.einsum("fqik,fi->fqk", gq, p.normals)
+        q = (p.areas[:, None] / 3.0 * un.sum(axis=1)).sum(axis=0)
+        best = max(best, float(np.abs(q).max() / p.area))
+    return mesh.characteristic_length() / best if best > 0 else prob.period / N
+
+
+def load_traffic():
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(path) as f:
+            return json.load(f)
+    except Exception:
+        return {}
+
+
+# ----------------------------------------------------------------------------- reference arm
+
+def cpu_reference_sample(prob, state, threads, budget_s, min_reps=1):
+    """Time the compiled reference (oracle/_ref/libhbref.so) on the host:
+    assemble_residual(threads) + assemble_tangent (serial by design,
+    assembly.cpp:550-666).  Uses the full mesh when one step fits the budget,
+    otherwise a leading sub-mesh of the (spatially ordered) elements."""
+    from oracle import bindings as ob
+    from paper_2411_14315_b200.mesh import Mesh
+
+    mesh = prob.mesh
+    ne = mesh.num_elements
+    ctx = ob.ref_context(prob, 0, auto_pseudo_dt(prob))
+    t0 = time.perf_counter()
+    ctx.residual(state, threads)
+    ctx.tangent(state)
+    full = time.perf_counter() - t0
+    frac = min(1.0, budget_s / max(full, 1e-9))
+    if frac < 1.0:
+        k = max(1000, int(ne * frac))
+        conn = mesh.conn[:k]
+        used = np.unique(conn)
+        remap = -np.ones(mesh.num_nodes, np.int64)
+        remap[used] = np.arange(len(used))
+        sub = Mesh(mesh.xyz[used], remap[conn].astype(np.int32), [], None).finalize()
+        from paper_2411_14315_b200.cases import Problem
+
+        sp = Problem(sub, prob.modes, prob.period, prob.rho, prob.mu,
+                     np.zeros(len(used) * 3 * prob.N), [], prob.backflow_beta)
+        st = state.reshape(mesh.num_nodes, 4 * prob.N)[used].reshape(-1)
+        ctx = ob.ref_context(sp, 0, auto_pseudo_dt(prob))
+        sample_desc = f"leading {k} of {ne} elements (sub-mesh), full step est {full:.1f}s"
+        ne_s, state_s = k, st
+    else:
+        sample_desc = f"full config-1 mesh ({ne} elements)"
+        ne_s, state_s = ne, state
+    return ctx, ne_s, state_s, sample_desc, full
+
+
+def run_reference(args):
+    rank, _, world = env_rank()
+    if rank != 0:
+        return
+    threads = os.cpu_count() or 1
+    prob, state = problem_and_state(1)
+    per_step_budget = max(2.0, 150.0 / (args.steps + args.warmup))
+    ctx, ne_s, st, desc, _ = cpu_reference_sample(prob, state, threads, per_step_budget)
+    for _ in range(max(0, args.warmup - 1)):
+        ctx.residual(st, threads)
+        ctx.tangent(st)
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        ctx.residual(st, threads)
+        ctx.tangent(st)
+        times.append(time.perf_counter() - t0)
+    t = float(np.mean(times))
+    value = ne_s * prob.modes / t
+    cpu = os.popen("lscpu | grep 'Model name' | head -1").read().split(":")[-1].strip()
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": {"workload": WORKLOAD, "sample": desc},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
+                         "sample": desc + f"; residual threads={threads}, tangent serial "
+                                          f"(reference design); host CPU: {cpu}; FFTW replaced by "
+                                          "the O(N^2) DFT shim (libfftw3 absent)"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------- our arm
+
+def run_ours(args):
+    import torch
+
+    from paper_2411_14315_b200 import hbgpu
+
+    rank, local, world = env_rank()
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    prob, state = problem_and_state(1)
+    mesh, N, M = prob.mesh, prob.N, prob.modes
+    ne, nn = mesh.num_elements, mesh.num_nodes
+    pdt = auto_pseudo_dt(prob)
+    ctx = hbgpu.GpuContext(mesh)
+    ctx.set_basis(M, prob.period)
+    ctx.set_fluid(prob.rho, prob.mu)
+    ctx.set_bcs(prob.dirichlet_g, prob.neumann, prob.backflow_beta)
+    ctx.set_assembly_config(0, pdt)
+    nnz = ctx.nnz
+    stream = torch.cuda.ExternalStream(ctx.stream)
+    d_state = torch.from_numpy(state).cuda()
+    d_r = torch.empty_like(d_state)
+    torch.cuda.synchronize()
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")  # 256 MB > L2
+    L = hbgpu._lib
+    L.hbgpu_profile_enable.argtypes = [hbgpu._vp, hbgpu.C.c_int]
+    L.hbgpu_profile_read.argtypes = [hbgpu._vp, hbgpu.C.c_int, hbgpu._vp, hbgpu._vp]
+    L.hbgpu_kernel_launches.restype = hbgpu.C.c_longlong
+    L.hbgpu_fp64_peak.argtypes = [hbgpu._vp]
+
+    def step():
+        ctx.assemble_residual_dev(d_state.data_ptr(), d_r.data_ptr())
+        ctx.assemble_tangent_dev(d_state.data_ptr())
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+
+    # ---- timed region: K steps, L2 flushed between steps (not timed)
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(args.steps)]
+    L.hbgpu_profile_enable(ctx.handle, 1)
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    launches0 = L.hbgpu_kernel_launches()
+    with ClockSampler(local) as clk, torch.cuda.stream(stream):
+        for k in range(args.steps):
+            flush.fill_(float(k))
+            evs[k][0].record(stream)
+            step()
+            evs[k][1].record(stream)
+        torch.cuda.synchronize()
+    launches = L.hbgpu_kernel_launches() - launches0
+    step_ms = [a.elapsed_time(b) for a, b in evs]
+    total_ms = float(np.sum(step_ms))
+    ph_ms = np.zeros(9)
+    ph_n = np.zeros(9, np.int32)
+    L.hbgpu_profile_read(ctx.handle, 9, ph_ms.ctypes.data, ph_n.ctypes.data)
+    L.hbgpu_profile_enable(ctx.handle, 0)
+    if dist:
+        t = torch.tensor([total_ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    ms_per_step = total_ms / args.steps
+    value = world * ne * M / (ms_per_step * 1e-3)
+
+    # ---- per-kernel rooflines (device time from events on the launching stream)
+    peak = np.zeros(1)
+    L.hbgpu_fp64_peak(peak.ctypes.data)
+    fp64_peak = float(peak[0])
+    res_elem_ms = ph_ms[2] / max(ph_n[2], 1)
+    tan_ms = ph_ms[4] / max(ph_n[4], 1)
+    res_all_ms = ph_ms[0] / max(ph_n[0], 1)
+    res_flops = CANON_RES_FLOP * ne * N
+    tan_flops = CANON_TAN_FLOP * ne * N
+    traffic = load_traffic()
+    kernels = {
+        "tangent_rows_kernel": {"ms": tan_ms, "tflops": tan_flops / (tan_ms * 1e-3) / 1e12},
+        "residual (all passes)": {"ms": res_all_ms, "tflops": res_flops / (res_all_ms * 1e-3) / 1e12},
+        "residual_color_kernel (all colours)": {"ms": res_elem_ms,
+                                                "tflops": res_flops / (res_elem_ms * 1e-3) / 1e12},
+    }
+    dom = "tangent_rows_kernel" if tan_ms >= res_all_ms else "residual (all passes)"
+    dk = kernels[dom]
+    roofline = {
+        "kernel": dom, "bound": "fp64", "achieved": dk["tflops"], "peak": fp64_peak,
+        "unit": "TFLOP/s", "frac": dk["tflops"] / fp64_peak if fp64_peak > 0 else None,
+        "traffic": traffic.get(dom.split(" ")[0]),
+        "algorithmic": f"{CANON_TAN_FLOP if dom.startswith('tangent') else CANON_RES_FLOP} FP64 "
+                       f"FLOP per (element, sample) x {ne}x{N}",
+        "peak_source": "measured DFMA loop (hbgpu_fp64_peak) on this GPU; MEASURED_PEAKS.json has no FP64 figure",
+        "other_kernels": kernels,
+    }
+
+    # ---- L-matvec: 100 back-to-back calls (BASELINE config-4 protocol), GB/s vs HBM
+    hbm_peak = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"] \
+        if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else 6650.0
+    y = torch.from_numpy(np.random.default_rng(5).uniform(-1, 1, nn * 4 * N)).cuda()
+    out = torch.empty_like(y)
+    ctx.assemble_mass()
+    for _ in range(3):
+        ctx.matvec_dev(y.data_ptr(), out.data_ptr())
+    reps = args.spmv_reps
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(stream):
+        flush.fill_(1.0)
+        e0.record(stream)
+        for _ in range(reps):
+            ctx.matvec_dev(y.data_ptr(), out.data_ptr())
+        e1.record(stream)
+    torch.cuda.synchronize()
+    mv_ms = e0.elapsed_time(e1) / reps
+    mv_bytes = spmv_bytes(nnz, nn, N)
+    spmv = {"ms": mv_ms, "gbs": mv_bytes / (mv_ms * 1e-3) / 1e9, "peak_gbs": hbm_peak,
+            "frac": mv_bytes / (mv_ms * 1e-3) / 1e9 / hbm_peak, "compulsory_bytes": mv_bytes,
+            "traffic": traffic.get("matvec_kernel"), "reps": reps,
+            "peak_source": "MEASURED_PEAKS.json hbm_gbs (of measured)"}
+
+    # ---- e2e through the C ABI with pinned host buffers (H2D state, D2H residual)
+    h_state = torch.from_numpy(state).pin_memory()
+    h_r = torch.empty_like(h_state).pin_memory()
+    hs, hr = h_state.numpy(), h_r.numpy()
+    ctx.assemble_residual(hs)
+    e2e_times = []
+    for _ in range(max(3, args.steps // 2)):
+        t0 = time.perf_counter()
+        hbgpu._residual(ctx.handle, hs.ctypes.data, hr.ctypes.data)
+        hbgpu._tangent(ctx.handle, hs.ctypes.data, None)
+        e2e_times.append(time.perf_counter() - t0)
+    e2e_s = float(np.mean(e2e_times))
+    e2e = {"value": world * ne * M / e2e_s, "unit": UNIT,
+           "h2d_bytes_per_step": 2 * state.nbytes, "d2h_bytes_per_step": state.nbytes,
+           "note": "hbgpu_assemble_residual(host state -> host r) + hbgpu_assemble_tangent(host state, "
+                   "P kept on device as the GPU Newton loop uses it); pinned host buffers; wall clock"}
+
+    # ---- converged solve time (config 0, reference default tolerances)
+    solve = None
+    if args.solve and rank == 0:
+        solve = solve_config0()
+
+    cpu_baseline = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            threads = os.cpu_count() or 1
+            cctx, ne_s, st, desc, full = cpu_reference_sample(prob, state, threads, 12.0)
+            t0 = time.perf_counter()
+            reps_c = 0
+            while True:
+                cctx.residual(st, threads)
+                cctx.tangent(st)
+                reps_c += 1
+                if time.perf_counter() - t0 > 10.0:
+                    break
+            tc = (time.perf_counter() - t0) / reps_c
+            cpu_baseline = {"value": ne_s * M / tc, "unit": UNIT, "cores": threads, "kind": "reference",
+                            "sample": f"{desc}; {reps_c} timed steps; residual threads={threads}, "
+                                      "tangent serial as in the reference"}
+        except Exception as exc:  # oracle library absent on this box
+            cpu_baseline = {"value": None, "unit": UNIT, "cores": 0, "kind": "reference",
+                            "sample": f"unavailable: {exc}"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": WORKLOAD, "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
+                       "l2": "256 MB buffer written between timed steps (not timed)",
+                       "elements": ne, "nodes": nn, "nnz_blocks": nnz, "modes": M, "time_points": N,
+                       "pseudo_dt": pdt},
+            "phases_ms_per_step": {k: float(ph_ms[i] / args.steps) for i, k in
+                                   enumerate(["residual", "res_hu", "res_elements", "res_finalize",
+                                              "tangent", "matvec", "jacobi", "gmres", "mass"])},
+            "roofline": roofline,
+            "spmv": spmv,
+            "solve": solve,
+            "cpu_baseline": cpu_baseline,
+            "e2e": e2e,
+            "clocks": clk.summary(),
+            "gpu_launches": int(launches),
+            "fp64_peak_tflops": fp64_peak,
+        }
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def solve_config0():
+    from paper_2411_14315_b200 import cases, hbgpu
+
+    prob = cases.config_problem(0)
+    ctx = hbgpu.GpuContext(prob.mesh)
+    ctx.set_basis(prob.modes, prob.period)
+    ctx.set_fluid(prob.rho, prob.mu)
+    ctx.set_bcs(prob.dirichlet_g, prob.neumann, prob.backflow_beta)
+    try:
+        sol = ctx.solve_harmonic(hbgpu.SolverConfig())
+        return {"config": "config0 (36000 tets, Nm=3), reference defaults (3 orders, GMRES 0.03, restart 200)",
+                "seconds": sol.total_seconds, "newton_iters": int(len(sol.log.iters)),
+                "gmres_iters": int(sol.log.linear_iters.sum()), "converged": sol.log.converged,
+                "final_rel": float(sol.log.res_rel[-1]), "assembly_seconds": sol.assembly_seconds,
+                "linear_seconds": sol.linear_seconds}
+    except Exception as exc:
+        return {"error": f"{type(exc).__name__}: {exc}"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--spmv-reps", type=int, default=100)
+    ap.add_argument("--no-solve", dest="solve", action="store_false")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

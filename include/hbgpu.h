@@ -176,6 +176,19 @@ int hbgpu_solve_harmonic(hbgpu_ctx* ctx, const hbgpu_solver_cfg* cfg, double* st
                          hbgpu_solve_info* info, int capacity, int* log_iter, double* log_res,
                          double* log_rel, int* log_linear, double* log_seconds);
 
+/* ---- measurement ------------------------------------------------------- */
+
+/* Per-phase CUDA-event timing on the context stream (reset on enable).
+ * Phases: 0 residual (all), 1 nodal H*u pass, 2 residual element kernels,
+ * 3 residual finalize (H*s, boundary, Dirichlet), 4 tangent, 5 L-matvec,
+ * 6 Jacobi, 7 GMRES (all), 8 mass. */
+int hbgpu_profile_enable(hbgpu_ctx* ctx, int on);
+int hbgpu_profile_read(hbgpu_ctx* ctx, int num_phases, double* ms, int* count);
+/* Kernel launches issued by the library since load (process-wide). */
+long long hbgpu_kernel_launches(void);
+/* Measured dense FP64 FMA throughput of the current device (DFMA loop). */
+int hbgpu_fp64_peak(double* tflops);
+
 #ifdef __cplusplus
 }
 #endif

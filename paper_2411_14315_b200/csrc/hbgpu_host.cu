@@ -116,6 +116,16 @@ struct hbgpu_ctx {
     int* h_int = nullptr;  // pinned
 
     bool mass_valid = false, p_valid = false, inv_valid = false;
+
+    // optional per-phase CUDA-event timing on the context stream
+    bool prof = false;
+    std::vector<cudaEvent_t> ev_pool;
+    size_t ev_used = 0;
+    struct Pair {
+        int phase;
+        size_t e0, e1;
+    };
+    std::vector<Pair> pairs;
     cudaStream_t stream = nullptr;
     std::string err;
 
@@ -137,6 +147,37 @@ struct hbgpu_ctx {
         if (s_ != HBGPU_OK)  \
             return s_;       \
     } while (0)
+
+enum Phase {
+    kPhResidual = 0,
+    kPhResHu,
+    kPhResElem,
+    kPhResFinal,
+    kPhTangent,
+    kPhMatvec,
+    kPhJacobi,
+    kPhGmres,
+    kPhMass,
+    kPhCount
+};
+
+static long prof_mark(hbgpu_ctx* c) {
+    if (!c->prof)
+        return -1;
+    if (c->ev_used == c->ev_pool.size()) {
+        cudaEvent_t e;
+        if (cudaEventCreate(&e) != cudaSuccess)
+            return -1;
+        c->ev_pool.push_back(e);
+    }
+    cudaEventRecord(c->ev_pool[c->ev_used], c->stream);
+    return long(c->ev_used++);
+}
+
+static void prof_pair(hbgpu_ctx* c, int phase, long e0, long e1) {
+    if (e0 >= 0 && e1 >= 0)
+        c->pairs.push_back({phase, size_t(e0), size_t(e1)});
+}
 
 static int fail(hbgpu_ctx* c, int code, const std::string& msg) {
     c->err = msg;
@@ -373,12 +414,14 @@ static int residual_dev(hbgpu_ctx* c, const double* d_state, double* d_r) {
     const int N = c->N;
     cudaStream_t st = c->stream;
     const size_t tot = size_t(c->nn) * 4 * size_t(N);
+    const long p0 = prof_mark(c);
     CK(c, cudaMemsetAsync(d_r, 0, sizeof(double) * tot, st));
     CK(c, cudaMemsetAsync(c->s.p, 0, sizeof(double) * size_t(c->nn) * 3 * size_t(N), st));
     if (N > 1)
         launch_apply_h_series(c->H.p, N, d_state, 4 * N, c->hu.p, 3 * N, c->nn, st);
     else
         CK(c, cudaMemsetAsync(c->hu.p, 0, sizeof(double) * size_t(c->nn) * 3, st));
+    const long p1 = prof_mark(c);
     ResidualArgs a;
     a.conn = c->conn.p;
     a.geom = c->geom.p;
@@ -395,6 +438,7 @@ static int residual_dev(hbgpu_ctx* c, const double* d_state, double* d_r) {
     for (size_t k = 0; k + 1 < c->color_ptr.size(); ++k)
         launch_residual_color(a, c->color_elems.p + c->color_ptr[k],
                               c->color_ptr[k + 1] - c->color_ptr[k], st);
+    const long p2 = prof_mark(c);
     launch_residual_finalize(c->H.p, N, c->s.p, c->dir.p, d_r, c->nn, st);
     if (c->nbnodes > 0) {
         BoundaryArgs b;
@@ -415,6 +459,11 @@ static int residual_dev(hbgpu_ctx* c, const double* d_state, double* d_r) {
         b.beta = c->beta;
         launch_boundary(b, st);
     }
+    const long p3 = prof_mark(c);
+    prof_pair(c, kPhResidual, p0, p3);
+    prof_pair(c, kPhResHu, p0, p1);
+    prof_pair(c, kPhResElem, p1, p2);
+    prof_pair(c, kPhResFinal, p2, p3);
     return check_launch(c);
 }
 
@@ -441,15 +490,19 @@ static int tangent_dev(hbgpu_ctx* c, const double* d_state) {
     a.pseudo_c = pseudo ? c->pseudo_c1 * c->rho / c->pseudo_dt : 0.0;
     a.tau_mode = c->tau_mode;
     a.flag = c->flag.p;
+    const long p0 = prof_mark(c);
     launch_tangent_rows(a, int(c->tcta_h.size()) - 1, c->tthreads, c->tsmem, c->stream);
+    prof_pair(c, kPhTangent, p0, prof_mark(c));
     c->p_valid = true;
     c->inv_valid = false;
     return check_launch(c);
 }
 
 static int mass_dev(hbgpu_ctx* c) {
+    const long p0 = prof_mark(c);
     launch_mass_rows(c->conn.p, c->geom.p, c->row_ptr.p, c->inc_ptr.p, c->inc_elem.p,
                      c->inc_cols.p, c->rho, c->mass.p, c->nn, c->stream);
+    prof_pair(c, kPhMass, p0, prof_mark(c));
     c->mass_valid = true;
     return check_launch(c);
 }
@@ -474,7 +527,9 @@ static int matvec_dev(hbgpu_ctx* c, const double* d_y, double* d_out, const doub
     a.N = c->N;
     a.rows_per_cta = rows_per_matvec_cta(c->N);
     a.with_c = (with_c && c->N > 1) ? 1 : 0;
+    const long p0 = prof_mark(c);
     launch_matvec(a, c->stream);
+    prof_pair(c, kPhMatvec, p0, prof_mark(c));
     return check_launch(c);
 }
 
@@ -482,7 +537,9 @@ static int jacobi_dev(hbgpu_ctx* c, int* degenerate) {
     if (!c->p_valid)
         return fail(c, HBGPU_ERR_INVALID, "jacobi before assemble_tangent / set_pvals");
     CK(c, cudaMemsetAsync(c->ideg.p, 0, sizeof(int), c->stream));
+    const long p0 = prof_mark(c);
     launch_jacobi(c->pvals.p, c->diag_blk.p, c->nn, c->N, c->inv.p, c->ideg.p, c->stream);
+    prof_pair(c, kPhJacobi, p0, prof_mark(c));
     TRY(check_launch(c));
     CK(c, cudaMemcpyAsync(c->h_int + 1, c->ideg.p, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
     CK(c, cudaStreamSynchronize(c->stream));
@@ -764,6 +821,8 @@ void hbgpu_destroy(hbgpu_ctx* c) {
     c->edmask.release();
     c->inc_elem.release();
     c->inc_cols.release();
+    for (cudaEvent_t e : c->ev_pool)
+        cudaEventDestroy(e);
     if (c->stream)
         cudaStreamDestroy(c->stream);
     delete c;
@@ -1048,7 +1107,51 @@ int hbgpu_gmres_dev(hbgpu_ctx* c, const double* d_rhs, const hbgpu_krylov_cfg* c
     TRY(ensure_basis(c));
     if (!c->inv_valid)
         TRY(jacobi_dev(c, nullptr));
-    return gmres_dev(c, d_rhs, c->inv.p, cfg, d_x, result, history, hcap);
+    const long p0 = prof_mark(c);
+    const int st = gmres_dev(c, d_rhs, c->inv.p, cfg, d_x, result, history, hcap);
+    prof_pair(c, kPhGmres, p0, prof_mark(c));
+    return st;
+}
+
+int hbgpu_profile_enable(hbgpu_ctx* c, int on) {
+    CK(c, cudaStreamSynchronize(c->stream));
+    c->prof = on != 0;
+    c->ev_used = 0;
+    c->pairs.clear();
+    return HBGPU_OK;
+}
+
+int hbgpu_profile_read(hbgpu_ctx* c, int nphase, double* ms, int* count) {
+    CK(c, cudaStreamSynchronize(c->stream));
+    for (int k = 0; k < nphase; ++k) {
+        ms[k] = 0.0;
+        count[k] = 0;
+    }
+    for (const auto& p : c->pairs) {
+        if (p.phase >= nphase)
+            continue;
+        float t = 0.0f;
+        CK(c, cudaEventElapsedTime(&t, c->ev_pool[p.e0], c->ev_pool[p.e1]));
+        ms[p.phase] += double(t);
+        count[p.phase] += 1;
+    }
+    return HBGPU_OK;
+}
+
+long long hbgpu_kernel_launches(void) { return g_launches.load(); }
+
+int hbgpu_fp64_peak(double* tflops) {
+    const int blocks = 148 * 8, threads = 256, iters = 4096;
+    double* d = nullptr;
+    if (cudaMalloc(&d, sizeof(double)) != cudaSuccess)
+        return HBGPU_ERR_CUDA;
+    float ms = 0.0f;
+    const cudaError_t e = run_fp64_peak(blocks, threads, iters, d, &ms);
+    cudaFree(d);
+    if (e != cudaSuccess)
+        return HBGPU_ERR_CUDA;
+    *tflops = 2.0 * 8.0 * double(iters) * blocks * threads / (double(ms) * 1e-3) / 1e12;
+    return HBGPU_OK;
 }
 
 int hbgpu_gmres(hbgpu_ctx* c, const double* rhs, const double* inv_diag, const hbgpu_krylov_cfg* cfg,

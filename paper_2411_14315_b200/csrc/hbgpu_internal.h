@@ -4,6 +4,7 @@
 
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstdint>
 #include <string>
 #include <vector>
@@ -16,6 +17,10 @@ constexpr double kQB = 0.1381966011250105151795414;
 // Gauss-Seidel block: number of partial sums of the deterministic reductions.
 constexpr int kRedBlocks = 592;  // 4 x 148 SMs
 constexpr int kRedThreads = 256;
+
+// Number of kernel launches issued by this library (bench.py's gpu_launches).
+extern std::atomic<long long> g_launches;
+cudaError_t run_fp64_peak(int blocks, int threads, int iters, double* out, float* ms);
 
 // ---------------------------------------------------------------- kernel args
 

@@ -17,7 +17,11 @@
 
 namespace hbgpu {
 
+std::atomic<long long> g_launches{0};
+
 namespace {
+
+inline void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
 __device__ __forceinline__ double ldg(const double* p) { return __ldg(p); }
 
@@ -128,6 +132,7 @@ void launch_geometry(const double* xyz, const int4* conn, int ne, double* geom, 
                      cudaStream_t st) {
     if (ne <= 0)
         return;
+    note_launch();
     geometry_kernel<<<(ne + 255) / 256, 256, 0, st>>>(xyz, conn, ne, geom, flag);
 }
 
@@ -163,6 +168,7 @@ void launch_apply_h_series(const double* H, int N, const double* in, int in_node
     const int per = (N >= 256) ? 1 : 256 / N;
     const long nser = 3L * nnodes;
     const int blocks = (int)((nser + per - 1) / per);
+    note_launch();
     apply_h_series_kernel<<<blocks, per * N, sizeof(double) * N * N, st>>>(
         H, N, in, in_node_stride, out, out_node_stride, nnodes);
 }
@@ -290,6 +296,7 @@ void launch_residual_color(const ResidualArgs& a, const int* elems, int count, c
     if (count <= 0)
         return;
     const long threads = (long)count * a.N;
+    note_launch();
     residual_color_kernel<<<(int)((threads + 255) / 256), 256, 0, st>>>(a, elems, count);
 }
 
@@ -325,6 +332,7 @@ void launch_residual_finalize(const double* H, int N, const double* s, const uin
                               double* r, int nn, cudaStream_t st) {
     const int per = (N >= 256) ? 1 : 256 / N;
     const long nser = 3L * nn;
+    note_launch();
     residual_finalize_kernel<<<(int)((nser + per - 1) / per), per * N,
                                sizeof(double) * N * N, st>>>(H, N, s, dir, r, nn);
 }
@@ -381,6 +389,7 @@ void launch_boundary(const BoundaryArgs& a, cudaStream_t st) {
     if (a.nbnodes <= 0)
         return;
     const long threads = (long)a.nbnodes * a.N;
+    note_launch();
     boundary_kernel<<<(int)((threads + 255) / 256), 256, 0, st>>>(a);
 }
 
@@ -518,6 +527,7 @@ void launch_tangent_rows(const TangentArgs& a, int nctas, int threads, size_t sm
                          cudaStream_t st) {
     if (nctas <= 0)
         return;
+    note_launch();
     tangent_rows_kernel<<<nctas, threads, smem, st>>>(a);
 }
 
@@ -550,6 +560,7 @@ void launch_mass_rows(const int4* conn, const double* geom, const int* row_ptr,
                       double rho, double* mass, int nn, cudaStream_t st) {
     if (nn <= 0)
         return;
+    note_launch();
     mass_rows_kernel<<<(nn + 127) / 128, 128, 0, st>>>(conn, geom, row_ptr, inc_ptr, inc_elem,
                                                        inc_cols, rho, mass, nn);
 }
@@ -647,6 +658,7 @@ void launch_matvec(const MatvecArgs& a, cudaStream_t st) {
         return;
     const int blocks = (a.nn + a.rows_per_cta - 1) / a.rows_per_cta;
     const size_t smem = a.with_c ? sizeof(double) * ((size_t)a.N * a.N + 3 * (size_t)a.N * a.rows_per_cta) : 0;
+    note_launch();
     matvec_kernel<<<blocks, a.rows_per_cta * a.N, smem, st>>>(a);
 }
 
@@ -674,6 +686,7 @@ void launch_jacobi(const double* vals, const int* diag_blk, int nn, int N, doubl
     const long total = (long)nn * 4 * N;
     if (total <= 0)
         return;
+    note_launch();
     jacobi_kernel<<<(int)((total + 255) / 256), 256, 0, st>>>(vals, diag_blk, nn, N, inv_diag,
                                                               degenerate);
 }
@@ -697,6 +710,7 @@ void launch_install_dirichlet(const double* g, const uint8_t* dir, int nn, int N
     const long tot = 3L * nn * N;
     if (tot <= 0)
         return;
+    note_launch();
     install_dirichlet_kernel<<<(int)((tot + 255) / 256), 256, 0, st>>>(g, dir, nn, N, state);
 }
 
@@ -712,6 +726,7 @@ void launch_fill_pressure(double p0, int nn, int N, double* state, cudaStream_t 
     const long tot = (long)nn * N;
     if (tot <= 0)
         return;
+    note_launch();
     fill_pressure_kernel<<<(int)((tot + 255) / 256), 256, 0, st>>>(p0, nn, N, state);
 }
 
@@ -733,6 +748,7 @@ void launch_newton_update(const double* dx, const uint8_t* dir, int nn, int N, d
     const long tot = 4L * nn * N;
     if (tot <= 0)
         return;
+    note_launch();
     newton_update_kernel<<<(int)((tot + 255) / 256), 256, 0, st>>>(dx, dir, nn, N, state);
 }
 
@@ -744,6 +760,7 @@ __global__ void sqrt_abs_kernel(const double* in, double* out, long n) {
         out[k] = sqrt(fabs(in[k]));
 }
 void launch_sqrt_abs(const double* in, double* out, long n, cudaStream_t st) {
+    note_launch();
     sqrt_abs_kernel<<<4 * 148, 256, 0, st>>>(in, out, n);
 }
 
@@ -753,6 +770,7 @@ __global__ void mul_kernel(const double* a, const double* b, double* out, long n
         out[k] = a[k] * b[k];
 }
 void launch_mul(const double* a, const double* b, double* out, long n, cudaStream_t st) {
+    note_launch();
     mul_kernel<<<4 * 148, 256, 0, st>>>(a, b, out, n);
 }
 
@@ -764,6 +782,7 @@ __global__ void scaled_diff_kernel(const double* s, const double* a, const doubl
 }
 void launch_scaled_diff(const double* s, const double* a, const double* b, double* out, long n,
                         cudaStream_t st) {
+    note_launch();
     scaled_diff_kernel<<<4 * 148, 256, 0, st>>>(s, a, b, out, n);
 }
 
@@ -776,6 +795,7 @@ __global__ void scale_copy_kernel(const double* in, const double* alpha, int inv
 }
 void launch_scale_copy(const double* in, const double* alpha_dev, int inv, double* out, long n,
                        cudaStream_t st) {
+    note_launch();
     scale_copy_kernel<<<4 * 148, 256, 0, st>>>(in, alpha_dev, inv, out, n);
 }
 
@@ -816,6 +836,7 @@ __global__ void __launch_bounds__(kRedThreads) multidot_kernel(const double* __r
 }
 void launch_multidot(const double* V, long ld, int nv, const double* w, long n, double* partial,
                      cudaStream_t st) {
+    note_launch();
     multidot_kernel<<<kRedBlocks, kRedThreads, 0, st>>>(V, ld, nv, w, n, partial);
 }
 
@@ -834,6 +855,7 @@ void launch_reduce_partials(const double* partial, int nv, double* out, int take
                             cudaStream_t st) {
     if (nv <= 0)
         return;
+    note_launch();
     reduce_partials_kernel<<<nv, kRedThreads, 0, st>>>(partial, out, take_sqrt);
 }
 
@@ -853,6 +875,7 @@ __global__ void gemv_sub_kernel(const double* __restrict__ V, long ld, int nv,
 }
 void launch_gemv_sub(const double* V, long ld, int nv, const double* h, double* w, long n,
                      cudaStream_t st) {
+    note_launch();
     gemv_sub_kernel<<<8 * 148, 256, sizeof(double) * (nv > 0 ? nv : 1), st>>>(V, ld, nv, h, w, n);
 }
 
@@ -873,8 +896,45 @@ __global__ void gemv_add_scaled_kernel(const double* __restrict__ V, long ld, in
 }
 void launch_gemv_add_scaled(const double* V, long ld, int nv, const double* y, const double* s,
                             double* x, long n, cudaStream_t st) {
+    note_launch();
     gemv_add_scaled_kernel<<<8 * 148, 256, sizeof(double) * (nv > 0 ? nv : 1), st>>>(V, ld, nv, y,
                                                                                    s, x, n);
+}
+
+// DFMA throughput probe: 8 independent FMA chains per thread, enough CTAs
+// to fill every SM.  Used once by bench.py for the FP64 roofline peak (the
+// driver's MEASURED_PEAKS.json has HBM and bf16 only).
+__global__ void fp64_peak_kernel(double* out, int iters, double a, double b) {
+    double x[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+        x[k] = threadIdx.x * 1e-7 + k;
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+            x[k] = fma(x[k], a, b);
+    }
+    double s = 0.0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+        s += x[k];
+    if (s == 12345.678)
+        out[0] = s;
+}
+
+cudaError_t run_fp64_peak(int blocks, int threads, int iters, double* out, float* ms) {
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    fp64_peak_kernel<<<blocks, threads>>>(out, iters, 0.999999, 1e-9);  // warm-up
+    cudaEventRecord(e0);
+    fp64_peak_kernel<<<blocks, threads>>>(out, iters, 0.999999, 1e-9);
+    cudaEventRecord(e1);
+    cudaError_t err = cudaEventSynchronize(e1);
+    cudaEventElapsedTime(ms, e0, e1);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    return err == cudaSuccess ? cudaGetLastError() : err;
 }
 
 }  // namespace hbgpu
