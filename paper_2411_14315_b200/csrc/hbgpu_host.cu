@@ -85,8 +85,13 @@ struct hbgpu_ctx {
     DBuf<uint8_t> dir, edmask;
     DBuf<int> row_ptr, col_idx, diag_blk, inc_ptr;
     DBuf<uint32_t> inc_elem, inc_cols;
-    std::vector<int> color_ptr;
-    DBuf<int> color_elems;
+    // residual element chunks
+    int nchunks = 0, max_nloc = 0;
+    long npairs = 0;
+    DBuf<uint32_t> lconn;
+    DBuf<int> chunk_node_ptr, chunk_nodes, slot_ptr, npart_ptr, npart;
+    DBuf<uint8_t> slot_idx;
+    DBuf<double> rpartial;
 
     // tangent CTA plan (depends on N)
     std::vector<int> tcta_h;
@@ -107,7 +112,7 @@ struct hbgpu_ctx {
     int nbnodes = 0;
 
     // work buffers
-    DBuf<double> state, r, hu, s, pvals, mass, inv, y, out, x, w, scale, b, tmp;
+    DBuf<double> state, r, hu, pvals, mass, inv, y, out, x, w, scale, b, tmp;
     DBuf<double> V;
     size_t V_vecs = 0;
     DBuf<double> partial, red;
@@ -328,41 +333,70 @@ static int upload_all(hbgpu_ctx* c, const hbgpu_mesh_desc* d) {
                           cudaMemcpyHostToDevice, st));
     CK(c, cudaMemcpyAsync(c->edmask.p, edm.data(), edm.size(), cudaMemcpyHostToDevice, st));
 
-    // greedy element colouring (element order, smallest free colour):
-    // elements of one class share no node
-    std::vector<uint64_t> used(size_t(nn) * 2, 0);
-    std::vector<int> color(static_cast<size_t>(ne));
-    int ncol = 0;
-    for (long e = 0; e < ne; ++e) {
-        uint64_t f0 = 0, f1 = 0;
-        for (int a = 0; a < 4; ++a) {
-            f0 |= used[2 * size_t(d->conn[4 * e + a])];
-            f1 |= used[2 * size_t(d->conn[4 * e + a]) + 1];
+    // element chunks of kChunkElems consecutive elements: distinct nodes,
+    // chunk-local connectivity, per (chunk, node) slot lists in element order,
+    // and per node the (chunk, node) records in chunk order
+    const int CE = kChunkElems;
+    const int nch = (ne + CE - 1) / CE;
+    std::vector<int> cnp(size_t(nch) + 1, 0), cnodes, sptr{0}, npp(size_t(nn) + 1, 0), npl;
+    std::vector<uint8_t> sidx;
+    std::vector<uint32_t> lconn(static_cast<size_t>(ne));
+    int maxnloc = 0;
+    for (int ch = 0; ch < nch; ++ch) {
+        const long e0 = long(ch) * CE, e1 = std::min<long>(ne, e0 + CE);
+        std::vector<int> loc;
+        for (long e = e0; e < e1; ++e)
+            for (int a = 0; a < 4; ++a)
+                loc.push_back(d->conn[4 * e + a]);
+        std::sort(loc.begin(), loc.end());
+        loc.erase(std::unique(loc.begin(), loc.end()), loc.end());
+        if (loc.size() > 255)
+            return fail(c, HBGPU_ERR_INVALID, "element chunk with more than 255 nodes");
+        maxnloc = std::max(maxnloc, int(loc.size()));
+        std::vector<std::vector<uint8_t>> inc(loc.size());
+        for (long e = e0; e < e1; ++e) {
+            uint32_t pk = 0;
+            for (int a = 0; a < 4; ++a) {
+                const int ln = int(std::lower_bound(loc.begin(), loc.end(), d->conn[4 * e + a]) - loc.begin());
+                pk |= uint32_t(ln) << (8 * a);
+                inc[size_t(ln)].push_back(uint8_t((e - e0) * 4 + a));
+            }
+            lconn[size_t(e)] = pk;
         }
-        int col;
-        if (~f0)
-            col = __builtin_ctzll(~f0);
-        else if (~f1)
-            col = 64 + __builtin_ctzll(~f1);
-        else
-            return fail(c, HBGPU_ERR_INVALID, "element colouring needs more than 128 colours");
-        color[size_t(e)] = col;
-        ncol = std::max(ncol, col + 1);
-        for (int a = 0; a < 4; ++a)
-            used[2 * size_t(d->conn[4 * e + a]) + (col >> 6)] |= uint64_t(1) << (col & 63);
+        for (size_t ln = 0; ln < loc.size(); ++ln) {
+            cnodes.push_back(loc[ln]);
+            sidx.insert(sidx.end(), inc[ln].begin(), inc[ln].end());
+            sptr.push_back(int(sidx.size()));
+            npp[size_t(loc[ln]) + 1] += 1;
+        }
+        cnp[size_t(ch) + 1] = int(cnodes.size());
     }
-    c->color_ptr.assign(size_t(ncol) + 1, 0);
-    for (long e = 0; e < ne; ++e)
-        c->color_ptr[size_t(color[size_t(e)]) + 1] += 1;
-    for (int k = 0; k < ncol; ++k)
-        c->color_ptr[size_t(k) + 1] += c->color_ptr[size_t(k)];
-    std::vector<int> celem(static_cast<size_t>(ne));
-    std::vector<int> cf(c->color_ptr.begin(), c->color_ptr.end() - 1);
-    for (long e = 0; e < ne; ++e)
-        celem[size_t(cf[size_t(color[size_t(e)])]++)] = int(e);
-    CK(c, c->color_elems.alloc(size_t(ne)));
-    CK(c, cudaMemcpyAsync(c->color_elems.p, celem.data(), sizeof(int) * size_t(ne),
-                          cudaMemcpyHostToDevice, st));
+    for (int A = 0; A < nn; ++A)
+        npp[size_t(A) + 1] += npp[size_t(A)];
+    npl.assign(cnodes.size(), 0);
+    {
+        std::vector<int> f(npp.begin(), npp.end() - 1);
+        for (size_t p = 0; p < cnodes.size(); ++p)
+            npl[size_t(f[size_t(cnodes[p])]++)] = int(p);
+    }
+    c->nchunks = nch;
+    c->max_nloc = maxnloc;
+    c->npairs = long(cnodes.size());
+    CK(c, c->lconn.alloc(lconn.size()));
+    CK(c, c->chunk_node_ptr.alloc(cnp.size()));
+    CK(c, c->chunk_nodes.alloc(cnodes.size()));
+    CK(c, c->slot_ptr.alloc(sptr.size()));
+    CK(c, c->slot_idx.alloc(sidx.size()));
+    CK(c, c->npart_ptr.alloc(npp.size()));
+    CK(c, c->npart.alloc(npl.size()));
+    CK(c, cudaMemcpyAsync(c->lconn.p, lconn.data(), sizeof(uint32_t) * lconn.size(), cudaMemcpyHostToDevice, st));
+    CK(c, cudaMemcpyAsync(c->chunk_node_ptr.p, cnp.data(), sizeof(int) * cnp.size(), cudaMemcpyHostToDevice, st));
+    CK(c, cudaMemcpyAsync(c->chunk_nodes.p, cnodes.data(), sizeof(int) * cnodes.size(), cudaMemcpyHostToDevice, st));
+    CK(c, cudaMemcpyAsync(c->slot_ptr.p, sptr.data(), sizeof(int) * sptr.size(), cudaMemcpyHostToDevice, st));
+    CK(c, cudaMemcpyAsync(c->slot_idx.p, sidx.data(), sidx.size(), cudaMemcpyHostToDevice, st));
+    CK(c, cudaMemcpyAsync(c->npart_ptr.p, npp.data(), sizeof(int) * npp.size(), cudaMemcpyHostToDevice, st));
+    CK(c, cudaMemcpyAsync(c->npart.p, npl.data(), sizeof(int) * npl.size(), cudaMemcpyHostToDevice, st));
+    CK(c, cudaStreamSynchronize(st));
 
     CK(c, c->partial.alloc(size_t(kRedBlocks) * 1024));
     CK(c, c->red.alloc(1024));
@@ -413,33 +447,37 @@ static int rows_per_matvec_cta(int N) { return std::max(1, 256 / N); }
 static int residual_dev(hbgpu_ctx* c, const double* d_state, double* d_r) {
     const int N = c->N;
     cudaStream_t st = c->stream;
-    const size_t tot = size_t(c->nn) * 4 * size_t(N);
     const long p0 = prof_mark(c);
-    CK(c, cudaMemsetAsync(d_r, 0, sizeof(double) * tot, st));
-    CK(c, cudaMemsetAsync(c->s.p, 0, sizeof(double) * size_t(c->nn) * 3 * size_t(N), st));
+    // nodal H*u at every node, Dirichlet ones included (assembly.cpp:453-463)
     if (N > 1)
         launch_apply_h_series(c->H.p, N, d_state, 4 * N, c->hu.p, 3 * N, c->nn, st);
     else
         CK(c, cudaMemsetAsync(c->hu.p, 0, sizeof(double) * size_t(c->nn) * 3, st));
     const long p1 = prof_mark(c);
-    ResidualArgs a;
-    a.conn = c->conn.p;
-    a.geom = c->geom.p;
-    a.state = d_state;
-    a.hu = c->hu.p;
-    a.r = d_r;
-    a.s = c->s.p;
-    a.N = N;
-    a.rho = c->rho;
-    a.mu = c->mu;
-    a.nu = c->mu / c->rho;
-    a.tau_mode = c->tau_mode;
-    a.flag = c->flag.p;
-    for (size_t k = 0; k + 1 < c->color_ptr.size(); ++k)
-        launch_residual_color(a, c->color_elems.p + c->color_ptr[k],
-                              c->color_ptr[k + 1] - c->color_ptr[k], st);
+    ResidualChunkArgs ca;
+    ca.geom = c->geom.p;
+    ca.state = d_state;
+    ca.hu = c->hu.p;
+    ca.lconn = c->lconn.p;
+    ca.chunk_node_ptr = c->chunk_node_ptr.p;
+    ca.chunk_nodes = c->chunk_nodes.p;
+    ca.slot_ptr = c->slot_ptr.p;
+    ca.slot_idx = c->slot_idx.p;
+    ca.partial = c->rpartial.p;
+    ca.ne = c->ne;
+    ca.N = N;
+    ca.T = kResTile;
+    ca.CE = kChunkElems;
+    ca.max_nloc = c->max_nloc;
+    ca.rho = c->rho;
+    ca.mu = c->mu;
+    ca.nu = c->mu / c->rho;
+    ca.tau_mode = c->tau_mode;
+    ca.flag = c->flag.p;
+    launch_residual_chunks(ca, c->nchunks, st);
     const long p2 = prof_mark(c);
-    launch_residual_finalize(c->H.p, N, c->s.p, c->dir.p, d_r, c->nn, st);
+    launch_residual_nodes(c->H.p, N, c->nn, c->npart_ptr.p, c->npart.p, c->rpartial.p, c->dir.p,
+                          d_r, st);
     if (c->nbnodes > 0) {
         BoundaryArgs b;
         b.bnode = c->bnode.p;
@@ -809,10 +847,10 @@ void hbgpu_destroy(hbgpu_ctx* c) {
     if (c->h_int)
         cudaFreeHost(c->h_int);
     for (DBuf<double>* b : {&c->geom, &c->H, &c->g, &c->hN, &c->fnormal, &c->farea, &c->state,
-                            &c->r, &c->hu, &c->s, &c->pvals, &c->mass, &c->inv, &c->y, &c->out,
-                            &c->x, &c->w, &c->scale, &c->b, &c->tmp, &c->V, &c->partial, &c->red})
+                            &c->r, &c->hu, &c->pvals, &c->mass, &c->inv, &c->y, &c->out,
+                            &c->x, &c->w, &c->scale, &c->b, &c->tmp, &c->V, &c->partial, &c->red, &c->rpartial})
         b->release();
-    for (DBuf<int>* b : {&c->row_ptr, &c->col_idx, &c->diag_blk, &c->inc_ptr, &c->color_elems,
+    for (DBuf<int>* b : {&c->row_ptr, &c->col_idx, &c->diag_blk, &c->inc_ptr, &c->chunk_node_ptr, &c->chunk_nodes, &c->slot_ptr, &c->npart_ptr, &c->npart,
                          &c->tcta, &c->bnode, &c->bptr, &c->binc, &c->fac, &c->fbc, &c->flag,
                          &c->ideg})
         b->release();
@@ -821,6 +859,8 @@ void hbgpu_destroy(hbgpu_ctx* c) {
     c->edmask.release();
     c->inc_elem.release();
     c->inc_cols.release();
+    c->lconn.release();
+    c->slot_idx.release();
     for (cudaEvent_t e : c->ev_pool)
         cudaEventDestroy(e);
     if (c->stream)
@@ -871,7 +911,8 @@ int hbgpu_set_basis(hbgpu_ctx* c, int modes, double period) {
                             &c->b, &c->tmp})
         CK(c, b->alloc(n));
     CK(c, c->hu.alloc(size_t(c->nn) * 3 * size_t(N)));
-    CK(c, c->s.alloc(size_t(c->nn) * 3 * size_t(N)));
+    CK(c, c->rpartial.alloc(size_t(c->npairs) * 7 * size_t(N)));
+    CK(c, configure_residual_smem(sizeof(double) * (size_t(c->max_nloc) * 7 * kResTile + size_t(kChunkElems) * 22 + size_t(kChunkElems) * 29 * kResTile)));
     CK(c, c->pvals.alloc(size_t(c->nnz) * 8 * size_t(N)));
     CK(c, c->mass.alloc(size_t(c->nnz)));
     CK(c, c->g.alloc(size_t(c->nn) * 3 * size_t(N)));

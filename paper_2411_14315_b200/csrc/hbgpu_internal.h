@@ -17,6 +17,9 @@ constexpr double kQB = 0.1381966011250105151795414;
 // Gauss-Seidel block: number of partial sums of the deterministic reductions.
 constexpr int kRedBlocks = 592;  // 4 x 148 SMs
 constexpr int kRedThreads = 256;
+// Residual element chunks: elements per chunk and time samples per CTA.
+constexpr int kChunkElems = 64;
+constexpr int kResTile = 4;
 
 // Number of kernel launches issued by this library (bench.py's gpu_launches).
 extern std::atomic<long long> g_launches;
@@ -24,17 +27,23 @@ cudaError_t run_fp64_peak(int blocks, int threads, int iters, double* out, float
 
 // ---------------------------------------------------------------- kernel args
 
-struct ResidualArgs {
-    const int4* conn;
-    const double* geom;   // 22 doubles / element
-    const double* state;  // (A*4+c)*N+n
-    const double* hu;     // (A*3+i)*N+n
-    double* r;            // (A*4+c)*N+n, accumulated
-    double* s;            // (A*3+i)*N+n, accumulated
-    int N;
+// Element-chunk residual: chunk c = elements [c*CE, (c+1)*CE); its distinct
+// nodes (sorted) are chunk_nodes[chunk_node_ptr[c] ..]; every (chunk, node)
+// pair p owns one partial-sum record of 7N doubles (r_u0..2, r_p, s0..2).
+struct ResidualChunkArgs {
+    const double* geom;
+    const double* state;
+    const double* hu;
+    const uint32_t* lconn;       // per element: 4 x uint8 chunk-local node ids
+    const int* chunk_node_ptr;   // nchunks + 1
+    const int* chunk_nodes;      // global node id per (chunk, node) pair
+    const int* slot_ptr;         // per pair: range in slot_idx
+    const uint8_t* slot_idx;     // el_local*4 + a, element order
+    double* partial;             // pairs * 7N
+    int ne, N, T, CE, max_nloc;
     double rho, mu, nu;
     int tau_mode;
-    int* flag;  // bit0: singular tau
+    int* flag;
 };
 
 struct TangentArgs {
@@ -92,9 +101,10 @@ void launch_geometry(const double* xyz, const int4* conn, int ne, double* geom, 
                      cudaStream_t st);
 void launch_apply_h_series(const double* H, int N, const double* in, int in_node_stride,
                            double* out, int out_node_stride, int nnodes, cudaStream_t st);
-void launch_residual_color(const ResidualArgs& a, const int* elems, int count, cudaStream_t st);
-void launch_residual_finalize(const double* H, int N, const double* s, const uint8_t* dir,
-                              double* r, int nn, cudaStream_t st);
+void launch_residual_chunks(const ResidualChunkArgs& a, int nchunks, cudaStream_t st);
+cudaError_t configure_residual_smem(size_t bytes);
+void launch_residual_nodes(const double* H, int N, int nn, const int* npart_ptr, const int* npart,
+                           const double* partial, const uint8_t* dir, double* r, cudaStream_t st);
 void launch_boundary(const BoundaryArgs& a, cudaStream_t st);
 cudaError_t configure_tangent_smem(size_t bytes);
 void launch_tangent_rows(const TangentArgs& a, int nctas, int threads, size_t smem,

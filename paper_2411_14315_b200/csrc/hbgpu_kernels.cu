@@ -175,166 +175,263 @@ void launch_apply_h_series(const double* H, int N, const double* in, int in_node
 
 // ---------------------------------------------------------------- residual
 
-// One (element, time sample) per thread, all elements of one colour class:
-// no two elements of a class share a node, so the scatter is a plain
-// read-modify-write (deterministic: each node sums its elements in colour
-// order).  Element residual of assembly.cpp:141-263 with the per-node sums
-// hoisted: u_q = B*sum_a u_a + (A-B)*u_q (same for Hu).
-__global__ void __launch_bounds__(256) residual_color_kernel(ResidualArgs a,
-                                                             const int* __restrict__ elems,
-                                                             int count) {
-    const int N = a.N;
-    const long t = (long)blockIdx.x * blockDim.x + threadIdx.x;
-    const int k = (int)(t / N);
-    const int n = (int)(t - (long)k * N);
-    if (k >= count)
-        return;
-    const int e = elems[k];
-    const int4 c = __ldg(&a.conn[e]);
-    const int nd[4] = {c.x, c.y, c.z, c.w};
-    Geo G;
-    load_geo(a.geom + 22 * (long)e, G);
 
-    double u[4][3], hu[4][3], p[4];
-#pragma unroll
-    for (int b = 0; b < 4; ++b) {
-        const double* sb = a.state + (long)nd[b] * 4 * N + n;
-        const double* hb = a.hu + (long)nd[b] * 3 * N + n;
-#pragma unroll
-        for (int i = 0; i < 3; ++i) {
-            u[b][i] = ldg(sb + i * N);
-            hu[b][i] = ldg(hb + i * N);
-        }
-        p[b] = ldg(sb + 3 * N);
-    }
-    const double rho = a.rho, V = G.V, w = 0.25 * V;
-
-    // element_fields (assembly.cpp:92-118)
-    double gu[3][3], gp[3];
+// Element residual at one (element, sample) with the quadrature sums
+// factored (W-trick), reading nodal data from shared memory and writing the
+// 28 element outputs into the element's shared-memory slots:
+//   r_m[a][i] = mu V gradN_a.grad u_i - dN_a/dx_i (V/4) sum p + rho V/20 (sum_b Hu_b,i + Hu_a,i)
+//             + w rho (B Cs_i + (A-B) conv_{q=a,i}) + w gradN_a . W_{:,i}
+//   s[a][i]   = w (B TLs_i + (A-B) tl_{q=a,i})
+//   r_c[a]    = w div u + (w/rho) gradN_a . TLs
+// with conv_q = u_q . grad u, tl_q = tau_q (rho Hu_q + rho conv_q + grad p),
+// Cs = sum_q conv_q, TLs = sum_q tl_q, W_ji = sum_q u_q,j tl_q,i.  Algebraically
+// identical to element_residual (assembly.cpp:141-263): N_a(q) = B + (A-B) delta_aq.
+// Slot layout: out[(a*7 + c) * T], c = 0..2 r_m, 3 r_c, 4..6 s.
+__device__ __forceinline__ void element_residual_smem(const double* __restrict__ g,
+                                                      const double* __restrict__ nd, int ndst,
+                                                      const int lc[4], int T, int t,
+                                                      double rho, double mu, double nu,
+                                                      int tau_mode, int* flag,
+                                                      double* __restrict__ out) {
+    // nd: node data [ln][c][t], c = u0 u1 u2 p hu0 hu1 hu2, node stride ndst
+    auto U = [&](int b, int c) { return nd[lc[b] * ndst + c * T + t]; };
+    const double V = g[12], w = 0.25 * V;
+    double gu[3][3], gp[3], usum[3], hsum[3], psum = 0.0;
 #pragma unroll
     for (int i = 0; i < 3; ++i) {
+        gp[i] = 0.0;
+        usum[i] = 0.0;
+        hsum[i] = 0.0;
 #pragma unroll
         for (int j = 0; j < 3; ++j)
-            gu[i][j] = G.gN[0][j] * u[0][i] + G.gN[1][j] * u[1][i] + G.gN[2][j] * u[2][i] +
-                       G.gN[3][j] * u[3][i];
-        gp[i] = G.gN[0][i] * p[0] + G.gN[1][i] * p[1] + G.gN[2][i] * p[2] + G.gN[3][i] * p[3];
+            gu[i][j] = 0.0;
     }
-    const double div = gu[0][0] + gu[1][1] + gu[2][2];
-    const double psum = p[0] + p[1] + p[2] + p[3];
-    double usum[3], hsum[3];
-#pragma unroll
-    for (int i = 0; i < 3; ++i) {
-        usum[i] = u[0][i] + u[1][i] + u[2][i] + u[3][i];
-        hsum[i] = hu[0][i] + hu[1][i] + hu[2][i] + hu[3][i];
-    }
-
-    // constant-gradient Galerkin rows (assembly.cpp:156-192):
-    // mu V gradN_a.grad u_i - dN_a/dx_i (V/4) sum p + rho sum_b M_ab Hu_b,i
-    double rm[4][3], sv[4][3], rc[4];
-    const double muV = a.mu * V, moff = rho * V / 20.0;
 #pragma unroll
     for (int b = 0; b < 4; ++b) {
+        const double pb = U(b, 3);
+        psum += pb;
 #pragma unroll
         for (int i = 0; i < 3; ++i) {
-            rm[b][i] = muV * (G.gN[b][0] * gu[i][0] + G.gN[b][1] * gu[i][1] +
-                              G.gN[b][2] * gu[i][2]) -
-                       G.gN[b][i] * w * psum + moff * (hsum[i] + hu[b][i]);
-            sv[b][i] = 0.0;
+            const double ub = U(b, i);
+            usum[i] += ub;
+            hsum[i] += U(b, 4 + i);
+            gp[i] += g[3 * b + i] * pb;
+#pragma unroll
+            for (int j = 0; j < 3; ++j)
+                gu[i][j] += g[3 * b + j] * ub;
         }
-        rc[b] = w * div;
     }
-
-    const double diff = 3.0 * a.nu * a.nu * xi_dd(G);
+    const double div = gu[0][0] + gu[1][1] + gu[2][2];
+    double xx = 0.0;
+#pragma unroll
+    for (int k = 0; k < 9; ++k)
+        xx += g[13 + k] * g[13 + k];
+    const double diff = 3.0 * nu * nu * xx;
     double tau_mean = 0.0;
-    if (a.tau_mode == 1) {
-        const double um[3] = {0.25 * usum[0], 0.25 * usum[1], 0.25 * usum[2]};
-        tau_mean = tau_of(G, um, diff, a.flag);
+    if (tau_mode == 1) {
+        double um[3] = {0.25 * usum[0], 0.25 * usum[1], 0.25 * usum[2]};
+        double conv = 0.0;
+#pragma unroll
+        for (int i = 0; i < 3; ++i)
+            conv += um[i] * (g[13 + 3 * i] * um[0] + g[14 + 3 * i] * um[1] + g[15 + 3 * i] * um[2]);
+        const double arg = conv + diff;
+        if (!(arg > 0.0))
+            atomicOr(flag, 1);
+        tau_mean = arg > 0.0 ? rsqrt(arg) : 0.0;
     }
-    const double dAB = kQA - kQB, wr = w / rho;
+    const double dAB = kQA - kQB;
+    double Cs[3] = {0, 0, 0}, TLs[3] = {0, 0, 0}, W[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
         double uq[3], huq[3];
 #pragma unroll
         for (int i = 0; i < 3; ++i) {
-            uq[i] = kQB * usum[i] + dAB * u[q][i];
-            huq[i] = kQB * hsum[i] + dAB * hu[q][i];
+            uq[i] = kQB * usum[i] + dAB * U(q, i);
+            huq[i] = kQB * hsum[i] + dAB * U(q, 4 + i);
         }
-        const double tau = a.tau_mode == 0 ? tau_of(G, uq, diff, a.flag) : tau_mean;
-        double conv[3], tl[3];
+        double tau = tau_mean;
+        if (tau_mode == 0) {
+            double conv = 0.0;
+#pragma unroll
+            for (int i = 0; i < 3; ++i)
+                conv += uq[i] * (g[13 + 3 * i] * uq[0] + g[14 + 3 * i] * uq[1] + g[15 + 3 * i] * uq[2]);
+            const double arg = conv + diff;
+            if (!(arg > 0.0))
+                atomicOr(flag, 1);
+            tau = arg > 0.0 ? rsqrt(arg) : 0.0;
+        }
+        double* oq = out + q * 7 * T;
 #pragma unroll
         for (int i = 0; i < 3; ++i) {
-            conv[i] = uq[0] * gu[i][0] + uq[1] * gu[i][1] + uq[2] * gu[i][2];
-            tl[i] = tau * (rho * huq[i] + rho * conv[i] + gp[i]);  // tau * strong residual
-        }
+            const double cv = uq[0] * gu[i][0] + uq[1] * gu[i][1] + uq[2] * gu[i][2];
+            const double tl = tau * (rho * huq[i] + rho * cv + gp[i]);
+            Cs[i] += cv;
+            TLs[i] += tl;
 #pragma unroll
-        for (int b = 0; b < 4; ++b) {
-            const double sa = (b == q) ? kQA : kQB;
-            const double adv = uq[0] * G.gN[b][0] + uq[1] * G.gN[b][1] + uq[2] * G.gN[b][2];
-#pragma unroll
-            for (int i = 0; i < 3; ++i) {
-                rm[b][i] += w * (rho * sa * conv[i] + adv * tl[i]);
-                sv[b][i] += w * sa * tl[i];
-            }
-            rc[b] += wr * (G.gN[b][0] * tl[0] + G.gN[b][1] * tl[1] + G.gN[b][2] * tl[2]);
+            for (int j = 0; j < 3; ++j)
+                W[j][i] += uq[j] * tl;
+            oq[i * T] = w * rho * dAB * cv;     // node a = q part of the convection row
+            oq[(4 + i) * T] = w * dAB * tl;     // node a = q part of the LS time row
         }
     }
-
+    const double muV = mu * V, moff = rho * V / 20.0, wr = w / rho;
 #pragma unroll
-    for (int b = 0; b < 4; ++b) {
-        double* rb = a.r + (long)nd[b] * 4 * N + n;
-        double* sb = a.s + (long)nd[b] * 3 * N + n;
+    for (int a = 0; a < 4; ++a) {
+        const double ga0 = g[3 * a], ga1 = g[3 * a + 1], ga2 = g[3 * a + 2];
+        double* oa = out + a * 7 * T;
 #pragma unroll
         for (int i = 0; i < 3; ++i) {
-            rb[i * N] += rm[b][i];
-            sb[i * N] += sv[b][i];
+            const double gai = g[3 * a + i];
+            oa[i * T] += muV * (ga0 * gu[i][0] + ga1 * gu[i][1] + ga2 * gu[i][2]) - gai * w * psum +
+                         moff * (hsum[i] + U(a, 4 + i)) + w * rho * kQB * Cs[i] +
+                         w * (ga0 * W[0][i] + ga1 * W[1][i] + ga2 * W[2][i]);
+            oa[(4 + i) * T] += w * kQB * TLs[i];
         }
-        rb[3 * N] += rc[b];
+        oa[3 * T] = w * div + wr * (ga0 * TLs[0] + ga1 * TLs[1] + ga2 * TLs[2]);
     }
 }
 
-void launch_residual_color(const ResidualArgs& a, const int* elems, int count, cudaStream_t st) {
-    if (count <= 0)
-        return;
-    const long threads = (long)count * a.N;
-    note_launch();
-    residual_color_kernel<<<(int)((threads + 255) / 256), 256, 0, st>>>(a, elems, count);
-}
+// One CTA per (element chunk, time-sample tile).  Phase 0 stages the chunk's
+// nodal data (u, p, Hu) and element geometry in shared memory; phase 1 runs
+// one (element, sample) per thread into per-element slots; phase 2 reduces
+// the slots of every chunk node in fixed (element, local index) order and
+// writes one partial sum per (chunk, node).  Deterministic, no atomics.
+__global__ void __launch_bounds__(256, 2) residual_chunk_kernel(ResidualChunkArgs a) {
+    extern __shared__ double sm[];
+    const int N = a.N, T = a.T, CE = a.CE;
+    const int c = blockIdx.x;
+    const int n0 = blockIdx.y * T;
+    const int nb = a.chunk_node_ptr[c];
+    const int nloc = a.chunk_node_ptr[c + 1] - nb;
+    const int e0 = c * CE;
+    const int ecount = min(CE, a.ne - e0);
+    const int ndst = 7 * T;
+    const int es = 29 * T;  // padded element slot stride (bank spread)
+    double* nd = sm;
+    double* geo = nd + (size_t)a.max_nloc * ndst;
+    double* slots = geo + (size_t)CE * 22;
 
-// r_u -= H s, then zero the Dirichlet velocity rows (assembly.cpp:523-535,541-544).
-__global__ void residual_finalize_kernel(const double* __restrict__ H, int N,
-                                         const double* __restrict__ s,
-                                         const uint8_t* __restrict__ dir, double* __restrict__ r,
-                                         int nn) {
-    extern __shared__ double sh[];
-    for (int k = threadIdx.x; k < N * N; k += blockDim.x)
-        sh[k] = H[k];
+    for (int k = threadIdx.x; k < nloc * ndst; k += blockDim.x) {
+        const int ln = k / ndst, rem = k - ln * ndst;
+        const int cc = rem / T, t = rem - cc * T;
+        const int n = n0 + t;
+        const long A = a.chunk_nodes[nb + ln];
+        double v = 0.0;
+        if (n < N)
+            v = cc < 4 ? a.state[(A * 4 + cc) * N + n] : a.hu[(A * 3 + (cc - 4)) * N + n];
+        nd[k] = v;
+    }
+    for (int k = threadIdx.x; k < ecount * 22; k += blockDim.x)
+        geo[k] = a.geom[(long)e0 * 22 + k];
     __syncthreads();
-    const int per = blockDim.x / N;
-    const int ls = threadIdx.x / N, n = threadIdx.x - ls * N;
-    const long sr = (long)blockIdx.x * per + ls;
-    if (ls >= per || sr >= 3L * nn)
-        return;
-    const long A = sr / 3;
-    const int i = (int)(sr - 3 * A);
-    double* out = r + A * 4 * N + (long)i * N + n;
-    if (dir[A]) {
-        *out = 0.0;
-        return;
+
+    {
+        const int el = threadIdx.x / T, t = threadIdx.x - el * T;
+        if (el < ecount && n0 + t < N) {
+            const uint32_t pk = a.lconn[e0 + el];
+            const int lc[4] = {int(pk & 0xFF), int((pk >> 8) & 0xFF), int((pk >> 16) & 0xFF),
+                               int(pk >> 24)};
+            element_residual_smem(geo + el * 22, nd, ndst, lc, T, t, a.rho, a.mu, a.nu,
+                                  a.tau_mode, a.flag, slots + el * es + t);
+        }
     }
-    const double* src = s + sr * N;
-    double acc = 0.0;
-    for (int m = 0; m < N; ++m)
-        acc += sh[n * N + m] * src[m];
-    *out -= acc;
+    __syncthreads();
+
+    for (int k = threadIdx.x; k < nloc * ndst; k += blockDim.x) {
+        const int ln = k / ndst, rem = k - ln * ndst;
+        const int cc = rem / T, t = rem - cc * T;
+        const int n = n0 + t;
+        if (n >= N)
+            continue;
+        const int p = nb + ln;
+        double acc = 0.0;
+        for (int q = a.slot_ptr[p]; q < a.slot_ptr[p + 1]; ++q) {
+            const int sl = a.slot_idx[q];  // el*4 + a
+            acc += slots[(sl >> 2) * es + ((sl & 3) * 7 + cc) * T + t];
+        }
+        a.partial[(long)p * 7 * N + (long)cc * N + n] = acc;
+    }
 }
 
-void launch_residual_finalize(const double* H, int N, const double* s, const uint8_t* dir,
-                              double* r, int nn, cudaStream_t st) {
-    const int per = (N >= 256) ? 1 : 256 / N;
-    const long nser = 3L * nn;
+void launch_residual_chunks(const ResidualChunkArgs& a, int nchunks, cudaStream_t st) {
+    if (nchunks <= 0)
+        return;
+    const dim3 grid(nchunks, (a.N + a.T - 1) / a.T);
+    const size_t smem = sizeof(double) * ((size_t)a.max_nloc * 7 * a.T + (size_t)a.CE * 22 +
+                                          (size_t)a.CE * 29 * a.T);
     note_launch();
-    residual_finalize_kernel<<<(int)((nser + per - 1) / per), per * N,
-                               sizeof(double) * N * N, st>>>(H, N, s, dir, r, nn);
+    residual_chunk_kernel<<<grid, a.CE * a.T, smem, st>>>(a);
+}
+
+cudaError_t configure_residual_smem(size_t bytes) {
+    return cudaFuncSetAttribute(residual_chunk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                int(bytes < 48 * 1024 ? 48 * 1024 : bytes));
+}
+
+// Node pass: sums the node's chunk partials in chunk order, completes the
+// least-squares rows r_u -= H s (assembly.cpp:523-535) and zeroes Dirichlet
+// velocity rows (assembly.cpp:541-544).  Thread (node, n); the N threads of a
+// node exchange s through shared memory for the dense H product.
+__global__ void __launch_bounds__(256) residual_nodes_kernel(const double* __restrict__ H, int N,
+                                                             int nn, int rows_per_cta,
+                                                             const int* __restrict__ npart_ptr,
+                                                             const int* __restrict__ npart,
+                                                             const double* __restrict__ partial,
+                                                             const uint8_t* __restrict__ dir,
+                                                             double* __restrict__ r) {
+    extern __shared__ double sh[];
+    double* sH = sh;
+    double* ss = sh + N * N;
+    for (int k = threadIdx.x; k < N * N; k += blockDim.x)
+        sH[k] = H[k];
+    const int rr = threadIdx.x / N, n = threadIdx.x - rr * N;
+    const long A = (long)blockIdx.x * rows_per_cta + rr;
+    const bool valid = rr < rows_per_cta && A < nn;
+    double v[7] = {0, 0, 0, 0, 0, 0, 0};
+    if (valid) {
+        for (int q = npart_ptr[A]; q < npart_ptr[A + 1]; ++q) {
+            const double* pp = partial + (long)npart[q] * 7 * N + n;
+#pragma unroll
+            for (int cc = 0; cc < 7; ++cc)
+                v[cc] += pp[cc * N];
+        }
+#pragma unroll
+        for (int i = 0; i < 3; ++i)
+            ss[(rr * 3 + i) * N + n] = v[4 + i];
+    }
+    __syncthreads();
+    if (!valid)
+        return;
+    double* out = r + A * 4 * N + n;
+    if (dir[A]) {
+        out[0] = 0.0;
+        out[N] = 0.0;
+        out[2 * N] = 0.0;
+    } else {
+        const double* h = sH + n * N;
+        const double* s0 = ss + rr * 3 * N;
+        double h0 = 0.0, h1 = 0.0, h2 = 0.0;
+        for (int m = 0; m < N; ++m) {
+            h0 += h[m] * s0[m];
+            h1 += h[m] * s0[N + m];
+            h2 += h[m] * s0[2 * N + m];
+        }
+        out[0] = v[0] - h0;
+        out[N] = v[1] - h1;
+        out[2 * N] = v[2] - h2;
+    }
+    out[3 * N] = v[3];
+}
+
+void launch_residual_nodes(const double* H, int N, int nn, const int* npart_ptr, const int* npart,
+                           const double* partial, const uint8_t* dir, double* r, cudaStream_t st) {
+    if (nn <= 0)
+        return;
+    const int rows = N >= 256 ? 1 : 256 / N;
+    const size_t smem = sizeof(double) * ((size_t)N * N + 3 * (size_t)N * rows);
+    note_launch();
+    residual_nodes_kernel<<<(nn + rows - 1) / rows, rows * N, smem, st>>>(H, N, nn, rows, npart_ptr,
+                                                                         npart, partial, dir, r);
 }
 
 // Neumann traction + backflow (assembly.cpp:376-413), node-centric: one
