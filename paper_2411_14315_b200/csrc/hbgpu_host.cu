@@ -86,7 +86,7 @@ struct hbgpu_ctx {
     DBuf<int> row_ptr, col_idx, diag_blk, inc_ptr;
     DBuf<uint32_t> inc_elem, inc_cols;
     // residual element chunks
-    int nchunks = 0, max_nloc = 0;
+    int nchunks = 0, max_nloc = 0, res_grid = 0;
     long npairs = 0;
     DBuf<uint32_t> lconn;
     DBuf<int> chunk_node_ptr, chunk_nodes, slot_ptr, npart_ptr, npart;
@@ -414,6 +414,7 @@ static int plan_tangent(hbgpu_ctx* c) {
     c->tcta_h.clear();
     c->tcta_h.push_back(0);
     size_t maxsmem = 0;
+    int used_rows = 1;
     int A = 0;
     while (A < c->nn) {
         int B = A;
@@ -427,13 +428,14 @@ static int plan_tangent(hbgpu_ctx* c) {
             ++B;
         }
         maxsmem = std::max(maxsmem, bytes);
+        used_rows = std::max(used_rows, B - A);
         c->tcta_h.push_back(B);
         A = B;
     }
     if (maxsmem > 227 * 1024)
         return fail(c, HBGPU_ERR_INVALID, "a block row exceeds the shared-memory budget");
     c->tsmem = maxsmem;
-    c->tthreads = ((max_rows * N + 31) / 32) * 32;
+    c->tthreads = ((used_rows * N + 31) / 32) * 32;
     CK(c, c->tcta.alloc(c->tcta_h.size()));
     CK(c, cudaMemcpyAsync(c->tcta.p, c->tcta_h.data(), sizeof(int) * c->tcta_h.size(),
                           cudaMemcpyHostToDevice, c->stream));
@@ -469,15 +471,17 @@ static int residual_dev(hbgpu_ctx* c, const double* d_state, double* d_r) {
     ca.T = kResTile;
     ca.CE = kChunkElems;
     ca.max_nloc = c->max_nloc;
+    ca.nchunks = c->nchunks;
+    ca.npairs = c->npairs;
     ca.rho = c->rho;
     ca.mu = c->mu;
     ca.nu = c->mu / c->rho;
     ca.tau_mode = c->tau_mode;
     ca.flag = c->flag.p;
-    launch_residual_chunks(ca, c->nchunks, st);
+    launch_residual_chunks(ca, c->res_grid, st);
     const long p2 = prof_mark(c);
     launch_residual_nodes(c->H.p, N, c->nn, c->npart_ptr.p, c->npart.p, c->rpartial.p, c->dir.p,
-                          d_r, st);
+                          d_r, kResTile, c->npairs, st);
     if (c->nbnodes > 0) {
         BoundaryArgs b;
         b.bnode = c->bnode.p;
@@ -911,8 +915,16 @@ int hbgpu_set_basis(hbgpu_ctx* c, int modes, double period) {
                             &c->b, &c->tmp})
         CK(c, b->alloc(n));
     CK(c, c->hu.alloc(size_t(c->nn) * 3 * size_t(N)));
-    CK(c, c->rpartial.alloc(size_t(c->npairs) * 7 * size_t(N)));
-    CK(c, configure_residual_smem(sizeof(double) * (size_t(c->max_nloc) * 7 * kResTile + size_t(kChunkElems) * 22 + size_t(kChunkElems) * 29 * kResTile)));
+    CK(c, c->rpartial.alloc(size_t(c->npairs) * 7 * size_t((N + kResTile - 1) / kResTile) * kResTile));
+    {
+        const size_t rs = residual_smem_bytes(c->max_nloc, kChunkElems, kResTile);
+        CK(c, configure_residual_smem(rs));
+        int per_sm = 0, nsm = 0, dev = 0;
+        CK(c, cudaGetDevice(&dev));
+        CK(c, cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+        CK(c, residual_occupancy(&per_sm, rs));
+        c->res_grid = nsm * std::max(1, per_sm);
+    }
     CK(c, c->pvals.alloc(size_t(c->nnz) * 8 * size_t(N)));
     CK(c, c->mass.alloc(size_t(c->nnz)));
     CK(c, c->g.alloc(size_t(c->nn) * 3 * size_t(N)));

@@ -40,7 +40,8 @@ struct ResidualChunkArgs {
     const int* slot_ptr;         // per pair: range in slot_idx
     const uint8_t* slot_idx;     // el_local*4 + a, element order
     double* partial;             // pairs * 7N
-    int ne, N, T, CE, max_nloc;
+    int ne, N, T, CE, max_nloc, nchunks;
+    long npairs;
     double rho, mu, nu;
     int tau_mode;
     int* flag;
@@ -101,10 +102,13 @@ void launch_geometry(const double* xyz, const int4* conn, int ne, double* geom, 
                      cudaStream_t st);
 void launch_apply_h_series(const double* H, int N, const double* in, int in_node_stride,
                            double* out, int out_node_stride, int nnodes, cudaStream_t st);
-void launch_residual_chunks(const ResidualChunkArgs& a, int nchunks, cudaStream_t st);
+size_t residual_smem_bytes(int max_nloc, int CE, int T);
+void launch_residual_chunks(const ResidualChunkArgs& a, int grid, cudaStream_t st);
 cudaError_t configure_residual_smem(size_t bytes);
+cudaError_t residual_occupancy(int* blocks_per_sm, size_t smem);
 void launch_residual_nodes(const double* H, int N, int nn, const int* npart_ptr, const int* npart,
-                           const double* partial, const uint8_t* dir, double* r, cudaStream_t st);
+                           const double* partial, const uint8_t* dir, double* r, int T,
+                           long npairs, cudaStream_t st);
 void launch_boundary(const BoundaryArgs& a, cudaStream_t st);
 cudaError_t configure_tangent_smem(size_t bytes);
 void launch_tangent_rows(const TangentArgs& a, int nctas, int threads, size_t smem,

@@ -291,76 +291,116 @@ __device__ __forceinline__ void element_residual_smem(const double* __restrict__
     }
 }
 
-// One CTA per (element chunk, time-sample tile).  Phase 0 stages the chunk's
-// nodal data (u, p, Hu) and element geometry in shared memory; phase 1 runs
-// one (element, sample) per thread into per-element slots; phase 2 reduces
-// the slots of every chunk node in fixed (element, local index) order and
-// writes one partial sum per (chunk, node).  Deterministic, no atomics.
-__global__ void __launch_bounds__(256, 2) residual_chunk_kernel(ResidualChunkArgs a) {
-    extern __shared__ double sm[];
-    const int N = a.N, T = a.T, CE = a.CE;
-    const int c = blockIdx.x;
-    const int n0 = blockIdx.y * T;
-    const int nb = a.chunk_node_ptr[c];
-    const int nloc = a.chunk_node_ptr[c + 1] - nb;
-    const int e0 = c * CE;
-    const int ecount = min(CE, a.ne - e0);
-    const int ndst = 7 * T;
-    const int es = 29 * T;  // padded element slot stride (bank spread)
-    double* nd = sm;
-    double* geo = nd + (size_t)a.max_nloc * ndst;
-    double* slots = geo + (size_t)CE * 22;
+// Residual element pass as a persistent, double-buffered pipeline.  Work
+// item = (element chunk, time-sample tile); CTA b handles items b, b+G, ...
+// (tile fastest, so the tiles of a chunk reuse its data from L2).  While the
+// CTA computes item k from shared memory, cp.async (LDGSTS) gathers the nodal
+// data (u, p, Hu) and geometry of item k+1 into the other buffer.  Per item:
+// one (element, sample) per thread into per-element slots, then every chunk
+// node's slots are reduced in fixed (element, local index) order and written
+// as one partial record.  Partials are tile-major and contiguous per item:
+// partial[((tile*npairs + p)*7 + c)*T + t].  Deterministic, no atomics.
+__device__ __forceinline__ void cp_async8(double* smem_dst, const double* gsrc) {
+    const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem_dst));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gsrc));
+}
+__device__ __forceinline__ void cp_async16(double* smem_dst, const double* gsrc) {
+    const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem_dst));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gsrc));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int K>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(K));
+}
 
+__device__ __forceinline__ void residual_issue(const ResidualChunkArgs& a, int item, int ntiles,
+                                               double* nd, double* geo) {
+    const int N = a.N, T = a.T, CE = a.CE, ndst = 7 * T;
+    const int ch = item / ntiles, n0 = (item - ch * ntiles) * T;
+    const int nb = a.chunk_node_ptr[ch], nloc = a.chunk_node_ptr[ch + 1] - nb;
+    const int e0 = ch * CE, ecount = min(CE, a.ne - e0);
     for (int k = threadIdx.x; k < nloc * ndst; k += blockDim.x) {
         const int ln = k / ndst, rem = k - ln * ndst;
         const int cc = rem / T, t = rem - cc * T;
         const int n = n0 + t;
         const long A = a.chunk_nodes[nb + ln];
-        double v = 0.0;
         if (n < N)
-            v = cc < 4 ? a.state[(A * 4 + cc) * N + n] : a.hu[(A * 3 + (cc - 4)) * N + n];
-        nd[k] = v;
+            cp_async8(nd + k, cc < 4 ? a.state + (A * 4 + cc) * N + n
+                                     : a.hu + (A * 3 + (cc - 4)) * N + n);
+        else
+            nd[k] = 0.0;
     }
-    for (int k = threadIdx.x; k < ecount * 22; k += blockDim.x)
-        geo[k] = a.geom[(long)e0 * 22 + k];
-    __syncthreads();
-
-    {
-        const int el = threadIdx.x / T, t = threadIdx.x - el * T;
-        if (el < ecount && n0 + t < N) {
-            const uint32_t pk = a.lconn[e0 + el];
-            const int lc[4] = {int(pk & 0xFF), int((pk >> 8) & 0xFF), int((pk >> 16) & 0xFF),
-                               int(pk >> 24)};
-            element_residual_smem(geo + el * 22, nd, ndst, lc, T, t, a.rho, a.mu, a.nu,
-                                  a.tau_mode, a.flag, slots + el * es + t);
-        }
-    }
-    __syncthreads();
-
-    for (int k = threadIdx.x; k < nloc * ndst; k += blockDim.x) {
-        const int ln = k / ndst, rem = k - ln * ndst;
-        const int cc = rem / T, t = rem - cc * T;
-        const int n = n0 + t;
-        if (n >= N)
-            continue;
-        const int p = nb + ln;
-        double acc = 0.0;
-        for (int q = a.slot_ptr[p]; q < a.slot_ptr[p + 1]; ++q) {
-            const int sl = a.slot_idx[q];  // el*4 + a
-            acc += slots[(sl >> 2) * es + ((sl & 3) * 7 + cc) * T + t];
-        }
-        a.partial[(long)p * 7 * N + (long)cc * N + n] = acc;
-    }
+    const double* gsrc = a.geom + (long)e0 * 22;
+    for (int k = threadIdx.x; k < ecount * 11; k += blockDim.x)
+        cp_async16(geo + 2 * k, gsrc + 2 * k);
 }
 
-void launch_residual_chunks(const ResidualChunkArgs& a, int nchunks, cudaStream_t st) {
-    if (nchunks <= 0)
+__global__ void __launch_bounds__(256, 2) residual_chunk_kernel(ResidualChunkArgs a) {
+    extern __shared__ __align__(16) double sm[];
+    const int N = a.N, T = a.T, CE = a.CE;
+    const int ntiles = (N + T - 1) / T;
+    const int nitems = a.nchunks * ntiles;
+    const int ndst = 7 * T;
+    const int es = 29 * T;  // padded element slot stride (bank spread)
+    const int bufsz = a.max_nloc * ndst + CE * 22;
+    double* buf[2] = {sm, sm + bufsz};
+    double* slots = sm + 2 * bufsz;
+
+    int item = blockIdx.x;
+    int cur = 0;
+    if (item < nitems)
+        residual_issue(a, item, ntiles, buf[0], buf[0] + a.max_nloc * ndst);
+    cp_async_commit();
+    for (; item < nitems; item += gridDim.x, cur ^= 1) {
+        const int next = item + gridDim.x;
+        if (next < nitems)
+            residual_issue(a, next, ntiles, buf[cur ^ 1], buf[cur ^ 1] + a.max_nloc * ndst);
+        cp_async_commit();
+        cp_async_wait<1>();
+        __syncthreads();
+
+        const int ch = item / ntiles, tile = item - ch * ntiles, n0 = tile * T;
+        const int nb = a.chunk_node_ptr[ch], nloc = a.chunk_node_ptr[ch + 1] - nb;
+        const int e0 = ch * CE, ecount = min(CE, a.ne - e0);
+        const double* nd = buf[cur];
+        const double* geo = buf[cur] + a.max_nloc * ndst;
+        {
+            const int el = threadIdx.x / T, t = threadIdx.x - el * T;
+            if (el < ecount && n0 + t < N) {
+                const uint32_t pk = a.lconn[e0 + el];
+                const int lc[4] = {int(pk & 0xFF), int((pk >> 8) & 0xFF), int((pk >> 16) & 0xFF),
+                                   int(pk >> 24)};
+                element_residual_smem(geo + el * 22, nd, ndst, lc, T, t, a.rho, a.mu, a.nu,
+                                      a.tau_mode, a.flag, slots + el * es + t);
+            }
+        }
+        __syncthreads();
+        double* out = a.partial + ((long)tile * a.npairs + nb) * ndst;
+        for (int k = threadIdx.x; k < nloc * ndst; k += blockDim.x) {
+            const int ln = k / ndst, rem = k - ln * ndst;
+            const int cc = rem / T, t = rem - cc * T;
+            const int p = nb + ln;
+            double acc = 0.0;
+            for (int q = a.slot_ptr[p]; q < a.slot_ptr[p + 1]; ++q) {
+                const int sl = a.slot_idx[q];  // el*4 + a
+                acc += slots[(sl >> 2) * es + ((sl & 3) * 7 + cc) * T + t];
+            }
+            out[k] = acc;
+        }
+    }
+    cp_async_wait<0>();
+}
+
+size_t residual_smem_bytes(int max_nloc, int CE, int T) {
+    return sizeof(double) * (2 * ((size_t)max_nloc * 7 * T + (size_t)CE * 22) + (size_t)CE * 29 * T);
+}
+
+void launch_residual_chunks(const ResidualChunkArgs& a, int grid, cudaStream_t st) {
+    if (a.nchunks <= 0)
         return;
-    const dim3 grid(nchunks, (a.N + a.T - 1) / a.T);
-    const size_t smem = sizeof(double) * ((size_t)a.max_nloc * 7 * a.T + (size_t)a.CE * 22 +
-                                          (size_t)a.CE * 29 * a.T);
     note_launch();
-    residual_chunk_kernel<<<grid, a.CE * a.T, smem, st>>>(a);
+    residual_chunk_kernel<<<grid, a.CE * a.T, residual_smem_bytes(a.max_nloc, a.CE, a.T), st>>>(a);
 }
 
 cudaError_t configure_residual_smem(size_t bytes) {
@@ -378,7 +418,8 @@ __global__ void __launch_bounds__(256) residual_nodes_kernel(const double* __res
                                                              const int* __restrict__ npart,
                                                              const double* __restrict__ partial,
                                                              const uint8_t* __restrict__ dir,
-                                                             double* __restrict__ r) {
+                                                             double* __restrict__ r, int T,
+                                                             long npairs) {
     extern __shared__ double sh[];
     double* sH = sh;
     double* ss = sh + N * N;
@@ -390,10 +431,11 @@ __global__ void __launch_bounds__(256) residual_nodes_kernel(const double* __res
     double v[7] = {0, 0, 0, 0, 0, 0, 0};
     if (valid) {
         for (int q = npart_ptr[A]; q < npart_ptr[A + 1]; ++q) {
-            const double* pp = partial + (long)npart[q] * 7 * N + n;
+            const int tile = n / T, t = n - tile * T;
+            const double* pp = partial + ((long)tile * npairs + npart[q]) * 7 * T + t;
 #pragma unroll
             for (int cc = 0; cc < 7; ++cc)
-                v[cc] += pp[cc * N];
+                v[cc] += pp[cc * T];
         }
 #pragma unroll
         for (int i = 0; i < 3; ++i)
@@ -424,14 +466,15 @@ __global__ void __launch_bounds__(256) residual_nodes_kernel(const double* __res
 }
 
 void launch_residual_nodes(const double* H, int N, int nn, const int* npart_ptr, const int* npart,
-                           const double* partial, const uint8_t* dir, double* r, cudaStream_t st) {
+                           const double* partial, const uint8_t* dir, double* r, int T,
+                           long npairs, cudaStream_t st) {
     if (nn <= 0)
         return;
     const int rows = N >= 256 ? 1 : 256 / N;
     const size_t smem = sizeof(double) * ((size_t)N * N + 3 * (size_t)N * rows);
     note_launch();
     residual_nodes_kernel<<<(nn + rows - 1) / rows, rows * N, smem, st>>>(H, N, nn, rows, npart_ptr,
-                                                                         npart, partial, dir, r);
+                                                                         npart, partial, dir, r, T, npairs);
 }
 
 // Neumann traction + backflow (assembly.cpp:376-413), node-centric: one
@@ -1034,4 +1077,11 @@ cudaError_t run_fp64_peak(int blocks, int threads, int iters, double* out, float
     return err == cudaSuccess ? cudaGetLastError() : err;
 }
 
+}  // namespace hbgpu
+
+namespace hbgpu {
+cudaError_t residual_occupancy(int* blocks_per_sm, size_t smem) {
+    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, residual_chunk_kernel,
+                                                         kChunkElems * kResTile, smem);
+}
 }  // namespace hbgpu
