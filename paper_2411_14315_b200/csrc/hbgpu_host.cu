@@ -82,9 +82,10 @@ struct hbgpu_ctx {
     // device mesh structures
     DBuf<int4> conn;
     DBuf<double> geom;
-    DBuf<uint8_t> dir, edmask;
+    DBuf<uint8_t> dir;
+    DBuf<int4> inc_rec;
+    DBuf<double> tgeom;
     DBuf<int> row_ptr, col_idx, diag_blk, inc_ptr;
-    DBuf<uint32_t> inc_elem, inc_cols;
     // residual element chunks
     int nchunks = 0, max_nloc = 0, res_grid = 0;
     long npairs = 0;
@@ -297,14 +298,13 @@ static int upload_all(hbgpu_ctx* c, const hbgpu_mesh_desc* d) {
             iptr[size_t(d->conn[4 * e + a]) + 1] += 1;
     for (int A = 0; A < nn; ++A)
         iptr[size_t(A) + 1] += iptr[size_t(A)];
-    std::vector<uint32_t> ielem(size_t(4) * size_t(ne)), icols(size_t(4) * size_t(ne));
+    // record per incidence: conn[4] | {e | a<<30, 4 x u8 block offsets, Dirichlet mask, 0}
+    std::vector<int4> irec(size_t(8) * size_t(ne));
     std::vector<int> fill(iptr.begin(), iptr.end() - 1);
-    std::vector<uint8_t> edm(static_cast<size_t>(ne));
     for (long e = 0; e < ne; ++e) {
-        uint8_t m = 0;
+        int m = 0;
         for (int b = 0; b < 4; ++b)
-            m |= uint8_t((c->dir_h[size_t(d->conn[4 * e + b])] ? 1 : 0) << b);
-        edm[size_t(e)] = m;
+            m |= (c->dir_h[size_t(d->conn[4 * e + b])] ? 1 : 0) << b;
         for (int a = 0; a < 4; ++a) {
             const int A = d->conn[4 * e + a];
             const int* r0 = c->col_idx_h.data() + c->row_ptr_h[size_t(A)];
@@ -317,21 +317,21 @@ static int upload_all(hbgpu_ctx* c, const hbgpu_mesh_desc* d) {
                 cols |= uint32_t(off) << (8 * b);
             }
             const int slot = fill[size_t(A)]++;
-            ielem[size_t(slot)] = uint32_t(e) | (uint32_t(a) << 30);
-            icols[size_t(slot)] = cols;
+            irec[2 * size_t(slot)] = make_int4(d->conn[4 * e], d->conn[4 * e + 1],
+                                               d->conn[4 * e + 2], d->conn[4 * e + 3]);
+            irec[2 * size_t(slot) + 1] =
+                make_int4(int(uint32_t(e) | (uint32_t(a) << 30)), int(cols), m, 0);
         }
     }
     CK(c, c->inc_ptr.alloc(size_t(nn) + 1));
-    CK(c, c->inc_elem.alloc(ielem.size()));
-    CK(c, c->inc_cols.alloc(icols.size()));
-    CK(c, c->edmask.alloc(size_t(ne)));
+    CK(c, c->inc_rec.alloc(irec.size()));
     CK(c, cudaMemcpyAsync(c->inc_ptr.p, iptr.data(), sizeof(int) * iptr.size(),
                           cudaMemcpyHostToDevice, st));
-    CK(c, cudaMemcpyAsync(c->inc_elem.p, ielem.data(), sizeof(uint32_t) * ielem.size(),
+    CK(c, cudaMemcpyAsync(c->inc_rec.p, irec.data(), sizeof(int4) * irec.size(),
                           cudaMemcpyHostToDevice, st));
-    CK(c, cudaMemcpyAsync(c->inc_cols.p, icols.data(), sizeof(uint32_t) * icols.size(),
-                          cudaMemcpyHostToDevice, st));
-    CK(c, cudaMemcpyAsync(c->edmask.p, edm.data(), edm.size(), cudaMemcpyHostToDevice, st));
+    CK(c, c->tgeom.alloc(size_t(ne) * kTGeo));
+    launch_tangent_geometry(c->geom.p, ne, c->tgeom.p, st);
+    TRY(check_launch(c));
 
     // element chunks of kChunkElems consecutive elements: distinct nodes,
     // chunk-local connectivity, per (chunk, node) slot lists in element order,
@@ -409,33 +409,30 @@ static int upload_all(hbgpu_ctx* c, const hbgpu_mesh_desc* d) {
 static int plan_tangent(hbgpu_ctx* c) {
     const int N = c->N;
     const size_t row_bytes_per_blk = sizeof(double) * 8 * size_t(N);
-    const size_t budget = 100 * 1024;
+    const size_t budget = 112 * 1024;  // two CTAs per SM
     const int max_rows = std::max(1, 256 / N);
     c->tcta_h.clear();
     c->tcta_h.push_back(0);
+    // fixed rows per CTA (every thread busy); the largest CTA sets the smem size
+    int rows = std::max(1, std::min(max_rows, 128 / N));
     size_t maxsmem = 0;
-    int used_rows = 1;
-    int A = 0;
-    while (A < c->nn) {
-        int B = A;
-        size_t bytes = 0;
-        while (B < c->nn && B - A < max_rows) {
-            const size_t rb = size_t(c->row_ptr_h[size_t(B) + 1] - c->row_ptr_h[size_t(B)]) *
-                              row_bytes_per_blk;
-            if (B > A && bytes + rb > budget)
-                break;
-            bytes += rb;
-            ++B;
+    for (;;) {
+        maxsmem = 0;
+        c->tcta_h.assign(1, 0);
+        for (int A = 0; A < c->nn; A += rows) {
+            const int B = std::min(c->nn, A + rows);
+            maxsmem = std::max(maxsmem, size_t(c->row_ptr_h[size_t(B)] - c->row_ptr_h[size_t(A)]) *
+                                            row_bytes_per_blk);
+            c->tcta_h.push_back(B);
         }
-        maxsmem = std::max(maxsmem, bytes);
-        used_rows = std::max(used_rows, B - A);
-        c->tcta_h.push_back(B);
-        A = B;
+        if (maxsmem <= budget || rows == 1)
+            break;
+        rows -= 1;
     }
     if (maxsmem > 227 * 1024)
         return fail(c, HBGPU_ERR_INVALID, "a block row exceeds the shared-memory budget");
     c->tsmem = maxsmem;
-    c->tthreads = ((used_rows * N + 31) / 32) * 32;
+    c->tthreads = ((rows * N + 31) / 32) * 32;
     CK(c, c->tcta.alloc(c->tcta_h.size()));
     CK(c, cudaMemcpyAsync(c->tcta.p, c->tcta_h.data(), sizeof(int) * c->tcta_h.size(),
                           cudaMemcpyHostToDevice, c->stream));
@@ -513,15 +510,12 @@ static int tangent_dev(hbgpu_ctx* c, const double* d_state) {
     if (c->backflow_tangent)
         return fail(c, HBGPU_ERR_INVALID, "backflow_in_tangent is not supported on the GPU path yet");
     TangentArgs a;
-    a.conn = c->conn.p;
-    a.geom = c->geom.p;
+    a.tgeom = c->tgeom.p;
     a.state = d_state;
-    a.edmask = c->edmask.p;
     a.dir = c->dir.p;
     a.row_ptr = c->row_ptr.p;
     a.inc_ptr = c->inc_ptr.p;
-    a.inc_elem = c->inc_elem.p;
-    a.inc_cols = c->inc_cols.p;
+    a.inc_rec = c->inc_rec.p;
     a.cta_rows = c->tcta.p;
     a.pvals = c->pvals.p;
     a.N = c->N;
@@ -542,8 +536,8 @@ static int tangent_dev(hbgpu_ctx* c, const double* d_state) {
 
 static int mass_dev(hbgpu_ctx* c) {
     const long p0 = prof_mark(c);
-    launch_mass_rows(c->conn.p, c->geom.p, c->row_ptr.p, c->inc_ptr.p, c->inc_elem.p,
-                     c->inc_cols.p, c->rho, c->mass.p, c->nn, c->stream);
+    launch_mass_rows(c->geom.p, c->row_ptr.p, c->inc_ptr.p, c->inc_rec.p, c->rho, c->mass.p,
+                     c->nn, c->stream);
     prof_pair(c, kPhMass, p0, prof_mark(c));
     c->mass_valid = true;
     return check_launch(c);
@@ -860,9 +854,8 @@ void hbgpu_destroy(hbgpu_ctx* c) {
         b->release();
     c->conn.release();
     c->dir.release();
-    c->edmask.release();
-    c->inc_elem.release();
-    c->inc_cols.release();
+    c->inc_rec.release();
+    c->tgeom.release();
     c->lconn.release();
     c->slot_idx.release();
     for (cudaEvent_t e : c->ev_pool)

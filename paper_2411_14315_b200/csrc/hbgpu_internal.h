@@ -20,6 +20,8 @@ constexpr int kRedThreads = 256;
 // Residual element chunks: elements per chunk and time samples per CTA.
 constexpr int kChunkElems = 64;
 constexpr int kResTile = 4;
+// Compact tangent geometry record (gradN 12, V, symmetric xi 6, xi:xi).
+constexpr int kTGeo = 20;
 
 // Number of kernel launches issued by this library (bench.py's gpu_launches).
 extern std::atomic<long long> g_launches;
@@ -48,15 +50,12 @@ struct ResidualChunkArgs {
 };
 
 struct TangentArgs {
-    const int4* conn;
-    const double* geom;
+    const double* tgeom;     // kTGeo doubles / element (compact tangent geometry)
     const double* state;
-    const uint8_t* edmask;   // per element: bit b = node b Dirichlet
     const uint8_t* dir;      // per node
     const int* row_ptr;
-    const int* inc_ptr;      // per node, into inc_elem / inc_cols
-    const uint32_t* inc_elem;  // e | a<<30
-    const uint32_t* inc_cols;  // 4 x uint8 block offset within the row
+    const int* inc_ptr;      // per node, into inc_rec
+    const int4* inc_rec;     // 2 per incidence: conn[4]; {e | a<<30, cols(4 x u8), dirichlet mask, 0}
     const int* cta_rows;     // row range per CTA
     double* pvals;
     int N;
@@ -113,9 +112,9 @@ void launch_boundary(const BoundaryArgs& a, cudaStream_t st);
 cudaError_t configure_tangent_smem(size_t bytes);
 void launch_tangent_rows(const TangentArgs& a, int nctas, int threads, size_t smem,
                          cudaStream_t st);
-void launch_mass_rows(const int4* conn, const double* geom, const int* row_ptr,
-                      const int* inc_ptr, const uint32_t* inc_elem, const uint32_t* inc_cols,
+void launch_mass_rows(const double* geom, const int* row_ptr, const int* inc_ptr, const int4* rec,
                       double rho, double* mass, int nn, cudaStream_t st);
+void launch_tangent_geometry(const double* geom, int ne, double* tg, cudaStream_t st);
 void launch_matvec(const MatvecArgs& a, cudaStream_t st);
 void launch_jacobi(const double* vals, const int* diag_blk, int nn, int N, double* inv_diag,
                    int* degenerate, cudaStream_t st);

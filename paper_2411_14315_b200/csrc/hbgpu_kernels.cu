@@ -187,14 +187,28 @@ void launch_apply_h_series(const double* H, int N, const double* in, int in_node
 // Cs = sum_q conv_q, TLs = sum_q tl_q, W_ji = sum_q u_q,j tl_q,i.  Algebraically
 // identical to element_residual (assembly.cpp:141-263): N_a(q) = B + (A-B) delta_aq.
 // Slot layout: out[(a*7 + c) * T], c = 0..2 r_m, 3 r_c, 4..6 s.
-__device__ __forceinline__ void element_residual_smem(const double* __restrict__ g,
+// Shared-memory operand read the compiler may not hoist or keep live: the
+// element kernels re-read geometry / nodal operands where they are used
+// instead of pinning ~50 doubles in registers (which forced spills).
+__device__ __forceinline__ double lds(const double* p) {
+    double v;
+    asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"((unsigned)__cvta_generic_to_shared(p)));
+    return v;
+}
+struct SmemRow {
+    const double* p;
+    __device__ __forceinline__ double operator[](int k) const { return lds(p + k); }
+};
+
+__device__ __forceinline__ void element_residual_smem(const double* __restrict__ gsm,
                                                       const double* __restrict__ nd, int ndst,
                                                       const int lc[4], int T, int t,
                                                       double rho, double mu, double nu,
                                                       int tau_mode, int* flag,
                                                       double* __restrict__ out) {
     // nd: node data [ln][c][t], c = u0 u1 u2 p hu0 hu1 hu2, node stride ndst
-    auto U = [&](int b, int c) { return nd[lc[b] * ndst + c * T + t]; };
+    const SmemRow g{gsm};
+    auto U = [&](int b, int c) { return lds(nd + lc[b] * ndst + c * T + t); };
     const double V = g[12], w = 0.25 * V;
     double gu[3][3], gp[3], usum[3], hsum[3], psum = 0.0;
 #pragma unroll
@@ -531,178 +545,6 @@ void launch_boundary(const BoundaryArgs& a, cudaStream_t st) {
     const long threads = (long)a.nbnodes * a.N;
     note_launch();
     boundary_kernel<<<(int)((threads + 255) / 256), 256, 0, st>>>(a);
-}
-
-// ---------------------------------------------------------------- tangent
-
-// Row-owned assembly of the pointwise tangent P (assembly.cpp:265-374,
-// 550-666).  A CTA owns a contiguous range of block rows; its shared memory
-// holds exactly the P.vals segment of those rows ([blk][slot][n], the global
-// layout), so the block values are accumulated on chip and written once,
-// coalesced.  Thread (row A, sample n) walks the elements containing A in
-// element order (the reference's summation order per block) and adds that
-// element's contribution to the 4 blocks (A, conn[e][b]).
-//
-// Per element and sample the q-sums factor through 8 scalars:
-//   K_ab = kc_ab + kappa_a . gradN_b,  kappa_a = w rho sum_q (N_a(q) + tau_q adv_a(q)) u_q
-//   G_ab = -dN_a V/4 + alpha_a gradN_b, alpha_a = w sum_q tau_q adv_a(q)
-//   D_ab = dN_b V/4 + dN_a (w z . gradN_b), z = sum_q tau_q u_q
-//   L_ab = gradN_a.gradN_b * (w/rho) sum_q tau_q
-__global__ void __launch_bounds__(256) tangent_rows_kernel(TangentArgs a) {
-    extern __shared__ double sm[];
-    const int N = a.N;
-    const int row_lo = a.cta_rows[blockIdx.x], row_hi = a.cta_rows[blockIdx.x + 1];
-    const long blk_lo = a.row_ptr[row_lo];
-    const long nvals = ((long)a.row_ptr[row_hi] - blk_lo) * 8 * N;
-    for (long k = threadIdx.x; k < nvals; k += blockDim.x)
-        sm[k] = 0.0;
-    __syncthreads();
-
-    const int r = threadIdx.x / N, n = threadIdx.x - r * N;
-    const int A = row_lo + r;
-    if (A < row_hi) {
-        const long rowoff = (long)a.row_ptr[A] - blk_lo;
-        const double rho = a.rho;
-        long diag_local = -1;
-        for (int ii = a.inc_ptr[A]; ii < a.inc_ptr[A + 1]; ++ii) {
-            const uint32_t ie = __ldg(&a.inc_elem[ii]);
-            const int e = (int)(ie & 0x3FFFFFFFu);
-            const int la = (int)(ie >> 30);
-            const uint32_t cols = __ldg(&a.inc_cols[ii]);
-            const int em = a.edmask[e];
-            const int4 c = __ldg(&a.conn[e]);
-            const int nd[4] = {c.x, c.y, c.z, c.w};
-            Geo G;
-            load_geo(a.geom + 22 * (long)e, G);
-            double u[4][3];
-#pragma unroll
-            for (int b = 0; b < 4; ++b) {
-                const double* sb = a.state + (long)nd[b] * 4 * N + n;
-#pragma unroll
-                for (int i = 0; i < 3; ++i)
-                    u[b][i] = ldg(sb + i * N);
-            }
-            const double V = G.V, w = 0.25 * V;
-            double usum[3];
-#pragma unroll
-            for (int i = 0; i < 3; ++i)
-                usum[i] = u[0][i] + u[1][i] + u[2][i] + u[3][i];
-            const double diff = 3.0 * a.nu * a.nu * xi_dd(G);
-            double tau_mean = 0.0;
-            if (a.tau_mode == 1) {
-                const double um[3] = {0.25 * usum[0], 0.25 * usum[1], 0.25 * usum[2]};
-                tau_mean = tau_of(G, um, diff, a.flag);
-            }
-            double ga[3];
-#pragma unroll
-            for (int i = 0; i < 3; ++i)
-                ga[i] = (la == 0) ? G.gN[0][i] : (la == 1) ? G.gN[1][i] : (la == 2) ? G.gN[2][i] : G.gN[3][i];
-            double asum = 0.0, tsum = 0.0, z[3] = {0.0, 0.0, 0.0}, kap[3] = {0.0, 0.0, 0.0};
-            const double dAB = kQA - kQB;
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                double uq[3];
-#pragma unroll
-                for (int i = 0; i < 3; ++i)
-                    uq[i] = kQB * usum[i] + dAB * u[q][i];
-                const double tq = a.tau_mode == 0 ? tau_of(G, uq, diff, a.flag) : tau_mean;
-                const double adv = uq[0] * ga[0] + uq[1] * ga[1] + uq[2] * ga[2];
-                const double tadv = tq * adv;
-                const double na = (q == la) ? kQA : kQB;
-                asum += tadv;
-                tsum += tq;
-#pragma unroll
-                for (int i = 0; i < 3; ++i) {
-                    z[i] += tq * uq[i];
-                    kap[i] += (na + tadv) * uq[i];
-                }
-            }
-            const double alpha_a = w * asum, beta = (w / rho) * tsum, wr = w * rho;
-            const bool afix = (em >> la) & 1;
-#pragma unroll
-            for (int b = 0; b < 4; ++b) {
-                const int j = (cols >> (8 * b)) & 0xFF;
-                double* acc = sm + (rowoff + j) * 8 * N + n;
-                const bool bfix = (em >> b) & 1;
-                const double* gb = G.gN[b];
-                const double gg = ga[0] * gb[0] + ga[1] * gb[1] + ga[2] * gb[2];
-                if (!afix && !bfix) {
-                    const double kc = a.mu * V * gg + a.pseudo_c * (b == la ? V / 10.0 : V / 20.0);
-                    acc[0] += kc + wr * (kap[0] * gb[0] + kap[1] * gb[1] + kap[2] * gb[2]);
-                }
-                if (!afix) {
-#pragma unroll
-                    for (int i = 0; i < 3; ++i)
-                        acc[(1 + i) * N] += -ga[i] * w + alpha_a * gb[i];
-                }
-                if (!bfix) {
-                    const double alpha_b = w * (z[0] * gb[0] + z[1] * gb[1] + z[2] * gb[2]);
-#pragma unroll
-                    for (int i = 0; i < 3; ++i)
-                        acc[(4 + i) * N] += gb[i] * w + ga[i] * alpha_b;
-                }
-                acc[7 * N] += gg * beta;
-                if (b == la)
-                    diag_local = rowoff + j;
-            }
-        }
-        // identity on constrained velocity diagonals (assembly.cpp:659-665)
-        if (a.dir[A] && diag_local >= 0)
-            sm[diag_local * 8 * N + n] = 1.0;
-    }
-    __syncthreads();
-    double* dst = a.pvals + blk_lo * 8 * N;
-    const double2* s2 = reinterpret_cast<const double2*>(sm);
-    double2* d2 = reinterpret_cast<double2*>(dst);
-    for (long k = threadIdx.x; k < nvals / 2; k += blockDim.x)
-        d2[k] = s2[k];
-}
-
-cudaError_t configure_tangent_smem(size_t bytes) {
-    return cudaFuncSetAttribute(tangent_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                int(bytes < 48 * 1024 ? 48 * 1024 : bytes));
-}
-
-void launch_tangent_rows(const TangentArgs& a, int nctas, int threads, size_t smem,
-                         cudaStream_t st) {
-    if (nctas <= 0)
-        return;
-    note_launch();
-    tangent_rows_kernel<<<nctas, threads, smem, st>>>(a);
-}
-
-// assemble_mass (assembly.cpp:668-681), row-owned: each block row sums its
-// elements in element order — the reference's order, hence bit-identical.
-__global__ void mass_rows_kernel(const int4* __restrict__ conn, const double* __restrict__ geom,
-                                 const int* __restrict__ row_ptr, const int* __restrict__ inc_ptr,
-                                 const uint32_t* __restrict__ inc_elem,
-                                 const uint32_t* __restrict__ inc_cols, double rho,
-                                 double* __restrict__ mass, int nn) {
-    const int A = blockIdx.x * blockDim.x + threadIdx.x;
-    if (A >= nn)
-        return;
-    double* m = mass + row_ptr[A];
-    for (int k = row_ptr[A]; k < row_ptr[A + 1]; ++k)
-        mass[k] = 0.0;
-    for (int ii = inc_ptr[A]; ii < inc_ptr[A + 1]; ++ii) {
-        const uint32_t ie = inc_elem[ii];
-        const int e = (int)(ie & 0x3FFFFFFFu), la = (int)(ie >> 30);
-        const uint32_t cols = inc_cols[ii];
-        const double V = geom[22 * (long)e + 12];
-        const double diag = rho * V / 10.0, off = rho * V / 20.0;
-        for (int b = 0; b < 4; ++b)
-            m[(cols >> (8 * b)) & 0xFF] += (b == la) ? diag : off;
-    }
-}
-
-void launch_mass_rows(const int4* conn, const double* geom, const int* row_ptr,
-                      const int* inc_ptr, const uint32_t* inc_elem, const uint32_t* inc_cols,
-                      double rho, double* mass, int nn, cudaStream_t st) {
-    if (nn <= 0)
-        return;
-    note_launch();
-    mass_rows_kernel<<<(nn + 127) / 128, 128, 0, st>>>(conn, geom, row_ptr, inc_ptr, inc_elem,
-                                                       inc_cols, rho, mass, nn);
 }
 
 // ---------------------------------------------------------------- operator

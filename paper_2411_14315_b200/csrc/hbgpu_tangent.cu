@@ -1,0 +1,277 @@
+// Pointwise tangent P and consistent mass, row-owned (sm_100a, FP64).
+//
+// Replaces element_tangent_p + assemble_tangent (reference
+// src/assembly.cpp:265-374, 550-666) and assemble_mass (:668-681).
+#include "hbgpu_internal.h"
+
+namespace hbgpu {
+
+namespace {
+inline void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+}  // namespace
+
+// Compact per-element geometry for the tangent: gradN[4][3], V, symmetric xi
+// (00 01 02 11 12 22), xi:xi  -> 20 doubles, 16-byte aligned records.
+__global__ void tangent_geometry_kernel(const double* __restrict__ geom, int ne,
+                                        double* __restrict__ tg) {
+    const int e = blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= ne)
+        return;
+    const double* g = geom + 22 * (long)e;
+    double* o = tg + kTGeo * (long)e;
+    for (int k = 0; k < 13; ++k)
+        o[k] = g[k];
+    o[13] = g[13];
+    o[14] = g[14];
+    o[15] = g[15];
+    o[16] = g[17];
+    o[17] = g[18];
+    o[18] = g[21];
+    double s = 0.0;
+    for (int k = 0; k < 9; ++k)
+        s += g[13 + k] * g[13 + k];
+    o[19] = s;
+}
+
+void launch_tangent_geometry(const double* geom, int ne, double* tg, cudaStream_t st) {
+    if (ne <= 0)
+        return;
+    note_launch();
+    tangent_geometry_kernel<<<(ne + 255) / 256, 256, 0, st>>>(geom, ne, tg);
+}
+
+namespace {
+
+struct IncData {
+    double g[kTGeo];
+    double u[4][3];
+};
+
+__device__ __forceinline__ void fetch_inc(const TangentArgs& a, const int4 r0, const int4 r1, int n,
+                                          IncData& d) {
+    const int e = r1.x & 0x3FFFFFFF;
+    const double2* g2 = reinterpret_cast<const double2*>(a.tgeom + (long)kTGeo * e);
+#pragma unroll
+    for (int k = 0; k < kTGeo / 2; ++k) {
+        const double2 v = __ldg(g2 + k);
+        d.g[2 * k] = v.x;
+        d.g[2 * k + 1] = v.y;
+    }
+    const int nd[4] = {r0.x, r0.y, r0.z, r0.w};
+    const int N = a.N;
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+        const double* sb = a.state + (long)nd[b] * 4 * N + n;
+#pragma unroll
+        for (int i = 0; i < 3; ++i)
+            d.u[b][i] = __ldg(sb + i * N);
+    }
+}
+
+__device__ __forceinline__ double xi_quad(const double* g, const double u[3]) {
+    // u . xi u with the symmetric xi of the compact record
+    return g[13] * u[0] * u[0] + g[16] * u[1] * u[1] + g[18] * u[2] * u[2] +
+           2.0 * (g[14] * u[0] * u[1] + g[15] * u[0] * u[2] + g[17] * u[1] * u[2]);
+}
+
+}  // namespace
+
+// Row-owned assembly of P.  A CTA owns `rows` consecutive block rows; its
+// shared memory holds exactly their P.vals segment ([blk][slot][n], the
+// global layout), accumulated on chip and written once, coalesced.  Thread
+// (row A, sample n) walks the elements containing A in element order — the
+// reference's summation order per block — and adds each element's
+// contribution to the 4 blocks (A, conn[e][b]).  Incidence records are
+// prefetched two ahead and their geometry / velocities one ahead, so global
+// latency overlaps the FP64 work of the current element.
+//
+// Per element and sample the quadrature sums factor through 8 scalars:
+//   K_ab = kc_ab + kappa_a . gradN_b,  kappa_a = w rho sum_q (N_a(q) + tau_q adv_a(q)) u_q
+//   G_ab = -dN_a V/4 + alpha_a gradN_b, alpha_a = w sum_q tau_q adv_a(q)
+//   D_ab = dN_b V/4 + dN_a (w z . gradN_b), z = sum_q tau_q u_q
+//   L_ab = gradN_a.gradN_b * (w/rho) sum_q tau_q
+// (Picard-frozen tangent of assembly.cpp:265-374; masking of :583-607.)
+template <int TAU>
+__global__ void __launch_bounds__(128) tangent_rows_kernel(TangentArgs a) {
+    extern __shared__ double sm[];
+    const int N = a.N;
+    const int row_lo = a.cta_rows[blockIdx.x], row_hi = a.cta_rows[blockIdx.x + 1];
+    const long blk_lo = a.row_ptr[row_lo];
+    const long nvals = ((long)a.row_ptr[row_hi] - blk_lo) * 8 * N;
+    for (long k = threadIdx.x; k < nvals; k += blockDim.x)
+        sm[k] = 0.0;
+    __syncthreads();
+
+    const int r = threadIdx.x / N, n = threadIdx.x - r * N;
+    const int A = row_lo + r;
+    if (A < row_hi) {
+        const long rowoff = (long)a.row_ptr[A] - blk_lo;
+        const double rho = a.rho, diffc = 3.0 * a.nu * a.nu;
+        const int i0 = a.inc_ptr[A], i1 = a.inc_ptr[A + 1];
+        const int4* rec = a.inc_rec;
+        int4 c0 = make_int4(0, 0, 0, 0), c1 = c0, n0 = c0, n1 = c0;
+        IncData cur, nxt;
+        if (i0 < i1) {
+            c0 = __ldg(rec + 2 * i0);
+            c1 = __ldg(rec + 2 * i0 + 1);
+            if (i0 + 1 < i1) {
+                n0 = __ldg(rec + 2 * i0 + 2);
+                n1 = __ldg(rec + 2 * i0 + 3);
+            }
+            fetch_inc(a, c0, c1, n, cur);
+        }
+        long diag_local = -1;
+        for (int ii = i0; ii < i1; ++ii) {
+            int4 m0 = make_int4(0, 0, 0, 0), m1 = m0;
+            if (ii + 2 < i1) {
+                m0 = __ldg(rec + 2 * ii + 4);
+                m1 = __ldg(rec + 2 * ii + 5);
+            }
+            if (ii + 1 < i1)
+                fetch_inc(a, n0, n1, n, nxt);
+
+            const int la = (unsigned)c1.x >> 30;
+            const unsigned cols = (unsigned)c1.y;
+            const int em = c1.z;
+            const double* g = cur.g;
+            const double V = g[12], w = 0.25 * V;
+            double usum[3];
+#pragma unroll
+            for (int i = 0; i < 3; ++i)
+                usum[i] = cur.u[0][i] + cur.u[1][i] + cur.u[2][i] + cur.u[3][i];
+            const double diff = diffc * g[19];
+            double tau_mean = 0.0;
+            if (TAU == 1) {
+                const double um[3] = {0.25 * usum[0], 0.25 * usum[1], 0.25 * usum[2]};
+                const double arg = xi_quad(g, um) + diff;
+                if (!(arg > 0.0))
+                    atomicOr(a.flag, 1);
+                tau_mean = arg > 0.0 ? rsqrt(arg) : 0.0;
+            }
+            double ga[3];
+#pragma unroll
+            for (int i = 0; i < 3; ++i)
+                ga[i] = la == 0 ? g[i] : la == 1 ? g[3 + i] : la == 2 ? g[6 + i] : g[9 + i];
+            double asum = 0.0, tsum = 0.0, z[3] = {0.0, 0.0, 0.0}, kap[3] = {0.0, 0.0, 0.0};
+            const double dAB = kQA - kQB;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                double uq[3];
+#pragma unroll
+                for (int i = 0; i < 3; ++i)
+                    uq[i] = kQB * usum[i] + dAB * cur.u[q][i];
+                double tq = tau_mean;
+                if (TAU == 0) {
+                    const double arg = xi_quad(g, uq) + diff;
+                    if (!(arg > 0.0))
+                        atomicOr(a.flag, 1);
+                    tq = arg > 0.0 ? rsqrt(arg) : 0.0;
+                }
+                const double tadv = tq * (uq[0] * ga[0] + uq[1] * ga[1] + uq[2] * ga[2]);
+                const double na = (q == la) ? kQA : kQB;
+                asum += tadv;
+                tsum += tq;
+#pragma unroll
+                for (int i = 0; i < 3; ++i) {
+                    z[i] += tq * uq[i];
+                    kap[i] += (na + tadv) * uq[i];
+                }
+            }
+            const double alpha_a = w * asum, beta = (w / rho) * tsum, wr = w * rho;
+            const bool afix = (em >> la) & 1;
+            const double muV = a.mu * V, pcV = a.pseudo_c * V;
+#pragma unroll
+            for (int b = 0; b < 4; ++b) {
+                const int j = (cols >> (8 * b)) & 0xFF;
+                double* acc = sm + (rowoff + j) * 8 * N + n;
+                const bool bfix = (em >> b) & 1;
+                const double* gb = g + 3 * b;
+                const double gg = ga[0] * gb[0] + ga[1] * gb[1] + ga[2] * gb[2];
+                if (!afix && !bfix) {
+                    const double kc = muV * gg + pcV * (b == la ? 0.1 : 0.05);
+                    acc[0] += kc + wr * (kap[0] * gb[0] + kap[1] * gb[1] + kap[2] * gb[2]);
+                }
+                if (!afix) {
+#pragma unroll
+                    for (int i = 0; i < 3; ++i)
+                        acc[(1 + i) * N] += -ga[i] * w + alpha_a * gb[i];
+                }
+                if (!bfix) {
+                    const double alpha_b = w * (z[0] * gb[0] + z[1] * gb[1] + z[2] * gb[2]);
+#pragma unroll
+                    for (int i = 0; i < 3; ++i)
+                        acc[(4 + i) * N] += gb[i] * w + ga[i] * alpha_b;
+                }
+                acc[7 * N] += gg * beta;
+                if (b == la)
+                    diag_local = rowoff + j;
+            }
+            c0 = n0;
+            c1 = n1;
+            n0 = m0;
+            n1 = m1;
+            cur = nxt;
+        }
+        // identity on constrained velocity diagonals (assembly.cpp:659-665)
+        if (a.dir[A] && diag_local >= 0)
+            sm[diag_local * 8 * N + n] = 1.0;
+    }
+    __syncthreads();
+    const double2* s2 = reinterpret_cast<const double2*>(sm);
+    double2* d2 = reinterpret_cast<double2*>(a.pvals + blk_lo * 8 * N);
+    for (long k = threadIdx.x; k < nvals / 2; k += blockDim.x)
+        d2[k] = s2[k];
+}
+
+cudaError_t configure_tangent_smem(size_t bytes) {
+    const int b = int(bytes < 48 * 1024 ? 48 * 1024 : bytes);
+    cudaError_t e = cudaFuncSetAttribute(tangent_rows_kernel<0>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, b);
+    if (e != cudaSuccess)
+        return e;
+    return cudaFuncSetAttribute(tangent_rows_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                b);
+}
+
+void launch_tangent_rows(const TangentArgs& a, int nctas, int threads, size_t smem,
+                         cudaStream_t st) {
+    if (nctas <= 0)
+        return;
+    note_launch();
+    if (a.tau_mode == 1)
+        tangent_rows_kernel<1><<<nctas, threads, smem, st>>>(a);
+    else
+        tangent_rows_kernel<0><<<nctas, threads, smem, st>>>(a);
+}
+
+// assemble_mass (assembly.cpp:668-681), row-owned: each block row sums its
+// elements in element order — the reference's order, hence bit-identical.
+__global__ void mass_rows_kernel(const double* __restrict__ geom, const int* __restrict__ row_ptr,
+                                 const int* __restrict__ inc_ptr, const int4* __restrict__ rec,
+                                 double rho, double* __restrict__ mass, int nn) {
+    const int A = blockIdx.x * blockDim.x + threadIdx.x;
+    if (A >= nn)
+        return;
+    double* m = mass + row_ptr[A];
+    for (int k = row_ptr[A]; k < row_ptr[A + 1]; ++k)
+        mass[k] = 0.0;
+    for (int ii = inc_ptr[A]; ii < inc_ptr[A + 1]; ++ii) {
+        const int4 r1 = rec[2 * ii + 1];
+        const int e = r1.x & 0x3FFFFFFF, la = (unsigned)r1.x >> 30;
+        const unsigned cols = (unsigned)r1.y;
+        const double V = geom[22 * (long)e + 12];
+        const double diag = rho * V / 10.0, off = rho * V / 20.0;
+        for (int b = 0; b < 4; ++b)
+            m[(cols >> (8 * b)) & 0xFF] += (b == la) ? diag : off;
+    }
+}
+
+void launch_mass_rows(const double* geom, const int* row_ptr, const int* inc_ptr, const int4* rec,
+                      double rho, double* mass, int nn, cudaStream_t st) {
+    if (nn <= 0)
+        return;
+    note_launch();
+    mass_rows_kernel<<<(nn + 127) / 128, 128, 0, st>>>(geom, row_ptr, inc_ptr, rec, rho, mass, nn);
+}
+
+}  // namespace hbgpu
