@@ -93,6 +93,24 @@ class ClockSampler:
                 "reasons": names, "samples": len(self.samples)}
 
 
+def max_over_ranks(value, dist, device):
+    """Device-timed value of this rank -> max over all ranks (replicas)."""
+    if dist is None:
+        return float(value)
+    import torch
+
+    t = torch.tensor([float(value)], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def replica_throughput(world, units_per_replica_step, ms_per_step):
+    """Whole-job throughput of `world` independent replicas (weak scaling):
+    every rank processes its own copy of the workload per step; the step time
+    is the slowest rank's."""
+    return world * units_per_replica_step / (ms_per_step * 1e-3)
+
+
 def spmv_bytes(nnz, nn, N):
     """Compulsory bytes of one L-matvec: P.vals, mass, col_idx,
     row_ptr, y in, out, Dirichlet mask."""
@@ -271,12 +289,9 @@ def run_ours(args):
     ph_n = np.zeros(9, np.int32)
     L.hbgpu_profile_read(ctx.handle, 9, ph_ms.ctypes.data, ph_n.ctypes.data)
     L.hbgpu_profile_enable(ctx.handle, 0)
-    if dist:
-        t = torch.tensor([total_ms], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms = float(t.item())
+    total_ms = max_over_ranks(total_ms, dist, "cuda")
     ms_per_step = total_ms / args.steps
-    value = world * ne * M / (ms_per_step * 1e-3)
+    value = replica_throughput(world, ne * M, ms_per_step)
 
     # ---- per-kernel rooflines (device time from events on the launching stream)
     peak = np.zeros(1)

@@ -84,6 +84,35 @@ def test_small_tube_all_ops(gpu, modes, tau, pdt):
         assert rel(ctx.matvec(y), ref.matvec(y)) < TOL
 
 
+@pytest.mark.parametrize("name", ["tube_m3_qp", "tube_m4_mean", "tube_m1_steady", "bifurcation_m3"])
+def test_against_golden_fixtures(gpu, name):
+    """GPU path vs the committed outputs of the compiled reference."""
+    from goldens import load
+    from paper_2411_14315_b200.hbgpu import GpuContext, KrylovConfig
+
+    prob, d = load(name)
+    # geometry passed as the reference's ElementGeometry array (zero-copy drop-in)
+    ctx = GpuContext(prob.mesh, geometry=d["geometry"])
+    ctx.set_basis(prob.modes, prob.period)
+    ctx.set_fluid(prob.rho, prob.mu)
+    ctx.set_bcs(prob.dirichlet_g, prob.neumann, prob.backflow_beta)
+    ctx.set_assembly_config(int(d["tau_mode"]), d["pseudo_dt_eff"])
+    rp, ci = ctx.pattern()
+    assert np.array_equal(rp, d["row_ptr"]) and np.array_equal(ci, d["col_idx"])
+    assert rel(ctx.assemble_residual(d["state"]), d["residual"]) < TOL
+    assert rel(ctx.assemble_tangent(d["state"]), d["pvals"]) < TOL
+    assert rel(ctx.assemble_mass(), d["mass"]) < 1e-15
+    assert rel(ctx.matvec(d["y"]), d["matvec"]) < TOL
+    ctx.set_pvals(d["pvals"])
+    inv, deg = ctx.jacobi()
+    assert deg == int(d["degenerate"]) and rel(inv, d["inv_diag"]) < 1e-15
+    res = ctx.gmres(d["matvec"], KrylovConfig(restart=40, max_iters=400, tolerance=1e-9))
+    assert res.relative_residual <= 1e-9 or res.status == 1
+    assert abs(res.iterations - int(d["gmres_iters"])) <= max(3, 0.05 * int(d["gmres_iters"]))
+    if float(d["gmres_relres"]) <= 1e-9:  # both converged: solutions agree to ~kappa * tol
+        assert rel(res.x, d["gmres_x"]) < 1e-6
+
+
 def test_pattern_bit_exact(gpu):
     from paper_2411_14315_b200 import meshgen
 
@@ -166,6 +195,65 @@ def test_gmres_identity_zero_and_stagnation(gpu):
     res = ctx.gmres(b, KrylovConfig(tolerance=1e-10, restart=80, max_iters=800))
     assert res.status == 0
     assert rel(orc.matvec(vals.reshape(-1), m, res.x), b) < 1e-9
+
+
+def _modes(state, nn, N, comps):
+    """PeriodicSignal::coefficients (spectral.cpp:35-50): c_m = (1/N) sum_n v_n e^{-2 pi i m n/N}."""
+    v = state.reshape(nn, 4, N)[:, comps, :]
+    return np.fft.fft(v, axis=-1) / N
+
+
+@pytest.mark.skipif(not HAVE_REF, reason="compiled reference absent")
+def test_converged_solve_matches_reference(gpu):
+    """Converged periodic velocity / pressure within 1e-8 relative L2, in time
+    samples and in Fourier modes, with tight tolerances on both sides
+    (Newton 10 orders, GMRES 1e-10, CFL 3)."""
+    from paper_2411_14315_b200.hbgpu import GpuContext, KrylovConfig, SolverConfig
+
+    rm = ob.RefMesh.tube(0.3, 1.5, 0.15)
+    mesh = rm.to_mesh()
+    M, N = 3, 5
+    q = cases.flow_samples(2.0, [0.2, -0.1], [0.1, 0.05], M, 1.0)
+    g = cases.parabolic_dirichlet(mesh, mesh.patch_index("inlet"), q)
+    neu = [(k, np.full(N, -100.0)) for k, p in enumerate(mesh.patches) if p.kind == NEUMANN]
+    prob = Problem(mesh, M, 1.0, 1.06, 0.04, g, neu, 0.2)
+    rc = ob.ref_context(prob)
+    dt = 3.0 * rc.suggest_pseudo_dt()
+    ref = rc.solve(pseudo_dt=dt, orders=10, max_newton=300, restart=200, max_iters=5000, tol=1e-10)
+    assert ref["converged"]
+    ctx = GpuContext(mesh)
+    ctx.set_basis(M, 1.0)
+    ctx.set_fluid(1.06, 0.04)
+    ctx.set_bcs(g, neu, 0.2)
+    sol = ctx.solve_harmonic(SolverConfig(pseudo_dt=dt, newton_tol_orders=10, max_newton_iters=300,
+                                          krylov=KrylovConfig(200, 5000, 1e-10)))
+    assert sol.log.converged
+    assert abs(sol.cfl - ref["cfl"]) < 1e-12 * ref["cfl"]
+    nn = mesh.num_nodes
+    su, sr = sol.state.reshape(nn, 4, N), ref["state"].reshape(nn, 4, N)
+    assert rel(su[:, :3], sr[:, :3]) < 1e-8
+    assert rel(su[:, 3], sr[:, 3]) < 1e-8
+    assert rel(_modes(sol.state, nn, N, slice(0, 3)), _modes(ref["state"], nn, N, slice(0, 3))) < 1e-8
+    assert rel(_modes(sol.state, nn, N, 3), _modes(ref["state"], nn, N, 3)) < 1e-8
+    # same Newton trajectory length within a couple of iterations
+    assert abs(len(sol.log.iters) - len(ref["res"])) <= 3
+
+
+def test_solver_is_deterministic(gpu):
+    """Bit-identical convergence history and state across runs (test_hb_solver.cpp:124-141)."""
+    from paper_2411_14315_b200.hbgpu import GpuContext, SolverConfig
+
+    prob = cases.config_problem(0)
+    runs = []
+    for _ in range(2):
+        ctx = GpuContext(prob.mesh)
+        ctx.set_basis(prob.modes, prob.period)
+        ctx.set_fluid(prob.rho, prob.mu)
+        ctx.set_bcs(prob.dirichlet_g, prob.neumann, prob.backflow_beta)
+        runs.append(ctx.solve_harmonic(SolverConfig(max_newton_iters=5)))
+    assert np.array_equal(runs[0].state, runs[1].state)
+    assert np.array_equal(runs[0].log.res, runs[1].log.res)
+    assert np.array_equal(runs[0].log.linear_iters, runs[1].log.linear_iters)
 
 
 @pytest.mark.parametrize("modes", [1, 3])

@@ -1,0 +1,103 @@
+"""Pin the plain-C restatement (oracle/hbgls_oracle.c) against the golden
+fixtures produced by the compiled reference, and — where the reference
+library is present — against the reference directly on fresh inputs.
+CPU only."""
+import os
+
+import numpy as np
+import pytest
+
+from oracle import bindings as ob
+from paper_2411_14315_b200 import cases
+
+from goldens import NAMES, load
+
+HAVE_REF = os.path.exists(ob.REF_SO)
+
+
+def rel(a, b):
+    nb = np.linalg.norm(b)
+    return float(np.linalg.norm(np.asarray(a) - np.asarray(b)) / (nb if nb > 0 else 1.0))
+
+
+@pytest.mark.parametrize("name", NAMES)
+def test_restatement_matches_golden(name):
+    prob, d = load(name)
+    orc = ob.Restated(prob, tau_mode=int(d["tau_mode"]), pseudo_dt=d["pseudo_dt_eff"])
+    # pattern and geometry: bit-exact (linalg.cpp:10-30, mesh.cpp:159-203)
+    assert np.array_equal(orc.row_ptr, d["row_ptr"]) and np.array_equal(orc.col_idx, d["col_idx"])
+    assert np.array_equal(ob.restated_geometry(prob.mesh.xyz, prob.mesh.conn), d["geometry"])
+    s = d["state"]
+    assert rel(orc.residual(s), d["residual"]) < 1e-13
+    assert rel(orc.residual(s), d["oracle_residual"]) < 1e-12  # tests/oracles.cpp straight loops
+    p = orc.tangent(s)
+    assert rel(p, d["pvals"]) < 1e-14
+    m = orc.mass()
+    assert np.array_equal(m, d["mass"])
+    assert rel(orc.matvec(d["pvals"], d["mass"], d["y"]), d["matvec"]) < 1e-13
+    inv, deg = orc.jacobi(d["pvals"])
+    assert deg == int(d["degenerate"]) and np.array_equal(inv, d["inv_diag"])
+    g = orc.gmres(d["pvals"], d["mass"], d["matvec"], d["inv_diag"], restart=40, max_iters=400, tol=1e-9)
+    assert g["iterations"] == int(d["gmres_iters"])
+    assert rel(g["x"], d["gmres_x"]) < 1e-10
+
+
+def test_spectral_h_dense_and_fftw_path():
+    """H = E^-1 Omega E: restated dense formula vs the reference's dense(),
+    its oracle_h_dense, and the FFTW(-shim) apply_many path
+    (test_spectral.cpp:104-151 bound 1e-11 omega |v|)."""
+    from goldens import GOLDEN
+
+    sp = np.load(os.path.join(GOLDEN, "spectral.npz"))
+    for M in (1, 2, 3, 4, 7, 13):
+        N = 2 * M - 1
+        H = ob.restated_h_dense(M, 0.7)
+        assert np.abs(H - sp[f"H_{M}"]).max() <= 1e-12 * max(1.0, np.abs(H).max())
+        assert np.abs(H - sp[f"Hora_{M}"]).max() <= 1e-12 * max(1.0, np.abs(H).max())
+        v = sp[f"v_{M}"].reshape(-1, N)
+        omega = 2 * np.pi / 0.7
+        assert np.abs(v @ H.T - sp[f"Hv_{M}"].reshape(-1, N)).max() <= 1e-11 * omega * np.abs(v).max() * N
+        assert np.allclose(H, -H.T, atol=1e-12 * omega)  # skew, zero diagonal
+        if M == 1:
+            assert np.all(H == 0.0)
+
+
+def test_tangent_is_fd_derivative_of_frozen_residual():
+    """P is the exact derivative of the frozen-coefficient residual
+    (test_assembly.cpp:340-384), checked on the restatement's tangent."""
+    if not HAVE_REF:
+        pytest.skip("needs the compiled reference (oracle_frozen_residual)")
+    rm = ob.RefMesh.tube(0.5, 1.0, 0.34)
+    mesh = rm.to_mesh()
+    M, N = 3, 5
+    prob = cases.Problem(mesh, M, 1.0, 1.06, 0.04, np.zeros(mesh.num_nodes * 3 * N), [], 0.2)
+    ref = ob.ref_context(prob, 0, float("inf"))
+    orc = ob.Restated(prob, tau_mode=0)
+    s0 = cases.random_state(mesh.num_nodes, N, 5)
+    p = orc.tangent(s0)
+    dy = cases.random_state(mesh.num_nodes, N, 6)
+    free = ~mesh.dirichlet.astype(bool)
+    dy.reshape(mesh.num_nodes, 4, N)[~free, :3, :] = 0.0
+    h = 1e-6
+    fd = (ref.frozen_residual(s0 + h * dy, s0) - ref.frozen_residual(s0 - h * dy, s0)) / (2 * h)
+    pd = orc.bsr_matvec(p, dy)
+    mask = np.ones((mesh.num_nodes, 4, N), bool)
+    mask[~free, :3, :] = False
+    mask = mask.reshape(-1)
+    assert rel(pd[mask], fd[mask]) < 1e-8
+
+
+@pytest.mark.skipif(not HAVE_REF, reason="compiled reference absent")
+@pytest.mark.parametrize("modes,tau", [(1, 0), (3, 0), (5, 1)])
+def test_restatement_matches_reference_fresh(modes, tau):
+    prob = cases.config_problem(0, modes=modes)
+    ref = ob.ref_context(prob, tau, 0.02)
+    orc = ob.Restated(prob, tau_mode=tau, pseudo_dt=0.02)
+    s = cases.random_state(prob.mesh.num_nodes, prob.N, 17, 2.0)
+    assert rel(orc.residual(s), ref.residual(s, 4)) < 1e-12
+    p = orc.tangent(s)
+    assert rel(p, ref.tangent(s)) < 1e-14
+    y = cases.random_state(prob.mesh.num_nodes, prob.N, 18)
+    assert rel(orc.matvec(p, orc.mass(), y), ref.matvec(y, 4)) < 1e-13
+    rp, ci = ob.RefMesh.from_mesh(prob.mesh).pattern()
+    assert np.array_equal(rp, orc.row_ptr) and np.array_equal(ci, orc.col_idx)
