@@ -113,7 +113,7 @@ struct hbgpu_ctx {
     int nbnodes = 0;
 
     // work buffers
-    DBuf<double> state, r, hu, pvals, mass, inv, y, out, x, w, scale, b, tmp;
+    DBuf<double> state, r, hu, pvals, mass, mass_c, inv, y, out, x, w, scale, b, tmp;
     DBuf<double> V;
     size_t V_vecs = 0;
     DBuf<double> partial, red;
@@ -538,6 +538,8 @@ static int mass_dev(hbgpu_ctx* c) {
     const long p0 = prof_mark(c);
     launch_mass_rows(c->geom.p, c->row_ptr.p, c->inc_ptr.p, c->inc_rec.p, c->rho, c->mass.p,
                      c->nn, c->stream);
+    launch_mask_mass(c->mass.p, c->row_ptr.p, c->col_idx.p, c->dir.p, c->nn, c->mass_c.p,
+                     c->stream);
     prof_pair(c, kPhMass, p0, prof_mark(c));
     c->mass_valid = true;
     return check_launch(c);
@@ -553,7 +555,7 @@ static int matvec_dev(hbgpu_ctx* c, const double* d_y, double* d_out, const doub
     a.row_ptr = c->row_ptr.p;
     a.col_idx = c->col_idx.p;
     a.vals = c->pvals.p;
-    a.mass = c->mass.p;
+    a.mass = c->mass_c.p;
     a.dir = c->dir.p;
     a.H = c->H.p;
     a.y = d_y;
@@ -564,7 +566,7 @@ static int matvec_dev(hbgpu_ctx* c, const double* d_y, double* d_out, const doub
     a.rows_per_cta = rows_per_matvec_cta(c->N);
     a.with_c = (with_c && c->N > 1) ? 1 : 0;
     const long p0 = prof_mark(c);
-    launch_matvec(a, c->stream);
+    launch_lmatvec(a, c->stream);
     prof_pair(c, kPhMatvec, p0, prof_mark(c));
     return check_launch(c);
 }
@@ -845,7 +847,7 @@ void hbgpu_destroy(hbgpu_ctx* c) {
     if (c->h_int)
         cudaFreeHost(c->h_int);
     for (DBuf<double>* b : {&c->geom, &c->H, &c->g, &c->hN, &c->fnormal, &c->farea, &c->state,
-                            &c->r, &c->hu, &c->pvals, &c->mass, &c->inv, &c->y, &c->out,
+                            &c->r, &c->hu, &c->pvals, &c->mass, &c->mass_c, &c->inv, &c->y, &c->out,
                             &c->x, &c->w, &c->scale, &c->b, &c->tmp, &c->V, &c->partial, &c->red, &c->rpartial})
         b->release();
     for (DBuf<int>* b : {&c->row_ptr, &c->col_idx, &c->diag_blk, &c->inc_ptr, &c->chunk_node_ptr, &c->chunk_nodes, &c->slot_ptr, &c->npart_ptr, &c->npart,
@@ -920,6 +922,7 @@ int hbgpu_set_basis(hbgpu_ctx* c, int modes, double period) {
     }
     CK(c, c->pvals.alloc(size_t(c->nnz) * 8 * size_t(N)));
     CK(c, c->mass.alloc(size_t(c->nnz)));
+    CK(c, c->mass_c.alloc(size_t(c->nnz)));
     CK(c, c->g.alloc(size_t(c->nn) * 3 * size_t(N)));
     CK(c, cudaMemsetAsync(c->g.p, 0, sizeof(double) * size_t(c->nn) * 3 * size_t(N), c->stream));
     c->g_h.assign(size_t(c->nn) * 3 * size_t(N), 0.0);

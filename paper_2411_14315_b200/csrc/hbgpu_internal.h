@@ -23,6 +23,17 @@ constexpr int kResTile = 4;
 // Compact tangent geometry record (gradN 12, V, symmetric xi 6, xi:xi).
 constexpr int kTGeo = 20;
 
+// Build-time tuning knobs of the residual element pass.
+#ifndef RES_VOLATILE_LDS
+#define RES_VOLATILE_LDS 1
+#endif
+#ifndef RES_MINB
+#define RES_MINB 2
+#endif
+#ifndef MV_UNROLL
+#define MV_UNROLL 2
+#endif
+
 // Number of kernel launches issued by this library (bench.py's gpu_launches).
 extern std::atomic<long long> g_launches;
 cudaError_t run_fp64_peak(int blocks, int threads, int iters, double* out, float* ms);
@@ -116,6 +127,9 @@ void launch_mass_rows(const double* geom, const int* row_ptr, const int* inc_ptr
                       double rho, double* mass, int nn, cudaStream_t st);
 void launch_tangent_geometry(const double* geom, int ne, double* tg, cudaStream_t st);
 void launch_matvec(const MatvecArgs& a, cudaStream_t st);
+void launch_lmatvec(const MatvecArgs& a, cudaStream_t st);
+void launch_mask_mass(const double* mass, const int* row_ptr, const int* col_idx,
+                      const uint8_t* dir, int nn, double* mass_c, cudaStream_t st);
 void launch_jacobi(const double* vals, const int* diag_blk, int nn, int N, double* inv_diag,
                    int* degenerate, cudaStream_t st);
 void launch_install_dirichlet(const double* g, const uint8_t* dir, int nn, int N, double* state,

@@ -192,7 +192,11 @@ void launch_apply_h_series(const double* H, int N, const double* in, int in_node
 // instead of pinning ~50 doubles in registers (which forced spills).
 __device__ __forceinline__ double lds(const double* p) {
     double v;
+#if RES_VOLATILE_LDS
     asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"((unsigned)__cvta_generic_to_shared(p)));
+#else
+    v = *p;
+#endif
     return v;
 }
 struct SmemRow {
@@ -350,7 +354,7 @@ __device__ __forceinline__ void residual_issue(const ResidualChunkArgs& a, int i
         cp_async16(geo + 2 * k, gsrc + 2 * k);
 }
 
-__global__ void __launch_bounds__(256, 2) residual_chunk_kernel(ResidualChunkArgs a) {
+__global__ void __launch_bounds__(256, RES_MINB) residual_chunk_kernel(ResidualChunkArgs a) {
     extern __shared__ __align__(16) double sm[];
     const int N = a.N, T = a.T, CE = a.CE;
     const int ntiles = (N + T - 1) / T;

@@ -1,0 +1,160 @@
+// Fused L-matvec (TangentOperator::matvec, reference src/linalg.cpp:78-128):
+//   out_A = sum_k P_k y_col(k) + [A free] H * sum_{k: col free} m_k y_col(k)[velocity]
+// HBM-bound: P.vals (64 N bytes per block) dominates the traffic and is
+// streamed exactly once with evict-first loads; y stays L2/L1 resident.
+#include "hbgpu_internal.h"
+
+namespace hbgpu {
+
+namespace {
+inline void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+__device__ __forceinline__ double ldcs(const double* p) { return __ldcs(p); }
+}  // namespace
+
+// Thread (row, n).  The Dirichlet masks of C are folded into `mass_c`
+// (m_k = 0 when row or column is constrained, linalg.cpp:109,115), so the
+// block loop is branch-free; two blocks per iteration keep 24+ independent
+// loads in flight per thread.  The N threads of a row exchange the gathered
+// velocity series through shared memory for the dense H product.
+template <bool SCALED, bool WITH_C>
+__global__ void __launch_bounds__(256) lmatvec_kernel(MatvecArgs a) {
+    extern __shared__ double sh[];
+    const int N = a.N;
+    double* sH = sh;
+    double* st = sh + (WITH_C ? N * N : 0);
+    if (WITH_C)
+        for (int k = threadIdx.x; k < N * N; k += blockDim.x)
+            sH[k] = a.H[k];
+    const int r = threadIdx.x / N, n = threadIdx.x - r * N;
+    const int A = blockIdx.x * a.rows_per_cta + r;
+    const bool valid = (r < a.rows_per_cta) && (A < a.nn);
+    double ou0 = 0.0, ou1 = 0.0, ou2 = 0.0, op = 0.0, t0 = 0.0, t1 = 0.0, t2 = 0.0;
+    const long N8 = 8L * N;
+    auto block = [&](int k) {
+        const int B = __ldg(&a.col_idx[k]);
+        const double* v = a.vals + (long)k * N8 + n;
+        const long yb = (long)B * 4 * N + n;
+        double y0 = __ldg(a.y + yb), y1 = __ldg(a.y + yb + N), y2 = __ldg(a.y + yb + 2 * N),
+               y3 = __ldg(a.y + yb + 3 * N);
+        if (SCALED) {
+            y0 *= __ldg(a.scale + yb);
+            y1 *= __ldg(a.scale + yb + N);
+            y2 *= __ldg(a.scale + yb + 2 * N);
+            y3 *= __ldg(a.scale + yb + 3 * N);
+        }
+        const double kd = ldcs(v), g0 = ldcs(v + N), g1 = ldcs(v + 2 * N), g2 = ldcs(v + 3 * N);
+        const double d0 = ldcs(v + 4 * N), d1 = ldcs(v + 5 * N), d2 = ldcs(v + 6 * N),
+                     ld = ldcs(v + 7 * N);
+        ou0 += kd * y0 + g0 * y3;
+        ou1 += kd * y1 + g1 * y3;
+        ou2 += kd * y2 + g2 * y3;
+        op += d0 * y0;
+        op += d1 * y1;
+        op += d2 * y2;
+        op += ld * y3;
+        if (WITH_C) {
+            const double m = __ldg(a.mass + k);
+            t0 += m * y0;
+            t1 += m * y1;
+            t2 += m * y2;
+        }
+    };
+    if (valid) {
+        const int kb = a.row_ptr[A], ke = a.row_ptr[A + 1];
+        int k = kb;
+#if MV_UNROLL >= 4
+        for (; k + 3 < ke; k += 4) {
+            block(k);
+            block(k + 1);
+            block(k + 2);
+            block(k + 3);
+        }
+#endif
+        for (; k + 1 < ke; k += 2) {
+            block(k);
+            block(k + 1);
+        }
+        if (k < ke)
+            block(k);
+    }
+    if (WITH_C) {
+        if (valid) {
+            st[(r * 3 + 0) * N + n] = t0;
+            st[(r * 3 + 1) * N + n] = t1;
+            st[(r * 3 + 2) * N + n] = t2;
+        }
+        __syncthreads();
+        if (valid) {
+            const double* h = sH + n * N;
+            const double* s0 = st + (r * 3) * N;
+            double h0 = 0.0, h1 = 0.0, h2 = 0.0;
+            for (int m = 0; m < N; ++m) {
+                const double hm = h[m];
+                h0 += hm * s0[m];
+                h1 += hm * s0[N + m];
+                h2 += hm * s0[2 * N + m];
+            }
+            ou0 += h0;
+            ou1 += h1;
+            ou2 += h2;
+        }
+    }
+    if (valid) {
+        const long o = (long)A * 4 * N + n;
+        if (SCALED) {
+            ou0 *= __ldg(a.scale + o);
+            ou1 *= __ldg(a.scale + o + N);
+            ou2 *= __ldg(a.scale + o + 2 * N);
+            op *= __ldg(a.scale + o + 3 * N);
+        }
+        a.out[o] = ou0;
+        a.out[o + N] = ou1;
+        a.out[o + 2 * N] = ou2;
+        a.out[o + 3 * N] = op;
+    }
+}
+
+void launch_lmatvec(const MatvecArgs& a, cudaStream_t st) {
+    if (a.nn <= 0)
+        return;
+    const int blocks = (a.nn + a.rows_per_cta - 1) / a.rows_per_cta;
+    const int threads = a.rows_per_cta * a.N;
+    const size_t smem =
+        a.with_c ? sizeof(double) * ((size_t)a.N * a.N + 3 * (size_t)a.N * a.rows_per_cta) : 0;
+    note_launch();
+    if (a.with_c) {
+        if (a.scale)
+            lmatvec_kernel<true, true><<<blocks, threads, smem, st>>>(a);
+        else
+            lmatvec_kernel<false, true><<<blocks, threads, smem, st>>>(a);
+    } else {
+        if (a.scale)
+            lmatvec_kernel<true, false><<<blocks, threads, smem, st>>>(a);
+        else
+            lmatvec_kernel<false, false><<<blocks, threads, smem, st>>>(a);
+    }
+}
+
+// mass_c[k] = mass[k] unless the row or the column node is Dirichlet
+// (the C-part masking of linalg.cpp:109,115).
+__global__ void mask_mass_kernel(const double* __restrict__ mass, const int* __restrict__ row_ptr,
+                                 const int* __restrict__ col_idx, const uint8_t* __restrict__ dir,
+                                 int nn, double* __restrict__ mass_c) {
+    const int A = blockIdx.x * blockDim.x + threadIdx.x;
+    if (A >= nn)
+        return;
+    const bool af = dir[A] != 0;
+    for (int k = row_ptr[A]; k < row_ptr[A + 1]; ++k)
+        mass_c[k] = (af || dir[col_idx[k]]) ? 0.0 : mass[k];
+}
+
+void launch_mask_mass(const double* mass, const int* row_ptr, const int* col_idx,
+                      const uint8_t* dir, int nn, double* mass_c, cudaStream_t st) {
+    if (nn <= 0)
+        return;
+    note_launch();
+    mask_mass_kernel<<<(nn + 255) / 256, 256, 0, st>>>(mass, row_ptr, col_idx, dir, nn, mass_c);
+}
+
+}  // namespace hbgpu

@@ -21,7 +21,7 @@ import numpy as np
 from .mesh import GeometryError, Mesh, ParseError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libhbgpu.so")
+LIB_PATH = os.environ.get("HBGPU_LIB") or os.path.join(_HERE, "libhbgpu.so")
 
 
 class StagnationError(RuntimeError):
