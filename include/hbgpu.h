@@ -106,6 +106,8 @@ int hbgpu_assemble_residual(hbgpu_ctx* ctx, const double* state, double* residua
 int hbgpu_assemble_tangent(hbgpu_ctx* ctx, const double* state, double* pvals);
 /* assemble_mass (assembly.hpp:145-146, assembly.cpp:668-681).  Kept on device; mass may be NULL. */
 int hbgpu_assemble_mass(hbgpu_ctx* ctx, double* mass);
+/* Replace the device node-pair mass (TangentOperator::mass, nnz doubles). */
+int hbgpu_set_mass(hbgpu_ctx* ctx, const double* mass);
 /* Replace the device P values (e.g. a P assembled elsewhere), nnz*8*N doubles. */
 int hbgpu_set_pvals(hbgpu_ctx* ctx, const double* pvals);
 /* TangentOperator::matvec (linalg.hpp:75, linalg.cpp:78-128): out = (P + H (x) mass) y. */

@@ -1,0 +1,117 @@
+// adapter_demo — the reference's own case plumbing driving both the reference
+// hot path and the GPU adapter (hbflow::gpu::*) on identical inputs.
+// Test infrastructure: links the compiled reference (oracle/_ref/libhbref.so)
+// for build_case / generate_tube / the CPU functions, and libhbgpu.so.
+// Prints one JSON line; exit code 0 iff every parity bound holds.
+#include "hbflow_gpu.hpp"
+
+#include "hbflow/cases.hpp"
+
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <random>
+
+using namespace hbflow;
+
+static double rel(const std::vector<double>& a, const std::vector<double>& b) {
+    double num = 0.0, den = 0.0;
+    for (size_t k = 0; k < a.size(); ++k) {
+        num += (a[k] - b[k]) * (a[k] - b[k]);
+        den += b[k] * b[k];
+    }
+    return std::sqrt(num / (den > 0 ? den : 1.0));
+}
+
+int main() {
+    CaseDefinition def;
+    def.mesh_kind = "tube";
+    def.tube_radius = 0.3;
+    def.tube_length = 1.5;
+    def.mesh_h = 0.15;
+    def.modes = 3;
+    def.mean_flow = 2.0;
+    def.outlet_pressure_mmhg = 10.0;
+    CaseInputs in = build_case(def);
+    const Mesh& mesh = in.mesh;
+    const auto geoms = precompute_geometry(mesh);
+    SpectralOperators ops(in.basis);
+    const int N = in.basis.time_points;
+
+    HarmonicState state(in.basis, mesh.num_nodes());
+    std::mt19937 rng(7);
+    std::uniform_real_distribution<double> dist(-1.0, 1.0);
+    for (auto& v : state.data)
+        v = dist(rng);
+    AssemblyConfig acfg;
+    acfg.pseudo_dt = 0.05;
+
+    const auto r_ref = assemble_residual(mesh, geoms, state, ops, in.props, in.bcs, acfg, 4);
+    const auto r_gpu = gpu::assemble_residual(mesh, geoms, state, ops, in.props, in.bcs, acfg);
+    const double e_res = rel(r_gpu, r_ref);
+
+    auto pattern = std::make_shared<NodePattern>(NodePattern::build(mesh));
+    TangentOperator L;
+    L.mesh = &mesh;
+    L.ops = &ops;
+    L.pattern = pattern;
+    L.P = BlockSparseMatrix(pattern, N);
+    L.mass = assemble_mass(mesh, geoms, in.props.rho, *pattern);
+    BlockSparseMatrix Pg(pattern, N);
+    assemble_tangent(mesh, geoms, state, in.props, in.bcs, acfg, L.P);
+    gpu::assemble_tangent(mesh, geoms, state, in.props, in.bcs, acfg, Pg);
+    const double e_tan = rel(Pg.vals, L.P.vals);
+    const auto mass_g = gpu::assemble_mass(mesh, geoms, in.props.rho, *pattern);
+    const double e_mass = rel(mass_g, L.mass);
+
+    std::vector<double> y(L.size()), o_ref(L.size()), o_gpu(L.size());
+    for (auto& v : y)
+        v = dist(rng);
+    L.matvec(y, o_ref);
+    gpu::matvec(L, y, o_gpu);
+    const double e_mv = rel(o_gpu, o_ref);
+
+    const auto pc_ref = jacobi_preconditioner(L);
+    const auto pc_gpu = gpu::jacobi_preconditioner(L);
+    const double e_jac = rel(pc_gpu.inv_diag, pc_ref.inv_diag);
+    KrylovConfig kc;
+    kc.tolerance = 1e-8;
+    const auto lin = gpu::gmres_solve(L, r_ref, pc_gpu, kc);
+    std::vector<double> Lx(L.size()), sres(L.size()), sb(L.size());
+    L.matvec(lin.x, Lx);
+    for (size_t k = 0; k < L.size(); ++k) {
+        const double s = std::sqrt(std::abs(pc_ref.inv_diag[k]));
+        sres[k] = s * (r_ref[k] - Lx[k]);
+        sb[k] = s * r_ref[k];
+    }
+    std::vector<double> zero(L.size(), 0.0);
+    const double gmres_scaled = rel(sres, zero) / rel(sb, zero);
+
+    SolverConfig scfg;
+    scfg.newton_tol_orders = 10.0;
+    scfg.max_newton_iters = 300;
+    scfg.krylov.tolerance = 1e-10;
+    scfg.krylov.max_iters = 5000;
+    scfg.pseudo_dt = 3.0 * suggest_pseudo_dt(mesh, in.bcs, in.basis).dt;
+    auto t0 = std::chrono::steady_clock::now();
+    const auto s_ref = solve_harmonic(mesh, geoms, in.basis, in.props, in.bcs, scfg);
+    auto t1 = std::chrono::steady_clock::now();
+    const auto s_gpu = gpu::solve_harmonic(mesh, geoms, in.basis, in.props, in.bcs, scfg);
+    auto t2 = std::chrono::steady_clock::now();
+    const double e_solve = rel(s_gpu.state.data, s_ref.state.data);
+
+    const bool ok = e_res < 1e-12 && e_tan < 1e-12 && e_mass < 1e-15 && e_mv < 1e-12 &&
+                    e_jac < 1e-15 && gmres_scaled <= 1e-8 * 1.0001 && s_ref.log.converged &&
+                    s_gpu.log.converged && e_solve < 1e-8;
+    std::printf(
+        "{\"elements\": %d, \"N\": %d, \"residual\": %.3e, \"tangent\": %.3e, \"mass\": %.3e, "
+        "\"matvec\": %.3e, \"jacobi\": %.3e, \"gmres_scaled_residual\": %.3e, \"gmres_iters\": %d, "
+        "\"solve_state\": %.3e, \"newton_ref\": %zu, \"newton_gpu\": %zu, \"solve_ref_s\": %.3f, "
+        "\"solve_gpu_s\": %.3f, \"ok\": %s}\n",
+        mesh.num_elements(), N, e_res, e_tan, e_mass, e_mv, e_jac, gmres_scaled, lin.iterations,
+        e_solve, s_ref.log.entries.size(), s_gpu.log.entries.size(),
+        std::chrono::duration<double>(t1 - t0).count(),
+        std::chrono::duration<double>(t2 - t1).count(), ok ? "true" : "false");
+    gpu::release(mesh);
+    return ok ? 0 : 1;
+}

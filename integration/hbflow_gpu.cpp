@@ -1,0 +1,291 @@
+// hbflow_gpu.cpp — implementation of the C++ drop-in adapter (see hbflow_gpu.hpp).
+// Compiles against the reference headers (/root/reference/proj/include) and
+// the C ABI of libhbgpu.so; contains no reference code.
+#include "hbflow_gpu.hpp"
+
+#include "hbflow/errors.hpp"
+#include "hbgpu.h"
+
+#include <cmath>
+#include <cstring>
+#include <limits>
+#include <map>
+#include <stdexcept>
+#include <string>
+
+namespace hbflow::gpu {
+
+namespace {
+
+struct Entry {
+    hbgpu_ctx* ctx = nullptr;
+    int modes = 0;
+    double period = 0.0;
+    double rho = -1.0, mu = -1.0;
+    const double* g_ptr = nullptr;
+    size_t g_size = 0;
+    std::vector<int> neu_patch;
+    std::vector<double> neu_h;
+    double beta = -1.0;
+    int tau = -1, backflow = -1;
+    double pseudo_dt = -2.0, c1 = 0.0;
+    const double* p_src = nullptr;     // host P.vals mirrored on the device
+    const double* mass_src = nullptr;  // host mass mirrored on the device
+};
+
+std::map<const Mesh*, Entry>& cache() {
+    static std::map<const Mesh*, Entry> c;
+    return c;
+}
+
+[[noreturn]] void rethrow(int status, const std::string& msg) {
+    switch (status) {
+    case HBGPU_ERR_INVALID: throw std::invalid_argument(msg);
+    case HBGPU_ERR_DOMAIN: throw std::domain_error(msg);
+    case HBGPU_ERR_GEOMETRY: throw GeometryError(msg);
+    case HBGPU_ERR_PARSE: throw ParseError(msg);
+    case HBGPU_ERR_STAGNATION: throw StagnationError(msg);
+    case HBGPU_ERR_DIVERGENCE: throw DivergenceError(msg);
+    case HBGPU_ERR_OOM: throw std::bad_alloc();
+    default: throw std::runtime_error("hbgpu: " + msg);
+    }
+}
+
+void check(hbgpu_ctx* c, int status) {
+    if (status != HBGPU_OK)
+        rethrow(status, hbgpu_last_error(c));
+}
+
+Entry& entry(const Mesh& mesh, const std::vector<ElementGeometry>* geoms) {
+    auto& m = cache();
+    auto it = m.find(&mesh);
+    if (it != m.end())
+        return it->second;
+    static_assert(sizeof(ElementGeometry) == 22 * sizeof(double));
+    static_assert(sizeof(std::array<int, 4>) == 4 * sizeof(int));
+    std::vector<int> kinds, nf, facets;
+    std::vector<double> normals, areas;
+    for (const auto& p : mesh.patches) {
+        kinds.push_back(p.kind == PatchKind::Dirichlet ? 0 : 1);
+        nf.push_back(int(p.facets.size()));
+        for (size_t f = 0; f < p.facets.size(); ++f) {
+            for (int k = 0; k < 3; ++k) {
+                facets.push_back(p.facets[f][size_t(k)]);
+                normals.push_back(p.normals[f][size_t(k)]);
+            }
+            areas.push_back(p.facet_areas[f]);
+        }
+    }
+    hbgpu_mesh_desc d{};
+    d.num_nodes = mesh.num_nodes();
+    d.num_elements = mesh.num_elements();
+    d.xyz = reinterpret_cast<const double*>(mesh.nodes.data());
+    d.conn = reinterpret_cast<const int*>(mesh.elements.data());
+    d.geometry = geoms ? reinterpret_cast<const double*>(geoms->data()) : nullptr;  // zero-copy
+    d.dirichlet = reinterpret_cast<const unsigned char*>(mesh.is_dirichlet_node.data());
+    d.num_patches = int(mesh.patches.size());
+    d.patch_kind = kinds.data();
+    d.patch_num_facets = nf.data();
+    d.facets = facets.data();
+    d.normals = normals.data();
+    d.areas = areas.data();
+    int st = 0;
+    hbgpu_ctx* c = hbgpu_create(&d, &st);
+    if (!c)
+        rethrow(st, hbgpu_create_error());
+    Entry& e = m[&mesh];
+    e.ctx = c;
+    return e;
+}
+
+void set_basis(Entry& e, const SpectralBasis& b) {
+    if (e.modes != b.modes || e.period != b.period) {
+        check(e.ctx, hbgpu_set_basis(e.ctx, b.modes, b.period));
+        e.modes = b.modes;
+        e.period = b.period;
+        e.g_ptr = nullptr;
+        e.neu_patch.clear();
+        e.beta = -1.0;
+        e.p_src = e.mass_src = nullptr;
+    }
+}
+
+void set_physics(Entry& e, const FluidProperties& props, const BoundaryConditionSet& bcs,
+                 const AssemblyConfig* cfg) {
+    if (props.rho != e.rho || props.mu != e.mu) {
+        check(e.ctx, hbgpu_set_fluid(e.ctx, props.rho, props.mu));
+        e.rho = props.rho;
+        e.mu = props.mu;
+        e.mass_src = nullptr;
+    }
+    const int N = 2 * e.modes - 1;
+    std::vector<int> np;
+    std::vector<double> nh;
+    for (const auto& nb : bcs.neumann) {
+        np.push_back(nb.patch_index);
+        nh.insert(nh.end(), nb.h.begin(), nb.h.end());
+        if (int(nb.h.size()) != N)
+            throw std::invalid_argument("Neumann data length does not match the basis");
+    }
+    const double* g = bcs.dirichlet_g.empty() ? nullptr : bcs.dirichlet_g.data();
+    if (g != e.g_ptr || bcs.dirichlet_g.size() != e.g_size || np != e.neu_patch || nh != e.neu_h ||
+        bcs.backflow_beta != e.beta) {
+        check(e.ctx, hbgpu_set_bcs(e.ctx, g, int(np.size()), np.data(), nh.data(), bcs.backflow_beta));
+        e.g_ptr = g;
+        e.g_size = bcs.dirichlet_g.size();
+        e.neu_patch = np;
+        e.neu_h = nh;
+        e.beta = bcs.backflow_beta;
+    }
+    if (cfg) {
+        const int tau = cfg->tau_mode == TauMode::ElementMean ? 1 : 0;
+        const double pdt = std::isfinite(cfg->pseudo_dt) ? cfg->pseudo_dt : 0.0;
+        const int bt = cfg->backflow_in_tangent ? 1 : 0;
+        if (tau != e.tau || pdt != e.pseudo_dt || cfg->pseudo_c1 != e.c1 || bt != e.backflow) {
+            check(e.ctx, hbgpu_set_assembly_config(e.ctx, tau, pdt, cfg->pseudo_c1, bt));
+            e.tau = tau;
+            e.pseudo_dt = pdt;
+            e.c1 = cfg->pseudo_c1;
+            e.backflow = bt;
+        }
+    }
+}
+
+void sync_operator(Entry& e, const TangentOperator& L) {
+    set_basis(e, L.ops->basis());
+    if (L.P.vals.data() != e.p_src) {
+        check(e.ctx, hbgpu_set_pvals(e.ctx, L.P.vals.data()));
+        e.p_src = L.P.vals.data();
+    }
+    if (L.mass.data() != e.mass_src) {
+        check(e.ctx, hbgpu_set_mass(e.ctx, L.mass.data()));
+        e.mass_src = L.mass.data();
+    }
+}
+
+}  // namespace
+
+std::vector<double> assemble_residual(const Mesh& mesh, const std::vector<ElementGeometry>& geoms,
+                                      const HarmonicState& state, const SpectralOperators& ops,
+                                      const FluidProperties& props,
+                                      const BoundaryConditionSet& bcs, const AssemblyConfig& cfg,
+                                      int /*threads: no GPU meaning*/) {
+    Entry& e = entry(mesh, &geoms);
+    set_basis(e, ops.basis());
+    set_physics(e, props, bcs, &cfg);
+    std::vector<double> r(state.data.size());
+    check(e.ctx, hbgpu_assemble_residual(e.ctx, state.data.data(), r.data()));
+    return r;
+}
+
+void assemble_tangent(const Mesh& mesh, const std::vector<ElementGeometry>& geoms,
+                      const HarmonicState& state, const FluidProperties& props,
+                      const BoundaryConditionSet& bcs, const AssemblyConfig& cfg,
+                      BlockSparseMatrix& P) {
+    Entry& e = entry(mesh, &geoms);
+    set_basis(e, state.basis);
+    set_physics(e, props, bcs, &cfg);
+    check(e.ctx, hbgpu_assemble_tangent(e.ctx, state.data.data(), P.vals.data()));
+    e.p_src = P.vals.data();  // the device copy is now current
+}
+
+std::vector<double> assemble_mass(const Mesh& mesh, const std::vector<ElementGeometry>& geoms,
+                                  double rho, const NodePattern& pattern) {
+    Entry& e = entry(mesh, &geoms);
+    if (e.modes == 0)
+        check(e.ctx, hbgpu_set_basis(e.ctx, 1, 1.0)), e.modes = 1, e.period = 1.0;
+    if (rho != e.rho) {
+        check(e.ctx, hbgpu_set_fluid(e.ctx, rho, e.mu > 0 ? e.mu : 1.0));
+        e.rho = rho;
+    }
+    std::vector<double> mass(size_t(pattern.nnz()));
+    check(e.ctx, hbgpu_assemble_mass(e.ctx, mass.data()));
+    return mass;
+}
+
+void matvec(const TangentOperator& L, std::span<const double> y, std::span<double> out) {
+    if (y.size() != L.size() || out.size() != L.size())
+        throw std::invalid_argument("tangent matvec: vector size mismatch");
+    Entry& e = entry(*L.mesh, nullptr);
+    sync_operator(e, L);
+    check(e.ctx, hbgpu_matvec(e.ctx, y.data(), out.data()));
+}
+
+JacobiPreconditioner jacobi_preconditioner(const TangentOperator& L) {
+    Entry& e = entry(*L.mesh, nullptr);
+    sync_operator(e, L);
+    JacobiPreconditioner pc;
+    pc.inv_diag.resize(L.size());
+    check(e.ctx, hbgpu_jacobi(e.ctx, pc.inv_diag.data(), &pc.degenerate_entries));
+    return pc;
+}
+
+KrylovResult gmres_solve(const TangentOperator& L, std::span<const double> rhs,
+                         const JacobiPreconditioner& pc, const KrylovConfig& cfg) {
+    Entry& e = entry(*L.mesh, nullptr);
+    sync_operator(e, L);
+    KrylovResult res;
+    res.x.resize(rhs.size());
+    res.history.resize(size_t(cfg.max_iters) + 2);
+    hbgpu_krylov_cfg kc{cfg.restart, cfg.max_iters, cfg.tolerance};
+    hbgpu_krylov_result kr{};
+    check(e.ctx, hbgpu_gmres(e.ctx, rhs.data(), pc.inv_diag.data(), &kc, res.x.data(), &kr,
+                             res.history.data(), int(res.history.size())));
+    res.history.resize(size_t(kr.history_len));
+    res.iterations = kr.iterations;
+    res.relative_residual = kr.relative_residual;
+    res.status = kr.status == 0 ? KrylovStatus::Converged
+                 : kr.status == 1 ? KrylovStatus::MaxIterations
+                                  : KrylovStatus::Stagnated;
+    return res;
+}
+
+HbSolution solve_harmonic(const Mesh& mesh, const std::vector<ElementGeometry>& geoms,
+                          const SpectralBasis& basis, const FluidProperties& props,
+                          const BoundaryConditionSet& bcs, const SolverConfig& cfg) {
+    Entry& e = entry(mesh, &geoms);
+    set_basis(e, basis);
+    set_physics(e, props, bcs, nullptr);
+    e.tau = -1;  // the driver sets the assembly config itself
+    hbgpu_solver_cfg sc{};
+    sc.pseudo_dt = cfg.pseudo_dt;
+    sc.newton_tol_orders = cfg.newton_tol_orders;
+    sc.max_newton_iters = cfg.max_newton_iters;
+    sc.krylov = {cfg.krylov.restart, cfg.krylov.max_iters, cfg.krylov.tolerance};
+    sc.tau_mode = cfg.tau_mode == TauMode::ElementMean ? 1 : 0;
+    sc.backflow_in_tangent = cfg.backflow_in_tangent ? 1 : 0;
+    sc.divergence_ratio = cfg.divergence_ratio;
+    const int cap = cfg.max_newton_iters + 2;
+    std::vector<int> it(static_cast<size_t>(cap)), lin(static_cast<size_t>(cap));
+    std::vector<double> res(static_cast<size_t>(cap)), rel(static_cast<size_t>(cap)),
+        sec(static_cast<size_t>(cap));
+    HbSolution sol;
+    sol.state = HarmonicState(basis, mesh.num_nodes());
+    hbgpu_solve_info info{};
+    const int st = hbgpu_solve_harmonic(e.ctx, &sc, sol.state.data.data(), &info, cap, it.data(),
+                                        res.data(), rel.data(), lin.data(), sec.data());
+    for (int k = 0; k < info.entries; ++k)
+        sol.log.entries.push_back({it[size_t(k)], res[size_t(k)], rel[size_t(k)], lin[size_t(k)],
+                                   sec[size_t(k)]});
+    sol.log.converged = info.converged != 0;
+    sol.pseudo_dt = info.pseudo_dt;
+    sol.cfl = info.cfl;
+    sol.assembly_seconds = info.assembly_seconds;
+    sol.linear_seconds = info.linear_seconds;
+    sol.total_seconds = info.total_seconds;
+    if (st == HBGPU_ERR_DIVERGENCE)
+        throw DivergenceError(hbgpu_last_error(e.ctx), sol.log.to_csv());
+    check(e.ctx, st);
+    return sol;
+}
+
+void release(const Mesh& mesh) {
+    auto& m = cache();
+    auto it = m.find(&mesh);
+    if (it != m.end()) {
+        hbgpu_destroy(it->second.ctx);
+        m.erase(it);
+    }
+}
+
+}  // namespace hbflow::gpu

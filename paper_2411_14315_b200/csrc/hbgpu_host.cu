@@ -1100,6 +1100,17 @@ int hbgpu_assemble_mass(hbgpu_ctx* c, double* mass) {
     return HBGPU_OK;
 }
 
+int hbgpu_set_mass(hbgpu_ctx* c, const double* mass) {
+    TRY(ensure_basis(c));
+    CK(c, cudaMemcpyAsync(c->mass.p, mass, sizeof(double) * size_t(c->nnz), cudaMemcpyHostToDevice,
+                          c->stream));
+    launch_mask_mass(c->mass.p, c->row_ptr.p, c->col_idx.p, c->dir.p, c->nn, c->mass_c.p, c->stream);
+    TRY(check_launch(c));
+    CK(c, cudaStreamSynchronize(c->stream));
+    c->mass_valid = true;
+    return HBGPU_OK;
+}
+
 int hbgpu_set_pvals(hbgpu_ctx* c, const double* pvals) {
     TRY(ensure_basis(c));
     CK(c, cudaMemcpyAsync(c->pvals.p, pvals, sizeof(double) * size_t(c->nnz) * 8 * size_t(c->N),

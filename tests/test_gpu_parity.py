@@ -239,6 +239,23 @@ def test_converged_solve_matches_reference(gpu):
     assert abs(len(sol.log.iters) - len(ref["res"])) <= 3
 
 
+def test_cpp_adapter_against_reference(gpu):
+    """The C++ drop-in adapter (integration/hbflow_gpu.cpp, reference
+    signatures) on the reference's own build_case tube, side by side with the
+    reference functions: residual, tangent, mass, matvec, Jacobi, GMRES and a
+    tight converged solve."""
+    import json
+    import subprocess
+
+    exe = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                       "integration", "_build", "adapter_demo")
+    if not os.path.exists(exe):
+        pytest.skip("adapter demo not built (needs /root/reference at build time)")
+    out = subprocess.run([exe], capture_output=True, text=True, timeout=600)
+    line = json.loads(out.stdout.strip().splitlines()[-1])
+    assert out.returncode == 0 and line["ok"], line
+
+
 def test_solver_is_deterministic(gpu):
     """Bit-identical convergence history and state across runs (test_hb_solver.cpp:124-141)."""
     from paper_2411_14315_b200.hbgpu import GpuContext, SolverConfig
