@@ -129,6 +129,7 @@ typedef struct {
     double relative_residual;
     int status;        /* KrylovStatus: 0 Converged, 1 MaxIterations, 2 Stagnated */
     int history_len;   /* entries written to `history` (<= capacity) */
+    int reorthogonalizations; /* Arnoldi steps that needed the second Gram-Schmidt pass */
 } hbgpu_krylov_result;
 
 /* gmres_solve(TangentOperator, rhs, JacobiPreconditioner, cfg)

@@ -113,11 +113,12 @@ struct hbgpu_ctx {
     int nbnodes = 0;
 
     // work buffers
-    DBuf<double> state, r, hu, pvals, mass, mass_c, inv, y, out, x, w, scale, b, tmp;
+    DBuf<double> state, r, hu, pvals, mass, mass_c, inv, y, out, x, w, z, scale, b, tmp;
     DBuf<double> V;
     size_t V_vecs = 0;
     DBuf<double> partial, red;
     double* h_red = nullptr;  // pinned
+    size_t red_cap = 1024;
     DBuf<int> flag, ideg;
     int* h_int = nullptr;  // pinned
 
@@ -506,9 +507,27 @@ static int residual_dev(hbgpu_ctx* c, const double* d_state, double* d_r) {
     return check_launch(c);
 }
 
+static BoundaryArgs boundary_args(hbgpu_ctx* c, const double* d_state, double* d_r) {
+    BoundaryArgs b;
+    b.bnode = c->bnode.p;
+    b.bptr = c->bptr.p;
+    b.binc = c->binc.p;
+    b.fac = c->fac.p;
+    b.fnormal = c->fnormal.p;
+    b.farea = c->farea.p;
+    b.fbc = c->fbc.p;
+    b.h = c->hN.p;
+    b.dir = c->dir.p;
+    b.state = d_state;
+    b.r = d_r;
+    b.nbnodes = c->nbnodes;
+    b.N = c->N;
+    b.rho = c->rho;
+    b.beta = c->beta;
+    return b;
+}
+
 static int tangent_dev(hbgpu_ctx* c, const double* d_state) {
-    if (c->backflow_tangent)
-        return fail(c, HBGPU_ERR_INVALID, "backflow_in_tangent is not supported on the GPU path yet");
     TangentArgs a;
     a.tgeom = c->tgeom.p;
     a.state = d_state;
@@ -528,6 +547,9 @@ static int tangent_dev(hbgpu_ctx* c, const double* d_state) {
     a.flag = c->flag.p;
     const long p0 = prof_mark(c);
     launch_tangent_rows(a, int(c->tcta_h.size()) - 1, c->tthreads, c->tsmem, c->stream);
+    if (c->backflow_tangent && c->nbnodes > 0)
+        launch_backflow_tangent(boundary_args(c, d_state, nullptr), c->row_ptr.p, c->col_idx.p,
+                                c->pvals.p, c->stream);
     prof_pair(c, kPhTangent, p0, prof_mark(c));
     c->p_valid = true;
     c->inv_valid = false;
@@ -546,7 +568,7 @@ static int mass_dev(hbgpu_ctx* c) {
 }
 
 static int matvec_dev(hbgpu_ctx* c, const double* d_y, double* d_out, const double* d_scale,
-                      bool with_c) {
+                      bool with_c, const double* d_scale_out = nullptr) {
     if (!c->p_valid)
         return fail(c, HBGPU_ERR_INVALID, "matvec before assemble_tangent / set_pvals");
     if (with_c && c->N > 1 && !c->mass_valid)
@@ -561,6 +583,7 @@ static int matvec_dev(hbgpu_ctx* c, const double* d_y, double* d_out, const doub
     a.y = d_y;
     a.out = d_out;
     a.scale = d_scale;
+    a.scale_out = d_scale_out ? d_scale_out : d_scale;
     a.nn = c->nn;
     a.N = c->N;
     a.rows_per_cta = rows_per_matvec_cta(c->N);
@@ -605,10 +628,23 @@ static int ensure_basis(hbgpu_ctx* c) {
     return HBGPU_OK;
 }
 
-// gmres_solve (linalg.cpp:167-293): split Jacobi scaling, restarted Arnoldi
-// with classical Gram-Schmidt + one DGKS re-orthogonalisation when the
-// projection removed more than half of the norm, Givens rotations, true
-// residual recompute per cycle, stagnation when a cycle does not decrease it.
+// gmres_solve (linalg.cpp:167-293): split Jacobi scaling, restarted Arnoldi,
+// Givens rotations, true residual recompute per cycle, stagnation when a
+// cycle does not decrease it.  Orthogonalisation: classical Gram-Schmidt with
+// delayed re-orthogonalisation (DCGS2): step j applies the operator to the
+// tentative vector u_j, and ONE pass over V_0..V_{j-1} yields both the
+// re-orthogonalisation coefficients of u_j (a = Q^T u_j) and the projections
+// of w = A u_j (b = Q^T w); a second pass writes q_j = (u_j - Q a)/rho and
+// the projected w.  Two passes over the basis per step instead of the four of
+// CGS2, one host synchronisation, MGS-level orthogonality.  Because A u_j and
+// A q_j differ, column j is derived from the Arnoldi relation A Q_j = Q_{j+1} H_j:
+//   rho = sqrt(<u,u> - |a|^2),  c = [b ; (<u,w> - a.b)/rho],
+//   h_{:,j} = (c - H_j a)/rho,  w' = (w - Q_{j+1} c)/rho,
+// and column j-1 is finalised with the re-orthogonalisation of u_j:
+//   h_{0:j,j-1} += h_{j,j-1} a,  h_{j,j-1} *= rho.
+// Column j-1 is therefore final (Givens, estimate, convergence test) one step
+// after its vector was produced; the reference's iteration count, history and
+// restart semantics are kept per finalised column.
 static int gmres_dev(hbgpu_ctx* c, const double* d_rhs, const double* d_inv,
                      const hbgpu_krylov_cfg* kc, double* d_x, hbgpu_krylov_result* res,
                      double* history, int hcap) {
@@ -619,6 +655,7 @@ static int gmres_dev(hbgpu_ctx* c, const double* d_rhs, const double* d_inv,
     res->relative_residual = 1.0;
     res->status = 0;
     res->history_len = 0;
+    res->reorthogonalizations = 0;
     auto push_hist = [&](double v) {
         if (history && res->history_len < hcap)
             history[res->history_len] = v;
@@ -628,9 +665,22 @@ static int gmres_dev(hbgpu_ctx* c, const double* d_rhs, const double* d_inv,
         CK(c, c->V.alloc((size_t(m) + 1) * size_t(n)));
         c->V_vecs = size_t(m) + 1;
     }
-    if (size_t(m) + 2 > 1024)
-        return fail(c, HBGPU_ERR_INVALID, "restart above 1022 not supported");
+    // scratch: red[0, 2m+4) dot results | [2m+4, 4m+8) update coefficients | [4m+8] |w'|
+    const size_t need = 4 * size_t(m) + 16;
+    if (c->red_cap < need) {
+        CK(c, c->red.alloc(need));
+        CK(c, c->partial.alloc((2 * size_t(m) + 16) * kRedBlocks));
+        if (c->h_red)
+            cudaFreeHost(c->h_red);
+        c->h_red = nullptr;
+        CK(c, cudaMallocHost(reinterpret_cast<void**>(&c->h_red), sizeof(double) * need));
+        c->red_cap = need;
+    }
     double* V = c->V.p;
+    const size_t o_coef = 2 * size_t(m) + 4, o_norm = 4 * size_t(m) + 8;
+    double* d_norm = c->red.p + o_norm;
+    double* d_coef = c->red.p + o_coef;
+    double* h_coef = c->h_red + o_coef;
     launch_sqrt_abs(d_inv, c->scale.p, n, st);
     launch_mul(c->scale.p, d_rhs, c->b.p, n, st);
     CK(c, cudaMemsetAsync(d_x, 0, sizeof(double) * size_t(n), st));
@@ -640,93 +690,134 @@ static int gmres_dev(hbgpu_ctx* c, const double* d_rhs, const double* d_inv,
         res->relative_residual = 0.0;
         return HBGPU_OK;
     }
-    std::vector<double> Hm(static_cast<size_t>((m + 1) * m)), cs(static_cast<size_t>(m)),
-        sn(static_cast<size_t>(m)), gv(static_cast<size_t>(m + 1)), yv(static_cast<size_t>(m));
-
-    auto HH = [&](int i, int j) -> double& { return Hm[size_t(j) * size_t(m + 1) + size_t(i)]; };
+    std::vector<double> Hm(static_cast<size_t>((m + 2) * (m + 1))), R(static_cast<size_t>((m + 2) * (m + 1))),
+        cs(static_cast<size_t>(m + 1)), sn(static_cast<size_t>(m + 1)), gv(static_cast<size_t>(m + 2)),
+        yv(static_cast<size_t>(m + 1)), av(static_cast<size_t>(m + 1));
+    // H: the (unrotated) Hessenberg matrix of the Arnoldi relation;
+    // R: its Givens-rotated copy (columns rotated once final)
+    auto HH = [&](int i, int j) -> double& { return Hm[size_t(j) * size_t(m + 2) + size_t(i)]; };
+    auto RR = [&](int i, int j) -> double& { return R[size_t(j) * size_t(m + 2) + size_t(i)]; };
     double rnorm = bnorm;
-    const double* rsrc = c->b.p;  // current residual vector (scaled)
+    const double* rsrc = c->b.p;
     push_hist(1.0);
     while (res->iterations < kc->max_iters) {
         const double cycle_start = rnorm;
         std::fill(Hm.begin(), Hm.end(), 0.0);
+        std::fill(R.begin(), R.end(), 0.0);
         std::fill(gv.begin(), gv.end(), 0.0);
         gv[0] = rnorm;
         c->h_red[0] = rnorm;
         CK(c, cudaMemcpyAsync(c->red.p, c->h_red, sizeof(double), cudaMemcpyHostToDevice, st));
-        launch_scale_copy(rsrc, c->red.p, 1, V, n, st);
-        int j = 0;
-        for (; j < m && res->iterations < kc->max_iters; ++j) {
-            double* vj = V + size_t(j) * size_t(n);
-            TRY(matvec_dev(c, vj, c->w.p, c->scale.p, true));
-            // h_i = <w, V_i>, i <= j, and <w,w>
-            launch_multidot(V, n, j + 1, c->w.p, n, c->partial.p, st);
-            launch_multidot(c->w.p, 0, 1, c->w.p, n, c->partial.p + size_t(j + 1) * kRedBlocks, st);
-            launch_reduce_partials(c->partial.p, j + 2, c->red.p, 0, st);
-            launch_gemv_sub(V, n, j + 1, c->red.p, c->w.p, n, st);
+        // V_0 = r/|r| (exactly normalised), z = S V_0
+        launch_normalize(rsrc, c->red.p, V, n, st, c->scale.p, c->z.p);
+        int ncols = 0;  // finalised columns of this cycle
+        bool stop = false;
+        for (int j = 0; !stop; ++j) {
+            double* u = V + size_t(j) * size_t(n);
+            // last step of the cycle: only finalise column j-1
+            const bool last = (j == m) || (res->iterations + (j >= 1 ? 1 : 0) >= kc->max_iters);
+            if (!last)
+                TRY(matvec_dev(c, c->z.p, c->w.p, nullptr, true, c->scale.p));  // w = S A S u_j
+            launch_dcgs_dots(V, n, j, u, last ? nullptr : c->w.p, n, c->partial.p, st);
+            const int rows = last ? j + 1 : 2 * j + 3;
+            launch_reduce_partials(c->partial.p, rows, c->red.p, 0, st);
             TRY(check_launch(c));
-            CK(c, cudaMemcpyAsync(c->h_red, c->red.p, sizeof(double) * size_t(j + 2),
+            CK(c, cudaMemcpyAsync(c->h_red, c->red.p, sizeof(double) * size_t(rows),
                                   cudaMemcpyDeviceToHost, st));
+            if (j >= 1)
+                CK(c, cudaMemcpyAsync(c->h_red + o_norm, d_norm, sizeof(double), cudaMemcpyDeviceToHost, st));
             CK(c, cudaStreamSynchronize(st));
-            double proj2 = 0.0;
-            for (int i = 0; i <= j; ++i) {
-                HH(i, j) = c->h_red[i];
-                proj2 += c->h_red[i] * c->h_red[i];
-            }
-            const double w2 = c->h_red[j + 1];
-            if (w2 - proj2 < 0.5 * w2) {
-                // re-orthogonalise once (twice is enough)
-                launch_multidot(V, n, j + 1, c->w.p, n, c->partial.p, st);
-                launch_reduce_partials(c->partial.p, j + 1, c->red.p, 0, st);
-                launch_gemv_sub(V, n, j + 1, c->red.p, c->w.p, n, st);
-                TRY(check_launch(c));
-                CK(c, cudaMemcpyAsync(c->h_red, c->red.p, sizeof(double) * size_t(j + 1),
-                                      cudaMemcpyDeviceToHost, st));
-                CK(c, cudaStreamSynchronize(st));
-                for (int i = 0; i <= j; ++i)
-                    HH(i, j) += c->h_red[i];
-            }
-            double hj1 = 0.0;
-            TRY(dot_dev(c, c->w.p, c->w.p, n, &hj1, true));
-            HH(j + 1, j) = hj1;
-            if (hj1 > 0.0) {
-                c->h_red[0] = hj1;
-                CK(c, cudaMemcpyAsync(c->red.p, c->h_red, sizeof(double), cudaMemcpyHostToDevice, st));
-                launch_scale_copy(c->w.p, c->red.p, 1, V + size_t(j + 1) * size_t(n), n, st);
-            }
+            const double* a = c->h_red;
+            const double uu = last ? c->h_red[j] : c->h_red[2 * j];
+            double aa = 0.0;
             for (int i = 0; i < j; ++i) {
-                const double t = cs[size_t(i)] * HH(i, j) + sn[size_t(i)] * HH(i + 1, j);
-                HH(i + 1, j) = -sn[size_t(i)] * HH(i, j) + cs[size_t(i)] * HH(i + 1, j);
-                HH(i, j) = t;
+                av[size_t(i)] = a[i];
+                aa += a[i] * a[i];
             }
-            const double den = std::hypot(HH(j, j), HH(j + 1, j));
-            cs[size_t(j)] = den == 0.0 ? 1.0 : HH(j, j) / den;
-            sn[size_t(j)] = den == 0.0 ? 0.0 : HH(j + 1, j) / den;
-            HH(j, j) = den;
-            HH(j + 1, j) = 0.0;
-            gv[size_t(j) + 1] = -sn[size_t(j)] * gv[size_t(j)];
-            gv[size_t(j)] = cs[size_t(j)] * gv[size_t(j)];
-            res->iterations += 1;
-            const double est = std::fabs(gv[size_t(j) + 1]);
-            push_hist(est / bnorm);
-            if (est / bnorm <= kc->tolerance || hj1 == 0.0) {
-                ++j;
+            const double rho2 = uu - aa;
+            const double rho = rho2 > 0.0 ? std::sqrt(rho2) : 0.0;
+            if (j >= 1) {
+                // finalise column j-1: H[j, j-1] held |w'_{j-1}| (the norm u_j was built with)
+                HH(j, j - 1) = c->h_red[o_norm];
+                const double hjj1 = HH(j, j - 1);
+                for (int i = 0; i < j; ++i)
+                    HH(i, j - 1) += hjj1 * av[size_t(i)];
+                HH(j, j - 1) = hjj1 * rho;
+                // Givens (linalg.cpp:237-258) on the final column
+                const int k = j - 1;
+                for (int i = 0; i <= j; ++i)
+                    RR(i, k) = HH(i, k);
+                for (int i = 0; i < k; ++i) {
+                    const double t = cs[size_t(i)] * RR(i, k) + sn[size_t(i)] * RR(i + 1, k);
+                    RR(i + 1, k) = -sn[size_t(i)] * RR(i, k) + cs[size_t(i)] * RR(i + 1, k);
+                    RR(i, k) = t;
+                }
+                const double den = std::hypot(RR(k, k), RR(k + 1, k));
+                cs[size_t(k)] = den == 0.0 ? 1.0 : RR(k, k) / den;
+                sn[size_t(k)] = den == 0.0 ? 0.0 : RR(k + 1, k) / den;
+                RR(k, k) = den;
+                RR(k + 1, k) = 0.0;
+                gv[size_t(k) + 1] = -sn[size_t(k)] * gv[size_t(k)];
+                gv[size_t(k)] = cs[size_t(k)] * gv[size_t(k)];
+                res->iterations += 1;
+                res->reorthogonalizations += 1;
+                ncols = j;
+                const double est = std::fabs(gv[size_t(k) + 1]);
+                push_hist(est / bnorm);
+                if (est / bnorm <= kc->tolerance || HH(j, j - 1) == 0.0)
+                    stop = true;
+            }
+            if (last || stop)
+                break;
+            // tentative column j and the update pass
+            const double* b = c->h_red + j;
+            const double uw = c->h_red[2 * j + 1];
+            double ab = 0.0;
+            for (int i = 0; i < j; ++i)
+                ab += av[size_t(i)] * b[i];
+            if (!(rho > 0.0)) {
+                stop = true;  // u_j in span(Q): breakdown
                 break;
             }
+            const double cj = (uw - ab) / rho;
+            for (int i = 0; i <= j; ++i) {
+                double ha = 0.0;
+                for (int l = 0; l < j; ++l)
+                    ha += HH(i, l) * av[size_t(l)];
+                HH(i, j) = ((i < j ? b[i] : cj) - ha) / rho;
+            }
+            const double cr = cj / rho;
+            for (int i = 0; i < j; ++i) {
+                h_coef[i] = av[size_t(i)];
+                h_coef[j + i] = b[i] - cr * av[size_t(i)];
+            }
+            h_coef[2 * j] = 1.0 / rho;
+            h_coef[2 * j + 1] = cr;
+            CK(c, cudaMemcpyAsync(d_coef, h_coef, sizeof(double) * size_t(2 * j + 2),
+                                  cudaMemcpyHostToDevice, st));
+            double* upart = c->partial.p + size_t(2 * m + 8) * kRedBlocks;
+            if (j == 0)
+                gv[0] *= rho;  // V_0 renormalised by its computed norm in the update pass
+            launch_dcgs_update(V, n, j, d_coef, u, c->w.p, n, upart, st);
+            launch_reduce_partials(upart, 1, d_norm, 1, st);
+            // tentative u_{j+1} = w'/|w'| and z = S u_{j+1}
+            launch_normalize(c->w.p, d_norm, V + size_t(j + 1) * size_t(n), n, st, c->scale.p, c->z.p);
+            TRY(check_launch(c));
         }
-        while (j > 0 && HH(j - 1, j - 1) == 0.0)
+        int j = ncols;
+        while (j > 0 && RR(j - 1, j - 1) == 0.0)
             --j;
         for (int i = j - 1; i >= 0; --i) {
             double sacc = gv[size_t(i)];
             for (int k = i + 1; k < j; ++k)
-                sacc -= HH(i, k) * yv[size_t(k)];
-            yv[size_t(i)] = sacc / HH(i, i);
+                sacc -= RR(i, k) * yv[size_t(k)];
+            yv[size_t(i)] = sacc / RR(i, i);
         }
         if (j > 0) {
             std::copy(yv.begin(), yv.begin() + j, c->h_red);
             CK(c, cudaMemcpyAsync(c->red.p, c->h_red, sizeof(double) * size_t(j),
                                   cudaMemcpyHostToDevice, st));
-            launch_gemv_add_scaled(V, n, j, c->red.p, c->scale.p, d_x, n, st);
+            launch_basis_combine(V, n, j, c->red.p, c->scale.p, d_x, n, st);
         }
         // recomputed scaled residual r = S (rhs - L x)
         TRY(matvec_dev(c, d_x, c->w.p, nullptr, true));
@@ -848,7 +939,7 @@ void hbgpu_destroy(hbgpu_ctx* c) {
         cudaFreeHost(c->h_int);
     for (DBuf<double>* b : {&c->geom, &c->H, &c->g, &c->hN, &c->fnormal, &c->farea, &c->state,
                             &c->r, &c->hu, &c->pvals, &c->mass, &c->mass_c, &c->inv, &c->y, &c->out,
-                            &c->x, &c->w, &c->scale, &c->b, &c->tmp, &c->V, &c->partial, &c->red, &c->rpartial})
+                            &c->x, &c->w, &c->z, &c->scale, &c->b, &c->tmp, &c->V, &c->partial, &c->red, &c->rpartial})
         b->release();
     for (DBuf<int>* b : {&c->row_ptr, &c->col_idx, &c->diag_blk, &c->inc_ptr, &c->chunk_node_ptr, &c->chunk_nodes, &c->slot_ptr, &c->npart_ptr, &c->npart,
                          &c->tcta, &c->bnode, &c->bptr, &c->binc, &c->fac, &c->fbc, &c->flag,
@@ -906,8 +997,8 @@ int hbgpu_set_basis(hbgpu_ctx* c, int modes, double period) {
     CK(c, cudaMemcpyAsync(c->H.p, H.data(), sizeof(double) * H.size(), cudaMemcpyHostToDevice,
                           c->stream));
     const size_t n = size_t(c->state_len());
-    for (DBuf<double>* b : {&c->state, &c->r, &c->inv, &c->y, &c->out, &c->x, &c->w, &c->scale,
-                            &c->b, &c->tmp})
+    for (DBuf<double>* b : {&c->state, &c->r, &c->inv, &c->y, &c->out, &c->x, &c->w, &c->z,
+                            &c->scale, &c->b, &c->tmp})
         CK(c, b->alloc(n));
     CK(c, c->hu.alloc(size_t(c->nn) * 3 * size_t(N)));
     CK(c, c->rpartial.alloc(size_t(c->npairs) * 7 * size_t((N + kResTile - 1) / kResTile) * kResTile));

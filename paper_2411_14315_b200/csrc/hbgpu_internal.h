@@ -84,7 +84,8 @@ struct MatvecArgs {
     const double* H;
     const double* y;
     double* out;
-    const double* scale;  // optional split scaling: out = S L (S y)
+    const double* scale;      // optional input scaling (gathered): L (S y)
+    const double* scale_out;  // optional output scaling: S L y
     int nn, N, rows_per_cta;
     int with_c;
 };
@@ -126,6 +127,8 @@ void launch_tangent_rows(const TangentArgs& a, int nctas, int threads, size_t sm
 void launch_mass_rows(const double* geom, const int* row_ptr, const int* inc_ptr, const int4* rec,
                       double rho, double* mass, int nn, cudaStream_t st);
 void launch_tangent_geometry(const double* geom, int ne, double* tg, cudaStream_t st);
+void launch_backflow_tangent(const BoundaryArgs& a, const int* row_ptr, const int* col_idx,
+                             double* pvals, cudaStream_t st);
 void launch_matvec(const MatvecArgs& a, cudaStream_t st);
 void launch_lmatvec(const MatvecArgs& a, cudaStream_t st);
 void launch_mask_mass(const double* mass, const int* row_ptr, const int* col_idx,
@@ -154,6 +157,19 @@ void launch_reduce_partials(const double* partial, int nv, double* out, int take
 // w -= sum_i h[i] V_i
 void launch_gemv_sub(const double* V, long ld, int nv, const double* h, double* w, long n,
                      cudaStream_t st);
+// GMRES orthogonalisation passes (hbgpu_krylov.cu)
+void launch_orth_dots(const double* V, long ld, int nv, const double* w, long n, double* partial,
+                      cudaStream_t st);
+void launch_orth_update(const double* V, long ld, int nv, const double* h, double* w, long n,
+                        double* partial, cudaStream_t st);
+void launch_dcgs_dots(const double* V, long ld, int nv, const double* u, const double* w, long n,
+                      double* partial, cudaStream_t st);
+void launch_dcgs_update(const double* V, long ld, int nv, const double* coef, double* u, double* w,
+                        long n, double* partial, cudaStream_t st);
+void launch_basis_combine(const double* V, long ld, int nv, const double* y, const double* s,
+                          double* x, long n, cudaStream_t st);
+void launch_normalize(const double* in, const double* alpha, double* out, long n, cudaStream_t st,
+                      const double* s = nullptr, double* z = nullptr);
 // x += s * sum_i y[i] V_i
 void launch_gemv_add_scaled(const double* V, long ld, int nv, const double* y, const double* s,
                             double* x, long n, cudaStream_t st);

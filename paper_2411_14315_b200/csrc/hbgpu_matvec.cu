@@ -102,11 +102,11 @@ __global__ void __launch_bounds__(256) lmatvec_kernel(MatvecArgs a) {
     }
     if (valid) {
         const long o = (long)A * 4 * N + n;
-        if (SCALED) {
-            ou0 *= __ldg(a.scale + o);
-            ou1 *= __ldg(a.scale + o + N);
-            ou2 *= __ldg(a.scale + o + 2 * N);
-            op *= __ldg(a.scale + o + 3 * N);
+        if (a.scale_out) {
+            ou0 *= __ldg(a.scale_out + o);
+            ou1 *= __ldg(a.scale_out + o + N);
+            ou2 *= __ldg(a.scale_out + o + 2 * N);
+            op *= __ldg(a.scale_out + o + 3 * N);
         }
         a.out[o] = ou0;
         a.out[o + N] = ou1;

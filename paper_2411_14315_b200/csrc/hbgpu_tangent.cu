@@ -244,6 +244,71 @@ void launch_tangent_rows(const TangentArgs& a, int nctas, int threads, size_t sm
         tangent_rows_kernel<0><<<nctas, threads, smem, st>>>(a);
 }
 
+// Optional frozen-coefficient backflow tangent (assembly.cpp:612-657):
+// K_AB -= w N_a(q) N_b(q) (rho beta / 2) min(u_q . n, 0) for free A, B on a
+// Neumann facet.  Node-centric: thread (boundary row A, n) walks A's facets in
+// the reference order (Neumann entry, facet, quadrature point, b).
+__global__ void backflow_tangent_kernel(BoundaryArgs a, const int* __restrict__ row_ptr,
+                                        const int* __restrict__ col_idx,
+                                        double* __restrict__ pvals) {
+    const int N = a.N;
+    const long t = (long)blockIdx.x * blockDim.x + threadIdx.x;
+    const int bn = (int)(t / N);
+    const int n = (int)(t - (long)bn * N);
+    if (bn >= a.nbnodes)
+        return;
+    const int A = a.bnode[bn];
+    if (a.dir[A])
+        return;
+    const int r0 = row_ptr[A], r1 = row_ptr[A + 1];
+    for (int k = a.bptr[bn]; k < a.bptr[bn + 1]; ++k) {
+        const int f = a.binc[k] >> 2, v = a.binc[k] & 3;
+        const int fn[3] = {a.fac[3 * f], a.fac[3 * f + 1], a.fac[3 * f + 2]};
+        const double nv[3] = {a.fnormal[3 * f], a.fnormal[3 * f + 1], a.fnormal[3 * f + 2]};
+        const double w = a.farea[f] / 3.0;
+        double uf[3][3];
+        for (int c = 0; c < 3; ++c)
+            for (int i = 0; i < 3; ++i)
+                uf[c][i] = a.state[((long)fn[c] * 4 + i) * N + n];
+        for (int q = 0; q < 3; ++q) {
+            double un = 0.0;
+            for (int i = 0; i < 3; ++i) {
+                double uq = 0.0;
+                for (int c = 0; c < 3; ++c)
+                    uq += (q == c ? 2.0 / 3.0 : 1.0 / 6.0) * uf[c][i];
+                un += uq * nv[i];
+            }
+            if (!(un < 0.0))
+                continue;
+            for (int b = 0; b < 3; ++b) {
+                const int B = fn[b];
+                if (a.dir[B])
+                    continue;
+                int lo = r0, hi = r1;
+                while (lo < hi) {
+                    const int mid = (lo + hi) >> 1;
+                    if (col_idx[mid] < B)
+                        lo = mid + 1;
+                    else
+                        hi = mid;
+                }
+                const double c = w * (q == v ? 2.0 / 3.0 : 1.0 / 6.0) * (q == b ? 2.0 / 3.0 : 1.0 / 6.0) *
+                                 0.5 * a.rho * a.beta;
+                pvals[((long)lo * 8) * N + n] -= c * un;
+            }
+        }
+    }
+}
+
+void launch_backflow_tangent(const BoundaryArgs& a, const int* row_ptr, const int* col_idx,
+                             double* pvals, cudaStream_t st) {
+    if (a.nbnodes <= 0)
+        return;
+    note_launch();
+    const long threads = (long)a.nbnodes * a.N;
+    backflow_tangent_kernel<<<(int)((threads + 127) / 128), 128, 0, st>>>(a, row_ptr, col_idx, pvals);
+}
+
 // assemble_mass (assembly.cpp:668-681), row-owned: each block row sums its
 // elements in element order — the reference's order, hence bit-identical.
 __global__ void mass_rows_kernel(const double* __restrict__ geom, const int* __restrict__ row_ptr,

@@ -91,6 +91,7 @@ class _KrylovRes(C.Structure):
         ("relative_residual", C.c_double),
         ("status", C.c_int),
         ("history_len", C.c_int),
+        ("reorthogonalizations", C.c_int),
     ]
 
 
@@ -278,7 +279,7 @@ class GpuContext:
 
     def __del__(self):
         h = getattr(self, "_h", None)
-        if h:
+        if h and _destroy is not None:  # module globals may be gone at interpreter exit
             _destroy(h)
             self._h = None
 
@@ -429,6 +430,7 @@ class GpuContext:
         kc = _KrylovCfg(cfg.restart, cfg.max_iters, cfg.tolerance)
         kr = _KrylovRes()
         self._check(_gmres_dev(self._h, d_rhs, C.byref(kc), d_x, C.byref(kr), None, 0))
+        self.last_reorthogonalizations = kr.reorthogonalizations
         return kr.iterations, kr.relative_residual, kr.status
 
     def pvals_dev(self) -> int:

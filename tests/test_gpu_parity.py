@@ -113,6 +113,24 @@ def test_against_golden_fixtures(gpu, name):
         assert rel(res.x, d["gmres_x"]) < 1e-6
 
 
+@pytest.mark.parametrize("modes", [1, 3])
+def test_backflow_in_tangent(gpu, modes):
+    """AssemblyConfig::backflow_in_tangent (assembly.cpp:612-657)."""
+    prob = tube_problem(modes, h=0.25)
+    ctx = gpu_ctx(prob, 0, 0.3)
+    ctx.set_assembly_config(0, 0.3, 1.5, True)
+    orc = ob.Restated(prob, tau_mode=0, pseudo_dt=0.3, backflow_tangent=True)
+    s = cases.random_state(prob.mesh.num_nodes, prob.N, 31)
+    p_gpu = ctx.assemble_tangent(s)
+    p_orc = orc.tangent(s)
+    assert rel(p_gpu, p_orc) < TOL
+    assert rel(p_orc, ob.Restated(prob, tau_mode=0, pseudo_dt=0.3).tangent(s)) > 1e-8  # term is active
+    if HAVE_REF:
+        ref = ob.ref_context(prob, 0, 0.3)
+        ref.set_cfg(0, 0.3, 1.5, True)
+        assert rel(p_gpu, ref.tangent(s)) < TOL
+
+
 def test_pattern_bit_exact(gpu):
     from paper_2411_14315_b200 import meshgen
 
