@@ -84,6 +84,10 @@ struct hbgpu_ctx {
     DBuf<double> geom;
     DBuf<uint8_t> dir;
     DBuf<int4> inc_rec;
+    DBuf<int> contrib_ptr;
+    DBuf<uint16_t> contrib;
+    int max_inc = 0;
+    size_t trow_smem = 0;
     DBuf<double> tgeom;
     DBuf<int> row_ptr, col_idx, diag_blk, inc_ptr;
     // residual element chunks
@@ -333,6 +337,42 @@ static int upload_all(hbgpu_ctx* c, const hbgpu_mesh_desc* d) {
     CK(c, c->tgeom.alloc(size_t(ne) * kTGeo));
     launch_tangent_geometry(c->geom.p, ne, c->tgeom.p, st);
     TRY(check_launch(c));
+    // per block: its (incidence-in-row, b) contributions in element order
+    {
+        std::vector<int> cptr(size_t(c->nnz) + 1, 0);
+        int max_inc = 0;
+        for (int A = 0; A < nn; ++A) {
+            max_inc = std::max(max_inc, iptr[size_t(A) + 1] - iptr[size_t(A)]);
+            for (int s = iptr[size_t(A)]; s < iptr[size_t(A) + 1]; ++s) {
+                const uint32_t cols = uint32_t(irec[2 * size_t(s) + 1].y);
+                for (int b = 0; b < 4; ++b)
+                    cptr[size_t(c->row_ptr_h[size_t(A)] + int((cols >> (8 * b)) & 0xFF)) + 1] += 1;
+            }
+        }
+        if (max_inc >= 16384)
+            return fail(c, HBGPU_ERR_INVALID, "node with more than 16383 elements");
+        for (long k = 0; k < c->nnz; ++k)
+            cptr[size_t(k) + 1] += cptr[size_t(k)];
+        std::vector<uint16_t> contrib(static_cast<size_t>(cptr[size_t(c->nnz)]));
+        std::vector<int> cf(cptr.begin(), cptr.end() - 1);
+        for (int A = 0; A < nn; ++A)
+            for (int s = iptr[size_t(A)]; s < iptr[size_t(A) + 1]; ++s) {
+                const uint32_t cols = uint32_t(irec[2 * size_t(s) + 1].y);
+                const int i = s - iptr[size_t(A)];
+                for (int b = 0; b < 4; ++b) {
+                    const int k = c->row_ptr_h[size_t(A)] + int((cols >> (8 * b)) & 0xFF);
+                    contrib[size_t(cf[size_t(k)]++)] = uint16_t((i << 2) | b);
+                }
+            }
+        c->max_inc = max_inc;
+        CK(c, c->contrib_ptr.alloc(cptr.size()));
+        CK(c, c->contrib.alloc(contrib.size()));
+        CK(c, cudaMemcpyAsync(c->contrib_ptr.p, cptr.data(), sizeof(int) * cptr.size(),
+                              cudaMemcpyHostToDevice, st));
+        CK(c, cudaMemcpyAsync(c->contrib.p, contrib.data(), sizeof(uint16_t) * contrib.size(),
+                              cudaMemcpyHostToDevice, st));
+        CK(c, cudaStreamSynchronize(st));
+    }
 
     // element chunks of kChunkElems consecutive elements: distinct nodes,
     // chunk-local connectivity, per (chunk, node) slot lists in element order,
@@ -546,7 +586,12 @@ static int tangent_dev(hbgpu_ctx* c, const double* d_state) {
     a.tau_mode = c->tau_mode;
     a.flag = c->flag.p;
     const long p0 = prof_mark(c);
-    launch_tangent_rows(a, int(c->tcta_h.size()) - 1, c->tthreads, c->tsmem, c->stream);
+    a.col_idx = c->col_idx.p;
+    a.diag_blk = c->diag_blk.p;
+    a.contrib_ptr = c->contrib_ptr.p;
+    a.contrib = c->contrib.p;
+    a.max_inc = c->max_inc;
+    launch_tangent_row(a, c->nn, c->trow_smem, c->stream);
     if (c->backflow_tangent && c->nbnodes > 0)
         launch_backflow_tangent(boundary_args(c, d_state, nullptr), c->row_ptr.p, c->col_idx.p,
                                 c->pvals.p, c->stream);
@@ -583,7 +628,9 @@ static int matvec_dev(hbgpu_ctx* c, const double* d_y, double* d_out, const doub
     a.y = d_y;
     a.out = d_out;
     a.scale = d_scale;
-    a.scale_out = d_scale_out ? d_scale_out : d_scale;
+    if (d_scale)
+        return fail(c, HBGPU_ERR_INVALID, "input-scaled matvec is not supported (scale z on the host side)");
+    a.scale_out = d_scale_out;
     a.nn = c->nn;
     a.N = c->N;
     a.rows_per_cta = rows_per_matvec_cta(c->N);
@@ -948,6 +995,8 @@ void hbgpu_destroy(hbgpu_ctx* c) {
     c->conn.release();
     c->dir.release();
     c->inc_rec.release();
+    c->contrib_ptr.release();
+    c->contrib.release();
     c->tgeom.release();
     c->lconn.release();
     c->slot_idx.release();
@@ -1023,6 +1072,10 @@ int hbgpu_set_basis(hbgpu_ctx* c, int modes, double period) {
     c->mass_valid = false;
     TRY(plan_tangent(c));
     CK(c, configure_tangent_smem(c->tsmem));
+    c->trow_smem = tangent_row_smem(c->max_inc, (c->max_inc + kTanPart - 1) / kTanPart, N);
+    if (c->trow_smem > 227 * 1024)
+        return fail(c, HBGPU_ERR_INVALID, "node valence too high for the tangent row kernel at this N");
+    CK(c, configure_tangent_row_smem(c->trow_smem));
     // clear previous Neumann data sized for another N
     c->hN.release();
     c->h_h.clear();

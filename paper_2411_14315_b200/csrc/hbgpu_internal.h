@@ -22,6 +22,9 @@ constexpr int kChunkElems = 64;
 constexpr int kResTile = 4;
 // Compact tangent geometry record (gradN 12, V, symmetric xi 6, xi:xi).
 constexpr int kTGeo = 20;
+// Tangent v3: threads per row CTA, contributions per diagonal part.
+constexpr int kTanThreads = 256;
+constexpr int kTanPart = 8;
 
 // Build-time tuning knobs of the residual element pass.
 #ifndef RES_VOLATILE_LDS
@@ -29,6 +32,9 @@ constexpr int kTGeo = 20;
 #endif
 #ifndef RES_MINB
 #define RES_MINB 2
+#endif
+#ifndef TAN_MINB
+#define TAN_MINB 3
 #endif
 #ifndef MV_UNROLL
 #define MV_UNROLL 2
@@ -73,6 +79,13 @@ struct TangentArgs {
     double rho, mu, nu, pseudo_c;
     int tau_mode;
     int* flag;
+    // tangent v3 (one CTA per row): per block, its contributions (i<<2 | b),
+    // i = incidence index within the row, in element order
+    const int* col_idx;
+    const int* diag_blk;
+    const int* contrib_ptr;        // nnz + 1
+    const uint16_t* contrib;
+    int max_inc;
 };
 
 struct MatvecArgs {
@@ -127,6 +140,9 @@ void launch_tangent_rows(const TangentArgs& a, int nctas, int threads, size_t sm
 void launch_mass_rows(const double* geom, const int* row_ptr, const int* inc_ptr, const int4* rec,
                       double rho, double* mass, int nn, cudaStream_t st);
 void launch_tangent_geometry(const double* geom, int ne, double* tg, cudaStream_t st);
+size_t tangent_row_smem(int max_inc, int max_dparts, int N);
+cudaError_t configure_tangent_row_smem(size_t bytes);
+void launch_tangent_row(const TangentArgs& a, int nrows, size_t smem, cudaStream_t st);
 void launch_backflow_tangent(const BoundaryArgs& a, const int* row_ptr, const int* col_idx,
                              double* pvals, cudaStream_t st);
 void launch_matvec(const MatvecArgs& a, cudaStream_t st);

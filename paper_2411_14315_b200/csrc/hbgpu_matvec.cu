@@ -37,12 +37,6 @@ __global__ void __launch_bounds__(256) lmatvec_kernel(MatvecArgs a) {
         const long yb = (long)B * 4 * N + n;
         double y0 = __ldg(a.y + yb), y1 = __ldg(a.y + yb + N), y2 = __ldg(a.y + yb + 2 * N),
                y3 = __ldg(a.y + yb + 3 * N);
-        if (SCALED) {
-            y0 *= __ldg(a.scale + yb);
-            y1 *= __ldg(a.scale + yb + N);
-            y2 *= __ldg(a.scale + yb + 2 * N);
-            y3 *= __ldg(a.scale + yb + 3 * N);
-        }
         const double kd = ldcs(v), g0 = ldcs(v + N), g1 = ldcs(v + 2 * N), g2 = ldcs(v + 3 * N);
         const double d0 = ldcs(v + 4 * N), d1 = ldcs(v + 5 * N), d2 = ldcs(v + 6 * N),
                      ld = ldcs(v + 7 * N);
@@ -102,7 +96,7 @@ __global__ void __launch_bounds__(256) lmatvec_kernel(MatvecArgs a) {
     }
     if (valid) {
         const long o = (long)A * 4 * N + n;
-        if (a.scale_out) {
+        if (SCALED) {
             ou0 *= __ldg(a.scale_out + o);
             ou1 *= __ldg(a.scale_out + o + N);
             ou2 *= __ldg(a.scale_out + o + 2 * N);
@@ -124,12 +118,12 @@ void launch_lmatvec(const MatvecArgs& a, cudaStream_t st) {
         a.with_c ? sizeof(double) * ((size_t)a.N * a.N + 3 * (size_t)a.N * a.rows_per_cta) : 0;
     note_launch();
     if (a.with_c) {
-        if (a.scale)
+        if (a.scale_out)
             lmatvec_kernel<true, true><<<blocks, threads, smem, st>>>(a);
         else
             lmatvec_kernel<false, true><<<blocks, threads, smem, st>>>(a);
     } else {
-        if (a.scale)
+        if (a.scale_out)
             lmatvec_kernel<true, false><<<blocks, threads, smem, st>>>(a);
         else
             lmatvec_kernel<false, false><<<blocks, threads, smem, st>>>(a);
