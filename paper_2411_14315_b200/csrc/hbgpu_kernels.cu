@@ -334,7 +334,9 @@ __device__ __forceinline__ void cp_async_wait() {
 
 __device__ __forceinline__ void residual_issue(const ResidualChunkArgs& a, int item, int ntiles,
                                                double* nd, double* geo) {
-    const int N = a.N, T = a.T, CE = a.CE, ndst = 7 * T;
+    // compile-time tile shape: the index arithmetic becomes shifts / multiplies
+    constexpr int T = kResTile, CE = kChunkElems, ndst = 7 * T;
+    const int N = a.N;
     const int ch = item / ntiles, n0 = (item - ch * ntiles) * T;
     const int nb = a.chunk_node_ptr[ch], nloc = a.chunk_node_ptr[ch + 1] - nb;
     const int e0 = ch * CE, ecount = min(CE, a.ne - e0);
@@ -356,7 +358,8 @@ __device__ __forceinline__ void residual_issue(const ResidualChunkArgs& a, int i
 
 __global__ void __launch_bounds__(256, RES_MINB) residual_chunk_kernel(ResidualChunkArgs a) {
     extern __shared__ __align__(16) double sm[];
-    const int N = a.N, T = a.T, CE = a.CE;
+    constexpr int T = kResTile, CE = kChunkElems;
+    const int N = a.N;
     const int ntiles = (N + T - 1) / T;
     const int nitems = a.nchunks * ntiles;
     const int ndst = 7 * T;
