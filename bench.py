@@ -443,6 +443,73 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
+def sweep_config4(args):
+    """BASELINE config 4: operator-only sweep on the Delaunay mesh of 700k
+    seeded points in the unit cube, Nm in {1,4,10,16,24} (N = 1..47): one
+    residual + one Jacobian assembly and 100 L-matvecs per Nm, random modes
+    c_k ~ N(0,1)/k^2.  Prints one JSON line (not the driver's bench line)."""
+    import torch
+
+    from paper_2411_14315_b200 import cases, hbgpu, meshgen
+
+    t0 = time.time()
+    mesh = meshgen.cube_delaunay(args.sweep_points, seed=4)
+    t_mesh = time.time() - t0
+    ctx = hbgpu.GpuContext(mesh)
+    ne, nn = mesh.num_elements, mesh.num_nodes
+    stream = torch.cuda.ExternalStream(ctx.stream)
+    hbm = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"]
+    peak = np.zeros(1)
+    hbgpu._lib.hbgpu_fp64_peak.argtypes = [hbgpu._vp]
+    hbgpu._lib.hbgpu_fp64_peak(peak.ctypes.data)
+    out = []
+    for M in (1, 4, 10, 16, 24):
+        N = 2 * M - 1
+        ctx.set_basis(M, 1.0)
+        ctx.set_fluid(1.06, 0.04)
+        neu = [(k, np.zeros(N)) for k, p in enumerate(mesh.patches) if p.kind == 1]
+        ctx.set_bcs(None, neu, 0.2)
+        ctx.set_assembly_config(0, 0.01)
+        nnz = ctx.nnz
+        s = torch.from_numpy(cases.random_modes_state(nn, M, 1000 + M)).cuda()
+        r = torch.empty_like(s)
+        y = torch.from_numpy(np.random.default_rng(M).uniform(-1, 1, nn * 4 * N)).cuda()
+        o = torch.empty_like(y)
+        for _ in range(2):
+            ctx.assemble_residual_dev(s.data_ptr(), r.data_ptr())
+            ctx.assemble_tangent_dev(s.data_ptr())
+        ctx.assemble_mass()
+        ctx.matvec_dev(y.data_ptr(), o.data_ptr())
+        torch.cuda.synchronize()
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+        with torch.cuda.stream(stream):
+            ev[0].record(stream)
+            ctx.assemble_residual_dev(s.data_ptr(), r.data_ptr())
+            ev[1].record(stream)
+            ctx.assemble_tangent_dev(s.data_ptr())
+            ev[2].record(stream)
+            for _ in range(100):
+                ctx.matvec_dev(y.data_ptr(), o.data_ptr())
+            ev[3].record(stream)
+        torch.cuda.synchronize()
+        ctx.synchronize()
+        t_res, t_tan = ev[0].elapsed_time(ev[1]), ev[1].elapsed_time(ev[2])
+        t_mv = ev[2].elapsed_time(ev[3]) / 100
+        mvb = spmv_bytes(nnz, nn, N)
+        out.append({
+            "Nm": M, "N": N, "nnz_blocks": nnz, "residual_ms": t_res, "tangent_ms": t_tan,
+            "assembly_elements_modes_per_s": ne * M / ((t_res + t_tan) * 1e-3),
+            "residual_tflops": CANON_RES_FLOP * ne * N / (t_res * 1e-3) / 1e12,
+            "tangent_tflops": CANON_TAN_FLOP * ne * N / (t_tan * 1e-3) / 1e12,
+            "matvec_ms": t_mv, "matvec_gbs": mvb / (t_mv * 1e-3) / 1e9,
+            "matvec_frac_hbm": mvb / (t_mv * 1e-3) / 1e9 / hbm,
+        })
+        del s, r, y, o
+    print(json.dumps({"sweep": "config4", "points": args.sweep_points, "elements": ne, "nodes": nn,
+                      "mesh_seconds": t_mesh, "fp64_peak_tflops": float(peak[0]),
+                      "hbm_peak_gbs": hbm, "results": out}), flush=True)
+
+
 def solve_config0():
     from paper_2411_14315_b200 import cases, hbgpu
 
@@ -471,7 +538,12 @@ def main():
     ap.add_argument("--spmv-reps", type=int, default=100)
     ap.add_argument("--no-solve", dest="solve", action="store_false")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--sweep4", action="store_true", help="config-4 operator sweep (separate run)")
+    ap.add_argument("--sweep-points", type=int, default=700_000)
     args = ap.parse_args()
+    if args.sweep4:
+        sweep_config4(args)
+        return
     if args.impl == "reference":
         run_reference(args)
     else:

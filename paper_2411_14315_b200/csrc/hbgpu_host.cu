@@ -86,7 +86,7 @@ struct hbgpu_ctx {
     DBuf<int4> inc_rec;
     DBuf<int> contrib_ptr;
     DBuf<uint16_t> contrib;
-    int max_inc = 0;
+    int max_inc = 0, tan_nt = 1;
     size_t trow_smem = 0;
     DBuf<double> tgeom;
     DBuf<int> row_ptr, col_idx, diag_blk, inc_ptr;
@@ -591,6 +591,7 @@ static int tangent_dev(hbgpu_ctx* c, const double* d_state) {
     a.contrib_ptr = c->contrib_ptr.p;
     a.contrib = c->contrib.p;
     a.max_inc = c->max_inc;
+    a.NT = c->tan_nt;
     launch_tangent_row(a, c->nn, c->trow_smem, c->stream);
     if (c->backflow_tangent && c->nbnodes > 0)
         launch_backflow_tangent(boundary_args(c, d_state, nullptr), c->row_ptr.p, c->col_idx.p,
@@ -1072,9 +1073,17 @@ int hbgpu_set_basis(hbgpu_ctx* c, int modes, double period) {
     c->mass_valid = false;
     TRY(plan_tangent(c));
     CK(c, configure_tangent_smem(c->tsmem));
-    c->trow_smem = tangent_row_smem(c->max_inc, (c->max_inc + kTanPart - 1) / kTanPart, N);
+    {
+        // largest time-sample tile whose row summaries fit 64 KB (3 CTAs / SM)
+        const int dp = (c->max_inc + kTanPart - 1) / kTanPart;
+        int nt = N;
+        while (nt > 1 && tangent_row_smem(c->max_inc, dp, nt) > 64 * 1024)
+            nt = (nt + 1) / 2;
+        c->tan_nt = nt;
+        c->trow_smem = tangent_row_smem(c->max_inc, dp, nt);
+    }
     if (c->trow_smem > 227 * 1024)
-        return fail(c, HBGPU_ERR_INVALID, "node valence too high for the tangent row kernel at this N");
+        return fail(c, HBGPU_ERR_INVALID, "node valence too high for the tangent row kernel");
     CK(c, configure_tangent_row_smem(c->trow_smem));
     // clear previous Neumann data sized for another N
     c->hN.release();

@@ -86,6 +86,7 @@ struct TangentArgs {
     const int* contrib_ptr;        // nnz + 1
     const uint16_t* contrib;
     int max_inc;
+    int NT;  // time samples per CTA (tile of N)
 };
 
 struct MatvecArgs {

@@ -243,20 +243,23 @@ __global__ void __launch_bounds__(kTanThreads, TAN_MINB) tangent_row_kernel(Tang
     extern __shared__ __align__(16) double sm[];
     const int N = a.N;
     const int A = blockIdx.x;
+    // time-sample tile of this CTA (all N unless a high-valence row at large
+    // N would overflow shared memory)
+    const int NT = a.NT, n0 = blockIdx.y * NT, nt = min(NT, N - n0);
     const int i0 = a.inc_ptr[A], ninc = a.inc_ptr[A + 1] - i0;
     const int k0 = a.row_ptr[A], nblk = a.row_ptr[A + 1] - k0;
-    double* summ = sm;                                   // [i][8][n]
-    double* geo = summ + (size_t)a.max_inc * 8 * N;      // [i][16]: gradN 12, V, la
-    double* dpart = geo + (size_t)a.max_inc * 16;        // [part][8][n] diagonal partials
+    double* summ = sm;                                   // [i][8][t]
+    double* geo = summ + (size_t)a.max_inc * 8 * NT;     // [i][16]: gradN 12, V, la
+    double* dpart = geo + (size_t)a.max_inc * 16;        // [part][8][t] diagonal partials
     const double rho = a.rho, diffc = 3.0 * a.nu * a.nu, dAB = kQA - kQB;
 
-    for (int it = threadIdx.x; it < ninc * N; it += blockDim.x) {
-        const int i = it / N, n = it - i * N;
+    for (int it = threadIdx.x; it < ninc * nt; it += blockDim.x) {
+        const int i = it / nt, t = it - i * nt, n = n0 + t;
         const int4 r0 = __ldg(a.inc_rec + 2 * (i0 + i));
         const int4 r1 = __ldg(a.inc_rec + 2 * (i0 + i) + 1);
         const int e = r1.x & 0x3FFFFFFF, la = (unsigned)r1.x >> 30;
         const double* g = a.tgeom + (long)kTGeo * e;
-        if (n == 0) {
+        if (t == 0) {
             for (int k = 0; k < 13; ++k)
                 geo[i * 16 + k] = __ldg(g + k);
             geo[i * 16 + 13] = double(la);
@@ -317,16 +320,16 @@ __global__ void __launch_bounds__(kTanThreads, TAN_MINB) tangent_row_kernel(Tang
                 kap[c] += (na + tadv) * uq[c];
             }
         }
-        double* s = summ + (size_t)i * 8 * N + n;
+        double* s = summ + (size_t)i * 8 * NT + t;
         const double wr = w * rho;
         s[0] = wr * kap[0];
-        s[N] = wr * kap[1];
-        s[2 * N] = wr * kap[2];
-        s[3 * N] = w * asum;
-        s[4 * N] = w * z[0];
-        s[5 * N] = w * z[1];
-        s[6 * N] = w * z[2];
-        s[7 * N] = (w / rho) * tsum;
+        s[NT] = wr * kap[1];
+        s[2 * NT] = wr * kap[2];
+        s[3 * NT] = w * asum;
+        s[4 * NT] = w * z[0];
+        s[5 * NT] = w * z[1];
+        s[6 * NT] = w * z[2];
+        s[7 * NT] = (w / rho) * tsum;
     }
     __syncthreads();
 
@@ -335,9 +338,9 @@ __global__ void __launch_bounds__(kTanThreads, TAN_MINB) tangent_row_kernel(Tang
     const int cb = a.contrib_ptr[k0];
     const int ndiag = a.contrib_ptr[k0 + kdiag + 1] - a.contrib_ptr[k0 + kdiag];
     const int dparts = (ndiag + kTanPart - 1) / kTanPart;
-    const int nitems = (nblk - 1 + dparts) * N;
+    const int nitems = (nblk - 1 + dparts) * nt;
     for (int it = threadIdx.x; it < nitems; it += blockDim.x) {
-        const int slot = it / N, n = it - slot * N;
+        const int slot = it / nt, t = it - slot * nt, n = n0 + t;
         int j, c0, c1, part = -1;
         if (slot < nblk - 1) {
             j = slot < kdiag ? slot : slot + 1;
@@ -359,19 +362,19 @@ __global__ void __launch_bounds__(kTanThreads, TAN_MINB) tangent_row_kernel(Tang
             const double ga0 = gi[3 * la], ga1 = gi[3 * la + 1], ga2 = gi[3 * la + 2];
             const double gb0 = gi[3 * b], gb1 = gi[3 * b + 1], gb2 = gi[3 * b + 2];
             const double V = gi[12], w = 0.25 * V;
-            const double* s = summ + (size_t)i * 8 * N + n;
+            const double* s = summ + (size_t)i * 8 * NT + t;
             const double gg = ga0 * gb0 + ga1 * gb1 + ga2 * gb2;
             K += a.mu * V * gg + a.pseudo_c * V * (b == la ? 0.1 : 0.05) +
-                 (s[0] * gb0 + s[N] * gb1 + s[2 * N] * gb2);
-            const double al = s[3 * N];
+                 (s[0] * gb0 + s[NT] * gb1 + s[2 * NT] * gb2);
+            const double al = s[3 * NT];
             G0 += -ga0 * w + al * gb0;
             G1 += -ga1 * w + al * gb1;
             G2 += -ga2 * w + al * gb2;
-            const double alb = s[4 * N] * gb0 + s[5 * N] * gb1 + s[6 * N] * gb2;
+            const double alb = s[4 * NT] * gb0 + s[5 * NT] * gb1 + s[6 * NT] * gb2;
             D0 += gb0 * w + ga0 * alb;
             D1 += gb1 * w + ga1 * alb;
             D2 += gb2 * w + ga2 * alb;
-            L += gg * s[7 * N];
+            L += gg * s[7 * NT];
         }
         if (afix || bfix)
             K = 0.0;
@@ -391,25 +394,25 @@ __global__ void __launch_bounds__(kTanThreads, TAN_MINB) tangent_row_kernel(Tang
             __stcs(out + 6 * N, D2);
             __stcs(out + 7 * N, L);
         } else {
-            double* o = dpart + (size_t)part * 8 * N + n;
+            double* o = dpart + (size_t)part * 8 * NT + t;
             o[0] = K;
-            o[N] = G0;
-            o[2 * N] = G1;
-            o[3 * N] = G2;
-            o[4 * N] = D0;
-            o[5 * N] = D1;
-            o[6 * N] = D2;
-            o[7 * N] = L;
+            o[NT] = G0;
+            o[2 * NT] = G1;
+            o[3 * NT] = G2;
+            o[4 * NT] = D0;
+            o[5 * NT] = D1;
+            o[6 * NT] = D2;
+            o[7 * NT] = L;
         }
     }
     (void)cb;
     __syncthreads();
     // diagonal block: sum the parts in order; identity K on Dirichlet rows (assembly.cpp:659-665)
-    for (int it = threadIdx.x; it < 8 * N; it += blockDim.x) {
-        const int sl = it / N, n = it - sl * N;
+    for (int it = threadIdx.x; it < 8 * nt; it += blockDim.x) {
+        const int sl = it / nt, t = it - sl * nt, n = n0 + t;
         double v = 0.0;
         for (int p = 0; p < dparts; ++p)
-            v += dpart[((size_t)p * 8 + sl) * N + n];
+            v += dpart[((size_t)p * 8 + sl) * NT + t];
         if (sl == 0 && afix)
             v = 1.0;
         __stcs(a.pvals + ((long)(k0 + kdiag) * 8 + sl) * N + n, v);
@@ -433,10 +436,11 @@ void launch_tangent_row(const TangentArgs& a, int nrows, size_t smem, cudaStream
     if (nrows <= 0)
         return;
     note_launch();
+    const dim3 grid(nrows, (a.N + a.NT - 1) / a.NT);
     if (a.tau_mode == 1)
-        tangent_row_kernel<1><<<nrows, kTanThreads, smem, st>>>(a);
+        tangent_row_kernel<1><<<grid, kTanThreads, smem, st>>>(a);
     else
-        tangent_row_kernel<0><<<nrows, kTanThreads, smem, st>>>(a);
+        tangent_row_kernel<0><<<grid, kTanThreads, smem, st>>>(a);
 }
 
 cudaError_t configure_tangent_smem(size_t bytes) {

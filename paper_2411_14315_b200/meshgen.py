@@ -74,9 +74,56 @@ def hex_cylinder(radius: float, length: float, nx: int, ny: int, nz: int) -> Mes
     return mesh.finalize()
 
 
+def _morton(p: np.ndarray, bits: int = 16) -> np.ndarray:
+    """Morton (Z-order) key of points in their bounding box."""
+    lo, hi = p.min(axis=0), p.max(axis=0)
+    q = ((p - lo) / np.maximum(hi - lo, 1e-300) * ((1 << bits) - 1)).astype(np.uint64)
+    key = np.zeros(len(p), dtype=np.uint64)
+    for b in range(bits):
+        for d in range(3):
+            key |= ((q[:, d] >> np.uint64(b)) & np.uint64(1)) << np.uint64(3 * b + d)
+    return key
+
+
+def cube_delaunay(npoints: int, seed: int = 4) -> Mesh:
+    """BASELINE config 4: Delaunay tetrahedralisation (scipy / Qhull) of
+    `npoints` seeded uniform points in the unit cube.  Nodes and elements are
+    renumbered along a Morton curve (the GPU kernels' gathers and element
+    chunks rely on spatial locality of the numbering).  Boundary facets are
+    split by outward normal: `inlet` (n_x <= -0.8, Dirichlet), `outlet`
+    (n_x >= 0.8, Neumann), `wall` (the rest, Dirichlet)."""
+    from scipy.spatial import Delaunay
+
+    pts = np.random.default_rng(seed).random((npoints, 3))
+    perm = np.argsort(_morton(pts), kind="stable")
+    pts = pts[perm]
+    tri = Delaunay(pts)
+    conn = tri.simplices.astype(np.int32)
+    conn = conn[np.argsort(_morton(pts[conn].mean(axis=1)), kind="stable")]
+    mesh = Mesh(xyz=pts, conn=conn, patches=[])
+    mesh.finalize()  # orientation only (no patches yet)
+    bf = boundary_faces(mesh.conn, mesh.num_nodes)
+    a, b, c = pts[bf[:, 0]], pts[bf[:, 1]], pts[bf[:, 2]]
+    nrm = np.cross(b - a, c - a)
+    nrm /= np.linalg.norm(nrm, axis=1)[:, None]
+    # orient outward: away from the cube centre (the hull is convex)
+    flip = np.einsum("ij,ij->i", nrm, (a + b + c) / 3.0 - 0.5) < 0
+    nrm[flip] = -nrm[flip]
+    inlet = nrm[:, 0] <= -0.8
+    outlet = nrm[:, 0] >= 0.8
+    mesh.patches = [
+        Patch("inlet", DIRICHLET, bf[inlet]),
+        Patch("outlet", NEUMANN, bf[outlet]),
+        Patch("wall", DIRICHLET, bf[~inlet & ~outlet]),
+    ]
+    return mesh.finalize()
+
+
 def config_mesh(cfg: int) -> Mesh:
     if cfg == 0:
         return hex_cylinder(0.3, 6.0, 10, 10, 60)
     if cfg == 1:
         return hex_cylinder(0.3, 6.0, 20, 20, 120)
+    if cfg == 4:
+        return cube_delaunay(700_000, seed=4)
     raise ValueError(f"no generator for config {cfg} yet")

@@ -131,6 +131,29 @@ def test_backflow_in_tangent(gpu, modes):
         assert rel(p_gpu, ref.tangent(s)) < TOL
 
 
+@pytest.mark.parametrize("modes", [1, 4, 24])
+def test_delaunay_cube_operator(gpu, modes):
+    """Config-4 style mesh (Delaunay, high-valence hull nodes, Morton order)
+    at N up to 47: exercises the time-sample tiling of the tangent kernel."""
+    from paper_2411_14315_b200 import meshgen
+
+    mesh = meshgen.cube_delaunay(4000, seed=11)
+    N = 2 * modes - 1
+    neu = [(k, np.full(N, 50.0)) for k, p in enumerate(mesh.patches) if p.kind == NEUMANN]
+    prob = Problem(mesh, modes, 1.0, 1.06, 0.04, np.zeros(mesh.num_nodes * 3 * N), neu, 0.2)
+    ctx = gpu_ctx(prob, 0, 0.05)
+    orc = ob.Restated(prob, tau_mode=0, pseudo_dt=0.05)
+    s = cases.random_modes_state(mesh.num_nodes, modes, 3)
+    assert rel(ctx.assemble_residual(s), orc.residual(s)) < TOL
+    p_gpu = ctx.assemble_tangent(s)
+    p_orc = orc.tangent(s)
+    assert rel(p_gpu, p_orc) < TOL
+    y = cases.random_state(mesh.num_nodes, N, 5)
+    assert rel(ctx.matvec(y), orc.matvec(p_orc, orc.mass(), y)) < TOL
+    rp, ci = ctx.pattern()
+    assert np.array_equal(ci, orc.col_idx)
+
+
 def test_pattern_bit_exact(gpu):
     from paper_2411_14315_b200 import meshgen
 
