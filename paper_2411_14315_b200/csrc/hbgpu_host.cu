@@ -86,8 +86,14 @@ struct hbgpu_ctx {
     DBuf<int4> inc_rec;
     DBuf<int> contrib_ptr;
     DBuf<uint16_t> contrib;
-    int max_inc = 0, tan_nt = 1;
-    size_t trow_smem = 0;
+    int max_inc = 0;
+    // tangent rows bucketed by valence (<= 32 incidences / more), so the few
+    // high-valence rows do not set the shared-memory size of every CTA
+    struct TanBucket {
+        DBuf<int> rows;
+        int count = 0, max_inc = 0, nt = 1;
+        size_t smem = 0;
+    } tb[2];
     DBuf<double> tgeom;
     DBuf<int> row_ptr, col_idx, diag_blk, inc_ptr;
     // residual element chunks
@@ -365,6 +371,21 @@ static int upload_all(hbgpu_ctx* c, const hbgpu_mesh_desc* d) {
                 }
             }
         c->max_inc = max_inc;
+        std::vector<int> brows[2];
+        for (int A = 0; A < nn; ++A) {
+            const int ni = iptr[size_t(A) + 1] - iptr[size_t(A)];
+            const int bk = ni <= 32 ? 0 : 1;
+            brows[bk].push_back(A);
+            c->tb[bk].max_inc = std::max(c->tb[bk].max_inc, ni);
+        }
+        for (int bk = 0; bk < 2; ++bk) {
+            c->tb[bk].count = int(brows[bk].size());
+            if (!c->tb[bk].count)
+                continue;
+            CK(c, c->tb[bk].rows.alloc(brows[bk].size()));
+            CK(c, cudaMemcpyAsync(c->tb[bk].rows.p, brows[bk].data(), sizeof(int) * brows[bk].size(),
+                                  cudaMemcpyHostToDevice, st));
+        }
         CK(c, c->contrib_ptr.alloc(cptr.size()));
         CK(c, c->contrib.alloc(contrib.size()));
         CK(c, cudaMemcpyAsync(c->contrib_ptr.p, cptr.data(), sizeof(int) * cptr.size(),
@@ -590,9 +611,14 @@ static int tangent_dev(hbgpu_ctx* c, const double* d_state) {
     a.diag_blk = c->diag_blk.p;
     a.contrib_ptr = c->contrib_ptr.p;
     a.contrib = c->contrib.p;
-    a.max_inc = c->max_inc;
-    a.NT = c->tan_nt;
-    launch_tangent_row(a, c->nn, c->trow_smem, c->stream);
+    for (const auto& b : c->tb) {
+        if (!b.count)
+            continue;
+        a.rows = b.rows.p;
+        a.max_inc = b.max_inc;
+        a.NT = b.nt;
+        launch_tangent_row(a, b.count, b.smem, c->stream);
+    }
     if (c->backflow_tangent && c->nbnodes > 0)
         launch_backflow_tangent(boundary_args(c, d_state, nullptr), c->row_ptr.p, c->col_idx.p,
                                 c->pvals.p, c->stream);
@@ -998,6 +1024,8 @@ void hbgpu_destroy(hbgpu_ctx* c) {
     c->inc_rec.release();
     c->contrib_ptr.release();
     c->contrib.release();
+    c->tb[0].rows.release();
+    c->tb[1].rows.release();
     c->tgeom.release();
     c->lconn.release();
     c->slot_idx.release();
@@ -1074,17 +1102,23 @@ int hbgpu_set_basis(hbgpu_ctx* c, int modes, double period) {
     TRY(plan_tangent(c));
     CK(c, configure_tangent_smem(c->tsmem));
     {
-        // largest time-sample tile whose row summaries fit 64 KB (3 CTAs / SM)
-        const int dp = (c->max_inc + kTanPart - 1) / kTanPart;
-        int nt = N;
-        while (nt > 1 && tangent_row_smem(c->max_inc, dp, nt) > 64 * 1024)
-            nt = (nt + 1) / 2;
-        c->tan_nt = nt;
-        c->trow_smem = tangent_row_smem(c->max_inc, dp, nt);
+        // per bucket: largest time-sample tile whose row summaries fit 64 KB (3 CTAs / SM)
+        size_t mx = 0;
+        for (auto& b : c->tb) {
+            if (!b.count)
+                continue;
+            const int dp = (b.max_inc + kTanPart - 1) / kTanPart;
+            int nt = N;
+            while (nt > 1 && tangent_row_smem(b.max_inc, dp, nt) > 64 * 1024)
+                nt = (nt + 1) / 2;
+            b.nt = nt;
+            b.smem = tangent_row_smem(b.max_inc, dp, nt);
+            mx = std::max(mx, b.smem);
+        }
+        if (mx > 227 * 1024)
+            return fail(c, HBGPU_ERR_INVALID, "node valence too high for the tangent row kernel");
+        CK(c, configure_tangent_row_smem(mx));
     }
-    if (c->trow_smem > 227 * 1024)
-        return fail(c, HBGPU_ERR_INVALID, "node valence too high for the tangent row kernel");
-    CK(c, configure_tangent_row_smem(c->trow_smem));
     // clear previous Neumann data sized for another N
     c->hN.release();
     c->h_h.clear();

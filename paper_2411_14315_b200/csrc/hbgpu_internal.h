@@ -23,7 +23,10 @@ constexpr int kResTile = 4;
 // Compact tangent geometry record (gradN 12, V, symmetric xi 6, xi:xi).
 constexpr int kTGeo = 20;
 // Tangent v3: threads per row CTA, contributions per diagonal part.
-constexpr int kTanThreads = 256;
+#ifndef TAN_THREADS
+#define TAN_THREADS 128
+#endif
+constexpr int kTanThreads = TAN_THREADS;
 constexpr int kTanPart = 8;
 
 // Build-time tuning knobs of the residual element pass.
@@ -34,7 +37,7 @@ constexpr int kTanPart = 8;
 #define RES_MINB 2
 #endif
 #ifndef TAN_MINB
-#define TAN_MINB 3
+#define TAN_MINB 6
 #endif
 #ifndef MV_UNROLL
 #define MV_UNROLL 2
@@ -86,7 +89,8 @@ struct TangentArgs {
     const int* contrib_ptr;        // nnz + 1
     const uint16_t* contrib;
     int max_inc;
-    int NT;  // time samples per CTA (tile of N)
+    int NT;            // time samples per CTA (tile of N)
+    const int* rows;   // block rows of this launch (one valence bucket)
 };
 
 struct MatvecArgs {

@@ -242,7 +242,7 @@ template <int TAU>
 __global__ void __launch_bounds__(kTanThreads, TAN_MINB) tangent_row_kernel(TangentArgs a) {
     extern __shared__ __align__(16) double sm[];
     const int N = a.N;
-    const int A = blockIdx.x;
+    const int A = a.rows[blockIdx.x];  // rows are bucketed by valence
     // time-sample tile of this CTA (all N unless a high-valence row at large
     // N would overflow shared memory)
     const int NT = a.NT, n0 = blockIdx.y * NT, nt = min(NT, N - n0);
