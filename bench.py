@@ -260,8 +260,8 @@ def run_ours(args):
     L.hbgpu_fp64_peak.argtypes = [hbgpu._vp]
 
     def step():
-        ctx.assemble_residual_dev(d_state.data_ptr(), d_r.data_ptr())
-        ctx.assemble_tangent_dev(d_state.data_ptr())
+        # one Newton iteration's assembly: residual + tangent of the iterate
+        ctx.assemble_dev(d_state.data_ptr(), d_r.data_ptr())
 
     for _ in range(args.warmup):
         step()

@@ -142,6 +142,9 @@ int hbgpu_gmres(hbgpu_ctx* ctx, const double* rhs, const double* inv_diag,
 /* ---- device-resident fast path (device pointers, ctx stream) ----------- */
 int hbgpu_assemble_residual_dev(hbgpu_ctx* ctx, const double* d_state, double* d_residual);
 int hbgpu_assemble_tangent_dev(hbgpu_ctx* ctx, const double* d_state);
+/* Residual + tangent of one state (one Newton iteration's assembly); the two
+ * run concurrently on the context's two streams.  Ordered on hbgpu_stream(). */
+int hbgpu_assemble_dev(hbgpu_ctx* ctx, const double* d_state, double* d_residual);
 int hbgpu_matvec_dev(hbgpu_ctx* ctx, const double* d_y, double* d_out);
 int hbgpu_bsr_matvec_dev(hbgpu_ctx* ctx, const double* d_y, double* d_out);
 int hbgpu_jacobi_dev(hbgpu_ctx* ctx, int* degenerate_entries);

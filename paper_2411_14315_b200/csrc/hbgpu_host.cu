@@ -91,7 +91,7 @@ struct hbgpu_ctx {
     // high-valence rows do not set the shared-memory size of every CTA
     struct TanBucket {
         DBuf<int> rows;
-        int count = 0, max_inc = 0, nt = 1;
+        int count = 0, max_inc = 0, max_blk = 0, nt = 1;
         size_t smem = 0;
     } tb[2];
     DBuf<double> tgeom;
@@ -144,6 +144,9 @@ struct hbgpu_ctx {
     };
     std::vector<Pair> pairs;
     cudaStream_t stream = nullptr;
+    // second stream: the tangent runs concurrently with the residual
+    cudaStream_t stream2 = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     std::string err;
 
     long long state_len() const { return (long long)nn * 4 * N; }
@@ -377,6 +380,8 @@ static int upload_all(hbgpu_ctx* c, const hbgpu_mesh_desc* d) {
             const int bk = ni <= 32 ? 0 : 1;
             brows[bk].push_back(A);
             c->tb[bk].max_inc = std::max(c->tb[bk].max_inc, ni);
+            c->tb[bk].max_blk = std::max(c->tb[bk].max_blk,
+                                         c->row_ptr_h[size_t(A) + 1] - c->row_ptr_h[size_t(A)]);
         }
         for (int bk = 0; bk < 2; ++bk) {
             c->tb[bk].count = int(brows[bk].size());
@@ -616,8 +621,13 @@ static int tangent_dev(hbgpu_ctx* c, const double* d_state) {
             continue;
         a.rows = b.rows.p;
         a.max_inc = b.max_inc;
+        a.max_blk = b.max_blk;
         a.NT = b.nt;
+#if TAN_V4
+        launch_tangent_row4(a, b.count, b.smem, c->stream);
+#else
         launch_tangent_row(a, b.count, b.smem, c->stream);
+#endif
     }
     if (c->backflow_tangent && c->nbnodes > 0)
         launch_backflow_tangent(boundary_args(c, d_state, nullptr), c->row_ptr.p, c->col_idx.p,
@@ -986,7 +996,10 @@ hbgpu_ctx* hbgpu_create(const hbgpu_mesh_desc* d, int* status) {
         }
         c->h_c = std::cbrt(6.0 * std::sqrt(2.0) * (total / double(c->ne)));
     }
-    if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess) {
+    if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&c->stream2, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming) != cudaSuccess) {
         set(HBGPU_ERR_CUDA, "cudaStreamCreate failed");
         delete c;
         return nullptr;
@@ -1031,6 +1044,12 @@ void hbgpu_destroy(hbgpu_ctx* c) {
     c->slot_idx.release();
     for (cudaEvent_t e : c->ev_pool)
         cudaEventDestroy(e);
+    if (c->ev_fork)
+        cudaEventDestroy(c->ev_fork);
+    if (c->ev_join)
+        cudaEventDestroy(c->ev_join);
+    if (c->stream2)
+        cudaStreamDestroy(c->stream2);
     if (c->stream)
         cudaStreamDestroy(c->stream);
     delete c;
@@ -1107,17 +1126,27 @@ int hbgpu_set_basis(hbgpu_ctx* c, int modes, double period) {
         for (auto& b : c->tb) {
             if (!b.count)
                 continue;
-            const int dp = (b.max_inc + kTanPart - 1) / kTanPart;
             int nt = N;
-            while (nt > 1 && tangent_row_smem(b.max_inc, dp, nt) > 64 * 1024)
+#if TAN_V4
+            while (nt > 1 && tangent_row4_smem(b.max_inc, b.max_blk, nt) > TAN_SMEM_KB * 1024)
                 nt = (nt + 1) / 2;
-            b.nt = nt;
+            b.smem = tangent_row4_smem(b.max_inc, b.max_blk, nt);
+#else
+            const int dp = (b.max_inc + kTanPart - 1) / kTanPart;
+            while (nt > 1 && tangent_row_smem(b.max_inc, dp, nt) > TAN_SMEM_KB * 1024)
+                nt = (nt + 1) / 2;
             b.smem = tangent_row_smem(b.max_inc, dp, nt);
+#endif
+            b.nt = nt;
             mx = std::max(mx, b.smem);
         }
         if (mx > 227 * 1024)
             return fail(c, HBGPU_ERR_INVALID, "node valence too high for the tangent row kernel");
+#if TAN_V4
+        CK(c, configure_tangent_row4_smem(mx));
+#else
         CK(c, configure_tangent_row_smem(mx));
+#endif
     }
     // clear previous Neumann data sized for another N
     c->hN.release();
@@ -1259,6 +1288,27 @@ int hbgpu_assemble_residual(hbgpu_ctx* c, const double* state, double* residual)
     CK(c, cudaMemcpyAsync(residual, c->r.p, sizeof(double) * n, cudaMemcpyDeviceToHost, c->stream));
     CK(c, cudaStreamSynchronize(c->stream));
     return check_flag(c);
+}
+
+// Residual and tangent of the same state, the tangent on the second stream so
+// the two latency-bound kernels share the SMs; ordered on ctx->stream after.
+static int assemble_both(hbgpu_ctx* c, const double* d_state, double* d_r) {
+    CK(c, cudaEventRecord(c->ev_fork, c->stream));
+    CK(c, cudaStreamWaitEvent(c->stream2, c->ev_fork, 0));
+    cudaStream_t main = c->stream;
+    c->stream = c->stream2;
+    const int st = tangent_dev(c, d_state);
+    c->stream = main;
+    TRY(st);
+    TRY(residual_dev(c, d_state, d_r));
+    CK(c, cudaEventRecord(c->ev_join, c->stream2));
+    CK(c, cudaStreamWaitEvent(c->stream, c->ev_join, 0));
+    return HBGPU_OK;
+}
+
+int hbgpu_assemble_dev(hbgpu_ctx* c, const double* d_state, double* d_residual) {
+    TRY(ensure_basis(c));
+    return assemble_both(c, d_state, d_residual);
 }
 
 int hbgpu_assemble_tangent_dev(hbgpu_ctx* c, const double* d_state) {
@@ -1514,7 +1564,9 @@ int hbgpu_solve_harmonic(hbgpu_ctx* c, const hbgpu_solver_cfg* cfg, double* stat
     for (int iter = 0; iter <= cfg->max_newton_iters; ++iter) {
         Timer t_iter;
         Timer t0;
-        int s = residual_dev(c, c->state.p, c->r.p);
+        // residual and (speculatively) the tangent of this iterate, concurrently;
+        // the tangent is unused only on the final iteration
+        int s = assemble_both(c, c->state.p, c->r.p);
         if (s != HBGPU_OK)
             return finish(s);
         double res = 0.0;
@@ -1547,13 +1599,6 @@ int hbgpu_solve_harmonic(hbgpu_ctx* c, const hbgpu_solver_cfg* cfg, double* stat
             log(iter, res, rel, 0, t_iter.seconds());
             break;
         }
-        Timer t1;
-        s = tangent_dev(c, c->state.p);
-        if (s == HBGPU_OK)
-            s = check_flag(c);
-        if (s != HBGPU_OK)
-            return finish(s);
-        inf.assembly_seconds += t1.seconds();
         Timer t2;
         s = jacobi_dev(c, nullptr);
         hbgpu_krylov_result kr{};

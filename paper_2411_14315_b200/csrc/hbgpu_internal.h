@@ -39,6 +39,12 @@ constexpr int kTanPart = 8;
 #ifndef TAN_MINB
 #define TAN_MINB 6
 #endif
+#ifndef TAN_V4
+#define TAN_V4 0
+#endif
+#ifndef TAN_SMEM_KB
+#define TAN_SMEM_KB 64
+#endif
 #ifndef MV_UNROLL
 #define MV_UNROLL 2
 #endif
@@ -91,6 +97,7 @@ struct TangentArgs {
     int max_inc;
     int NT;            // time samples per CTA (tile of N)
     const int* rows;   // block rows of this launch (one valence bucket)
+    int max_blk;       // longest block row of the bucket
 };
 
 struct MatvecArgs {
@@ -148,6 +155,9 @@ void launch_tangent_geometry(const double* geom, int ne, double* tg, cudaStream_
 size_t tangent_row_smem(int max_inc, int max_dparts, int N);
 cudaError_t configure_tangent_row_smem(size_t bytes);
 void launch_tangent_row(const TangentArgs& a, int nrows, size_t smem, cudaStream_t st);
+size_t tangent_row4_smem(int max_inc, int max_blk, int NT);
+cudaError_t configure_tangent_row4_smem(size_t bytes);
+void launch_tangent_row4(const TangentArgs& a, int nrows, size_t smem, cudaStream_t st);
 void launch_backflow_tangent(const BoundaryArgs& a, const int* row_ptr, const int* col_idx,
                              double* pvals, cudaStream_t st);
 void launch_matvec(const MatvecArgs& a, cudaStream_t st);

@@ -419,6 +419,240 @@ __global__ void __launch_bounds__(kTanThreads, TAN_MINB) tangent_row_kernel(Tang
     }
 }
 
+// Tangent v4 = v3 with a staging phase: before any FP64 work the CTA pulls
+// everything its row needs into shared memory with cp.async — the velocities
+// of the row's column nodes (the only nodes its elements touch), the compact
+// geometry and the records of its elements — so phases 1 and 2 run on
+// shared-memory operands only and the global latency is paid once per row,
+// in bulk, overlapped with the other resident rows.
+namespace {
+__device__ __forceinline__ void cpa8(double* dst, const double* src) {
+    const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(src));
+}
+__device__ __forceinline__ void cpa16(void* dst, const void* src) {
+    const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(src));
+}
+__device__ __forceinline__ void cpa_wait_all() {
+    asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::);
+}
+}  // namespace
+
+template <int TAU>
+__global__ void __launch_bounds__(kTanThreads, TAN_MINB) tangent_row4_kernel(TangentArgs a) {
+    extern __shared__ __align__(16) double sm[];
+    const int N = a.N;
+    const int A = a.rows[blockIdx.x];
+    const int NT = a.NT, n0 = blockIdx.y * NT, nt = min(NT, N - n0);
+    const int i0 = a.inc_ptr[A], ninc = a.inc_ptr[A + 1] - i0;
+    const int k0 = a.row_ptr[A], nblk = a.row_ptr[A + 1] - k0;
+    double* summ = sm;                                    // [i][8][t]
+    double* geo = summ + (size_t)a.max_inc * 8 * NT;      // [i][kTGeo]
+    double* dpart = geo + (size_t)a.max_inc * kTGeo;      // [part][8][t]
+    double* us = dpart + (size_t)((a.max_inc + kTanPart - 1) / kTanPart) * 8 * NT;  // [j][3][t]
+    int4* rec = reinterpret_cast<int4*>(us + ((size_t)a.max_blk * 3 * NT + 1) / 2 * 2);  // [i]
+
+    // ---- phase 0: stage records, geometry and column-node velocities
+    for (int i = threadIdx.x; i < ninc; i += blockDim.x) {
+        const int4 r1 = __ldg(a.inc_rec + 2 * (i0 + i) + 1);
+        rec[i] = r1;
+        const double* g = a.tgeom + (long)kTGeo * (r1.x & 0x3FFFFFFF);
+#pragma unroll
+        for (int k = 0; k < kTGeo / 2; ++k)
+            cpa16(geo + i * kTGeo + 2 * k, g + 2 * k);
+    }
+    for (int it = threadIdx.x; it < nblk * 3 * nt; it += blockDim.x) {
+        const int j = it / (3 * nt), rem = it - j * 3 * nt, c = rem / nt, t = rem - c * nt;
+        const long B = __ldg(a.col_idx + k0 + j);
+        cpa8(us + (j * 3 + c) * NT + t, a.state + (B * 4 + c) * N + n0 + t);
+    }
+    cpa_wait_all();
+    __syncthreads();
+
+    // ---- phase 1: element summaries per (incidence, sample)
+    const double rho = a.rho, diffc = 3.0 * a.nu * a.nu, dAB = kQA - kQB;
+    for (int it = threadIdx.x; it < ninc * nt; it += blockDim.x) {
+        const int i = it / nt, t = it - i * nt;
+        const int4 r1 = rec[i];
+        const int la = (unsigned)r1.x >> 30;
+        const unsigned cols = (unsigned)r1.y;
+        const double* g = geo + i * kTGeo;
+        double u[4][3], usum[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+            const double* ub = us + ((cols >> (8 * b)) & 0xFF) * 3 * NT + t;
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                u[b][c] = ub[c * NT];
+                usum[c] += u[b][c];
+            }
+        }
+        const double V = g[12], w = 0.25 * V, diff = diffc * g[19];
+        const double ga[3] = {g[3 * la], g[3 * la + 1], g[3 * la + 2]};
+        auto quad = [&](const double v[3]) {
+            return g[13] * v[0] * v[0] + g[16] * v[1] * v[1] + g[18] * v[2] * v[2] +
+                   2.0 * (g[14] * v[0] * v[1] + g[15] * v[0] * v[2] + g[17] * v[1] * v[2]);
+        };
+        double tau_mean = 0.0;
+        if (TAU == 1) {
+            const double um[3] = {0.25 * usum[0], 0.25 * usum[1], 0.25 * usum[2]};
+            const double arg = quad(um) + diff;
+            if (!(arg > 0.0))
+                atomicOr(a.flag, 1);
+            tau_mean = arg > 0.0 ? rsqrt(arg) : 0.0;
+        }
+        double asum = 0.0, tsum = 0.0, z[3] = {0.0, 0.0, 0.0}, kap[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            double uq[3];
+#pragma unroll
+            for (int c = 0; c < 3; ++c)
+                uq[c] = kQB * usum[c] + dAB * u[q][c];
+            double tq = tau_mean;
+            if (TAU == 0) {
+                const double arg = quad(uq) + diff;
+                if (!(arg > 0.0))
+                    atomicOr(a.flag, 1);
+                tq = arg > 0.0 ? rsqrt(arg) : 0.0;
+            }
+            const double tadv = tq * (uq[0] * ga[0] + uq[1] * ga[1] + uq[2] * ga[2]);
+            const double na = (q == la) ? kQA : kQB;
+            asum += tadv;
+            tsum += tq;
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                z[c] += tq * uq[c];
+                kap[c] += (na + tadv) * uq[c];
+            }
+        }
+        double* s = summ + (size_t)i * 8 * NT + t;
+        const double wr = w * rho;
+        s[0] = wr * kap[0];
+        s[NT] = wr * kap[1];
+        s[2 * NT] = wr * kap[2];
+        s[3 * NT] = w * asum;
+        s[4 * NT] = w * z[0];
+        s[5 * NT] = w * z[1];
+        s[6 * NT] = w * z[2];
+        s[7 * NT] = (w / rho) * tsum;
+    }
+    __syncthreads();
+
+    // ---- phase 2: blocks accumulate their contributions in element order
+    const bool afix = a.dir[A] != 0;
+    const int kdiag = a.diag_blk[A] - k0;
+    const int ndiag = a.contrib_ptr[k0 + kdiag + 1] - a.contrib_ptr[k0 + kdiag];
+    const int dparts = (ndiag + kTanPart - 1) / kTanPart;
+    const int nitems = (nblk - 1 + dparts) * nt;
+    const double muc = a.mu, pcc = a.pseudo_c;
+    for (int it = threadIdx.x; it < nitems; it += blockDim.x) {
+        const int slot = it / nt, t = it - slot * nt, n = n0 + t;
+        int j, c0, c1, part = -1;
+        if (slot < nblk - 1) {
+            j = slot < kdiag ? slot : slot + 1;
+            c0 = a.contrib_ptr[k0 + j];
+            c1 = a.contrib_ptr[k0 + j + 1];
+        } else {
+            j = kdiag;
+            part = slot - (nblk - 1);
+            c0 = a.contrib_ptr[k0 + j] + part * kTanPart;
+            c1 = min(c0 + kTanPart, a.contrib_ptr[k0 + j + 1]);
+        }
+        const bool bfix = a.dir[a.col_idx[k0 + j]] != 0;
+        double K = 0.0, G0 = 0.0, G1 = 0.0, G2 = 0.0, D0 = 0.0, D1 = 0.0, D2 = 0.0, L = 0.0;
+        for (int q = c0; q < c1; ++q) {
+            const int ent = a.contrib[q];
+            const int i = ent >> 2, b = ent & 3;
+            const double* gi = geo + i * kTGeo;
+            const int la = (unsigned)rec[i].x >> 30;
+            const double ga0 = gi[3 * la], ga1 = gi[3 * la + 1], ga2 = gi[3 * la + 2];
+            const double gb0 = gi[3 * b], gb1 = gi[3 * b + 1], gb2 = gi[3 * b + 2];
+            const double V = gi[12], w = 0.25 * V;
+            const double* s = summ + (size_t)i * 8 * NT + t;
+            const double gg = ga0 * gb0 + ga1 * gb1 + ga2 * gb2;
+            K += muc * V * gg + pcc * V * (b == la ? 0.1 : 0.05) +
+                 (s[0] * gb0 + s[NT] * gb1 + s[2 * NT] * gb2);
+            const double al = s[3 * NT];
+            G0 += -ga0 * w + al * gb0;
+            G1 += -ga1 * w + al * gb1;
+            G2 += -ga2 * w + al * gb2;
+            const double alb = s[4 * NT] * gb0 + s[5 * NT] * gb1 + s[6 * NT] * gb2;
+            D0 += gb0 * w + ga0 * alb;
+            D1 += gb1 * w + ga1 * alb;
+            D2 += gb2 * w + ga2 * alb;
+            L += gg * s[7 * NT];
+        }
+        if (afix || bfix)
+            K = 0.0;
+        if (afix)
+            G0 = G1 = G2 = 0.0;
+        if (bfix)
+            D0 = D1 = D2 = 0.0;
+        double* o;
+        long st;
+        if (part < 0) {
+            o = a.pvals + ((long)(k0 + j) * 8) * N + n;
+            st = N;
+            __stcs(o, K);
+            __stcs(o + st, G0);
+            __stcs(o + 2 * st, G1);
+            __stcs(o + 3 * st, G2);
+            __stcs(o + 4 * st, D0);
+            __stcs(o + 5 * st, D1);
+            __stcs(o + 6 * st, D2);
+            __stcs(o + 7 * st, L);
+        } else {
+            o = dpart + (size_t)part * 8 * NT + t;
+            o[0] = K;
+            o[NT] = G0;
+            o[2 * NT] = G1;
+            o[3 * NT] = G2;
+            o[4 * NT] = D0;
+            o[5 * NT] = D1;
+            o[6 * NT] = D2;
+            o[7 * NT] = L;
+        }
+    }
+    __syncthreads();
+    for (int it = threadIdx.x; it < 8 * nt; it += blockDim.x) {
+        const int sl = it / nt, t = it - sl * nt, n = n0 + t;
+        double v = 0.0;
+        for (int p = 0; p < dparts; ++p)
+            v += dpart[((size_t)p * 8 + sl) * NT + t];
+        if (sl == 0 && afix)
+            v = 1.0;  // identity on constrained velocity diagonals (assembly.cpp:659-665)
+        __stcs(a.pvals + ((long)(k0 + kdiag) * 8 + sl) * N + n, v);
+    }
+}
+
+size_t tangent_row4_smem(int max_inc, int max_blk, int NT) {
+    const int dparts = (max_inc + kTanPart - 1) / kTanPart;
+    return sizeof(double) * ((size_t)max_inc * 8 * NT + (size_t)max_inc * kTGeo +
+                             (size_t)dparts * 8 * NT + ((size_t)max_blk * 3 * NT + 1) / 2 * 2) +
+           sizeof(int4) * (size_t)max_inc;
+}
+
+cudaError_t configure_tangent_row4_smem(size_t bytes) {
+    const int b = int(bytes < 48 * 1024 ? 48 * 1024 : bytes);
+    cudaError_t e = cudaFuncSetAttribute(tangent_row4_kernel<0>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, b);
+    if (e != cudaSuccess)
+        return e;
+    return cudaFuncSetAttribute(tangent_row4_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, b);
+}
+
+void launch_tangent_row4(const TangentArgs& a, int nrows, size_t smem, cudaStream_t st) {
+    if (nrows <= 0)
+        return;
+    note_launch();
+    const dim3 grid(nrows, (a.N + a.NT - 1) / a.NT);
+    if (a.tau_mode == 1)
+        tangent_row4_kernel<1><<<grid, kTanThreads, smem, st>>>(a);
+    else
+        tangent_row4_kernel<0><<<grid, kTanThreads, smem, st>>>(a);
+}
+
 size_t tangent_row_smem(int max_inc, int max_dparts, int N) {
     return sizeof(double) * ((size_t)max_inc * 8 * N + (size_t)max_inc * 16 + (size_t)max_dparts * 8 * N);
 }

@@ -149,6 +149,7 @@ _jacobi = _sig("hbgpu_jacobi", C.c_int, [_vp, _vp, _ip])
 _gmres = _sig("hbgpu_gmres", C.c_int, [_vp, _vp, _vp, C.POINTER(_KrylovCfg), _vp, C.POINTER(_KrylovRes), _vp, C.c_int])
 _residual_dev = _sig("hbgpu_assemble_residual_dev", C.c_int, [_vp, _vp, _vp])
 _tangent_dev = _sig("hbgpu_assemble_tangent_dev", C.c_int, [_vp, _vp])
+_assemble_dev = _sig("hbgpu_assemble_dev", C.c_int, [_vp, _vp, _vp])
 _matvec_dev = _sig("hbgpu_matvec_dev", C.c_int, [_vp, _vp, _vp])
 _bsr_matvec_dev = _sig("hbgpu_bsr_matvec_dev", C.c_int, [_vp, _vp, _vp])
 _jacobi_dev = _sig("hbgpu_jacobi_dev", C.c_int, [_vp, _ip])
@@ -413,6 +414,10 @@ class GpuContext:
 
     def assemble_tangent_dev(self, d_state: int):
         self._check(_tangent_dev(self._h, d_state))
+
+    def assemble_dev(self, d_state: int, d_r: int):
+        """Residual + tangent of one iterate (concurrent on two streams)."""
+        self._check(_assemble_dev(self._h, d_state, d_r))
 
     def matvec_dev(self, d_y: int, d_out: int):
         self._check(_matvec_dev(self._h, d_y, d_out))
