@@ -102,6 +102,7 @@ struct hbgpu_ctx {
     DBuf<uint32_t> lconn;
     DBuf<int> chunk_node_ptr, chunk_nodes, slot_ptr, npart_ptr, npart;
     DBuf<uint8_t> slot_idx;
+    DBuf<uint16_t> slot_off;
     DBuf<double> rpartial;
 
     // tangent CTA plan (depends on N)
@@ -461,6 +462,17 @@ static int upload_all(hbgpu_ctx* c, const hbgpu_mesh_desc* d) {
     CK(c, cudaMemcpyAsync(c->chunk_nodes.p, cnodes.data(), sizeof(int) * cnodes.size(), cudaMemcpyHostToDevice, st));
     CK(c, cudaMemcpyAsync(c->slot_ptr.p, sptr.data(), sizeof(int) * sptr.size(), cudaMemcpyHostToDevice, st));
     CK(c, cudaMemcpyAsync(c->slot_idx.p, sidx.data(), sidx.size(), cudaMemcpyHostToDevice, st));
+    {
+        // the same slots as shared-memory offsets of the residual kernel's slot
+        // array: element stride 29T (bank padding), output-group stride 7T
+        std::vector<uint16_t> soff(sidx.size());
+        for (size_t q = 0; q < sidx.size(); ++q)
+            soff[q] = uint16_t((sidx[q] >> 2) * 29 * kResTile + (sidx[q] & 3) * 7 * kResTile);
+        CK(c, c->slot_off.alloc(soff.size()));
+        CK(c, cudaMemcpyAsync(c->slot_off.p, soff.data(), sizeof(uint16_t) * soff.size(),
+                              cudaMemcpyHostToDevice, st));
+        CK(c, cudaStreamSynchronize(st));
+    }
     CK(c, cudaMemcpyAsync(c->npart_ptr.p, npp.data(), sizeof(int) * npp.size(), cudaMemcpyHostToDevice, st));
     CK(c, cudaMemcpyAsync(c->npart.p, npl.data(), sizeof(int) * npl.size(), cudaMemcpyHostToDevice, st));
     CK(c, cudaStreamSynchronize(st));
@@ -529,6 +541,7 @@ static int residual_dev(hbgpu_ctx* c, const double* d_state, double* d_r) {
     ca.chunk_nodes = c->chunk_nodes.p;
     ca.slot_ptr = c->slot_ptr.p;
     ca.slot_idx = c->slot_idx.p;
+    ca.slot_off = c->slot_off.p;
     ca.partial = c->rpartial.p;
     ca.ne = c->ne;
     ca.N = N;
@@ -1042,6 +1055,7 @@ void hbgpu_destroy(hbgpu_ctx* c) {
     c->tgeom.release();
     c->lconn.release();
     c->slot_idx.release();
+    c->slot_off.release();
     for (cudaEvent_t e : c->ev_pool)
         cudaEventDestroy(e);
     if (c->ev_fork)

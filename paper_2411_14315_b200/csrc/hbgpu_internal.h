@@ -67,6 +67,7 @@ struct ResidualChunkArgs {
     const int* chunk_nodes;      // global node id per (chunk, node) pair
     const int* slot_ptr;         // per pair: range in slot_idx
     const uint8_t* slot_idx;     // el_local*4 + a, element order
+    const uint16_t* slot_off;    // same slots as shared-memory offsets el*29T + a*7T
     double* partial;             // pairs * 7N
     int ne, N, T, CE, max_nloc, nchunks;
     long npairs;

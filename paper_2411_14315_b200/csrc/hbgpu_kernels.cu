@@ -398,16 +398,22 @@ __global__ void __launch_bounds__(256, RES_MINB) residual_chunk_kernel(ResidualC
         }
         __syncthreads();
         double* out = a.partial + ((long)tile * a.npairs + nb) * ndst;
-        for (int k = threadIdx.x; k < nloc * ndst; k += blockDim.x) {
-            const int ln = k / ndst, rem = k - ln * ndst;
-            const int cc = rem / T, t = rem - cc * T;
+        // thread per (chunk node, sample): walk the node's slot offsets once,
+        // accumulating all 7 outputs
+        for (int k = threadIdx.x; k < nloc * T; k += blockDim.x) {
+            const int ln = k / T, t = k - ln * T;
             const int p = nb + ln;
-            double acc = 0.0;
-            for (int q = a.slot_ptr[p]; q < a.slot_ptr[p + 1]; ++q) {
-                const int sl = a.slot_idx[q];  // el*4 + a
-                acc += slots[(sl >> 2) * es + ((sl & 3) * 7 + cc) * T + t];
+            double acc[7] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+            const int q1 = a.slot_ptr[p + 1];
+            for (int q = a.slot_ptr[p]; q < q1; ++q) {
+                const double* sp = slots + a.slot_off[q] + t;  // el*es + a*7T
+#pragma unroll
+                for (int cc = 0; cc < 7; ++cc)
+                    acc[cc] += sp[cc * T];
             }
-            out[k] = acc;
+#pragma unroll
+            for (int cc = 0; cc < 7; ++cc)
+                out[(ln * 7 + cc) * T + t] = acc[cc];
         }
     }
     cp_async_wait<0>();
