@@ -95,7 +95,39 @@ __global__ void __launch_bounds__(kRedThreads) dcgs_dots_kernel(const double* __
     chunk_of(n, lo, hi);
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
     const bool hw = w != nullptr;
-    for (int r = wid; r <= nv; r += nw) {
+    // tasks: groups of four basis vectors (u and w read once per group), then
+    // the three scalar products
+    const int ngroups = (nv + 3) / 4;
+    for (int task = wid; task < ngroups; task += nw) {
+        const int r0 = 4 * task, nr = min(4, nv - r0);
+        double du[4] = {0.0, 0.0, 0.0, 0.0}, dw[4] = {0.0, 0.0, 0.0, 0.0};
+        for (long k = lo + lane; k < hi; k += 32) {
+            const double uk = u[k];
+            const double wk = hw ? w[k] : 0.0;
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+                if (q < nr) {
+                    const double x = V[(long)(r0 + q) * ld + k];
+                    du[q] += x * uk;
+                    dw[q] += x * wk;
+                }
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                du[q] += __shfl_down_sync(0xffffffffu, du[q], o);
+                dw[q] += __shfl_down_sync(0xffffffffu, dw[q], o);
+            }
+            if (lane == 0 && q < nr) {
+                partial[(long)(r0 + q) * kRedBlocks + blockIdx.x] = du[q];
+                if (hw)
+                    partial[(long)(nv + r0 + q) * kRedBlocks + blockIdx.x] = dw[q];
+            }
+        }
+    }
+    if (wid == (ngroups % nw)) {  // the scalar task goes to the least loaded warp
+        const int r = nv;
         double du0 = 0.0, du1 = 0.0, dw0 = 0.0, dw1 = 0.0, dx0 = 0.0, dx1 = 0.0;
         if (r < nv) {
             const double* x = V + (long)r * ld;
@@ -179,6 +211,18 @@ __global__ void __launch_bounds__(kRedThreads) dcgs_update_kernel(const double* 
          k += (long)gridDim.x * blockDim.x) {
         double sa0 = 0.0, sa1 = 0.0, sd0 = 0.0, sd1 = 0.0;
         int i = 0;
+        for (; i + 3 < nv; i += 4) {
+            const double v0 = __ldcs(V + (long)i * ld + k), v1 = __ldcs(V + (long)(i + 1) * ld + k);
+            const double v2 = __ldcs(V + (long)(i + 2) * ld + k), v3 = __ldcs(V + (long)(i + 3) * ld + k);
+            sa0 += ca[i] * v0;
+            sa1 += ca[i + 1] * v1;
+            sd0 += cd[i] * v0;
+            sd1 += cd[i + 1] * v1;
+            sa0 += ca[i + 2] * v2;
+            sa1 += ca[i + 3] * v3;
+            sd0 += cd[i + 2] * v2;
+            sd1 += cd[i + 3] * v3;
+        }
         for (; i + 1 < nv; i += 2) {
             const double v0 = __ldcs(V + (long)i * ld + k), v1 = __ldcs(V + (long)(i + 1) * ld + k);
             sa0 += ca[i] * v0;
