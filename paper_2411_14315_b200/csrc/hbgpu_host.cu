@@ -105,11 +105,6 @@ struct hbgpu_ctx {
     DBuf<uint16_t> slot_off;
     DBuf<double> rpartial;
 
-    // tangent CTA plan (depends on N)
-    std::vector<int> tcta_h;
-    DBuf<int> tcta;
-    size_t tsmem = 0;
-    int tthreads = 0;
 
     // spectral + BCs
     DBuf<double> H;
@@ -483,41 +478,6 @@ static int upload_all(hbgpu_ctx* c, const hbgpu_mesh_desc* d) {
     return HBGPU_OK;
 }
 
-// Tangent CTA plan: consecutive block rows per CTA such that the rows' P
-// segment fits the shared-memory budget and rows*N <= 256 threads.
-static int plan_tangent(hbgpu_ctx* c) {
-    const int N = c->N;
-    const size_t row_bytes_per_blk = sizeof(double) * 8 * size_t(N);
-    const size_t budget = 112 * 1024;  // two CTAs per SM
-    const int max_rows = std::max(1, 256 / N);
-    c->tcta_h.clear();
-    c->tcta_h.push_back(0);
-    // fixed rows per CTA (every thread busy); the largest CTA sets the smem size
-    int rows = std::max(1, std::min(max_rows, 128 / N));
-    size_t maxsmem = 0;
-    for (;;) {
-        maxsmem = 0;
-        c->tcta_h.assign(1, 0);
-        for (int A = 0; A < c->nn; A += rows) {
-            const int B = std::min(c->nn, A + rows);
-            maxsmem = std::max(maxsmem, size_t(c->row_ptr_h[size_t(B)] - c->row_ptr_h[size_t(A)]) *
-                                            row_bytes_per_blk);
-            c->tcta_h.push_back(B);
-        }
-        if (maxsmem <= budget || rows == 1)
-            break;
-        rows -= 1;
-    }
-    if (maxsmem > 227 * 1024)
-        return fail(c, HBGPU_ERR_INVALID, "a block row exceeds the shared-memory budget");
-    c->tsmem = maxsmem;
-    c->tthreads = ((rows * N + 31) / 32) * 32;
-    CK(c, c->tcta.alloc(c->tcta_h.size()));
-    CK(c, cudaMemcpyAsync(c->tcta.p, c->tcta_h.data(), sizeof(int) * c->tcta_h.size(),
-                          cudaMemcpyHostToDevice, c->stream));
-    return HBGPU_OK;
-}
-
 static int rows_per_matvec_cta(int N) { return std::max(1, 256 / N); }
 
 // ---------------------------------------------------------------- operations
@@ -614,7 +574,6 @@ static int tangent_dev(hbgpu_ctx* c, const double* d_state) {
     a.row_ptr = c->row_ptr.p;
     a.inc_ptr = c->inc_ptr.p;
     a.inc_rec = c->inc_rec.p;
-    a.cta_rows = c->tcta.p;
     a.pvals = c->pvals.p;
     a.N = c->N;
     a.rho = c->rho;
@@ -636,11 +595,7 @@ static int tangent_dev(hbgpu_ctx* c, const double* d_state) {
         a.max_inc = b.max_inc;
         a.max_blk = b.max_blk;
         a.NT = b.nt;
-#if TAN_V4
-        launch_tangent_row4(a, b.count, b.smem, c->stream);
-#else
         launch_tangent_row(a, b.count, b.smem, c->stream);
-#endif
     }
     if (c->backflow_tangent && c->nbnodes > 0)
         launch_backflow_tangent(boundary_args(c, d_state, nullptr), c->row_ptr.p, c->col_idx.p,
@@ -1042,7 +997,7 @@ void hbgpu_destroy(hbgpu_ctx* c) {
                             &c->x, &c->w, &c->z, &c->scale, &c->b, &c->tmp, &c->V, &c->partial, &c->red, &c->rpartial})
         b->release();
     for (DBuf<int>* b : {&c->row_ptr, &c->col_idx, &c->diag_blk, &c->inc_ptr, &c->chunk_node_ptr, &c->chunk_nodes, &c->slot_ptr, &c->npart_ptr, &c->npart,
-                         &c->tcta, &c->bnode, &c->bptr, &c->binc, &c->fac, &c->fbc, &c->flag,
+                         &c->bnode, &c->bptr, &c->binc, &c->fac, &c->fbc, &c->flag,
                          &c->ideg})
         b->release();
     c->conn.release();
@@ -1132,8 +1087,6 @@ int hbgpu_set_basis(hbgpu_ctx* c, int modes, double period) {
     c->V_vecs = 0;
     c->p_valid = c->inv_valid = false;
     c->mass_valid = false;
-    TRY(plan_tangent(c));
-    CK(c, configure_tangent_smem(c->tsmem));
     {
         // per bucket: largest time-sample tile whose row summaries fit 64 KB (3 CTAs / SM)
         size_t mx = 0;
@@ -1141,26 +1094,16 @@ int hbgpu_set_basis(hbgpu_ctx* c, int modes, double period) {
             if (!b.count)
                 continue;
             int nt = N;
-#if TAN_V4
-            while (nt > 1 && tangent_row4_smem(b.max_inc, b.max_blk, nt) > TAN_SMEM_KB * 1024)
-                nt = (nt + 1) / 2;
-            b.smem = tangent_row4_smem(b.max_inc, b.max_blk, nt);
-#else
             const int dp = (b.max_inc + kTanPart - 1) / kTanPart;
             while (nt > 1 && tangent_row_smem(b.max_inc, dp, nt) > TAN_SMEM_KB * 1024)
                 nt = (nt + 1) / 2;
             b.smem = tangent_row_smem(b.max_inc, dp, nt);
-#endif
             b.nt = nt;
             mx = std::max(mx, b.smem);
         }
         if (mx > 227 * 1024)
             return fail(c, HBGPU_ERR_INVALID, "node valence too high for the tangent row kernel");
-#if TAN_V4
-        CK(c, configure_tangent_row4_smem(mx));
-#else
         CK(c, configure_tangent_row_smem(mx));
-#endif
     }
     // clear previous Neumann data sized for another N
     c->hN.release();

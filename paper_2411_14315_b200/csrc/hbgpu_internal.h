@@ -39,9 +39,6 @@ constexpr int kTanPart = 8;
 #ifndef TAN_MINB
 #define TAN_MINB 6
 #endif
-#ifndef TAN_V4
-#define TAN_V4 0
-#endif
 #ifndef TAN_SMEM_KB
 #define TAN_SMEM_KB 64
 #endif
@@ -83,7 +80,6 @@ struct TangentArgs {
     const int* row_ptr;
     const int* inc_ptr;      // per node, into inc_rec
     const int4* inc_rec;     // 2 per incidence: conn[4]; {e | a<<30, cols(4 x u8), dirichlet mask, 0}
-    const int* cta_rows;     // row range per CTA
     double* pvals;
     int N;
     double rho, mu, nu, pseudo_c;
@@ -147,21 +143,14 @@ void launch_residual_nodes(const double* H, int N, int nn, const int* npart_ptr,
                            const double* partial, const uint8_t* dir, double* r, int T,
                            long npairs, cudaStream_t st);
 void launch_boundary(const BoundaryArgs& a, cudaStream_t st);
-cudaError_t configure_tangent_smem(size_t bytes);
-void launch_tangent_rows(const TangentArgs& a, int nctas, int threads, size_t smem,
-                         cudaStream_t st);
 void launch_mass_rows(const double* geom, const int* row_ptr, const int* inc_ptr, const int4* rec,
                       double rho, double* mass, int nn, cudaStream_t st);
 void launch_tangent_geometry(const double* geom, int ne, double* tg, cudaStream_t st);
 size_t tangent_row_smem(int max_inc, int max_dparts, int N);
 cudaError_t configure_tangent_row_smem(size_t bytes);
 void launch_tangent_row(const TangentArgs& a, int nrows, size_t smem, cudaStream_t st);
-size_t tangent_row4_smem(int max_inc, int max_blk, int NT);
-cudaError_t configure_tangent_row4_smem(size_t bytes);
-void launch_tangent_row4(const TangentArgs& a, int nrows, size_t smem, cudaStream_t st);
 void launch_backflow_tangent(const BoundaryArgs& a, const int* row_ptr, const int* col_idx,
                              double* pvals, cudaStream_t st);
-void launch_matvec(const MatvecArgs& a, cudaStream_t st);
 void launch_lmatvec(const MatvecArgs& a, cudaStream_t st);
 void launch_mask_mass(const double* mass, const int* row_ptr, const int* col_idx,
                       const uint8_t* dir, int nn, double* mass_c, cudaStream_t st);
@@ -178,22 +167,13 @@ void launch_sqrt_abs(const double* in, double* out, long n, cudaStream_t st);
 void launch_mul(const double* a, const double* b, double* out, long n, cudaStream_t st);
 void launch_scaled_diff(const double* s, const double* a, const double* b, double* out, long n,
                         cudaStream_t st);  // out = s*(a-b)
-void launch_scale_copy(const double* in, const double* alpha_dev, int inv, double* out, long n,
-                       cudaStream_t st);  // out = in * alpha or in / alpha
 // partial[i*kRedBlocks + b] = block b's share of <V_i, w>, i < nv.
 void launch_multidot(const double* V, long ld, int nv, const double* w, long n, double* partial,
                      cudaStream_t st);
 // out[i] = sum_b partial[i*kRedBlocks+b] (fixed order); optional sqrt of out[0]
 void launch_reduce_partials(const double* partial, int nv, double* out, int take_sqrt,
                             cudaStream_t st);
-// w -= sum_i h[i] V_i
-void launch_gemv_sub(const double* V, long ld, int nv, const double* h, double* w, long n,
-                     cudaStream_t st);
 // GMRES orthogonalisation passes (hbgpu_krylov.cu)
-void launch_orth_dots(const double* V, long ld, int nv, const double* w, long n, double* partial,
-                      cudaStream_t st);
-void launch_orth_update(const double* V, long ld, int nv, const double* h, double* w, long n,
-                        double* partial, cudaStream_t st);
 void launch_dcgs_dots(const double* V, long ld, int nv, const double* u, const double* w, long n,
                       double* partial, cudaStream_t st);
 void launch_dcgs_update(const double* V, long ld, int nv, const double* coef, double* u, double* w,
@@ -202,8 +182,5 @@ void launch_basis_combine(const double* V, long ld, int nv, const double* y, con
                           double* x, long n, cudaStream_t st);
 void launch_normalize(const double* in, const double* alpha, double* out, long n, cudaStream_t st,
                       const double* s = nullptr, double* z = nullptr);
-// x += s * sum_i y[i] V_i
-void launch_gemv_add_scaled(const double* V, long ld, int nv, const double* y, const double* s,
-                            double* x, long n, cudaStream_t st);
 
 }  // namespace hbgpu

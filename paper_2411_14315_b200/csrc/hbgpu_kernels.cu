@@ -12,7 +12,7 @@
 //
 // Every kernel is deterministic: no floating-point atomics, fixed reduction
 // trees, fixed summation order per output (element order for the tangent /
-// mass, colour order for the residual).
+// mass, (chunk, element, local index) order for the residual).
 #include "hbgpu_internal.h"
 
 namespace hbgpu {
@@ -20,55 +20,7 @@ namespace hbgpu {
 std::atomic<long long> g_launches{0};
 
 namespace {
-
 inline void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
-
-__device__ __forceinline__ double ldg(const double* p) { return __ldg(p); }
-
-struct Geo {
-    double gN[4][3];
-    double V;
-    double xi[9];
-};
-
-__device__ __forceinline__ void load_geo(const double* __restrict__ g, Geo& G) {
-#pragma unroll
-    for (int a = 0; a < 4; ++a)
-#pragma unroll
-        for (int j = 0; j < 3; ++j)
-            G.gN[a][j] = ldg(g + 3 * a + j);
-    G.V = ldg(g + 12);
-#pragma unroll
-    for (int k = 0; k < 9; ++k)
-        G.xi[k] = ldg(g + 13 + k);
-}
-
-// tau = (u.xi.u + 3 nu^2 xi:xi)^(-1/2)   (assembly.cpp:43-56).  A non-positive
-// argument is the reference's std::domain_error; flagged, tau set to 0.
-__device__ __forceinline__ double tau_of(const Geo& G, const double u[3], double diff,
-                                         int* flag) {
-    double conv = 0.0;
-#pragma unroll
-    for (int i = 0; i < 3; ++i) {
-        const double xu = G.xi[3 * i + 0] * u[0] + G.xi[3 * i + 1] * u[1] + G.xi[3 * i + 2] * u[2];
-        conv += u[i] * xu;
-    }
-    const double arg = conv + diff;
-    if (!(arg > 0.0)) {
-        atomicOr(flag, 1);
-        return 0.0;
-    }
-    return rsqrt(arg);
-}
-
-__device__ __forceinline__ double xi_dd(const Geo& G) {
-    double s = 0.0;
-#pragma unroll
-    for (int k = 0; k < 9; ++k)
-        s += G.xi[k] * G.xi[k];
-    return s;
-}
-
 }  // namespace
 
 // ---------------------------------------------------------------- geometry
@@ -560,103 +512,6 @@ void launch_boundary(const BoundaryArgs& a, cudaStream_t st) {
     boundary_kernel<<<(int)((threads + 255) / 256), 256, 0, st>>>(a);
 }
 
-// ---------------------------------------------------------------- operator
-
-// Fused L-matvec (linalg.cpp:78-128): out_A = sum_k P_k y_col(k)
-//   + [A free] H * sum_{k: col free} m_k y_col(k)[velocity].
-// Thread (row, n); the N threads of a row exchange the mass-gathered series
-// through shared memory for the dense H product.  Optional split scaling
-// (gmres_solve's S A S, linalg.cpp:214-219) is fused on load and store.
-__global__ void __launch_bounds__(256) matvec_kernel(MatvecArgs a) {
-    extern __shared__ double sh[];
-    const int N = a.N;
-    double* sH = sh;
-    double* st = sh + (a.with_c ? N * N : 0);
-    if (a.with_c)
-        for (int k = threadIdx.x; k < N * N; k += blockDim.x)
-            sH[k] = a.H[k];
-    const int r = threadIdx.x / N, n = threadIdx.x - r * N;
-    const int A = blockIdx.x * a.rows_per_cta + r;
-    const bool valid = (r < a.rows_per_cta) && (A < a.nn);
-    double ou0 = 0.0, ou1 = 0.0, ou2 = 0.0, op = 0.0, t0 = 0.0, t1 = 0.0, t2 = 0.0;
-    bool afree = false;
-    if (valid) {
-        afree = !a.dir[A];
-        const int kb = a.row_ptr[A], ke = a.row_ptr[A + 1];
-        for (int k = kb; k < ke; ++k) {
-            const int B = __ldg(&a.col_idx[k]);
-            const double* v = a.vals + (long)k * 8 * N + n;
-            const long yb = (long)B * 4 * N + n;
-            double y0 = ldg(a.y + yb), y1 = ldg(a.y + yb + N), y2 = ldg(a.y + yb + 2 * N),
-                   y3 = ldg(a.y + yb + 3 * N);
-            if (a.scale) {
-                y0 *= ldg(a.scale + yb);
-                y1 *= ldg(a.scale + yb + N);
-                y2 *= ldg(a.scale + yb + 2 * N);
-                y3 *= ldg(a.scale + yb + 3 * N);
-            }
-            const double kd = ldg(v);
-            ou0 += kd * y0 + ldg(v + 1 * N) * y3;
-            ou1 += kd * y1 + ldg(v + 2 * N) * y3;
-            ou2 += kd * y2 + ldg(v + 3 * N) * y3;
-            op += ldg(v + 4 * N) * y0;
-            op += ldg(v + 5 * N) * y1;
-            op += ldg(v + 6 * N) * y2;
-            op += ldg(v + 7 * N) * y3;
-            if (a.with_c && afree && !a.dir[B]) {
-                const double m = ldg(a.mass + k);
-                t0 += m * y0;
-                t1 += m * y1;
-                t2 += m * y2;
-            }
-        }
-    }
-    if (a.with_c) {
-        if (valid) {
-            st[(r * 3 + 0) * N + n] = t0;
-            st[(r * 3 + 1) * N + n] = t1;
-            st[(r * 3 + 2) * N + n] = t2;
-        }
-        __syncthreads();
-        if (valid && afree) {
-            const double* h = sH + n * N;
-            const double* s0 = st + (r * 3) * N;
-            double h0 = 0.0, h1 = 0.0, h2 = 0.0;
-            for (int m = 0; m < N; ++m) {
-                const double hm = h[m];
-                h0 += hm * s0[m];
-                h1 += hm * s0[N + m];
-                h2 += hm * s0[2 * N + m];
-            }
-            ou0 += h0;
-            ou1 += h1;
-            ou2 += h2;
-        }
-    }
-    if (valid) {
-        const long o = (long)A * 4 * N + n;
-        if (a.scale) {
-            ou0 *= ldg(a.scale + o);
-            ou1 *= ldg(a.scale + o + N);
-            ou2 *= ldg(a.scale + o + 2 * N);
-            op *= ldg(a.scale + o + 3 * N);
-        }
-        a.out[o] = ou0;
-        a.out[o + N] = ou1;
-        a.out[o + 2 * N] = ou2;
-        a.out[o + 3 * N] = op;
-    }
-}
-
-void launch_matvec(const MatvecArgs& a, cudaStream_t st) {
-    if (a.nn <= 0)
-        return;
-    const int blocks = (a.nn + a.rows_per_cta - 1) / a.rows_per_cta;
-    const size_t smem = a.with_c ? sizeof(double) * ((size_t)a.N * a.N + 3 * (size_t)a.N * a.rows_per_cta) : 0;
-    note_launch();
-    matvec_kernel<<<blocks, a.rows_per_cta * a.N, smem, st>>>(a);
-}
-
 // jacobi_preconditioner (linalg.cpp:130-154)
 __global__ void jacobi_kernel(const double* __restrict__ vals, const int* __restrict__ diag_blk,
                               int nn, int N, double* __restrict__ inv, int* degenerate) {
@@ -781,19 +636,6 @@ void launch_scaled_diff(const double* s, const double* a, const double* b, doubl
     scaled_diff_kernel<<<4 * 148, 256, 0, st>>>(s, a, b, out, n);
 }
 
-__global__ void scale_copy_kernel(const double* in, const double* alpha, int inv, double* out,
-                                  long n) {
-    const double al = *alpha;
-    for (long k = (long)blockIdx.x * blockDim.x + threadIdx.x; k < n;
-         k += (long)gridDim.x * blockDim.x)
-        out[k] = inv ? in[k] / al : in[k] * al;
-}
-void launch_scale_copy(const double* in, const double* alpha_dev, int inv, double* out, long n,
-                       cudaStream_t st) {
-    note_launch();
-    scale_copy_kernel<<<4 * 148, 256, 0, st>>>(in, alpha_dev, inv, out, n);
-}
-
 __device__ __forceinline__ double block_sum(double v, double* red) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1)
@@ -852,48 +694,6 @@ void launch_reduce_partials(const double* partial, int nv, double* out, int take
         return;
     note_launch();
     reduce_partials_kernel<<<nv, kRedThreads, 0, st>>>(partial, out, take_sqrt);
-}
-
-__global__ void gemv_sub_kernel(const double* __restrict__ V, long ld, int nv,
-                                const double* __restrict__ h, double* __restrict__ w, long n) {
-    extern __shared__ double sh[];
-    for (int i = threadIdx.x; i < nv; i += blockDim.x)
-        sh[i] = h[i];
-    __syncthreads();
-    for (long k = (long)blockIdx.x * blockDim.x + threadIdx.x; k < n;
-         k += (long)gridDim.x * blockDim.x) {
-        double acc = 0.0;
-        for (int i = 0; i < nv; ++i)
-            acc += sh[i] * V[(long)i * ld + k];
-        w[k] -= acc;
-    }
-}
-void launch_gemv_sub(const double* V, long ld, int nv, const double* h, double* w, long n,
-                     cudaStream_t st) {
-    note_launch();
-    gemv_sub_kernel<<<8 * 148, 256, sizeof(double) * (nv > 0 ? nv : 1), st>>>(V, ld, nv, h, w, n);
-}
-
-__global__ void gemv_add_scaled_kernel(const double* __restrict__ V, long ld, int nv,
-                                       const double* __restrict__ y, const double* __restrict__ s,
-                                       double* __restrict__ x, long n) {
-    extern __shared__ double sh[];
-    for (int i = threadIdx.x; i < nv; i += blockDim.x)
-        sh[i] = y[i];
-    __syncthreads();
-    for (long k = (long)blockIdx.x * blockDim.x + threadIdx.x; k < n;
-         k += (long)gridDim.x * blockDim.x) {
-        double acc = 0.0;
-        for (int i = 0; i < nv; ++i)
-            acc += sh[i] * V[(long)i * ld + k];
-        x[k] += s[k] * acc;
-    }
-}
-void launch_gemv_add_scaled(const double* V, long ld, int nv, const double* y, const double* s,
-                            double* x, long n, cudaStream_t st) {
-    note_launch();
-    gemv_add_scaled_kernel<<<8 * 148, 256, sizeof(double) * (nv > 0 ? nv : 1), st>>>(V, ld, nv, y,
-                                                                                   s, x, n);
 }
 
 // DFMA throughput probe: 8 independent FMA chains per thread, enough CTAs

@@ -10,8 +10,6 @@ namespace hbgpu {
 namespace {
 inline void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
-constexpr int kVB = 8;  // basis vectors per register block
-
 __device__ __forceinline__ void chunk_of(long n, long& lo, long& hi) {
     const long chunk = (n + kRedBlocks - 1) / kRedBlocks;
     lo = (long)blockIdx.x * chunk;
@@ -41,46 +39,6 @@ __device__ __forceinline__ void block_sum_vec(double (&v)[VB], double (*red)[VB]
     __syncthreads();
 }
 }  // namespace
-
-// partial[r*kRedBlocks + b] = block b's share of <V_r, w> for r < nv and of
-// <w, w> for r == nv (the Arnoldi projections plus the pre-projection norm in
-// one pass over V; eight basis vectors per register block).
-// Warp per basis vector: each warp streams one vector's chunk (coalesced,
-// four independent accumulators for memory-level parallelism), reduces by
-// shuffles, and writes its block partial; the w chunk is re-read from L1.
-__global__ void __launch_bounds__(kRedThreads) orth_dots_kernel(const double* __restrict__ V,
-                                                                long ld, int nv,
-                                                                const double* __restrict__ w,
-                                                                long n, double* partial) {
-    long lo, hi;
-    chunk_of(n, lo, hi);
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    for (int r = wid; r <= nv; r += nw) {
-        const double* v = r < nv ? V + (long)r * ld : w;
-        double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-        long k = lo + lane;
-        for (; k + 96 < hi; k += 128) {
-            a0 += v[k] * w[k];
-            a1 += v[k + 32] * w[k + 32];
-            a2 += v[k + 64] * w[k + 64];
-            a3 += v[k + 96] * w[k + 96];
-        }
-        for (; k < hi; k += 32)
-            a0 += v[k] * w[k];
-        double s = (a0 + a1) + (a2 + a3);
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1)
-            s += __shfl_down_sync(0xffffffffu, s, o);
-        if (lane == 0)
-            partial[(long)r * kRedBlocks + blockIdx.x] = s;
-    }
-}
-
-void launch_orth_dots(const double* V, long ld, int nv, const double* w, long n, double* partial,
-                      cudaStream_t st) {
-    note_launch();
-    orth_dots_kernel<<<kRedBlocks, kRedThreads, 0, st>>>(V, ld, nv, w, n, partial);
-}
 
 // Delayed-reorthogonalisation Arnoldi (DCGS2) dot pass: one read of
 // V_0..V_{nv-1} gives a_i = <V_i, u> and b_i = <V_i, w>, plus <u,u>, <u,w>,
@@ -251,49 +209,6 @@ void launch_dcgs_update(const double* V, long ld, int nv, const double* coef, do
     note_launch();
     dcgs_update_kernel<<<kRedBlocks, kRedThreads, sizeof(double) * (2 * nv + 2), st>>>(
         V, ld, nv, coef, u, w, n, partial);
-}
-
-// w <- w - sum_i h_i V_i (classical Gram-Schmidt update) and the block
-// partial of ||w||^2 after the update, in one pass.
-__global__ void __launch_bounds__(kRedThreads) orth_update_kernel(const double* __restrict__ V,
-                                                                  long ld, int nv,
-                                                                  const double* __restrict__ h,
-                                                                  double* __restrict__ w, long n,
-                                                                  double* partial) {
-    extern __shared__ double hs[];
-    __shared__ double red[kRedThreads / 32][1];
-    __shared__ double res[1];
-    for (int i = threadIdx.x; i < nv; i += blockDim.x)
-        hs[i] = h[i];
-    __syncthreads();
-    double acc[1] = {0.0};
-    // fixed interleaved partition (grid-stride over a fixed grid): deterministic
-    for (long k = (long)blockIdx.x * blockDim.x + threadIdx.x; k < n;
-         k += (long)gridDim.x * blockDim.x) {
-        double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-        int i = 0;
-        for (; i + 3 < nv; i += 4) {
-            s0 += hs[i] * __ldcs(V + (long)i * ld + k);
-            s1 += hs[i + 1] * __ldcs(V + (long)(i + 1) * ld + k);
-            s2 += hs[i + 2] * __ldcs(V + (long)(i + 2) * ld + k);
-            s3 += hs[i + 3] * __ldcs(V + (long)(i + 3) * ld + k);
-        }
-        for (; i < nv; ++i)
-            s0 += hs[i] * __ldcs(V + (long)i * ld + k);
-        const double v = w[k] - ((s0 + s1) + (s2 + s3));
-        w[k] = v;
-        acc[0] += v * v;
-    }
-    block_sum_vec<1>(acc, red, res);
-    if (threadIdx.x == 0)
-        partial[blockIdx.x] = res[0];
-}
-
-void launch_orth_update(const double* V, long ld, int nv, const double* h, double* w, long n,
-                        double* partial, cudaStream_t st) {
-    note_launch();
-    orth_update_kernel<<<kRedBlocks, kRedThreads, sizeof(double) * (nv > 0 ? nv : 1), st>>>(
-        V, ld, nv, h, w, n, partial);
 }
 
 // x <- x + s * sum_i y_i V_i (solution update x += S V y, linalg.cpp:272-274).
