@@ -87,13 +87,21 @@ struct hbgpu_ctx {
     DBuf<int> contrib_ptr;
     DBuf<uint16_t> contrib;
     int max_inc = 0;
-    // tangent rows bucketed by valence (<= 32 incidences / more), so the few
-    // high-valence rows do not set the shared-memory size of every CTA
+    // tangent rows bucketed by valence (<= 24 / <= 32 incidences / more), so
+    // the few high-valence rows do not set the shared-memory size of every CTA
     struct TanBucket {
         DBuf<int> rows;
+        DBuf<int4> desc;  // per row {A, i0, ninc, k0}, {nblk, cb, kdiag, 0}
         int count = 0, max_inc = 0, max_blk = 0, nt = 1;
         size_t smem = 0;
-    } tb[2];
+        // persistent row pipeline (used when its shared memory fits)
+        DBuf<unsigned char> pack;
+        DBuf<int> pack_ptr;
+        int max_pack = 0, grid = 0;
+        bool pipe = false;
+    } tb[3];
+    DBuf<double> blkc;        // per block: n-invariant tangent sums (8)
+    DBuf<uint8_t> blk_order;  // per row: off-diagonal blocks by descending contribution count
     DBuf<double> tgeom;
     DBuf<int> row_ptr, col_idx, diag_blk, inc_ptr;
     // residual element chunks
@@ -370,20 +378,79 @@ static int upload_all(hbgpu_ctx* c, const hbgpu_mesh_desc* d) {
                 }
             }
         c->max_inc = max_inc;
-        std::vector<int> brows[2];
+        // off-diagonal blocks of each row, longest contribution list first
+        std::vector<uint8_t> order(size_t(c->nnz), 0);
+        for (int A = 0; A < nn; ++A) {
+            const int k0 = c->row_ptr_h[size_t(A)], nb = c->row_ptr_h[size_t(A) + 1] - k0;
+            std::vector<int> js;
+            for (int j = 0; j < nb; ++j)
+                if (c->col_idx_h[size_t(k0 + j)] != A)
+                    js.push_back(j);
+            std::stable_sort(js.begin(), js.end(), [&](int x, int y) {
+                return cptr[size_t(k0 + x) + 1] - cptr[size_t(k0 + x)] >
+                       cptr[size_t(k0 + y) + 1] - cptr[size_t(k0 + y)];
+            });
+            for (size_t s2 = 0; s2 < js.size(); ++s2)
+                order[size_t(k0) + s2] = uint8_t(js[s2]);
+        }
+        std::vector<int> brows[3];
         for (int A = 0; A < nn; ++A) {
             const int ni = iptr[size_t(A) + 1] - iptr[size_t(A)];
-            const int bk = ni <= 32 ? 0 : 1;
+            const int bk = ni <= 24 ? 0 : ni <= 32 ? 1 : 2;
             brows[bk].push_back(A);
             c->tb[bk].max_inc = std::max(c->tb[bk].max_inc, ni);
             c->tb[bk].max_blk = std::max(c->tb[bk].max_blk,
                                          c->row_ptr_h[size_t(A) + 1] - c->row_ptr_h[size_t(A)]);
         }
-        for (int bk = 0; bk < 2; ++bk) {
+        for (int bk = 0; bk < 3; ++bk) {
             c->tb[bk].count = int(brows[bk].size());
             if (!c->tb[bk].count)
                 continue;
             CK(c, c->tb[bk].rows.alloc(brows[bk].size()));
+            std::vector<int4> desc;
+            for (int A : brows[bk]) {
+                const int k0 = c->row_ptr_h[size_t(A)];
+                desc.push_back(make_int4(A, iptr[size_t(A)], iptr[size_t(A) + 1] - iptr[size_t(A)], k0));
+                desc.push_back(make_int4(c->row_ptr_h[size_t(A) + 1] - k0, cptr[size_t(k0)],
+                                         diag[size_t(A)] - k0, 0));
+            }
+            CK(c, c->tb[bk].desc.alloc(desc.size()));
+            CK(c, cudaMemcpyAsync(c->tb[bk].desc.p, desc.data(), sizeof(int4) * desc.size(),
+                                  cudaMemcpyHostToDevice, st));
+            // row packs for the persistent pipeline
+            std::vector<int> pptr{0};
+            for (int A : brows[bk]) {
+                const int ni = iptr[size_t(A) + 1] - iptr[size_t(A)];
+                const int nb = c->row_ptr_h[size_t(A) + 1] - c->row_ptr_h[size_t(A)];
+                const int bytes = int(tangent_pack_bytes(ni, nb));
+                c->tb[bk].max_pack = std::max(c->tb[bk].max_pack, bytes);
+                pptr.push_back(pptr.back() + bytes / 16);
+            }
+            std::vector<unsigned char> pk(size_t(pptr.back()) * 16);
+            std::vector<int2> incl;
+            std::vector<int> rcptr;
+            for (size_t r = 0; r < brows[bk].size(); ++r) {
+                const int A = brows[bk][r];
+                const int k0 = c->row_ptr_h[size_t(A)];
+                const int nb = c->row_ptr_h[size_t(A) + 1] - k0;
+                const int ni = iptr[size_t(A) + 1] - iptr[size_t(A)];
+                incl.resize(size_t(ni));
+                for (int i = 0; i < ni; ++i) {
+                    const int4 r1 = irec[2 * size_t(iptr[size_t(A)] + i) + 1];
+                    incl[size_t(i)] = make_int2(r1.x, r1.y);
+                }
+                rcptr.resize(size_t(nb) + 1);
+                for (int j = 0; j <= nb; ++j)
+                    rcptr[size_t(j)] = cptr[size_t(k0 + j)] - cptr[size_t(k0)];
+                tangent_pack_write(pk.data() + size_t(pptr[r]) * 16, A, k0, ni, nb, diag[size_t(A)] - k0,
+                                   c->col_idx_h.data() + k0, incl.data(),
+                                   contrib.data() + cptr[size_t(k0)], rcptr.data(), order.data() + k0);
+            }
+            CK(c, c->tb[bk].pack.alloc(pk.size()));
+            CK(c, c->tb[bk].pack_ptr.alloc(pptr.size()));
+            CK(c, cudaMemcpyAsync(c->tb[bk].pack.p, pk.data(), pk.size(), cudaMemcpyHostToDevice, st));
+            CK(c, cudaMemcpyAsync(c->tb[bk].pack_ptr.p, pptr.data(), sizeof(int) * pptr.size(),
+                                  cudaMemcpyHostToDevice, st));
             CK(c, cudaMemcpyAsync(c->tb[bk].rows.p, brows[bk].data(), sizeof(int) * brows[bk].size(),
                                   cudaMemcpyHostToDevice, st));
         }
@@ -393,6 +460,14 @@ static int upload_all(hbgpu_ctx* c, const hbgpu_mesh_desc* d) {
                               cudaMemcpyHostToDevice, st));
         CK(c, cudaMemcpyAsync(c->contrib.p, contrib.data(), sizeof(uint16_t) * contrib.size(),
                               cudaMemcpyHostToDevice, st));
+        CK(c, c->blk_order.alloc(order.size()));
+        CK(c, cudaMemcpyAsync(c->blk_order.p, order.data(), order.size(), cudaMemcpyHostToDevice, st));
+        CK(c, c->blkc.alloc(size_t(c->nnz) * 8));
+        launch_tangent_blockconst(c->tgeom.p, c->row_ptr.p, c->inc_ptr.p, c->inc_rec.p,
+                                  c->contrib_ptr.p, c->contrib.p, nn, c->blkc.p, st);
+        for (auto& b : c->tb)
+            launch_tangent_pack_refresh(b.pack.p, b.pack_ptr.p, b.count, c->dir.p, c->blkc.p, st);
+        TRY(check_launch(c));
         CK(c, cudaStreamSynchronize(st));
     }
 
@@ -588,14 +663,27 @@ static int tangent_dev(hbgpu_ctx* c, const double* d_state) {
     a.diag_blk = c->diag_blk.p;
     a.contrib_ptr = c->contrib_ptr.p;
     a.contrib = c->contrib.p;
+    a.blkc = c->blkc.p;
+    a.blk_order = c->blk_order.p;
+
     for (const auto& b : c->tb) {
         if (!b.count)
             continue;
         a.rows = b.rows.p;
+        a.rowdesc = b.desc.p;
         a.max_inc = b.max_inc;
         a.max_blk = b.max_blk;
         a.NT = b.nt;
-        launch_tangent_row(a, b.count, b.smem, c->stream);
+        if (b.pipe) {
+            PipeArgs pa;
+            pa.pack = b.pack.p;
+            pa.pack_ptr = b.pack_ptr.p;
+            pa.nrows = b.count;
+            pa.max_pack = b.max_pack;
+            launch_tangent_pipe(a, pa, b.grid, b.smem, c->stream);
+        } else {
+            launch_tangent_row(a, b.count, b.smem, c->stream);
+        }
     }
     if (c->backflow_tangent && c->nbnodes > 0)
         launch_backflow_tangent(boundary_args(c, d_state, nullptr), c->row_ptr.p, c->col_idx.p,
@@ -1005,8 +1093,14 @@ void hbgpu_destroy(hbgpu_ctx* c) {
     c->inc_rec.release();
     c->contrib_ptr.release();
     c->contrib.release();
-    c->tb[0].rows.release();
-    c->tb[1].rows.release();
+    for (auto& b : c->tb) {
+        b.rows.release();
+        b.desc.release();
+        b.pack.release();
+        b.pack_ptr.release();
+    }
+    c->blkc.release();
+    c->blk_order.release();
     c->tgeom.release();
     c->lconn.release();
     c->slot_idx.release();
@@ -1088,22 +1182,52 @@ int hbgpu_set_basis(hbgpu_ctx* c, int modes, double period) {
     c->p_valid = c->inv_valid = false;
     c->mass_valid = false;
     {
-        // per bucket: largest time-sample tile whose row summaries fit 64 KB (3 CTAs / SM)
-        size_t mx = 0;
+        // per bucket: the persistent row pipeline with the largest time-sample
+        // tile that fits TAN6_SMEM_KB (3 CTAs / SM); rows whose neighbour
+        // records cannot be double-buffered at all use the tiled row kernel
+        size_t mx = 0, mxp = 0;
+        int dev = 0, nsm = 0;
+        CK(c, cudaGetDevice(&dev));
+        CK(c, cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
         for (auto& b : c->tb) {
             if (!b.count)
                 continue;
             int nt = N;
-            const int dp = (b.max_inc + kTanPart - 1) / kTanPart;
-            while (nt > 1 && tangent_row_smem(b.max_inc, dp, nt) > TAN_SMEM_KB * 1024)
+            while (nt > 1 && tangent_pipe_smem(b.max_pack, b.max_inc, b.max_blk, N, nt) > TAN6_SMEM_KB * 1024)
                 nt = (nt + 1) / 2;
-            b.smem = tangent_row_smem(b.max_inc, dp, nt);
+            const size_t ps = tangent_pipe_smem(b.max_pack, b.max_inc, b.max_blk, N, nt);
+            b.pipe = TAN_PIPE && ps <= 227 * 1024;
+            if (b.pipe) {
+                b.nt = nt;
+                b.smem = ps;
+                mxp = std::max(mxp, ps);
+                continue;
+            }
+            nt = N;
+            const int dp = (b.max_inc + kTanPart - 1) / kTanPart;
+            while (nt > 1 && tangent_row_smem(b.max_inc, b.max_blk, dp, nt) > TAN_SMEM_KB * 1024)
+                nt = (nt + 1) / 2;
+            b.smem = tangent_row_smem(b.max_inc, b.max_blk, dp, nt);
             b.nt = nt;
             mx = std::max(mx, b.smem);
         }
         if (mx > 227 * 1024)
             return fail(c, HBGPU_ERR_INVALID, "node valence too high for the tangent row kernel");
-        CK(c, configure_tangent_row_smem(mx));
+        if (mx)
+            CK(c, configure_tangent_row_smem(mx));
+        if (mxp) {
+            CK(c, configure_tangent_pipe_smem(mxp));
+            for (auto& b : c->tb) {
+                if (!b.count || !b.pipe)
+                    continue;
+                int per_sm = 0;
+                CK(c, tangent_pipe_occupancy(&per_sm, b.smem));
+                if (per_sm < 1)
+                    return fail(c, HBGPU_ERR_INVALID, "tangent pipeline does not fit on an SM");
+                const int tiles = (N + b.nt - 1) / b.nt;
+                b.grid = std::max(1, std::min(b.count, (nsm * per_sm + tiles - 1) / tiles));
+            }
+        }
     }
     // clear previous Neumann data sized for another N
     c->hN.release();

@@ -22,6 +22,7 @@ constexpr int kChunkElems = 64;
 constexpr int kResTile = 4;
 // Compact tangent geometry record (gradN 12, V, symmetric xi 6, xi:xi).
 constexpr int kTGeo = 20;
+
 // Tangent v3: threads per row CTA, contributions per diagonal part.
 #ifndef TAN_THREADS
 #define TAN_THREADS 128
@@ -39,11 +40,40 @@ constexpr int kTanPart = 8;
 #ifndef TAN_MINB
 #define TAN_MINB 6
 #endif
+#ifndef TAN_VER
+#define TAN_VER 5
+#endif
+#ifndef TAN5_MINB
+#define TAN5_MINB 4
+#endif
+#ifndef TAN_PIPE
+#define TAN_PIPE 1
+#endif
+#ifndef TAN6_MINB
+#define TAN6_MINB 4
+#endif
+#ifndef TAN6_SMEM_KB
+#define TAN6_SMEM_KB 56
+#endif
 #ifndef TAN_SMEM_KB
 #define TAN_SMEM_KB 64
 #endif
 #ifndef MV_UNROLL
 #define MV_UNROLL 2
+#endif
+
+// 1/sqrt(x) for x > 0: MUFU seed + two Newton steps, branch-free (the
+// library rsqrt carries special-case branches the element kernels never need;
+// x <= 0 / NaN is flagged and masked by the callers).  Within a few ulp.
+#ifdef __CUDACC__
+__device__ __forceinline__ double rsqrt_nr(double x) {
+    double y;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+    const double h = 0.5 * x;
+    y = fma(y, fma(-h * y, y, 0.5), y);
+    y = fma(y, fma(-h * y, y, 0.5), y);
+    return y;
+}
 #endif
 
 // Number of kernel launches issued by this library (bench.py's gpu_launches).
@@ -95,6 +125,18 @@ struct TangentArgs {
     int NT;            // time samples per CTA (tile of N)
     const int* rows;   // block rows of this launch (one valence bucket)
     int max_blk;       // longest block row of the bucket
+    // tangent v5: per-block n-invariant sums and off-diagonal visiting order
+    const double* blkc;         // nnz x 8
+    const uint8_t* blk_order;   // per row: off-diagonal block offsets, descending count
+    const int4* rowdesc;        // per bucket row: {A, i0, ninc, k0}, {nblk, cb, kdiag, 0}
+};
+
+// Persistent tangent row pipeline (hbgpu_tangent_pipe.cu): per-row packs.
+struct PipeArgs {
+    const unsigned char* pack;  // row packs, 16-byte aligned
+    const int* pack_ptr;        // nrows + 1, in 16-byte units
+    int nrows;
+    int max_pack;               // bytes
 };
 
 struct MatvecArgs {
@@ -146,9 +188,23 @@ void launch_boundary(const BoundaryArgs& a, cudaStream_t st);
 void launch_mass_rows(const double* geom, const int* row_ptr, const int* inc_ptr, const int4* rec,
                       double rho, double* mass, int nn, cudaStream_t st);
 void launch_tangent_geometry(const double* geom, int ne, double* tg, cudaStream_t st);
-size_t tangent_row_smem(int max_inc, int max_dparts, int N);
+size_t tangent_row_smem(int max_inc, int max_blk, int max_dparts, int NT);
+void launch_tangent_blockconst(const double* tgeom, const int* row_ptr, const int* inc_ptr,
+                               const int4* inc_rec, const int* contrib_ptr, const uint16_t* contrib,
+                               int nn, double* blkc, cudaStream_t st);
 cudaError_t configure_tangent_row_smem(size_t bytes);
 void launch_tangent_row(const TangentArgs& a, int nrows, size_t smem, cudaStream_t st);
+size_t tangent_pack_bytes(int ninc, int nblk);
+void tangent_pack_write(unsigned char* dst, int A, int k0, int ninc, int nblk, int kdiag,
+                        const int* cols, const int2* inc, const uint16_t* cont, const int* cptr,
+                        const uint8_t* order);
+void launch_tangent_pack_refresh(unsigned char* pack, const int* pack_ptr, int nrows,
+                                 const uint8_t* dir, const double* blkc, cudaStream_t st);
+size_t tangent_pipe_smem(int max_pack, int max_inc, int max_blk, int N, int NT);
+cudaError_t configure_tangent_pipe_smem(size_t bytes);
+cudaError_t tangent_pipe_occupancy(int* blocks_per_sm, size_t smem);
+void launch_tangent_pipe(const TangentArgs& a, const PipeArgs& p, int grid_x, size_t smem,
+                         cudaStream_t st);
 void launch_backflow_tangent(const BoundaryArgs& a, const int* row_ptr, const int* col_idx,
                              double* pvals, cudaStream_t st);
 void launch_lmatvec(const MatvecArgs& a, cudaStream_t st);

@@ -1,0 +1,474 @@
+// Pointwise tangent P, persistent row pipeline (sm_100a, FP64).
+//
+// Replaces element_tangent_p + assemble_tangent (reference
+// src/assembly.cpp:265-374, 550-666) for every block row.  Same arithmetic as
+// the row kernel in hbgpu_tangent.cu (see the v5 comment there); what changes
+// is how a row's operands reach shared memory:
+//
+//   * Each bucket row has a contiguous "row pack" in HBM, built at setup:
+//       hdr   int4 {A, ninc, nblk, kdiag}, int4 {k0, nslots, dparts, afix}
+//       sinfo int4 per phase-2 slot {c0, c1, j, bfix}
+//       cols  int per block (column node), inc int2 per incidence
+//       {e | la << 30, 4 x u8 block offsets}, cont u16 per contribution
+//       (i << 2 | b, list order), blkc 8 doubles per block (n-invariant sums).
+//     Dirichlet flags and blkc are (re)written on the device by
+//     tangent_pack_refresh_kernel whenever the Dirichlet set changes.
+//   * A persistent CTA walks rows r = blockIdx.x + k * gridDim.x.  Warp 0
+//     streams them with bulk async copies (cp.async.bulk, the TMA engine's
+//     1-D mode) completing on mbarriers: the pack of row k+1 lands during
+//     phase 1 of row k, its gathers (each neighbour node's 4N state record,
+//     each incidence's 20-double geometry record) during phase 2 of row k.
+//     Two pack slots, one gather buffer.
+//   * The compute of a row is three barrier-separated phases: contribution
+//     records + per-(incidence, sample) summaries, per-(slot, sample)
+//     accumulation, diagonal parts.  No global loads remain in them.
+#include "hbgpu_internal.h"
+
+#include <algorithm>
+
+namespace hbgpu {
+
+namespace {
+inline void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n\t"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n\t"
+        "@!P1 bra WAIT_%=;\n\t}" ::"r"(smem_u32(b)),
+        "r"(parity), "r"(0x989680u)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* b) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(b))
+        : "memory");
+}
+}  // namespace
+
+// ---------------------------------------------------------------- row packs
+
+__host__ __device__ inline int pack_align16(int bytes) { return (bytes + 15) & ~15; }
+
+// Byte offsets of the sections of a row pack.
+struct PackSections {
+    int sinfo, cols, inc, cont, blkc, total;
+};
+__host__ __device__ inline PackSections pack_sections(int ninc, int nblk, int nslots) {
+    PackSections s;
+    s.sinfo = 32;
+    s.cols = s.sinfo + 16 * nslots;
+    s.inc = s.cols + pack_align16(4 * nblk);
+    s.cont = s.inc + pack_align16(8 * ninc);
+    s.blkc = s.cont + pack_align16(2 * 4 * ninc);
+    s.total = s.blkc + 64 * nblk;
+    return s;
+}
+
+size_t tangent_pack_bytes(int ninc, int nblk) {
+    const int dparts = (ninc + kTanPart - 1) / kTanPart;
+    return (size_t)pack_sections(ninc, nblk, dparts + nblk - 1).total;
+}
+
+// Host: write the pack of one row (flags and blkc are left for the refresh
+// kernel).  `cont` are the row's contributions in list order (i << 2 | b),
+// `cptr` the row's per-block list offsets relative to the row start.
+void tangent_pack_write(unsigned char* dst, int A, int k0, int ninc, int nblk, int kdiag,
+                        const int* cols, const int2* inc, const uint16_t* cont, const int* cptr,
+                        const uint8_t* order) {
+    const int dparts = (ninc + kTanPart - 1) / kTanPart;
+    const int nslots = dparts + nblk - 1;
+    const PackSections s = pack_sections(ninc, nblk, nslots);
+    std::fill(dst, dst + s.total, (unsigned char)0);
+    int* h = reinterpret_cast<int*>(dst);
+    h[0] = A;
+    h[1] = ninc;
+    h[2] = nblk;
+    h[3] = kdiag;
+    h[4] = k0;
+    h[5] = nslots;
+    h[6] = dparts;
+    h[7] = 0;
+    int* si = reinterpret_cast<int*>(dst + s.sinfo);
+    for (int p = 0; p < dparts; ++p) {
+        si[4 * p] = cptr[kdiag] + p * kTanPart;
+        si[4 * p + 1] = std::min(cptr[kdiag] + (p + 1) * kTanPart, cptr[kdiag + 1]);
+        si[4 * p + 2] = kdiag;
+    }
+    for (int q = 0; q + 1 < nblk; ++q) {
+        const int j = order[q];
+        si[4 * (dparts + q)] = cptr[j];
+        si[4 * (dparts + q) + 1] = cptr[j + 1];
+        si[4 * (dparts + q) + 2] = j;
+    }
+    std::copy(cols, cols + nblk, reinterpret_cast<int*>(dst + s.cols));
+    std::copy(inc, inc + ninc, reinterpret_cast<int2*>(dst + s.inc));
+    std::copy(cont, cont + 4 * ninc, reinterpret_cast<uint16_t*>(dst + s.cont));
+}
+
+// Device: Dirichlet flags (afix, bfix per slot) and block constants into the
+// packs of one bucket; thread per row.
+__global__ void tangent_pack_refresh_kernel(unsigned char* __restrict__ pack,
+                                            const int* __restrict__ pack_ptr, int nrows,
+                                            const uint8_t* __restrict__ dir,
+                                            const double* __restrict__ blkc) {
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= nrows)
+        return;
+    unsigned char* p = pack + (size_t)pack_ptr[r] * 16;
+    int* h = reinterpret_cast<int*>(p);
+    const int A = h[0], ninc = h[1], nblk = h[2], k0 = h[4], nslots = h[5];
+    const PackSections s = pack_sections(ninc, nblk, nslots);
+    h[7] = dir[A] != 0;
+    int* si = reinterpret_cast<int*>(p + s.sinfo);
+    const int* cols = reinterpret_cast<const int*>(p + s.cols);
+    for (int q = 0; q < nslots; ++q)
+        si[4 * q + 3] = dir[cols[si[4 * q + 2]]] != 0;
+    double* bc = reinterpret_cast<double*>(p + s.blkc);
+    for (int k = 0; k < 8 * nblk; ++k)
+        bc[k] = blkc[(size_t)k0 * 8 + k];
+}
+
+void launch_tangent_pack_refresh(unsigned char* pack, const int* pack_ptr, int nrows,
+                                 const uint8_t* dir, const double* blkc, cudaStream_t st) {
+    if (nrows <= 0)
+        return;
+    note_launch();
+    tangent_pack_refresh_kernel<<<(nrows + 127) / 128, 128, 0, st>>>(pack, pack_ptr, nrows, dir, blkc);
+}
+
+// ---------------------------------------------------------------- kernel
+
+struct PipeSmem {
+    int meta, su, tg, summ, rec, dpart, mbar, total;  // byte offsets
+};
+__host__ __device__ inline PipeSmem pipe_layout(int max_pack, int mi, int max_blk, int N, int NT) {
+    PipeSmem L;
+    const int dpmax = (mi + kTanPart - 1) / kTanPart;
+    L.meta = 0;                                                   // 2 x max_pack
+    L.su = L.meta + 2 * pack_align16(max_pack);                   // [blk][4N]
+    L.tg = L.su + max_blk * 4 * N * 8;                            // [inc][20]
+    L.summ = L.tg + mi * kTGeo * 8;                               // [i][8][NT]
+    L.rec = L.summ + mi * 8 * NT * 8;                             // [p][8]
+    L.dpart = L.rec + 4 * mi * 64;                                // [part][8][NT]
+    L.mbar = pack_align16(L.dpart + dpmax * 8 * NT * 8);          // 3 mbarriers
+    L.total = L.mbar + 32;
+    return L;
+}
+
+size_t tangent_pipe_smem(int max_pack, int max_inc, int max_blk, int N, int NT) {
+    return (size_t)pipe_layout(max_pack, max_inc, max_blk, N, NT).total;
+}
+
+template <int TAU>
+__global__ void __launch_bounds__(kTanThreads, TAN6_MINB) tangent_pipe_kernel(TangentArgs a, PipeArgs pa) {
+    extern __shared__ __align__(128) unsigned char smraw[];
+    const int N = a.N, NT = a.NT, n0 = blockIdx.y * NT, nt = min(NT, N - n0);
+    const PipeSmem Ls = pipe_layout(pa.max_pack, a.max_inc, a.max_blk, N, NT);
+    const int mpack = pack_align16(pa.max_pack);
+    uint64_t* mbar = reinterpret_cast<uint64_t*>(smraw + Ls.mbar);  // [0..1] packs, [2] gathers
+    double* summ = reinterpret_cast<double*>(smraw + Ls.summ);
+    double* rec = reinterpret_cast<double*>(smraw + Ls.rec);
+    double* dpart = reinterpret_cast<double*>(smraw + Ls.dpart);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const double rho = a.rho, diffc = 3.0 * a.nu * a.nu, dAB = kQA - kQB;
+    const double mu = a.mu, pc = a.pseudo_c;
+
+    const int r0 = blockIdx.x, rs = gridDim.x, nrows = pa.nrows;
+    if (threadIdx.x == 0) {
+        for (int k = 0; k < 3; ++k)
+            mbar_init(mbar + k, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+
+    auto issue_pack = [&](int r, int slot) {  // warp 0, lane 0
+        const int p0 = __ldg(pa.pack_ptr + r), p1 = __ldg(pa.pack_ptr + r + 1);
+        const uint32_t bytes = (uint32_t)(p1 - p0) * 16u;
+        mbar_expect_tx(mbar + slot, bytes);
+        bulk_g2s(smraw + Ls.meta + slot * mpack, pa.pack + (size_t)p0 * 16, bytes, mbar + slot);
+    };
+    auto issue_gather = [&](int slot) {  // warp 0, all lanes
+        const unsigned char* m = smraw + Ls.meta + slot * mpack;
+        const int* h = reinterpret_cast<const int*>(m);
+        const int ninc = h[1], nblk = h[2];
+        const PackSections s = pack_sections(ninc, nblk, h[5]);
+        const int* cols = reinterpret_cast<const int*>(m + s.cols);
+        const int2* inc = reinterpret_cast<const int2*>(m + s.inc);
+        double* su = reinterpret_cast<double*>(smraw + Ls.su);
+        double* tg = reinterpret_cast<double*>(smraw + Ls.tg);
+        if (lane == 0)
+            mbar_expect_tx(mbar + 2, (uint32_t)(nblk * 4 * N * 8 + ninc * kTGeo * 8));
+        __syncwarp();
+        for (int j = lane; j < nblk; j += 32)
+            bulk_g2s(su + (size_t)j * 4 * N, a.state + (size_t)cols[j] * 4 * N, 4 * N * 8, mbar + 2);
+        for (int i = lane; i < ninc; i += 32)
+            bulk_g2s(tg + (size_t)i * kTGeo, a.tgeom + (size_t)(inc[i].x & 0x3FFFFFFF) * kTGeo,
+                     kTGeo * 8, mbar + 2);
+    };
+
+    // prologue: pack and gathers of row 0
+    if (warp == 0 && r0 < nrows) {
+        if (lane == 0)
+            issue_pack(r0, 0);
+        mbar_wait(mbar + 0, 0);
+        issue_gather(0);
+    }
+
+    const int di = blockDim.x / nt, dt = blockDim.x - di * nt;
+    const int i_start = threadIdx.x / nt, t_start = threadIdx.x - i_start * nt;
+    // Diagonal block of the previous row: sum its parts in order, identity K on
+    // Dirichlet rows (assembly.cpp:659-665).  Deferred into the next row's first
+    // region so a row costs two barriers, not three.
+    long pd_blk = -1;
+    int pd_parts = 0;
+    bool pd_fix = false;
+    auto diag_sum = [&]() {
+        if (pd_blk < 0)
+            return;
+        for (int it = threadIdx.x; it < 8 * nt; it += blockDim.x) {
+            const int sl = it / nt, t = it - sl * nt, n = n0 + t;
+            double v = 0.0;
+            for (int p = 0; p < pd_parts; ++p)
+                v += dpart[((size_t)p * 8 + sl) * NT + t];
+            if (sl == 0 && pd_fix)
+                v = 1.0;
+            __stcs(a.pvals + (pd_blk * 8 + sl) * N + n, v);
+        }
+    };
+    int k = 0;
+    for (int r = r0; r < nrows; r += rs, ++k) {
+        // Pipeline: the pack of row k+1 is fetched during phase 1 of row k, its
+        // gathers (into the single gather buffer, dead once phase 1 has read
+        // it) during phase 2 and the diagonal pass of row k.
+        const int ms = k & 1;
+        const bool more = r + rs < nrows;
+        if (warp == 0 && lane == 0 && more)
+            issue_pack(r + rs, ms ^ 1);
+        mbar_wait(mbar + ms, (k >> 1) & 1);  // pack landed (acquire for every thread)
+        mbar_wait(mbar + 2, k & 1);           // gathers landed
+
+        const unsigned char* m = smraw + Ls.meta + ms * mpack;
+        const int* h = reinterpret_cast<const int*>(m);
+        const int ninc = h[1], nblk = h[2], kdiag = h[3], k0 = h[4], nslots = h[5], dparts = h[6];
+        const bool afix = h[7] != 0;
+        const PackSections s = pack_sections(ninc, nblk, nslots);
+        const int4* sinfo = reinterpret_cast<const int4*>(m + s.sinfo);
+        const int2* inc = reinterpret_cast<const int2*>(m + s.inc);
+        const uint16_t* cont = reinterpret_cast<const uint16_t*>(m + s.cont);
+        const double* blkc = reinterpret_cast<const double*>(m + s.blkc);
+        const double* su = reinterpret_cast<const double*>(smraw + Ls.su);
+        const double* tg = reinterpret_cast<const double*>(smraw + Ls.tg);
+
+        // ---- diagonal block of the previous row (its parts are in dpart)
+        diag_sum();
+        // ---- contribution records {dN_a (3), gg, dN_b (3), summary offset}
+        for (int p = threadIdx.x; p < 4 * ninc; p += blockDim.x) {
+            const int ent = cont[p];
+            const int i = ent >> 2, b = ent & 3;
+            const int la = (unsigned)inc[i].x >> 30;
+            const double* gi = tg + i * kTGeo;
+            const double ga0 = gi[3 * la], ga1 = gi[3 * la + 1], ga2 = gi[3 * la + 2];
+            const double gb0 = gi[3 * b], gb1 = gi[3 * b + 1], gb2 = gi[3 * b + 2];
+            double2* o = reinterpret_cast<double2*>(rec + p * 8);
+            o[0] = make_double2(ga0, ga1);
+            o[1] = make_double2(ga2, fma(ga0, gb0, fma(ga1, gb1, ga2 * gb2)));
+            o[2] = make_double2(gb0, gb1);
+            o[3] = make_double2(gb2, __longlong_as_double((long long)i * 8 * NT));
+        }
+        // ---- phase 1: per (incidence, sample) summaries
+        for (int it = threadIdx.x, i = i_start, t = t_start; it < ninc * nt;
+             it += blockDim.x, t += dt, i += di + (t >= nt), t -= (t >= nt ? nt : 0)) {
+            const double* gi = tg + i * kTGeo;
+            const int2 ic = inc[i];
+            const int la = (unsigned)ic.x >> 30;
+            const unsigned cols = (unsigned)ic.y;
+            const double2 xv = *reinterpret_cast<const double2*>(gi + 12);  // V, xi00
+            const double2 x1 = *reinterpret_cast<const double2*>(gi + 14);  // xi01, xi02
+            const double2 x2 = *reinterpret_cast<const double2*>(gi + 16);  // xi11, xi12
+            const double2 x3 = *reinterpret_cast<const double2*>(gi + 18);  // xi22, xi:xi
+            const double x01 = 2.0 * x1.x, x02 = 2.0 * x1.y, x12 = 2.0 * x2.y, diff = diffc * x3.y;
+            const double ga[3] = {gi[3 * la], gi[3 * la + 1], gi[3 * la + 2]};
+            const double V = xv.x, w = 0.25 * V;
+            auto quad = [&](const double v[3]) {
+                const double q0 = fma(x02, v[2], fma(x01, v[1], xv.y * v[0]));
+                const double q1 = fma(x12, v[2], x2.x * v[1]);
+                return fma(v[0], q0, fma(v[1], q1, fma(v[2], x3.x * v[2], diff)));
+            };
+            const int n = n0 + t;
+            double u[4][3], usum[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+            for (int b = 0; b < 4; ++b) {
+                const double* sb = su + (size_t)((cols >> (8 * b)) & 0xFFu) * 4 * N + n;
+#pragma unroll
+                for (int c = 0; c < 3; ++c) {
+                    u[b][c] = sb[c * N];
+                    usum[c] += u[b][c];
+                }
+            }
+            double bu[3];
+#pragma unroll
+            for (int c = 0; c < 3; ++c)
+                bu[c] = kQB * usum[c];
+            bool bad = false;
+            double tau_mean = 0.0;
+            if (TAU == 1) {
+                const double um[3] = {0.25 * usum[0], 0.25 * usum[1], 0.25 * usum[2]};
+                const double arg = quad(um);
+                bad = !(arg > 0.0);
+                tau_mean = bad ? 0.0 : rsqrt_nr(fmax(arg, 1e-300));
+            }
+            double asum = 0.0, tsum = 0.0, z[3] = {0.0, 0.0, 0.0}, kap[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                double uq[3];
+#pragma unroll
+                for (int c = 0; c < 3; ++c)
+                    uq[c] = fma(dAB, u[q][c], bu[c]);
+                double tq = tau_mean;
+                if (TAU == 0) {
+                    const double arg = quad(uq);
+                    const bool bq = !(arg > 0.0);
+                    bad |= bq;
+                    tq = bq ? 0.0 : rsqrt_nr(fmax(arg, 1e-300));
+                }
+                const double tadv = tq * fma(uq[0], ga[0], fma(uq[1], ga[1], uq[2] * ga[2]));
+                const double na = (q == la) ? kQA : kQB;
+                asum += tadv;
+                tsum += tq;
+#pragma unroll
+                for (int c = 0; c < 3; ++c) {
+                    z[c] = fma(tq, uq[c], z[c]);
+                    kap[c] = fma(na + tadv, uq[c], kap[c]);
+                }
+            }
+            if (bad)
+                atomicOr(a.flag, 1);
+            double* so = summ + (size_t)i * 8 * NT + t;
+            const double wr = w * rho;
+            so[0] = wr * kap[0];
+            so[NT] = wr * kap[1];
+            so[2 * NT] = wr * kap[2];
+            so[3 * NT] = w * asum;
+            so[4 * NT] = w * z[0];
+            so[5 * NT] = w * z[1];
+            so[6 * NT] = w * z[2];
+            so[7 * NT] = (w / rho) * tsum;
+        }
+        __syncthreads();
+
+        if (warp == 0 && more) {
+            mbar_wait(mbar + (ms ^ 1), ((k + 1) >> 1) & 1);
+            issue_gather(ms ^ 1);
+        }
+        // ---- phase 2: per (slot, sample) register accumulation
+        for (int it = threadIdx.x, slot = i_start, t = t_start; it < nslots * nt;
+             it += blockDim.x, t += dt, slot += di + (t >= nt), t -= (t >= nt ? nt : 0)) {
+            const int n = n0 + t;
+            const int4 info = sinfo[slot];
+            const int j = info.z;
+            const bool bfix = info.w != 0;
+            double K = 0.0, G0 = 0.0, G1 = 0.0, G2 = 0.0, D0 = 0.0, D1 = 0.0, D2 = 0.0, L = 0.0;
+#pragma unroll 2
+            for (int p = info.x; p < info.y; ++p) {
+                const double2* rp = reinterpret_cast<const double2*>(rec + p * 8);
+                const double2 ra = rp[0], rb = rp[1], rc = rp[2], rd = rp[3];
+                const double* sp = summ + __double_as_longlong(rd.y) + t;
+                const double gb0 = rc.x, gb1 = rc.y, gb2 = rd.x;
+                K = fma(sp[0], gb0, fma(sp[NT], gb1, fma(sp[2 * NT], gb2, K)));
+                const double al = sp[3 * NT];
+                G0 = fma(al, gb0, G0);
+                G1 = fma(al, gb1, G1);
+                G2 = fma(al, gb2, G2);
+                const double alb = fma(sp[4 * NT], gb0, fma(sp[5 * NT], gb1, sp[6 * NT] * gb2));
+                D0 = fma(ra.x, alb, D0);
+                D1 = fma(ra.y, alb, D1);
+                D2 = fma(rb.x, alb, D2);
+                L = fma(rb.y, sp[7 * NT], L);
+            }
+            if (slot >= dparts || slot == 0) {
+                const double2* bc = reinterpret_cast<const double2*>(blkc + j * 8);
+                const double2 b0 = bc[0], b1 = bc[1], b2 = bc[2], b3 = bc[3];
+                K += fma(mu, b0.x, pc * b0.y);
+                G0 += b1.x;
+                G1 += b1.y;
+                G2 += b2.x;
+                D0 += b2.y;
+                D1 += b3.x;
+                D2 += b3.y;
+            }
+            if (afix || bfix)
+                K = 0.0;
+            if (afix)
+                G0 = G1 = G2 = 0.0;
+            if (bfix)
+                D0 = D1 = D2 = 0.0;
+            if (slot >= dparts) {
+                double* out = a.pvals + ((long)(k0 + j) * 8) * N + n;
+                __stcs(out, K);
+                __stcs(out + N, G0);
+                __stcs(out + 2 * N, G1);
+                __stcs(out + 3 * N, G2);
+                __stcs(out + 4 * N, D0);
+                __stcs(out + 5 * N, D1);
+                __stcs(out + 6 * N, D2);
+                __stcs(out + 7 * N, L);
+            } else {
+                double* o = dpart + (size_t)slot * 8 * NT + t;
+                o[0] = K;
+                o[NT] = G0;
+                o[2 * NT] = G1;
+                o[3 * NT] = G2;
+                o[4 * NT] = D0;
+                o[5 * NT] = D1;
+                o[6 * NT] = D2;
+                o[7 * NT] = L;
+            }
+        }
+        __syncthreads();
+        pd_blk = k0 + kdiag;
+        pd_parts = dparts;
+        pd_fix = afix;
+    }
+    diag_sum();
+}
+
+cudaError_t configure_tangent_pipe_smem(size_t bytes) {
+    const int b = int(bytes < 48 * 1024 ? 48 * 1024 : bytes);
+    cudaError_t e = cudaFuncSetAttribute(tangent_pipe_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, b);
+    if (e != cudaSuccess)
+        return e;
+    return cudaFuncSetAttribute(tangent_pipe_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, b);
+}
+
+cudaError_t tangent_pipe_occupancy(int* blocks_per_sm, size_t smem) {
+    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, tangent_pipe_kernel<0>,
+                                                         kTanThreads, smem);
+}
+
+void launch_tangent_pipe(const TangentArgs& a, const PipeArgs& p, int grid_x, size_t smem,
+                         cudaStream_t st) {
+    if (p.nrows <= 0)
+        return;
+    note_launch();
+    const dim3 grid(grid_x, (a.N + a.NT - 1) / a.NT);
+    if (a.tau_mode == 1)
+        tangent_pipe_kernel<1><<<grid, kTanThreads, smem, st>>>(a, p);
+    else
+        tangent_pipe_kernel<0><<<grid, kTanThreads, smem, st>>>(a, p);
+}
+
+}  // namespace hbgpu
