@@ -14,6 +14,7 @@
 #include <cmath>
 #include <complex>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <limits>
 #include <numeric>
@@ -90,7 +91,6 @@ struct hbgpu_ctx {
     // tangent rows bucketed by valence (<= 24 / <= 32 incidences / more), so
     // the few high-valence rows do not set the shared-memory size of every CTA
     struct TanBucket {
-        DBuf<int> rows;
         DBuf<int4> desc;  // per row {A, i0, ninc, k0}, {nblk, cb, kdiag, 0}
         int count = 0, max_inc = 0, max_blk = 0, nt = 1;
         size_t smem = 0;
@@ -406,7 +406,6 @@ static int upload_all(hbgpu_ctx* c, const hbgpu_mesh_desc* d) {
             c->tb[bk].count = int(brows[bk].size());
             if (!c->tb[bk].count)
                 continue;
-            CK(c, c->tb[bk].rows.alloc(brows[bk].size()));
             std::vector<int4> desc;
             for (int A : brows[bk]) {
                 const int k0 = c->row_ptr_h[size_t(A)];
@@ -450,8 +449,6 @@ static int upload_all(hbgpu_ctx* c, const hbgpu_mesh_desc* d) {
             CK(c, c->tb[bk].pack_ptr.alloc(pptr.size()));
             CK(c, cudaMemcpyAsync(c->tb[bk].pack.p, pk.data(), pk.size(), cudaMemcpyHostToDevice, st));
             CK(c, cudaMemcpyAsync(c->tb[bk].pack_ptr.p, pptr.data(), sizeof(int) * pptr.size(),
-                                  cudaMemcpyHostToDevice, st));
-            CK(c, cudaMemcpyAsync(c->tb[bk].rows.p, brows[bk].data(), sizeof(int) * brows[bk].size(),
                                   cudaMemcpyHostToDevice, st));
         }
         CK(c, c->contrib_ptr.alloc(cptr.size()));
@@ -669,7 +666,6 @@ static int tangent_dev(hbgpu_ctx* c, const double* d_state) {
     for (const auto& b : c->tb) {
         if (!b.count)
             continue;
-        a.rows = b.rows.p;
         a.rowdesc = b.desc.p;
         a.max_inc = b.max_inc;
         a.max_blk = b.max_blk;
@@ -1094,7 +1090,6 @@ void hbgpu_destroy(hbgpu_ctx* c) {
     c->contrib_ptr.release();
     c->contrib.release();
     for (auto& b : c->tb) {
-        b.rows.release();
         b.desc.release();
         b.pack.release();
         b.pack_ptr.release();
@@ -1187,6 +1182,9 @@ int hbgpu_set_basis(hbgpu_ctx* c, int modes, double period) {
         // records cannot be double-buffered at all use the tiled row kernel
         size_t mx = 0, mxp = 0;
         int dev = 0, nsm = 0;
+        // test knob: HBGPU_TANGENT_KERNEL=rows forces the row-kernel fallback
+        const char* tk = std::getenv("HBGPU_TANGENT_KERNEL");
+        const bool force_rows = tk && std::strcmp(tk, "rows") == 0;
         CK(c, cudaGetDevice(&dev));
         CK(c, cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
         for (auto& b : c->tb) {
@@ -1196,7 +1194,7 @@ int hbgpu_set_basis(hbgpu_ctx* c, int modes, double period) {
             while (nt > 1 && tangent_pipe_smem(b.max_pack, b.max_inc, b.max_blk, N, nt) > TAN6_SMEM_KB * 1024)
                 nt = (nt + 1) / 2;
             const size_t ps = tangent_pipe_smem(b.max_pack, b.max_inc, b.max_blk, N, nt);
-            b.pipe = TAN_PIPE && ps <= 227 * 1024;
+            b.pipe = TAN_PIPE && !force_rows && ps <= 227 * 1024;
             if (b.pipe) {
                 b.nt = nt;
                 b.smem = ps;

@@ -37,12 +37,6 @@ constexpr int kTanPart = 8;
 #ifndef RES_MINB
 #define RES_MINB 2
 #endif
-#ifndef TAN_MINB
-#define TAN_MINB 6
-#endif
-#ifndef TAN_VER
-#define TAN_VER 5
-#endif
 #ifndef TAN5_MINB
 #define TAN5_MINB 4
 #endif
@@ -115,15 +109,14 @@ struct TangentArgs {
     double rho, mu, nu, pseudo_c;
     int tau_mode;
     int* flag;
-    // tangent v3 (one CTA per row): per block, its contributions (i<<2 | b),
-    // i = incidence index within the row, in element order
+    // per block, its contributions (i<<2 | b), i = incidence index within
+    // the row, in element order
     const int* col_idx;
     const int* diag_blk;
     const int* contrib_ptr;        // nnz + 1
     const uint16_t* contrib;
     int max_inc;
     int NT;            // time samples per CTA (tile of N)
-    const int* rows;   // block rows of this launch (one valence bucket)
     int max_blk;       // longest block row of the bucket
     // tangent v5: per-block n-invariant sums and off-diagonal visiting order
     const double* blkc;         // nnz x 8

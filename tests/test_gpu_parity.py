@@ -154,6 +154,28 @@ def test_delaunay_cube_operator(gpu, modes):
     assert np.array_equal(ci, orc.col_idx)
 
 
+@pytest.mark.parametrize("mesh_kind,modes,tau", [("tube", 3, 0), ("tube", 4, 1), ("delaunay", 4, 0),
+                                                  ("delaunay", 24, 0)])
+def test_tangent_row_kernel_fallback(gpu, monkeypatch, mesh_kind, modes, tau):
+    """The tiled row kernel (used for rows whose neighbour records do not fit
+    the persistent pipeline's shared memory) against the oracle; forced with
+    the HBGPU_TANGENT_KERNEL=rows test knob, read when the basis is set."""
+    from paper_2411_14315_b200 import meshgen
+
+    monkeypatch.setenv("HBGPU_TANGENT_KERNEL", "rows")
+    if mesh_kind == "tube":
+        prob = tube_problem(modes)
+    else:
+        mesh = meshgen.cube_delaunay(3000, seed=5)
+        N = 2 * modes - 1
+        neu = [(k, np.full(N, 50.0)) for k, p in enumerate(mesh.patches) if p.kind == NEUMANN]
+        prob = Problem(mesh, modes, 1.0, 1.06, 0.04, np.zeros(mesh.num_nodes * 3 * N), neu, 0.2)
+    ctx = gpu_ctx(prob, tau, 0.3)
+    orc = ob.Restated(prob, tau_mode=tau, pseudo_dt=0.3)
+    s = cases.random_modes_state(prob.mesh.num_nodes, modes, 7)
+    assert rel(ctx.assemble_tangent(s), orc.tangent(s)) < TOL
+
+
 def test_pattern_bit_exact(gpu):
     from paper_2411_14315_b200 import meshgen
 
