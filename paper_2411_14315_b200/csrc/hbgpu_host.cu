@@ -107,10 +107,9 @@ struct hbgpu_ctx {
     // residual element chunks
     int nchunks = 0, max_nloc = 0, res_grid = 0;
     long npairs = 0;
-    DBuf<uint32_t> lconn;
-    DBuf<int> chunk_node_ptr, chunk_nodes, slot_ptr, npart_ptr, npart;
-    DBuf<uint8_t> slot_idx;
-    DBuf<uint16_t> slot_off;
+    DBuf<int> rpack_ptr, npart_ptr, npart;
+    DBuf<unsigned char> rpack;  // chunk packs (see ResidualChunkArgs)
+    int max_rpack = 0;
     DBuf<double> rpartial;
 
 
@@ -473,12 +472,12 @@ static int upload_all(hbgpu_ctx* c, const hbgpu_mesh_desc* d) {
     // and per node the (chunk, node) records in chunk order
     const int CE = kChunkElems;
     const int nch = (ne + CE - 1) / CE;
-    std::vector<int> cnp(size_t(nch) + 1, 0), cnodes, sptr{0}, npp(size_t(nn) + 1, 0), npl;
-    std::vector<uint8_t> sidx;
-    std::vector<uint32_t> lconn(static_cast<size_t>(ne));
-    int maxnloc = 0;
+    std::vector<int> cnodes, npp(size_t(nn) + 1, 0), npl, rpp{0};
+    std::vector<unsigned char> rpk;
+    int maxnloc = 0, maxpk = 0;
     for (int ch = 0; ch < nch; ++ch) {
         const long e0 = long(ch) * CE, e1 = std::min<long>(ne, e0 + CE);
+        const int ecount = int(e1 - e0);
         std::vector<int> loc;
         for (long e = e0; e < e1; ++e)
             for (int a = 0; a < 4; ++a)
@@ -487,8 +486,10 @@ static int upload_all(hbgpu_ctx* c, const hbgpu_mesh_desc* d) {
         loc.erase(std::unique(loc.begin(), loc.end()), loc.end());
         if (loc.size() > 255)
             return fail(c, HBGPU_ERR_INVALID, "element chunk with more than 255 nodes");
-        maxnloc = std::max(maxnloc, int(loc.size()));
+        const int nloc = int(loc.size());
+        maxnloc = std::max(maxnloc, nloc);
         std::vector<std::vector<uint8_t>> inc(loc.size());
+        std::vector<uint32_t> lconn(size_t(ecount), 0);
         for (long e = e0; e < e1; ++e) {
             uint32_t pk = 0;
             for (int a = 0; a < 4; ++a) {
@@ -496,15 +497,26 @@ static int upload_all(hbgpu_ctx* c, const hbgpu_mesh_desc* d) {
                 pk |= uint32_t(ln) << (8 * a);
                 inc[size_t(ln)].push_back(uint8_t((e - e0) * 4 + a));
             }
-            lconn[size_t(e)] = pk;
+            lconn[size_t(e - e0)] = pk;
         }
-        for (size_t ln = 0; ln < loc.size(); ++ln) {
-            cnodes.push_back(loc[ln]);
-            sidx.insert(sidx.end(), inc[ln].begin(), inc[ln].end());
-            sptr.push_back(int(sidx.size()));
-            npp[size_t(loc[ln]) + 1] += 1;
+        // slot lists as offsets into the kernel's per-element slot array:
+        // element stride 29T (bank padding), output-group stride 7T
+        std::vector<int> sptr{0};
+        std::vector<uint16_t> soff;
+        const int nb = int(cnodes.size());
+        for (int ln = 0; ln < nloc; ++ln) {
+            cnodes.push_back(loc[size_t(ln)]);
+            for (uint8_t sl : inc[size_t(ln)])
+                soff.push_back(uint16_t((sl >> 2) * 29 * kResTile + (sl & 3) * 7 * kResTile));
+            sptr.push_back(int(soff.size()));
+            npp[size_t(loc[size_t(ln)]) + 1] += 1;
         }
-        cnp[size_t(ch) + 1] = int(cnodes.size());
+        const int bytes = int(residual_pack_bytes(nloc, ecount));
+        maxpk = std::max(maxpk, bytes);
+        rpk.resize(rpk.size() + size_t(bytes));
+        residual_pack_write(rpk.data() + rpk.size() - size_t(bytes), nloc, ecount, nb, loc.data(),
+                            sptr.data(), soff.data(), lconn.data());
+        rpp.push_back(rpp.back() + bytes / 16);
     }
     for (int A = 0; A < nn; ++A)
         npp[size_t(A) + 1] += npp[size_t(A)];
@@ -516,30 +528,14 @@ static int upload_all(hbgpu_ctx* c, const hbgpu_mesh_desc* d) {
     }
     c->nchunks = nch;
     c->max_nloc = maxnloc;
+    c->max_rpack = maxpk;
     c->npairs = long(cnodes.size());
-    CK(c, c->lconn.alloc(lconn.size()));
-    CK(c, c->chunk_node_ptr.alloc(cnp.size()));
-    CK(c, c->chunk_nodes.alloc(cnodes.size()));
-    CK(c, c->slot_ptr.alloc(sptr.size()));
-    CK(c, c->slot_idx.alloc(sidx.size()));
+    CK(c, c->rpack.alloc(rpk.size()));
+    CK(c, c->rpack_ptr.alloc(rpp.size()));
     CK(c, c->npart_ptr.alloc(npp.size()));
     CK(c, c->npart.alloc(npl.size()));
-    CK(c, cudaMemcpyAsync(c->lconn.p, lconn.data(), sizeof(uint32_t) * lconn.size(), cudaMemcpyHostToDevice, st));
-    CK(c, cudaMemcpyAsync(c->chunk_node_ptr.p, cnp.data(), sizeof(int) * cnp.size(), cudaMemcpyHostToDevice, st));
-    CK(c, cudaMemcpyAsync(c->chunk_nodes.p, cnodes.data(), sizeof(int) * cnodes.size(), cudaMemcpyHostToDevice, st));
-    CK(c, cudaMemcpyAsync(c->slot_ptr.p, sptr.data(), sizeof(int) * sptr.size(), cudaMemcpyHostToDevice, st));
-    CK(c, cudaMemcpyAsync(c->slot_idx.p, sidx.data(), sidx.size(), cudaMemcpyHostToDevice, st));
-    {
-        // the same slots as shared-memory offsets of the residual kernel's slot
-        // array: element stride 29T (bank padding), output-group stride 7T
-        std::vector<uint16_t> soff(sidx.size());
-        for (size_t q = 0; q < sidx.size(); ++q)
-            soff[q] = uint16_t((sidx[q] >> 2) * 29 * kResTile + (sidx[q] & 3) * 7 * kResTile);
-        CK(c, c->slot_off.alloc(soff.size()));
-        CK(c, cudaMemcpyAsync(c->slot_off.p, soff.data(), sizeof(uint16_t) * soff.size(),
-                              cudaMemcpyHostToDevice, st));
-        CK(c, cudaStreamSynchronize(st));
-    }
+    CK(c, cudaMemcpyAsync(c->rpack.p, rpk.data(), rpk.size(), cudaMemcpyHostToDevice, st));
+    CK(c, cudaMemcpyAsync(c->rpack_ptr.p, rpp.data(), sizeof(int) * rpp.size(), cudaMemcpyHostToDevice, st));
     CK(c, cudaMemcpyAsync(c->npart_ptr.p, npp.data(), sizeof(int) * npp.size(), cudaMemcpyHostToDevice, st));
     CK(c, cudaMemcpyAsync(c->npart.p, npl.data(), sizeof(int) * npl.size(), cudaMemcpyHostToDevice, st));
     CK(c, cudaStreamSynchronize(st));
@@ -568,17 +564,12 @@ static int residual_dev(hbgpu_ctx* c, const double* d_state, double* d_r) {
     ca.geom = c->geom.p;
     ca.state = d_state;
     ca.hu = c->hu.p;
-    ca.lconn = c->lconn.p;
-    ca.chunk_node_ptr = c->chunk_node_ptr.p;
-    ca.chunk_nodes = c->chunk_nodes.p;
-    ca.slot_ptr = c->slot_ptr.p;
-    ca.slot_idx = c->slot_idx.p;
-    ca.slot_off = c->slot_off.p;
+    ca.rpack = c->rpack.p;
+    ca.rpack_ptr = c->rpack_ptr.p;
+    ca.max_rpack = c->max_rpack;
     ca.partial = c->rpartial.p;
     ca.ne = c->ne;
     ca.N = N;
-    ca.T = kResTile;
-    ca.CE = kChunkElems;
     ca.max_nloc = c->max_nloc;
     ca.nchunks = c->nchunks;
     ca.npairs = c->npairs;
@@ -1080,7 +1071,7 @@ void hbgpu_destroy(hbgpu_ctx* c) {
                             &c->r, &c->hu, &c->pvals, &c->mass, &c->mass_c, &c->inv, &c->y, &c->out,
                             &c->x, &c->w, &c->z, &c->scale, &c->b, &c->tmp, &c->V, &c->partial, &c->red, &c->rpartial})
         b->release();
-    for (DBuf<int>* b : {&c->row_ptr, &c->col_idx, &c->diag_blk, &c->inc_ptr, &c->chunk_node_ptr, &c->chunk_nodes, &c->slot_ptr, &c->npart_ptr, &c->npart,
+    for (DBuf<int>* b : {&c->row_ptr, &c->col_idx, &c->diag_blk, &c->inc_ptr, &c->rpack_ptr, &c->npart_ptr, &c->npart,
                          &c->bnode, &c->bptr, &c->binc, &c->fac, &c->fbc, &c->flag,
                          &c->ideg})
         b->release();
@@ -1097,9 +1088,7 @@ void hbgpu_destroy(hbgpu_ctx* c) {
     c->blkc.release();
     c->blk_order.release();
     c->tgeom.release();
-    c->lconn.release();
-    c->slot_idx.release();
-    c->slot_off.release();
+    c->rpack.release();
     for (cudaEvent_t e : c->ev_pool)
         cudaEventDestroy(e);
     if (c->ev_fork)
@@ -1158,7 +1147,7 @@ int hbgpu_set_basis(hbgpu_ctx* c, int modes, double period) {
     CK(c, c->hu.alloc(size_t(c->nn) * 3 * size_t(N)));
     CK(c, c->rpartial.alloc(size_t(c->npairs) * 7 * size_t((N + kResTile - 1) / kResTile) * kResTile));
     {
-        const size_t rs = residual_smem_bytes(c->max_nloc, kChunkElems, kResTile);
+        const size_t rs = residual_smem_bytes(c->max_nloc, c->max_rpack);
         CK(c, configure_residual_smem(rs));
         int per_sm = 0, nsm = 0, dev = 0;
         CK(c, cudaGetDevice(&dev));

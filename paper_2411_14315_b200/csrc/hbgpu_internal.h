@@ -68,6 +68,34 @@ __device__ __forceinline__ double rsqrt_nr(double x) {
     y = fma(y, fma(-h * y, y, 0.5), y);
     return y;
 }
+
+// mbarrier + bulk async copy (cp.async.bulk, the TMA engine's 1-D mode)
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n\t"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n\t"
+        "@!P1 bra WAIT_%=;\n\t}" ::"r"(smem_u32(b)),
+        "r"(parity), "r"(0x989680u)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* b) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(b))
+        : "memory");
+}
 #endif
 
 // Number of kernel launches issued by this library (bench.py's gpu_launches).
@@ -83,14 +111,16 @@ struct ResidualChunkArgs {
     const double* geom;
     const double* state;
     const double* hu;
-    const uint32_t* lconn;       // per element: 4 x uint8 chunk-local node ids
-    const int* chunk_node_ptr;   // nchunks + 1
-    const int* chunk_nodes;      // global node id per (chunk, node) pair
-    const int* slot_ptr;         // per pair: range in slot_idx
-    const uint8_t* slot_idx;     // el_local*4 + a, element order
-    const uint16_t* slot_off;    // same slots as shared-memory offsets el*29T + a*7T
+    // per chunk, a contiguous "chunk pack" (16-byte aligned):
+    //   hdr int4 {nloc, ecount, nb (first pair), 0}, nodes int[nloc],
+    //   sptr int[nloc + 1] (chunk-relative slot ranges, element order),
+    //   soff u16[4 ecount] (slot -> shared-memory offset el*29T + a*7T),
+    //   lconn u32[ecount] (4 x u8 chunk-local node ids)
+    const unsigned char* rpack;
+    const int* rpack_ptr;        // nchunks + 1, 16-byte units
+    int max_rpack;               // bytes
     double* partial;             // pairs * 7N
-    int ne, N, T, CE, max_nloc, nchunks;
+    int ne, N, max_nloc, nchunks;
     long npairs;
     double rho, mu, nu;
     int tau_mode;
@@ -170,7 +200,10 @@ void launch_geometry(const double* xyz, const int4* conn, int ne, double* geom, 
                      cudaStream_t st);
 void launch_apply_h_series(const double* H, int N, const double* in, int in_node_stride,
                            double* out, int out_node_stride, int nnodes, cudaStream_t st);
-size_t residual_smem_bytes(int max_nloc, int CE, int T);
+size_t residual_smem_bytes(int max_nloc, int max_rpack);
+size_t residual_pack_bytes(int nloc, int ecount);
+void residual_pack_write(unsigned char* dst, int nloc, int ecount, int nb, const int* nodes,
+                         const int* sptr_rel, const uint16_t* soff, const uint32_t* lconn);
 void launch_residual_chunks(const ResidualChunkArgs& a, int grid, cudaStream_t st);
 cudaError_t configure_residual_smem(size_t bytes);
 cudaError_t residual_occupancy(int* blocks_per_sm, size_t smem);

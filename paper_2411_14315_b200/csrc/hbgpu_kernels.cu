@@ -15,6 +15,8 @@
 // mass, (chunk, element, local index) order for the residual).
 #include "hbgpu_internal.h"
 
+#include <cstring>
+
 namespace hbgpu {
 
 std::atomic<long long> g_launches{0};
@@ -197,6 +199,7 @@ __device__ __forceinline__ void element_residual_smem(const double* __restrict__
     for (int k = 0; k < 9; ++k)
         xx += g[13 + k] * g[13 + k];
     const double diff = 3.0 * nu * nu * xx;
+    bool bad = false;
     double tau_mean = 0.0;
     if (tau_mode == 1) {
         double um[3] = {0.25 * usum[0], 0.25 * usum[1], 0.25 * usum[2]};
@@ -205,9 +208,8 @@ __device__ __forceinline__ void element_residual_smem(const double* __restrict__
         for (int i = 0; i < 3; ++i)
             conv += um[i] * (g[13 + 3 * i] * um[0] + g[14 + 3 * i] * um[1] + g[15 + 3 * i] * um[2]);
         const double arg = conv + diff;
-        if (!(arg > 0.0))
-            atomicOr(flag, 1);
-        tau_mean = arg > 0.0 ? rsqrt(arg) : 0.0;
+        bad = !(arg > 0.0);
+        tau_mean = bad ? 0.0 : rsqrt_nr(fmax(arg, 1e-300));
     }
     const double dAB = kQA - kQB;
     double Cs[3] = {0, 0, 0}, TLs[3] = {0, 0, 0}, W[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
@@ -226,9 +228,9 @@ __device__ __forceinline__ void element_residual_smem(const double* __restrict__
             for (int i = 0; i < 3; ++i)
                 conv += uq[i] * (g[13 + 3 * i] * uq[0] + g[14 + 3 * i] * uq[1] + g[15 + 3 * i] * uq[2]);
             const double arg = conv + diff;
-            if (!(arg > 0.0))
-                atomicOr(flag, 1);
-            tau = arg > 0.0 ? rsqrt(arg) : 0.0;
+            const bool bq = !(arg > 0.0);
+            bad |= bq;
+            tau = bq ? 0.0 : rsqrt_nr(fmax(arg, 1e-300));
         }
         double* oq = out + q * 7 * T;
 #pragma unroll
@@ -244,6 +246,8 @@ __device__ __forceinline__ void element_residual_smem(const double* __restrict__
             oq[(4 + i) * T] = w * dAB * tl;     // node a = q part of the LS time row
         }
     }
+    if (bad)
+        atomicOr(flag, 1);
     const double muV = mu * V, moff = rho * V / 20.0, wr = w / rho;
 #pragma unroll
     for (int a = 0; a < 4; ++a) {
@@ -261,22 +265,22 @@ __device__ __forceinline__ void element_residual_smem(const double* __restrict__
     }
 }
 
-// Residual element pass as a persistent, double-buffered pipeline.  Work
-// item = (element chunk, time-sample tile); CTA b handles items b, b+G, ...
-// (tile fastest, so the tiles of a chunk reuse its data from L2).  While the
-// CTA computes item k from shared memory, cp.async (LDGSTS) gathers the nodal
-// data (u, p, Hu) and geometry of item k+1 into the other buffer.  Per item:
-// one (element, sample) per thread into per-element slots, then every chunk
-// node's slots are reduced in fixed (element, local index) order and written
-// as one partial record.  Partials are tile-major and contiguous per item:
-// partial[((tile*npairs + p)*7 + c)*T + t].  Deterministic, no atomics.
+// Residual element pass as a persistent pipeline.  CTA b walks element
+// chunks b, b+G, ... and, per chunk, its time-sample tiles of kResTile samples.
+//  * The chunk's metadata ("chunk pack": local nodes, per-node slot lists,
+//    local connectivity) and its 64 geometry records arrive by bulk async copy
+//    (cp.async.bulk on an mbarrier), issued one chunk ahead.
+//  * The nodal data (u, p, Hu) of the next tile is gathered with cp.async
+//    (LDGSTS) while the current tile computes: one thread per (chunk node,
+//    component) issues the tile's samples, addresses come from shared memory.
+//  * Per tile: one (element, sample) per thread into per-element slots, then
+//    every chunk node's slots are reduced in fixed (element, local index)
+//    order and written as one partial record.  Partials are tile-major and
+//    contiguous per chunk: partial[((tile*npairs + p)*7 + c)*T + t].
+// Deterministic, no atomics.
 __device__ __forceinline__ void cp_async8(double* smem_dst, const double* gsrc) {
     const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem_dst));
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gsrc));
-}
-__device__ __forceinline__ void cp_async16(double* smem_dst, const double* gsrc) {
-    const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem_dst));
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gsrc));
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 template <int K>
@@ -284,102 +288,172 @@ __device__ __forceinline__ void cp_async_wait() {
     asm volatile("cp.async.wait_group %0;\n" ::"n"(K));
 }
 
-__device__ __forceinline__ void residual_issue(const ResidualChunkArgs& a, int item, int ntiles,
-                                               double* nd, double* geo) {
-    // compile-time tile shape: the index arithmetic becomes shifts / multiplies
-    constexpr int T = kResTile, CE = kChunkElems, ndst = 7 * T;
-    const int N = a.N;
-    const int ch = item / ntiles, n0 = (item - ch * ntiles) * T;
-    const int nb = a.chunk_node_ptr[ch], nloc = a.chunk_node_ptr[ch + 1] - nb;
-    const int e0 = ch * CE, ecount = min(CE, a.ne - e0);
-    for (int k = threadIdx.x; k < nloc * ndst; k += blockDim.x) {
-        const int ln = k / ndst, rem = k - ln * ndst;
-        const int cc = rem / T, t = rem - cc * T;
-        const int n = n0 + t;
-        const long A = a.chunk_nodes[nb + ln];
-        if (n < N)
-            cp_async8(nd + k, cc < 4 ? a.state + (A * 4 + cc) * N + n
-                                     : a.hu + (A * 3 + (cc - 4)) * N + n);
-        else
-            nd[k] = 0.0;
-    }
-    const double* gsrc = a.geom + (long)e0 * 22;
-    for (int k = threadIdx.x; k < ecount * 11; k += blockDim.x)
-        cp_async16(geo + 2 * k, gsrc + 2 * k);
+__host__ __device__ inline int rp_align16(int bytes) { return (bytes + 15) & ~15; }
+struct ResPackSec {
+    int nodes, sptr, soff, lconn, total;
+};
+__host__ __device__ inline ResPackSec res_pack_sections(int nloc, int ecount) {
+    ResPackSec s;
+    s.nodes = 16;
+    s.sptr = s.nodes + rp_align16(4 * nloc);
+    s.soff = s.sptr + rp_align16(4 * (nloc + 1));
+    s.lconn = s.soff + rp_align16(2 * 4 * ecount);
+    s.total = s.lconn + rp_align16(4 * ecount);
+    return s;
+}
+size_t residual_pack_bytes(int nloc, int ecount) { return (size_t)res_pack_sections(nloc, ecount).total; }
+
+void residual_pack_write(unsigned char* dst, int nloc, int ecount, int nb, const int* nodes,
+                         const int* sptr_rel, const uint16_t* soff, const uint32_t* lconn) {
+    const ResPackSec s = res_pack_sections(nloc, ecount);
+    memset(dst, 0, (size_t)s.total);
+    int* h = reinterpret_cast<int*>(dst);
+    h[0] = nloc;
+    h[1] = ecount;
+    h[2] = nb;
+    memcpy(dst + s.nodes, nodes, sizeof(int) * (size_t)nloc);
+    memcpy(dst + s.sptr, sptr_rel, sizeof(int) * (size_t)(nloc + 1));
+    memcpy(dst + s.soff, soff, sizeof(uint16_t) * (size_t)(4 * ecount));
+    memcpy(dst + s.lconn, lconn, sizeof(uint32_t) * (size_t)ecount);
+}
+
+struct ResSmem {
+    int pk, geo, nd, slots, mbar, total;  // byte offsets
+};
+__host__ __device__ inline ResSmem res_layout(int max_nloc, int max_rpack) {
+    constexpr int T = kResTile, CE = kChunkElems;
+    ResSmem L;
+    L.pk = 0;                                              // 2 x max_rpack
+    L.geo = L.pk + 2 * rp_align16(max_rpack);              // 2 x [CE][22]
+    L.nd = L.geo + 2 * CE * 22 * 8;                        // 2 x [nloc][7][T]
+    L.slots = L.nd + 2 * max_nloc * 7 * T * 8;             // [CE][29T]
+    L.mbar = L.slots + CE * 29 * T * 8;
+    L.total = L.mbar + 16;
+    return L;
+}
+size_t residual_smem_bytes(int max_nloc, int max_rpack) {
+    return (size_t)res_layout(max_nloc, max_rpack).total;
 }
 
 __global__ void __launch_bounds__(256, RES_MINB) residual_chunk_kernel(ResidualChunkArgs a) {
-    extern __shared__ __align__(16) double sm[];
-    constexpr int T = kResTile, CE = kChunkElems;
-    const int N = a.N;
+    extern __shared__ __align__(128) unsigned char smraw[];
+    constexpr int T = kResTile, CE = kChunkElems, ndst = 7 * T, es = 29 * T;
+    const int N = a.N, nch = a.nchunks;
     const int ntiles = (N + T - 1) / T;
-    const int nitems = a.nchunks * ntiles;
-    const int ndst = 7 * T;
-    const int es = 29 * T;  // padded element slot stride (bank spread)
-    const int bufsz = a.max_nloc * ndst + CE * 22;
-    double* buf[2] = {sm, sm + bufsz};
-    double* slots = sm + 2 * bufsz;
+    const ResSmem Ls = res_layout(a.max_nloc, a.max_rpack);
+    const int mpk = rp_align16(a.max_rpack);
+    uint64_t* mbar = reinterpret_cast<uint64_t*>(smraw + Ls.mbar);
+    double* slots = reinterpret_cast<double*>(smraw + Ls.slots);
+    int ch = blockIdx.x;
+    if (ch >= nch)
+        return;
+    if (threadIdx.x == 0) {
+        mbar_init(mbar, 1);
+        mbar_init(mbar + 1, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
 
-    int item = blockIdx.x;
-    int cur = 0;
-    if (item < nitems)
-        residual_issue(a, item, ntiles, buf[0], buf[0] + a.max_nloc * ndst);
-    cp_async_commit();
-    for (; item < nitems; item += gridDim.x, cur ^= 1) {
-        const int next = item + gridDim.x;
-        if (next < nitems)
-            residual_issue(a, next, ntiles, buf[cur ^ 1], buf[cur ^ 1] + a.max_nloc * ndst);
-        cp_async_commit();
-        cp_async_wait<1>();
-        __syncthreads();
-
-        const int ch = item / ntiles, tile = item - ch * ntiles, n0 = tile * T;
-        const int nb = a.chunk_node_ptr[ch], nloc = a.chunk_node_ptr[ch + 1] - nb;
-        const int e0 = ch * CE, ecount = min(CE, a.ne - e0);
-        const double* nd = buf[cur];
-        const double* geo = buf[cur] + a.max_nloc * ndst;
-        {
-            const int el = threadIdx.x / T, t = threadIdx.x - el * T;
-            if (el < ecount && n0 + t < N) {
-                const uint32_t pk = a.lconn[e0 + el];
-                const int lc[4] = {int(pk & 0xFF), int((pk >> 8) & 0xFF), int((pk >> 16) & 0xFF),
-                                   int(pk >> 24)};
-                element_residual_smem(geo + el * 22, nd, ndst, lc, T, t, a.rho, a.mu, a.nu,
-                                      a.tau_mode, a.flag, slots + el * es + t);
+    auto issue_pack = [&](int c, int slot) {  // one thread
+        const int p0 = __ldg(a.rpack_ptr + c), p1 = __ldg(a.rpack_ptr + c + 1);
+        const int ecount = min(CE, a.ne - c * CE);
+        const uint32_t pb = (uint32_t)(p1 - p0) * 16u, gb = (uint32_t)ecount * 22u * 8u;
+        mbar_expect_tx(mbar + slot, pb + gb);
+        bulk_g2s(smraw + Ls.pk + slot * mpk, a.rpack + (size_t)p0 * 16, pb, mbar + slot);
+        bulk_g2s(smraw + Ls.geo + slot * CE * 22 * 8, a.geom + (size_t)c * CE * 22, gb, mbar + slot);
+    };
+    auto issue_tile = [&](int slot, int tile, int b) {  // all threads
+        const unsigned char* pk = smraw + Ls.pk + slot * mpk;
+        const int* h = reinterpret_cast<const int*>(pk);
+        const int nloc = h[0];
+        const ResPackSec s = res_pack_sections(nloc, h[1]);
+        const int* nodes = reinterpret_cast<const int*>(pk + s.nodes);
+        double* nd = reinterpret_cast<double*>(smraw + Ls.nd) + (size_t)b * a.max_nloc * ndst;
+        const int n0 = tile * T;
+        for (int k = threadIdx.x; k < nloc * 7; k += blockDim.x) {
+            const int ln = k / 7, cc = k - 7 * ln;
+            const long A = nodes[ln];
+            const double* src = cc < 4 ? a.state + (A * 4 + cc) * N + n0 : a.hu + (A * 3 + (cc - 4)) * N + n0;
+            double* dst = nd + ln * ndst + cc * T;
+#pragma unroll
+            for (int t = 0; t < T; ++t) {
+                if (n0 + t < N)
+                    cp_async8(dst + t, src + t);
+                else
+                    dst[t] = 0.0;
             }
         }
-        __syncthreads();
-        double* out = a.partial + ((long)tile * a.npairs + nb) * ndst;
-        // thread per (chunk node, sample): walk the node's slot offsets once,
-        // accumulating all 7 outputs
-        for (int k = threadIdx.x; k < nloc * T; k += blockDim.x) {
-            const int ln = k / T, t = k - ln * T;
-            const int p = nb + ln;
-            double acc[7] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
-            const int q1 = a.slot_ptr[p + 1];
-            for (int q = a.slot_ptr[p]; q < q1; ++q) {
-                const double* sp = slots + a.slot_off[q] + t;  // el*es + a*7T
+    };
+
+    if (threadIdx.x == 0)
+        issue_pack(ch, 0);
+    mbar_wait(mbar, 0);
+    issue_tile(0, 0, 0);
+    cp_async_commit();
+    int gt = 0;
+    for (int jj = 0; ch < nch; ++jj, ch += gridDim.x) {
+        const int ps = jj & 1, nextch = ch + gridDim.x;
+        const unsigned char* pk = smraw + Ls.pk + ps * mpk;
+        const int* h = reinterpret_cast<const int*>(pk);
+        const int nloc = h[0], ecount = h[1], nb = h[2];
+        const ResPackSec sec = res_pack_sections(nloc, ecount);
+        const int* sptr = reinterpret_cast<const int*>(pk + sec.sptr);
+        const uint16_t* soff = reinterpret_cast<const uint16_t*>(pk + sec.soff);
+        const uint32_t* lconn = reinterpret_cast<const uint32_t*>(pk + sec.lconn);
+        const double* geo = reinterpret_cast<const double*>(smraw + Ls.geo + ps * CE * 22 * 8);
+        for (int tile = 0; tile < ntiles; ++tile, ++gt) {
+            const int b = gt & 1, n0 = tile * T;
+            cp_async_wait<0>();
+            __syncthreads();  // tile data visible; previous reduction done
+            if (tile == 0 && threadIdx.x == 0 && nextch < nch)
+                issue_pack(nextch, ps ^ 1);
+            if (tile + 1 < ntiles) {
+                issue_tile(ps, tile + 1, b ^ 1);
+            } else if (nextch < nch) {
+                mbar_wait(mbar + (ps ^ 1), ((jj + 1) >> 1) & 1);
+                issue_tile(ps ^ 1, 0, b ^ 1);
+            }
+            cp_async_commit();
+            const double* nd = reinterpret_cast<const double*>(smraw + Ls.nd) + (size_t)b * a.max_nloc * ndst;
+            {
+                const int el = threadIdx.x / T, t = threadIdx.x - el * T;
+                if (el < ecount && n0 + t < N) {
+                    const uint32_t pkc = lconn[el];
+                    const int lc[4] = {int(pkc & 0xFF), int((pkc >> 8) & 0xFF), int((pkc >> 16) & 0xFF),
+                                       int(pkc >> 24)};
+                    element_residual_smem(geo + el * 22, nd, ndst, lc, T, t, a.rho, a.mu, a.nu,
+                                          a.tau_mode, a.flag, slots + el * es + t);
+                }
+            }
+            __syncthreads();
+            double* out = a.partial + ((long)tile * a.npairs + nb) * ndst;
+            // thread per (chunk node, sample): walk the node's slot offsets once,
+            // accumulating all 7 outputs
+            for (int k = threadIdx.x; k < nloc * T; k += blockDim.x) {
+                const int ln = k / T, t = k - ln * T;
+                double acc[7] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+                const int q1 = sptr[ln + 1];
+                for (int q = sptr[ln]; q < q1; ++q) {
+                    const double* sp = slots + soff[q] + t;  // el*es + a*7T
+#pragma unroll
+                    for (int cc = 0; cc < 7; ++cc)
+                        acc[cc] += sp[cc * T];
+                }
 #pragma unroll
                 for (int cc = 0; cc < 7; ++cc)
-                    acc[cc] += sp[cc * T];
+                    out[(ln * 7 + cc) * T + t] = acc[cc];
             }
-#pragma unroll
-            for (int cc = 0; cc < 7; ++cc)
-                out[(ln * 7 + cc) * T + t] = acc[cc];
         }
     }
     cp_async_wait<0>();
-}
-
-size_t residual_smem_bytes(int max_nloc, int CE, int T) {
-    return sizeof(double) * (2 * ((size_t)max_nloc * 7 * T + (size_t)CE * 22) + (size_t)CE * 29 * T);
 }
 
 void launch_residual_chunks(const ResidualChunkArgs& a, int grid, cudaStream_t st) {
     if (a.nchunks <= 0)
         return;
     note_launch();
-    residual_chunk_kernel<<<grid, a.CE * a.T, residual_smem_bytes(a.max_nloc, a.CE, a.T), st>>>(a);
+    residual_chunk_kernel<<<min(grid, a.nchunks), kChunkElems * kResTile,
+                            residual_smem_bytes(a.max_nloc, a.max_rpack), st>>>(a);
 }
 
 cudaError_t configure_residual_smem(size_t bytes) {
