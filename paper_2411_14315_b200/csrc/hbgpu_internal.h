@@ -58,15 +58,33 @@ constexpr int kTanPart = 8;
 
 // 1/sqrt(x) for x > 0: MUFU seed + two Newton steps, branch-free (the
 // library rsqrt carries special-case branches the element kernels never need;
-// x <= 0 / NaN is flagged and masked by the callers).  Within a few ulp.
+// x <= 0 / NaN is flagged and masked by the callers).  Within a few ulp.  One
+// volatile asm block, so the compiler cannot sink it into a branch on the
+// caller's select (which would cost a BSSY/BRA pair per quadrature point).
 #ifdef __CUDACC__
 __device__ __forceinline__ double rsqrt_nr(double x) {
     double y;
-    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
-    const double h = 0.5 * x;
-    y = fma(y, fma(-h * y, y, 0.5), y);
-    y = fma(y, fma(-h * y, y, 0.5), y);
+    asm volatile(
+        "{\n\t.reg .f64 h, t, e, y0;\n\t"
+        "rsqrt.approx.ftz.f64 y0, %1;\n\t"
+        "mul.rn.f64 h, %1, 0d3FE0000000000000;\n\t"
+        "mul.rn.f64 t, h, y0;\n\t"
+        "neg.f64 t, t;\n\t"
+        "fma.rn.f64 e, t, y0, 0d3FE0000000000000;\n\t"
+        "fma.rn.f64 y0, y0, e, y0;\n\t"
+        "mul.rn.f64 t, h, y0;\n\t"
+        "neg.f64 t, t;\n\t"
+        "fma.rn.f64 e, t, y0, 0d3FE0000000000000;\n\t"
+        "fma.rn.f64 %0, y0, e, y0;\n\t}"
+        : "=d"(y)
+        : "d"(x));
     return y;
+}
+// tau = arg^-1/2, or 0 when arg <= 0 / NaN (`bad`, flagged by the caller).
+// The argument is sanitised and the result masked by a multiply, so the
+// Newton iteration is always executed and never sits behind a branch.
+__device__ __forceinline__ double tau_or_zero(double arg, bool bad) {
+    return rsqrt_nr(bad ? 1.0 : arg) * (bad ? 0.0 : 1.0);
 }
 
 // mbarrier + bulk async copy (cp.async.bulk, the TMA engine's 1-D mode)

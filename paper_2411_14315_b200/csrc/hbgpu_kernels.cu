@@ -209,7 +209,7 @@ __device__ __forceinline__ void element_residual_smem(const double* __restrict__
             conv += um[i] * (g[13 + 3 * i] * um[0] + g[14 + 3 * i] * um[1] + g[15 + 3 * i] * um[2]);
         const double arg = conv + diff;
         bad = !(arg > 0.0);
-        tau_mean = bad ? 0.0 : rsqrt_nr(fmax(arg, 1e-300));
+        tau_mean = tau_or_zero(arg, bad);
     }
     const double dAB = kQA - kQB;
     double Cs[3] = {0, 0, 0}, TLs[3] = {0, 0, 0}, W[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
@@ -230,7 +230,7 @@ __device__ __forceinline__ void element_residual_smem(const double* __restrict__
             const double arg = conv + diff;
             const bool bq = !(arg > 0.0);
             bad |= bq;
-            tau = bq ? 0.0 : rsqrt_nr(fmax(arg, 1e-300));
+            tau = tau_or_zero(arg, bq);
         }
         double* oq = out + q * 7 * T;
 #pragma unroll

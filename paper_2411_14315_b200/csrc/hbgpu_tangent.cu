@@ -224,7 +224,7 @@ __global__ void __launch_bounds__(kTanThreads, TAN5_MINB) tangent_row5_kernel(Ta
             const double um[3] = {0.25 * usum[0], 0.25 * usum[1], 0.25 * usum[2]};
             const double arg = quad(um);
             bad = !(arg > 0.0);
-            tau_mean = bad ? 0.0 : rsqrt_nr(fmax(arg, 1e-300));
+            tau_mean = tau_or_zero(arg, bad);
         }
         double asum = 0.0, tsum = 0.0, z[3] = {0.0, 0.0, 0.0}, kap[3] = {0.0, 0.0, 0.0};
 #pragma unroll
@@ -238,7 +238,7 @@ __global__ void __launch_bounds__(kTanThreads, TAN5_MINB) tangent_row5_kernel(Ta
                 const double arg = quad(uq);
                 const bool bq = !(arg > 0.0);
                 bad |= bq;
-                tq = bq ? 0.0 : rsqrt_nr(fmax(arg, 1e-300));
+                tq = tau_or_zero(arg, bq);
             }
             const double tadv = tq * fma(uq[0], ga[0], fma(uq[1], ga[1], uq[2] * ga[2]));
             const double na = (q == la) ? kQA : kQB;

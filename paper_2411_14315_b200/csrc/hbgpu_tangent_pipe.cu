@@ -159,6 +159,7 @@ __global__ void __launch_bounds__(kTanThreads, TAN6_MINB) tangent_pipe_kernel(Ta
     double* dpart = reinterpret_cast<double*>(smraw + Ls.dpart);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const double rho = a.rho, diffc = 3.0 * a.nu * a.nu, dAB = kQA - kQB;
+    const double c1 = kQB * (1.0 + dAB), c2 = dAB * dAB;
     const double mu = a.mu, pc = a.pseudo_c;
 
     const int r0 = blockIdx.x, rs = gridDim.x, nrows = pa.nrows;
@@ -303,7 +304,7 @@ __global__ void __launch_bounds__(kTanThreads, TAN6_MINB) tangent_pipe_kernel(Ta
                 const double um[3] = {0.25 * usum[0], 0.25 * usum[1], 0.25 * usum[2]};
                 const double arg = quad(um);
                 bad = !(arg > 0.0);
-                tau_mean = bad ? 0.0 : rsqrt_nr(fmax(arg, 1e-300));
+                tau_mean = tau_or_zero(arg, bad);
             }
             double asum = 0.0, tsum = 0.0, z[3] = {0.0, 0.0, 0.0}, kap[3] = {0.0, 0.0, 0.0};
 #pragma unroll
@@ -317,17 +318,23 @@ __global__ void __launch_bounds__(kTanThreads, TAN6_MINB) tangent_pipe_kernel(Ta
                     const double arg = quad(uq);
                     const bool bq = !(arg > 0.0);
                     bad |= bq;
-                    tq = bq ? 0.0 : rsqrt_nr(fmax(arg, 1e-300));
+                    tq = tau_or_zero(arg, bq);
                 }
                 const double tadv = tq * fma(uq[0], ga[0], fma(uq[1], ga[1], uq[2] * ga[2]));
-                const double na = (q == la) ? kQA : kQB;
                 asum += tadv;
                 tsum += tq;
 #pragma unroll
                 for (int c = 0; c < 3; ++c) {
                     z[c] = fma(tq, uq[c], z[c]);
-                    kap[c] = fma(na + tadv, uq[c], kap[c]);
+                    kap[c] = fma(tadv, uq[c], kap[c]);
                 }
+            }
+            // + sum_q N_a(q) u_q = B usum + (A-B) u_{q=a} = c1 usum + c2 u_A (u_A: the row node)
+            {
+                const double* sA = su + (size_t)kdiag * 4 * N + n;
+#pragma unroll
+                for (int c = 0; c < 3; ++c)
+                    kap[c] = fma(c1, usum[c], fma(c2, sA[c * N], kap[c]));
             }
             if (bad)
                 atomicOr(a.flag, 1);
