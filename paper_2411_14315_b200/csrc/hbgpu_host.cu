@@ -561,7 +561,7 @@ static int residual_dev(hbgpu_ctx* c, const double* d_state, double* d_r) {
         CK(c, cudaMemsetAsync(c->hu.p, 0, sizeof(double) * size_t(c->nn) * 3, st));
     const long p1 = prof_mark(c);
     ResidualChunkArgs ca;
-    ca.geom = c->geom.p;
+    ca.tgeom = c->tgeom.p;
     ca.state = d_state;
     ca.hu = c->hu.p;
     ca.rpack = c->rpack.p;

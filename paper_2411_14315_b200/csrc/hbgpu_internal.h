@@ -32,7 +32,7 @@ constexpr int kTanPart = 8;
 
 // Build-time tuning knobs of the residual element pass.
 #ifndef RES_VOLATILE_LDS
-#define RES_VOLATILE_LDS 1
+#define RES_VOLATILE_LDS 0
 #endif
 #ifndef RES_MINB
 #define RES_MINB 2
@@ -126,7 +126,7 @@ cudaError_t run_fp64_peak(int blocks, int threads, int iters, double* out, float
 // nodes (sorted) are chunk_nodes[chunk_node_ptr[c] ..]; every (chunk, node)
 // pair p owns one partial-sum record of 7N doubles (r_u0..2, r_p, s0..2).
 struct ResidualChunkArgs {
-    const double* geom;
+    const double* tgeom;         // compact geometry records (kTGeo doubles per element)
     const double* state;
     const double* hu;
     // per chunk, a contiguous "chunk pack" (16-byte aligned):

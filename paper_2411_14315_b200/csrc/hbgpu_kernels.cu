@@ -194,20 +194,19 @@ __device__ __forceinline__ void element_residual_smem(const double* __restrict__
         }
     }
     const double div = gu[0][0] + gu[1][1] + gu[2][2];
-    double xx = 0.0;
-#pragma unroll
-    for (int k = 0; k < 9; ++k)
-        xx += g[13 + k] * g[13 + k];
-    const double diff = 3.0 * nu * nu * xx;
+    // compact geometry record (tangent_geometry_kernel): xi00 xi01 xi02 xi11 xi12 xi22 at
+    // 13..18, xi:xi at 19; u . xi . u in symmetric form
+    const double diff = 3.0 * nu * nu * g[19];
+    auto quad = [&](const double v[3]) {
+        const double q0 = fma(2.0 * g[15], v[2], fma(2.0 * g[14], v[1], g[13] * v[0]));
+        const double q1 = fma(2.0 * g[17], v[2], g[16] * v[1]);
+        return fma(v[0], q0, fma(v[1], q1, fma(v[2], g[18] * v[2], diff)));
+    };
     bool bad = false;
     double tau_mean = 0.0;
     if (tau_mode == 1) {
-        double um[3] = {0.25 * usum[0], 0.25 * usum[1], 0.25 * usum[2]};
-        double conv = 0.0;
-#pragma unroll
-        for (int i = 0; i < 3; ++i)
-            conv += um[i] * (g[13 + 3 * i] * um[0] + g[14 + 3 * i] * um[1] + g[15 + 3 * i] * um[2]);
-        const double arg = conv + diff;
+        const double um[3] = {0.25 * usum[0], 0.25 * usum[1], 0.25 * usum[2]};
+        const double arg = quad(um);
         bad = !(arg > 0.0);
         tau_mean = tau_or_zero(arg, bad);
     }
@@ -223,11 +222,7 @@ __device__ __forceinline__ void element_residual_smem(const double* __restrict__
         }
         double tau = tau_mean;
         if (tau_mode == 0) {
-            double conv = 0.0;
-#pragma unroll
-            for (int i = 0; i < 3; ++i)
-                conv += uq[i] * (g[13 + 3 * i] * uq[0] + g[14 + 3 * i] * uq[1] + g[15 + 3 * i] * uq[2]);
-            const double arg = conv + diff;
+            const double arg = quad(uq);
             const bool bq = !(arg > 0.0);
             bad |= bq;
             tau = tau_or_zero(arg, bq);
@@ -324,8 +319,8 @@ __host__ __device__ inline ResSmem res_layout(int max_nloc, int max_rpack) {
     constexpr int T = kResTile, CE = kChunkElems;
     ResSmem L;
     L.pk = 0;                                              // 2 x max_rpack
-    L.geo = L.pk + 2 * rp_align16(max_rpack);              // 2 x [CE][22]
-    L.nd = L.geo + 2 * CE * 22 * 8;                        // 2 x [nloc][7][T]
+    L.geo = L.pk + 2 * rp_align16(max_rpack);              // 2 x [CE][kTGeo]
+    L.nd = L.geo + 2 * CE * kTGeo * 8;                     // 2 x [nloc][7][T]
     L.slots = L.nd + 2 * max_nloc * 7 * T * 8;             // [CE][29T]
     L.mbar = L.slots + CE * 29 * T * 8;
     L.total = L.mbar + 16;
@@ -357,10 +352,10 @@ __global__ void __launch_bounds__(256, RES_MINB) residual_chunk_kernel(ResidualC
     auto issue_pack = [&](int c, int slot) {  // one thread
         const int p0 = __ldg(a.rpack_ptr + c), p1 = __ldg(a.rpack_ptr + c + 1);
         const int ecount = min(CE, a.ne - c * CE);
-        const uint32_t pb = (uint32_t)(p1 - p0) * 16u, gb = (uint32_t)ecount * 22u * 8u;
+        const uint32_t pb = (uint32_t)(p1 - p0) * 16u, gb = (uint32_t)ecount * kTGeo * 8u;
         mbar_expect_tx(mbar + slot, pb + gb);
         bulk_g2s(smraw + Ls.pk + slot * mpk, a.rpack + (size_t)p0 * 16, pb, mbar + slot);
-        bulk_g2s(smraw + Ls.geo + slot * CE * 22 * 8, a.geom + (size_t)c * CE * 22, gb, mbar + slot);
+        bulk_g2s(smraw + Ls.geo + slot * CE * kTGeo * 8, a.tgeom + (size_t)c * CE * kTGeo, gb, mbar + slot);
     };
     auto issue_tile = [&](int slot, int tile, int b) {  // all threads
         const unsigned char* pk = smraw + Ls.pk + slot * mpk;
@@ -400,7 +395,7 @@ __global__ void __launch_bounds__(256, RES_MINB) residual_chunk_kernel(ResidualC
         const int* sptr = reinterpret_cast<const int*>(pk + sec.sptr);
         const uint16_t* soff = reinterpret_cast<const uint16_t*>(pk + sec.soff);
         const uint32_t* lconn = reinterpret_cast<const uint32_t*>(pk + sec.lconn);
-        const double* geo = reinterpret_cast<const double*>(smraw + Ls.geo + ps * CE * 22 * 8);
+        const double* geo = reinterpret_cast<const double*>(smraw + Ls.geo + ps * CE * kTGeo * 8);
         for (int tile = 0; tile < ntiles; ++tile, ++gt) {
             const int b = gt & 1, n0 = tile * T;
             cp_async_wait<0>();
@@ -421,7 +416,7 @@ __global__ void __launch_bounds__(256, RES_MINB) residual_chunk_kernel(ResidualC
                     const uint32_t pkc = lconn[el];
                     const int lc[4] = {int(pkc & 0xFF), int((pkc >> 8) & 0xFF), int((pkc >> 16) & 0xFF),
                                        int(pkc >> 24)};
-                    element_residual_smem(geo + el * 22, nd, ndst, lc, T, t, a.rho, a.mu, a.nu,
+                    element_residual_smem(geo + el * kTGeo, nd, ndst, lc, T, t, a.rho, a.mu, a.nu,
                                           a.tau_mode, a.flag, slots + el * es + t);
                 }
             }
