@@ -323,11 +323,11 @@ def run_ours(args):
     tan_flops = CANON_TAN_FLOP * ne * N
     traffic = load_traffic()
     kernels = {
-        "tangent_row_kernel": {"ms": tan_ms, "tflops": tan_flops / (tan_ms * 1e-3) / 1e12},
+        "tangent_pipe_kernel": {"ms": tan_ms, "tflops": tan_flops / (tan_ms * 1e-3) / 1e12},
         "residual (all passes)": {"ms": res_all_ms, "tflops": res_flops / (res_all_ms * 1e-3) / 1e12},
         "residual_chunk_kernel": {"ms": res_elem_ms, "tflops": res_flops / (res_elem_ms * 1e-3) / 1e12},
     }
-    dom = "tangent_row_kernel" if tan_ms >= res_all_ms else "residual (all passes)"
+    dom = "tangent_pipe_kernel" if tan_ms >= res_all_ms else "residual (all passes)"
     dk = kernels[dom]
     roofline = {
         "kernel": dom, "bound": "fp64", "achieved": dk["tflops"], "peak": fp64_peak,
@@ -361,7 +361,7 @@ def run_ours(args):
     mv_bytes = spmv_bytes(nnz, nn, N)
     spmv = {"ms": mv_ms, "gbs": mv_bytes / (mv_ms * 1e-3) / 1e9, "peak_gbs": hbm_peak,
             "frac": mv_bytes / (mv_ms * 1e-3) / 1e9 / hbm_peak, "compulsory_bytes": mv_bytes,
-            "traffic": traffic.get("matvec_kernel"), "reps": reps,
+            "traffic": traffic.get("lmatvec_kernel"), "reps": reps,
             "peak_source": "MEASURED_PEAKS.json hbm_gbs (of measured)"}
 
     # ---- one full Newton iteration at Newton iterate 0 (residual, tangent, Jacobi,
@@ -528,6 +528,106 @@ def sweep_config4(args):
                       "hbm_peak_gbs": hbm, "results": out}), flush=True)
 
 
+def sweep_configs(args):
+    """BASELINE configs 0-3 at full size: assembly (residual, tangent, both on
+    two streams), 100 L-matvecs, and one Newton iteration at Newton iterate 0
+    (assembly + Jacobi + GMRES with the reference defaults).  Prints one JSON
+    line (not the driver's bench line)."""
+    import torch
+
+    from paper_2411_14315_b200 import cases, hbgpu
+
+    hbm = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"]
+    peak = np.zeros(1)
+    hbgpu._lib.hbgpu_fp64_peak.argtypes = [hbgpu._vp]
+    hbgpu._lib.hbgpu_fp64_peak(peak.ctypes.data)
+    L = hbgpu._lib
+    out = []
+    for cfg in [int(c) for c in args.configs.split(",")]:
+        t0 = time.time()
+        prob = cases.config_problem(cfg)
+        t_mesh = time.time() - t0
+        mesh, M, N = prob.mesh, prob.modes, prob.N
+        ne, nn = mesh.num_elements, mesh.num_nodes
+        ctx = hbgpu.GpuContext(mesh)
+        ctx.set_basis(M, prob.period)
+        ctx.set_fluid(prob.rho, prob.mu)
+        ctx.set_bcs(prob.dirichlet_g, prob.neumann, prob.backflow_beta)
+        ctx.set_assembly_config(0, auto_pseudo_dt(prob))
+        stream = torch.cuda.ExternalStream(ctx.stream)
+        s = torch.from_numpy(cases.random_state(nn, N, 1000 + cfg)).cuda()
+        r = torch.empty_like(s)
+        y = torch.from_numpy(np.random.default_rng(cfg).uniform(-1, 1, nn * 4 * N)).cuda()
+        o = torch.empty_like(y)
+        flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")
+        for _ in range(3):
+            ctx.assemble_dev(s.data_ptr(), r.data_ptr())
+        ctx.assemble_mass()
+        ctx.matvec_dev(y.data_ptr(), o.data_ptr())
+        torch.cuda.synchronize()
+        ctx.synchronize()
+
+        def timed(fn, reps=5):
+            ts = []
+            for _ in range(reps):
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                with torch.cuda.stream(stream):
+                    flush.fill_(1.0)
+                    a.record(stream)
+                    fn()
+                    b.record(stream)
+                torch.cuda.synchronize()
+                ctx.synchronize()
+                ts.append(a.elapsed_time(b))
+            return float(np.median(ts))
+
+        t_res = timed(lambda: ctx.assemble_residual_dev(s.data_ptr(), r.data_ptr()))
+        t_tan = timed(lambda: ctx.assemble_tangent_dev(s.data_ptr()))
+        t_both = timed(lambda: ctx.assemble_dev(s.data_ptr(), r.data_ptr()))
+
+        def mv100():
+            for _ in range(100):
+                ctx.matvec_dev(y.data_ptr(), o.data_ptr())
+
+        t_mv = timed(mv100, 3) / 100
+        mvb = spmv_bytes(ctx.nnz, nn, N)
+        d_s0 = torch.from_numpy(cases.initial_state(prob)).cuda()
+        d_x = torch.empty_like(d_s0)
+        torch.cuda.synchronize()
+        L.hbgpu_profile_enable(ctx.handle, 1)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        ctx.assemble_dev(d_s0.data_ptr(), r.data_ptr())
+        ctx.jacobi_dev()
+        g_it, g_rr, g_st = ctx.gmres_dev(r.data_ptr(), d_x.data_ptr(), hbgpu.KrylovConfig())
+        b.record(stream)
+        torch.cuda.synchronize()
+        ph_ms = np.zeros(9)
+        ph_n = np.zeros(9, np.int32)
+        L.hbgpu_profile_read(ctx.handle, 9, ph_ms.ctypes.data, ph_n.ctypes.data)
+        L.hbgpu_profile_enable(ctx.handle, 0)
+        out.append({
+            "config": cfg, "elements": ne, "nodes": nn, "nnz_blocks": ctx.nnz, "Nm": M, "N": N,
+            "mesh_seconds": t_mesh,
+            "residual_ms": t_res, "tangent_ms": t_tan, "assembly_ms": t_both,
+            "assembly_elements_modes_per_s": ne * M / (t_both * 1e-3),
+            "residual_tflops": CANON_RES_FLOP * ne * N / (t_res * 1e-3) / 1e12,
+            "tangent_tflops": CANON_TAN_FLOP * ne * N / (t_tan * 1e-3) / 1e12,
+            "matvec_ms": t_mv, "matvec_gbs": mvb / (t_mv * 1e-3) / 1e9, "matvec_frac_hbm": mvb / (t_mv * 1e-3) / 1e9 / hbm,
+            "newton_iter0": {"ms": a.elapsed_time(b), "gmres_iters": g_it, "gmres_relres": g_rr,
+                             "gmres_status": g_st, "gmres_ms": float(ph_ms[7]), "matvec_ms": float(ph_ms[5])},
+        })
+        print(json.dumps(out[-1]), file=sys.stderr, flush=True)
+        del ctx, s, r, y, o, d_s0, d_x, flush
+        torch.cuda.empty_cache()
+    print(json.dumps({"sweep": "configs", "fp64_peak_tflops": float(peak[0]), "hbm_peak_gbs": hbm,
+                      "notes": "config 2: T-junction Delaunay (seeded points), two Dirichlet inlets; "
+                               "config 3: curved tapered 60% stenosis, zero-traction outlet (the "
+                               "BASELINE resistance outlet is not in the reference); random states "
+                               "for assembly/matvec timing, Newton iterate 0 for the GMRES step",
+                      "results": out}), flush=True)
+
+
 def solve_config0():
     from paper_2411_14315_b200 import cases, hbgpu
 
@@ -558,9 +658,13 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--sweep4", action="store_true", help="config-4 operator sweep (separate run)")
     ap.add_argument("--sweep-points", type=int, default=700_000)
+    ap.add_argument("--configs", default=None, help="e.g. 0,1,2,3: per-config operator/Newton sweep")
     args = ap.parse_args()
     if args.sweep4:
         sweep_config4(args)
+        return
+    if args.configs:
+        sweep_configs(args)
         return
     if args.impl == "reference":
         run_reference(args)

@@ -44,11 +44,22 @@ def inflow_coefficients(cfg: int, seed: int | None = None):
         a = rng.uniform(-0.3, 0.3, 2)
         b = rng.uniform(-0.3, 0.3, 2)
         return 2.0, a, b
-    if cfg == 1:
+    if cfg in (1, 2):
         k = np.arange(1, 10)
         phase = rng.uniform(0.0, 2.0 * np.pi, 9)
         amp = 0.5 / k
         return 2.0, amp * np.cos(phase), amp * np.sin(phase)
+    if cfg == 3:
+        # coronary-like, diastole-dominant: a broad diastolic bump minus a
+        # short systolic dip, 16 harmonics, each perturbed by a seeded +-10 %
+        t = np.arange(4096) / 4096.0
+        bump = lambda c, w: np.exp(-(((t - c + 0.5) % 1.0 - 0.5) / w) ** 2)
+        f = 0.9 * bump(0.65, 0.18) - 0.45 * bump(0.12, 0.06)
+        f = f - f.mean()
+        c = np.fft.rfft(f) / len(t)
+        k = np.arange(1, 17)
+        jit = 1.0 + 0.1 * rng.standard_normal(16)
+        return 1.0, 2.0 * c[k].real * jit, -2.0 * c[k].imag * jit
     raise ValueError(f"no inflow for config {cfg}")
 
 
@@ -109,14 +120,29 @@ def parabolic_dirichlet(mesh: Mesh, inlet: int, q: np.ndarray) -> np.ndarray:
     return g.reshape(-1)
 
 
-def config_problem(cfg: int, modes: int | None = None) -> Problem:
-    """BASELINE.json configs 0 and 1 (hex-mapped pipe, parabolic pulsatile
-    inflow, no-slip wall, zero-traction outlet, rho 1.06, mu 0.04, T = 1)."""
-    mesh = meshgen.config_mesh(cfg)
-    M = modes if modes is not None else {0: 3, 1: 10}[cfg]
+def config_problem(cfg: int, modes: int | None = None, mesh: Mesh | None = None) -> Problem:
+    """BASELINE.json configs 0-3 (rho 1.06, mu 0.04, T = 1, no-slip walls,
+    zero-traction outlets, parabolic pulsatile inflow).
+      0/1: hex-mapped pipe, one inlet (Nm 3 / 10);
+      2:   T-junction, two Dirichlet inlets carrying Q1, Q2 with seeded means
+           U(15, 25) mL/s and the config-1 harmonic shape (Nm 10) — beyond
+           build_case's single inlet (cases.cpp:653-658): dirichlet_g is
+           supplied directly, as SURVEY.md §8(d) prescribes;
+      3:   curved tapered stenosis, coronary-like inflow with 16 seeded
+           harmonics (Nm 16: k = 16 is out of band and truncated); the
+           BASELINE resistance outlet (R = 1e4) is not in the reference, so
+           parity and timing use zero traction.
+    `mesh` overrides the full-size generator (tests use small meshes)."""
+    mesh = meshgen.config_mesh(cfg) if mesh is None else mesh
+    M = modes if modes is not None else {0: 3, 1: 10, 2: 10, 3: 16}[cfg]
     Q0, a, b = inflow_coefficients(cfg)
-    q = flow_samples(Q0, a, b, M, 1.0)
-    g = parabolic_dirichlet(mesh, mesh.patch_index("inlet"), q)
+    if cfg == 2:
+        means = np.random.default_rng(cfg + 100).uniform(15.0, 25.0, 2)
+        g = sum(parabolic_dirichlet(mesh, mesh.patch_index(name), flow_samples(qm, a, b, M, 1.0))
+                for name, qm in zip(("inlet1", "inlet2"), means))
+    else:
+        q = flow_samples(Q0, a, b, M, 1.0)
+        g = parabolic_dirichlet(mesh, mesh.patch_index("inlet"), q)
     N = 2 * M - 1
     neumann = [(k, np.zeros(N)) for k, p in enumerate(mesh.patches) if p.kind == NEUMANN]
     return Problem(mesh, M, 1.0, 1.06, 0.04, g, neumann, 0.2)

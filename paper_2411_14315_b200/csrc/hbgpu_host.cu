@@ -88,8 +88,9 @@ struct hbgpu_ctx {
     DBuf<int> contrib_ptr;
     DBuf<uint16_t> contrib;
     int max_inc = 0;
-    // tangent rows bucketed by valence (<= 24 / <= 32 incidences / more), so
-    // the few high-valence rows do not set the shared-memory size of every CTA
+    // tangent rows bucketed by valence (incidences <= 24 / 32 / 48 / 64 / 96 /
+    // more), so high-valence rows do not set the shared-memory size (and CTA
+    // width) of every CTA
     struct TanBucket {
         DBuf<int4> desc;  // per row {A, i0, ninc, k0}, {nblk, cb, kdiag, 0}
         int count = 0, max_inc = 0, max_blk = 0, nt = 1;
@@ -97,9 +98,9 @@ struct hbgpu_ctx {
         // persistent row pipeline (used when its shared memory fits)
         DBuf<unsigned char> pack;
         DBuf<int> pack_ptr;
-        int max_pack = 0, grid = 0;
+        int max_pack = 0, grid = 0, threads = 128;
         bool pipe = false;
-    } tb[3];
+    } tb[6];
     DBuf<double> blkc;        // per block: n-invariant tangent sums (8)
     DBuf<uint8_t> blk_order;  // per row: off-diagonal blocks by descending contribution count
     DBuf<double> tgeom;
@@ -392,16 +393,16 @@ static int upload_all(hbgpu_ctx* c, const hbgpu_mesh_desc* d) {
             for (size_t s2 = 0; s2 < js.size(); ++s2)
                 order[size_t(k0) + s2] = uint8_t(js[s2]);
         }
-        std::vector<int> brows[3];
+        std::vector<int> brows[6];
         for (int A = 0; A < nn; ++A) {
             const int ni = iptr[size_t(A) + 1] - iptr[size_t(A)];
-            const int bk = ni <= 24 ? 0 : ni <= 32 ? 1 : 2;
+            const int bk = ni <= 24 ? 0 : ni <= 32 ? 1 : ni <= 48 ? 2 : ni <= 64 ? 3 : ni <= 96 ? 4 : 5;
             brows[bk].push_back(A);
             c->tb[bk].max_inc = std::max(c->tb[bk].max_inc, ni);
             c->tb[bk].max_blk = std::max(c->tb[bk].max_blk,
                                          c->row_ptr_h[size_t(A) + 1] - c->row_ptr_h[size_t(A)]);
         }
-        for (int bk = 0; bk < 3; ++bk) {
+        for (int bk = 0; bk < 6; ++bk) {
             c->tb[bk].count = int(brows[bk].size());
             if (!c->tb[bk].count)
                 continue;
@@ -667,7 +668,7 @@ static int tangent_dev(hbgpu_ctx* c, const double* d_state) {
             pa.pack_ptr = b.pack_ptr.p;
             pa.nrows = b.count;
             pa.max_pack = b.max_pack;
-            launch_tangent_pipe(a, pa, b.grid, b.smem, c->stream);
+            launch_tangent_pipe(a, pa, b.threads, b.grid, b.smem, c->stream);
         } else {
             launch_tangent_row(a, b.count, b.smem, c->stream);
         }
@@ -1166,31 +1167,51 @@ int hbgpu_set_basis(hbgpu_ctx* c, int modes, double period) {
     c->p_valid = c->inv_valid = false;
     c->mass_valid = false;
     {
-        // per bucket: the persistent row pipeline with the largest time-sample
-        // tile that fits TAN6_SMEM_KB (3 CTAs / SM); rows whose neighbour
-        // records cannot be double-buffered at all use the tiled row kernel
-        size_t mx = 0, mxp = 0;
+        // per bucket: the persistent row pipeline at the narrowest CTA (128 /
+        // 256 / 512 threads) whose shared memory holds the whole time series at
+        // 16 resident warps per SM; otherwise 512 threads and the largest
+        // time-sample tile that fits.  Rows whose neighbour records cannot be
+        // buffered at all use the tiled row kernel.
+        size_t mx = 0, mxp[3] = {0, 0, 0};
         int dev = 0, nsm = 0;
         // test knob: HBGPU_TANGENT_KERNEL=rows forces the row-kernel fallback
         const char* tk = std::getenv("HBGPU_TANGENT_KERNEL");
         const bool force_rows = tk && std::strcmp(tk, "rows") == 0;
         CK(c, cudaGetDevice(&dev));
         CK(c, cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+        const int widths[3] = {128, 256, 512};
         for (auto& b : c->tb) {
             if (!b.count)
                 continue;
-            int nt = N;
-            while (nt > 1 && tangent_pipe_smem(b.max_pack, b.max_inc, b.max_blk, N, nt) > TAN6_SMEM_KB * 1024)
-                nt = (nt + 1) / 2;
-            const size_t ps = tangent_pipe_smem(b.max_pack, b.max_inc, b.max_blk, N, nt);
-            b.pipe = TAN_PIPE && !force_rows && ps <= 227 * 1024;
+            auto ps = [&](int nt) { return tangent_pipe_smem(b.max_pack, b.max_inc, b.max_blk, N, nt); };
+            b.pipe = false;
+            if (TAN_PIPE && !force_rows) {
+                for (int w = 0; w < 3 && !b.pipe; ++w) {
+                    const size_t budget = size_t(227 * 1024) / size_t(512 / widths[w]) - 1024;
+                    if (ps(N) <= budget) {
+                        b.pipe = true;
+                        b.threads = widths[w];
+                        b.nt = N;
+                    }
+                }
+                if (!b.pipe) {
+                    int nt = N;
+                    while (nt > 1 && ps(nt) > size_t(226 * 1024))
+                        nt = (nt + 1) / 2;
+                    if (ps(nt) <= size_t(226 * 1024)) {
+                        b.pipe = true;
+                        b.threads = 512;
+                        b.nt = nt;
+                    }
+                }
+            }
             if (b.pipe) {
-                b.nt = nt;
-                b.smem = ps;
-                mxp = std::max(mxp, ps);
+                b.smem = ps(b.nt);
+                const int w = b.threads == 128 ? 0 : b.threads == 256 ? 1 : 2;
+                mxp[w] = std::max(mxp[w], b.smem);
                 continue;
             }
-            nt = N;
+            int nt = N;
             const int dp = (b.max_inc + kTanPart - 1) / kTanPart;
             while (nt > 1 && tangent_row_smem(b.max_inc, b.max_blk, dp, nt) > TAN_SMEM_KB * 1024)
                 nt = (nt + 1) / 2;
@@ -1202,18 +1223,18 @@ int hbgpu_set_basis(hbgpu_ctx* c, int modes, double period) {
             return fail(c, HBGPU_ERR_INVALID, "node valence too high for the tangent row kernel");
         if (mx)
             CK(c, configure_tangent_row_smem(mx));
-        if (mxp) {
-            CK(c, configure_tangent_pipe_smem(mxp));
-            for (auto& b : c->tb) {
-                if (!b.count || !b.pipe)
-                    continue;
-                int per_sm = 0;
-                CK(c, tangent_pipe_occupancy(&per_sm, b.smem));
-                if (per_sm < 1)
-                    return fail(c, HBGPU_ERR_INVALID, "tangent pipeline does not fit on an SM");
-                const int tiles = (N + b.nt - 1) / b.nt;
-                b.grid = std::max(1, std::min(b.count, (nsm * per_sm + tiles - 1) / tiles));
-            }
+        for (int w = 0; w < 3; ++w)
+            if (mxp[w])
+                CK(c, configure_tangent_pipe_smem(widths[w], mxp[w]));
+        for (auto& b : c->tb) {
+            if (!b.count || !b.pipe)
+                continue;
+            int per_sm = 0;
+            CK(c, tangent_pipe_occupancy(b.threads, &per_sm, b.smem));
+            if (per_sm < 1)
+                return fail(c, HBGPU_ERR_INVALID, "tangent pipeline does not fit on an SM");
+            const int tiles = (N + b.nt - 1) / b.nt;
+            b.grid = std::max(1, std::min(b.count, (nsm * per_sm + tiles - 1) / tiles));
         }
     }
     // clear previous Neumann data sized for another N

@@ -43,12 +43,6 @@ constexpr int kTanPart = 8;
 #ifndef TAN_PIPE
 #define TAN_PIPE 1
 #endif
-#ifndef TAN6_MINB
-#define TAN6_MINB 4
-#endif
-#ifndef TAN6_SMEM_KB
-#define TAN6_SMEM_KB 56
-#endif
 #ifndef TAN_SMEM_KB
 #define TAN_SMEM_KB 64
 #endif
@@ -245,9 +239,9 @@ void tangent_pack_write(unsigned char* dst, int A, int k0, int ninc, int nblk, i
 void launch_tangent_pack_refresh(unsigned char* pack, const int* pack_ptr, int nrows,
                                  const uint8_t* dir, const double* blkc, cudaStream_t st);
 size_t tangent_pipe_smem(int max_pack, int max_inc, int max_blk, int N, int NT);
-cudaError_t configure_tangent_pipe_smem(size_t bytes);
-cudaError_t tangent_pipe_occupancy(int* blocks_per_sm, size_t smem);
-void launch_tangent_pipe(const TangentArgs& a, const PipeArgs& p, int grid_x, size_t smem,
+cudaError_t configure_tangent_pipe_smem(int threads, size_t bytes);
+cudaError_t tangent_pipe_occupancy(int threads, int* blocks_per_sm, size_t smem);
+void launch_tangent_pipe(const TangentArgs& a, const PipeArgs& p, int threads, int grid_x, size_t smem,
                          cudaStream_t st);
 void launch_backflow_tangent(const BoundaryArgs& a, const int* row_ptr, const int* col_idx,
                              double* pvals, cudaStream_t st);

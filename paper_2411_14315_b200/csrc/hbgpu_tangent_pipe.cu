@@ -147,8 +147,10 @@ size_t tangent_pipe_smem(int max_pack, int max_inc, int max_blk, int N, int NT) 
     return (size_t)pipe_layout(max_pack, max_inc, max_blk, N, NT).total;
 }
 
-template <int TAU>
-__global__ void __launch_bounds__(kTanThreads, TAN6_MINB) tangent_pipe_kernel(TangentArgs a, PipeArgs pa) {
+// THREADS per CTA is chosen per valence bucket (128 / 256 / 512) so a row's
+// summaries fit shared memory at 16 resident warps per SM.
+template <int TAU, int THREADS>
+__global__ void __launch_bounds__(THREADS, 512 / THREADS) tangent_pipe_kernel(TangentArgs a, PipeArgs pa) {
     extern __shared__ __align__(128) unsigned char smraw[];
     const int N = a.N, NT = a.NT, n0 = blockIdx.y * NT, nt = min(NT, N - n0);
     const PipeSmem Ls = pipe_layout(pa.max_pack, a.max_inc, a.max_blk, N, NT);
@@ -427,29 +429,53 @@ __global__ void __launch_bounds__(kTanThreads, TAN6_MINB) tangent_pipe_kernel(Ta
     diag_sum();
 }
 
-cudaError_t configure_tangent_pipe_smem(size_t bytes) {
+template <int T>
+static cudaError_t configure_pipe_t(size_t bytes) {
     const int b = int(bytes < 48 * 1024 ? 48 * 1024 : bytes);
-    cudaError_t e = cudaFuncSetAttribute(tangent_pipe_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, b);
+    cudaError_t e = cudaFuncSetAttribute(tangent_pipe_kernel<0, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, b);
     if (e != cudaSuccess)
         return e;
-    return cudaFuncSetAttribute(tangent_pipe_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, b);
+    return cudaFuncSetAttribute(tangent_pipe_kernel<1, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, b);
 }
 
-cudaError_t tangent_pipe_occupancy(int* blocks_per_sm, size_t smem) {
-    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, tangent_pipe_kernel<0>,
-                                                         kTanThreads, smem);
+cudaError_t configure_tangent_pipe_smem(int threads, size_t bytes) {
+    switch (threads) {
+    case 128: return configure_pipe_t<128>(bytes);
+    case 256: return configure_pipe_t<256>(bytes);
+    case 512: return configure_pipe_t<512>(bytes);
+    default: return cudaErrorInvalidValue;
+    }
 }
 
-void launch_tangent_pipe(const TangentArgs& a, const PipeArgs& p, int grid_x, size_t smem,
+cudaError_t tangent_pipe_occupancy(int threads, int* blocks_per_sm, size_t smem) {
+    switch (threads) {
+    case 128: return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, tangent_pipe_kernel<0, 128>, 128, smem);
+    case 256: return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, tangent_pipe_kernel<0, 256>, 256, smem);
+    case 512: return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, tangent_pipe_kernel<0, 512>, 512, smem);
+    default: return cudaErrorInvalidValue;
+    }
+}
+
+template <int T>
+static void launch_pipe_t(const TangentArgs& a, const PipeArgs& p, dim3 grid, size_t smem, cudaStream_t st) {
+    if (a.tau_mode == 1)
+        tangent_pipe_kernel<1, T><<<grid, T, smem, st>>>(a, p);
+    else
+        tangent_pipe_kernel<0, T><<<grid, T, smem, st>>>(a, p);
+}
+
+void launch_tangent_pipe(const TangentArgs& a, const PipeArgs& p, int threads, int grid_x, size_t smem,
                          cudaStream_t st) {
     if (p.nrows <= 0)
         return;
     note_launch();
     const dim3 grid(grid_x, (a.N + a.NT - 1) / a.NT);
-    if (a.tau_mode == 1)
-        tangent_pipe_kernel<1><<<grid, kTanThreads, smem, st>>>(a, p);
+    if (threads == 512)
+        launch_pipe_t<512>(a, p, grid, smem, st);
+    else if (threads == 256)
+        launch_pipe_t<256>(a, p, grid, smem, st);
     else
-        tangent_pipe_kernel<0><<<grid, kTanThreads, smem, st>>>(a, p);
+        launch_pipe_t<128>(a, p, grid, smem, st);
 }
 
 }  // namespace hbgpu

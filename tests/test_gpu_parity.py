@@ -192,9 +192,14 @@ def test_pattern_bit_exact(gpu):
     assert np.abs(g - ob.restated_geometry(mesh.xyz, mesh.conn)).max() <= 1e-12 * np.abs(g).max()
 
 
-@pytest.mark.parametrize("cfg", [0, 1])
+@pytest.mark.parametrize("cfg", [0, 1, 2, 3])
 def test_config_residual_tangent_matvec(gpu, cfg):
-    prob = cases.config_problem(cfg)
+    """Configs 0/1 at full size; configs 2/3 (T-junction Delaunay, curved
+    stenosis) on reduced meshes of the same generators, full N (19 / 31)."""
+    from paper_2411_14315_b200 import meshgen
+
+    small = {2: lambda: meshgen.tjunction_delaunay(20000, seed=2), 3: lambda: meshgen.stenosis_tube(10, 120)}
+    prob = cases.config_problem(cfg, mesh=small[cfg]() if cfg in small else None)
     nn, N = prob.mesh.num_nodes, prob.N
     ctx = gpu_ctx(prob, 0, 0.05)
     orc = ob.Restated(prob, tau_mode=0, pseudo_dt=0.05)

@@ -96,3 +96,41 @@ def test_random_modes_state_is_real_and_band_limited():
     assert np.allclose(c.imag[:, 0], 0, atol=1e-14)
     # |c_k| ~ 1/k^2 scaling: modes 1..3 present, no content beyond M-1
     assert v.shape == (20, 7)
+
+
+@pytest.mark.parametrize("cfg", [2, 3])
+def test_config2_3_generators(cfg):
+    """Small instances of the T-junction (Delaunay) and curved stenosis
+    (swept, Kuhn) generators: positive volumes, every boundary facet in a
+    patch, inflow carried by the inlets, and — when the compiled reference is
+    present — Mesh::finalize agreement and residual parity of the restated
+    oracle against the reference on the config's boundary data."""
+    mesh = meshgen.tjunction_delaunay(3000, seed=2) if cfg == 2 else meshgen.stenosis_tube(4, 24)
+    g = ob.restated_geometry(mesh.xyz, mesh.conn)
+    assert (g[:, 12] > 0).all()
+    names = [p.name for p in mesh.patches]
+    if cfg == 2:
+        assert names == ["inlet1", "inlet2", "outlet1", "outlet2", "wall"]
+    else:
+        assert names == ["inlet", "outlet", "wall"]
+        # 60 % area stenosis at mid-length: the narrowest slice radius
+        nxy = 25
+        rad = np.linalg.norm(mesh.xyz[:, 1:2], axis=1).reshape(-1, nxy).max(axis=1)
+        assert abs((rad.min() / 0.175) ** 2 - 0.4) < 0.05
+    prob = cases.config_problem(cfg, modes=2, mesh=mesh)
+    inlets = [k for k, p in enumerate(mesh.patches) if p.name.startswith("inlet")]
+    N = prob.N
+    gg = prob.dirichlet_g.reshape(mesh.num_nodes, 3, N)
+    for k in inlets:
+        p = mesh.patches[k]
+        tri = np.array([[2 / 3, 1 / 6, 1 / 6], [1 / 6, 2 / 3, 1 / 6], [1 / 6, 1 / 6, 2 / 3]])
+        un = np.einsum("fvin,fi->fvn", gg[p.facets], -p.normals)  # inflow through the patch
+        flux = (p.areas[:, None] / 3.0 * np.einsum("qv,fvn->fqn", tri, un).sum(axis=1)).sum(axis=0)
+        assert (flux > 0).all()
+    if HAVE_REF:
+        theirs = ob.RefMesh.from_mesh(mesh).to_mesh()
+        assert np.array_equal(mesh.conn, theirs.conn)
+        s = cases.random_state(mesh.num_nodes, N, 9)
+        r_ref = ob.ref_context(prob).residual(s)
+        r_orc = ob.Restated(prob).residual(s)
+        assert np.linalg.norm(r_orc - r_ref) <= 1e-12 * np.linalg.norm(r_ref)
