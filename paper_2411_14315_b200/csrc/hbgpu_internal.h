@@ -56,8 +56,23 @@ constexpr int kTanPart = 8;
 // volatile asm block, so the compiler cannot sink it into a branch on the
 // caller's select (which would cost a BSSY/BRA pair per quadrature point).
 #ifdef __CUDACC__
+#ifndef RSQRT_NEWTON
+#define RSQRT_NEWTON 2
+#endif
 __device__ __forceinline__ double rsqrt_nr(double x) {
     double y;
+#if RSQRT_NEWTON == 1
+    asm volatile(
+        "{\n\t.reg .f64 h, t, e, y0;\n\t"
+        "rsqrt.approx.ftz.f64 y0, %1;\n\t"
+        "mul.rn.f64 h, %1, 0d3FE0000000000000;\n\t"
+        "mul.rn.f64 t, h, y0;\n\t"
+        "neg.f64 t, t;\n\t"
+        "fma.rn.f64 e, t, y0, 0d3FE0000000000000;\n\t"
+        "fma.rn.f64 %0, y0, e, y0;\n\t}"
+        : "=d"(y)
+        : "d"(x));
+#else
     asm volatile(
         "{\n\t.reg .f64 h, t, e, y0;\n\t"
         "rsqrt.approx.ftz.f64 y0, %1;\n\t"
@@ -72,6 +87,7 @@ __device__ __forceinline__ double rsqrt_nr(double x) {
         "fma.rn.f64 %0, y0, e, y0;\n\t}"
         : "=d"(y)
         : "d"(x));
+#endif
     return y;
 }
 // tau = arg^-1/2, or 0 when arg <= 0 / NaN (`bad`, flagged by the caller).

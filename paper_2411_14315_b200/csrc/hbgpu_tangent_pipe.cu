@@ -149,10 +149,14 @@ size_t tangent_pipe_smem(int max_pack, int max_inc, int max_blk, int N, int NT) 
 
 // THREADS per CTA is chosen per valence bucket (128 / 256 / 512) so a row's
 // summaries fit shared memory at 16 resident warps per SM.
-template <int TAU, int THREADS>
+// NC > 0: the time-sample count is the compile-time constant NC (and the
+// whole series is one tile), so every N-strided shared/global address folds
+// to an immediate offset; NC = 0 is the generic kernel.
+template <int TAU, int THREADS, int NC>
 __global__ void __launch_bounds__(THREADS, 512 / THREADS) tangent_pipe_kernel(TangentArgs a, PipeArgs pa) {
     extern __shared__ __align__(128) unsigned char smraw[];
-    const int N = a.N, NT = a.NT, n0 = blockIdx.y * NT, nt = min(NT, N - n0);
+    const int N = NC ? NC : a.N, NT = NC ? NC : a.NT;
+    const int n0 = NC ? 0 : blockIdx.y * NT, nt = NC ? NC : min(NT, N - n0);
     const PipeSmem Ls = pipe_layout(pa.max_pack, a.max_inc, a.max_blk, N, NT);
     const int mpack = pack_align16(pa.max_pack);
     uint64_t* mbar = reinterpret_cast<uint64_t*>(smraw + Ls.mbar);  // [0..1] packs, [2] gathers
@@ -429,13 +433,27 @@ __global__ void __launch_bounds__(THREADS, 512 / THREADS) tangent_pipe_kernel(Ta
     diag_sum();
 }
 
+// Compile-time time-sample counts of the BASELINE configs (N = 2 Nm - 1).
+#define HBGPU_PIPE_NC_LIST(X) X(5) X(7) X(19) X(31) X(47)
+
+template <int T, int NC>
+static cudaError_t configure_pipe_tn(int b) {
+    cudaError_t e = cudaFuncSetAttribute(tangent_pipe_kernel<0, T, NC>, cudaFuncAttributeMaxDynamicSharedMemorySize, b);
+    if (e != cudaSuccess)
+        return e;
+    return cudaFuncSetAttribute(tangent_pipe_kernel<1, T, NC>, cudaFuncAttributeMaxDynamicSharedMemorySize, b);
+}
+
 template <int T>
 static cudaError_t configure_pipe_t(size_t bytes) {
     const int b = int(bytes < 48 * 1024 ? 48 * 1024 : bytes);
-    cudaError_t e = cudaFuncSetAttribute(tangent_pipe_kernel<0, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, b);
-    if (e != cudaSuccess)
-        return e;
-    return cudaFuncSetAttribute(tangent_pipe_kernel<1, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, b);
+    cudaError_t e = configure_pipe_tn<T, 0>(b);
+#define HBGPU_CFG_NC(n)            \
+    if (e == cudaSuccess)          \
+        e = configure_pipe_tn<T, n>(b);
+    HBGPU_PIPE_NC_LIST(HBGPU_CFG_NC)
+#undef HBGPU_CFG_NC
+    return e;
 }
 
 cudaError_t configure_tangent_pipe_smem(int threads, size_t bytes) {
@@ -449,19 +467,35 @@ cudaError_t configure_tangent_pipe_smem(int threads, size_t bytes) {
 
 cudaError_t tangent_pipe_occupancy(int threads, int* blocks_per_sm, size_t smem) {
     switch (threads) {
-    case 128: return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, tangent_pipe_kernel<0, 128>, 128, smem);
-    case 256: return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, tangent_pipe_kernel<0, 256>, 256, smem);
-    case 512: return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, tangent_pipe_kernel<0, 512>, 512, smem);
+    case 128: return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, tangent_pipe_kernel<0, 128, 0>, 128, smem);
+    case 256: return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, tangent_pipe_kernel<0, 256, 0>, 256, smem);
+    case 512: return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, tangent_pipe_kernel<0, 512, 0>, 512, smem);
     default: return cudaErrorInvalidValue;
     }
 }
 
+template <int T, int NC>
+static void launch_pipe_tn(const TangentArgs& a, const PipeArgs& p, dim3 grid, size_t smem, cudaStream_t st) {
+    if (a.tau_mode == 1)
+        tangent_pipe_kernel<1, T, NC><<<grid, T, smem, st>>>(a, p);
+    else
+        tangent_pipe_kernel<0, T, NC><<<grid, T, smem, st>>>(a, p);
+}
+
 template <int T>
 static void launch_pipe_t(const TangentArgs& a, const PipeArgs& p, dim3 grid, size_t smem, cudaStream_t st) {
-    if (a.tau_mode == 1)
-        tangent_pipe_kernel<1, T><<<grid, T, smem, st>>>(a, p);
-    else
-        tangent_pipe_kernel<0, T><<<grid, T, smem, st>>>(a, p);
+    if (a.NT == a.N) {
+        switch (a.N) {
+#define HBGPU_LAUNCH_NC(n) \
+    case n:                \
+        return launch_pipe_tn<T, n>(a, p, grid, smem, st);
+            HBGPU_PIPE_NC_LIST(HBGPU_LAUNCH_NC)
+#undef HBGPU_LAUNCH_NC
+        default:
+            break;
+        }
+    }
+    launch_pipe_tn<T, 0>(a, p, grid, smem, st);
 }
 
 void launch_tangent_pipe(const TangentArgs& a, const PipeArgs& p, int threads, int grid_x, size_t smem,
