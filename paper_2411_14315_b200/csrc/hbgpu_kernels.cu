@@ -100,20 +100,28 @@ __global__ void apply_h_series_kernel(const double* __restrict__ H, int N,
                                       double* __restrict__ out, int os, int nnodes) {
     extern __shared__ double sh[];
     double* sH = sh;
+    const int per = blockDim.x / N;
+    double* sx = sh + N * N;  // the CTA's `per` series, staged once (coalesced)
     for (int k = threadIdx.x; k < N * N; k += blockDim.x)
         sH[k] = H[k];
-    __syncthreads();
-    const int per = blockDim.x / N;
     const int ls = threadIdx.x / N, n = threadIdx.x - ls * N;
     const long s = (long)blockIdx.x * per + ls;
-    if (ls >= per || s >= 3L * nnodes)
+    const bool valid = ls < per && s < 3L * nnodes;
+    if (valid) {
+        const long A = s / 3;
+        const int i = (int)(s - 3 * A);
+        sx[ls * N + n] = __ldg(in + A * is + (long)i * N + n);
+    }
+    __syncthreads();
+    if (!valid)
         return;
     const long A = s / 3;
     const int i = (int)(s - 3 * A);
-    const double* src = in + A * is + (long)i * N;
+    const double* h = sH + n * N;
+    const double* x = sx + ls * N;
     double acc = 0.0;
     for (int m = 0; m < N; ++m)
-        acc += sH[n * N + m] * src[m];
+        acc += h[m] * x[m];
     out[A * os + (long)i * N + n] = acc;
 }
 
@@ -123,7 +131,7 @@ void launch_apply_h_series(const double* H, int N, const double* in, int in_node
     const long nser = 3L * nnodes;
     const int blocks = (int)((nser + per - 1) / per);
     note_launch();
-    apply_h_series_kernel<<<blocks, per * N, sizeof(double) * N * N, st>>>(
+    apply_h_series_kernel<<<blocks, per * N, sizeof(double) * ((size_t)N * N + (size_t)per * N), st>>>(
         H, N, in, in_node_stride, out, out_node_stride, nnodes);
 }
 
@@ -478,12 +486,29 @@ __global__ void __launch_bounds__(256) residual_nodes_kernel(const double* __res
     const bool valid = rr < rows_per_cta && A < nn;
     double v[7] = {0, 0, 0, 0, 0, 0, 0};
     if (valid) {
-        for (int q = npart_ptr[A]; q < npart_ptr[A + 1]; ++q) {
-            const int tile = n / T, t = n - tile * T;
-            const double* pp = partial + ((long)tile * npairs + npart[q]) * 7 * T + t;
+        // two records per iteration (fixed order: q, then q+1) so 14 loads are in flight
+        const int tile = n / T, t = n - tile * T;
+        const double* base = partial + (long)tile * npairs * 7 * T + t;
+        int q = npart_ptr[A];
+        const int q1 = npart_ptr[A + 1];
+        for (; q + 1 < q1; q += 2) {
+            const double* p0 = base + (long)__ldg(npart + q) * 7 * T;
+            const double* p1 = base + (long)__ldg(npart + q + 1) * 7 * T;
+            double x0[7], x1[7];
+#pragma unroll
+            for (int cc = 0; cc < 7; ++cc) {
+                x0[cc] = __ldcs(p0 + cc * T);
+                x1[cc] = __ldcs(p1 + cc * T);
+            }
 #pragma unroll
             for (int cc = 0; cc < 7; ++cc)
-                v[cc] += pp[cc * T];
+                v[cc] = (v[cc] + x0[cc]) + x1[cc];
+        }
+        if (q < q1) {
+            const double* p0 = base + (long)__ldg(npart + q) * 7 * T;
+#pragma unroll
+            for (int cc = 0; cc < 7; ++cc)
+                v[cc] += __ldcs(p0 + cc * T);
         }
 #pragma unroll
         for (int i = 0; i < 3; ++i)

@@ -1,6 +1,6 @@
 """Summarise ncu captures into committed text (run here, no GPU needed).
 
-    python profiles/summarize.py <tag> <launches.csv> <full.ncu-rep>
+    python profiles/summarize.py <tag> <launches.csv> <full.ncu-rep> [<more.ncu-rep> ...]
 
 Writes profiles/<tag>_launches.txt (per-kernel share of the launch list:
 cold-cache, serialised per-launch times — compare shares, not absolutes),
@@ -63,9 +63,12 @@ def full(path):
     raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
     hdr, units = rows[0], rows[1]
-    out, traffic = [], {}
+    out, traffic, seen = [], {}, set()
     for r in rows[2:]:
-        name = r[hdr.index("Kernel Name")].split("(")[0].replace("hbgpu::", "")
+        name = r[hdr.index("Kernel Name")].split("(")[0].replace("hbgpu::", "").replace("void ", "")
+        if name in seen:  # one capture per kernel
+            continue
+        seen.add(name)
         out.append(f"== {name}")
         for key, label in KEYS:
             if key in hdr:
@@ -90,10 +93,16 @@ def full(path):
 
 
 def main():
-    tag, lcsv, rep = sys.argv[1:4]
+    tag, lcsv, reps = sys.argv[1], sys.argv[2], sys.argv[3:]
     with open(os.path.join(HERE, f"{tag}_launches.txt"), "w") as f:
         f.write(launches(lcsv) + "\n")
-    text, traffic = full(rep)
+    text, traffic = "", {}
+    for rep in reps:
+        t, tr = full(rep)
+        text += t + "\n"
+        for k, v in tr.items():
+            traffic.setdefault(k, v)
+    text = text.rstrip("\n")
     with open(os.path.join(HERE, f"{tag}_ncu_full.txt"), "w") as f:
         f.write(text + "\n")
     with open(os.path.join(HERE, "ncu_traffic.json"), "w") as f:
