@@ -44,96 +44,98 @@ __device__ __forceinline__ void block_sum_vec(double (&v)[VB], double (*red)[VB]
 // V_0..V_{nv-1} gives a_i = <V_i, u> and b_i = <V_i, w>, plus <u,u>, <u,w>,
 // <w,w>.  Row layout of `partial`: a (nv) | b (nv) | uu | uw | ww.  Without w
 // (final step of a cycle): a (nv) | uu.
+// The CTA's chunk is split into one contiguous segment per warp; all warps
+// walk the same group of four basis vectors (so every warp has the same
+// work), two elements per lane per iteration keep 12 loads in flight, and
+// the per-warp sums are combined in warp order (fixed tree, deterministic).
 __global__ void __launch_bounds__(kRedThreads) dcgs_dots_kernel(const double* __restrict__ V,
                                                                 long ld, int nv,
                                                                 const double* __restrict__ u,
                                                                 const double* __restrict__ w,
                                                                 long n, double* partial) {
+    constexpr int NW = kRedThreads / 32;
+    __shared__ double red[2][NW][8];
     long lo, hi;
     chunk_of(n, lo, hi);
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const long seg = (hi - lo + NW - 1) / NW;
+    const long wlo = min(hi, lo + wid * seg), whi = min(hi, wlo + seg);
     const bool hw = w != nullptr;
-    // tasks: groups of four basis vectors (u and w read once per group), then
-    // the three scalar products
     const int ngroups = (nv + 3) / 4;
-    for (int task = wid; task < ngroups; task += nw) {
-        const int r0 = 4 * task, nr = min(4, nv - r0);
+    // groups 0..ngroups-1: basis vectors; group ngroups: the scalar products
+    for (int g = 0; g <= ngroups; ++g) {
+        const int buf = g & 1;
         double du[4] = {0.0, 0.0, 0.0, 0.0}, dw[4] = {0.0, 0.0, 0.0, 0.0};
-        for (long k = lo + lane; k < hi; k += 32) {
-            const double uk = u[k];
-            const double wk = hw ? w[k] : 0.0;
+        if (g < ngroups) {
+            const int r0 = 4 * g, nr = min(4, nv - r0);
+            const double* v0 = V + (long)r0 * ld;
+            long k = wlo + lane;
+            for (; k + 32 < whi; k += 64) {
+                const double ua = u[k], ub = u[k + 32];
+                const double wa = hw ? w[k] : 0.0, wb = hw ? w[k + 32] : 0.0;
 #pragma unroll
-            for (int q = 0; q < 4; ++q)
-                if (q < nr) {
-                    const double x = V[(long)(r0 + q) * ld + k];
-                    du[q] += x * uk;
-                    dw[q] += x * wk;
+                for (int q = 0; q < 4; ++q)
+                    if (q < nr) {
+                        const double xa = __ldcs(v0 + (long)q * ld + k), xb = __ldcs(v0 + (long)q * ld + k + 32);
+                        du[q] += xa * ua + xb * ub;
+                        dw[q] += xa * wa + xb * wb;
+                    }
+            }
+            for (; k < whi; k += 32) {
+                const double ua = u[k], wa = hw ? w[k] : 0.0;
+#pragma unroll
+                for (int q = 0; q < 4; ++q)
+                    if (q < nr) {
+                        const double xa = __ldcs(v0 + (long)q * ld + k);
+                        du[q] += xa * ua;
+                        dw[q] += xa * wa;
+                    }
+            }
+        } else {
+            for (long k = wlo + lane; k < whi; k += 32) {
+                const double uk = u[k];
+                du[0] += uk * uk;
+                if (hw) {
+                    const double wk = w[k];
+                    du[1] += uk * wk;
+                    du[2] += wk * wk;
                 }
+            }
         }
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
+        for (int q = 0; q < 4; ++q)
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) {
                 du[q] += __shfl_down_sync(0xffffffffu, du[q], o);
                 dw[q] += __shfl_down_sync(0xffffffffu, dw[q], o);
             }
-            if (lane == 0 && q < nr) {
-                partial[(long)(r0 + q) * kRedBlocks + blockIdx.x] = du[q];
-                if (hw)
-                    partial[(long)(nv + r0 + q) * kRedBlocks + blockIdx.x] = dw[q];
-            }
-        }
-    }
-    if (wid == (ngroups % nw)) {  // the scalar task goes to the least loaded warp
-        const int r = nv;
-        double du0 = 0.0, du1 = 0.0, dw0 = 0.0, dw1 = 0.0, dx0 = 0.0, dx1 = 0.0;
-        if (r < nv) {
-            const double* x = V + (long)r * ld;
-            long k = lo + lane;
-            for (; k + 32 < hi; k += 64) {
-                const double x0 = x[k], x1 = x[k + 32];
-                du0 += x0 * u[k];
-                du1 += x1 * u[k + 32];
-                if (hw) {
-                    dw0 += x0 * w[k];
-                    dw1 += x1 * w[k + 32];
-                }
-            }
-            for (; k < hi; k += 32) {
-                du0 += x[k] * u[k];
-                if (hw)
-                    dw0 += x[k] * w[k];
-            }
-        } else {
-            long k = lo + lane;
-            for (; k < hi; k += 32) {
-                const double uk = u[k];
-                du0 += uk * uk;
-                if (hw) {
-                    const double wk = w[k];
-                    dw0 += uk * wk;
-                    dx0 += wk * wk;
-                }
-            }
-        }
-        double su = du0 + du1, sw = dw0 + dw1, sx = dx0 + dx1;
+        if (lane == 0)
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            su += __shfl_down_sync(0xffffffffu, su, o);
-            sw += __shfl_down_sync(0xffffffffu, sw, o);
-            sx += __shfl_down_sync(0xffffffffu, sx, o);
-        }
-        if (lane == 0) {
-            if (r < nv) {
-                partial[(long)r * kRedBlocks + blockIdx.x] = su;
+            for (int q = 0; q < 4; ++q) {
+                red[buf][wid][q] = du[q];
+                red[buf][wid][4 + q] = dw[q];
+            }
+        __syncthreads();  // red[buf] complete; red[buf ^ 1] free for the next group
+        if (threadIdx.x < 8) {
+            const int c = threadIdx.x;
+            double sum = 0.0;
+#pragma unroll
+            for (int k2 = 0; k2 < NW; ++k2)
+                sum += red[buf][k2][c];
+            const int q = c & 3;
+            if (g < ngroups) {
+                const int r = 4 * g + q;
+                if (r < nv) {
+                    if (c < 4)
+                        partial[(long)r * kRedBlocks + blockIdx.x] = sum;
+                    else if (hw)
+                        partial[(long)(nv + r) * kRedBlocks + blockIdx.x] = sum;
+                }
+            } else if (c < 3) {
                 if (hw)
-                    partial[(long)(nv + r) * kRedBlocks + blockIdx.x] = sw;
-            } else if (hw) {
-                partial[(long)(2 * nv) * kRedBlocks + blockIdx.x] = su;
-                partial[(long)(2 * nv + 1) * kRedBlocks + blockIdx.x] = sw;
-                partial[(long)(2 * nv + 2) * kRedBlocks + blockIdx.x] = sx;
-            } else {
-                partial[(long)nv * kRedBlocks + blockIdx.x] = su;
+                    partial[(long)(2 * nv + c) * kRedBlocks + blockIdx.x] = sum;
+                else if (c == 0)
+                    partial[(long)nv * kRedBlocks + blockIdx.x] = sum;
             }
         }
     }
@@ -169,6 +171,19 @@ __global__ void __launch_bounds__(kRedThreads) dcgs_update_kernel(const double* 
          k += (long)gridDim.x * blockDim.x) {
         double sa0 = 0.0, sa1 = 0.0, sd0 = 0.0, sd1 = 0.0;
         int i = 0;
+        for (; i + 7 < nv; i += 8) {  // eight basis vectors in flight per thread
+            double v[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+                v[q] = __ldcs(V + (long)(i + q) * ld + k);
+#pragma unroll
+            for (int q = 0; q < 8; q += 2) {
+                sa0 += ca[i + q] * v[q];
+                sa1 += ca[i + q + 1] * v[q + 1];
+                sd0 += cd[i + q] * v[q];
+                sd1 += cd[i + q + 1] * v[q + 1];
+            }
+        }
         for (; i + 3 < nv; i += 4) {
             const double v0 = __ldcs(V + (long)i * ld + k), v1 = __ldcs(V + (long)(i + 1) * ld + k);
             const double v2 = __ldcs(V + (long)(i + 2) * ld + k), v3 = __ldcs(V + (long)(i + 3) * ld + k);
