@@ -1167,30 +1167,45 @@ int hbgpu_set_basis(hbgpu_ctx* c, int modes, double period) {
     c->p_valid = c->inv_valid = false;
     c->mass_valid = false;
     {
-        // per bucket: the persistent row pipeline at the narrowest CTA (128 /
-        // 256 / 512 threads) whose shared memory holds the whole time series at
-        // 16 resident warps per SM; otherwise 512 threads and the largest
-        // time-sample tile that fits.  Rows whose neighbour records cannot be
-        // buffered at all use the tiled row kernel.
-        size_t mx = 0, mxp[3] = {0, 0, 0};
+        // per bucket: the persistent row pipeline.  CTA width w (32 ... 512) is
+        // picked by a throughput score: useful thread fraction of the row's
+        // phase-1 items (incidences x samples) times min(1, resident warps / 12),
+        // residency limited by shared memory (whole time series per CTA), 128
+        // registers per thread and 32 CTAs per SM; ties go to the narrower CTA.
+        // If no width holds the whole series, 512 threads and the largest tile
+        // that fits.  Rows whose neighbour records cannot be buffered at all use
+        // the tiled row kernel.
+        size_t mx = 0, mxp[5] = {0, 0, 0, 0, 0};
         int dev = 0, nsm = 0;
         // test knob: HBGPU_TANGENT_KERNEL=rows forces the row-kernel fallback
         const char* tk = std::getenv("HBGPU_TANGENT_KERNEL");
         const bool force_rows = tk && std::strcmp(tk, "rows") == 0;
         CK(c, cudaGetDevice(&dev));
         CK(c, cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-        const int widths[3] = {128, 256, 512};
+        const int widths[5] = {32, 64, 128, 256, 512};
         for (auto& b : c->tb) {
             if (!b.count)
                 continue;
             auto ps = [&](int nt) { return tangent_pipe_smem(b.max_pack, b.max_inc, b.max_blk, N, nt); };
             b.pipe = false;
             if (TAN_PIPE && !force_rows) {
-                for (int w = 0; w < 3 && !b.pipe; ++w) {
-                    const size_t budget = size_t(227 * 1024) / size_t(512 / widths[w]) - 1024;
-                    if (ps(N) <= budget) {
+                const double items = double(b.max_inc) * N;
+                double best = 0.0;
+                for (int w : widths) {
+                    const size_t sm = ps(N);
+                    if (sm > size_t(227 * 1024))
+                        continue;
+                    const int by_smem = int(size_t(228 * 1024) / (sm + 1024));
+                    const int by_regs = 65536 / (w * 128);
+                    const int ctas = std::min({32, by_smem, by_regs});
+                    if (ctas < 1)
+                        continue;
+                    const double rounds = std::ceil(items / w);
+                    const double score = items / (rounds * w) * std::min(1.0, ctas * (w / 32) / 12.0);
+                    if (score > best * 1.0001) {
+                        best = score;
                         b.pipe = true;
-                        b.threads = widths[w];
+                        b.threads = w;
                         b.nt = N;
                     }
                 }
@@ -1207,7 +1222,7 @@ int hbgpu_set_basis(hbgpu_ctx* c, int modes, double period) {
             }
             if (b.pipe) {
                 b.smem = ps(b.nt);
-                const int w = b.threads == 128 ? 0 : b.threads == 256 ? 1 : 2;
+                const int w = int(std::find(widths, widths + 5, b.threads) - widths);
                 mxp[w] = std::max(mxp[w], b.smem);
                 continue;
             }
@@ -1223,7 +1238,7 @@ int hbgpu_set_basis(hbgpu_ctx* c, int modes, double period) {
             return fail(c, HBGPU_ERR_INVALID, "node valence too high for the tangent row kernel");
         if (mx)
             CK(c, configure_tangent_row_smem(mx));
-        for (int w = 0; w < 3; ++w)
+        for (int w = 0; w < 5; ++w)
             if (mxp[w])
                 CK(c, configure_tangent_pipe_smem(widths[w], mxp[w]));
         for (auto& b : c->tb) {

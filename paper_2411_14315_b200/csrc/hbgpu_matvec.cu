@@ -17,7 +17,9 @@ __device__ __forceinline__ double ldcs(const double* p) { return __ldcs(p); }
 // block loop is branch-free; two blocks per iteration keep 24+ independent
 // loads in flight per thread.  The N threads of a row exchange the gathered
 // velocity series through shared memory for the dense H product.
-template <bool SCALED, bool WITH_C>
+// N1: N == 1 (steady / time-stepping case): a block's 8 slots are 64 contiguous
+// bytes and y's 4 components 32 — loaded as 16-byte vectors (H is 0, no C part).
+template <bool SCALED, bool WITH_C, bool N1>
 __global__ void __launch_bounds__(256) lmatvec_kernel(MatvecArgs a) {
     extern __shared__ double sh[];
     const int N = a.N;
@@ -33,13 +35,30 @@ __global__ void __launch_bounds__(256) lmatvec_kernel(MatvecArgs a) {
     const long N8 = 8L * N;
     auto block = [&](int k) {
         const int B = __ldg(&a.col_idx[k]);
-        const double* v = a.vals + (long)k * N8 + n;
-        const long yb = (long)B * 4 * N + n;
-        double y0 = __ldg(a.y + yb), y1 = __ldg(a.y + yb + N), y2 = __ldg(a.y + yb + 2 * N),
-               y3 = __ldg(a.y + yb + 3 * N);
-        const double kd = ldcs(v), g0 = ldcs(v + N), g1 = ldcs(v + 2 * N), g2 = ldcs(v + 3 * N);
-        const double d0 = ldcs(v + 4 * N), d1 = ldcs(v + 5 * N), d2 = ldcs(v + 6 * N),
-                     ld = ldcs(v + 7 * N);
+        double y0, y1, y2, y3, kd, g0, g1, g2, d0, d1, d2, ld;
+        if (N1) {
+            const double2* v = reinterpret_cast<const double2*>(a.vals + (long)k * 8);
+            const double2* yv = reinterpret_cast<const double2*>(a.y + (long)B * 4);
+            const double2 ya = __ldg(yv), yb2 = __ldg(yv + 1);
+            const double2 p0 = __ldcs(v), p1 = __ldcs(v + 1), p2 = __ldcs(v + 2), p3 = __ldcs(v + 3);
+            y0 = ya.x; y1 = ya.y; y2 = yb2.x; y3 = yb2.y;
+            kd = p0.x; g0 = p0.y; g1 = p1.x; g2 = p1.y; d0 = p2.x; d1 = p2.y; d2 = p3.x; ld = p3.y;
+        } else {
+            const double* v = a.vals + (long)k * N8 + n;
+            const long yb = (long)B * 4 * N + n;
+            y0 = __ldg(a.y + yb);
+            y1 = __ldg(a.y + yb + N);
+            y2 = __ldg(a.y + yb + 2 * N);
+            y3 = __ldg(a.y + yb + 3 * N);
+            kd = ldcs(v);
+            g0 = ldcs(v + N);
+            g1 = ldcs(v + 2 * N);
+            g2 = ldcs(v + 3 * N);
+            d0 = ldcs(v + 4 * N);
+            d1 = ldcs(v + 5 * N);
+            d2 = ldcs(v + 6 * N);
+            ld = ldcs(v + 7 * N);
+        }
         ou0 += kd * y0 + g0 * y3;
         ou1 += kd * y1 + g1 * y3;
         ou2 += kd * y2 + g2 * y3;
@@ -117,16 +136,21 @@ void launch_lmatvec(const MatvecArgs& a, cudaStream_t st) {
     const size_t smem =
         a.with_c ? sizeof(double) * ((size_t)a.N * a.N + 3 * (size_t)a.N * a.rows_per_cta) : 0;
     note_launch();
-    if (a.with_c) {
+    if (a.N == 1) {  // H = 0: P only
         if (a.scale_out)
-            lmatvec_kernel<true, true><<<blocks, threads, smem, st>>>(a);
+            lmatvec_kernel<true, false, true><<<blocks, threads, 0, st>>>(a);
         else
-            lmatvec_kernel<false, true><<<blocks, threads, smem, st>>>(a);
+            lmatvec_kernel<false, false, true><<<blocks, threads, 0, st>>>(a);
+    } else if (a.with_c) {
+        if (a.scale_out)
+            lmatvec_kernel<true, true, false><<<blocks, threads, smem, st>>>(a);
+        else
+            lmatvec_kernel<false, true, false><<<blocks, threads, smem, st>>>(a);
     } else {
         if (a.scale_out)
-            lmatvec_kernel<true, false><<<blocks, threads, smem, st>>>(a);
+            lmatvec_kernel<true, false, false><<<blocks, threads, smem, st>>>(a);
         else
-            lmatvec_kernel<false, false><<<blocks, threads, smem, st>>>(a);
+            lmatvec_kernel<false, false, false><<<blocks, threads, smem, st>>>(a);
     }
 }
 

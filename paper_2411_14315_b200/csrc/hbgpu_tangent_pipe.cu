@@ -147,8 +147,8 @@ size_t tangent_pipe_smem(int max_pack, int max_inc, int max_blk, int N, int NT) 
     return (size_t)pipe_layout(max_pack, max_inc, max_blk, N, NT).total;
 }
 
-// THREADS per CTA is chosen per valence bucket (128 / 256 / 512) so a row's
-// summaries fit shared memory at 16 resident warps per SM.
+// THREADS per CTA (32 ... 512) is chosen per valence bucket from the row's
+// work (incidences x samples) and the shared memory its summaries need.
 // NC > 0: the time-sample count is the compile-time constant NC (and the
 // whole series is one tile), so every N-strided shared/global address folds
 // to an immediate offset; NC = 0 is the generic kernel.
@@ -434,7 +434,7 @@ __global__ void __launch_bounds__(THREADS, 512 / THREADS) tangent_pipe_kernel(Ta
 }
 
 // Compile-time time-sample counts of the BASELINE configs (N = 2 Nm - 1).
-#define HBGPU_PIPE_NC_LIST(X) X(5) X(7) X(19) X(31) X(47)
+#define HBGPU_PIPE_NC_LIST(X) X(1) X(5) X(7) X(19) X(31) X(47)
 
 template <int T, int NC>
 static cudaError_t configure_pipe_tn(int b) {
@@ -458,6 +458,8 @@ static cudaError_t configure_pipe_t(size_t bytes) {
 
 cudaError_t configure_tangent_pipe_smem(int threads, size_t bytes) {
     switch (threads) {
+    case 32: return configure_pipe_t<32>(bytes);
+    case 64: return configure_pipe_t<64>(bytes);
     case 128: return configure_pipe_t<128>(bytes);
     case 256: return configure_pipe_t<256>(bytes);
     case 512: return configure_pipe_t<512>(bytes);
@@ -467,6 +469,8 @@ cudaError_t configure_tangent_pipe_smem(int threads, size_t bytes) {
 
 cudaError_t tangent_pipe_occupancy(int threads, int* blocks_per_sm, size_t smem) {
     switch (threads) {
+    case 32: return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, tangent_pipe_kernel<0, 32, 0>, 32, smem);
+    case 64: return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, tangent_pipe_kernel<0, 64, 0>, 64, smem);
     case 128: return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, tangent_pipe_kernel<0, 128, 0>, 128, smem);
     case 256: return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, tangent_pipe_kernel<0, 256, 0>, 256, smem);
     case 512: return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, tangent_pipe_kernel<0, 512, 0>, 512, smem);
@@ -504,12 +508,13 @@ void launch_tangent_pipe(const TangentArgs& a, const PipeArgs& p, int threads, i
         return;
     note_launch();
     const dim3 grid(grid_x, (a.N + a.NT - 1) / a.NT);
-    if (threads == 512)
-        launch_pipe_t<512>(a, p, grid, smem, st);
-    else if (threads == 256)
-        launch_pipe_t<256>(a, p, grid, smem, st);
-    else
-        launch_pipe_t<128>(a, p, grid, smem, st);
+    switch (threads) {
+    case 32: launch_pipe_t<32>(a, p, grid, smem, st); break;
+    case 64: launch_pipe_t<64>(a, p, grid, smem, st); break;
+    case 256: launch_pipe_t<256>(a, p, grid, smem, st); break;
+    case 512: launch_pipe_t<512>(a, p, grid, smem, st); break;
+    default: launch_pipe_t<128>(a, p, grid, smem, st); break;
+    }
 }
 
 }  // namespace hbgpu
