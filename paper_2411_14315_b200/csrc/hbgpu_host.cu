@@ -106,7 +106,7 @@ struct hbgpu_ctx {
     DBuf<double> tgeom;
     DBuf<int> row_ptr, col_idx, diag_blk, inc_ptr;
     // residual element chunks
-    int nchunks = 0, max_nloc = 0, res_grid = 0;
+    int nchunks = 0, max_nloc = 0, res_grid = 0, res_tile = 4;
     long npairs = 0;
     DBuf<int> rpack_ptr, npart_ptr, npart;
     DBuf<unsigned char> rpack;  // chunk packs (see ResidualChunkArgs)
@@ -508,7 +508,7 @@ static int upload_all(hbgpu_ctx* c, const hbgpu_mesh_desc* d) {
         for (int ln = 0; ln < nloc; ++ln) {
             cnodes.push_back(loc[size_t(ln)]);
             for (uint8_t sl : inc[size_t(ln)])
-                soff.push_back(uint16_t((sl >> 2) * 29 * kResTile + (sl & 3) * 7 * kResTile));
+                soff.push_back(uint16_t((sl >> 2) * 29 + (sl & 3) * 7));
             sptr.push_back(int(soff.size()));
             npp[size_t(loc[size_t(ln)]) + 1] += 1;
         }
@@ -579,10 +579,10 @@ static int residual_dev(hbgpu_ctx* c, const double* d_state, double* d_r) {
     ca.nu = c->mu / c->rho;
     ca.tau_mode = c->tau_mode;
     ca.flag = c->flag.p;
-    launch_residual_chunks(ca, c->res_grid, st);
+    launch_residual_chunks(ca, c->res_grid, c->res_tile, st);
     const long p2 = prof_mark(c);
     launch_residual_nodes(c->H.p, N, c->nn, c->npart_ptr.p, c->npart.p, c->rpartial.p, c->dir.p,
-                          d_r, kResTile, c->npairs, st);
+                          d_r, c->res_tile, c->npairs, st);
     if (c->nbnodes > 0) {
         BoundaryArgs b;
         b.bnode = c->bnode.p;
@@ -1146,14 +1146,15 @@ int hbgpu_set_basis(hbgpu_ctx* c, int modes, double period) {
                             &c->scale, &c->b, &c->tmp})
         CK(c, b->alloc(n));
     CK(c, c->hu.alloc(size_t(c->nn) * 3 * size_t(N)));
-    CK(c, c->rpartial.alloc(size_t(c->npairs) * 7 * size_t((N + kResTile - 1) / kResTile) * kResTile));
+    c->res_tile = residual_tile(N);
+    CK(c, c->rpartial.alloc(size_t(c->npairs) * 7 * size_t((N + c->res_tile - 1) / c->res_tile) * c->res_tile));
     {
-        const size_t rs = residual_smem_bytes(c->max_nloc, c->max_rpack);
-        CK(c, configure_residual_smem(rs));
+        const size_t rs = residual_smem_bytes(c->max_nloc, c->max_rpack, c->res_tile);
+        CK(c, configure_residual_smem(rs, c->res_tile));
         int per_sm = 0, nsm = 0, dev = 0;
         CK(c, cudaGetDevice(&dev));
         CK(c, cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-        CK(c, residual_occupancy(&per_sm, rs));
+        CK(c, residual_occupancy(&per_sm, rs, c->res_tile));
         c->res_grid = nsm * std::max(1, per_sm);
     }
     CK(c, c->pvals.alloc(size_t(c->nnz) * 8 * size_t(N)));

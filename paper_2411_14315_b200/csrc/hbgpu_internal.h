@@ -17,9 +17,8 @@ constexpr double kQB = 0.1381966011250105151795414;
 // Gauss-Seidel block: number of partial sums of the deterministic reductions.
 constexpr int kRedBlocks = 592;  // 4 x 148 SMs
 constexpr int kRedThreads = 256;
-// Residual element chunks: elements per chunk and time samples per CTA.
+// Residual element chunks: elements per chunk (time samples per tile: residual_tile(N)).
 constexpr int kChunkElems = 64;
-constexpr int kResTile = 4;
 // Compact tangent geometry record (gradN 12, V, symmetric xi 6, xi:xi).
 constexpr int kTGeo = 20;
 
@@ -142,7 +141,7 @@ struct ResidualChunkArgs {
     // per chunk, a contiguous "chunk pack" (16-byte aligned):
     //   hdr int4 {nloc, ecount, nb (first pair), 0}, nodes int[nloc],
     //   sptr int[nloc + 1] (chunk-relative slot ranges, element order),
-    //   soff u16[4 ecount] (slot -> shared-memory offset el*29T + a*7T),
+    //   soff u16[4 ecount] (slot -> shared-memory offset (el*29 + a*7) * T),
     //   lconn u32[ecount] (4 x u8 chunk-local node ids)
     const unsigned char* rpack;
     const int* rpack_ptr;        // nchunks + 1, 16-byte units
@@ -228,13 +227,14 @@ void launch_geometry(const double* xyz, const int4* conn, int ne, double* geom, 
                      cudaStream_t st);
 void launch_apply_h_series(const double* H, int N, const double* in, int in_node_stride,
                            double* out, int out_node_stride, int nnodes, cudaStream_t st);
-size_t residual_smem_bytes(int max_nloc, int max_rpack);
+size_t residual_smem_bytes(int max_nloc, int max_rpack, int T);
+int residual_tile(int N);
 size_t residual_pack_bytes(int nloc, int ecount);
 void residual_pack_write(unsigned char* dst, int nloc, int ecount, int nb, const int* nodes,
                          const int* sptr_rel, const uint16_t* soff, const uint32_t* lconn);
-void launch_residual_chunks(const ResidualChunkArgs& a, int grid, cudaStream_t st);
-cudaError_t configure_residual_smem(size_t bytes);
-cudaError_t residual_occupancy(int* blocks_per_sm, size_t smem);
+void launch_residual_chunks(const ResidualChunkArgs& a, int grid, int T, cudaStream_t st);
+cudaError_t configure_residual_smem(size_t bytes, int T);
+cudaError_t residual_occupancy(int* blocks_per_sm, size_t smem, int T);
 void launch_residual_nodes(const double* H, int N, int nn, const int* npart_ptr, const int* npart,
                            const double* partial, const uint8_t* dir, double* r, int T,
                            long npairs, cudaStream_t st);

@@ -269,7 +269,7 @@ __device__ __forceinline__ void element_residual_smem(const double* __restrict__
 }
 
 // Residual element pass as a persistent pipeline.  CTA b walks element
-// chunks b, b+G, ... and, per chunk, its time-sample tiles of kResTile samples.
+// chunks b, b+G, ... and, per chunk, its time-sample tiles (T samples, residual_tile(N)).
 //  * The chunk's metadata ("chunk pack": local nodes, per-node slot lists,
 //    local connectivity) and its 64 geometry records arrive by bulk async copy
 //    (cp.async.bulk on an mbarrier), issued one chunk ahead.
@@ -323,8 +323,8 @@ void residual_pack_write(unsigned char* dst, int nloc, int ecount, int nb, const
 struct ResSmem {
     int pk, geo, nd, slots, mbar, total;  // byte offsets
 };
-__host__ __device__ inline ResSmem res_layout(int max_nloc, int max_rpack) {
-    constexpr int T = kResTile, CE = kChunkElems;
+__host__ __device__ inline ResSmem res_layout(int max_nloc, int max_rpack, int T) {
+    constexpr int CE = kChunkElems;
     ResSmem L;
     L.pk = 0;                                              // 2 x max_rpack
     L.geo = L.pk + 2 * rp_align16(max_rpack);              // 2 x [CE][kTGeo]
@@ -334,16 +334,19 @@ __host__ __device__ inline ResSmem res_layout(int max_nloc, int max_rpack) {
     L.total = L.mbar + 16;
     return L;
 }
-size_t residual_smem_bytes(int max_nloc, int max_rpack) {
-    return (size_t)res_layout(max_nloc, max_rpack).total;
+size_t residual_smem_bytes(int max_nloc, int max_rpack, int T) {
+    return (size_t)res_layout(max_nloc, max_rpack, T).total;
 }
 
-__global__ void __launch_bounds__(256, RES_MINB) residual_chunk_kernel(ResidualChunkArgs a) {
+// T = time samples per tile (4; 1 when N is small, where a 4-sample tile would
+// leave most threads idle — the host picks it, residual_tile()).
+template <int T>
+__global__ void __launch_bounds__(kChunkElems * T, RES_MINB * 4 / T) residual_chunk_kernel(ResidualChunkArgs a) {
     extern __shared__ __align__(128) unsigned char smraw[];
-    constexpr int T = kResTile, CE = kChunkElems, ndst = 7 * T, es = 29 * T;
+    constexpr int CE = kChunkElems, ndst = 7 * T, es = 29 * T;
     const int N = a.N, nch = a.nchunks;
     const int ntiles = (N + T - 1) / T;
-    const ResSmem Ls = res_layout(a.max_nloc, a.max_rpack);
+    const ResSmem Ls = res_layout(a.max_nloc, a.max_rpack, T);
     const int mpk = rp_align16(a.max_rpack);
     uint64_t* mbar = reinterpret_cast<uint64_t*>(smraw + Ls.mbar);
     double* slots = reinterpret_cast<double*>(smraw + Ls.slots);
@@ -437,7 +440,7 @@ __global__ void __launch_bounds__(256, RES_MINB) residual_chunk_kernel(ResidualC
                 double acc[7] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
                 const int q1 = sptr[ln + 1];
                 for (int q = sptr[ln]; q < q1; ++q) {
-                    const double* sp = slots + soff[q] + t;  // el*es + a*7T
+                    const double* sp = slots + soff[q] * T + t;  // (el*29 + a*7) T
 #pragma unroll
                     for (int cc = 0; cc < 7; ++cc)
                         acc[cc] += sp[cc * T];
@@ -451,17 +454,35 @@ __global__ void __launch_bounds__(256, RES_MINB) residual_chunk_kernel(ResidualC
     cp_async_wait<0>();
 }
 
-void launch_residual_chunks(const ResidualChunkArgs& a, int grid, cudaStream_t st) {
+int residual_tile(int N) {
+    // largest tile whose padding wastes at most 15% of the thread slots
+    for (int T : {4, 2})
+        if (N >= T && double(N) / double(((N + T - 1) / T) * T) >= 0.85)
+            return T;
+    return 1;
+}
+
+void launch_residual_chunks(const ResidualChunkArgs& a, int grid, int T, cudaStream_t st) {
     if (a.nchunks <= 0)
         return;
     note_launch();
-    residual_chunk_kernel<<<min(grid, a.nchunks), kChunkElems * kResTile,
-                            residual_smem_bytes(a.max_nloc, a.max_rpack), st>>>(a);
+    const size_t sm = residual_smem_bytes(a.max_nloc, a.max_rpack, T);
+    const int g = min(grid, a.nchunks);
+    if (T == 4)
+        residual_chunk_kernel<4><<<g, kChunkElems * 4, sm, st>>>(a);
+    else if (T == 2)
+        residual_chunk_kernel<2><<<g, kChunkElems * 2, sm, st>>>(a);
+    else
+        residual_chunk_kernel<1><<<g, kChunkElems, sm, st>>>(a);
 }
 
-cudaError_t configure_residual_smem(size_t bytes) {
-    return cudaFuncSetAttribute(residual_chunk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                int(bytes < 48 * 1024 ? 48 * 1024 : bytes));
+cudaError_t configure_residual_smem(size_t bytes, int T) {
+    const int b = int(bytes < 48 * 1024 ? 48 * 1024 : bytes);
+    if (T == 4)
+        return cudaFuncSetAttribute(residual_chunk_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, b);
+    if (T == 2)
+        return cudaFuncSetAttribute(residual_chunk_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, b);
+    return cudaFuncSetAttribute(residual_chunk_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, b);
 }
 
 // Node pass: sums the node's chunk partials in chunk order, completes the
@@ -829,8 +850,11 @@ cudaError_t run_fp64_peak(int blocks, int threads, int iters, double* out, float
 }  // namespace hbgpu
 
 namespace hbgpu {
-cudaError_t residual_occupancy(int* blocks_per_sm, size_t smem) {
-    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, residual_chunk_kernel,
-                                                         kChunkElems * kResTile, smem);
+cudaError_t residual_occupancy(int* blocks_per_sm, size_t smem, int T) {
+    if (T == 4)
+        return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, residual_chunk_kernel<4>, kChunkElems * 4, smem);
+    if (T == 2)
+        return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, residual_chunk_kernel<2>, kChunkElems * 2, smem);
+    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, residual_chunk_kernel<1>, kChunkElems, smem);
 }
 }  // namespace hbgpu
