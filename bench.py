@@ -410,7 +410,7 @@ def run_ours(args):
     # ---- converged solve time (config 0, reference default tolerances)
     solve = None
     if args.solve and rank == 0:
-        solve = solve_config0()
+        solve = solve_config0(args.cpu_solve)
 
     cpu_baseline = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -628,23 +628,46 @@ def sweep_configs(args):
                       "results": out}), flush=True)
 
 
-def solve_config0():
+def solve_config0(cpu_reference=False):
+    """Converged-solve time of config 0 (BASELINE metric 3).  The reference
+    defaults (3 orders, GMRES 0.03 / restart 200, pseudo-dt = h_c/u_c, 60
+    Newton iterations) stall at res_rel ~0.037 on this pipe — on the CPU
+    reference too — so the converged solve uses the same defaults with the
+    pseudo time step at CFL 10 (10 h_c/u_c) and an 80-iteration cap; the
+    defaults are reported beside it.  With cpu_reference the compiled
+    reference runs the same converged solve on the host (slow: ~minute)."""
     from paper_2411_14315_b200 import cases, hbgpu
 
     prob = cases.config_problem(0)
-    ctx = hbgpu.GpuContext(prob.mesh)
-    ctx.set_basis(prob.modes, prob.period)
-    ctx.set_fluid(prob.rho, prob.mu)
-    ctx.set_bcs(prob.dirichlet_g, prob.neumann, prob.backflow_beta)
-    try:
-        sol = ctx.solve_harmonic(hbgpu.SolverConfig())
-        return {"config": "config0 (36000 tets, Nm=3), reference defaults (3 orders, GMRES 0.03, restart 200)",
-                "seconds": sol.total_seconds, "newton_iters": int(len(sol.log.iters)),
-                "gmres_iters": int(sol.log.linear_iters.sum()), "converged": sol.log.converged,
-                "final_rel": float(sol.log.res_rel[-1]), "assembly_seconds": sol.assembly_seconds,
-                "linear_seconds": sol.linear_seconds}
-    except Exception as exc:
-        return {"error": f"{type(exc).__name__}: {exc}"}
+    out = {}
+    for key, scale, cap in (("converged", 10.0, 80), ("reference_defaults", None, 60)):
+        ctx = hbgpu.GpuContext(prob.mesh)
+        ctx.set_basis(prob.modes, prob.period)
+        ctx.set_fluid(prob.rho, prob.mu)
+        ctx.set_bcs(prob.dirichlet_g, prob.neumann, prob.backflow_beta)
+        cfg = hbgpu.SolverConfig()
+        cfg.max_newton_iters = cap
+        if scale is not None:
+            cfg.pseudo_dt = auto_pseudo_dt(prob) * scale
+        try:
+            sol = ctx.solve_harmonic(cfg)
+            out[key] = {"seconds": sol.total_seconds, "newton_iters": int(len(sol.log.iters)),
+                        "gmres_iters": int(sol.log.linear_iters.sum()), "converged": sol.log.converged,
+                        "final_rel": float(sol.log.res_rel[-1]), "assembly_seconds": sol.assembly_seconds,
+                        "linear_seconds": sol.linear_seconds, "pseudo_dt": cfg.pseudo_dt}
+        except Exception as exc:
+            out[key] = {"error": f"{type(exc).__name__}: {exc}"}
+    out["config"] = ("config0 (36000 tets, Nm=3): 'converged' = reference defaults with pseudo-dt "
+                     "10 h_c/u_c and 80 Newton iterations; 'reference_defaults' = pure defaults")
+    if cpu_reference:
+        from oracle import bindings as ob
+
+        rc = ob.ref_context(prob)
+        ref = rc.solve(pseudo_dt=auto_pseudo_dt(prob) * 10.0, max_newton=80, threads=os.cpu_count() or 1)
+        out["cpu_reference"] = {"seconds": ref["total_seconds"], "newton_iters": int(len(ref["rel"])),
+                                "gmres_iters": int(ref["linear"].sum()), "converged": ref["converged"],
+                                "final_rel": float(ref["rel"][-1]), "threads": os.cpu_count() or 1}
+    return out
 
 
 def main():
@@ -656,6 +679,7 @@ def main():
     ap.add_argument("--spmv-reps", type=int, default=100)
     ap.add_argument("--no-solve", dest="solve", action="store_false")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-solve", action="store_true", help="also time the reference's converged config-0 solve")
     ap.add_argument("--sweep4", action="store_true", help="config-4 operator sweep (separate run)")
     ap.add_argument("--sweep-points", type=int, default=700_000)
     ap.add_argument("--configs", default=None, help="e.g. 0,1,2,3: per-config operator/Newton sweep")
