@@ -398,14 +398,14 @@ def run_ours(args):
     e2e_times = []
     for _ in range(max(3, args.steps // 2)):
         t0 = time.perf_counter()
-        hbgpu._residual(ctx.handle, hs.ctypes.data, hr.ctypes.data)
-        hbgpu._tangent(ctx.handle, hs.ctypes.data, None)
+        hbgpu._assemble(ctx.handle, hs.ctypes.data, hr.ctypes.data)
         e2e_times.append(time.perf_counter() - t0)
     e2e_s = float(np.mean(e2e_times))
     e2e = {"value": world * ne * M / e2e_s, "unit": UNIT,
-           "h2d_bytes_per_step": 2 * state.nbytes, "d2h_bytes_per_step": state.nbytes,
-           "note": "hbgpu_assemble_residual(host state -> host r) + hbgpu_assemble_tangent(host state, "
-                   "P kept on device as the GPU Newton loop uses it); pinned host buffers; wall clock"}
+           "h2d_bytes_per_step": state.nbytes, "d2h_bytes_per_step": state.nbytes,
+           "note": "hbgpu_assemble(host state -> host residual, tangent P kept on device as the GPU "
+                   "Newton loop uses it): one upload, residual copy-back overlapping the tangent; "
+                   "pinned host buffers; wall clock"}
 
     # ---- converged solve time (config 0, reference default tolerances)
     solve = None

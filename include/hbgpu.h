@@ -101,6 +101,12 @@ int hbgpu_get_geometry(hbgpu_ctx* ctx, double* geometry);
 
 /* assemble_residual (assembly.hpp:129-134, assembly.cpp:443-548). */
 int hbgpu_assemble_residual(hbgpu_ctx* ctx, const double* state, double* residual);
+/* One Newton iteration's assembly of a host state: assemble_residual (into
+ * the host `residual`) and assemble_tangent (P kept on the device for the
+ * following matvec / jacobi / gmres calls) of the same state — the pair of
+ * calls at hb_solver.cpp:152,161 with a single upload; the residual's copy back
+ * overlaps the tangent. */
+int hbgpu_assemble(hbgpu_ctx* ctx, const double* state, double* residual);
 /* assemble_tangent (assembly.hpp:138-141, assembly.cpp:550-666).  P stays on
  * the device for hbgpu_matvec / hbgpu_jacobi / hbgpu_gmres; pvals may be NULL. */
 int hbgpu_assemble_tangent(hbgpu_ctx* ctx, const double* state, double* pvals);

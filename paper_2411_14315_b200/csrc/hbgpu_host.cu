@@ -1397,7 +1397,9 @@ int hbgpu_assemble_residual(hbgpu_ctx* c, const double* state, double* residual)
 
 // Residual and tangent of the same state, the tangent on the second stream so
 // the two latency-bound kernels share the SMs; ordered on ctx->stream after.
-static int assemble_both(hbgpu_ctx* c, const double* d_state, double* d_r) {
+// With host_r the residual's copy to the host is queued right behind the
+// residual, so it overlaps the tangent.
+static int assemble_both(hbgpu_ctx* c, const double* d_state, double* d_r, double* host_r = nullptr) {
     CK(c, cudaEventRecord(c->ev_fork, c->stream));
     CK(c, cudaStreamWaitEvent(c->stream2, c->ev_fork, 0));
     cudaStream_t main = c->stream;
@@ -1406,9 +1408,21 @@ static int assemble_both(hbgpu_ctx* c, const double* d_state, double* d_r) {
     c->stream = main;
     TRY(st);
     TRY(residual_dev(c, d_state, d_r));
+    if (host_r)
+        CK(c, cudaMemcpyAsync(host_r, d_r, sizeof(double) * size_t(c->state_len()), cudaMemcpyDeviceToHost,
+                              c->stream));
     CK(c, cudaEventRecord(c->ev_join, c->stream2));
     CK(c, cudaStreamWaitEvent(c->stream, c->ev_join, 0));
     return HBGPU_OK;
+}
+
+int hbgpu_assemble(hbgpu_ctx* c, const double* state, double* residual) {
+    TRY(ensure_basis(c));
+    const size_t n = size_t(c->state_len());
+    CK(c, cudaMemcpyAsync(c->state.p, state, sizeof(double) * n, cudaMemcpyHostToDevice, c->stream));
+    TRY(assemble_both(c, c->state.p, c->r.p, residual));
+    CK(c, cudaStreamSynchronize(c->stream));
+    return check_flag(c);
 }
 
 int hbgpu_assemble_dev(hbgpu_ctx* c, const double* d_state, double* d_residual) {

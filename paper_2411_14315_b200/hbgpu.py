@@ -140,6 +140,7 @@ _sizes = _sig("hbgpu_sizes", C.c_int, [_vp, _ip, _ip, _ip, C.POINTER(C.c_longlon
 _get_pattern = _sig("hbgpu_get_pattern", C.c_int, [_vp, _vp, _vp])
 _get_geometry = _sig("hbgpu_get_geometry", C.c_int, [_vp, _vp])
 _residual = _sig("hbgpu_assemble_residual", C.c_int, [_vp, _vp, _vp])
+_assemble = _sig("hbgpu_assemble", C.c_int, [_vp, _vp, _vp])
 _tangent = _sig("hbgpu_assemble_tangent", C.c_int, [_vp, _vp, _vp])
 _mass = _sig("hbgpu_assemble_mass", C.c_int, [_vp, _vp])
 _set_pvals = _sig("hbgpu_set_pvals", C.c_int, [_vp, _vp])
@@ -360,6 +361,14 @@ class GpuContext:
         s = self._vec_in(state)
         r = np.empty_like(s)
         self._check(_residual(self._h, _ptr(s), _ptr(r)))
+        return r
+
+    def assemble(self, state) -> np.ndarray:
+        """Residual (returned) and tangent (kept on the device) of one host
+        state with a single upload (hbgpu_assemble)."""
+        s = self._vec_in(state)
+        r = np.empty_like(s)
+        self._check(_assemble(self._h, _ptr(s), _ptr(r)))
         return r
 
     def assemble_tangent(self, state, download: bool = True):

@@ -176,6 +176,22 @@ def test_tangent_row_kernel_fallback(gpu, monkeypatch, mesh_kind, modes, tau):
     assert rel(ctx.assemble_tangent(s), orc.tangent(s)) < TOL
 
 
+def test_combined_assemble_host_call(gpu):
+    """hbgpu_assemble (one upload, residual to the host, P kept on the device)
+    equals the separate calls: residual vs the oracle, and the L-matvec that
+    follows uses the freshly assembled P."""
+    prob = tube_problem(4)
+    ctx = gpu_ctx(prob, 0, 0.3)
+    orc = ob.Restated(prob, tau_mode=0, pseudo_dt=0.3)
+    nn, N = prob.mesh.num_nodes, prob.N
+    s = cases.random_state(nn, N, 21)
+    r = ctx.assemble(s)
+    assert rel(r, orc.residual(s)) < TOL
+    ctx.assemble_mass()
+    y = cases.random_state(nn, N, 22)
+    assert rel(ctx.matvec(y), orc.matvec(orc.tangent(s), orc.mass(), y)) < TOL
+
+
 def test_pattern_bit_exact(gpu):
     from paper_2411_14315_b200 import meshgen
 
