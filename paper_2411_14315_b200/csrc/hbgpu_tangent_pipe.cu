@@ -136,7 +136,7 @@ __host__ __device__ inline PipeSmem pipe_layout(int max_pack, int mi, int max_bl
     L.su = L.meta + 2 * pack_align16(max_pack);                   // [blk][4N]
     L.tg = L.su + max_blk * 4 * N * 8;                            // [inc][20]
     L.summ = L.tg + mi * kTGeo * 8;                               // [i][8][NT]
-    L.rec = L.summ + mi * 8 * NT * 8;                             // [p][8]
+    L.rec = L.summ + ((mi * 7 * NT + 1) & ~1) * 8;                // [p][8]
     L.dpart = L.rec + 4 * mi * 64;                                // [part][8][NT]
     L.mbar = pack_align16(L.dpart + dpmax * 8 * NT * 8);          // 3 mbarriers
     L.total = L.mbar + 32;
@@ -268,7 +268,7 @@ __global__ void __launch_bounds__(THREADS, 512 / THREADS) tangent_pipe_kernel(Ta
             o[0] = make_double2(ga0, ga1);
             o[1] = make_double2(ga2, fma(ga0, gb0, fma(ga1, gb1, ga2 * gb2)));
             o[2] = make_double2(gb0, gb1);
-            o[3] = make_double2(gb2, __longlong_as_double((long long)i * 8 * NT));
+            o[3] = make_double2(gb2, __longlong_as_double((long long)i * 7 * NT));
         }
         // ---- phase 1: per (incidence, sample) summaries
         for (int it = threadIdx.x, i = i_start, t = t_start; it < ninc * nt;
@@ -312,7 +312,7 @@ __global__ void __launch_bounds__(THREADS, 512 / THREADS) tangent_pipe_kernel(Ta
                 bad = !(arg > 0.0);
                 tau_mean = tau_or_zero(arg, bad);
             }
-            double asum = 0.0, tsum = 0.0, z[3] = {0.0, 0.0, 0.0}, kap[3] = {0.0, 0.0, 0.0};
+            double tsum = 0.0, z[3] = {0.0, 0.0, 0.0}, kap[3] = {0.0, 0.0, 0.0};
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
                 double uq[3];
@@ -327,7 +327,6 @@ __global__ void __launch_bounds__(THREADS, 512 / THREADS) tangent_pipe_kernel(Ta
                     tq = tau_or_zero(arg, bq);
                 }
                 const double tadv = tq * fma(uq[0], ga[0], fma(uq[1], ga[1], uq[2] * ga[2]));
-                asum += tadv;
                 tsum += tq;
 #pragma unroll
                 for (int c = 0; c < 3; ++c) {
@@ -344,16 +343,15 @@ __global__ void __launch_bounds__(THREADS, 512 / THREADS) tangent_pipe_kernel(Ta
             }
             if (bad)
                 atomicOr(a.flag, 1);
-            double* so = summ + (size_t)i * 8 * NT + t;
+            double* so = summ + (size_t)i * 7 * NT + t;
             const double wr = w * rho;
             so[0] = wr * kap[0];
             so[NT] = wr * kap[1];
             so[2 * NT] = wr * kap[2];
-            so[3 * NT] = w * asum;
-            so[4 * NT] = w * z[0];
-            so[5 * NT] = w * z[1];
-            so[6 * NT] = w * z[2];
-            so[7 * NT] = (w / rho) * tsum;
+            so[3 * NT] = w * z[0];
+            so[4 * NT] = w * z[1];
+            so[5 * NT] = w * z[2];
+            so[6 * NT] = (w / rho) * tsum;
         }
         __syncthreads();
 
@@ -376,15 +374,18 @@ __global__ void __launch_bounds__(THREADS, 512 / THREADS) tangent_pipe_kernel(Ta
                 const double* sp = summ + __double_as_longlong(rd.y) + t;
                 const double gb0 = rc.x, gb1 = rc.y, gb2 = rd.x;
                 K = fma(sp[0], gb0, fma(sp[NT], gb1, fma(sp[2 * NT], gb2, K)));
-                const double al = sp[3 * NT];
+                // w alpha_a = (w z) . dN_a (phase 1 stores w z only: one shared
+                // load fewer per contribution; phase 2 is shared-memory bound)
+                const double z0 = sp[3 * NT], z1 = sp[4 * NT], z2 = sp[5 * NT];
+                const double al = fma(z0, ra.x, fma(z1, ra.y, z2 * rb.x));
                 G0 = fma(al, gb0, G0);
                 G1 = fma(al, gb1, G1);
                 G2 = fma(al, gb2, G2);
-                const double alb = fma(sp[4 * NT], gb0, fma(sp[5 * NT], gb1, sp[6 * NT] * gb2));
+                const double alb = fma(z0, gb0, fma(z1, gb1, z2 * gb2));
                 D0 = fma(ra.x, alb, D0);
                 D1 = fma(ra.y, alb, D1);
                 D2 = fma(rb.x, alb, D2);
-                L = fma(rb.y, sp[7 * NT], L);
+                L = fma(rb.y, sp[6 * NT], L);
             }
             if (slot >= dparts || slot == 0) {
                 const double2* bc = reinterpret_cast<const double2*>(blkc + j * 8);
