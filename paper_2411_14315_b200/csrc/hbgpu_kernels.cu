@@ -220,6 +220,8 @@ __device__ __forceinline__ void element_residual_smem(const double* __restrict__
     }
     const double dAB = kQA - kQB;
     double Cs[3] = {0, 0, 0}, TLs[3] = {0, 0, 0}, W[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
+    double tauq[4];
+    // pass 1 over the quadrature points: the q-sums Cs, TLs, W (and tau_q)
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
         double uq[3], huq[3];
@@ -235,7 +237,7 @@ __device__ __forceinline__ void element_residual_smem(const double* __restrict__
             bad |= bq;
             tau = tau_or_zero(arg, bq);
         }
-        double* oq = out + q * 7 * T;
+        tauq[q] = tau;
 #pragma unroll
         for (int i = 0; i < 3; ++i) {
             const double cv = uq[0] * gu[i][0] + uq[1] * gu[i][1] + uq[2] * gu[i][2];
@@ -245,24 +247,35 @@ __device__ __forceinline__ void element_residual_smem(const double* __restrict__
 #pragma unroll
             for (int j = 0; j < 3; ++j)
                 W[j][i] += uq[j] * tl;
-            oq[i * T] = w * rho * dAB * cv;     // node a = q part of the convection row
-            oq[(4 + i) * T] = w * dAB * tl;     // node a = q part of the LS time row
         }
     }
     if (bad)
         atomicOr(flag, 1);
+    // pass 2, node a = quadrature point a: the q = a parts (conv_q, tl_q
+    // recomputed from tau_a) plus the q-sum and Galerkin terms, each output
+    // written once
     const double muV = mu * V, moff = rho * V / 20.0, wr = w / rho;
 #pragma unroll
     for (int a = 0; a < 4; ++a) {
         const double ga0 = g[3 * a], ga1 = g[3 * a + 1], ga2 = g[3 * a + 2];
+        double uq[3], huq[3];
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {
+            uq[i] = kQB * usum[i] + dAB * U(a, i);
+            huq[i] = U(a, 4 + i);  // raw nodal Hu_a (Galerkin mass term), huq at q = a below
+        }
         double* oa = out + a * 7 * T;
 #pragma unroll
         for (int i = 0; i < 3; ++i) {
+            const double cv = uq[0] * gu[i][0] + uq[1] * gu[i][1] + uq[2] * gu[i][2];
+            const double hq = kQB * hsum[i] + dAB * huq[i];
+            const double tl = tauq[a] * (rho * hq + rho * cv + gp[i]);
             const double gai = g[3 * a + i];
-            oa[i * T] += muV * (ga0 * gu[i][0] + ga1 * gu[i][1] + ga2 * gu[i][2]) - gai * w * psum +
-                         moff * (hsum[i] + U(a, 4 + i)) + w * rho * kQB * Cs[i] +
-                         w * (ga0 * W[0][i] + ga1 * W[1][i] + ga2 * W[2][i]);
-            oa[(4 + i) * T] += w * kQB * TLs[i];
+            oa[i * T] = w * rho * dAB * cv +
+                        (muV * (ga0 * gu[i][0] + ga1 * gu[i][1] + ga2 * gu[i][2]) - gai * w * psum +
+                         moff * (hsum[i] + huq[i]) + w * rho * kQB * Cs[i] +
+                         w * (ga0 * W[0][i] + ga1 * W[1][i] + ga2 * W[2][i]));
+            oa[(4 + i) * T] = w * dAB * tl + w * kQB * TLs[i];
         }
         oa[3 * T] = w * div + wr * (ga0 * TLs[0] + ga1 * TLs[1] + ga2 * TLs[2]);
     }
