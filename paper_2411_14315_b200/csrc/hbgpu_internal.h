@@ -45,6 +45,9 @@ constexpr int kTanPart = 8;
 #ifndef TAN_SMEM_KB
 #define TAN_SMEM_KB 64
 #endif
+#ifndef MV_PREFETCH
+#define MV_PREFETCH 1
+#endif
 #ifndef MV_UNROLL
 #define MV_UNROLL 2
 #endif

@@ -9,7 +9,23 @@ namespace hbgpu {
 namespace {
 inline void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
-__device__ __forceinline__ double ldcs(const double* p) { return __ldcs(p); }
+__device__ __forceinline__ double ldcs(const double* p) {
+#if MV_PREFETCH == 1
+    double v;
+    asm volatile("ld.global.cs.L2::256B.f64 %0, [%1];" : "=d"(v) : "l"(p));
+    return v;
+#elif MV_PREFETCH == 2
+    double v;
+    asm volatile("ld.global.L1::no_allocate.L2::256B.f64 %0, [%1];" : "=d"(v) : "l"(p));
+    return v;
+#elif MV_PREFETCH == 3
+    double v;
+    asm volatile("ld.global.cs.L2::128B.f64 %0, [%1];" : "=d"(v) : "l"(p));
+    return v;
+#else
+    return __ldcs(p);
+#endif
+}
 }  // namespace
 
 // Thread (row, n).  The Dirichlet masks of C are folded into `mass_c`
