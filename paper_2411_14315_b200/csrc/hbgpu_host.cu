@@ -105,6 +105,7 @@ struct hbgpu_ctx {
     DBuf<uint8_t> blk_order;  // per row: off-diagonal blocks by descending contribution count
     DBuf<double> tgeom;
     DBuf<int> row_ptr, col_idx, diag_blk, inc_ptr;
+    DBuf<int> mv_perm;  // L-matvec row order: by descending length within 4096-row windows
     // residual element chunks
     int nchunks = 0, max_nloc = 0, res_grid = 0, res_tile = 4;
     long npairs = 0;
@@ -308,6 +309,24 @@ static int upload_all(hbgpu_ctx* c, const hbgpu_mesh_desc* d) {
                           cudaMemcpyHostToDevice, st));
     CK(c, cudaMemcpyAsync(c->diag_blk.p, diag.data(), sizeof(int) * size_t(nn),
                           cudaMemcpyHostToDevice, st));
+    {
+        // L-matvec row order: a CTA's rows finish together when their block
+        // counts match, so rows are stably sorted by descending length inside
+        // windows of 4096 consecutive rows (y stays L2-local per window)
+        std::vector<int> perm(static_cast<size_t>(nn));
+        for (int A = 0; A < nn; ++A)
+            perm[size_t(A)] = A;
+        const int* rp = c->row_ptr_h.data();
+        for (int w0 = 0; w0 < nn; w0 += 4096) {
+            const int w1 = std::min(nn, w0 + 4096);
+            std::stable_sort(perm.begin() + w0, perm.begin() + w1, [rp](int x, int y) {
+                return rp[x + 1] - rp[x] > rp[y + 1] - rp[y];
+            });
+        }
+        CK(c, c->mv_perm.alloc(size_t(nn)));
+        CK(c, cudaMemcpyAsync(c->mv_perm.p, perm.data(), sizeof(int) * size_t(nn), cudaMemcpyHostToDevice, st));
+        CK(c, cudaStreamSynchronize(st));
+    }
 
     // element incidences per row, element order; local block offsets
     std::vector<int> iptr(size_t(nn) + 1, 0);
@@ -693,6 +712,15 @@ static int mass_dev(hbgpu_ctx* c) {
     return check_launch(c);
 }
 
+// L-matvec kernel variant: bit 0 = rows in length-balanced order (mv_perm),
+// bit 1 = N == 1 rows split over 4 lanes.  Default 3 (config 4, 700k points:
+// N = 1 0.277 -> 0.190 ms, N = 7 1.398 -> 1.279 ms, N = 19 3.53 -> 3.24 ms);
+// HBGPU_MV_VARIANT overrides it (tooling).
+static int mv_variant() {
+    const char* e = std::getenv("HBGPU_MV_VARIANT");
+    return e ? std::atoi(e) : 3;
+}
+
 static int matvec_dev(hbgpu_ctx* c, const double* d_y, double* d_out, const double* d_scale,
                       bool with_c, const double* d_scale_out = nullptr) {
     if (!c->p_valid)
@@ -712,6 +740,8 @@ static int matvec_dev(hbgpu_ctx* c, const double* d_y, double* d_out, const doub
     if (d_scale)
         return fail(c, HBGPU_ERR_INVALID, "input-scaled matvec is not supported (scale z on the host side)");
     a.scale_out = d_scale_out;
+    a.perm = c->mv_perm.p;
+    a.variant = mv_variant();
     a.nn = c->nn;
     a.N = c->N;
     a.rows_per_cta = rows_per_matvec_cta(c->N);
@@ -1072,7 +1102,7 @@ void hbgpu_destroy(hbgpu_ctx* c) {
                             &c->r, &c->hu, &c->pvals, &c->mass, &c->mass_c, &c->inv, &c->y, &c->out,
                             &c->x, &c->w, &c->z, &c->scale, &c->b, &c->tmp, &c->V, &c->partial, &c->red, &c->rpartial})
         b->release();
-    for (DBuf<int>* b : {&c->row_ptr, &c->col_idx, &c->diag_blk, &c->inc_ptr, &c->rpack_ptr, &c->npart_ptr, &c->npart,
+    for (DBuf<int>* b : {&c->row_ptr, &c->col_idx, &c->mv_perm, &c->diag_blk, &c->inc_ptr, &c->rpack_ptr, &c->npart_ptr, &c->npart,
                          &c->bnode, &c->bptr, &c->binc, &c->fac, &c->fbc, &c->flag,
                          &c->ideg})
         b->release();

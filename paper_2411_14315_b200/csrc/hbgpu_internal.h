@@ -203,8 +203,10 @@ struct MatvecArgs {
     double* out;
     const double* scale;      // optional input scaling (gathered): L (S y)
     const double* scale_out;  // optional output scaling: S L y
+    const int* perm;          // optional row order (rows of similar length per CTA)
     int nn, N, rows_per_cta;
     int with_c;
+    int variant;              // kernel variant (tooling: HBGPU_MV_VARIANT)
 };
 
 struct BoundaryArgs {

@@ -26,6 +26,7 @@ __device__ __forceinline__ double ldcs(const double* p) {
     return __ldcs(p);
 #endif
 }
+__device__ __forceinline__ double2 ldcs2(const double2* p) { return __ldcs(p); }
 }  // namespace
 
 // Thread (row, n).  The Dirichlet masks of C are folded into `mass_c`
@@ -45,8 +46,9 @@ __global__ void __launch_bounds__(256) lmatvec_kernel(MatvecArgs a) {
         for (int k = threadIdx.x; k < N * N; k += blockDim.x)
             sH[k] = a.H[k];
     const int r = threadIdx.x / N, n = threadIdx.x - r * N;
-    const int A = blockIdx.x * a.rows_per_cta + r;
-    const bool valid = (r < a.rows_per_cta) && (A < a.nn);
+    const int ridx = blockIdx.x * a.rows_per_cta + r;
+    const bool valid = (r < a.rows_per_cta) && (ridx < a.nn);
+    const int A = (valid && a.perm) ? __ldg(a.perm + ridx) : ridx;
     double ou0 = 0.0, ou1 = 0.0, ou2 = 0.0, op = 0.0, t0 = 0.0, t1 = 0.0, t2 = 0.0;
     const long N8 = 8L * N;
     auto block = [&](int k) {
@@ -144,9 +146,74 @@ __global__ void __launch_bounds__(256) lmatvec_kernel(MatvecArgs a) {
     }
 }
 
-void launch_lmatvec(const MatvecArgs& a, cudaStream_t st) {
-    if (a.nn <= 0)
+// N == 1 with G lanes per row: lane g takes blocks kb+g, kb+g+G, ... (64-byte
+// blocks as four 16-byte loads), the G partial sums are combined by a fixed
+// xor-shuffle tree (deterministic).  Rows are taken in `perm` order.
+template <bool SCALED, int G>
+__global__ void __launch_bounds__(256) lmatvec_n1g_kernel(MatvecArgs a) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    const int ridx = t / G, g = t & (G - 1);
+    const bool valid = ridx < a.nn;
+    const int A = valid ? (a.perm ? __ldg(a.perm + ridx) : ridx) : 0;
+    double ou0 = 0.0, ou1 = 0.0, ou2 = 0.0, op = 0.0;
+    if (valid) {
+        const int kb = __ldg(a.row_ptr + A), ke = __ldg(a.row_ptr + A + 1);
+#pragma unroll 2
+        for (int k = kb + g; k < ke; k += G) {
+            const int B = __ldg(&a.col_idx[k]);
+            const double2* v = reinterpret_cast<const double2*>(a.vals + (long)k * 8);
+            const double2* yv = reinterpret_cast<const double2*>(a.y + (long)B * 4);
+            const double2 ya = __ldg(yv), yb = __ldg(yv + 1);
+            const double2 p0 = ldcs2(v), p1 = ldcs2(v + 1), p2 = ldcs2(v + 2), p3 = ldcs2(v + 3);
+            ou0 += p0.x * ya.x + p0.y * yb.y;
+            ou1 += p0.x * ya.y + p1.x * yb.y;
+            ou2 += p0.x * yb.x + p1.y * yb.y;
+            op += p2.x * ya.x;
+            op += p2.y * ya.y;
+            op += p3.x * yb.x;
+            op += p3.y * yb.y;
+        }
+    }
+#pragma unroll
+    for (int off = 1; off < G; off <<= 1) {
+        ou0 += __shfl_xor_sync(0xffffffffu, ou0, off, G);
+        ou1 += __shfl_xor_sync(0xffffffffu, ou1, off, G);
+        ou2 += __shfl_xor_sync(0xffffffffu, ou2, off, G);
+        op += __shfl_xor_sync(0xffffffffu, op, off, G);
+    }
+    if (valid && g == 0) {
+        const long o = (long)A * 4;
+        if (SCALED) {
+            const double2 s0 = __ldg(reinterpret_cast<const double2*>(a.scale_out + o));
+            const double2 s1 = __ldg(reinterpret_cast<const double2*>(a.scale_out + o) + 1);
+            ou0 *= s0.x;
+            ou1 *= s0.y;
+            ou2 *= s1.x;
+            op *= s1.y;
+        }
+        double2* out = reinterpret_cast<double2*>(a.out + o);
+        out[0] = make_double2(ou0, ou1);
+        out[1] = make_double2(ou2, op);
+    }
+}
+
+void launch_lmatvec(const MatvecArgs& a_in, cudaStream_t st) {
+    if (a_in.nn <= 0)
         return;
+    MatvecArgs a = a_in;
+    // variant bit 0: row order by length (perm); bit 1 (N == 1): G-lane rows
+    if (!(a.variant & 1))
+        a.perm = nullptr;
+    if (a.N == 1 && (a.variant & 2)) {
+        constexpr int G = 4;
+        const int blocks = (int)(((long)a.nn * G + 255) / 256);
+        note_launch();
+        if (a.scale_out)
+            lmatvec_n1g_kernel<true, G><<<blocks, 256, 0, st>>>(a);
+        else
+            lmatvec_n1g_kernel<false, G><<<blocks, 256, 0, st>>>(a);
+        return;
+    }
     const int blocks = (a.nn + a.rows_per_cta - 1) / a.rows_per_cta;
     const int threads = a.rows_per_cta * a.N;
     const size_t smem =
