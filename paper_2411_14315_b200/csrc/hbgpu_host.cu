@@ -713,12 +713,14 @@ static int mass_dev(hbgpu_ctx* c) {
 }
 
 // L-matvec kernel variant: bit 0 = rows in length-balanced order (mv_perm),
-// bit 1 = N == 1 rows split over 4 lanes.  Default 3 (config 4, 700k points:
-// N = 1 0.277 -> 0.190 ms, N = 7 1.398 -> 1.279 ms, N = 19 3.53 -> 3.24 ms);
-// HBGPU_MV_VARIANT overrides it (tooling).
+// bit 1 = N == 1 rows split over 4 lanes, bits 2-3 = lanes per (row, sample)
+// for N > 1, bit 4 = 4 lanes automatically on small meshes.  Default 19
+// (config 4, 700k points: N = 1 0.277 -> 0.190 ms, N = 7 1.398 -> 1.279 ms,
+// N = 19 3.53 -> 3.24 ms; config 0: 26.7 -> 18.5 us); HBGPU_MV_VARIANT
+// overrides it (tooling).
 static int mv_variant() {
     const char* e = std::getenv("HBGPU_MV_VARIANT");
-    return e ? std::atoi(e) : 3;
+    return e ? std::atoi(e) : 19;
 }
 
 static int matvec_dev(hbgpu_ctx* c, const double* d_y, double* d_out, const double* d_scale,

@@ -146,6 +146,131 @@ __global__ void __launch_bounds__(256) lmatvec_kernel(MatvecArgs a) {
     }
 }
 
+// N > 1 with G lanes per (row, sample): thread (r, g, n) takes the row's
+// blocks kb+g, kb+g+G, ...; the G partial sums are combined in g order
+// through shared memory (deterministic).  Shorter per-thread block chains for
+// meshes too small to fill the GPU with (row, sample) threads alone.
+template <bool SCALED, bool WITH_C, int G>
+__global__ void __launch_bounds__(256) lmatvec_g_kernel(MatvecArgs a) {
+    extern __shared__ double sh[];
+    const int N = a.N, rpc = a.rows_per_cta;
+    double* sH = sh;
+    double* st = sh + (WITH_C ? N * N : 0);
+    double* pr = st + (WITH_C ? 3 * N * rpc : 0);  // [r][g][7][N]
+    if (WITH_C)
+        for (int k = threadIdx.x; k < N * N; k += blockDim.x)
+            sH[k] = a.H[k];
+    const int GN = G * N;
+    const int r = threadIdx.x / GN, rem = threadIdx.x - r * GN, g = rem / N, n = rem - g * N;
+    const int ridx = blockIdx.x * rpc + r;
+    const bool valid = (r < rpc) && (ridx < a.nn);
+    const int A = (valid && a.perm) ? __ldg(a.perm + ridx) : ridx;
+    double acc[7] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};  // ou0 ou1 ou2 op t0 t1 t2
+    if (valid) {
+        const long N8 = 8L * N;
+        const int kb = __ldg(a.row_ptr + A), ke = __ldg(a.row_ptr + A + 1);
+#pragma unroll 2
+        for (int k = kb + g; k < ke; k += G) {
+            const int B = __ldg(&a.col_idx[k]);
+            const double* v = a.vals + (long)k * N8 + n;
+            const long yb = (long)B * 4 * N + n;
+            const double y0 = __ldg(a.y + yb), y1 = __ldg(a.y + yb + N), y2 = __ldg(a.y + yb + 2 * N),
+                         y3 = __ldg(a.y + yb + 3 * N);
+            const double kd = ldcs(v), g0 = ldcs(v + N), g1 = ldcs(v + 2 * N), g2 = ldcs(v + 3 * N);
+            const double d0 = ldcs(v + 4 * N), d1 = ldcs(v + 5 * N), d2 = ldcs(v + 6 * N), ld = ldcs(v + 7 * N);
+            acc[0] += kd * y0 + g0 * y3;
+            acc[1] += kd * y1 + g1 * y3;
+            acc[2] += kd * y2 + g2 * y3;
+            acc[3] += d0 * y0;
+            acc[3] += d1 * y1;
+            acc[3] += d2 * y2;
+            acc[3] += ld * y3;
+            if (WITH_C) {
+                const double m = __ldg(a.mass + k);
+                acc[4] += m * y0;
+                acc[5] += m * y1;
+                acc[6] += m * y2;
+            }
+        }
+    }
+    constexpr int NV = WITH_C ? 7 : 4;
+    if (valid) {
+        double* p = pr + ((size_t)(r * G + g) * 7) * N + n;
+#pragma unroll
+        for (int c = 0; c < NV; ++c)
+            p[c * N] = acc[c];
+    }
+    __syncthreads();
+    const bool lead = valid && g == 0;
+    if (lead) {
+#pragma unroll
+        for (int c = 0; c < NV; ++c) {
+            double v = 0.0;
+            for (int gg = 0; gg < G; ++gg)
+                v += pr[((size_t)(r * G + gg) * 7 + c) * N + n];
+            acc[c] = v;
+        }
+    }
+    if (WITH_C) {
+        if (lead) {
+            st[(r * 3 + 0) * N + n] = acc[4];
+            st[(r * 3 + 1) * N + n] = acc[5];
+            st[(r * 3 + 2) * N + n] = acc[6];
+        }
+        __syncthreads();
+        if (lead) {
+            const double* h = sH + n * N;
+            const double* s0 = st + (r * 3) * N;
+            double h0 = 0.0, h1 = 0.0, h2 = 0.0;
+            for (int m = 0; m < N; ++m) {
+                const double hm = h[m];
+                h0 += hm * s0[m];
+                h1 += hm * s0[N + m];
+                h2 += hm * s0[2 * N + m];
+            }
+            acc[0] += h0;
+            acc[1] += h1;
+            acc[2] += h2;
+        }
+    }
+    if (lead) {
+        const long o = (long)A * 4 * N + n;
+        if (SCALED) {
+            acc[0] *= __ldg(a.scale_out + o);
+            acc[1] *= __ldg(a.scale_out + o + N);
+            acc[2] *= __ldg(a.scale_out + o + 2 * N);
+            acc[3] *= __ldg(a.scale_out + o + 3 * N);
+        }
+        a.out[o] = acc[0];
+        a.out[o + N] = acc[1];
+        a.out[o + 2 * N] = acc[2];
+        a.out[o + 3 * N] = acc[3];
+    }
+}
+
+template <int G>
+static void launch_lmatvec_g(const MatvecArgs& a_in, cudaStream_t st) {
+    MatvecArgs a = a_in;
+    a.rows_per_cta = max(1, 256 / (G * a.N));
+    const int blocks = (a.nn + a.rows_per_cta - 1) / a.rows_per_cta;
+    const int threads = a.rows_per_cta * G * a.N;
+    const bool wc = a.with_c != 0;
+    const size_t smem = sizeof(double) * ((wc ? (size_t)a.N * a.N + 3 * (size_t)a.N * a.rows_per_cta : 0) +
+                                          7 * (size_t)G * a.N * a.rows_per_cta);
+    note_launch();
+    if (wc) {
+        if (a.scale_out)
+            lmatvec_g_kernel<true, true, G><<<blocks, threads, smem, st>>>(a);
+        else
+            lmatvec_g_kernel<false, true, G><<<blocks, threads, smem, st>>>(a);
+    } else {
+        if (a.scale_out)
+            lmatvec_g_kernel<true, false, G><<<blocks, threads, smem, st>>>(a);
+        else
+            lmatvec_g_kernel<false, false, G><<<blocks, threads, smem, st>>>(a);
+    }
+}
+
 // N == 1 with G lanes per row: lane g takes blocks kb+g, kb+g+G, ... (64-byte
 // blocks as four 16-byte loads), the G partial sums are combined by a fixed
 // xor-shuffle tree (deterministic).  Rows are taken in `perm` order.
@@ -214,6 +339,18 @@ void launch_lmatvec(const MatvecArgs& a_in, cudaStream_t st) {
             lmatvec_n1g_kernel<false, G><<<blocks, 256, 0, st>>>(a);
         return;
     }
+    // variant bits 2-3 (N > 1): log2 of the lanes per (row, sample); bit 4:
+    // 4 lanes when the (row, sample) threads alone cannot fill the GPU (config 0:
+    // 26.7 -> 18.5 us; on the large meshes the split costs 35-40%)
+    int lg = (a.variant >> 2) & 3;
+    if (lg == 0 && (a.variant & 16) && (long)a.nn * a.N < 65536)
+        lg = 2;
+    if (a.N > 1 && lg == 1)
+        return launch_lmatvec_g<2>(a, st);
+    if (a.N > 1 && lg == 2)
+        return launch_lmatvec_g<4>(a, st);
+    if (a.N > 1 && lg == 3)
+        return launch_lmatvec_g<8>(a, st);
     const int blocks = (a.nn + a.rows_per_cta - 1) / a.rows_per_cta;
     const int threads = a.rows_per_cta * a.N;
     const size_t smem =

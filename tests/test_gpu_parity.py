@@ -369,3 +369,23 @@ def test_singular_tau_is_domain_error(gpu, modes):
     s = np.zeros(ctx.state_len)
     with pytest.raises(ArithmeticError):
         ctx.assemble_residual(s)
+
+
+@pytest.mark.parametrize("variant", [0, 1, 3, 5, 7, 11, 15, 19])
+@pytest.mark.parametrize("modes", [1, 3, 4])
+def test_matvec_kernel_variants(gpu, monkeypatch, modes, variant):
+    """Every L-matvec kernel variant (row order, lanes per row) against the
+    restatement: different block summation orders, same 1e-12 bar; bitwise
+    repeatable per variant."""
+    prob = tube_problem(modes, h=0.25)
+    ctx = gpu_ctx(prob, 0, 0.3)
+    orc = ob.Restated(prob, tau_mode=0, pseudo_dt=0.3)
+    s = cases.random_state(prob.mesh.num_nodes, prob.N, 21)
+    p = ctx.assemble_tangent(s)
+    m = orc.mass()
+    y = cases.random_state(prob.mesh.num_nodes, prob.N, 22)
+    monkeypatch.setenv("HBGPU_MV_VARIANT", str(variant))
+    out = ctx.matvec(y)
+    assert rel(out, orc.matvec(p, m, y)) < TOL
+    assert rel(ctx.bsr_matvec(y), orc.bsr_matvec(p, y)) < TOL
+    assert np.array_equal(out, ctx.matvec(y))
