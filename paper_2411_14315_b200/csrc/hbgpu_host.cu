@@ -136,6 +136,12 @@ struct hbgpu_ctx {
     size_t red_cap = 1024;
     DBuf<int> flag, ideg;
     int* h_int = nullptr;  // pinned
+    // device-resident Arnoldi state of gmres_dev (see arnoldi_step_kernel)
+    DBuf<double> arn;
+    DBuf<int> arn_ctl;
+    size_t arn_m = 0, arn_hist = 0;
+    int* h_ctl = nullptr;  // pinned, 3 slots x 4
+    cudaEvent_t ctl_ev[2] = {nullptr, nullptr};
 
     bool mass_valid = false, p_valid = false, inv_valid = false;
 
@@ -183,6 +189,10 @@ enum Phase {
     kPhJacobi,
     kPhGmres,
     kPhMass,
+    kPhGmDots,  // device-resident GMRES step: dot pass + its reduction
+    kPhGmArnoldi,
+    kPhGmUpdate,  // update pass + normalisation
+    kPhGmMatvec,
     kPhCount
 };
 
@@ -724,7 +734,7 @@ static int mv_variant() {
 }
 
 static int matvec_dev(hbgpu_ctx* c, const double* d_y, double* d_out, const double* d_scale,
-                      bool with_c, const double* d_scale_out = nullptr) {
+                      bool with_c, const double* d_scale_out = nullptr, const int* d_skip = nullptr) {
     if (!c->p_valid)
         return fail(c, HBGPU_ERR_INVALID, "matvec before assemble_tangent / set_pvals");
     if (with_c && c->N > 1 && !c->mass_valid)
@@ -743,6 +753,7 @@ static int matvec_dev(hbgpu_ctx* c, const double* d_y, double* d_out, const doub
         return fail(c, HBGPU_ERR_INVALID, "input-scaled matvec is not supported (scale z on the host side)");
     a.scale_out = d_scale_out;
     a.perm = c->mv_perm.p;
+    a.skip = d_skip;
     a.variant = mv_variant();
     a.nn = c->nn;
     a.N = c->N;
@@ -836,6 +847,47 @@ static int gmres_dev(hbgpu_ctx* c, const double* d_rhs, const double* d_inv,
         CK(c, cudaMallocHost(reinterpret_cast<void**>(&c->h_red), sizeof(double) * need));
         c->red_cap = need;
     }
+    // HBGPU_GMRES_HOST=1 (or a restart too long for the Arnoldi kernel's shared
+    // memory, m > ~700): the host-driven step loop, one synchronisation per
+    // step; else the device-resident cycle
+    const bool devloop = std::getenv("HBGPU_GMRES_HOST") == nullptr && arnoldi_step_smem(m) <= 200 * 1024;
+    ArnoldiDev ad{};
+    if (devloop) {
+        const size_t hsz = size_t(m + 2) * size_t(m + 1);
+        const size_t hist = size_t(std::max(kc->max_iters, 0)) + 2;
+        if (c->arn_m < size_t(m) || c->arn_hist < hist) {
+            CK(c, c->arn.alloc(2 * hsz + 3 * (size_t(m) + 2) + hist));
+            c->arn_m = size_t(m);
+            c->arn_hist = hist;
+        }
+        if (!c->arn_ctl.p) {
+            CK(c, c->arn_ctl.alloc(4));
+            CK(c, cudaMallocHost(reinterpret_cast<void**>(&c->h_ctl), sizeof(int) * 12));
+            for (auto& e : c->ctl_ev)
+                CK(c, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        }
+        ad.Hm = c->arn.p;
+        ad.R = ad.Hm + hsz;
+        ad.cs = ad.R + hsz;
+        ad.sn = ad.cs + (m + 2);
+        ad.gv = ad.sn + (m + 2);
+        ad.hist = ad.gv + (m + 2);
+        ad.ctl = c->arn_ctl.p;
+        ad.m = m;
+        ad.hcap = int(std::min<size_t>(hist, size_t(std::max(hcap, 0))));
+        if (arnoldi_step_smem(m) > 48 * 1024)
+            CK(c, configure_arnoldi_smem(m));
+    }
+    // device history (indexed by iteration) -> caller's buffer, at every exit
+    auto pull_hist = [&]() -> int {
+        if (!devloop || !history || hcap <= 1 || res->iterations <= 0)
+            return HBGPU_OK;
+        const int cnt = std::min(res->iterations + 1, std::min(hcap, ad.hcap));
+        if (cnt > 1)
+            CK(c, cudaMemcpy(history + 1, ad.hist + 1, sizeof(double) * size_t(cnt - 1), cudaMemcpyDeviceToHost));
+        res->history_len = cnt;
+        return HBGPU_OK;
+    };
     double* V = c->V.p;
     const size_t o_coef = 2 * size_t(m) + 4, o_norm = 4 * size_t(m) + 8;
     double* d_norm = c->red.p + o_norm;
@@ -866,103 +918,175 @@ static int gmres_dev(hbgpu_ctx* c, const double* d_rhs, const double* d_inv,
         std::fill(R.begin(), R.end(), 0.0);
         std::fill(gv.begin(), gv.end(), 0.0);
         gv[0] = rnorm;
-        c->h_red[0] = rnorm;
-        CK(c, cudaMemcpyAsync(c->red.p, c->h_red, sizeof(double), cudaMemcpyHostToDevice, st));
-        // V_0 = r/|r| (exactly normalised), z = S V_0
-        launch_normalize(rsrc, c->red.p, V, n, st, c->scale.p, c->z.p);
+        if (!devloop) {
+            c->h_red[0] = rnorm;
+            CK(c, cudaMemcpyAsync(c->red.p, c->h_red, sizeof(double), cudaMemcpyHostToDevice, st));
+            // V_0 = r/|r| (exactly normalised), z = S V_0
+            launch_normalize(rsrc, c->red.p, V, n, st, c->scale.p, c->z.p);
+        }
         int ncols = 0;  // finalised columns of this cycle
-        bool stop = false;
-        for (int j = 0; !stop; ++j) {
-            double* u = V + size_t(j) * size_t(n);
-            // last step of the cycle: only finalise column j-1
-            const bool last = (j == m) || (res->iterations + (j >= 1 ? 1 : 0) >= kc->max_iters);
-            if (!last)
-                TRY(matvec_dev(c, c->z.p, c->w.p, nullptr, true, c->scale.p));  // w = S A S u_j
-            launch_dcgs_dots(V, n, j, u, last ? nullptr : c->w.p, n, c->partial.p, st);
-            const int rows = last ? j + 1 : 2 * j + 3;
-            launch_reduce_partials(c->partial.p, rows, c->red.p, 0, st);
-            TRY(check_launch(c));
-            CK(c, cudaMemcpyAsync(c->h_red, c->red.p, sizeof(double) * size_t(rows),
-                                  cudaMemcpyDeviceToHost, st));
-            if (j >= 1)
-                CK(c, cudaMemcpyAsync(c->h_red + o_norm, d_norm, sizeof(double), cudaMemcpyDeviceToHost, st));
-            CK(c, cudaStreamSynchronize(st));
-            const double* a = c->h_red;
-            const double uu = last ? c->h_red[j] : c->h_red[2 * j];
-            double aa = 0.0;
-            for (int i = 0; i < j; ++i) {
-                av[size_t(i)] = a[i];
-                aa += a[i] * a[i];
-            }
-            const double rho2 = uu - aa;
-            const double rho = rho2 > 0.0 ? std::sqrt(rho2) : 0.0;
-            if (j >= 1) {
-                // finalise column j-1: H[j, j-1] held |w'_{j-1}| (the norm u_j was built with)
-                HH(j, j - 1) = c->h_red[o_norm];
-                const double hjj1 = HH(j, j - 1);
-                for (int i = 0; i < j; ++i)
-                    HH(i, j - 1) += hjj1 * av[size_t(i)];
-                HH(j, j - 1) = hjj1 * rho;
-                // Givens (linalg.cpp:237-258) on the final column
-                const int k = j - 1;
-                for (int i = 0; i <= j; ++i)
-                    RR(i, k) = HH(i, k);
-                for (int i = 0; i < k; ++i) {
-                    const double t = cs[size_t(i)] * RR(i, k) + sn[size_t(i)] * RR(i + 1, k);
-                    RR(i + 1, k) = -sn[size_t(i)] * RR(i, k) + cs[size_t(i)] * RR(i + 1, k);
-                    RR(i, k) = t;
+        if (devloop) {
+            // Device-resident cycle: the dense Arnoldi/Givens work of each step
+            // runs in arnoldi_step_kernel, so steps are enqueued in batches of
+            // kBatch with no host round trip; the host polls the stop flag one
+            // batch behind (steps enqueued past a stop return at once).
+            constexpr int kBatch = 8;
+            const int it0 = res->iterations;
+            launch_arnoldi_init(ad, rnorm, it0, res->reorthogonalizations, c->red.p, st);
+            launch_normalize(rsrc, c->red.p, V, n, st, c->scale.p, c->z.p);
+            int j = 0, batch = 0, pending = -1;
+            bool ended = false;
+            while (!ended) {
+                for (int q = 0; q < kBatch; ++q, ++j) {
+                    double* u = V + size_t(j) * size_t(n);
+                    const bool last = (j == m) || (j >= 1 && it0 + j >= kc->max_iters);
+                    const long q0 = prof_mark(c);
+                    if (!last)
+                        TRY(matvec_dev(c, c->z.p, c->w.p, nullptr, true, c->scale.p, ad.ctl));
+                    const long q1 = prof_mark(c);
+                    if (n <= kDots2dMax)
+                        launch_dcgs_dots2d(V, n, j, u, last ? nullptr : c->w.p, n, c->partial.p, st, ad.ctl);
+                    else
+                        launch_dcgs_dots(V, n, j, u, last ? nullptr : c->w.p, n, c->partial.p, st, ad.ctl);
+                    launch_reduce_partials(c->partial.p, last ? j + 1 : 2 * j + 3, c->red.p, 0, st, ad.ctl,
+                                           dcgs_dots_parts(n));
+                    const long q2 = prof_mark(c);
+                    launch_arnoldi_step(ad, j, last ? 1 : 0, c->red.p, d_norm, d_coef, bnorm, kc->tolerance, st);
+                    const long q3 = prof_mark(c);
+                    prof_pair(c, kPhGmMatvec, q0, q1);
+                    prof_pair(c, kPhGmDots, q1, q2);
+                    prof_pair(c, kPhGmArnoldi, q2, q3);
+                    if (last) {
+                        ended = true;
+                        break;
+                    }
+                    double* upart = c->partial.p + size_t(2 * m + 8) * kRedBlocks;
+                    if (n <= kDots2dMax)
+                        launch_dcgs_update2(V, n, j, d_coef, u, c->w.p, n, upart, st, ad.ctl);
+                    else
+                        launch_dcgs_update(V, n, j, d_coef, u, c->w.p, n, upart, st, ad.ctl);
+                    launch_normalize_partials(c->w.p, upart, dcgs_update_parts(n), d_norm,
+                                              V + size_t(j + 1) * size_t(n), c->scale.p, c->z.p, n, st, ad.ctl);
+                    prof_pair(c, kPhGmUpdate, q3, prof_mark(c));
                 }
-                const double den = std::hypot(RR(k, k), RR(k + 1, k));
-                cs[size_t(k)] = den == 0.0 ? 1.0 : RR(k, k) / den;
-                sn[size_t(k)] = den == 0.0 ? 0.0 : RR(k + 1, k) / den;
-                RR(k, k) = den;
-                RR(k + 1, k) = 0.0;
-                gv[size_t(k) + 1] = -sn[size_t(k)] * gv[size_t(k)];
-                gv[size_t(k)] = cs[size_t(k)] * gv[size_t(k)];
-                res->iterations += 1;
-                res->reorthogonalizations += 1;
-                ncols = j;
-                const double est = std::fabs(gv[size_t(k) + 1]);
-                push_hist(est / bnorm);
-                if (est / bnorm <= kc->tolerance || HH(j, j - 1) == 0.0)
-                    stop = true;
+                TRY(check_launch(c));
+                if (ended)
+                    break;
+                const int slot = batch & 1;
+                CK(c, cudaMemcpyAsync(c->h_ctl + 4 * slot, ad.ctl, sizeof(int) * 4, cudaMemcpyDeviceToHost, st));
+                CK(c, cudaEventRecord(c->ctl_ev[slot], st));
+                if (pending >= 0) {
+                    CK(c, cudaEventSynchronize(c->ctl_ev[pending]));
+                    if (c->h_ctl[4 * pending] != 0)
+                        ended = true;
+                }
+                pending = slot;
+                ++batch;
             }
-            if (last || stop)
-                break;
-            // tentative column j and the update pass
-            const double* b = c->h_red + j;
-            const double uw = c->h_red[2 * j + 1];
-            double ab = 0.0;
-            for (int i = 0; i < j; ++i)
-                ab += av[size_t(i)] * b[i];
-            if (!(rho > 0.0)) {
-                stop = true;  // u_j in span(Q): breakdown
-                break;
+            CK(c, cudaMemcpyAsync(c->h_ctl + 8, ad.ctl, sizeof(int) * 4, cudaMemcpyDeviceToHost, st));
+            CK(c, cudaStreamSynchronize(st));
+            res->iterations = c->h_ctl[9];
+            ncols = c->h_ctl[10];
+            res->reorthogonalizations = c->h_ctl[11];
+            if (ncols > 0) {
+                CK(c, cudaMemcpy(R.data(), ad.R, sizeof(double) * size_t(m + 2) * size_t(ncols),
+                                 cudaMemcpyDeviceToHost));
+                CK(c, cudaMemcpy(gv.data(), ad.gv, sizeof(double) * size_t(ncols + 1), cudaMemcpyDeviceToHost));
             }
-            const double cj = (uw - ab) / rho;
-            for (int i = 0; i <= j; ++i) {
-                double ha = 0.0;
-                for (int l = 0; l < j; ++l)
-                    ha += HH(i, l) * av[size_t(l)];
-                HH(i, j) = ((i < j ? b[i] : cj) - ha) / rho;
+        } else {
+            bool stop = false;
+            for (int j = 0; !stop; ++j) {
+                double* u = V + size_t(j) * size_t(n);
+                // last step of the cycle: only finalise column j-1
+                const bool last = (j == m) || (res->iterations + (j >= 1 ? 1 : 0) >= kc->max_iters);
+                if (!last)
+                    TRY(matvec_dev(c, c->z.p, c->w.p, nullptr, true, c->scale.p));  // w = S A S u_j
+                launch_dcgs_dots(V, n, j, u, last ? nullptr : c->w.p, n, c->partial.p, st);
+                const int rows = last ? j + 1 : 2 * j + 3;
+                launch_reduce_partials(c->partial.p, rows, c->red.p, 0, st);
+                TRY(check_launch(c));
+                CK(c, cudaMemcpyAsync(c->h_red, c->red.p, sizeof(double) * size_t(rows),
+                                      cudaMemcpyDeviceToHost, st));
+                if (j >= 1)
+                    CK(c, cudaMemcpyAsync(c->h_red + o_norm, d_norm, sizeof(double), cudaMemcpyDeviceToHost, st));
+                CK(c, cudaStreamSynchronize(st));
+                const double* a = c->h_red;
+                const double uu = last ? c->h_red[j] : c->h_red[2 * j];
+                double aa = 0.0;
+                for (int i = 0; i < j; ++i) {
+                    av[size_t(i)] = a[i];
+                    aa += a[i] * a[i];
+                }
+                const double rho2 = uu - aa;
+                const double rho = rho2 > 0.0 ? std::sqrt(rho2) : 0.0;
+                if (j >= 1) {
+                    // finalise column j-1: H[j, j-1] held |w'_{j-1}| (the norm u_j was built with)
+                    HH(j, j - 1) = c->h_red[o_norm];
+                    const double hjj1 = HH(j, j - 1);
+                    for (int i = 0; i < j; ++i)
+                        HH(i, j - 1) += hjj1 * av[size_t(i)];
+                    HH(j, j - 1) = hjj1 * rho;
+                    // Givens (linalg.cpp:237-258) on the final column
+                    const int k = j - 1;
+                    for (int i = 0; i <= j; ++i)
+                        RR(i, k) = HH(i, k);
+                    for (int i = 0; i < k; ++i) {
+                        const double t = cs[size_t(i)] * RR(i, k) + sn[size_t(i)] * RR(i + 1, k);
+                        RR(i + 1, k) = -sn[size_t(i)] * RR(i, k) + cs[size_t(i)] * RR(i + 1, k);
+                        RR(i, k) = t;
+                    }
+                    const double den = std::hypot(RR(k, k), RR(k + 1, k));
+                    cs[size_t(k)] = den == 0.0 ? 1.0 : RR(k, k) / den;
+                    sn[size_t(k)] = den == 0.0 ? 0.0 : RR(k + 1, k) / den;
+                    RR(k, k) = den;
+                    RR(k + 1, k) = 0.0;
+                    gv[size_t(k) + 1] = -sn[size_t(k)] * gv[size_t(k)];
+                    gv[size_t(k)] = cs[size_t(k)] * gv[size_t(k)];
+                    res->iterations += 1;
+                    res->reorthogonalizations += 1;
+                    ncols = j;
+                    const double est = std::fabs(gv[size_t(k) + 1]);
+                    push_hist(est / bnorm);
+                    if (est / bnorm <= kc->tolerance || HH(j, j - 1) == 0.0)
+                        stop = true;
+                }
+                if (last || stop)
+                    break;
+                // tentative column j and the update pass
+                const double* b = c->h_red + j;
+                const double uw = c->h_red[2 * j + 1];
+                double ab = 0.0;
+                for (int i = 0; i < j; ++i)
+                    ab += av[size_t(i)] * b[i];
+                if (!(rho > 0.0)) {
+                    stop = true;  // u_j in span(Q): breakdown
+                    break;
+                }
+                const double cj = (uw - ab) / rho;
+                for (int i = 0; i <= j; ++i) {
+                    double ha = 0.0;
+                    for (int l = 0; l < j; ++l)
+                        ha += HH(i, l) * av[size_t(l)];
+                    HH(i, j) = ((i < j ? b[i] : cj) - ha) / rho;
+                }
+                const double cr = cj / rho;
+                for (int i = 0; i < j; ++i) {
+                    h_coef[i] = av[size_t(i)];
+                    h_coef[j + i] = b[i] - cr * av[size_t(i)];
+                }
+                h_coef[2 * j] = 1.0 / rho;
+                h_coef[2 * j + 1] = cr;
+                CK(c, cudaMemcpyAsync(d_coef, h_coef, sizeof(double) * size_t(2 * j + 2),
+                                      cudaMemcpyHostToDevice, st));
+                double* upart = c->partial.p + size_t(2 * m + 8) * kRedBlocks;
+                if (j == 0)
+                    gv[0] *= rho;  // V_0 renormalised by its computed norm in the update pass
+                launch_dcgs_update(V, n, j, d_coef, u, c->w.p, n, upart, st);
+                launch_reduce_partials(upart, 1, d_norm, 1, st);
+                // tentative u_{j+1} = w'/|w'| and z = S u_{j+1}
+                launch_normalize(c->w.p, d_norm, V + size_t(j + 1) * size_t(n), n, st, c->scale.p, c->z.p);
+                TRY(check_launch(c));
             }
-            const double cr = cj / rho;
-            for (int i = 0; i < j; ++i) {
-                h_coef[i] = av[size_t(i)];
-                h_coef[j + i] = b[i] - cr * av[size_t(i)];
-            }
-            h_coef[2 * j] = 1.0 / rho;
-            h_coef[2 * j + 1] = cr;
-            CK(c, cudaMemcpyAsync(d_coef, h_coef, sizeof(double) * size_t(2 * j + 2),
-                                  cudaMemcpyHostToDevice, st));
-            double* upart = c->partial.p + size_t(2 * m + 8) * kRedBlocks;
-            if (j == 0)
-                gv[0] *= rho;  // V_0 renormalised by its computed norm in the update pass
-            launch_dcgs_update(V, n, j, d_coef, u, c->w.p, n, upart, st);
-            launch_reduce_partials(upart, 1, d_norm, 1, st);
-            // tentative u_{j+1} = w'/|w'| and z = S u_{j+1}
-            launch_normalize(c->w.p, d_norm, V + size_t(j + 1) * size_t(n), n, st, c->scale.p, c->z.p);
-            TRY(check_launch(c));
         }
         int j = ncols;
         while (j > 0 && RR(j - 1, j - 1) == 0.0)
@@ -987,15 +1111,15 @@ static int gmres_dev(hbgpu_ctx* c, const double* d_rhs, const double* d_inv,
         res->relative_residual = rnorm / bnorm;
         if (res->relative_residual <= kc->tolerance) {
             res->status = 0;
-            return HBGPU_OK;
+            return pull_hist();
         }
         if (rnorm >= cycle_start) {
             res->status = 2;
-            return HBGPU_OK;
+            return pull_hist();
         }
     }
     res->status = 1;
-    return HBGPU_OK;
+    return pull_hist();
 }
 
 // ---------------------------------------------------------------- C ABI
@@ -1100,6 +1224,13 @@ void hbgpu_destroy(hbgpu_ctx* c) {
         cudaFreeHost(c->h_red);
     if (c->h_int)
         cudaFreeHost(c->h_int);
+    if (c->h_ctl)
+        cudaFreeHost(c->h_ctl);
+    for (cudaEvent_t e : c->ctl_ev)
+        if (e)
+            cudaEventDestroy(e);
+    c->arn.release();
+    c->arn_ctl.release();
     for (DBuf<double>* b : {&c->geom, &c->H, &c->g, &c->hN, &c->fnormal, &c->farea, &c->state,
                             &c->r, &c->hu, &c->pvals, &c->mass, &c->mass_c, &c->inv, &c->y, &c->out,
                             &c->x, &c->w, &c->z, &c->scale, &c->b, &c->tmp, &c->V, &c->partial, &c->red, &c->rpartial})

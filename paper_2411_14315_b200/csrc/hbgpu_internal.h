@@ -204,6 +204,7 @@ struct MatvecArgs {
     const double* scale;      // optional input scaling (gathered): L (S y)
     const double* scale_out;  // optional output scaling: S L y
     const int* perm;          // optional row order (rows of similar length per CTA)
+    const int* skip;          // optional device stop flag (GMRES steps past convergence)
     int nn, N, rows_per_cta;
     int with_c;
     int variant;              // kernel variant (tooling: HBGPU_MV_VARIANT)
@@ -286,16 +287,53 @@ void launch_scaled_diff(const double* s, const double* a, const double* b, doubl
 void launch_multidot(const double* V, long ld, int nv, const double* w, long n, double* partial,
                      cudaStream_t st);
 // out[i] = sum_b partial[i*kRedBlocks+b] (fixed order); optional sqrt of out[0]
+// `skip` (nullable, device): when *skip != 0 the kernel returns at once (GMRES
+// steps enqueued past a device-side stop).
 void launch_reduce_partials(const double* partial, int nv, double* out, int take_sqrt,
-                            cudaStream_t st);
+                            cudaStream_t st, const int* skip = nullptr, int nparts = kRedBlocks);
 // GMRES orthogonalisation passes (hbgpu_krylov.cu)
 void launch_dcgs_dots(const double* V, long ld, int nv, const double* u, const double* w, long n,
-                      double* partial, cudaStream_t st);
+                      double* partial, cudaStream_t st, const int* skip = nullptr);
 void launch_dcgs_update(const double* V, long ld, int nv, const double* coef, double* u, double* w,
-                        long n, double* partial, cudaStream_t st);
+                        long n, double* partial, cudaStream_t st, const int* skip = nullptr);
+// Short vectors (n <= kDots2dMax): 2-D grid dot pass over dcgs_dots_parts(n)
+// element chunks (reduce with nparts = dcgs_dots_parts(n)).
+constexpr long kDots2dMax = 1L << 20;
+int dcgs_dots_parts(long n);
+void launch_dcgs_dots2d(const double* V, long ld, int nv, const double* u, const double* w, long n,
+                        double* partial, cudaStream_t st, const int* skip = nullptr);
+int dcgs_update_parts(long n);
+void launch_dcgs_update2(const double* V, long ld, int nv, const double* coef, double* u, double* w, long n,
+                         double* partial, cudaStream_t st, const int* skip = nullptr);
+// Device-resident Arnoldi/Givens state of one GMRES solve (hbgpu_krylov.cu).
+struct ArnoldiDev {
+    double* Hm;    // (m+2) x (m+1) Hessenberg, column-major, ld m+2
+    double* R;     // its Givens-rotated copy
+    double* cs;    // m+1
+    double* sn;    // m+1
+    double* gv;    // m+2
+    double* hist;  // residual history indexed by iteration (hcap entries)
+    int* ctl;      // [0] stop, [1] iterations, [2] final columns of the cycle, [3] reorthogonalisations
+    int m, hcap;
+};
+// Step j of a cycle: from the reduced dot pass `red`, finalise column j-1
+// (Givens, estimate, convergence test) and, unless the cycle ends, the
+// tentative column j and the update coefficients.  d_norm = |w'_{j-1}|.
+// H is row-major on the device, R column-major.
+void launch_arnoldi_step(const ArnoldiDev& d, int j, int last, const double* red, const double* d_norm,
+                         double* coef, double bnorm, double tol, cudaStream_t st);
+size_t arnoldi_step_smem(int m);
+cudaError_t configure_arnoldi_smem(int m);
+// out = in/|in|, z = s*out, |in| = sqrt(sum of nparts partials) (also -> norm_out)
+void launch_normalize_partials(const double* in, const double* partial, int nparts, double* norm_out,
+                               double* out, const double* s, double* z, long n, cudaStream_t st,
+                               const int* skip);
+// Cycle start: zero H, R, gv; gv[0] = red0[0] = rnorm; ctl = {0, it, 0, reorth}.
+void launch_arnoldi_init(const ArnoldiDev& d, double rnorm, int it, int reorth, double* red0,
+                         cudaStream_t st);
 void launch_basis_combine(const double* V, long ld, int nv, const double* y, const double* s,
                           double* x, long n, cudaStream_t st);
 void launch_normalize(const double* in, const double* alpha, double* out, long n, cudaStream_t st,
-                      const double* s = nullptr, double* z = nullptr);
+                      const double* s = nullptr, double* z = nullptr, const int* skip = nullptr);
 
 }  // namespace hbgpu

@@ -806,22 +806,24 @@ void launch_multidot(const double* V, long ld, int nv, const double* w, long n, 
 }
 
 __global__ void reduce_partials_kernel(const double* __restrict__ partial, double* out,
-                                       int take_sqrt) {
+                                       int take_sqrt, const int* skip, int nparts) {
+    if (skip && *skip)
+        return;
     __shared__ double red[kRedThreads / 32];
     const double* p = partial + (long)blockIdx.x * kRedBlocks;
     double acc = 0.0;
-    for (int k = threadIdx.x; k < kRedBlocks; k += blockDim.x)
+    for (int k = threadIdx.x; k < nparts; k += blockDim.x)
         acc += p[k];
     const double s = block_sum(acc, red);
     if (threadIdx.x == 0)
         out[blockIdx.x] = (take_sqrt && blockIdx.x == 0) ? sqrt(s) : s;
 }
 void launch_reduce_partials(const double* partial, int nv, double* out, int take_sqrt,
-                            cudaStream_t st) {
+                            cudaStream_t st, const int* skip, int nparts) {
     if (nv <= 0)
         return;
     note_launch();
-    reduce_partials_kernel<<<nv, kRedThreads, 0, st>>>(partial, out, take_sqrt);
+    reduce_partials_kernel<<<nv, kRedThreads, 0, st>>>(partial, out, take_sqrt, skip, nparts);
 }
 
 // DFMA throughput probe: 8 independent FMA chains per thread, enough CTAs

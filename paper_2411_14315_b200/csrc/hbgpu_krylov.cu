@@ -5,6 +5,8 @@
 // bit-reproducible run to run.
 #include "hbgpu_internal.h"
 
+#include <algorithm>
+
 namespace hbgpu {
 
 namespace {
@@ -52,7 +54,10 @@ __global__ void __launch_bounds__(kRedThreads) dcgs_dots_kernel(const double* __
                                                                 long ld, int nv,
                                                                 const double* __restrict__ u,
                                                                 const double* __restrict__ w,
-                                                                long n, double* partial) {
+                                                                long n, double* partial,
+                                                                const int* skip) {
+    if (skip && *skip)
+        return;
     constexpr int NW = kRedThreads / 32;
     __shared__ double red[2][NW][8];
     long lo, hi;
@@ -142,9 +147,135 @@ __global__ void __launch_bounds__(kRedThreads) dcgs_dots_kernel(const double* __
 }
 
 void launch_dcgs_dots(const double* V, long ld, int nv, const double* u, const double* w, long n,
-                      double* partial, cudaStream_t st) {
+                      double* partial, cudaStream_t st, const int* skip) {
     note_launch();
-    dcgs_dots_kernel<<<kRedBlocks, kRedThreads, 0, st>>>(V, ld, nv, u, w, n, partial);
+    dcgs_dots_kernel<<<kRedBlocks, kRedThreads, 0, st>>>(V, ld, nv, u, w, n, partial, skip);
+}
+
+// The same dot pass for short vectors (n <= kDots2dMax): a 2-D grid, x = element
+// chunk (nparts chunks of ~2048), y = group of eight basis vectors (the last
+// group: <u,u>, <u,w>, <w,w>).  Every CTA issues all its loads up front and
+// reduces once, so the pass is not a chain of per-group block reductions
+// (config 0: 147,620-long vectors, ~40 us -> bandwidth-bound).  Same partial
+// layout, nparts chunks per row.
+constexpr int kDotsChunk = 2048;  // elements per chunk: 256 threads x 4 x double2
+__global__ void __launch_bounds__(kRedThreads, 2) dcgs_dots2d_kernel(const double* __restrict__ V,
+                                                                     long ld, int nv,
+                                                                     const double* __restrict__ u,
+                                                                     const double* __restrict__ w,
+                                                                     long n, int nparts, double* partial,
+                                                                     const int* skip) {
+    if (skip && *skip)
+        return;
+    constexpr int NW = kRedThreads / 32, PER = kDotsChunk / (2 * kRedThreads);
+    __shared__ double red[NW][16];
+    const long lo = (long)blockIdx.x * kDotsChunk, hi = min(n, lo + kDotsChunk);
+    const int g = blockIdx.y, ngroups = (nv + 7) / 8;
+    const bool hw = w != nullptr;
+    const bool full = hi - lo == kDotsChunk;  // rows are 16-byte aligned (n % 4 == 0)
+    double du[8], dw[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+        du[q] = dw[q] = 0.0;
+    if (g < ngroups) {
+        const int r0 = 8 * g, nr = min(8, nv - r0);
+        const double* v0 = V + (long)r0 * ld;
+        if (full) {
+            // every load of the chunk is independent: 4 x double2 per vector per thread
+            double2 uu[PER], ww[PER];
+#pragma unroll
+            for (int i = 0; i < PER; ++i) {
+                const long k = lo + 2L * (threadIdx.x + i * kRedThreads);
+                uu[i] = *reinterpret_cast<const double2*>(u + k);
+                ww[i] = hw ? *reinterpret_cast<const double2*>(w + k) : make_double2(0.0, 0.0);
+            }
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+                if (q < nr) {
+                    double2 x[PER];
+#pragma unroll
+                    for (int i = 0; i < PER; ++i)
+                        x[i] = __ldcs(reinterpret_cast<const double2*>(v0 + (long)q * ld + lo +
+                                                                       2L * (threadIdx.x + i * kRedThreads)));
+#pragma unroll
+                    for (int i = 0; i < PER; ++i) {
+                        du[q] += x[i].x * uu[i].x + x[i].y * uu[i].y;
+                        dw[q] += x[i].x * ww[i].x + x[i].y * ww[i].y;
+                    }
+                }
+        } else {
+            for (long k = lo + threadIdx.x; k < hi; k += blockDim.x) {
+                const double uk = u[k], wk = hw ? w[k] : 0.0;
+#pragma unroll
+                for (int q = 0; q < 8; ++q)
+                    if (q < nr) {
+                        const double x = __ldcs(v0 + (long)q * ld + k);
+                        du[q] += x * uk;
+                        dw[q] += x * wk;
+                    }
+            }
+        }
+    } else {
+        for (long k = lo + threadIdx.x; k < hi; k += blockDim.x) {
+            const double uk = u[k];
+            du[0] += uk * uk;
+            if (hw) {
+                const double wk = w[k];
+                du[1] += uk * wk;
+                du[2] += wk * wk;
+            }
+        }
+    }
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            du[q] += __shfl_down_sync(0xffffffffu, du[q], o);
+            dw[q] += __shfl_down_sync(0xffffffffu, dw[q], o);
+        }
+    if (lane == 0)
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            red[wid][q] = du[q];
+            red[wid][8 + q] = dw[q];
+        }
+    __syncthreads();
+    if (threadIdx.x < 16) {
+        const int c = threadIdx.x, q = c & 7;
+        double sum = 0.0;
+#pragma unroll
+        for (int k2 = 0; k2 < NW; ++k2)
+            sum += red[k2][c];
+        if (g < ngroups) {
+            const int r = 8 * g + q;
+            if (r < nv) {
+                if (c < 8)
+                    partial[(long)r * kRedBlocks + blockIdx.x] = sum;
+                else if (hw)
+                    partial[(long)(nv + r) * kRedBlocks + blockIdx.x] = sum;
+            }
+        } else if (c < 3) {
+            if (hw)
+                partial[(long)(2 * nv + c) * kRedBlocks + blockIdx.x] = sum;
+            else if (c == 0)
+                partial[(long)nv * kRedBlocks + blockIdx.x] = sum;
+        }
+    }
+}
+
+int dcgs_dots_parts(long n) {
+    if (n > kDots2dMax)
+        return kRedBlocks;
+    const long p = (n + kDotsChunk - 1) / kDotsChunk;
+    return (int)(p < 1 ? 1 : (p > kRedBlocks ? kRedBlocks : p));
+}
+
+void launch_dcgs_dots2d(const double* V, long ld, int nv, const double* u, const double* w, long n,
+                        double* partial, cudaStream_t st, const int* skip) {
+    note_launch();
+    const dim3 grid(dcgs_dots_parts(n), (nv + 7) / 8 + 1);
+    dcgs_dots2d_kernel<<<grid, kRedThreads, 0, st>>>(V, ld, nv, u, w, n, (int)grid.x, partial, skip);
 }
 
 // DCGS2 update pass, one read of V_0..V_{nv-1}:
@@ -156,7 +287,9 @@ __global__ void __launch_bounds__(kRedThreads) dcgs_update_kernel(const double* 
                                                                   const double* __restrict__ coef,
                                                                   double* __restrict__ u,
                                                                   double* __restrict__ w, long n,
-                                                                  double* partial) {
+                                                                  double* partial, const int* skip) {
+    if (skip && *skip)
+        return;
     extern __shared__ double cs[];
     for (int i = threadIdx.x; i < 2 * nv + 2; i += blockDim.x)
         cs[i] = coef[i];
@@ -220,10 +353,76 @@ __global__ void __launch_bounds__(kRedThreads) dcgs_update_kernel(const double* 
 }
 
 void launch_dcgs_update(const double* V, long ld, int nv, const double* coef, double* u, double* w,
-                        long n, double* partial, cudaStream_t st) {
+                        long n, double* partial, cudaStream_t st, const int* skip) {
     note_launch();
     dcgs_update_kernel<<<kRedBlocks, kRedThreads, sizeof(double) * (2 * nv + 2), st>>>(
-        V, ld, nv, coef, u, w, n, partial);
+        V, ld, nv, coef, u, w, n, partial, skip);
+}
+
+// The update pass for short vectors (n <= kDots2dMax, n % 4 == 0): thread per
+// pair of elements (16-byte loads), sixteen basis vectors in flight, grid of
+// dcgs_update_parts(n) CTAs (one ||w'||^2 partial each).
+__global__ void __launch_bounds__(kRedThreads) dcgs_update2_kernel(const double* __restrict__ V,
+                                                                   long ld, int nv,
+                                                                   const double* __restrict__ coef,
+                                                                   double* __restrict__ u,
+                                                                   double* __restrict__ w, long n,
+                                                                   double* partial, const int* skip) {
+    if (skip && *skip)
+        return;
+    extern __shared__ double cs[];
+    for (int i = threadIdx.x; i < 2 * nv + 2; i += blockDim.x)
+        cs[i] = coef[i];
+    __syncthreads();
+    __shared__ double red[kRedThreads / 32][1];
+    __shared__ double res[1];
+    const double* ca = cs;
+    const double* cd = cs + nv;
+    const double inv_rho = cs[2 * nv], cr = cs[2 * nv + 1];
+    double acc[1] = {0.0};
+    for (long k = 2 * ((long)blockIdx.x * blockDim.x + threadIdx.x); k < n; k += 2L * gridDim.x * blockDim.x) {
+        double2 sa = make_double2(0.0, 0.0), sd = make_double2(0.0, 0.0);
+        for (int i = 0; i < nv; i += 16) {
+            double2 v[16];
+#pragma unroll
+            for (int q = 0; q < 16; ++q)
+                v[q] = (i + q < nv) ? __ldcs(reinterpret_cast<const double2*>(V + (long)(i + q) * ld + k))
+                                    : make_double2(0.0, 0.0);
+#pragma unroll
+            for (int q = 0; q < 16; ++q)
+                if (i + q < nv) {
+                    const double a = ca[i + q], dd = cd[i + q];
+                    sa.x += a * v[q].x;
+                    sa.y += a * v[q].y;
+                    sd.x += dd * v[q].x;
+                    sd.y += dd * v[q].y;
+                }
+        }
+        const double2 uk = *reinterpret_cast<const double2*>(u + k);
+        const double2 wk = *reinterpret_cast<const double2*>(w + k);
+        *reinterpret_cast<double2*>(u + k) = make_double2((uk.x - sa.x) * inv_rho, (uk.y - sa.y) * inv_rho);
+        const double2 wn = make_double2((wk.x - cr * uk.x - sd.x) * inv_rho, (wk.y - cr * uk.y - sd.y) * inv_rho);
+        *reinterpret_cast<double2*>(w + k) = wn;
+        acc[0] += wn.x * wn.x + wn.y * wn.y;
+    }
+    block_sum_vec<1>(acc, red, res);
+    if (threadIdx.x == 0)
+        partial[blockIdx.x] = res[0];
+}
+
+int dcgs_update_parts(long n) {
+    if (n > kDots2dMax)
+        return kRedBlocks;
+    const long per = 2L * kRedThreads;
+    const long p = (n + per - 1) / per;
+    return (int)(p < 1 ? 1 : (p > kRedBlocks ? kRedBlocks : p));
+}
+
+void launch_dcgs_update2(const double* V, long ld, int nv, const double* coef, double* u, double* w, long n,
+                         double* partial, cudaStream_t st, const int* skip) {
+    note_launch();
+    dcgs_update2_kernel<<<dcgs_update_parts(n), kRedThreads, sizeof(double) * (2 * nv + 2), st>>>(
+        V, ld, nv, coef, u, w, n, partial, skip);
 }
 
 // x <- x + s * sum_i y_i V_i (solution update x += S V y, linalg.cpp:272-274).
@@ -264,7 +463,9 @@ void launch_basis_combine(const double* V, long ld, int nv, const double* y, con
 // (linalg.cpp:214-216), produced in the same pass.
 __global__ void normalize_kernel(const double* __restrict__ in, const double* __restrict__ alpha,
                                  double* __restrict__ out, const double* __restrict__ s,
-                                 double* __restrict__ z, long n) {
+                                 double* __restrict__ z, long n, const int* skip) {
+    if (skip && *skip)
+        return;
     const double a = *alpha;
     for (long k = (long)blockIdx.x * blockDim.x + threadIdx.x; k < n;
          k += (long)gridDim.x * blockDim.x) {
@@ -276,9 +477,263 @@ __global__ void normalize_kernel(const double* __restrict__ in, const double* __
 }
 
 void launch_normalize(const double* in, const double* alpha, double* out, long n,
-                      cudaStream_t st, const double* s, double* z) {
+                      cudaStream_t st, const double* s, double* z, const int* skip) {
     note_launch();
-    normalize_kernel<<<8 * 148, 256, 0, st>>>(in, alpha, out, s, z, n);
+    normalize_kernel<<<8 * 148, 256, 0, st>>>(in, alpha, out, s, z, n, skip);
+}
+
+// ---------------------------------------------------------------- Arnoldi step
+// The small dense part of one DCGS2 GMRES step (what gmres_dev's host loop
+// does between the dot pass and the update pass, see hbgpu_host.cu), so a
+// cycle runs without a host round trip per step:
+//   rho = sqrt(<u,u> - |a|^2) from the reduced dot pass;
+//   column j-1 is finalised with the re-orthogonalisation of u_j, rotated
+//   (Givens, linalg.cpp:237-258), and the residual estimate / convergence /
+//   breakdown test sets ctl[0];  unless the cycle ends, the tentative column
+//   j = (c - H_j a)/rho and the update coefficients [a | b - cr a | 1/rho | cr].
+// One CTA of 256.  H is row-major (row i contiguous), so the O(j^2) product
+// H_j a is read as (row, 32-column segment) items, each a run of independent
+// loads; warp 0 runs the Givens chain on shared-memory copies meanwhile.
+// Every sum has a fixed order (deterministic).
+constexpr int kArnThreads = 256;
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1)
+        v += __shfl_down_sync(0xffffffffu, v, o);
+    return v;  // lane 0
+}
+
+__global__ void __launch_bounds__(kArnThreads) arnoldi_step_kernel(ArnoldiDev d, int j, int last,
+                                                                   const double* __restrict__ red,
+                                                                   const double* __restrict__ d_norm,
+                                                                   double* __restrict__ coef, double bnorm,
+                                                                   double tol) {
+    if (*d.ctl)
+        return;
+    extern __shared__ double sh[];
+    const int m = d.m, ldh = m + 1;  // H row-major: H(i, l) = Hm[i * ldh + l]
+    const size_t ldr = (size_t)m + 2;  // R column-major
+    double* av = sh;                // j
+    double* bv = av + (m + 1);      // j
+    double* gcs = bv + (m + 1);     // Givens copies: cs, sn (k), column k of R (k + 2)
+    double* gsn = gcs + (m + 1);
+    double* grc = gsn + (m + 1);
+    double* ps = grc + (m + 2);     // (j + 1) x nseg partial row products
+    __shared__ double s_sc[4];      // uu, uw, aa, ab
+    __shared__ double s_rho, s_cj;
+    __shared__ int s_stop;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    // 1. dot results (reduced by reduce_partials): a | b | <u,u> | <u,w>
+    for (int i = tid; i < j; i += kArnThreads) {
+        av[i] = red[i];
+        if (!last)
+            bv[i] = red[j + i];
+    }
+    if (tid == 0) {
+        s_sc[0] = last ? red[j] : red[2 * j];
+        s_sc[1] = last ? 0.0 : red[2 * j + 1];
+    }
+    __syncthreads();
+    // 2. |a|^2 and a.b (warps 0 and 1), then rho and cj
+    if (warp < 2 && (warp == 0 || !last)) {
+        double acc = 0.0;
+        for (int i = lane; i < j; i += 32)
+            acc += av[i] * (warp == 0 ? av[i] : bv[i]);
+        acc = warp_sum(acc);
+        if (lane == 0)
+            s_sc[2 + warp] = acc;
+    }
+    __syncthreads();
+    if (tid == 0) {
+        const double rho2 = s_sc[0] - s_sc[2];
+        const double rho = rho2 > 0.0 ? sqrt(rho2) : 0.0;
+        s_rho = rho;
+        s_cj = (!last && rho > 0.0) ? (s_sc[1] - s_sc[3]) / rho : 0.0;
+        s_stop = 0;
+    }
+    __syncthreads();
+    const double rho = s_rho;
+    const int k = j - 1;
+    if (j >= 1) {
+        // 3. finalise column j-1: H[j, j-1] held |w'_{j-1}| (the norm u_j was built with)
+        const double hjj1 = *d_norm;
+        for (int i = tid; i <= j; i += kArnThreads) {
+            double h = (i < j) ? d.Hm[(size_t)i * ldh + k] + hjj1 * av[i] : hjj1 * rho;
+            d.Hm[(size_t)i * ldh + k] = h;
+            grc[i] = h;
+        }
+        for (int i = tid; i < k; i += kArnThreads) {
+            gcs[i] = d.cs[i];
+            gsn[i] = d.sn[i];
+        }
+    }
+    __syncthreads();
+    if (warp == 0) {
+        if (j >= 1 && lane == 0) {
+            // 4. Givens rotations of column k (chain in registers, operands in smem)
+            double x = grc[0];
+            for (int i = 0; i < k; ++i) {
+                const double y = grc[i + 1], c = gcs[i], sg = gsn[i];
+                grc[i] = c * x + sg * y;
+                x = -sg * x + c * y;
+            }
+            const double xk1 = grc[k + 1];
+            const double den = hypot(x, xk1);
+            const double c = den == 0.0 ? 1.0 : x / den;
+            const double sg = den == 0.0 ? 0.0 : xk1 / den;
+            d.cs[k] = c;
+            d.sn[k] = sg;
+            grc[k] = den;
+            grc[k + 1] = 0.0;
+            const double gk = d.gv[k];
+            d.gv[k + 1] = -sg * gk;
+            d.gv[k] = c * gk;
+            const int it = d.ctl[1] + 1;
+            d.ctl[1] = it;
+            d.ctl[2] = j;
+            d.ctl[3] += 1;
+            const double est = fabs(sg * gk);
+            if (it < d.hcap)
+                d.hist[it] = est / bnorm;
+            if (est / bnorm <= tol || d.Hm[(size_t)j * ldh + k] == 0.0)
+                s_stop = 1;
+        }
+    } else if (!last && rho > 0.0) {
+        // 5. tentative column j: (row i, 32-column segment) items of H_j a
+        const int nseg = (j + 31) / 32;
+        for (int it = tid - 32; it < (j + 1) * nseg; it += kArnThreads - 32) {
+            const int i = it / nseg, sg = it - i * nseg;
+            const int l0 = max(32 * sg, i - 1), l1 = min(j, 32 * sg + 32);
+            const double* hr = d.Hm + (size_t)i * ldh;
+            double acc = 0.0;
+            if (l0 < l1) {
+                double v[32];
+#pragma unroll
+                for (int q = 0; q < 32; ++q)
+                    v[q] = (l0 + q < l1) ? hr[l0 + q] : 0.0;
+#pragma unroll
+                for (int q = 0; q < 32; ++q)
+                    if (l0 + q < l1)
+                        acc += v[q] * av[l0 + q];
+            }
+            ps[it] = acc;
+        }
+    }
+    __syncthreads();
+    if (j >= 1)
+        for (int i = tid; i <= j; i += kArnThreads)
+            d.R[(size_t)k * ldr + i] = grc[i];
+    if (last)
+        return;
+    if (s_stop || !(rho > 0.0)) {  // converged, or u_j in span(Q) (breakdown)
+        if (tid == 0)
+            d.ctl[0] = 1;
+        return;
+    }
+    const int nseg = (j + 31) / 32;
+    const double cj = s_cj, cr = cj / rho;
+    for (int i = tid; i <= j; i += kArnThreads) {
+        double ha = 0.0;
+        for (int sg = 0; sg < nseg; ++sg)
+            ha += ps[i * nseg + sg];
+        d.Hm[(size_t)i * ldh + j] = ((i < j ? bv[i] : cj) - ha) / rho;
+    }
+    for (int i = tid; i < j; i += kArnThreads) {
+        coef[i] = av[i];
+        coef[j + i] = bv[i] - cr * av[i];
+    }
+    if (tid == 0) {
+        coef[2 * j] = 1.0 / rho;
+        coef[2 * j + 1] = cr;
+        if (j == 0)
+            d.gv[0] *= rho;  // V_0 renormalised by its computed norm in the update pass
+    }
+}
+
+void launch_arnoldi_step(const ArnoldiDev& d, int j, int last, const double* red, const double* d_norm,
+                         double* coef, double bnorm, double tol, cudaStream_t st) {
+    note_launch();
+    const int nseg = (j + 31) / 32;
+    const size_t smem = sizeof(double) * (5 * (size_t)d.m + 6 + (size_t)(j + 1) * (nseg > 0 ? nseg : 1));
+    arnoldi_step_kernel<<<1, kArnThreads, smem, st>>>(d, j, last, red, d_norm, coef, bnorm, tol);
+}
+
+size_t arnoldi_step_smem(int m) {
+    return sizeof(double) * (5 * (size_t)m + 6 + (size_t)(m + 1) * (size_t)((m + 31) / 32));
+}
+
+cudaError_t configure_arnoldi_smem(int m) {
+    return cudaFuncSetAttribute(arnoldi_step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)arnoldi_step_smem(m));
+}
+
+// V_{j+1} = w' / |w'| and z = s V_{j+1}, with |w'| = sqrt of the update pass's
+// nparts partials summed in fixed order by every CTA (CTA 0 stores it for the
+// next Arnoldi step): one launch instead of reduce + normalize.
+__global__ void normalize_partials_kernel(const double* __restrict__ in,
+                                          const double* __restrict__ partial, int nparts,
+                                          double* __restrict__ norm_out, double* __restrict__ out,
+                                          const double* __restrict__ s, double* __restrict__ z, long n,
+                                          const int* skip) {
+    if (skip && *skip)
+        return;
+    __shared__ double red[8];
+    __shared__ double s_a;
+    double acc = 0.0;
+    for (int q = threadIdx.x; q < nparts; q += blockDim.x)
+        acc += partial[q];
+    acc = warp_sum(acc);
+    if ((threadIdx.x & 31) == 0)
+        red[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w)
+            t += red[w];
+        s_a = sqrt(t);
+        if (blockIdx.x == 0)
+            *norm_out = s_a;
+    }
+    __syncthreads();
+    const double a = s_a;
+    for (long k = (long)blockIdx.x * blockDim.x + threadIdx.x; k < n; k += (long)gridDim.x * blockDim.x) {
+        const double v = a != 0.0 ? in[k] / a : 0.0;
+        out[k] = v;
+        z[k] = s[k] * v;
+    }
+}
+
+void launch_normalize_partials(const double* in, const double* partial, int nparts, double* norm_out,
+                               double* out, const double* s, double* z, long n, cudaStream_t st,
+                               const int* skip) {
+    note_launch();
+    const long per = 256L * 4;
+    const int blocks = (int)std::min<long>(8 * 148, (n + per - 1) / per);
+    normalize_partials_kernel<<<blocks > 0 ? blocks : 1, 256, 0, st>>>(in, partial, nparts, norm_out, out, s, z,
+                                                                       n, skip);
+}
+
+__global__ void arnoldi_init_kernel(ArnoldiDev d, double rnorm, int it, int reorth, double* red0) {
+    const size_t nhr = ((size_t)d.m + 2) * ((size_t)d.m + 1);
+    for (size_t k = (size_t)blockIdx.x * blockDim.x + threadIdx.x; k < nhr; k += (size_t)gridDim.x * blockDim.x) {
+        d.Hm[k] = 0.0;
+        d.R[k] = 0.0;
+        if (k < (size_t)d.m + 2)
+            d.gv[k] = k == 0 ? rnorm : 0.0;
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        d.ctl[0] = 0;
+        d.ctl[1] = it;
+        d.ctl[2] = 0;
+        d.ctl[3] = reorth;
+        red0[0] = rnorm;
+    }
+}
+
+void launch_arnoldi_init(const ArnoldiDev& d, double rnorm, int it, int reorth, double* red0,
+                         cudaStream_t st) {
+    note_launch();
+    arnoldi_init_kernel<<<64, 256, 0, st>>>(d, rnorm, it, reorth, red0);
 }
 
 }  // namespace hbgpu

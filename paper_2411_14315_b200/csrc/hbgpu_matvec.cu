@@ -38,6 +38,8 @@ __device__ __forceinline__ double2 ldcs2(const double2* p) { return __ldcs(p); }
 // bytes and y's 4 components 32 — loaded as 16-byte vectors (H is 0, no C part).
 template <bool SCALED, bool WITH_C, bool N1>
 __global__ void __launch_bounds__(256) lmatvec_kernel(MatvecArgs a) {
+    if (a.skip && *a.skip)
+        return;
     extern __shared__ double sh[];
     const int N = a.N;
     double* sH = sh;
@@ -152,6 +154,8 @@ __global__ void __launch_bounds__(256) lmatvec_kernel(MatvecArgs a) {
 // meshes too small to fill the GPU with (row, sample) threads alone.
 template <bool SCALED, bool WITH_C, int G>
 __global__ void __launch_bounds__(256) lmatvec_g_kernel(MatvecArgs a) {
+    if (a.skip && *a.skip)
+        return;
     extern __shared__ double sh[];
     const int N = a.N, rpc = a.rows_per_cta;
     double* sH = sh;
@@ -276,6 +280,8 @@ static void launch_lmatvec_g(const MatvecArgs& a_in, cudaStream_t st) {
 // xor-shuffle tree (deterministic).  Rows are taken in `perm` order.
 template <bool SCALED, int G>
 __global__ void __launch_bounds__(256) lmatvec_n1g_kernel(MatvecArgs a) {
+    if (a.skip && *a.skip)
+        return;
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
     const int ridx = t / G, g = t & (G - 1);
     const bool valid = ridx < a.nn;
