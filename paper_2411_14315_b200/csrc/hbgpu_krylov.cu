@@ -511,99 +511,57 @@ __global__ void __launch_bounds__(kArnThreads) arnoldi_step_kernel(ArnoldiDev d,
     if (*d.ctl)
         return;
     extern __shared__ double sh[];
-    const int m = d.m, ldh = m + 1;  // H row-major: H(i, l) = Hm[i * ldh + l]
+    const int m = d.m, ldh = m + 1;    // H row-major: H(i, l) = Hm[i * ldh + l]
     const size_t ldr = (size_t)m + 2;  // R column-major
-    double* av = sh;                // j
-    double* bv = av + (m + 1);      // j
-    double* gcs = bv + (m + 1);     // Givens copies: cs, sn (k), column k of R (k + 2)
+    double* av = sh;                   // j
+    double* bv = av + (m + 1);         // j
+    double* gcs = bv + (m + 1);        // Givens copies: cs, sn (k), column k (k + 2)
     double* gsn = gcs + (m + 1);
     double* grc = gsn + (m + 1);
-    double* ps = grc + (m + 2);     // (j + 1) x nseg partial row products
-    __shared__ double s_sc[4];      // uu, uw, aa, ab
+    double* hkc = grc + (m + 2);       // finalised column k, unrotated
+    double* ps = hkc + (m + 2);        // (j + 1) x nseg partial row products
+    __shared__ double s_sc[6];         // uu, uw, aa, ab, |w'_{j-1}|, gv[k]
     __shared__ double s_rho, s_cj;
     __shared__ int s_stop;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    // 1. dot results (reduced by reduce_partials): a | b | <u,u> | <u,w>
+    const int k = j - 1;
+    const bool tent = !last;  // the tentative column j is needed (unless rho = 0 or stop)
+    // A. every independent global read at once: dot results, column k of H,
+    //    the Givens history, |w'_{j-1}|, gv[k]
     for (int i = tid; i < j; i += kArnThreads) {
         av[i] = red[i];
         if (!last)
             bv[i] = red[j + i];
-    }
-    if (tid == 0) {
-        s_sc[0] = last ? red[j] : red[2 * j];
-        s_sc[1] = last ? 0.0 : red[2 * j + 1];
-    }
-    __syncthreads();
-    // 2. |a|^2 and a.b (warps 0 and 1), then rho and cj
-    if (warp < 2 && (warp == 0 || !last)) {
-        double acc = 0.0;
-        for (int i = lane; i < j; i += 32)
-            acc += av[i] * (warp == 0 ? av[i] : bv[i]);
-        acc = warp_sum(acc);
-        if (lane == 0)
-            s_sc[2 + warp] = acc;
-    }
-    __syncthreads();
-    if (tid == 0) {
-        const double rho2 = s_sc[0] - s_sc[2];
-        const double rho = rho2 > 0.0 ? sqrt(rho2) : 0.0;
-        s_rho = rho;
-        s_cj = (!last && rho > 0.0) ? (s_sc[1] - s_sc[3]) / rho : 0.0;
-        s_stop = 0;
-    }
-    __syncthreads();
-    const double rho = s_rho;
-    const int k = j - 1;
-    if (j >= 1) {
-        // 3. finalise column j-1: H[j, j-1] held |w'_{j-1}| (the norm u_j was built with)
-        const double hjj1 = *d_norm;
-        for (int i = tid; i <= j; i += kArnThreads) {
-            double h = (i < j) ? d.Hm[(size_t)i * ldh + k] + hjj1 * av[i] : hjj1 * rho;
-            d.Hm[(size_t)i * ldh + k] = h;
-            grc[i] = h;
-        }
-        for (int i = tid; i < k; i += kArnThreads) {
+        grc[i] = d.Hm[(size_t)i * ldh + k];
+        if (i < k) {
             gcs[i] = d.cs[i];
             gsn[i] = d.sn[i];
         }
     }
+    if (tid == 0) {
+        s_sc[0] = last ? red[j] : red[2 * j];
+        s_sc[1] = last ? 0.0 : red[2 * j + 1];
+        s_sc[4] = j >= 1 ? *d_norm : 0.0;
+        s_sc[5] = j >= 1 ? d.gv[k] : 0.0;
+        s_stop = 0;
+    }
     __syncthreads();
-    if (warp == 0) {
-        if (j >= 1 && lane == 0) {
-            // 4. Givens rotations of column k (chain in registers, operands in smem)
-            double x = grc[0];
-            for (int i = 0; i < k; ++i) {
-                const double y = grc[i + 1], c = gcs[i], sg = gsn[i];
-                grc[i] = c * x + sg * y;
-                x = -sg * x + c * y;
-            }
-            const double xk1 = grc[k + 1];
-            const double den = hypot(x, xk1);
-            const double c = den == 0.0 ? 1.0 : x / den;
-            const double sg = den == 0.0 ? 0.0 : xk1 / den;
-            d.cs[k] = c;
-            d.sn[k] = sg;
-            grc[k] = den;
-            grc[k + 1] = 0.0;
-            const double gk = d.gv[k];
-            d.gv[k + 1] = -sg * gk;
-            d.gv[k] = c * gk;
-            const int it = d.ctl[1] + 1;
-            d.ctl[1] = it;
-            d.ctl[2] = j;
-            d.ctl[3] += 1;
-            const double est = fabs(sg * gk);
-            if (it < d.hcap)
-                d.hist[it] = est / bnorm;
-            if (est / bnorm <= tol || d.Hm[(size_t)j * ldh + k] == 0.0)
-                s_stop = 1;
+    // B. |a|^2 (warp 0), a.b (warp 1); warps 2.. the part of H_j a over the
+    //    final columns l < k (row i, 32-column segment items)
+    const int nseg = (j + 31) / 32;
+    if (warp < 2) {
+        if (warp == 0 || !last) {
+            double acc = 0.0;
+            for (int i = lane; i < j; i += 32)
+                acc += av[i] * (warp == 0 ? av[i] : bv[i]);
+            acc = warp_sum(acc);
+            if (lane == 0)
+                s_sc[2 + warp] = acc;
         }
-    } else if (!last && rho > 0.0) {
-        // 5. tentative column j: (row i, 32-column segment) items of H_j a
-        const int nseg = (j + 31) / 32;
-        for (int it = tid - 32; it < (j + 1) * nseg; it += kArnThreads - 32) {
+    } else if (tent) {
+        for (int it = tid - 64; it < (j + 1) * nseg; it += kArnThreads - 64) {
             const int i = it / nseg, sg = it - i * nseg;
-            const int l0 = max(32 * sg, i - 1), l1 = min(j, 32 * sg + 32);
+            const int l0 = max(32 * sg, i - 1), l1 = min(k, 32 * sg + 32);
             const double* hr = d.Hm + (size_t)i * ldh;
             double acc = 0.0;
             if (l0 < l1) {
@@ -620,6 +578,72 @@ __global__ void __launch_bounds__(kArnThreads) arnoldi_step_kernel(ArnoldiDev d,
         }
     }
     __syncthreads();
+    if (tid == 0) {
+        const double rho2 = s_sc[0] - s_sc[2];
+        const double rho = rho2 > 0.0 ? sqrt(rho2) : 0.0;
+        s_rho = rho;
+        s_cj = (!last && rho > 0.0) ? (s_sc[1] - s_sc[3]) / rho : 0.0;
+    }
+    __syncthreads();
+    const double rho = s_rho;
+    // C. finalise column k = j-1 with the re-orthogonalisation of u_j:
+    //    H[0:j, k] += |w'_{j-1}| a,  H[j, k] = |w'_{j-1}| rho
+    if (j >= 1) {
+        const double hjj1 = s_sc[4];
+        for (int i = tid; i <= j; i += kArnThreads) {
+            const double h = i < j ? grc[i] + hjj1 * av[i] : hjj1 * rho;
+            grc[i] = h;
+            hkc[i] = h;
+            d.Hm[(size_t)i * ldh + k] = h;
+        }
+    }
+    __syncthreads();
+    if (warp == 0) {
+        if (j >= 1 && lane == 0) {
+            // D. Givens rotations of column k (chain in registers, operands in smem)
+            const bool zero_sub = grc[j] == 0.0;
+            double x = grc[0];
+#pragma unroll 4
+            for (int i = 0; i < k; ++i) {
+                const double y = grc[i + 1], c = gcs[i], sg = gsn[i];
+                grc[i] = c * x + sg * y;
+                x = -sg * x + c * y;
+            }
+            const double xk1 = grc[k + 1];
+            const double den = hypot(x, xk1);
+            const double c = den == 0.0 ? 1.0 : x / den;
+            const double sg = den == 0.0 ? 0.0 : xk1 / den;
+            d.cs[k] = c;
+            d.sn[k] = sg;
+            grc[k] = den;
+            grc[k + 1] = 0.0;
+            const double gk = s_sc[5];
+            d.gv[k + 1] = -sg * gk;
+            d.gv[k] = c * gk;
+            const int it = d.ctl[1] + 1;
+            d.ctl[1] = it;
+            d.ctl[2] = j;
+            d.ctl[3] += 1;
+            const double est = fabs(sg * gk);
+            if (it < d.hcap)
+                d.hist[it] = est / bnorm;
+            if (est / bnorm <= tol || zero_sub)
+                s_stop = 1;
+        }
+    } else if (tent && rho > 0.0) {
+        // D'. tentative column j: h_i = ((i < j ? b_i : cj) - H_j a) / rho, with
+        //     the finalised column k added to the partial products
+        const double cj = s_cj, ak = j >= 1 ? av[k] : 0.0;
+        for (int i = tid - 32; i <= j; i += kArnThreads - 32) {
+            double ha = 0.0;
+            for (int sg = 0; sg < nseg; ++sg)
+                ha += ps[i * nseg + sg];
+            if (j >= 1)
+                ha += hkc[i] * ak;
+            d.Hm[(size_t)i * ldh + j] = ((i < j ? bv[i] : cj) - ha) / rho;
+        }
+    }
+    __syncthreads();
     if (j >= 1)
         for (int i = tid; i <= j; i += kArnThreads)
             d.R[(size_t)k * ldr + i] = grc[i];
@@ -630,14 +654,7 @@ __global__ void __launch_bounds__(kArnThreads) arnoldi_step_kernel(ArnoldiDev d,
             d.ctl[0] = 1;
         return;
     }
-    const int nseg = (j + 31) / 32;
-    const double cj = s_cj, cr = cj / rho;
-    for (int i = tid; i <= j; i += kArnThreads) {
-        double ha = 0.0;
-        for (int sg = 0; sg < nseg; ++sg)
-            ha += ps[i * nseg + sg];
-        d.Hm[(size_t)i * ldh + j] = ((i < j ? bv[i] : cj) - ha) / rho;
-    }
+    const double cr = s_cj / rho;
     for (int i = tid; i < j; i += kArnThreads) {
         coef[i] = av[i];
         coef[j + i] = bv[i] - cr * av[i];
@@ -654,12 +671,12 @@ void launch_arnoldi_step(const ArnoldiDev& d, int j, int last, const double* red
                          double* coef, double bnorm, double tol, cudaStream_t st) {
     note_launch();
     const int nseg = (j + 31) / 32;
-    const size_t smem = sizeof(double) * (5 * (size_t)d.m + 6 + (size_t)(j + 1) * (nseg > 0 ? nseg : 1));
+    const size_t smem = sizeof(double) * (6 * (size_t)d.m + 8 + (size_t)(j + 1) * (nseg > 0 ? nseg : 1));
     arnoldi_step_kernel<<<1, kArnThreads, smem, st>>>(d, j, last, red, d_norm, coef, bnorm, tol);
 }
 
 size_t arnoldi_step_smem(int m) {
-    return sizeof(double) * (5 * (size_t)m + 6 + (size_t)(m + 1) * (size_t)((m + 31) / 32));
+    return sizeof(double) * (6 * (size_t)m + 8 + (size_t)(m + 1) * (size_t)((m + 31) / 32));
 }
 
 cudaError_t configure_arnoldi_smem(int m) {
