@@ -961,10 +961,7 @@ static int gmres_dev(hbgpu_ctx* c, const double* d_rhs, const double* d_inv,
                         break;
                     }
                     double* upart = c->partial.p + size_t(2 * m + 8) * kRedBlocks;
-                    if (n <= kDots2dMax)
-                        launch_dcgs_update2(V, n, j, d_coef, u, c->w.p, n, upart, st, ad.ctl);
-                    else
-                        launch_dcgs_update(V, n, j, d_coef, u, c->w.p, n, upart, st, ad.ctl);
+                    launch_dcgs_update2(V, n, j, d_coef, u, c->w.p, n, upart, st, ad.ctl);
                     launch_normalize_partials(c->w.p, upart, dcgs_update_parts(n), d_norm,
                                               V + size_t(j + 1) * size_t(n), c->scale.p, c->z.p, n, st, ad.ctl);
                     prof_pair(c, kPhGmUpdate, q3, prof_mark(c));
