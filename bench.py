@@ -370,6 +370,9 @@ def run_ours(args):
 
     d_s0 = torch.from_numpy(_cases.initial_state(prob)).cuda()
     d_x = torch.empty_like(d_s0)
+    # one-time GMRES workspace allocation (Krylov basis, Arnoldi state) outside the timing
+    ctx.jacobi_dev()
+    ctx.gmres_dev(d_r.data_ptr(), d_x.data_ptr(), hbgpu.KrylovConfig(max_iters=1))
     torch.cuda.synchronize()
     L.hbgpu_profile_enable(ctx.handle, 1)
     e0.record(stream)
@@ -593,6 +596,9 @@ def sweep_configs(args):
         mvb = spmv_bytes(ctx.nnz, nn, N)
         d_s0 = torch.from_numpy(cases.initial_state(prob)).cuda()
         d_x = torch.empty_like(d_s0)
+        # one-time GMRES workspace allocation (Krylov basis, Arnoldi state) outside the timing
+        ctx.jacobi_dev()
+        ctx.gmres_dev(r.data_ptr(), d_x.data_ptr(), hbgpu.KrylovConfig(max_iters=1))
         torch.cuda.synchronize()
         L.hbgpu_profile_enable(ctx.handle, 1)
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
