@@ -188,6 +188,41 @@ int hbgpu_solve_harmonic(hbgpu_ctx* ctx, const hbgpu_solver_cfg* cfg, double* st
                          hbgpu_solve_info* info, int capacity, int* log_iter, double* log_res,
                          double* log_rel, int* log_linear, double* log_seconds);
 
+/* ---- time-domain solver (the paper's comparison baseline) --------------- */
+
+/* TimeDirichletFn (cases.hpp:132-133): g and dg/dt (node*3+i, all nodes) at time t. */
+typedef void (*hbgpu_time_dirichlet_fn)(double t, double* g, double* gdot, void* user);
+
+typedef struct {
+    int steps_per_cycle;       /* TimeSolverConfig (time_solver.hpp:11-22): 500 */
+    int cycles;                /* 4 */
+    double rho_inf;            /* 0.2 */
+    double newton_tol_orders;  /* 3 */
+    int max_newton_iters;      /* 8 */
+    hbgpu_krylov_cfg krylov;
+    int steady;                /* drop the acceleration term, one steady solve */
+} hbgpu_time_cfg;
+
+typedef struct {
+    double cycle_change;       /* TimeSolution (time_solver.hpp:42-49) */
+    double total_seconds;
+    int total_steps;
+    int total_newton_iters;
+    double omega_hat_last;
+} hbgpu_time_result;
+
+/* solve_time (time_solver.hpp:51-54, time_solver.cpp:269-485): generalized-alpha
+ * GLS time stepping on the device (time_residual / time_tangent kernels, the
+ * N = 1 L-matvec, Jacobi and GMRES).  The context must carry the N = 1 basis
+ * (hbgpu_set_basis(ctx, 1, period)); its Neumann values are the steady outlet
+ * tractions h[0].  cycle_u / cycle_p (nullable) receive the CycleHistory of
+ * the last cycle: (steps+1) x nodes*3 and (steps+1) x nodes snapshots (steady:
+ * one snapshot).  HBGPU_ERR_DIVERGENCE / HBGPU_ERR_STAGNATION where the
+ * reference throws DivergenceError / StagnationError. */
+int hbgpu_solve_time(hbgpu_ctx* ctx, const hbgpu_time_cfg* cfg, double period,
+                     hbgpu_time_dirichlet_fn dirichlet, void* user, double* cycle_u,
+                     double* cycle_p, hbgpu_time_result* result);
+
 /* ---- measurement ------------------------------------------------------- */
 
 /* Per-phase CUDA-event timing on the context stream (reset on enable).

@@ -94,6 +94,8 @@ class _RefLib:
         self.suggest_dt = s("hbref_suggest_pseudo_dt", _d, [_vp])
         self.dense_tangent = s("hbref_dense_tangent", _i, [_vp, _vp, _vp])
         self.solve = s("hbref_solve", _i, [_vp, _d, _d, _i, _i, _i, _d, _i, _i, _vp, _vp, _i, _vp, _vp, _vp, _vp, _vp])
+        self.solve_time = s("hbref_solve_time", _i, [_vp, _d, _i, _i, _d, _d, _i, _i, _i, _d, _i, _i, _vp, _vp,
+                                                     _vp, _vp, _vp])
 
     def check(self, st):
         if st != 0:
@@ -335,6 +337,36 @@ class RefCtx:
         return dict(state=state, converged=bool(conv.value), res=res[:k], rel=rel[:k], linear=lin[:k],
                     pseudo_dt=sc[0], cfl=sc[1], assembly_seconds=sc[2], linear_seconds=sc[3],
                     total_seconds=sc[4])
+
+
+    def solve_time(self, dirichlet, period, steps=500, cycles=4, rho_inf=0.2, orders=3.0, max_newton=8,
+                   restart=200, max_iters=1000, tol=0.03, steady=False, threads=1):
+        """Reference solve_time (time_solver.cpp:269-485).  `dirichlet(t) -> (g, gdot)`
+        (node*3+i arrays).  Returns the last cycle's snapshots and the TimeSolution scalars."""
+        nn = self.n // (4 * self.N)
+        cb = time_dirichlet_callback(dirichlet, nn)
+        nsnap = 1 if steady else steps + 1
+        u = np.empty(nsnap * nn * 3)
+        p = np.empty(nsnap * nn)
+        sc = np.zeros(5)
+        self.R.check(self.R.solve_time(self.h, period, steps, cycles, rho_inf, orders, max_newton, restart,
+                                       max_iters, tol, int(steady), threads, C.cast(cb, _vp), None, _ptr(u),
+                                       _ptr(p), _ptr(sc)))
+        return dict(u=u.reshape(nsnap, nn * 3), p=p.reshape(nsnap, nn), cycle_change=sc[0],
+                    total_seconds=sc[1], omega_hat_last=sc[2], total_steps=int(sc[3]),
+                    total_newton_iters=int(sc[4]))
+
+
+TIME_DIRICHLET_FN = C.CFUNCTYPE(None, C.c_double, C.POINTER(C.c_double), C.POINTER(C.c_double), C.c_void_p)
+
+
+def time_dirichlet_callback(fn, nn):
+    """C callback (t, g*, gdot*, user) around a Python `fn(t) -> (g, gdot)`."""
+    def cb(t, g, gd, _user):
+        a, b = fn(t)
+        C.memmove(g, _f64(a).ctypes.data, nn * 3 * 8)
+        C.memmove(gd, _f64(b).ctypes.data, nn * 3 * 8)
+    return TIME_DIRICHLET_FN(cb)
 
 
 def ref_context(prob, tau_mode=0, pseudo_dt=float("inf")):

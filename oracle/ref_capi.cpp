@@ -13,6 +13,7 @@
 //   jacobi_preconditioner linalg.cpp:130-154
 //   gmres_solve         linalg.cpp:167-293
 //   solve_harmonic      hb_solver.cpp:113-221
+//   solve_time          time_solver.cpp:269-485 (the paper's time-stepping baseline)
 // plus the reference's independent test oracles (tests/oracles.cpp).
 // The product path (paper_2411_14315_b200/) never links or loads this.
 
@@ -22,6 +23,8 @@
 #include "hbflow/linalg.hpp"
 #include "hbflow/mesh.hpp"
 #include "hbflow/spectral.hpp"
+#include "hbflow/time_solver.hpp"
+#include "hbflow/cases.hpp"
 #include "oracles.hpp"
 
 #include <cmath>
@@ -493,6 +496,51 @@ int hbref_solve(void* ch, double pseudo_dt, double orders, int max_newton, int r
         out_scalars[2] = sol.assembly_seconds;
         out_scalars[3] = sol.linear_seconds;
         out_scalars[4] = sol.total_seconds;
+    });
+}
+
+// Reference time-stepping solve (time_solver.cpp:269-485) on the context's
+// mesh, fluid and boundary data (Neumann h[0] = steady outlet traction), with
+// the Dirichlet data g(t), dg/dt(t) from a C callback (TimeDirichletFn).
+// out_scalars: cycle_change, total_seconds, omega_hat_last, total_steps,
+// total_newton_iters.
+typedef void (*hbref_time_dirichlet_fn)(double t, double* g, double* gdot, void* user);
+int hbref_solve_time(void* ch, double period, int steps, int cycles, double rho_inf, double orders,
+                     int max_newton, int restart, int max_iters, double tol, int steady, int threads,
+                     hbref_time_dirichlet_fn fn, void* user, double* cycle_u, double* cycle_p,
+                     double* out_scalars) {
+    auto* c = static_cast<RefCtx*>(ch);
+    return guard([&] {
+        CaseInputs in;
+        in.def.period = period;
+        in.mesh = *c->mesh;
+        in.props = c->props;
+        in.basis = c->basis;
+        in.bcs = c->bcs;
+        in.time_dirichlet = [fn, user](double t, std::vector<double>& g, std::vector<double>& gd) {
+            fn(t, g.data(), gd.data(), user);
+        };
+        TimeSolverConfig tc;
+        tc.steps_per_cycle = steps;
+        tc.cycles = cycles;
+        tc.rho_inf = rho_inf;
+        tc.newton_tol_orders = orders;
+        tc.max_newton_iters = max_newton;
+        tc.krylov.restart = restart;
+        tc.krylov.max_iters = max_iters;
+        tc.krylov.tolerance = tol;
+        tc.steady = steady != 0;
+        tc.threads = threads;
+        const auto sol = solve_time(in, tc);
+        if (cycle_u)
+            std::memcpy(cycle_u, sol.cycle.u.data(), sol.cycle.u.size() * sizeof(double));
+        if (cycle_p)
+            std::memcpy(cycle_p, sol.cycle.p.data(), sol.cycle.p.size() * sizeof(double));
+        out_scalars[0] = sol.cycle_change;
+        out_scalars[1] = sol.total_seconds;
+        out_scalars[2] = sol.omega_hat_last;
+        out_scalars[3] = double(sol.total_steps);
+        out_scalars[4] = double(sol.total_newton_iters);
     });
 }
 

@@ -120,6 +120,25 @@ def parabolic_dirichlet(mesh: Mesh, inlet: int, q: np.ndarray) -> np.ndarray:
     return g.reshape(-1)
 
 
+def time_dirichlet(mesh: Mesh, inlet: int, Q0: float, a, b, period: float):
+    """TimeDirichletFn for the time-stepping solver (cases.hpp:132-133): the
+    ParabolicRound inlet profile of `parabolic_dirichlet` carrying
+    Q(t) = Q0 (1 + sum_k a_k cos(2 pi k t / T) + b_k sin(2 pi k t / T)), and
+    dQ/dt, evaluated analytically.  Returns fn(t) -> (g, gdot), node*3+i."""
+    shape = parabolic_dirichlet(mesh, inlet, np.ones(1))  # unit-flow profile
+    a = np.asarray(a, float)
+    b = np.asarray(b, float)
+    k = np.arange(1, len(a) + 1)
+    w = 2.0 * np.pi / period
+
+    def fn(t: float):
+        q = Q0 * (1.0 + float(np.sum(a * np.cos(w * k * t) + b * np.sin(w * k * t))))
+        dq = Q0 * float(np.sum(w * k * (-a * np.sin(w * k * t) + b * np.cos(w * k * t))))
+        return shape * q, shape * dq
+
+    return fn
+
+
 def config_problem(cfg: int, modes: int | None = None, mesh: Mesh | None = None) -> Problem:
     """BASELINE.json configs 0-3 (rho 1.06, mu 0.04, T = 1, no-slip walls,
     zero-traction outlets, parabolic pulsatile inflow).

@@ -1899,3 +1899,210 @@ int hbgpu_solve_harmonic(hbgpu_ctx* c, const hbgpu_solver_cfg* cfg, double* stat
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------- time solver
+// solve_time (time_solver.cpp:269-485) on the device.  The Newton loop of
+// each step follows newton_step (time_solver.cpp:354-455) statement by
+// statement; the state lives on the device, the host keeps the scalars
+// (residual norms, omega_hat) and calls the Dirichlet callback per step.
+namespace {
+struct TimeBufs {
+    DBuf<double> u, ud, p, nu, nud, np, ual, aal, g, gd, s4, elem, w, prev;
+    ~TimeBufs() {
+        for (DBuf<double>* b : {&u, &ud, &p, &nu, &nud, &np, &ual, &aal, &g, &gd, &s4, &elem, &w, &prev})
+            b->release();
+    }
+};
+}  // namespace
+
+// two deterministic sums (partial rows 0, 1) -> host
+static int sum2_dev(hbgpu_ctx* c, double* s0, double* s1) {
+    launch_reduce_partials(c->partial.p, 2, c->red.p, 0, c->stream);
+    TRY(check_launch(c));
+    CK(c, cudaMemcpyAsync(c->h_red, c->red.p, 2 * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    CK(c, cudaStreamSynchronize(c->stream));
+    *s0 = c->h_red[0];
+    *s1 = c->h_red[1];
+    return HBGPU_OK;
+}
+
+extern "C" int hbgpu_solve_time(hbgpu_ctx* c, const hbgpu_time_cfg* cfg, double period,
+                                hbgpu_time_dirichlet_fn dirichlet, void* user, double* cycle_u,
+                                double* cycle_p, hbgpu_time_result* result) {
+    if (!c || !cfg || !dirichlet)
+        return c ? fail(c, HBGPU_ERR_INVALID, "solve_time: null config or Dirichlet callback") : HBGPU_ERR_INVALID;
+    if (c->N != 1)
+        return fail(c, HBGPU_ERR_INVALID, "solve_time needs the N = 1 basis (hbgpu_set_basis(ctx, 1, period))");
+    if (cfg->steps_per_cycle <= 0 || cfg->cycles <= 0 || !(period > 0.0))
+        return fail(c, HBGPU_ERR_INVALID, "solve_time: steps_per_cycle, cycles and period must be positive");
+    Timer total;
+    cudaStream_t st = c->stream;
+    const int nn = c->nn;
+    const long n3 = 3L * nn;
+    const bool steady = cfg->steady != 0;
+    const double dt = period / double(cfg->steps_per_cycle);
+    const double am = steady ? 0.0 : 0.5 * (3.0 - cfg->rho_inf) / (1.0 + cfg->rho_inf);
+    const double af = steady ? 1.0 : 1.0 / (1.0 + cfg->rho_inf);
+    const double gamma = steady ? 1.0 : 0.5 + am - af;
+    hbgpu_time_result res{};
+    TimeBufs tb;
+    for (DBuf<double>* b : {&tb.u, &tb.ud, &tb.nu, &tb.nud, &tb.ual, &tb.aal, &tb.g, &tb.gd})
+        CK(c, b->alloc(size_t(n3)));
+    for (DBuf<double>* b : {&tb.p, &tb.np, &tb.w})
+        CK(c, b->alloc(size_t(nn)));
+    CK(c, tb.s4.alloc(size_t(nn) * 4));
+    CK(c, tb.elem.alloc(size_t(c->ne) * 16));
+    const int steps = cfg->steps_per_cycle;
+    if (!steady && cfg->cycles > 1)
+        CK(c, tb.prev.alloc(size_t(steps) * size_t(n3)));
+    launch_nodal_volumes(c->geom.p, c->inc_ptr.p, c->inc_rec.p, nn, tb.w.p, st);
+
+    // initial fields (time_solver.cpp:297-308): rest, outlet pressure level,
+    // Dirichlet g(0), gdot(0)
+    double wsum = 0.0, acc = 0.0;
+    for (size_t k = 0; k < c->bc_patch.size(); ++k) {
+        const double area = c->patches[size_t(c->bc_patch[k])].area;
+        acc += area * (-c->h_h[k]);
+        wsum += area;
+    }
+    const double p0 = wsum > 0.0 ? acc / wsum : 0.0;
+    std::vector<double> hg(static_cast<size_t>(n3)), hgd(static_cast<size_t>(n3)), hu(static_cast<size_t>(n3), 0.0),
+        hud(static_cast<size_t>(n3), 0.0), hp(static_cast<size_t>(nn), p0);
+    dirichlet(0.0, hg.data(), hgd.data(), user);
+    for (int a = 0; a < nn; ++a)
+        if (c->dir_h[size_t(a)])
+            for (int i = 0; i < 3; ++i) {
+                hu[size_t(3 * a + i)] = hg[size_t(3 * a + i)];
+                hud[size_t(3 * a + i)] = hgd[size_t(3 * a + i)];
+            }
+    CK(c, cudaMemcpy(tb.u.p, hu.data(), sizeof(double) * size_t(n3), cudaMemcpyHostToDevice));
+    CK(c, cudaMemcpy(tb.ud.p, hud.data(), sizeof(double) * size_t(n3), cudaMemcpyHostToDevice));
+    CK(c, cudaMemcpy(tb.p.p, hp.data(), sizeof(double) * size_t(nn), cudaMemcpyHostToDevice));
+    if (c->partial.n < size_t(4) * kRedBlocks)
+        CK(c, c->partial.alloc(size_t(kRedBlocks) * 1024));
+
+    BoundaryArgs bargs = boundary_args(c, tb.s4.p, c->r.p);
+    double omega_hat = 0.0;
+    // one Newton-solved step to t_new (time_solver.cpp:354-455)
+    auto newton_step = [&](double t_new, int step_index) -> int {
+        dirichlet(t_new, hg.data(), hgd.data(), user);
+        CK(c, cudaMemcpyAsync(tb.g.p, hg.data(), sizeof(double) * size_t(n3), cudaMemcpyHostToDevice, st));
+        CK(c, cudaMemcpyAsync(tb.gd.p, hgd.data(), sizeof(double) * size_t(n3), cudaMemcpyHostToDevice, st));
+        launch_time_predict(tb.u.p, tb.ud.p, tb.p.p, tb.g.p, tb.gd.p, c->dir.p, nn, steady ? 1 : 0, gamma, dt,
+                            tb.nu.p, tb.nud.p, tb.np.p, st);
+        double r0 = -1.0;
+        const std::string where = " at step " + std::to_string(step_index);
+        for (int k = 0; k <= cfg->max_newton_iters; ++k) {
+            const double* eu = steady ? tb.nu.p : tb.ual.p;
+            const double* ea = steady ? tb.nud.p : tb.aal.p;
+            if (!steady) {
+                launch_time_alpha(tb.u.p, tb.ud.p, tb.nu.p, tb.nud.p, nn, af, am, tb.ual.p, tb.aal.p, st);
+                // acceleration scale of the current iterate
+                launch_time_wnorm(tb.w.p, tb.ual.p, tb.aal.p, nn, c->partial.p, st);
+                double su = 0.0, sa = 0.0;
+                TRY(sum2_dev(c, &su, &sa));
+                const double un = std::sqrt(su);
+                omega_hat = un > 1e-14 ? std::sqrt(sa) / un : 0.0;
+            } else {
+                omega_hat = 0.0;
+            }
+            launch_time_residual(c->geom.p, c->conn.p, c->ne, c->inc_ptr.p, c->inc_rec.p, c->dir.p, nn, eu, ea,
+                                 tb.np.p, c->rho, c->mu, omega_hat, tb.elem.p, c->r.p, st);
+            if (c->nbnodes > 0) {
+                launch_time_pack(eu, tb.np.p, nn, tb.s4.p, st);
+                launch_boundary(bargs, st);
+            }
+            TRY(check_launch(c));
+            double rn = 0.0;
+            TRY(dot_dev(c, c->r.p, c->r.p, 4L * nn, &rn, true));
+            if (!std::isfinite(rn))
+                return fail(c, HBGPU_ERR_DIVERGENCE, "time solver diverged" + where);
+            if (r0 < 0.0)
+                r0 = rn;
+            if (rn <= 1e-30 || rn <= r0 * std::pow(10.0, -cfg->newton_tol_orders))
+                break;
+            if (r0 > 0.0 && rn / r0 > 1e4)
+                return fail(c, HBGPU_ERR_DIVERGENCE, "time solver diverged" + where);
+            if (k == cfg->max_newton_iters)
+                break;
+            launch_time_tangent(c->geom.p, c->row_ptr.p, c->col_idx.p, c->inc_ptr.p, c->inc_rec.p, c->dir.p, nn,
+                                eu, c->rho, c->mu, omega_hat, am, steady ? 1.0 : af * gamma * dt, c->pvals.p, st);
+            TRY(check_launch(c));
+            c->p_valid = true;
+            c->inv_valid = false;
+            TRY(jacobi_dev(c, nullptr));
+            hbgpu_krylov_result kr{};
+            TRY(gmres_dev(c, c->r.p, c->inv.p, &cfg->krylov, c->x.p, &kr, nullptr, 0));
+            if (kr.status == 2)
+                return fail(c, HBGPU_ERR_STAGNATION, "time solver GMRES stagnated" + where);
+            res.total_newton_iters += 1;
+            launch_time_update(c->x.p, c->dir.p, nn, steady ? 1 : 0, gamma * dt, tb.nu.p, tb.nud.p, tb.np.p, st);
+            TRY(check_launch(c));
+        }
+        res.omega_hat_last = omega_hat;
+        std::swap(tb.u, tb.nu);
+        std::swap(tb.ud, tb.nud);
+        std::swap(tb.p, tb.np);
+        return HBGPU_OK;
+    };
+    auto finish = [&](int code) {
+        res.total_seconds = total.seconds();
+        if (result)
+            *result = res;
+        return code;
+    };
+
+    if (steady) {
+        const int s = newton_step(0.0, 0);
+        if (s != HBGPU_OK)
+            return finish(s);
+        if (cycle_u)
+            CK(c, cudaMemcpy(cycle_u, tb.u.p, sizeof(double) * size_t(n3), cudaMemcpyDeviceToHost));
+        if (cycle_p)
+            CK(c, cudaMemcpy(cycle_p, tb.p.p, sizeof(double) * size_t(nn), cudaMemcpyDeviceToHost));
+        res.total_steps = 1;
+        return finish(HBGPU_OK);
+    }
+    double diff2 = 0.0, norm2acc = 0.0;
+    for (int cycle = 0; cycle < cfg->cycles; ++cycle) {
+        const bool last = cycle == cfg->cycles - 1;
+        if (last) {
+            if (cycle_u)
+                CK(c, cudaMemcpy(cycle_u, tb.u.p, sizeof(double) * size_t(n3), cudaMemcpyDeviceToHost));
+            if (cycle_p)
+                CK(c, cudaMemcpy(cycle_p, tb.p.p, sizeof(double) * size_t(nn), cudaMemcpyDeviceToHost));
+        }
+        if (cycle == cfg->cycles - 1 || cycle == cfg->cycles - 2) {
+            diff2 = 0.0;
+            norm2acc = 0.0;
+        }
+        for (int j = 0; j < steps; ++j) {
+            const double t_new = (double(cycle) * steps + j + 1) * dt;
+            const int s = newton_step(t_new, cycle * steps + j);
+            if (s != HBGPU_OK)
+                return finish(s);
+            res.total_steps += 1;
+            if (tb.prev.p) {
+                launch_time_cycle(tb.u.p, tb.prev.p + size_t(j) * size_t(n3), n3, cycle > 0 ? 1 : 0, c->partial.p,
+                                  st);
+                if (cycle > 0) {
+                    double d2 = 0.0, u2 = 0.0;
+                    TRY(sum2_dev(c, &d2, &u2));
+                    diff2 += d2;
+                    norm2acc += u2;
+                }
+            }
+            if (last) {
+                if (cycle_u)
+                    CK(c, cudaMemcpy(cycle_u + size_t(j + 1) * size_t(n3), tb.u.p, sizeof(double) * size_t(n3),
+                                     cudaMemcpyDeviceToHost));
+                if (cycle_p)
+                    CK(c, cudaMemcpy(cycle_p + size_t(j + 1) * size_t(nn), tb.p.p, sizeof(double) * size_t(nn),
+                                     cudaMemcpyDeviceToHost));
+            }
+        }
+        if (cycle > 0)
+            res.cycle_change = norm2acc > 0.0 ? std::sqrt(diff2 / norm2acc) : 0.0;
+    }
+    return finish(HBGPU_OK);
+}

@@ -278,6 +278,27 @@ void launch_fill_pressure(double p0, int nn, int N, double* state, cudaStream_t 
 void launch_newton_update(const double* dx, const uint8_t* dir, int nn, int N, double* state,
                           cudaStream_t st);
 
+// time-domain operators (hbgpu_time.cu; reference src/time_solver.cpp)
+void launch_time_residual(const double* geom, const int4* conn, int ne, const int* inc_ptr, const int4* rec,
+                          const uint8_t* dir, int nn, const double* u, const double* udot, const double* p,
+                          double rho, double mu, double omega_hat, double* elem, double* r, cudaStream_t st);
+void launch_time_tangent(const double* geom, const int* row_ptr, const int* col_idx, const int* inc_ptr,
+                         const int4* rec, const uint8_t* dir, int nn, const double* u, double rho, double mu,
+                         double omega_hat, double am, double fg, double* vals, cudaStream_t st);
+void launch_time_predict(const double* u, const double* ud, const double* p, const double* g, const double* gd,
+                         const uint8_t* dir, int nn, int steady, double gamma, double dt, double* nu_, double* nud,
+                         double* np, cudaStream_t st);
+void launch_time_alpha(const double* u, const double* ud, const double* nu_, const double* nud, int nn,
+                       double af, double am, double* ual, double* aal, cudaStream_t st);
+void launch_time_update(const double* x, const uint8_t* dir, int nn, int steady, double gdt, double* nu_,
+                        double* nud, double* np, cudaStream_t st);
+void launch_time_pack(const double* u, const double* p, int nn, double* s4, cudaStream_t st);
+void launch_time_wnorm(const double* w, const double* f0, const double* f1, int nn, double* partial,
+                       cudaStream_t st);
+void launch_time_cycle(const double* f, double* buf, long n3, int accumulate, double* partial, cudaStream_t st);
+void launch_nodal_volumes(const double* geom, const int* inc_ptr, const int4* rec, int nn, double* w,
+                          cudaStream_t st);
+
 // vectors (length n), deterministic reductions
 void launch_sqrt_abs(const double* in, double* out, long n, cudaStream_t st);
 void launch_mul(const double* a, const double* b, double* out, long n, cudaStream_t st);

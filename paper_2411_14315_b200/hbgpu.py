@@ -119,6 +119,32 @@ class _SolveInfo(C.Structure):
     ]
 
 
+class _TimeCfg(C.Structure):
+    _fields_ = [
+        ("steps_per_cycle", C.c_int),
+        ("cycles", C.c_int),
+        ("rho_inf", C.c_double),
+        ("newton_tol_orders", C.c_double),
+        ("max_newton_iters", C.c_int),
+        ("krylov", _KrylovCfg),
+        ("steady", C.c_int),
+    ]
+
+
+class _TimeResult(C.Structure):
+    _fields_ = [
+        ("cycle_change", C.c_double),
+        ("total_seconds", C.c_double),
+        ("total_steps", C.c_int),
+        ("total_newton_iters", C.c_int),
+        ("omega_hat_last", C.c_double),
+    ]
+
+
+# TimeDirichletFn (cases.hpp:132-133): (t, g*, gdot*, user)
+TimeDirichletFn = C.CFUNCTYPE(None, C.c_double, C.POINTER(C.c_double), C.POINTER(C.c_double), C.c_void_p)
+
+
 def _sig(name, res, args):
     f = getattr(_lib, name)
     f.restype = res
@@ -156,6 +182,8 @@ _bsr_matvec_dev = _sig("hbgpu_bsr_matvec_dev", C.c_int, [_vp, _vp, _vp])
 _jacobi_dev = _sig("hbgpu_jacobi_dev", C.c_int, [_vp, _ip])
 _gmres_dev = _sig("hbgpu_gmres_dev", C.c_int, [_vp, _vp, C.POINTER(_KrylovCfg), _vp, C.POINTER(_KrylovRes), _vp, C.c_int])
 _pvals_dev = _sig("hbgpu_pvals_dev", _vp, [_vp])
+_solve_time = _sig("hbgpu_solve_time", C.c_int,
+                   [_vp, C.POINTER(_TimeCfg), C.c_double, TimeDirichletFn, _vp, _vp, _vp, C.POINTER(_TimeResult)])
 _solve = _sig(
     "hbgpu_solve_harmonic",
     C.c_int,
@@ -222,6 +250,34 @@ class ConvergenceLog:
                 % (self.iters[k], self.res[k], self.res_rel[k], self.linear_iters[k], self.seconds[k])
             )
         return "\n".join(lines) + "\n"
+
+
+@dataclass
+class TimeSolverConfig:
+    """time_solver.hpp:11-22"""
+
+    steps_per_cycle: int = 500
+    cycles: int = 4
+    rho_inf: float = 0.2
+    newton_tol_orders: float = 3.0
+    max_newton_iters: int = 8
+    krylov: KrylovConfig = field(default_factory=KrylovConfig)
+    steady: bool = False
+
+
+@dataclass
+class TimeSolution:
+    """time_solver.hpp:24-49: the last cycle's snapshots u[(steps+1), nodes*3],
+    p[(steps+1), nodes] (one snapshot when steady) and the run scalars."""
+
+    u: np.ndarray
+    p: np.ndarray
+    period: float
+    cycle_change: float
+    total_seconds: float
+    total_steps: int
+    total_newton_iters: int
+    omega_hat_last: float
 
 
 @dataclass
@@ -322,6 +378,7 @@ class GpuContext:
     def set_basis(self, modes: int, period: float = 1.0):
         self._check(_set_basis(self._h, int(modes), float(period)))
         self.M, self.N = int(modes), 2 * int(modes) - 1
+        self.period = float(period)
 
     def set_fluid(self, rho: float = 1.06, mu: float = 0.04):
         self._check(_set_fluid(self._h, float(rho), float(mu)))
@@ -449,6 +506,32 @@ class GpuContext:
 
     def pvals_dev(self) -> int:
         return _pvals_dev(self._h)
+
+    # ------------------------------------------------------------ time solver
+    def solve_time(self, dirichlet, cfg: TimeSolverConfig | None = None, period: float | None = None) -> TimeSolution:
+        """solve_time (time_solver.cpp:269-485) on the device.  The context must
+        hold the N = 1 basis (set_basis(1, period)) and steady Neumann data;
+        `dirichlet(t) -> (g, gdot)` returns node*3+i arrays (TimeDirichletFn)."""
+        cfg = cfg or TimeSolverConfig()
+        period = float(self.period if period is None else period)
+        nn = self.mesh.num_nodes
+
+        def cb(t, g, gd, _user):
+            a, b = dirichlet(t)
+            C.memmove(g, _f64(a).ctypes.data, nn * 3 * 8)
+            C.memmove(gd, _f64(b).ctypes.data, nn * 3 * 8)
+
+        fn = TimeDirichletFn(cb)
+        tc = _TimeCfg(int(cfg.steps_per_cycle), int(cfg.cycles), float(cfg.rho_inf), float(cfg.newton_tol_orders),
+                      int(cfg.max_newton_iters),
+                      _KrylovCfg(cfg.krylov.restart, cfg.krylov.max_iters, cfg.krylov.tolerance), int(bool(cfg.steady)))
+        nsnap = 1 if cfg.steady else cfg.steps_per_cycle + 1
+        u = np.empty(nsnap * nn * 3)
+        p = np.empty(nsnap * nn)
+        res = _TimeResult()
+        self._check(_solve_time(self._h, C.byref(tc), period, fn, None, _ptr(u), _ptr(p), C.byref(res)))
+        return TimeSolution(u.reshape(nsnap, nn * 3), p.reshape(nsnap, nn), period, res.cycle_change,
+                            res.total_seconds, res.total_steps, res.total_newton_iters, res.omega_hat_last)
 
     # ------------------------------------------------------------ Newton
     def solve_harmonic(self, cfg: SolverConfig | None = None) -> HbSolution:
