@@ -676,6 +676,58 @@ def solve_config0(cpu_reference=False):
     return out
 
 
+def time_solve(args):
+    """The paper's comparison baseline: generalized-alpha
+    time stepping (time_solver.cpp:269-485) of config 0 on the GPU with the
+    reference defaults (500 steps per cycle, 4 cycles, rho_inf 0.2, 3 orders,
+    8 Newton iterations, GMRES 0.03 / restart 200), next to the harmonic-balance
+    converged solve of the same pipe.  The compiled reference runs a bounded
+    sample: the first `--time-cpu-steps` steps of the same run (same dt, same
+    inflow), and the GPU runs the same sample for a per-step ratio."""
+    import time as _time
+
+    from oracle import bindings as ob
+    from paper_2411_14315_b200 import cases, hbgpu
+
+    prob = cases.config_problem(0)
+    mesh = prob.mesh
+    Q0, a, b = cases.inflow_coefficients(0)
+    fn = cases.time_dirichlet(mesh, mesh.patch_index("inlet"), Q0, a, b, 1.0)
+    neu = [(k, np.array([0.0])) for k, p in enumerate(mesh.patches) if p.kind == 1]
+    ctx = hbgpu.GpuContext(mesh)
+    ctx.set_basis(1, 1.0)
+    ctx.set_fluid(prob.rho, prob.mu)
+    ctx.set_bcs(None, neu, prob.backflow_beta)
+    full = hbgpu.TimeSolverConfig()
+    ns = args.time_cpu_steps
+    dt = 1.0 / full.steps_per_cycle
+    sample = hbgpu.TimeSolverConfig(steps_per_cycle=ns, cycles=1)
+    ctx.solve_time(fn, sample, period=ns * dt)  # warm-up (allocations)
+    t0 = _time.perf_counter()
+    gs = ctx.solve_time(fn, sample, period=ns * dt)
+    t_gs = _time.perf_counter() - t0
+    t0 = _time.perf_counter()
+    g = ctx.solve_time(fn, full)
+    t_full = _time.perf_counter() - t0
+    out = {"sweep": "time_solver", "workload": "config 0 pipe (36000 tets, 7381 nodes), generalized-alpha "
+           "time stepping with the reference defaults (500 steps/cycle, 4 cycles)",
+           "gpu": {"seconds": t_full, "steps": g.total_steps, "newton_iters": g.total_newton_iters,
+                   "ms_per_step": 1e3 * t_full / max(g.total_steps, 1), "cycle_change": g.cycle_change},
+           "sample": {"steps": ns, "gpu_seconds": t_gs, "gpu_newton_iters": gs.total_newton_iters}}
+    if not args.no_cpu_baseline and os.path.exists(ob.REF_SO):
+        rm = ob.RefMesh.from_mesh(mesh)
+        ref = ob.RefCtx(rm, 1, ns * dt, prob.rho, prob.mu)
+        ref.set_bcs(None, neu, prob.backflow_beta)
+        t0 = _time.perf_counter()
+        r = ref.solve_time(fn, ns * dt, steps=ns, cycles=1)
+        t_cpu = _time.perf_counter() - t0
+        rel = float(np.linalg.norm(gs.u[-1] - r["u"][-1]) / np.linalg.norm(r["u"][-1]))
+        out["sample"].update({"cpu_seconds": t_cpu, "cpu_newton_iters": r["total_newton_iters"], "cores": 1,
+                              "kind": "reference", "rel_l2_u_last_step": rel,
+                              "cpu_extrapolated_full_seconds": t_cpu / ns * full.steps_per_cycle * full.cycles})
+    print(json.dumps(out), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -689,7 +741,12 @@ def main():
     ap.add_argument("--sweep4", action="store_true", help="config-4 operator sweep (separate run)")
     ap.add_argument("--sweep-points", type=int, default=700_000)
     ap.add_argument("--configs", default=None, help="e.g. 0,1,2,3: per-config operator/Newton sweep")
+    ap.add_argument("--time-solve", action="store_true", help="time-stepping solver on config 0 (separate run)")
+    ap.add_argument("--time-cpu-steps", type=int, default=10)
     args = ap.parse_args()
+    if args.time_solve:
+        time_solve(args)
+        return
     if args.sweep4:
         sweep_config4(args)
         return

@@ -211,6 +211,15 @@ typedef struct {
     double omega_hat_last;
 } hbgpu_time_result;
 
+/* time_residual (time_solver.cpp:58-166) at (u, udot, p) = (node*3+i, node*3+i,
+ * node), host buffers; r: node*4+c.  N = 1 context. */
+int hbgpu_time_residual(hbgpu_ctx* ctx, const double* u, const double* udot, const double* p,
+                        double omega_hat, double* r);
+/* time_tangent (time_solver.cpp:172-254) into the context's N = 1 P (kept on
+ * the device for hbgpu_matvec / hbgpu_gmres); pvals (nullable) receives it. */
+int hbgpu_time_tangent(hbgpu_ctx* ctx, const double* u, double omega_hat, double am, double fg,
+                       double* pvals);
+
 /* solve_time (time_solver.hpp:51-54, time_solver.cpp:269-485): generalized-alpha
  * GLS time stepping on the device (time_residual / time_tangent kernels, the
  * N = 1 L-matvec, Jacobi and GMRES).  The context must carry the N = 1 basis

@@ -416,6 +416,8 @@ class Restated:
         _sig(L, "hbo_tangent_matvec", None, [_vp, _vp, _vp, _vp, _vp, _vp, _vp])
         _sig(L, "hbo_jacobi", _i, [_i, _i, _vp, _vp, _vp, _vp])
         _sig(L, "hbo_gmres_tangent", None, [_vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp])
+        _sig(L, "hbo_time_residual", None, [_vp, _vp, _vp, _vp, _d, _vp])
+        _sig(L, "hbo_time_tangent", None, [_vp, _vp, _vp, _vp, _d, _d, _d, _vp])
         m = prob.mesh
         self.prob = prob
         self.N = prob.N
@@ -462,6 +464,21 @@ class Restated:
         v = np.empty(len(self.col_idx) * 8 * self.N)
         if self.L.hbo_tangent(C.byref(self.p), _ptr(self.row_ptr), _ptr(self.col_idx), _ptr(s), _ptr(v)):
             raise ArithmeticError("singular stabilization parameter")
+        return v
+
+    def time_residual(self, u, udot, p, omega_hat):
+        """time_solver.cpp:58-166 (u, udot node*3+i, p node) -> r node*4+c"""
+        u, ud, pp = _f64(u), _f64(udot), _f64(p)
+        r = np.empty(self.nn * 4)
+        self.L.hbo_time_residual(C.byref(self.p), _ptr(u), _ptr(ud), _ptr(pp), float(omega_hat), _ptr(r))
+        return r
+
+    def time_tangent(self, u, omega_hat, am, fg):
+        """time_solver.cpp:172-254 -> N = 1 BSR values (blk*8+slot)"""
+        u = _f64(u)
+        v = np.empty(len(self.col_idx) * 8)
+        self.L.hbo_time_tangent(C.byref(self.p), _ptr(self.row_ptr), _ptr(self.col_idx), _ptr(u),
+                                float(omega_hat), float(am), float(fg), _ptr(v))
         return v
 
     def mass(self):

@@ -695,3 +695,171 @@ void hbo_gmres_tangent(const hbo_problem* p, const int* row_ptr, const int* col_
     tangent_user u = {p, row_ptr, col_idx, vals, mass};
     hbo_gmres(tangent_apply, &u, (long)p->nn * 4 * p->N, rhs, inv_diag, cfg, x, res, history);
 }
+
+/* ---------------------------------------------------------------- time solver */
+
+/* time_solver.cpp:34-43: (omega_hat^2 + u.xi.u + 3 nu^2 xi:xi)^(-1/2), full 3x3 xi */
+static double tau_hat_of(const double* g, const double u[3], double nu, double omega_hat) {
+    double conv = 0.0, xx = 0.0;
+    for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j) {
+            const double x = g[13 + 3 * i + j];
+            conv += u[i] * x * u[j];
+            xx += x * x;
+        }
+    return 1.0 / sqrt(omega_hat * omega_hat + conv + 3.0 * nu * nu * xx);
+}
+
+void hbo_time_residual(const hbo_problem* p, const double* u, const double* udot, const double* pres,
+                       double omega_hat, double* r) {
+    const double rho = p->rho, mu = p->mu, nu = mu / rho;
+    memset(r, 0, sizeof(double) * (size_t)p->nn * 4);
+    for (int e = 0; e < p->ne; ++e) {
+        const int* cn = p->conn + 4 * e;
+        const double* g = p->geom + 22 * (size_t)e;
+        const double w = g[12] / 4.0;
+        double gu[3][3] = {{0}}, gp[3] = {0};
+        for (int a = 0; a < 4; ++a)
+            for (int i = 0; i < 3; ++i) {
+                for (int j = 0; j < 3; ++j)
+                    gu[i][j] += GN(g, a, j) * u[3 * (size_t)cn[a] + i];
+                gp[i] += GN(g, a, i) * pres[cn[a]];
+            }
+        const double divu = gu[0][0] + gu[1][1] + gu[2][2];
+        for (int q = 0; q < 4; ++q) {
+            double uq[3] = {0, 0, 0}, aq[3] = {0, 0, 0}, pq = 0.0;
+            for (int a = 0; a < 4; ++a) {
+                const double sa = tet_shape(q, a);
+                for (int i = 0; i < 3; ++i) {
+                    uq[i] += sa * u[3 * (size_t)cn[a] + i];
+                    aq[i] += sa * udot[3 * (size_t)cn[a] + i];
+                }
+                pq += sa * pres[cn[a]];
+            }
+            const double th = tau_hat_of(g, uq, nu, omega_hat);
+            double lq[3];
+            for (int i = 0; i < 3; ++i) {
+                double cv = 0.0;
+                for (int j = 0; j < 3; ++j)
+                    cv += uq[j] * gu[i][j];
+                lq[i] = rho * aq[i] + rho * cv + gp[i];
+            }
+            for (int a = 0; a < 4; ++a) {
+                const double sa = tet_shape(q, a);
+                double adv = 0.0;
+                for (int j = 0; j < 3; ++j)
+                    adv += uq[j] * GN(g, a, j);
+                for (int i = 0; i < 3; ++i) {
+                    double cv = 0.0, visc = 0.0;
+                    for (int j = 0; j < 3; ++j) {
+                        cv += uq[j] * gu[i][j];
+                        visc += GN(g, a, j) * gu[i][j];
+                    }
+                    r[4 * (size_t)cn[a] + i] +=
+                        w * (rho * sa * (aq[i] + cv) - GN(g, a, i) * pq + mu * visc + adv * th * lq[i]);
+                }
+                double pspg = 0.0;
+                for (int i = 0; i < 3; ++i)
+                    pspg += GN(g, a, i) * th * lq[i];
+                r[4 * (size_t)cn[a] + 3] += w * (sa * divu + pspg / rho);
+            }
+        }
+    }
+    /* Neumann traction (steady h[0]) and backflow (time_solver.cpp:130-160) */
+    for (int f = 0; f < p->nfac; ++f) {
+        const int* fac = p->fac + 3 * f;
+        const double* nv = p->fnormal + 3 * f;
+        const double h = p->h[(size_t)p->fbc[f] * p->N];
+        const double w = p->farea[f] / 3.0;
+        for (int q = 0; q < 3; ++q) {
+            double uq[3] = {0, 0, 0};
+            for (int a = 0; a < 3; ++a)
+                for (int i = 0; i < 3; ++i)
+                    uq[i] += tri_shape(q, a) * u[3 * (size_t)fac[a] + i];
+            const double un = uq[0] * nv[0] + uq[1] * nv[1] + uq[2] * nv[2];
+            const double neg = un < 0.0 ? un : 0.0;
+            for (int a = 0; a < 3; ++a)
+                for (int i = 0; i < 3; ++i)
+                    r[4 * (size_t)fac[a] + i] +=
+                        w * tri_shape(q, a) * (-h * nv[i] - 0.5 * rho * p->beta * neg * uq[i]);
+        }
+    }
+    for (int A = 0; A < p->nn; ++A)
+        if (p->dirichlet[A])
+            for (int i = 0; i < 3; ++i)
+                r[4 * (size_t)A + i] = 0.0;
+}
+
+void hbo_time_tangent(const hbo_problem* p, const int* row_ptr, const int* col_idx, const double* u,
+                      double omega_hat, double am, double fg, double* vals) {
+    const double rho = p->rho, mu = p->mu, nu = mu / rho;
+    memset(vals, 0, sizeof(double) * (size_t)row_ptr[p->nn] * 8);
+    for (int e = 0; e < p->ne; ++e) {
+        const int* cn = p->conn + 4 * e;
+        const double* g = p->geom + 22 * (size_t)e;
+        const double V = g[12], w = V / 4.0;
+        double K[16] = {0}, G[16][3] = {{0}}, D[16][3] = {{0}}, L[16] = {0};
+        for (int a = 0; a < 4; ++a)
+            for (int b = 0; b < 4; ++b) {
+                double gg = 0.0;
+                for (int j = 0; j < 3; ++j)
+                    gg += GN(g, a, j) * GN(g, b, j);
+                const double m = a == b ? V / 10.0 : V / 20.0; /* element_mass(g, 1), assembly.cpp:58-66 */
+                K[a * 4 + b] += am * rho * m + fg * mu * V * gg;
+                L[a * 4 + b] = 0.0;
+                for (int i = 0; i < 3; ++i) {
+                    G[a * 4 + b][i] += -GN(g, a, i) * V / 4.0;
+                    D[a * 4 + b][i] += fg * GN(g, b, i) * V / 4.0;
+                }
+            }
+        for (int q = 0; q < 4; ++q) {
+            double uq[3] = {0, 0, 0};
+            for (int a = 0; a < 4; ++a)
+                for (int i = 0; i < 3; ++i)
+                    uq[i] += tet_shape(q, a) * u[3 * (size_t)cn[a] + i];
+            const double th = tau_hat_of(g, uq, nu, omega_hat);
+            double adv[4];
+            for (int a = 0; a < 4; ++a) {
+                adv[a] = 0.0;
+                for (int j = 0; j < 3; ++j)
+                    adv[a] += uq[j] * GN(g, a, j);
+            }
+            for (int a = 0; a < 4; ++a) {
+                const double sa = tet_shape(q, a);
+                for (int b = 0; b < 4; ++b) {
+                    const double sb = tet_shape(q, b);
+                    K[a * 4 + b] += w * (fg * rho * (sa * adv[b] + adv[a] * th * adv[b]) + am * rho * adv[a] * th * sb);
+                    double gg = 0.0;
+                    for (int j = 0; j < 3; ++j)
+                        gg += GN(g, a, j) * GN(g, b, j);
+                    L[a * 4 + b] += w * gg * th / rho;
+                    for (int i = 0; i < 3; ++i) {
+                        G[a * 4 + b][i] += w * adv[a] * th * GN(g, b, i);
+                        D[a * 4 + b][i] += w * GN(g, a, i) * th * (am * sb + fg * adv[b]);
+                    }
+                }
+            }
+        }
+        for (int a = 0; a < 4; ++a) {
+            const int A = cn[a];
+            const int afix = p->dirichlet[A] != 0;
+            for (int b = 0; b < 4; ++b) {
+                const int B = cn[b];
+                const int bfix = p->dirichlet[B] != 0;
+                double* v = vals + 8 * (size_t)hbo_find(row_ptr, col_idx, A, B);
+                if (!afix && !bfix)
+                    v[0] += K[a * 4 + b];
+                for (int i = 0; i < 3; ++i) {
+                    if (!afix)
+                        v[1 + i] += G[a * 4 + b][i];
+                    if (!bfix)
+                        v[4 + i] += D[a * 4 + b][i];
+                }
+                v[7] += L[a * 4 + b];
+            }
+        }
+    }
+    for (int A = 0; A < p->nn; ++A)
+        if (p->dirichlet[A])
+            vals[8 * (size_t)hbo_find(row_ptr, col_idx, A, A)] = 1.0;
+}

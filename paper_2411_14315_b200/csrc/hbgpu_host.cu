@@ -2106,3 +2106,54 @@ extern "C" int hbgpu_solve_time(hbgpu_ctx* c, const hbgpu_time_cfg* cfg, double 
     }
     return finish(HBGPU_OK);
 }
+
+extern "C" int hbgpu_time_residual(hbgpu_ctx* c, const double* u, const double* udot, const double* p,
+                                   double omega_hat, double* r) {
+    if (!c || !u || !udot || !p || !r)
+        return c ? fail(c, HBGPU_ERR_INVALID, "time_residual: null buffer") : HBGPU_ERR_INVALID;
+    if (c->N != 1)
+        return fail(c, HBGPU_ERR_INVALID, "time_residual needs the N = 1 basis");
+    const int nn = c->nn;
+    cudaStream_t st = c->stream;
+    TimeBufs tb;
+    for (DBuf<double>* b : {&tb.u, &tb.ud})
+        CK(c, b->alloc(size_t(nn) * 3));
+    CK(c, tb.p.alloc(size_t(nn)));
+    CK(c, tb.s4.alloc(size_t(nn) * 4));
+    CK(c, tb.elem.alloc(size_t(c->ne) * 16));
+    CK(c, cudaMemcpyAsync(tb.u.p, u, sizeof(double) * size_t(nn) * 3, cudaMemcpyHostToDevice, st));
+    CK(c, cudaMemcpyAsync(tb.ud.p, udot, sizeof(double) * size_t(nn) * 3, cudaMemcpyHostToDevice, st));
+    CK(c, cudaMemcpyAsync(tb.p.p, p, sizeof(double) * size_t(nn), cudaMemcpyHostToDevice, st));
+    launch_time_residual(c->geom.p, c->conn.p, c->ne, c->inc_ptr.p, c->inc_rec.p, c->dir.p, nn, tb.u.p, tb.ud.p,
+                         tb.p.p, c->rho, c->mu, omega_hat, tb.elem.p, c->r.p, st);
+    if (c->nbnodes > 0) {
+        launch_time_pack(tb.u.p, tb.p.p, nn, tb.s4.p, st);
+        launch_boundary(boundary_args(c, tb.s4.p, c->r.p), st);
+    }
+    TRY(check_launch(c));
+    CK(c, cudaMemcpyAsync(r, c->r.p, sizeof(double) * size_t(nn) * 4, cudaMemcpyDeviceToHost, st));
+    CK(c, cudaStreamSynchronize(st));
+    return HBGPU_OK;
+}
+
+extern "C" int hbgpu_time_tangent(hbgpu_ctx* c, const double* u, double omega_hat, double am, double fg,
+                                  double* pvals) {
+    if (!c || !u)
+        return c ? fail(c, HBGPU_ERR_INVALID, "time_tangent: null buffer") : HBGPU_ERR_INVALID;
+    if (c->N != 1)
+        return fail(c, HBGPU_ERR_INVALID, "time_tangent needs the N = 1 basis");
+    const int nn = c->nn;
+    cudaStream_t st = c->stream;
+    TimeBufs tb;
+    CK(c, tb.u.alloc(size_t(nn) * 3));
+    CK(c, cudaMemcpyAsync(tb.u.p, u, sizeof(double) * size_t(nn) * 3, cudaMemcpyHostToDevice, st));
+    launch_time_tangent(c->geom.p, c->row_ptr.p, c->col_idx.p, c->inc_ptr.p, c->inc_rec.p, c->dir.p, nn, tb.u.p,
+                        c->rho, c->mu, omega_hat, am, fg, c->pvals.p, st);
+    TRY(check_launch(c));
+    c->p_valid = true;
+    c->inv_valid = false;
+    if (pvals)
+        CK(c, cudaMemcpyAsync(pvals, c->pvals.p, sizeof(double) * size_t(c->nnz) * 8, cudaMemcpyDeviceToHost, st));
+    CK(c, cudaStreamSynchronize(st));
+    return HBGPU_OK;
+}

@@ -182,6 +182,8 @@ _bsr_matvec_dev = _sig("hbgpu_bsr_matvec_dev", C.c_int, [_vp, _vp, _vp])
 _jacobi_dev = _sig("hbgpu_jacobi_dev", C.c_int, [_vp, _ip])
 _gmres_dev = _sig("hbgpu_gmres_dev", C.c_int, [_vp, _vp, C.POINTER(_KrylovCfg), _vp, C.POINTER(_KrylovRes), _vp, C.c_int])
 _pvals_dev = _sig("hbgpu_pvals_dev", _vp, [_vp])
+_time_residual = _sig("hbgpu_time_residual", C.c_int, [_vp, _vp, _vp, _vp, C.c_double, _vp])
+_time_tangent = _sig("hbgpu_time_tangent", C.c_int, [_vp, _vp, C.c_double, C.c_double, C.c_double, _vp])
 _solve_time = _sig("hbgpu_solve_time", C.c_int,
                    [_vp, C.POINTER(_TimeCfg), C.c_double, TimeDirichletFn, _vp, _vp, _vp, C.POINTER(_TimeResult)])
 _solve = _sig(
@@ -508,6 +510,20 @@ class GpuContext:
         return _pvals_dev(self._h)
 
     # ------------------------------------------------------------ time solver
+    def time_residual(self, u, udot, p, omega_hat: float = 0.0) -> np.ndarray:
+        """time_residual (time_solver.cpp:58-166); N = 1 context."""
+        u, ud, pp = _f64(u), _f64(udot), _f64(p)
+        r = np.empty(self.mesh.num_nodes * 4)
+        self._check(_time_residual(self._h, _ptr(u), _ptr(ud), _ptr(pp), float(omega_hat), _ptr(r)))
+        return r
+
+    def time_tangent(self, u, omega_hat: float, am: float, fg: float) -> np.ndarray:
+        """time_tangent (time_solver.cpp:172-254) -> N = 1 P values (kept on device)."""
+        u = _f64(u)
+        v = np.empty(self.nnz * 8)
+        self._check(_time_tangent(self._h, _ptr(u), float(omega_hat), float(am), float(fg), _ptr(v)))
+        return v
+
     def solve_time(self, dirichlet, cfg: TimeSolverConfig | None = None, period: float | None = None) -> TimeSolution:
         """solve_time (time_solver.cpp:269-485) on the device.  The context must
         hold the N = 1 basis (set_basis(1, period)) and steady Neumann data;

@@ -142,3 +142,29 @@ def test_time_needs_n1_basis(gpu):
     z = np.zeros(mesh.num_nodes * 3)
     with pytest.raises(ValueError):
         ctx.solve_time(lambda t: (z, z), time_cfg(5, 1))
+
+
+def _time_problem(mesh, h_out):
+    return cases.Problem(mesh, 1, PERIOD, 1.06, 0.04, np.zeros(mesh.num_nodes * 3),
+                         [(k, np.array([h_out])) for k, p in enumerate(mesh.patches) if p.kind == NEUMANN], 0.2)
+
+
+@pytest.mark.parametrize("which", ["tube", "config0"])
+def test_time_operators_match_restatement(gpu, which):
+    """time_residual / time_tangent kernels vs the plain-C restatement of
+    time_solver.cpp:58-254 at 1e-12, on a random state (both omega_hat regimes,
+    generalized-alpha and steady factors)."""
+    if which == "tube":
+        _, mesh = tube()
+    else:
+        mesh = cases.config_problem(0).mesh
+    prob = _time_problem(mesh, -20.0)
+    orc = ob.Restated(prob)
+    ctx = gpu_time_ctx(mesh, -20.0)
+    rng = np.random.default_rng(7)
+    nn = mesh.num_nodes
+    u, ud, p = rng.uniform(-2, 2, nn * 3), rng.uniform(-20, 20, nn * 3), rng.uniform(-50, 50, nn)
+    for om in (0.0, 3.7):
+        assert rel(ctx.time_residual(u, ud, p, om), orc.time_residual(u, ud, p, om)) < 1e-12
+        for am, fg in ((0.9166666, 0.00138), (0.0, 1.0)):
+            assert rel(ctx.time_tangent(u, om, am, fg), orc.time_tangent(u, om, am, fg)) < 1e-12

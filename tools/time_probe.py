@@ -12,14 +12,23 @@ from paper_2411_14315_b200 import cases  # noqa: E402
 from paper_2411_14315_b200.hbgpu import GpuContext, KrylovConfig, TimeSolverConfig  # noqa: E402
 from paper_2411_14315_b200.mesh import NEUMANN  # noqa: E402
 
-h = float(sys.argv[1]) if len(sys.argv) > 1 else 0.15
+arg = sys.argv[1] if len(sys.argv) > 1 else "0.15"
 steps = int(sys.argv[2]) if len(sys.argv) > 2 else 20
 cycles = int(sys.argv[3]) if len(sys.argv) > 3 else 2
-T = 0.5
-rm = ob.RefMesh.tube(0.3, 0.6, h)
-mesh = rm.to_mesh()
-fn = cases.time_dirichlet(mesh, mesh.patch_index("inlet"), 2.0, [0.2, -0.1], [0.1, 0.05], T)
-neu = [(k, np.array([-20.0])) for k, p in enumerate(mesh.patches) if p.kind == NEUMANN]
+if arg == "cfg0":  # BASELINE config 0 pipe, its inflow, dt of the 500-step cycle
+    prob = cases.config_problem(0)
+    mesh = prob.mesh
+    rm = ob.RefMesh.from_mesh(mesh)
+    Q0, a, b = cases.inflow_coefficients(0)
+    fn = cases.time_dirichlet(mesh, mesh.patch_index("inlet"), Q0, a, b, 1.0)
+    T = steps / 500.0
+    neu = [(k, np.array([0.0])) for k, p in enumerate(mesh.patches) if p.kind == NEUMANN]
+else:
+    T = 0.5
+    rm = ob.RefMesh.tube(0.3, 0.6, float(arg))
+    mesh = rm.to_mesh()
+    fn = cases.time_dirichlet(mesh, mesh.patch_index("inlet"), 2.0, [0.2, -0.1], [0.1, 0.05], T)
+    neu = [(k, np.array([-20.0])) for k, p in enumerate(mesh.patches) if p.kind == NEUMANN]
 rel = lambda a, b: float(np.linalg.norm(a - b) / np.linalg.norm(b))  # noqa: E731
 for orders, tol, mx in ((10.0, 1e-10, 12), (3.0, 0.03, 8)):
     ref = ob.RefCtx(rm, 1, T)
