@@ -201,6 +201,8 @@ typedef struct {
     int max_newton_iters;      /* 8 */
     hbgpu_krylov_cfg krylov;
     int steady;                /* drop the acceleration term, one steady solve */
+    double initial_pressure;   /* initial_pressure_level (assembly.cpp:415-427) of the HB
+                                  Neumann data; NaN = from the context's (steady) data */
 } hbgpu_time_cfg;
 
 typedef struct {

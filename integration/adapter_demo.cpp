@@ -100,18 +100,34 @@ int main() {
     auto t2 = std::chrono::steady_clock::now();
     const double e_solve = rel(s_gpu.state.data, s_ref.state.data);
 
+    // time-stepping solver (time_solver.cpp) on the same case plumbing
+    TimeSolverConfig tcfg = TimeSolverConfig::from_case(def);
+    tcfg.steps_per_cycle = 40;
+    tcfg.cycles = 2;
+    auto t3 = std::chrono::steady_clock::now();
+    const auto ts_ref = solve_time(in, tcfg);
+    auto t4 = std::chrono::steady_clock::now();
+    const auto ts_gpu = gpu::solve_time(in, tcfg);
+    auto t5 = std::chrono::steady_clock::now();
+    const double e_time_u = rel(ts_gpu.cycle.u, ts_ref.cycle.u);
+    const double e_time_p = rel(ts_gpu.cycle.p, ts_ref.cycle.p);
+
     const bool ok = e_res < 1e-12 && e_tan < 1e-12 && e_mass < 1e-15 && e_mv < 1e-12 &&
                     e_jac < 1e-15 && gmres_scaled <= 1e-8 * 1.0001 && s_ref.log.converged &&
-                    s_gpu.log.converged && e_solve < 1e-8;
+                    s_gpu.log.converged && e_solve < 1e-8 && e_time_u < 1e-8 && e_time_p < 1e-8 &&
+                    ts_gpu.total_steps == ts_ref.total_steps;
     std::printf(
         "{\"elements\": %d, \"N\": %d, \"residual\": %.3e, \"tangent\": %.3e, \"mass\": %.3e, "
         "\"matvec\": %.3e, \"jacobi\": %.3e, \"gmres_scaled_residual\": %.3e, \"gmres_iters\": %d, "
         "\"solve_state\": %.3e, \"newton_ref\": %zu, \"newton_gpu\": %zu, \"solve_ref_s\": %.3f, "
-        "\"solve_gpu_s\": %.3f, \"ok\": %s}\n",
+        "\"solve_gpu_s\": %.3f, \"time_u\": %.3e, \"time_p\": %.3e, \"time_newton_ref\": %d, "
+        "\"time_newton_gpu\": %d, \"time_ref_s\": %.3f, \"time_gpu_s\": %.3f, \"ok\": %s}\n",
         mesh.num_elements(), N, e_res, e_tan, e_mass, e_mv, e_jac, gmres_scaled, lin.iterations,
         e_solve, s_ref.log.entries.size(), s_gpu.log.entries.size(),
         std::chrono::duration<double>(t1 - t0).count(),
-        std::chrono::duration<double>(t2 - t1).count(), ok ? "true" : "false");
+        std::chrono::duration<double>(t2 - t1).count(), e_time_u, e_time_p, ts_ref.total_newton_iters,
+        ts_gpu.total_newton_iters, std::chrono::duration<double>(t4 - t3).count(),
+        std::chrono::duration<double>(t5 - t4).count(), ok ? "true" : "false");
     gpu::release(mesh);
     return ok ? 0 : 1;
 }

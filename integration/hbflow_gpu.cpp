@@ -279,6 +279,59 @@ HbSolution solve_harmonic(const Mesh& mesh, const std::vector<ElementGeometry>& 
     return sol;
 }
 
+TimeSolution solve_time(const CaseInputs& inputs, const TimeSolverConfig& cfg) {
+    const Mesh& mesh = inputs.mesh;
+    Entry& e = entry(mesh, nullptr);  // geometry on the device (mesh.cpp:159-211)
+    const double T = inputs.def.period;
+    set_basis(e, SpectralBasis(1, T));
+    // the time residual reads the steady outlet traction h[0] (time_solver.cpp:133)
+    BoundaryConditionSet b1 = inputs.bcs;
+    for (auto& nb : b1.neumann)
+        nb.h.assign(1, nb.h.empty() ? 0.0 : nb.h[0]);
+    b1.dirichlet_g.clear();
+    set_physics(e, inputs.props, b1, nullptr);
+    e.g_ptr = nullptr;  // b1 is a temporary
+    e.neu_patch.clear();
+    hbgpu_time_cfg tc{};
+    tc.steps_per_cycle = cfg.steps_per_cycle;
+    tc.cycles = cfg.cycles;
+    tc.rho_inf = cfg.rho_inf;
+    tc.newton_tol_orders = cfg.newton_tol_orders;
+    tc.max_newton_iters = cfg.max_newton_iters;
+    tc.krylov = {cfg.krylov.restart, cfg.krylov.max_iters, cfg.krylov.tolerance};
+    tc.steady = cfg.steady ? 1 : 0;
+    tc.initial_pressure = initial_pressure_level(mesh, inputs.bcs);  // over the HB samples
+    struct Tramp {
+        const TimeDirichletFn* fn;
+        std::vector<double> g, gd;
+    } tr{&inputs.time_dirichlet, {}, {}};
+    const size_t n3 = size_t(mesh.num_nodes()) * 3;
+    tr.g.resize(n3);
+    tr.gd.resize(n3);
+    auto cb = [](double t, double* g, double* gd, void* user) {
+        auto* s = static_cast<Tramp*>(user);
+        (*s->fn)(t, s->g, s->gd);
+        std::copy(s->g.begin(), s->g.end(), g);
+        std::copy(s->gd.begin(), s->gd.end(), gd);
+    };
+    TimeSolution sol;
+    const int nn = mesh.num_nodes();
+    const int snaps = cfg.steady ? 1 : cfg.steps_per_cycle + 1;
+    sol.cycle.period = T;
+    sol.cycle.steps = cfg.steady ? 0 : cfg.steps_per_cycle;
+    sol.cycle.num_nodes = nn;
+    sol.cycle.u.assign(size_t(snaps) * n3, 0.0);
+    sol.cycle.p.assign(size_t(snaps) * size_t(nn), 0.0);
+    hbgpu_time_result res{};
+    check(e.ctx, hbgpu_solve_time(e.ctx, &tc, T, cb, &tr, sol.cycle.u.data(), sol.cycle.p.data(), &res));
+    sol.cycle_change = res.cycle_change;
+    sol.total_seconds = res.total_seconds;
+    sol.total_steps = res.total_steps;
+    sol.total_newton_iters = res.total_newton_iters;
+    sol.omega_hat_last = res.omega_hat_last;
+    return sol;
+}
+
 void release(const Mesh& mesh) {
     auto& m = cache();
     auto it = m.find(&mesh);

@@ -12,6 +12,7 @@
 //   hbflow::jacobi_preconditioner  linalg.hpp:84
 //   hbflow::gmres_solve            linalg.hpp:111-115
 //   hbflow::solve_harmonic         hb_solver.hpp:70-72
+//   hbflow::solve_time             time_solver.hpp:51-54
 // Device contexts are cached per Mesh (geometry, pattern, incidence lists
 // are uploaded once); status codes are rethrown as the reference exceptions.
 #pragma once
@@ -19,6 +20,7 @@
 #include "hbflow/assembly.hpp"
 #include "hbflow/hb_solver.hpp"
 #include "hbflow/linalg.hpp"
+#include "hbflow/time_solver.hpp"
 
 #include <span>
 #include <vector>
@@ -51,6 +53,10 @@ KrylovResult gmres_solve(const TangentOperator& L, std::span<const double> rhs,
 HbSolution solve_harmonic(const Mesh& mesh, const std::vector<ElementGeometry>& geoms,
                           const SpectralBasis& basis, const FluidProperties& props,
                           const BoundaryConditionSet& bcs, const SolverConfig& cfg);
+
+/// Generalized-alpha time stepping (the paper's comparison baseline) on the
+/// device: time_residual / time_tangent kernels, N = 1 L-matvec and GMRES.
+TimeSolution solve_time(const CaseInputs& inputs, const TimeSolverConfig& cfg);
 
 /// Drop the cached device context of a mesh.
 void release(const Mesh& mesh);

@@ -1965,7 +1965,7 @@ extern "C" int hbgpu_solve_time(hbgpu_ctx* c, const hbgpu_time_cfg* cfg, double 
         acc += area * (-c->h_h[k]);
         wsum += area;
     }
-    const double p0 = wsum > 0.0 ? acc / wsum : 0.0;
+    const double p0 = std::isnan(cfg->initial_pressure) ? (wsum > 0.0 ? acc / wsum : 0.0) : cfg->initial_pressure;
     std::vector<double> hg(static_cast<size_t>(n3)), hgd(static_cast<size_t>(n3)), hu(static_cast<size_t>(n3), 0.0),
         hud(static_cast<size_t>(n3), 0.0), hp(static_cast<size_t>(nn), p0);
     dirichlet(0.0, hg.data(), hgd.data(), user);

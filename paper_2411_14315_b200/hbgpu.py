@@ -128,6 +128,7 @@ class _TimeCfg(C.Structure):
         ("max_newton_iters", C.c_int),
         ("krylov", _KrylovCfg),
         ("steady", C.c_int),
+        ("initial_pressure", C.c_double),
     ]
 
 
@@ -265,6 +266,7 @@ class TimeSolverConfig:
     max_newton_iters: int = 8
     krylov: KrylovConfig = field(default_factory=KrylovConfig)
     steady: bool = False
+    initial_pressure: float = float("nan")  # NaN: from the context's Neumann data
 
 
 @dataclass
@@ -540,7 +542,8 @@ class GpuContext:
         fn = TimeDirichletFn(cb)
         tc = _TimeCfg(int(cfg.steps_per_cycle), int(cfg.cycles), float(cfg.rho_inf), float(cfg.newton_tol_orders),
                       int(cfg.max_newton_iters),
-                      _KrylovCfg(cfg.krylov.restart, cfg.krylov.max_iters, cfg.krylov.tolerance), int(bool(cfg.steady)))
+                      _KrylovCfg(cfg.krylov.restart, cfg.krylov.max_iters, cfg.krylov.tolerance), int(bool(cfg.steady)),
+                      float(cfg.initial_pressure))
         nsnap = 1 if cfg.steady else cfg.steps_per_cycle + 1
         u = np.empty(nsnap * nn * 3)
         p = np.empty(nsnap * nn)
