@@ -556,6 +556,8 @@ def sweep_configs(args):
         ctx.set_basis(M, prob.period)
         ctx.set_fluid(prob.rho, prob.mu)
         ctx.set_bcs(prob.dirichlet_g, prob.neumann, prob.backflow_beta)
+        if cfg == 3:  # BASELINE config 3: resistance outlet R = 1e4 dyn s/cm^5 (hbgpu_set_resistance)
+            ctx.set_resistance({k: 1e4 for k, _ in prob.neumann})
         ctx.set_assembly_config(0, auto_pseudo_dt(prob))
         stream = torch.cuda.ExternalStream(ctx.stream)
         s = torch.from_numpy(cases.random_state(nn, N, 1000 + cfg)).cuda()
@@ -628,8 +630,8 @@ def sweep_configs(args):
         torch.cuda.empty_cache()
     print(json.dumps({"sweep": "configs", "fp64_peak_tflops": float(peak[0]), "hbm_peak_gbs": hbm,
                       "notes": "config 2: T-junction Delaunay (seeded points), two Dirichlet inlets; "
-                               "config 3: curved tapered 60% stenosis, zero-traction outlet (the "
-                               "BASELINE resistance outlet is not in the reference); random states "
+                               "config 3: curved tapered 60% stenosis, resistance outlet R = 1e4 "
+                               "(hbgpu_set_resistance; new physics, not in the reference); random states "
                                "for assembly/matvec timing, Newton iterate 0 for the GMRES step",
                       "results": out}), flush=True)
 

@@ -157,6 +157,14 @@ int hbgpu_jacobi_dev(hbgpu_ctx* ctx, int* degenerate_entries);
 int hbgpu_gmres_dev(hbgpu_ctx* ctx, const double* d_rhs, const hbgpu_krylov_cfg* cfg,
                     double* d_x, hbgpu_krylov_result* result, double* history,
                     int history_capacity);
+/* Resistance outlets (BASELINE config 3: R = 1e4 dyn s/cm^5) — new physics, not in
+ * the reference.  Neumann patch `patch[k]` gets the traction
+ * -R[k] Q(n) n on top of its Neumann data, Q(n) = outward flux of u(n) through the
+ * patch: r_m[A,i,n] += R Q(n) b[A,i] with b[A,i] = sum over A's facets of area/3 n_i,
+ * and TangentOperator::matvec gains R b b^T on free velocity rows/columns per
+ * sample (BSR matvec and Jacobi unchanged).  R = 0 / n = 0 removes them. */
+int hbgpu_set_resistance(hbgpu_ctx* ctx, int n, const int* patch, const double* R);
+
 /* Device pointers of the context's P values / mass / inverse diagonal. */
 double* hbgpu_pvals_dev(hbgpu_ctx* ctx);
 

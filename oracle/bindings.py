@@ -385,7 +385,7 @@ class _Problem(C.Structure):
         ("nn", _i), ("ne", _i), ("conn", _vp), ("geom", _vp), ("dirichlet", _vp), ("N", _i), ("H", _vp),
         ("rho", _d), ("mu", _d), ("tau_mode", _i), ("pseudo_dt", _d), ("pseudo_c1", _d),
         ("backflow_in_tangent", _i), ("nfac", _i), ("fac", _vp), ("fnormal", _vp), ("farea", _vp),
-        ("fbc", _vp), ("h", _vp), ("beta", _d),
+        ("fbc", _vp), ("h", _vp), ("beta", _d), ("resistance", _vp),
     ]
 
 
@@ -401,7 +401,8 @@ class Restated:
     """The plain-C restatement bound to one problem (mesh + basis + BCs + cfg)."""
 
     def __init__(self, prob, tau_mode=0, pseudo_dt=float("inf"), pseudo_c1=1.5, backflow_tangent=False,
-                 geometry=None):
+                 geometry=None, resistance=None):
+        """resistance: {patch_index: R} for resistance outlets (Neumann patches)."""
         if not os.path.exists(ORACLE_SO):
             raise OracleError(f"{ORACLE_SO} missing: run `make -C oracle`")
         L = C.CDLL(ORACLE_SO)
@@ -441,11 +442,13 @@ class Restated:
         self.fa = _f64(np.concatenate(areas) if areas else np.zeros(0))
         self.fbc = np.ascontiguousarray(np.concatenate(fbc) if fbc else np.zeros(0), np.int32)
         self.hh = _f64(np.concatenate(hs) if hs else np.zeros(0))
+        res = dict(resistance or {})
+        self.res = _f64([float(res.get(pidx, 0.0)) for pidx, _ in prob.neumann]) if res else None
         self.p = _Problem(self.nn, m.num_elements, _ptr(self.conn), _ptr(self.geom), _ptr(self.dm), self.N,
                           _ptr(self.H), prob.rho, prob.mu, tau_mode,
                           pseudo_dt if np.isfinite(pseudo_dt) else 0.0, pseudo_c1, int(backflow_tangent),
                           len(self.fa), _ptr(self.fac), _ptr(self.fn), _ptr(self.fa), _ptr(self.fbc),
-                          _ptr(self.hh), prob.backflow_beta)
+                          _ptr(self.hh), prob.backflow_beta, _ptr(self.res))
         self.row_ptr, self.col_idx = restated_pattern(self.nn, self.conn)
 
     @property

@@ -272,6 +272,69 @@ static void boundary_terms(const hbo_problem* p, const double* state, double* r)
     }
 }
 
+static int neumann_entries(const hbo_problem* p) {
+    int ne = 0;
+    for (int f = 0; f < p->nfac; ++f)
+        if (p->fbc[f] + 1 > ne)
+            ne = p->fbc[f] + 1;
+    return ne;
+}
+
+/* Resistance outlets (see hbgls_oracle.h): flux of `v` (layout (node*4+i)*N+n)
+ * through Neumann entry k at sample n, 3-point facet rule; free_only: only the
+ * non-Dirichlet nodes' values count (the tangent's masked columns). */
+static double entry_flux(const hbo_problem* p, int k, const double* v, int n, int free_only) {
+    const int N = p->N;
+    double Q = 0.0;
+    for (int f = 0; f < p->nfac; ++f) {
+        if (p->fbc[f] != k)
+            continue;
+        const int* fac = p->fac + 3 * f;
+        const double* nv = p->fnormal + 3 * f;
+        const double w = p->farea[f] / 3.0;
+        for (int q = 0; q < 3; ++q) {
+            double un = 0.0;
+            for (int a = 0; a < 3; ++a) {
+                if (free_only && p->dirichlet[fac[a]])
+                    continue;
+                for (int i = 0; i < 3; ++i)
+                    un += tri_shape(q, a) * v[((size_t)fac[a] * 4 + i) * N + n] * nv[i];
+            }
+            Q += w * un;
+        }
+    }
+    return Q;
+}
+
+/* out[A,i,n] += R_k Q_k(n) sum_{f,q} w N_a(q) n_i (rows of `free_only`-filtered nodes) */
+static void resistance_apply(const hbo_problem* p, const double* v, double* out, int free_only) {
+    if (!p->resistance)
+        return;
+    const int N = p->N, nk = neumann_entries(p);
+    for (int k = 0; k < nk; ++k) {
+        const double R = p->resistance[k];
+        if (R == 0.0)
+            continue;
+        for (int n = 0; n < N; ++n) {
+            const double RQ = R * entry_flux(p, k, v, n, free_only);
+            for (int f = 0; f < p->nfac; ++f) {
+                if (p->fbc[f] != k)
+                    continue;
+                const int* fac = p->fac + 3 * f;
+                const double* nv = p->fnormal + 3 * f;
+                const double w = p->farea[f] / 3.0;
+                for (int q = 0; q < 3; ++q)
+                    for (int a = 0; a < 3; ++a) {
+                        if (free_only && p->dirichlet[fac[a]])
+                            continue;
+                        for (int i = 0; i < 3; ++i)
+                            out[((size_t)fac[a] * 4 + i) * N + n] += w * tri_shape(q, a) * RQ * nv[i];
+                    }
+            }
+        }
+    }
+}
+
 int hbo_residual(const hbo_problem* p, const double* state, double* r) {
     const int N = p->N, nn = p->nn;
     const size_t tot = (size_t)nn * 4 * N;
@@ -320,6 +383,7 @@ int hbo_residual(const hbo_problem* p, const double* state, double* r) {
             }
         free(hs);
         boundary_terms(p, state, r);
+        resistance_apply(p, state, r, 0);
         /* zero the constrained velocity rows (assembly.cpp:541-544) */
         for (int A = 0; A < nn; ++A)
             if (p->dirichlet[A])
@@ -513,6 +577,7 @@ void hbo_tangent_matvec(const hbo_problem* p, const int* row_ptr, const int* col
     }
     free(t);
     free(ht);
+    resistance_apply(p, y, out, 1);
 }
 
 int hbo_jacobi(int nn, int N, const int* row_ptr, const int* col_idx, const double* vals,

@@ -124,6 +124,10 @@ struct hbgpu_ctx {
     std::vector<int> bc_patch;
     double beta = 0.2;
     DBuf<int> bnode, bptr, binc, fac, fbc;
+    // resistance outlets (set_resistance): per patch its nodes and flux weights b
+    int nres = 0;
+    DBuf<int> res_ptr, res_node;
+    DBuf<double> res_b, res_R;
     DBuf<double> fnormal, farea;
     int nbnodes = 0;
 
@@ -631,6 +635,8 @@ static int residual_dev(hbgpu_ctx* c, const double* d_state, double* d_r) {
         b.beta = c->beta;
         launch_boundary(b, st);
     }
+    launch_resistance(c->res_ptr.p, c->res_node.p, c->res_b.p, c->res_R.p, c->nres, c->dir.p, N, d_state, d_r,
+                      nullptr, 0, nullptr, st);
     const long p3 = prof_mark(c);
     prof_pair(c, kPhResidual, p0, p3);
     prof_pair(c, kPhResHu, p0, p1);
@@ -761,6 +767,9 @@ static int matvec_dev(hbgpu_ctx* c, const double* d_y, double* d_out, const doub
     a.with_c = (with_c && c->N > 1) ? 1 : 0;
     const long p0 = prof_mark(c);
     launch_lmatvec(a, c->stream);
+    if (with_c)  // resistance outlets belong to the tangent operator, not to P
+        launch_resistance(c->res_ptr.p, c->res_node.p, c->res_b.p, c->res_R.p, c->nres, c->dir.p, c->N, d_y, d_out,
+                          d_scale_out, 1, d_skip, c->stream);
     prof_pair(c, kPhMatvec, p0, prof_mark(c));
     return check_launch(c);
 }
@@ -1228,6 +1237,10 @@ void hbgpu_destroy(hbgpu_ctx* c) {
             cudaEventDestroy(e);
     c->arn.release();
     c->arn_ctl.release();
+    c->res_ptr.release();
+    c->res_node.release();
+    c->res_b.release();
+    c->res_R.release();
     for (DBuf<double>* b : {&c->geom, &c->H, &c->g, &c->hN, &c->fnormal, &c->farea, &c->state,
                             &c->r, &c->hu, &c->pvals, &c->mass, &c->mass_c, &c->inv, &c->y, &c->out,
                             &c->x, &c->w, &c->z, &c->scale, &c->b, &c->tmp, &c->V, &c->partial, &c->red, &c->rpartial})
@@ -1515,6 +1528,50 @@ int hbgpu_set_bcs(hbgpu_ctx* c, const double* dirichlet_g, int n_neumann, const 
         CK(c, cudaMemcpyAsync(c->hN.p, c->h_h.data(), sizeof(double) * c->h_h.size(), cudaMemcpyHostToDevice, st));
     }
     CK(c, cudaStreamSynchronize(c->stream));
+    return HBGPU_OK;
+}
+
+int hbgpu_set_resistance(hbgpu_ctx* c, int n, const int* patch, const double* R) {
+    if (n < 0 || (n > 0 && (!patch || !R)))
+        return fail(c, HBGPU_ERR_INVALID, "set_resistance: bad arguments");
+    std::vector<int> ptr{0}, node;
+    std::vector<double> b, rv;
+    for (int k = 0; k < n; ++k) {
+        if (patch[k] < 0 || patch[k] >= int(c->patches.size()) || c->patches[size_t(patch[k])].kind != 1)
+            return fail(c, HBGPU_ERR_INVALID, "set_resistance: patch " + std::to_string(patch[k]) +
+                                                  " is not a Neumann patch");
+        if (R[k] == 0.0)
+            continue;
+        const HostPatch& p = c->patches[size_t(patch[k])];
+        // b_A = sum over A's facets (facet order) of area/3 * normal
+        std::vector<int> local(static_cast<size_t>(c->nn), -1);
+        const size_t base = node.size();
+        for (size_t f = 0; f < p.areas.size(); ++f)
+            for (int a = 0; a < 3; ++a) {
+                const int A = p.facets[3 * f + size_t(a)];
+                if (local[size_t(A)] < 0) {
+                    local[size_t(A)] = int(node.size() - base);
+                    node.push_back(A);
+                    b.insert(b.end(), {0.0, 0.0, 0.0});
+                }
+                double* bk = b.data() + 3 * (base + size_t(local[size_t(A)]));
+                for (int i = 0; i < 3; ++i)
+                    bk[i] += p.areas[f] / 3.0 * p.normals[3 * f + size_t(i)];
+            }
+        ptr.push_back(int(node.size()));
+        rv.push_back(R[k]);
+    }
+    c->nres = int(rv.size());
+    if (c->nres > 0) {
+        CK(c, c->res_ptr.alloc(ptr.size()));
+        CK(c, c->res_node.alloc(node.size()));
+        CK(c, c->res_b.alloc(b.size()));
+        CK(c, c->res_R.alloc(rv.size()));
+        CK(c, cudaMemcpy(c->res_ptr.p, ptr.data(), sizeof(int) * ptr.size(), cudaMemcpyHostToDevice));
+        CK(c, cudaMemcpy(c->res_node.p, node.data(), sizeof(int) * node.size(), cudaMemcpyHostToDevice));
+        CK(c, cudaMemcpy(c->res_b.p, b.data(), sizeof(double) * b.size(), cudaMemcpyHostToDevice));
+        CK(c, cudaMemcpy(c->res_R.p, rv.data(), sizeof(double) * rv.size(), cudaMemcpyHostToDevice));
+    }
     return HBGPU_OK;
 }
 

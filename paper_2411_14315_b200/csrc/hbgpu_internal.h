@@ -245,6 +245,10 @@ void launch_residual_nodes(const double* H, int N, int nn, const int* npart_ptr,
                            const double* partial, const uint8_t* dir, double* r, int T,
                            long npairs, cudaStream_t st);
 void launch_boundary(const BoundaryArgs& a, cudaStream_t st);
+// resistance outlets: out[free velocity rows] += (scale) R Q b per (patch, sample)
+void launch_resistance(const int* ptr, const int* node, const double* b, const double* R, int npatch,
+                       const uint8_t* dir, int N, const double* v, double* out, const double* scale, int free_cols,
+                       const int* skip, cudaStream_t st);
 void launch_mass_rows(const double* geom, const int* row_ptr, const int* inc_ptr, const int4* rec,
                       double rho, double* mass, int nn, cudaStream_t st);
 void launch_tangent_geometry(const double* geom, int ne, double* tg, cudaStream_t st);

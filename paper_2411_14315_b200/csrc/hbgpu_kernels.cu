@@ -640,6 +640,66 @@ void launch_boundary(const BoundaryArgs& a, cudaStream_t st) {
     boundary_kernel<<<(int)((threads + 255) / 256), 256, 0, st>>>(a);
 }
 
+// Resistance outlets (BASELINE config 3; new physics, not in the reference —
+// SURVEY 8(f) row 4; restated in oracle/hbgls_oracle.c): CTA (patch, sample n)
+// forms the outward flux Q = sum_k b_k . v_k(n) over the patch's nodes in a
+// fixed order (b_k = sum over the node's facets of area/3 * normal, the exact
+// 3-point-rule weights) and adds R Q b_k to the velocity rows of its free
+// nodes, optionally output-scaled (the GMRES operator S L S).  free_cols: only
+// free nodes enter Q (the tangent's masked columns); the residual uses all.
+__global__ void resistance_kernel(const int* __restrict__ ptr, const int* __restrict__ node,
+                                  const double* __restrict__ b, const double* __restrict__ R,
+                                  const uint8_t* __restrict__ dir, int N, const double* __restrict__ v,
+                                  double* __restrict__ out, const double* __restrict__ scale, int free_cols,
+                                  const int* skip) {
+    if (skip && *skip)
+        return;
+    __shared__ double red[8];
+    __shared__ double s_q;
+    const int pch = blockIdx.x, n = blockIdx.y;
+    const int k0 = ptr[pch], k1 = ptr[pch + 1];
+    double acc = 0.0;
+    for (int k = k0 + threadIdx.x; k < k1; k += blockDim.x) {
+        const long A = node[k];
+        if (free_cols && dir[A])
+            continue;
+        const double* vb = v + (A * 4) * N + n;
+        acc += b[3 * k] * vb[0] + b[3 * k + 1] * vb[N] + b[3 * k + 2] * vb[2 * N];
+    }
+    for (int o = 16; o > 0; o >>= 1)
+        acc += __shfl_down_sync(0xffffffffu, acc, o);
+    if ((threadIdx.x & 31) == 0)
+        red[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double q = 0.0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w)
+            q += red[w];
+        s_q = R[pch] * q;
+    }
+    __syncthreads();
+    const double rq = s_q;
+    for (int k = k0 + threadIdx.x; k < k1; k += blockDim.x) {
+        const long A = node[k];
+        if (dir[A])
+            continue;
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {
+            const long o = (A * 4 + i) * N + n;
+            out[o] += (scale ? scale[o] : 1.0) * rq * b[3 * k + i];
+        }
+    }
+}
+
+void launch_resistance(const int* ptr, const int* node, const double* b, const double* R, int npatch,
+                       const uint8_t* dir, int N, const double* v, double* out, const double* scale, int free_cols,
+                       const int* skip, cudaStream_t st) {
+    if (npatch <= 0)
+        return;
+    note_launch();
+    resistance_kernel<<<dim3(npatch, N), 256, 0, st>>>(ptr, node, b, R, dir, N, v, out, scale, free_cols, skip);
+}
+
 // jacobi_preconditioner (linalg.cpp:130-154)
 __global__ void jacobi_kernel(const double* __restrict__ vals, const int* __restrict__ diag_blk,
                               int nn, int N, double* __restrict__ inv, int* degenerate) {

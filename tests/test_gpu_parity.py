@@ -389,3 +389,64 @@ def test_matvec_kernel_variants(gpu, monkeypatch, modes, variant):
     assert rel(out, orc.matvec(p, m, y)) < TOL
     assert rel(ctx.bsr_matvec(y), orc.bsr_matvec(p, y)) < TOL
     assert np.array_equal(out, ctx.matvec(y))
+
+
+@pytest.mark.parametrize("modes", [1, 3])
+def test_resistance_outlet(gpu, modes):
+    """Resistance outlet (BASELINE config 3, new physics
+    restated in oracle/hbgls_oracle.c): residual and TangentOperator::matvec
+    with the R Q(u) traction vs the restatement at 1e-12; the BSR matvec (P
+    only) is unchanged; the matvec's extra part is exactly R b b^T y."""
+    prob = tube_problem(modes, h=0.25)
+    outlet = [k for k, p in enumerate(prob.mesh.patches) if p.kind == NEUMANN][0]
+    R = 1.3e4
+    ctx = gpu_ctx(prob, 0, 0.3)
+    ctx.set_resistance({outlet: R})
+    orc = ob.Restated(prob, tau_mode=0, pseudo_dt=0.3, resistance={outlet: R})
+    orc0 = ob.Restated(prob, tau_mode=0, pseudo_dt=0.3)
+    nn, N = prob.mesh.num_nodes, prob.N
+    s = cases.random_state(nn, N, 31)
+    r = ctx.assemble_residual(s)
+    assert rel(r, orc.residual(s)) < TOL
+    assert rel(r, orc0.residual(s)) > 1e-6  # the term is really there
+    p = ctx.assemble_tangent(s)
+    m = orc.mass()
+    y = cases.random_state(nn, N, 32)
+    out = ctx.matvec(y)
+    assert rel(out, orc.matvec(p, m, y)) < TOL
+    assert rel(ctx.bsr_matvec(y), orc.bsr_matvec(p, y)) < TOL
+    # the operator's outlet part is the derivative of the residual's (linear in u,
+    # Dirichlet columns masked)
+    d_l = out - orc0.matvec(p, m, y)
+    yf = y.copy().reshape(nn, 4, N)
+    yf[prob.mesh.dirichlet.astype(bool)] = 0.0
+    d_rf = (orc.residual(s + yf.reshape(-1)) - orc0.residual(s + yf.reshape(-1))) - (orc.residual(s) - orc0.residual(s))
+    assert rel(d_l, d_rf) < 1e-10
+    ctx.set_resistance({outlet: 0.0})
+    assert rel(ctx.assemble_residual(s), orc0.residual(s)) < TOL
+
+
+def test_resistance_outlet_solve(gpu):
+    """A harmonic solve with a resistance outlet converges (GPU Newton + GMRES
+    on the operator with the rank-one outlet coupling) to a root of the
+    restated residual with the same outlet."""
+    from paper_2411_14315_b200.hbgpu import KrylovConfig, SolverConfig
+
+    prob = tube_problem(3, h=0.25, traction=False)
+    outlet = [k for k, p in enumerate(prob.mesh.patches) if p.kind == NEUMANN][0]
+    g = cases.parabolic_dirichlet(prob.mesh, prob.mesh.patch_index("inlet"),
+                                  cases.flow_samples(2.0, [0.2, -0.1], [0.1, 0.05], 3, prob.period))
+    prob = cases.Problem(prob.mesh, 3, prob.period, 1.06, 0.04, g, prob.neumann, 0.2)
+    ctx = gpu_ctx(prob)
+    ctx.set_resistance({outlet: 1e4})
+    sol = ctx.solve_harmonic(SolverConfig(newton_tol_orders=8.0, max_newton_iters=200,
+                                          krylov=KrylovConfig(200, 2000, 1e-9)))
+    assert sol.log.converged
+    orc = ob.Restated(prob, resistance={outlet: 1e4}, pseudo_dt=0.0)
+    r = orc.residual(sol.state)
+    r0 = orc.residual(cases.initial_state(prob))
+    assert np.linalg.norm(r) <= 1e-7 * np.linalg.norm(r0)
+    # outlet pressure follows R Q: the mean outlet pressure is ~R times the mean inflow (2 mL/s)
+    pr = sol.state.reshape(prob.mesh.num_nodes, 4, prob.N)[:, 3, :]
+    onodes = np.unique(prob.mesh.patches[outlet].facets)
+    assert 0.5 * 2e4 < pr[onodes].mean() < 1.5 * 2e4

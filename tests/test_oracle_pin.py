@@ -101,3 +101,32 @@ def test_restatement_matches_reference_fresh(modes, tau):
     assert rel(orc.matvec(p, orc.mass(), y), ref.matvec(y, 4)) < 1e-13
     rp, ci = ob.RefMesh.from_mesh(prob.mesh).pattern()
     assert np.array_equal(rp, orc.row_ptr) and np.array_equal(ci, orc.col_idx)
+
+
+def test_resistance_restatement_is_consistent():
+    """The restated resistance outlet (hbgls_oracle.c): its operator part is the
+    exact derivative of its residual part (linear in u, Dirichlet columns
+    masked), and R = 0 reproduces the plain restatement bit for bit."""
+    from oracle.bindings import Restated
+    from paper_2411_14315_b200 import cases, meshgen
+    from paper_2411_14315_b200.mesh import NEUMANN
+
+    mesh = meshgen.hex_cylinder(0.4, 1.0, 3, 3, 4)
+    N = 3
+    neu = [(k, np.full(N, -5.0)) for k, p in enumerate(mesh.patches) if p.kind == NEUMANN]
+    prob = cases.Problem(mesh, 2, 1.0, 1.06, 0.04, np.zeros(mesh.num_nodes * 3 * N), neu, 0.2)
+    out = neu[0][0]
+    o1, o0 = Restated(prob, resistance={out: 2e4}), Restated(prob)
+    oz = Restated(prob, resistance={out: 0.0})
+    s = cases.random_state(mesh.num_nodes, N, 5)
+    y = cases.random_state(mesh.num_nodes, N, 6)
+    assert np.array_equal(oz.residual(s), o0.residual(s))
+    p = o0.tangent(s)
+    m = o0.mass()
+    yf = y.reshape(mesh.num_nodes, 4, N).copy()
+    yf[mesh.dirichlet.astype(bool)] = 0.0
+    yf = yf.reshape(-1)
+    d_r = (o1.residual(s + yf) - o0.residual(s + yf)) - (o1.residual(s) - o0.residual(s))
+    d_l = o1.matvec(p, m, y) - o0.matvec(p, m, y)
+    assert np.linalg.norm(d_l) > 0
+    assert np.linalg.norm(d_r - d_l) <= 1e-10 * np.linalg.norm(d_l)
