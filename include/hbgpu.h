@@ -165,6 +165,10 @@ int hbgpu_gmres_dev(hbgpu_ctx* ctx, const double* d_rhs, const hbgpu_krylov_cfg*
  * sample (BSR matvec and Jacobi unchanged).  R = 0 / n = 0 removes them. */
 int hbgpu_set_resistance(hbgpu_ctx* ctx, int n, const int* patch, const double* R);
 
+/* Copy of the context's current P values (BlockSparseMatrix::vals layout), e.g.
+ * after hbgpu_assemble, which keeps P on the device. */
+int hbgpu_get_pvals(hbgpu_ctx* ctx, double* pvals);
+
 /* Device pointers of the context's P values / mass / inverse diagonal. */
 double* hbgpu_pvals_dev(hbgpu_ctx* ctx);
 

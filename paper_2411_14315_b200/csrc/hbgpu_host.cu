@@ -100,12 +100,20 @@ struct hbgpu_ctx {
         DBuf<int> pack_ptr;
         int max_pack = 0, grid = 0, threads = 128;
         bool pipe = false;
+        // fused assembly variant (tangent_fused_kernel)
+        size_t fsmem = 0;
+        int fgrid = 0;
     } tb[6];
     DBuf<double> blkc;        // per block: n-invariant tangent sums (8)
     DBuf<uint8_t> blk_order;  // per row: off-diagonal blocks by descending contribution count
     DBuf<double> tgeom;
     DBuf<int> row_ptr, col_idx, diag_blk, inc_ptr;
     DBuf<int> mv_perm;  // L-matvec row order: by descending length within 4096-row windows
+    // fused assembly: element summaries written by the residual pass, read by the
+    // tangent rows (all pipe buckets hold whole series); disabled if not
+    bool fused_ok = false;
+    int summ_ns = 0;
+    DBuf<double> tsumm;
     // residual element chunks
     int nchunks = 0, max_nloc = 0, res_grid = 0, res_tile = 4;
     long npairs = 0;
@@ -584,7 +592,7 @@ static int rows_per_matvec_cta(int N) { return std::max(1, 256 / N); }
 
 // ---------------------------------------------------------------- operations
 
-static int residual_dev(hbgpu_ctx* c, const double* d_state, double* d_r) {
+static int residual_dev(hbgpu_ctx* c, const double* d_state, double* d_r, double* d_summ = nullptr) {
     const int N = c->N;
     cudaStream_t st = c->stream;
     const long p0 = prof_mark(c);
@@ -612,6 +620,8 @@ static int residual_dev(hbgpu_ctx* c, const double* d_state, double* d_r) {
     ca.nu = c->mu / c->rho;
     ca.tau_mode = c->tau_mode;
     ca.flag = c->flag.p;
+    ca.summ = d_summ;
+    ca.summ_ns = c->summ_ns;
     launch_residual_chunks(ca, c->res_grid, c->res_tile, st);
     const long p2 = prof_mark(c);
     launch_residual_nodes(c->H.p, N, c->nn, c->npart_ptr.p, c->npart.p, c->rpartial.p, c->dir.p,
@@ -1425,6 +1435,43 @@ int hbgpu_set_basis(hbgpu_ctx* c, int modes, double period) {
             const int tiles = (N + b.nt - 1) / b.nt;
             b.grid = std::max(1, std::min(b.count, (nsm * per_sm + tiles - 1) / tiles));
         }
+        // fused assembly: every bucket on the pipeline with whole series
+        c->summ_ns = N + (N & 1);
+        c->tsumm.release();
+        // opt-in (HBGPU_FUSED=1): measured at config 1, the residual pass grows
+        // 0.60 -> 0.82 ms with the summaries while the tangent rows drop 0.92 ->
+        // 0.74 ms (gather-latency bound), a net loss against the concurrent pair
+        c->fused_ok = std::getenv("HBGPU_FUSED") != nullptr;
+        size_t fx[5] = {0, 0, 0, 0, 0};
+        for (auto& b : c->tb) {
+            if (!b.count)
+                continue;
+            if (!b.pipe || b.nt != N) {
+                c->fused_ok = false;
+                continue;
+            }
+            b.fsmem = tangent_fused_smem(b.max_pack, b.max_inc, N, c->summ_ns);
+            if (b.fsmem > size_t(227 * 1024))
+                c->fused_ok = false;
+            const int w = int(std::find(widths, widths + 5, b.threads) - widths);
+            fx[w] = std::max(fx[w], b.fsmem);
+        }
+        if (c->fused_ok) {
+            for (int w = 0; w < 5; ++w)
+                if (fx[w])
+                    CK(c, configure_tangent_fused_smem(widths[w], fx[w]));
+            for (auto& b : c->tb) {
+                if (!b.count)
+                    continue;
+                int per_sm = 0;
+                CK(c, tangent_fused_occupancy(b.threads, &per_sm, b.fsmem));
+                if (per_sm < 1) {
+                    c->fused_ok = false;
+                    break;
+                }
+                b.fgrid = std::max(1, std::min(b.count, nsm * per_sm));
+            }
+        }
     }
     // clear previous Neumann data sized for another N
     c->hN.release();
@@ -1616,7 +1663,89 @@ int hbgpu_assemble_residual(hbgpu_ctx* c, const double* state, double* residual)
 // the two latency-bound kernels share the SMs; ordered on ctx->stream after.
 // With host_r the residual's copy to the host is queued right behind the
 // residual, so it overlaps the tangent.
+// Fused assembly: the residual pass also writes the tangent's element
+// summaries; the tangent rows then run without recomputing them.
+static int tangent_fused_dev(hbgpu_ctx* c, cudaStream_t st) {
+    TangentArgs a{};
+    a.tgeom = c->tgeom.p;
+    a.pvals = c->pvals.p;
+    a.N = c->N;
+    a.rho = c->rho;
+    a.mu = c->mu;
+    a.nu = c->mu / c->rho;
+    a.pseudo_c = std::isfinite(c->pseudo_dt) ? c->pseudo_c1 * c->rho / c->pseudo_dt : 0.0;
+    a.tau_mode = c->tau_mode;
+    a.flag = c->flag.p;
+    for (const auto& b : c->tb) {
+        if (!b.count)
+            continue;
+        a.max_inc = b.max_inc;
+        a.max_blk = b.max_blk;
+        a.NT = c->N;
+        PipeArgs pa;
+        pa.pack = b.pack.p;
+        pa.pack_ptr = b.pack_ptr.p;
+        pa.nrows = b.count;
+        pa.max_pack = b.max_pack;
+        pa.summ = c->tsumm.p;
+        pa.summ_ns = c->summ_ns;
+        launch_tangent_fused(a, pa, b.threads, b.fgrid, b.fsmem, st);
+    }
+    return check_launch(c);
+}
+
+static bool fused_ready(hbgpu_ctx* c) {
+    if (!c->fused_ok || c->backflow_tangent)
+        return false;
+    const size_t need = size_t(c->ne) * 16 * size_t(c->summ_ns);
+    if (c->tsumm.n < need && (c->tsumm.alloc(need) != cudaSuccess)) {
+        cudaGetLastError();
+        c->tsumm.release();
+        c->fused_ok = false;  // not enough memory: separate kernels from now on
+        return false;
+    }
+    return true;
+}
+
 static int assemble_both(hbgpu_ctx* c, const double* d_state, double* d_r, double* host_r = nullptr) {
+    if (host_r && !fused_ready(c)) {
+        // host copy-back wanted: residual first, then the tangent on the second
+        // stream while the residual travels back (concurrent kernels would finish
+        // together and leave the copy exposed)
+        TRY(residual_dev(c, d_state, d_r));
+        CK(c, cudaEventRecord(c->ev_fork, c->stream));
+        CK(c, cudaStreamWaitEvent(c->stream2, c->ev_fork, 0));
+        CK(c, cudaMemcpyAsync(host_r, d_r, sizeof(double) * size_t(c->state_len()), cudaMemcpyDeviceToHost,
+                              c->stream));
+        cudaStream_t main = c->stream;
+        c->stream = c->stream2;
+        const int st = tangent_dev(c, d_state);
+        c->stream = main;
+        TRY(st);
+        CK(c, cudaEventRecord(c->ev_join, c->stream2));
+        CK(c, cudaStreamWaitEvent(c->stream, c->ev_join, 0));
+        return HBGPU_OK;
+    }
+    if (fused_ready(c)) {
+        // residual (+ element summaries) on the main stream, then the tangent rows
+        // on the second stream; the residual's copy-back overlaps the tangent
+        const long p0 = prof_mark(c);
+        TRY(residual_dev(c, d_state, d_r, c->tsumm.p));
+        CK(c, cudaEventRecord(c->ev_fork, c->stream));
+        CK(c, cudaStreamWaitEvent(c->stream2, c->ev_fork, 0));
+        if (host_r)
+            CK(c, cudaMemcpyAsync(host_r, d_r, sizeof(double) * size_t(c->state_len()), cudaMemcpyDeviceToHost,
+                                  c->stream));
+        const long p1 = prof_mark(c);
+        TRY(tangent_fused_dev(c, c->stream2));
+        c->p_valid = true;
+        c->inv_valid = false;
+        CK(c, cudaEventRecord(c->ev_join, c->stream2));
+        CK(c, cudaStreamWaitEvent(c->stream, c->ev_join, 0));
+        prof_pair(c, kPhTangent, p1, prof_mark(c));
+        (void)p0;
+        return HBGPU_OK;
+    }
     CK(c, cudaEventRecord(c->ev_fork, c->stream));
     CK(c, cudaStreamWaitEvent(c->stream2, c->ev_fork, 0));
     cudaStream_t main = c->stream;
@@ -1695,6 +1824,14 @@ int hbgpu_set_pvals(hbgpu_ctx* c, const double* pvals) {
 }
 
 double* hbgpu_pvals_dev(hbgpu_ctx* c) { return c->pvals.p; }
+
+int hbgpu_get_pvals(hbgpu_ctx* c, double* pvals) {
+    if (!c->p_valid)
+        return fail(c, HBGPU_ERR_INVALID, "get_pvals before assemble_tangent / set_pvals");
+    CK(c, cudaStreamSynchronize(c->stream));
+    CK(c, cudaMemcpy(pvals, c->pvals.p, sizeof(double) * size_t(c->nnz) * 8 * size_t(c->N), cudaMemcpyDeviceToHost));
+    return HBGPU_OK;
+}
 
 int hbgpu_matvec_dev(hbgpu_ctx* c, const double* d_y, double* d_out) {
     TRY(ensure_basis(c));

@@ -183,6 +183,7 @@ _bsr_matvec_dev = _sig("hbgpu_bsr_matvec_dev", C.c_int, [_vp, _vp, _vp])
 _jacobi_dev = _sig("hbgpu_jacobi_dev", C.c_int, [_vp, _ip])
 _gmres_dev = _sig("hbgpu_gmres_dev", C.c_int, [_vp, _vp, C.POINTER(_KrylovCfg), _vp, C.POINTER(_KrylovRes), _vp, C.c_int])
 _pvals_dev = _sig("hbgpu_pvals_dev", _vp, [_vp])
+_get_pvals = _sig("hbgpu_get_pvals", C.c_int, [_vp, _vp])
 _set_resistance = _sig("hbgpu_set_resistance", C.c_int, [_vp, C.c_int, _vp, _vp])
 _time_residual = _sig("hbgpu_time_residual", C.c_int, [_vp, _vp, _vp, _vp, C.c_double, _vp])
 _time_tangent = _sig("hbgpu_time_tangent", C.c_int, [_vp, _vp, C.c_double, C.c_double, C.c_double, _vp])
@@ -394,6 +395,12 @@ class GpuContext:
         pidx = np.array([p for p, _ in neumann], dtype=np.int32)
         hh = _f64(np.array([np.asarray(h, dtype=np.float64) for _, h in neumann]).reshape(-1)) if neumann else np.zeros(0)
         self._check(_set_bcs(self._h, _ptr(g), len(pidx), _ptr(pidx), _ptr(hh), float(backflow_beta)))
+
+    def pvals(self) -> np.ndarray:
+        """The current P values (after assemble / assemble_tangent / set_pvals)."""
+        v = np.empty(self.nnz * 8 * self.N)
+        self._check(_get_pvals(self._h, _ptr(v)))
+        return v
 
     def set_resistance(self, resistance: dict):
         """{neumann patch index: R} resistance outlets (hbgpu_set_resistance)."""
