@@ -503,3 +503,61 @@ def test_fused_assembly_delaunay(gpu, monkeypatch):
     r = ctx.assemble(s)
     assert rel(r, orc.residual(s)) < TOL
     assert rel(ctx.pvals(), orc.tangent(s)) < TOL
+
+
+def test_error_paths(gpu):
+    """The reference's exceptions through the C ABI: degenerate element ->
+    GeometryError (mesh.cpp:173-174, the device geometry pass), bad basis / fluid
+    -> ParseError (spectral.cpp:19-22, assembly.cpp:38-41), Neumann data on a
+    missing patch -> invalid_argument (the reference would index out of range).
+    Neumann data on a Dirichlet patch is accepted, as in the reference
+    (accumulate_boundary_terms does not check the kind): it only touches
+    constrained rows, which are zeroed."""
+    from paper_2411_14315_b200 import meshgen
+    from paper_2411_14315_b200.hbgpu import GpuContext
+    from paper_2411_14315_b200.mesh import GeometryError, ParseError
+
+    mesh = meshgen.hex_cylinder(0.3, 1.0, 2, 2, 3)
+    mesh.finalize()
+    bad = mesh.xyz.copy()
+    e0 = mesh.conn[0]
+    bad[e0[3]] = bad[e0[0]] + 0.5 * (bad[e0[1]] - bad[e0[0]])  # collapse element 0
+    mesh.xyz = bad
+    with pytest.raises(GeometryError):
+        GpuContext(mesh)
+    mesh = meshgen.hex_cylinder(0.3, 1.0, 2, 2, 3)
+    ctx = GpuContext(mesh)
+    with pytest.raises(ParseError):
+        ctx.set_basis(0, 1.0)
+    ctx.set_basis(2, 1.0)
+    with pytest.raises(ParseError):
+        ctx.set_fluid(-1.0, 0.04)
+    ctx.set_bcs(None, [(mesh.patch_index("wall"), np.ones(3))], 0.2)
+    with pytest.raises(ValueError):
+        ctx.set_bcs(None, [(len(mesh.patches) + 3, np.zeros(3))], 0.2)
+
+
+def test_all_dirichlet_boundary(gpu):
+    """No Neumann patch at all (every boundary node constrained): residual,
+    tangent and L-matvec parity; Dirichlet velocity rows zero, pressure rows kept."""
+    from paper_2411_14315_b200 import meshgen
+    from paper_2411_14315_b200.mesh import DIRICHLET, Mesh, Patch
+
+    m0 = meshgen.hex_cylinder(0.4, 1.0, 3, 3, 4)
+    mesh = Mesh(xyz=m0.xyz, conn=m0.conn,
+                patches=[Patch(p.name, DIRICHLET, p.facets) for p in m0.patches])
+    mesh.finalize()
+    N = 5
+    g = np.random.default_rng(3).uniform(-1, 1, mesh.num_nodes * 3 * N)
+    prob = cases.Problem(mesh, 3, 1.0, 1.06, 0.04, g, [], 0.2)
+    ctx = gpu_ctx(prob, 0, 0.2)
+    orc = ob.Restated(prob, tau_mode=0, pseudo_dt=0.2)
+    s = cases.random_state(mesh.num_nodes, N, 51)
+    r = ctx.assemble_residual(s)
+    assert rel(r, orc.residual(s)) < TOL
+    rv = r.reshape(mesh.num_nodes, 4, N)
+    assert np.all(rv[mesh.dirichlet.astype(bool), :3] == 0.0)
+    p = ctx.assemble_tangent(s)
+    assert rel(p, orc.tangent(s)) < TOL
+    y = cases.random_state(mesh.num_nodes, N, 52)
+    assert rel(ctx.matvec(y), orc.matvec(p, orc.mass(), y)) < TOL
