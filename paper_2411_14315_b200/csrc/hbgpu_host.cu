@@ -109,6 +109,7 @@ struct hbgpu_ctx {
     DBuf<double> tgeom;
     DBuf<int> row_ptr, col_idx, diag_blk, inc_ptr;
     DBuf<int> mv_perm;  // L-matvec row order: by descending length within 4096-row windows
+    DBuf<int4> mv_rows; // {A, row_ptr[A], row_ptr[A+1], 0} in that order
     // fused assembly: element summaries written by the residual pass, read by the
     // tangent rows (all pipe buckets hold whole series); disabled if not
     bool fused_ok = false;
@@ -347,6 +348,13 @@ static int upload_all(hbgpu_ctx* c, const hbgpu_mesh_desc* d) {
         }
         CK(c, c->mv_perm.alloc(size_t(nn)));
         CK(c, cudaMemcpyAsync(c->mv_perm.p, perm.data(), sizeof(int) * size_t(nn), cudaMemcpyHostToDevice, st));
+        std::vector<int4> rows(static_cast<size_t>(nn));
+        for (int q = 0; q < nn; ++q) {
+            const int A = perm[size_t(q)];
+            rows[size_t(q)] = make_int4(A, rp[A], rp[A + 1], 0);
+        }
+        CK(c, c->mv_rows.alloc(size_t(nn)));
+        CK(c, cudaMemcpyAsync(c->mv_rows.p, rows.data(), sizeof(int4) * size_t(nn), cudaMemcpyHostToDevice, st));
         CK(c, cudaStreamSynchronize(st));
     }
 
@@ -740,13 +748,13 @@ static int mass_dev(hbgpu_ctx* c) {
 
 // L-matvec kernel variant: bit 0 = rows in length-balanced order (mv_perm),
 // bit 1 = N == 1 rows split over 4 lanes, bits 2-3 = lanes per (row, sample)
-// for N > 1, bit 4 = 4 lanes automatically on small meshes.  Default 19
-// (config 4, 700k points: N = 1 0.277 -> 0.190 ms, N = 7 1.398 -> 1.279 ms,
-// N = 19 3.53 -> 3.24 ms; config 0: 26.7 -> 18.5 us); HBGPU_MV_VARIANT
-// overrides it (tooling).
+// for N > 1, bit 4 = 4 lanes automatically on small meshes, bit 6 = row records
+// {A, kb, ke} in one load.  Default 83 (config 4, 700k points: N = 1 0.277 ->
+// 0.189 ms, N = 7 1.398 -> 1.261 ms, N = 19 3.53 -> 3.22 ms; config 0: 26.7 ->
+// 14.9 us); HBGPU_MV_VARIANT overrides it (tooling).
 static int mv_variant() {
     const char* e = std::getenv("HBGPU_MV_VARIANT");
-    return e ? std::atoi(e) : 19;
+    return e ? std::atoi(e) : 83;
 }
 
 static int matvec_dev(hbgpu_ctx* c, const double* d_y, double* d_out, const double* d_scale,
@@ -769,6 +777,7 @@ static int matvec_dev(hbgpu_ctx* c, const double* d_y, double* d_out, const doub
         return fail(c, HBGPU_ERR_INVALID, "input-scaled matvec is not supported (scale z on the host side)");
     a.scale_out = d_scale_out;
     a.perm = c->mv_perm.p;
+    a.rows = c->mv_rows.p;
     a.skip = d_skip;
     a.variant = mv_variant();
     a.nn = c->nn;
@@ -1247,6 +1256,7 @@ void hbgpu_destroy(hbgpu_ctx* c) {
             cudaEventDestroy(e);
     c->arn.release();
     c->arn_ctl.release();
+    c->mv_rows.release();
     c->res_ptr.release();
     c->res_node.release();
     c->res_b.release();

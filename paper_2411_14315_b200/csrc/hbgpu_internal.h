@@ -216,6 +216,7 @@ struct MatvecArgs {
     const double* scale;      // optional input scaling (gathered): L (S y)
     const double* scale_out;  // optional output scaling: S L y
     const int* perm;          // optional row order (rows of similar length per CTA)
+    const int4* rows;         // optional {A, row_ptr[A], row_ptr[A+1], 0} in perm order
     const int* skip;          // optional device stop flag (GMRES steps past convergence)
     int nn, N, rows_per_cta;
     int with_c;

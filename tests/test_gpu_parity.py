@@ -371,7 +371,7 @@ def test_singular_tau_is_domain_error(gpu, modes):
         ctx.assemble_residual(s)
 
 
-@pytest.mark.parametrize("variant", [0, 1, 3, 5, 7, 11, 15, 19])
+@pytest.mark.parametrize("variant", [0, 1, 3, 5, 7, 11, 15, 19, 65, 83, 95])
 @pytest.mark.parametrize("modes", [1, 3, 4])
 def test_matvec_kernel_variants(gpu, monkeypatch, modes, variant):
     """Every L-matvec kernel variant (row order, lanes per row) against the
