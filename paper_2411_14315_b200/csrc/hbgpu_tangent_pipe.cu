@@ -152,6 +152,11 @@ size_t tangent_pipe_smem(int max_pack, int max_inc, int max_blk, int N, int NT) 
 // NC > 0: the time-sample count is the compile-time constant NC (and the
 // whole series is one tile), so every N-strided shared/global address folds
 // to an immediate offset; NC = 0 is the generic kernel.
+// TAN_P1_PAIR=1 (two phase-1 items per iteration) measured slower at config 1
+// (0.909 -> 0.938 ms); off.
+#ifndef TAN_P1_PAIR
+#define TAN_P1_PAIR 0
+#endif
 template <int TAU, int THREADS, int NC>
 __global__ void __launch_bounds__(THREADS, 512 / THREADS) tangent_pipe_kernel(TangentArgs a, PipeArgs pa) {
     extern __shared__ __align__(128) unsigned char smraw[];
@@ -270,9 +275,11 @@ __global__ void __launch_bounds__(THREADS, 512 / THREADS) tangent_pipe_kernel(Ta
             o[2] = make_double2(gb0, gb1);
             o[3] = make_double2(gb2, __longlong_as_double((long long)i * 7 * NT));
         }
-        // ---- phase 1: per (incidence, sample) summaries
-        for (int it = threadIdx.x, i = i_start, t = t_start; it < ninc * nt;
-             it += blockDim.x, t += dt, i += di + (t >= nt), t -= (t >= nt ? nt : 0)) {
+        // ---- phase 1: per (incidence, sample) summaries.  TAN_P1_PAIR: two
+        // items per iteration (independent dependency chains for the scheduler;
+        // the second one clamped and not stored past the end)
+        bool bad_acc = false;
+        auto p1item = [&](int i, int t, bool store) {
             const double* gi = tg + i * kTGeo;
             const int2 ic = inc[i];
             const int la = (unsigned)ic.x >> 30;
@@ -341,8 +348,9 @@ __global__ void __launch_bounds__(THREADS, 512 / THREADS) tangent_pipe_kernel(Ta
                 for (int c = 0; c < 3; ++c)
                     kap[c] = fma(c1, usum[c], fma(c2, sA[c * N], kap[c]));
             }
-            if (bad)
-                atomicOr(a.flag, 1);
+            bad_acc |= bad;
+            if (!store)
+                return;
             double* so = summ + (size_t)i * 7 * NT + t;
             const double wr = w * rho;
             so[0] = wr * kap[0];
@@ -352,7 +360,29 @@ __global__ void __launch_bounds__(THREADS, 512 / THREADS) tangent_pipe_kernel(Ta
             so[4 * NT] = w * z[1];
             so[5 * NT] = w * z[2];
             so[6 * NT] = (w / rho) * tsum;
+                };
+#if TAN_P1_PAIR
+        {
+            const int total = ninc * nt, step = blockDim.x;
+            int i = i_start, t = t_start;
+            for (int it = threadIdx.x; it < total; it += 2 * step) {
+                int t2 = t + dt, i2 = i + di + (t2 >= nt);
+                t2 -= (t2 >= nt ? nt : 0);
+                const bool v2 = it + step < total;
+                p1item(i, t, true);
+                p1item(v2 ? i2 : i, v2 ? t2 : t, v2);
+                t = t2 + dt;
+                i = i2 + di + (t >= nt);
+                t -= (t >= nt ? nt : 0);
+            }
         }
+#else
+        for (int it = threadIdx.x, i = i_start, t = t_start; it < ninc * nt;
+             it += blockDim.x, t += dt, i += di + (t >= nt), t -= (t >= nt ? nt : 0))
+            p1item(i, t, true);
+#endif
+        if (bad_acc)
+            atomicOr(a.flag, 1);
         __syncthreads();
 
         if (warp == 0 && more) {
