@@ -152,6 +152,10 @@ size_t tangent_pipe_smem(int max_pack, int max_inc, int max_blk, int N, int NT) 
 // NC > 0: the time-sample count is the compile-time constant NC (and the
 // whole series is one tile), so every N-strided shared/global address folds
 // to an immediate offset; NC = 0 is the generic kernel.
+#ifndef TAN_P2_UNROLL
+#define TAN_P2_UNROLL 1
+#endif
+constexpr int kTanP2Unroll = TAN_P2_UNROLL;  // phase-2 contribution loop unroll (1: 0.899 ms, 2: 0.909, 4: 0.901 at config 1)
 // TAN_P1_PAIR=1 (two phase-1 items per iteration) measured slower at config 1
 // (0.909 -> 0.938 ms); off.
 #ifndef TAN_P1_PAIR
@@ -397,7 +401,7 @@ __global__ void __launch_bounds__(THREADS, 512 / THREADS) tangent_pipe_kernel(Ta
             const int j = info.z;
             const bool bfix = info.w != 0;
             double K = 0.0, G0 = 0.0, G1 = 0.0, G2 = 0.0, D0 = 0.0, D1 = 0.0, D2 = 0.0, L = 0.0;
-#pragma unroll 2
+#pragma unroll kTanP2Unroll
             for (int p = info.x; p < info.y; ++p) {
                 const double2* rp = reinterpret_cast<const double2*>(rec + p * 8);
                 const double2 ra = rp[0], rb = rp[1], rc = rp[2], rd = rp[3];
