@@ -1403,6 +1403,12 @@ int hbgpu_set_basis(hbgpu_ctx* c, int modes, double period) {
                         b.nt = N;
                     }
                 }
+                // tooling: HBGPU_TAN_WIDTH forces the CTA width of every pipe bucket
+                if (const char* tw = std::getenv("HBGPU_TAN_WIDTH")) {
+                    const int w = std::atoi(tw);
+                    if (b.pipe && std::find(widths, widths + 5, w) != widths + 5 && ps(N) <= size_t(227 * 1024))
+                        b.threads = w;
+                }
                 if (!b.pipe) {
                     int nt = N;
                     while (nt > 1 && ps(nt) > size_t(226 * 1024))
