@@ -443,7 +443,7 @@ size_t residual_smem_bytes(int max_nloc, int max_rpack, int T) {
 
 // T = time samples per tile (4; 1 when N is small, where a 4-sample tile would
 // leave most threads idle — the host picks it, residual_tile()).
-template <int T>
+template <int T, bool SUMM>
 __global__ void __launch_bounds__(kChunkElems * T, RES_MINB * 4 / T) residual_chunk_kernel(ResidualChunkArgs a) {
     extern __shared__ __align__(128) unsigned char smraw[];
     constexpr int CE = kChunkElems, ndst = 7 * T, es = 29 * T;
@@ -532,7 +532,7 @@ __global__ void __launch_bounds__(kChunkElems * T, RES_MINB * 4 / T) residual_ch
                                        int(pkc >> 24)};
                     element_residual_smem(geo + el * kTGeo, nd, ndst, lc, T, t, a.rho, a.mu, a.nu,
                                           a.tau_mode, a.flag, slots + el * es + t);
-                    if (a.summ)
+                    if (SUMM)  // separate pass: inlining it into the residual's pass 2 spilled 248 B
                         element_tangent_summary_smem(geo + el * kTGeo, nd, ndst, lc, T, t, a.rho, a.nu, a.tau_mode,
                                                      a.flag,
                                                      a.summ + ((size_t)(ch * CE + el) * 16) * a.summ_ns + n0 + t,
@@ -570,27 +570,41 @@ int residual_tile(int N) {
     return 1;
 }
 
+template <bool SUMM>
+static void launch_res_t(const ResidualChunkArgs& a, int g, int T, size_t sm, cudaStream_t st) {
+    if (T == 4)
+        residual_chunk_kernel<4, SUMM><<<g, kChunkElems * 4, sm, st>>>(a);
+    else if (T == 2)
+        residual_chunk_kernel<2, SUMM><<<g, kChunkElems * 2, sm, st>>>(a);
+    else
+        residual_chunk_kernel<1, SUMM><<<g, kChunkElems, sm, st>>>(a);
+}
+
 void launch_residual_chunks(const ResidualChunkArgs& a, int grid, int T, cudaStream_t st) {
     if (a.nchunks <= 0)
         return;
     note_launch();
     const size_t sm = residual_smem_bytes(a.max_nloc, a.max_rpack, T);
     const int g = min(grid, a.nchunks);
-    if (T == 4)
-        residual_chunk_kernel<4><<<g, kChunkElems * 4, sm, st>>>(a);
-    else if (T == 2)
-        residual_chunk_kernel<2><<<g, kChunkElems * 2, sm, st>>>(a);
+    if (a.summ)
+        launch_res_t<true>(a, g, T, sm, st);
     else
-        residual_chunk_kernel<1><<<g, kChunkElems, sm, st>>>(a);
+        launch_res_t<false>(a, g, T, sm, st);
+}
+
+template <bool SUMM>
+static cudaError_t configure_res_t(int b, int T) {
+    if (T == 4)
+        return cudaFuncSetAttribute(residual_chunk_kernel<4, SUMM>, cudaFuncAttributeMaxDynamicSharedMemorySize, b);
+    if (T == 2)
+        return cudaFuncSetAttribute(residual_chunk_kernel<2, SUMM>, cudaFuncAttributeMaxDynamicSharedMemorySize, b);
+    return cudaFuncSetAttribute(residual_chunk_kernel<1, SUMM>, cudaFuncAttributeMaxDynamicSharedMemorySize, b);
 }
 
 cudaError_t configure_residual_smem(size_t bytes, int T) {
     const int b = int(bytes < 48 * 1024 ? 48 * 1024 : bytes);
-    if (T == 4)
-        return cudaFuncSetAttribute(residual_chunk_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, b);
-    if (T == 2)
-        return cudaFuncSetAttribute(residual_chunk_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, b);
-    return cudaFuncSetAttribute(residual_chunk_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, b);
+    const cudaError_t e = configure_res_t<false>(b, T);
+    return e != cudaSuccess ? e : configure_res_t<true>(b, T);
 }
 
 // Node pass: sums the node's chunk partials in chunk order, completes the
@@ -1022,9 +1036,9 @@ cudaError_t run_fp64_peak(int blocks, int threads, int iters, double* out, float
 namespace hbgpu {
 cudaError_t residual_occupancy(int* blocks_per_sm, size_t smem, int T) {
     if (T == 4)
-        return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, residual_chunk_kernel<4>, kChunkElems * 4, smem);
+        return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, residual_chunk_kernel<4, false>, kChunkElems * 4, smem);
     if (T == 2)
-        return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, residual_chunk_kernel<2>, kChunkElems * 2, smem);
-    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, residual_chunk_kernel<1>, kChunkElems, smem);
+        return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, residual_chunk_kernel<2, false>, kChunkElems * 2, smem);
+    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, residual_chunk_kernel<1, false>, kChunkElems, smem);
 }
 }  // namespace hbgpu
