@@ -340,8 +340,10 @@ static int upload_all(hbgpu_ctx* c, const hbgpu_mesh_desc* d) {
         for (int A = 0; A < nn; ++A)
             perm[size_t(A)] = A;
         const int* rp = c->row_ptr_h.data();
-        for (int w0 = 0; w0 < nn; w0 += 4096) {
-            const int w1 = std::min(nn, w0 + 4096);
+        const char* pw = std::getenv("HBGPU_MV_WINDOW");  // tooling: window length
+        const int win = pw ? std::max(1, std::atoi(pw)) : 4096;
+        for (int w0 = 0; w0 < nn; w0 += win) {
+            const int w1 = std::min(nn, w0 + win);
             std::stable_sort(perm.begin() + w0, perm.begin() + w1, [rp](int x, int y) {
                 return rp[x + 1] - rp[x] > rp[y + 1] - rp[y];
             });
