@@ -561,3 +561,28 @@ def test_all_dirichlet_boundary(gpu):
     assert rel(p, orc.tangent(s)) < TOL
     y = cases.random_state(mesh.num_nodes, N, 52)
     assert rel(ctx.matvec(y), orc.matvec(p, orc.mass(), y)) < TOL
+
+
+@pytest.mark.parametrize("restart", [8, 600, 1000])
+def test_gmres_device_and_host_loops(gpu, monkeypatch, restart):
+    """The device-resident GMRES cycle (batched steps, device Arnoldi kernel;
+    restart 600 needs the large shared-memory opt-in) and the host-driven loop
+    (restart 1000 exceeds the Arnoldi kernel's shared memory; HBGPU_GMRES_HOST
+    forces it) reach the same solution, iteration counts and history."""
+    from paper_2411_14315_b200.hbgpu import KrylovConfig
+
+    prob = tube_problem(3, h=0.25, traction=False)
+    ctx = gpu_ctx(prob, 0, 0.3)
+    s = cases.random_state(prob.mesh.num_nodes, prob.N, 61, 0.5)
+    ctx.assemble_tangent(s)
+    ctx.jacobi()
+    b = cases.random_state(prob.mesh.num_nodes, prob.N, 62)
+    cfg = KrylovConfig(restart=restart, max_iters=400, tolerance=1e-9)
+    dev = ctx.gmres(b, cfg)
+    monkeypatch.setenv("HBGPU_GMRES_HOST", "1")
+    host = ctx.gmres(b, cfg)
+    assert dev.status == host.status
+    assert abs(dev.iterations - host.iterations) <= 1
+    assert rel(dev.x, host.x) < 1e-7
+    n = min(len(dev.history), len(host.history))
+    assert n > 1 and np.allclose(dev.history[:n], host.history[:n], rtol=1e-6, atol=1e-14)
