@@ -6,6 +6,7 @@
 #include "hbgpu_internal.h"
 
 #include <algorithm>
+#include <cstdlib>
 
 namespace hbgpu {
 
@@ -504,14 +505,13 @@ __device__ __forceinline__ double warp_sum(double v) {
     return v;  // lane 0
 }
 
-__global__ void __launch_bounds__(kArnThreads) arnoldi_step_kernel(ArnoldiDev d, int j, int last,
-                                                                   const double* __restrict__ red,
-                                                                   const double* __restrict__ d_norm,
-                                                                   double* __restrict__ coef, double bnorm,
-                                                                   double tol) {
-    if (*d.ctl)
+__device__ __forceinline__ void arnoldi_step_body(const ArnoldiDev& d, int j, int last,
+                                                  const double* __restrict__ red,
+                                                  const double* __restrict__ d_norm,
+                                                  double* __restrict__ coef, double bnorm, double tol,
+                                                  double* __restrict__ sh) {
+    if (*(volatile int*)d.ctl)
         return;
-    extern __shared__ double sh[];
     const int m = d.m, ldh = m + 1;    // H row-major: H(i, l) = Hm[i * ldh + l]
     const size_t ldr = (size_t)m + 2;  // R column-major
     double* av = sh;                   // j
@@ -666,6 +666,15 @@ __global__ void __launch_bounds__(kArnThreads) arnoldi_step_kernel(ArnoldiDev d,
         if (j == 0)
             d.gv[0] *= rho;  // V_0 renormalised by its computed norm in the update pass
     }
+}
+
+__global__ void __launch_bounds__(kArnThreads) arnoldi_step_kernel(ArnoldiDev d, int j, int last,
+                                                                   const double* __restrict__ red,
+                                                                   const double* __restrict__ d_norm,
+                                                                   double* __restrict__ coef, double bnorm,
+                                                                   double tol) {
+    extern __shared__ double sh[];
+    arnoldi_step_body(d, j, last, red, d_norm, coef, bnorm, tol, sh);
 }
 
 void launch_arnoldi_step(const ArnoldiDev& d, int j, int last, const double* red, const double* d_norm,
