@@ -1342,6 +1342,11 @@ int hbgpu_set_basis(hbgpu_ctx* c, int modes, double period) {
         CK(c, b->alloc(n));
     CK(c, c->hu.alloc(size_t(c->nn) * 3 * size_t(N)));
     c->res_tile = residual_tile(N);
+    if (const char* rt = std::getenv("HBGPU_RES_TILE")) {  // tooling: 1, 2 or 4 samples per tile
+        const int t = std::atoi(rt);
+        if (t == 1 || t == 2 || t == 4)
+            c->res_tile = t;
+    }
     CK(c, c->rpartial.alloc(size_t(c->npairs) * 7 * size_t((N + c->res_tile - 1) / c->res_tile) * c->res_tile));
     {
         const size_t rs = residual_smem_bytes(c->max_nloc, c->max_rpack, c->res_tile);

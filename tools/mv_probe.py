@@ -17,7 +17,8 @@ variants = (sys.argv[3] if len(sys.argv) > 3 else "0").split(",")
 reps = 100
 t0 = time.perf_counter()
 mesh = (meshgen.hex_cylinder(0.3, 6.0, 20, 20, 120) if arg == "pipe" else
-        meshgen.hex_cylinder(0.3, 6.0, 10, 10, 60) if arg == "pipe0" else meshgen.cube_delaunay(int(arg), seed=4))
+        meshgen.hex_cylinder(0.3, 6.0, 10, 10, 60) if arg == "pipe0" else
+        meshgen.config_mesh(int(arg[3:])) if arg.startswith("cfg") else meshgen.cube_delaunay(int(arg), seed=4))
 tm = time.perf_counter() - t0
 
 
