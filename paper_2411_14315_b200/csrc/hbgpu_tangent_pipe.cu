@@ -152,6 +152,9 @@ size_t tangent_pipe_smem(int max_pack, int max_inc, int max_blk, int N, int NT) 
 // NC > 0: the time-sample count is the compile-time constant NC (and the
 // whole series is one tile), so every N-strided shared/global address folds
 // to an immediate offset; NC = 0 is the generic kernel.
+#ifndef TAN_SUMM_CMAJOR
+#define TAN_SUMM_CMAJOR 1
+#endif
 #ifndef TAN_P2_UNROLL
 #define TAN_P2_UNROLL 1
 #endif
@@ -167,6 +170,9 @@ __global__ void __launch_bounds__(THREADS, 512 / THREADS) tangent_pipe_kernel(Ta
     const int N = NC ? NC : a.N, NT = NC ? NC : a.NT;
     const int n0 = NC ? 0 : blockIdx.y * NT, nt = NC ? NC : min(NT, N - n0);
     const PipeSmem Ls = pipe_layout(pa.max_pack, a.max_inc, a.max_blk, N, NT);
+    // summary layout: TAN_SUMM_CMAJOR = component-major [c][i][t] (item-contiguous
+    // stores in phase 1), else incidence-major [i][c][t]
+    const int SI = TAN_SUMM_CMAJOR ? NT : 7 * NT, SC = TAN_SUMM_CMAJOR ? a.max_inc * NT : NT;
     const int mpack = pack_align16(pa.max_pack);
     uint64_t* mbar = reinterpret_cast<uint64_t*>(smraw + Ls.mbar);  // [0..1] packs, [2] gathers
     double* summ = reinterpret_cast<double*>(smraw + Ls.summ);
@@ -277,7 +283,7 @@ __global__ void __launch_bounds__(THREADS, 512 / THREADS) tangent_pipe_kernel(Ta
             o[0] = make_double2(ga0, ga1);
             o[1] = make_double2(ga2, fma(ga0, gb0, fma(ga1, gb1, ga2 * gb2)));
             o[2] = make_double2(gb0, gb1);
-            o[3] = make_double2(gb2, __longlong_as_double((long long)i * 7 * NT));
+            o[3] = make_double2(gb2, __longlong_as_double((long long)i * SI));
         }
         // ---- phase 1: per (incidence, sample) summaries.  TAN_P1_PAIR: two
         // items per iteration (independent dependency chains for the scheduler;
@@ -355,15 +361,15 @@ __global__ void __launch_bounds__(THREADS, 512 / THREADS) tangent_pipe_kernel(Ta
             bad_acc |= bad;
             if (!store)
                 return;
-            double* so = summ + (size_t)i * 7 * NT + t;
+            double* so = summ + (size_t)i * SI + t;
             const double wr = w * rho;
             so[0] = wr * kap[0];
-            so[NT] = wr * kap[1];
-            so[2 * NT] = wr * kap[2];
-            so[3 * NT] = w * z[0];
-            so[4 * NT] = w * z[1];
-            so[5 * NT] = w * z[2];
-            so[6 * NT] = (w / rho) * tsum;
+            so[1 * SC] = wr * kap[1];
+            so[2 * SC] = wr * kap[2];
+            so[3 * SC] = w * z[0];
+            so[4 * SC] = w * z[1];
+            so[5 * SC] = w * z[2];
+            so[6 * SC] = (w / rho) * tsum;
                 };
 #if TAN_P1_PAIR
         {
@@ -407,10 +413,10 @@ __global__ void __launch_bounds__(THREADS, 512 / THREADS) tangent_pipe_kernel(Ta
                 const double2 ra = rp[0], rb = rp[1], rc = rp[2], rd = rp[3];
                 const double* sp = summ + __double_as_longlong(rd.y) + t;
                 const double gb0 = rc.x, gb1 = rc.y, gb2 = rd.x;
-                K = fma(sp[0], gb0, fma(sp[NT], gb1, fma(sp[2 * NT], gb2, K)));
+                K = fma(sp[0], gb0, fma(sp[SC], gb1, fma(sp[2 * SC], gb2, K)));
                 // w alpha_a = (w z) . dN_a (phase 1 stores w z only: one shared
                 // load fewer per contribution; phase 2 is shared-memory bound)
-                const double z0 = sp[3 * NT], z1 = sp[4 * NT], z2 = sp[5 * NT];
+                const double z0 = sp[3 * SC], z1 = sp[4 * SC], z2 = sp[5 * SC];
                 const double al = fma(z0, ra.x, fma(z1, ra.y, z2 * rb.x));
                 G0 = fma(al, gb0, G0);
                 G1 = fma(al, gb1, G1);
@@ -419,7 +425,7 @@ __global__ void __launch_bounds__(THREADS, 512 / THREADS) tangent_pipe_kernel(Ta
                 D0 = fma(ra.x, alb, D0);
                 D1 = fma(ra.y, alb, D1);
                 D2 = fma(rb.x, alb, D2);
-                L = fma(rb.y, sp[6 * NT], L);
+                L = fma(rb.y, sp[6 * SC], L);
             }
             if (slot >= dparts || slot == 0) {
                 const double2* bc = reinterpret_cast<const double2*>(blkc + j * 8);
