@@ -423,6 +423,13 @@ void residual_pack_write(unsigned char* dst, int nloc, int ecount, int nb, const
     memcpy(dst + s.lconn, lconn, sizeof(uint32_t) * (size_t)ecount);
 }
 
+// shared-memory node-record stride of the residual tiles: 7T doubles, padded
+// to 7T + 1 for T = 4 so the 8 node records a warp reads start on spread banks
+#ifndef RES_ND_PAD
+#define RES_ND_PAD 1
+#endif
+__host__ __device__ constexpr int res_nd_stride(int T) { return 7 * T + ((T == 4 && RES_ND_PAD) ? 1 : 0); }
+
 struct ResSmem {
     int pk, geo, nd, slots, mbar, total;  // byte offsets
 };
@@ -432,7 +439,7 @@ __host__ __device__ inline ResSmem res_layout(int max_nloc, int max_rpack, int T
     L.pk = 0;                                              // 2 x max_rpack
     L.geo = L.pk + 2 * rp_align16(max_rpack);              // 2 x [CE][kTGeo]
     L.nd = L.geo + 2 * CE * kTGeo * 8;                     // 2 x [nloc][7][T]
-    L.slots = L.nd + 2 * max_nloc * 7 * T * 8;             // [CE][29T]
+    L.slots = L.nd + 2 * max_nloc * res_nd_stride(T) * 8;  // [CE][29T]
     L.mbar = L.slots + CE * 29 * T * 8;
     L.total = L.mbar + 16;
     return L;
@@ -446,7 +453,7 @@ size_t residual_smem_bytes(int max_nloc, int max_rpack, int T) {
 template <int T, bool SUMM>
 __global__ void __launch_bounds__(kChunkElems * T, RES_MINB * 4 / T) residual_chunk_kernel(ResidualChunkArgs a) {
     extern __shared__ __align__(128) unsigned char smraw[];
-    constexpr int CE = kChunkElems, ndst = 7 * T, es = 29 * T;
+    constexpr int CE = kChunkElems, ndst = 7 * T, es = 29 * T, nds = res_nd_stride(T);
     const int N = a.N, nch = a.nchunks;
     const int ntiles = (N + T - 1) / T;
     const ResSmem Ls = res_layout(a.max_nloc, a.max_rpack, T);
@@ -477,13 +484,13 @@ __global__ void __launch_bounds__(kChunkElems * T, RES_MINB * 4 / T) residual_ch
         const int nloc = h[0];
         const ResPackSec s = res_pack_sections(nloc, h[1]);
         const int* nodes = reinterpret_cast<const int*>(pk + s.nodes);
-        double* nd = reinterpret_cast<double*>(smraw + Ls.nd) + (size_t)b * a.max_nloc * ndst;
+        double* nd = reinterpret_cast<double*>(smraw + Ls.nd) + (size_t)b * a.max_nloc * nds;
         const int n0 = tile * T;
         for (int k = threadIdx.x; k < nloc * 7; k += blockDim.x) {
             const int ln = k / 7, cc = k - 7 * ln;
             const long A = nodes[ln];
             const double* src = cc < 4 ? a.state + (A * 4 + cc) * N + n0 : a.hu + (A * 3 + (cc - 4)) * N + n0;
-            double* dst = nd + ln * ndst + cc * T;
+            double* dst = nd + ln * nds + cc * T;
 #pragma unroll
             for (int t = 0; t < T; ++t) {
                 if (n0 + t < N)
@@ -523,17 +530,17 @@ __global__ void __launch_bounds__(kChunkElems * T, RES_MINB * 4 / T) residual_ch
                 issue_tile(ps ^ 1, 0, b ^ 1);
             }
             cp_async_commit();
-            const double* nd = reinterpret_cast<const double*>(smraw + Ls.nd) + (size_t)b * a.max_nloc * ndst;
+            const double* nd = reinterpret_cast<const double*>(smraw + Ls.nd) + (size_t)b * a.max_nloc * nds;
             {
                 const int el = threadIdx.x / T, t = threadIdx.x - el * T;
                 if (el < ecount && n0 + t < N) {
                     const uint32_t pkc = lconn[el];
                     const int lc[4] = {int(pkc & 0xFF), int((pkc >> 8) & 0xFF), int((pkc >> 16) & 0xFF),
                                        int(pkc >> 24)};
-                    element_residual_smem(geo + el * kTGeo, nd, ndst, lc, T, t, a.rho, a.mu, a.nu,
+                    element_residual_smem(geo + el * kTGeo, nd, nds, lc, T, t, a.rho, a.mu, a.nu,
                                           a.tau_mode, a.flag, slots + el * es + t);
                     if (SUMM)  // separate pass: inlining it into the residual's pass 2 spilled 248 B
-                        element_tangent_summary_smem(geo + el * kTGeo, nd, ndst, lc, T, t, a.rho, a.nu, a.tau_mode,
+                        element_tangent_summary_smem(geo + el * kTGeo, nd, nds, lc, T, t, a.rho, a.nu, a.tau_mode,
                                                      a.flag,
                                                      a.summ + ((size_t)(ch * CE + el) * 16) * a.summ_ns + n0 + t,
                                                      a.summ_ns);
