@@ -126,6 +126,21 @@ void launch_tangent_pack_refresh(unsigned char* pack, const int* pack_ptr, int n
 
 // ---------------------------------------------------------------- kernel
 
+// contribution-record stride (doubles): 8 used, padded to 10 so the two records a
+// warp's halves read in phase 2 do not fall on the same banks (TAN_REC_STRIDE)
+// neighbour state records in shared memory: 4N doubles, padded (even, keeps the
+// 16-byte bulk-copy alignment) to spread their bank offsets
+#ifndef TAN_SU_PAD
+#define TAN_SU_PAD 0
+#endif
+#ifndef TAN_SUMM_PAD
+#define TAN_SUMM_PAD 0
+#endif
+#ifndef TAN_REC_STRIDE
+#define TAN_REC_STRIDE 10
+#endif
+constexpr int kRecStride = TAN_REC_STRIDE;
+
 struct PipeSmem {
     int meta, su, tg, summ, rec, dpart, mbar, total;  // byte offsets
 };
@@ -134,10 +149,10 @@ __host__ __device__ inline PipeSmem pipe_layout(int max_pack, int mi, int max_bl
     const int dpmax = (mi + kTanPart - 1) / kTanPart;
     L.meta = 0;                                                   // 2 x max_pack
     L.su = L.meta + 2 * pack_align16(max_pack);                   // [blk][4N]
-    L.tg = L.su + max_blk * 4 * N * 8;                            // [inc][20]
+    L.tg = L.su + max_blk * (4 * N + TAN_SU_PAD) * 8;             // [inc][20]
     L.summ = L.tg + mi * kTGeo * 8;                               // [i][8][NT]
-    L.rec = L.summ + ((mi * 7 * NT + 1) & ~1) * 8;                // [p][8]
-    L.dpart = L.rec + 4 * mi * 64;                                // [part][8][NT]
+    L.rec = L.summ + ((mi * 7 * (NT + TAN_SUMM_PAD) + 1) & ~1) * 8;  // [p][8]
+    L.dpart = L.rec + 4 * mi * kRecStride * 8;                    // [part][8][NT]
     L.mbar = pack_align16(L.dpart + dpmax * 8 * NT * 8);          // 3 mbarriers
     L.total = L.mbar + 32;
     return L;
@@ -172,7 +187,7 @@ __global__ void __launch_bounds__(THREADS, 512 / THREADS) tangent_pipe_kernel(Ta
     const PipeSmem Ls = pipe_layout(pa.max_pack, a.max_inc, a.max_blk, N, NT);
     // summary layout: TAN_SUMM_CMAJOR = component-major [c][i][t] (item-contiguous
     // stores in phase 1), else incidence-major [i][c][t]
-    const int SI = TAN_SUMM_CMAJOR ? NT : 7 * NT, SC = TAN_SUMM_CMAJOR ? a.max_inc * NT : NT;
+    const int SI = TAN_SUMM_CMAJOR ? NT + TAN_SUMM_PAD : 7 * NT, SC = TAN_SUMM_CMAJOR ? a.max_inc * SI : NT;
     const int mpack = pack_align16(pa.max_pack);
     uint64_t* mbar = reinterpret_cast<uint64_t*>(smraw + Ls.mbar);  // [0..1] packs, [2] gathers
     double* summ = reinterpret_cast<double*>(smraw + Ls.summ);
@@ -210,7 +225,7 @@ __global__ void __launch_bounds__(THREADS, 512 / THREADS) tangent_pipe_kernel(Ta
             mbar_expect_tx(mbar + 2, (uint32_t)(nblk * 4 * N * 8 + ninc * kTGeo * 8));
         __syncwarp();
         for (int j = lane; j < nblk; j += 32)
-            bulk_g2s(su + (size_t)j * 4 * N, a.state + (size_t)cols[j] * 4 * N, 4 * N * 8, mbar + 2);
+            bulk_g2s(su + (size_t)j * (4 * N + TAN_SU_PAD), a.state + (size_t)cols[j] * 4 * N, 4 * N * 8, mbar + 2);
         for (int i = lane; i < ninc; i += 32)
             bulk_g2s(tg + (size_t)i * kTGeo, a.tgeom + (size_t)(inc[i].x & 0x3FFFFFFF) * kTGeo,
                      kTGeo * 8, mbar + 2);
@@ -279,7 +294,7 @@ __global__ void __launch_bounds__(THREADS, 512 / THREADS) tangent_pipe_kernel(Ta
             const double* gi = tg + i * kTGeo;
             const double ga0 = gi[3 * la], ga1 = gi[3 * la + 1], ga2 = gi[3 * la + 2];
             const double gb0 = gi[3 * b], gb1 = gi[3 * b + 1], gb2 = gi[3 * b + 2];
-            double2* o = reinterpret_cast<double2*>(rec + p * 8);
+            double2* o = reinterpret_cast<double2*>(rec + p * kRecStride);
             o[0] = make_double2(ga0, ga1);
             o[1] = make_double2(ga2, fma(ga0, gb0, fma(ga1, gb1, ga2 * gb2)));
             o[2] = make_double2(gb0, gb1);
@@ -310,7 +325,7 @@ __global__ void __launch_bounds__(THREADS, 512 / THREADS) tangent_pipe_kernel(Ta
             double u[4][3], usum[3] = {0.0, 0.0, 0.0};
 #pragma unroll
             for (int b = 0; b < 4; ++b) {
-                const double* sb = su + (size_t)((cols >> (8 * b)) & 0xFFu) * 4 * N + n;
+                const double* sb = su + (size_t)((cols >> (8 * b)) & 0xFFu) * (4 * N + TAN_SU_PAD) + n;
 #pragma unroll
                 for (int c = 0; c < 3; ++c) {
                     u[b][c] = sb[c * N];
@@ -353,7 +368,7 @@ __global__ void __launch_bounds__(THREADS, 512 / THREADS) tangent_pipe_kernel(Ta
             }
             // + sum_q N_a(q) u_q = B usum + (A-B) u_{q=a} = c1 usum + c2 u_A (u_A: the row node)
             {
-                const double* sA = su + (size_t)kdiag * 4 * N + n;
+                const double* sA = su + (size_t)kdiag * (4 * N + TAN_SU_PAD) + n;
 #pragma unroll
                 for (int c = 0; c < 3; ++c)
                     kap[c] = fma(c1, usum[c], fma(c2, sA[c * N], kap[c]));
@@ -409,7 +424,7 @@ __global__ void __launch_bounds__(THREADS, 512 / THREADS) tangent_pipe_kernel(Ta
             double K = 0.0, G0 = 0.0, G1 = 0.0, G2 = 0.0, D0 = 0.0, D1 = 0.0, D2 = 0.0, L = 0.0;
 #pragma unroll kTanP2Unroll
             for (int p = info.x; p < info.y; ++p) {
-                const double2* rp = reinterpret_cast<const double2*>(rec + p * 8);
+                const double2* rp = reinterpret_cast<const double2*>(rec + p * kRecStride);
                 const double2 ra = rp[0], rb = rp[1], rc = rp[2], rd = rp[3];
                 const double* sp = summ + __double_as_longlong(rd.y) + t;
                 const double gb0 = rc.x, gb1 = rc.y, gb2 = rd.x;
