@@ -425,6 +425,9 @@ void residual_pack_write(unsigned char* dst, int nloc, int ecount, int nb, const
 
 // shared-memory node-record stride of the residual tiles: 7T doubles, padded
 // to 7T + 1 for T = 4 so the 8 node records a warp reads start on spread banks
+#ifndef RES_GATHER_LINEAR
+#define RES_GATHER_LINEAR 1
+#endif
 #ifndef RES_ND_PAD
 #define RES_ND_PAD 1
 #endif
@@ -486,6 +489,21 @@ __global__ void __launch_bounds__(kChunkElems * T, RES_MINB * 4 / T) residual_ch
         const int* nodes = reinterpret_cast<const int*>(pk + s.nodes);
         double* nd = reinterpret_cast<double*>(smraw + Ls.nd) + (size_t)b * a.max_nloc * nds;
         const int n0 = tile * T;
+#if RES_GATHER_LINEAR
+        // thread per (node, component, sample), sample fastest: a warp's shared
+        // stores are one contiguous run (the per-(node, component) mapping put
+        // consecutive threads 4 doubles apart: 8-way bank conflicts)
+        for (int k = threadIdx.x; k < nloc * 7 * T; k += blockDim.x) {
+            const int ln = k / (7 * T), rem = k - ln * 7 * T, cc = rem / T, t = rem - cc * T;
+            const long A = nodes[ln];
+            const double* src = cc < 4 ? a.state + (A * 4 + cc) * N + n0 : a.hu + (A * 3 + (cc - 4)) * N + n0;
+            double* dst = nd + ln * nds + rem;
+            if (n0 + t < N)
+                cp_async8(dst, src + t);
+            else
+                *dst = 0.0;
+        }
+#else
         for (int k = threadIdx.x; k < nloc * 7; k += blockDim.x) {
             const int ln = k / 7, cc = k - 7 * ln;
             const long A = nodes[ln];
@@ -499,6 +517,7 @@ __global__ void __launch_bounds__(kChunkElems * T, RES_MINB * 4 / T) residual_ch
                     dst[t] = 0.0;
             }
         }
+#endif
     };
 
     if (threadIdx.x == 0)
