@@ -426,7 +426,7 @@ void residual_pack_write(unsigned char* dst, int nloc, int ecount, int nb, const
 // shared-memory node-record stride of the residual tiles: 7T doubles, padded
 // to 7T + 1 for T = 4 so the 8 node records a warp reads start on spread banks
 #ifndef RES_GATHER_LINEAR
-#define RES_GATHER_LINEAR 1
+#define RES_GATHER_LINEAR 2
 #endif
 #ifndef RES_ND_PAD
 #define RES_ND_PAD 1
@@ -489,7 +489,23 @@ __global__ void __launch_bounds__(kChunkElems * T, RES_MINB * 4 / T) residual_ch
         const int* nodes = reinterpret_cast<const int*>(pk + s.nodes);
         double* nd = reinterpret_cast<double*>(smraw + Ls.nd) + (size_t)b * a.max_nloc * nds;
         const int n0 = tile * T;
-#if RES_GATHER_LINEAR
+#if RES_GATHER_LINEAR == 2
+        // thread per (node, component, sample pair): stores 16 B apart
+        constexpr int P = (T % 2 == 0) ? 2 : 1, TG = T / P;
+        for (int k = threadIdx.x; k < nloc * 7 * TG; k += blockDim.x) {
+            const int ln = k / (7 * TG), rem = k - ln * 7 * TG, cc = rem / TG, t = P * (rem - cc * TG);
+            const long A = nodes[ln];
+            const double* src = cc < 4 ? a.state + (A * 4 + cc) * N + n0 : a.hu + (A * 3 + (cc - 4)) * N + n0;
+            double* dst = nd + ln * nds + cc * T + t;
+#pragma unroll
+            for (int q = 0; q < P; ++q) {
+                if (n0 + t + q < N)
+                    cp_async8(dst + q, src + t + q);
+                else
+                    dst[q] = 0.0;
+            }
+        }
+#elif RES_GATHER_LINEAR
         // thread per (node, component, sample), sample fastest: a warp's shared
         // stores are one contiguous run (the per-(node, component) mapping put
         // consecutive threads 4 doubles apart: 8-way bank conflicts)
