@@ -154,6 +154,36 @@ def test_delaunay_cube_operator(gpu, modes):
     assert np.array_equal(ci, orc.col_idx)
 
 
+@pytest.mark.parametrize("tile", ["1", "2", "4"])
+@pytest.mark.parametrize("modes", [2, 4, 10])
+def test_residual_tile_widths(gpu, monkeypatch, tile, modes):
+    """Every residual tile width (samples per tile; HBGPU_RES_TILE, read when
+    the basis is set) against the oracle, including partial last tiles
+    (N = 3, 7, 19) and the sample-pair gathers of the even widths."""
+    from paper_2411_14315_b200 import meshgen
+
+    monkeypatch.setenv("HBGPU_RES_TILE", tile)
+    mesh = meshgen.cube_delaunay(3000, seed=9)
+    N = 2 * modes - 1
+    neu = [(k, np.full(N, 50.0)) for k, p in enumerate(mesh.patches) if p.kind == NEUMANN]
+    prob = Problem(mesh, modes, 1.0, 1.06, 0.04, np.zeros(mesh.num_nodes * 3 * N), neu, 0.2)
+    ctx = gpu_ctx(prob, 0, 0.05)
+    orc = ob.Restated(prob, tau_mode=0, pseudo_dt=0.05)
+    s = cases.random_modes_state(mesh.num_nodes, modes, 13)
+    assert rel(ctx.assemble_residual(s), orc.residual(s)) < TOL
+
+
+@pytest.mark.parametrize("width", ["64", "256"])
+def test_tangent_pipe_widths(gpu, monkeypatch, width):
+    """The persistent tangent pipeline at forced CTA widths (HBGPU_TAN_WIDTH)."""
+    monkeypatch.setenv("HBGPU_TAN_WIDTH", width)
+    prob = tube_problem(4)
+    ctx = gpu_ctx(prob, 0, 0.3)
+    orc = ob.Restated(prob, tau_mode=0, pseudo_dt=0.3)
+    s = cases.random_modes_state(prob.mesh.num_nodes, 4, 17)
+    assert rel(ctx.assemble_tangent(s), orc.tangent(s)) < TOL
+
+
 @pytest.mark.parametrize("mesh_kind,modes,tau", [("tube", 3, 0), ("tube", 4, 1), ("delaunay", 4, 0),
                                                   ("delaunay", 24, 0)])
 def test_tangent_row_kernel_fallback(gpu, monkeypatch, mesh_kind, modes, tau):
