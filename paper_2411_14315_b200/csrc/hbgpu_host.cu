@@ -960,7 +960,7 @@ static int gmres_dev(hbgpu_ctx* c, const double* d_rhs, const double* d_inv,
             // runs in arnoldi_step_kernel, so steps are enqueued in batches of
             // kBatch with no host round trip; the host polls the stop flag one
             // batch behind (steps enqueued past a stop return at once).
-            constexpr int kBatch = 8;
+            const int kBatch = std::getenv("HBGPU_GMRES_BATCH") ? std::max(1, std::atoi(std::getenv("HBGPU_GMRES_BATCH"))) : 8;
             const int it0 = res->iterations;
             launch_arnoldi_init(ad, rnorm, it0, res->reorthogonalizations, c->red.p, st);
             launch_normalize(rsrc, c->red.p, V, n, st, c->scale.p, c->z.p);
