@@ -1,14 +1,18 @@
 #!/usr/bin/env python
-"""B200 HB-GLS hot-path benchmark (BASELINE.json metric, config 1).
+"""B200 HB-GLS hot-path benchmark (BASELINE.json metric).
 
-Step = one pass of the hot path's assembly over the config-1 workload:
-element residual + scatter (assemble_residual) and element Jacobian + BSR
-scatter (assemble_tangent), inputs resident in HBM.  value = elements*Nm/s
-(Nm = modes = 10).  The same JSON line carries the other two BASELINE
-metric items — L-matvec (BSR SpMV + H(x)mass) GB/s vs HBM over 100
-back-to-back calls, and a converged solve time (config 0) — plus the
-roofline of the dominant kernel, the reference CPU baseline, e2e through the
-C ABI with host buffers, clocks and the launch count.
+Headline workload: BASELINE config 4 at Nm = 24 (N = 47 time samples), the
+largest single-GPU configuration — the Delaunay tetrahedralisation of 700k
+seeded uniform points in the unit cube (4.72M tets, 700k nodes, 11.5M node
+blocks, P.vals 34.6 GB), random modes ~N(0,1)/k^2.  Step = one pass of the
+hot path's assembly: element residual + scatter (assemble_residual) and
+element Jacobian + BSR scatter (assemble_tangent), inputs resident in HBM.
+value = elements*Nm/s.  The same JSON line carries the other BASELINE metric
+items — the L-matvec (BSR SpMV + H(x)mass) GB/s vs HBM over 100 back-to-back
+calls on the same mesh, one Newton iteration of config 1 and a converged
+solve time (config 0) — plus the roofline of the dominant kernel, the
+reference CPU baseline, e2e through the C ABI with host buffers, clocks and
+the launch count.  `--headline-config 1` runs the round-1 workload (config 1).
 
   python bench.py [--gpus N --steps K --warmup W] [--impl reference]
 
@@ -33,9 +37,16 @@ METRIC = "HB-GLS assembly elements*modes/s; BSR SpMV GB/s vs HBM; converged solv
 UNIT = "elements*modes/s"
 CANON_RES_FLOP = 1198  # per (element, time sample), SURVEY.md §8(d) / Appendix A2
 CANON_TAN_FLOP = 1532
-WORKLOAD = ("config1: rigid pipe r=0.3 cm L=6 cm, 20x20x120 hex grid mapped to the disk, "
-            "6 Kuhn tets/hex -> 288000 tets / 53361 nodes; Nm=10 (N=19 samples); "
-            "step = assemble_residual + assemble_tangent")
+WORKLOADS = {
+    4: ("config4: Delaunay tetrahedralisation of 700000 seeded uniform points in the unit cube "
+        "(4721772 tets, 700000 nodes, Morton order), Nm=24 (N=47 samples), random modes "
+        "c_k ~ N(0,1)/k^2; step = assemble_residual + assemble_tangent"),
+    1: ("config1: rigid pipe r=0.3 cm L=6 cm, 20x20x120 hex grid mapped to the disk, "
+        "6 Kuhn tets/hex -> 288000 tets / 53361 nodes; Nm=10 (N=19 samples); "
+        "step = assemble_residual + assemble_tangent"),
+}
+L2_NOTE = ("inputs larger than L2 at config 4 (P.vals 34.6 GB written per step, state 1.05 GB); "
+           "GPU arm also writes a 256 MB buffer between timed steps (not timed)")
 
 
 def env_rank():
@@ -118,11 +129,28 @@ def spmv_bytes(nnz, nn, N):
 
 
 def problem_and_state(cfg):
-    from paper_2411_14315_b200 import cases
+    """The headline problem: BASELINE config 4 at Nm = 24 (operator sweep mesh,
+    zero-traction outlet, zero Dirichlet data, random modes state, pseudo-dt
+    0.01) or config 1 (the seeded pipe, random state, auto pseudo-dt)."""
+    from paper_2411_14315_b200 import cases, meshgen
+    from paper_2411_14315_b200.mesh import NEUMANN
 
+    if cfg == 4:
+        mesh = meshgen.config_mesh(4)
+        M = 24
+        N = 2 * M - 1
+        neu = [(k, np.zeros(N)) for k, p in enumerate(mesh.patches) if p.kind == NEUMANN]
+        prob = cases.Problem(mesh, M, 1.0, 1.06, 0.04, np.zeros(mesh.num_nodes * 3 * N), neu, 0.2)
+        return prob, cases.random_modes_state(mesh.num_nodes, M, 1000 + M), 0.01
     prob = cases.config_problem(cfg)
     state = cases.random_state(prob.mesh.num_nodes, prob.N, 1000 + cfg)
-    return prob, state
+    return prob, state, auto_pseudo_dt(prob)
+
+
+def bench_config(cfg, prob, pdt):
+    """`config` of the JSON line — identical for both arms."""
+    return {"workload": WORKLOADS[cfg], "elements": prob.mesh.num_elements, "nodes": prob.mesh.num_nodes,
+            "modes": prob.modes, "time_points": prob.N, "pseudo_dt": pdt, "l2": L2_NOTE}
 
 
 def auto_pseudo_dt(prob):
@@ -152,41 +180,63 @@ def load_traffic():
 
 # ----------------------------------------------------------------------------- reference arm
 
-def cpu_reference_sample(prob, state, threads, budget_s, min_reps=1):
-    """Time the compiled reference (oracle/_ref/libhbref.so) on the host:
-    assemble_residual(threads) + assemble_tangent (serial by design,
-    assembly.cpp:550-666).  Uses the full mesh when one step fits the budget,
-    otherwise a leading sub-mesh of the (spatially ordered) elements."""
-    from oracle import bindings as ob
-    from paper_2411_14315_b200.mesh import Mesh
+def _sub_problem(prob, state, k):
+    """The leading k elements (spatially ordered numbering) as a mesh of their
+    own (its whole boundary one Dirichlet patch), with the state restricted to
+    its nodes."""
+    from paper_2411_14315_b200.cases import Problem
+    from paper_2411_14315_b200.mesh import DIRICHLET, Mesh, Patch
+    from paper_2411_14315_b200.meshgen import boundary_faces
 
     mesh = prob.mesh
-    ne = mesh.num_elements
-    ctx = ob.ref_context(prob, 0, auto_pseudo_dt(prob))
-    t0 = time.perf_counter()
-    ctx.residual(state, threads)
-    ctx.tangent(state)
-    full = time.perf_counter() - t0
-    frac = min(1.0, budget_s / max(full, 1e-9))
-    if frac < 1.0:
-        k = max(1000, int(ne * frac))
-        conn = mesh.conn[:k]
-        used = np.unique(conn)
-        remap = -np.ones(mesh.num_nodes, np.int64)
-        remap[used] = np.arange(len(used))
-        sub = Mesh(mesh.xyz[used], remap[conn].astype(np.int32), [], None).finalize()
-        from paper_2411_14315_b200.cases import Problem
+    conn = mesh.conn[:k]
+    used = np.unique(conn)
+    remap = -np.ones(mesh.num_nodes, np.int64)
+    remap[used] = np.arange(len(used))
+    sub = Mesh(mesh.xyz[used], remap[conn].astype(np.int32), [], None).finalize()
+    sub.patches = [Patch("wall", DIRICHLET, boundary_faces(sub.conn, sub.num_nodes))]
+    sub = sub.finalize()
+    sp = Problem(sub, prob.modes, prob.period, prob.rho, prob.mu,
+                 np.zeros(len(used) * 3 * prob.N), [], prob.backflow_beta)
+    st = state.reshape(mesh.num_nodes, 4 * prob.N)[used].reshape(-1)
+    return sp, st
 
-        sp = Problem(sub, prob.modes, prob.period, prob.rho, prob.mu,
-                     np.zeros(len(used) * 3 * prob.N), [], prob.backflow_beta)
-        st = state.reshape(mesh.num_nodes, 4 * prob.N)[used].reshape(-1)
-        ctx = ob.ref_context(sp, 0, auto_pseudo_dt(prob))
-        sample_desc = f"leading {k} of {ne} elements (sub-mesh), full step est {full:.1f}s"
-        ne_s, state_s = k, st
-    else:
-        sample_desc = f"full config-1 mesh ({ne} elements)"
-        ne_s, state_s = ne, state
-    return ctx, ne_s, state_s, sample_desc, full
+
+def cpu_reference_sample(prob, state, threads, budget_s, pdt):
+    """The compiled reference (oracle/_ref/libhbref.so) on the host:
+    assemble_residual(threads) + assemble_tangent (serial by design,
+    assembly.cpp:550-666).  The full mesh when one step fits `budget_s`,
+    otherwise the leading sub-mesh of the (Morton / lattice ordered) elements
+    sized from a timed 20k-element probe.  Returns (ctx, elements, state,
+    description, estimated full-step seconds)."""
+    from oracle import bindings as ob
+
+    ne = prob.mesh.num_elements
+    k0 = min(ne, 20000)
+    sp, st = _sub_problem(prob, state, k0)
+    ctx = ob.ref_context(sp, 0, pdt)
+    t0 = time.perf_counter()
+    ctx.residual(st, threads)
+    ctx.tangent(st)
+    t_probe = time.perf_counter() - t0
+    full = t_probe * ne / k0
+    k = min(ne, max(k0, int(k0 * budget_s / max(t_probe, 1e-9))))
+    if k >= ne:
+        ctx = ob.ref_context(prob, 0, pdt)
+        return ctx, ne, state, f"full mesh ({ne} elements)", full
+    if k != k0:
+        sp, st = _sub_problem(prob, state, k)
+        ctx = ob.ref_context(sp, 0, pdt)
+    desc = (f"leading {k} of {ne} elements as a sub-mesh ({sp.mesh.num_nodes} nodes, boundary "
+            f"Dirichlet), same state restricted; full step estimated {full:.0f} s")
+    return ctx, k, st, desc, full
+
+
+def cpu_model():
+    try:
+        return os.popen("lscpu | grep 'Model name' | head -1").read().split(":")[-1].strip()
+    except Exception:
+        return "unknown"
 
 
 def run_reference(args):
@@ -194,9 +244,9 @@ def run_reference(args):
     if rank != 0:
         return
     threads = os.cpu_count() or 1
-    prob, state = problem_and_state(1)
+    prob, state, pdt = problem_and_state(args.headline_config)
     per_step_budget = max(2.0, 150.0 / (args.steps + args.warmup))
-    ctx, ne_s, st, desc, _ = cpu_reference_sample(prob, state, threads, per_step_budget)
+    ctx, ne_s, st, desc, _ = cpu_reference_sample(prob, state, threads, per_step_budget, pdt)
     for _ in range(max(0, args.warmup - 1)):
         ctx.residual(st, threads)
         ctx.tangent(st)
@@ -208,15 +258,14 @@ def run_reference(args):
         times.append(time.perf_counter() - t0)
     t = float(np.mean(times))
     value = ne_s * prob.modes / t
-    cpu = os.popen("lscpu | grep 'Model name' | head -1").read().split(":")[-1].strip()
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic", "config": {"workload": WORKLOAD, "sample": desc},
+        "data": "synthetic", "config": bench_config(args.headline_config, prob, pdt),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
                          "sample": desc + f"; residual threads={threads}, tangent serial "
-                                          f"(reference design); host CPU: {cpu}; FFTW replaced by "
+                                          f"(reference design); host CPU: {cpu_model()}; FFTW replaced by "
                                           "the O(N^2) DFT shim (libfftw3 absent)"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -224,6 +273,56 @@ def run_reference(args):
 
 
 # ----------------------------------------------------------------------------- our arm
+
+def newton_step_config1(hbgpu, torch):
+    """One full Newton iteration at Newton iterate 0 of config 1 (residual,
+    tangent, Jacobi, GMRES with the reference defaults) with its phase split."""
+    from paper_2411_14315_b200 import cases as _cases
+
+    prob = _cases.config_problem(1)
+    ctx = hbgpu.GpuContext(prob.mesh)
+    ctx.set_basis(prob.modes, prob.period)
+    ctx.set_fluid(prob.rho, prob.mu)
+    ctx.set_bcs(prob.dirichlet_g, prob.neumann, prob.backflow_beta)
+    ctx.set_assembly_config(0, auto_pseudo_dt(prob))
+    ctx.assemble_mass()
+    stream = torch.cuda.ExternalStream(ctx.stream)
+    L = hbgpu._lib
+    d_s0 = torch.from_numpy(_cases.initial_state(prob)).cuda()
+    d_r = torch.empty_like(d_s0)
+    d_x = torch.empty_like(d_s0)
+    # one-time GMRES workspace allocation (Krylov basis, Arnoldi state) outside the timing
+    ctx.assemble_residual_dev(d_s0.data_ptr(), d_r.data_ptr())
+    ctx.assemble_tangent_dev(d_s0.data_ptr())
+    ctx.jacobi_dev()
+    ctx.gmres_dev(d_r.data_ptr(), d_x.data_ptr(), hbgpu.KrylovConfig(max_iters=1))
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t_runs = []
+    for rep in range(2):
+        if rep == 1:
+            L.hbgpu_profile_enable(ctx.handle, 1)
+        e0.record(stream)
+        ctx.assemble_residual_dev(d_s0.data_ptr(), d_r.data_ptr())
+        ctx.assemble_tangent_dev(d_s0.data_ptr())
+        ctx.jacobi_dev()
+        g_it, g_rr, g_st = ctx.gmres_dev(d_r.data_ptr(), d_x.data_ptr(), hbgpu.KrylovConfig())
+        e1.record(stream)
+        torch.cuda.synchronize()
+        t_runs.append(e0.elapsed_time(e1))
+    ph_ms = np.zeros(9)
+    ph_n = np.zeros(9, np.int32)
+    L.hbgpu_profile_read(ctx.handle, 9, ph_ms.ctypes.data, ph_n.ctypes.data)
+    L.hbgpu_profile_enable(ctx.handle, 0)
+    out = {"ms": min(t_runs), "runs_ms": t_runs, "gmres_iters": g_it, "gmres_relres": g_rr,
+           "gmres_status": g_st, "reorthogonalizations": ctx.last_reorthogonalizations,
+           "gmres_ms": float(ph_ms[7]), "matvecs": int(ph_n[5]), "matvec_ms": float(ph_ms[5]),
+           "orthogonalisation_ms": float(ph_ms[7] - ph_ms[5]), "assembly_ms": float(ph_ms[0] + ph_ms[4]),
+           "note": "Newton iterate 0 of config 1 (288000 tets, N=19); GMRES restart 200, tol 0.03 "
+                   "(reference defaults)"}
+    ctx.close()
+    return out
+
 
 def run_ours(args):
     import torch
@@ -238,10 +337,10 @@ def run_ours(args):
 
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
-    prob, state = problem_and_state(1)
+    hcfg = args.headline_config
+    prob, state, pdt = problem_and_state(hcfg)
     mesh, N, M = prob.mesh, prob.N, prob.modes
     ne, nn = mesh.num_elements, mesh.num_nodes
-    pdt = auto_pseudo_dt(prob)
     ctx = hbgpu.GpuContext(mesh)
     ctx.set_basis(M, prob.period)
     ctx.set_fluid(prob.rho, prob.mu)
@@ -300,8 +399,9 @@ def run_ours(args):
     peak = np.zeros(1)
     L.hbgpu_fp64_peak(peak.ctypes.data)
     fp64_peak = float(peak[0])
+    nominal_peak = 148 * 64 * 2 * 1.965e9 / 1e12  # 148 SMs x 64 DFMA/clk x 2 FLOP x 1965 MHz
 
-    def isolated(fn, phase, reps=5):
+    def isolated(fn, reps=5):
         L.hbgpu_profile_enable(ctx.handle, 1)
         with torch.cuda.stream(stream):
             for _ in range(reps):
@@ -314,29 +414,34 @@ def run_ours(args):
         L.hbgpu_profile_enable(ctx.handle, 0)
         return ms, cnt
 
-    rms, rcnt = isolated(lambda: ctx.assemble_residual_dev(d_state.data_ptr(), d_r.data_ptr()), 0)
-    tms, tcnt = isolated(lambda: ctx.assemble_tangent_dev(d_state.data_ptr()), 4)
+    rms, rcnt = isolated(lambda: ctx.assemble_residual_dev(d_state.data_ptr(), d_r.data_ptr()))
+    tms, tcnt = isolated(lambda: ctx.assemble_tangent_dev(d_state.data_ptr()))
     res_all_ms = rms[0] / max(rcnt[0], 1)
     res_elem_ms = rms[2] / max(rcnt[2], 1)
     tan_ms = tms[4] / max(tcnt[4], 1)
     res_flops = CANON_RES_FLOP * ne * N
     tan_flops = CANON_TAN_FLOP * ne * N
-    traffic = load_traffic()
+    traffic = load_traffic().get(f"config{hcfg}", {})
     kernels = {
-        "tangent_pipe_kernel": {"ms": tan_ms, "tflops": tan_flops / (tan_ms * 1e-3) / 1e12},
+        "tangent": {"ms": tan_ms, "tflops": tan_flops / (tan_ms * 1e-3) / 1e12},
         "residual (all passes)": {"ms": res_all_ms, "tflops": res_flops / (res_all_ms * 1e-3) / 1e12},
-        "residual_chunk_kernel": {"ms": res_elem_ms, "tflops": res_flops / (res_elem_ms * 1e-3) / 1e12},
+        "residual element pass": {"ms": res_elem_ms, "tflops": res_flops / (res_elem_ms * 1e-3) / 1e12},
     }
-    dom = "tangent_pipe_kernel" if tan_ms >= res_all_ms else "residual (all passes)"
+    for k in kernels.values():
+        k["frac_measured_peak"] = k["tflops"] / fp64_peak if fp64_peak > 0 else None
+        k["frac_nominal_peak"] = k["tflops"] / nominal_peak
+    dom = "tangent" if tan_ms >= res_all_ms else "residual (all passes)"
     dk = kernels[dom]
     roofline = {
         "kernel": dom, "bound": "fp64", "achieved": dk["tflops"], "peak": fp64_peak,
         "unit": "TFLOP/s", "frac": dk["tflops"] / fp64_peak if fp64_peak > 0 else None,
-        "traffic": traffic.get(dom.split(" ")[0]),
+        "frac_nominal": dk["tflops"] / nominal_peak, "nominal_peak": nominal_peak,
+        "traffic": traffic.get(dom),
         "algorithmic": f"{CANON_TAN_FLOP if dom.startswith('tangent') else CANON_RES_FLOP} FP64 "
                        f"FLOP per (element, sample) x {ne}x{N}",
         "timing": "kernel alone, CUDA events on its stream, L2 flushed, mean of 5",
-        "peak_source": "measured DFMA loop (hbgpu_fp64_peak) on this GPU; MEASURED_PEAKS.json has no FP64 figure",
+        "peak_source": "measured DFMA loop (hbgpu_fp64_peak) on this GPU; MEASURED_PEAKS.json has no "
+                       "FP64 figure; nominal = 148 SMs x 64 DFMA/clk x 2 x 1965 MHz",
         "other_kernels": kernels,
     }
 
@@ -361,43 +466,9 @@ def run_ours(args):
     mv_bytes = spmv_bytes(nnz, nn, N)
     spmv = {"ms": mv_ms, "gbs": mv_bytes / (mv_ms * 1e-3) / 1e9, "peak_gbs": hbm_peak,
             "frac": mv_bytes / (mv_ms * 1e-3) / 1e9 / hbm_peak, "compulsory_bytes": mv_bytes,
-            "traffic": traffic.get("lmatvec_kernel"), "reps": reps,
+            "traffic": traffic.get("lmatvec"), "reps": reps,
             "peak_source": "MEASURED_PEAKS.json hbm_gbs (of measured)"}
-
-    # ---- one full Newton iteration at Newton iterate 0 (residual, tangent, Jacobi,
-    #      GMRES with the reference defaults), with its phase split
-    from paper_2411_14315_b200 import cases as _cases
-
-    d_s0 = torch.from_numpy(_cases.initial_state(prob)).cuda()
-    d_x = torch.empty_like(d_s0)
-    # one-time GMRES workspace allocation (Krylov basis, Arnoldi state) outside the timing
-    ctx.jacobi_dev()
-    ctx.gmres_dev(d_r.data_ptr(), d_x.data_ptr(), hbgpu.KrylovConfig(max_iters=1))
-    torch.cuda.synchronize()
-    # twice, the faster run reported (run-to-run host jitter of the step loop was
-    # seen on the box); the second run is the profiled one for the phase split
-    t_runs = []
-    for rep in range(2):
-        if rep == 1:
-            L.hbgpu_profile_enable(ctx.handle, 1)
-        e0.record(stream)
-        ctx.assemble_residual_dev(d_s0.data_ptr(), d_r.data_ptr())
-        ctx.assemble_tangent_dev(d_s0.data_ptr())
-        ctx.jacobi_dev()
-        g_it, g_rr, g_st = ctx.gmres_dev(d_r.data_ptr(), d_x.data_ptr(), hbgpu.KrylovConfig())
-        e1.record(stream)
-        torch.cuda.synchronize()
-        t_runs.append(e0.elapsed_time(e1))
-    ph_ms = np.zeros(9)  # the step phases were already reported above
-    ph_n = np.zeros(9, np.int32)
-    L.hbgpu_profile_read(ctx.handle, 9, ph_ms.ctypes.data, ph_n.ctypes.data)
-    L.hbgpu_profile_enable(ctx.handle, 0)
-    newton = {"ms": min(t_runs), "runs_ms": t_runs, "gmres_iters": g_it, "gmres_relres": g_rr, "gmres_status": g_st,
-              "reorthogonalizations": ctx.last_reorthogonalizations,
-              "gmres_ms": float(ph_ms[7]), "matvecs": int(ph_n[5]), "matvec_ms": float(ph_ms[5]),
-              "orthogonalisation_ms": float(ph_ms[7] - ph_ms[5]),
-              "assembly_ms": float(ph_ms[0] + ph_ms[4]),
-              "note": "Newton iterate 0 of config 1; GMRES restart 200, tol 0.03 (reference defaults)"}
+    del y, out
 
     # ---- e2e through the C ABI with pinned host buffers (H2D state, D2H residual)
     h_state = torch.from_numpy(state).pin_memory()
@@ -415,6 +486,42 @@ def run_ours(args):
            "note": "hbgpu_assemble(host state -> host residual, tangent P kept on device as the GPU "
                    "Newton loop uses it): one upload, residual copy-back overlapping the tangent; "
                    "pinned host buffers; wall clock"}
+    # the five-call drop-in path (gpu::assemble_residual + gpu::assemble_tangent into
+    # a host BlockSparseMatrix): P itself crosses PCIe every step
+    pbytes = nnz * 8 * N * 8
+    five = None
+    try:
+        import psutil
+
+        avail = psutil.virtual_memory().available
+    except Exception:
+        avail = 0
+    if args.five_call and avail > 2.5 * pbytes:
+        h_p = np.empty(nnz * 8 * N)
+        h_p[:: 512] = 0.0  # touch
+        t5 = []
+        for _ in range(2):
+            t0 = time.perf_counter()
+            hbgpu._residual(ctx.handle, hs.ctypes.data, hr.ctypes.data)
+            hbgpu._tangent(ctx.handle, hs.ctypes.data, h_p.ctypes.data)
+            t5.append(time.perf_counter() - t0)
+        five = {"value": world * ne * M / min(t5), "unit": UNIT, "seconds": t5,
+                "h2d_bytes_per_step": 2 * state.nbytes, "d2h_bytes_per_step": state.nbytes + pbytes,
+                "note": "hbgpu_assemble_residual + hbgpu_assemble_tangent with P copied to pageable host "
+                        "memory, as the C++ adapter's five-call drop-in does; best of 2, wall clock"}
+        del h_p
+    elif args.five_call:
+        five = {"value": None, "note": f"skipped: {avail / 1e9:.0f} GB host memory available, P is "
+                                       f"{pbytes / 1e9:.1f} GB"}
+    del h_state, h_r
+    phases = {k: float(step_ph_ms[i] / args.steps) for i, k in
+              enumerate(["residual", "res_hu", "res_elements", "res_finalize",
+                         "tangent", "matvec", "jacobi", "gmres", "mass"])}
+    ctx.close()
+    del d_state, d_r
+    torch.cuda.empty_cache()
+
+    newton = newton_step_config1(hbgpu, torch) if rank == 0 and args.newton else None
 
     # ---- converged solve time (config 0, reference default tolerances)
     solve = None
@@ -425,7 +532,7 @@ def run_ours(args):
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
             threads = os.cpu_count() or 1
-            cctx, ne_s, st, desc, full = cpu_reference_sample(prob, state, threads, 12.0)
+            cctx, ne_s, st, desc, full = cpu_reference_sample(prob, state, threads, 12.0, pdt)
             t0 = time.perf_counter()
             reps_c = 0
             while True:
@@ -437,29 +544,28 @@ def run_ours(args):
             tc = (time.perf_counter() - t0) / reps_c
             cpu_baseline = {"value": ne_s * M / tc, "unit": UNIT, "cores": threads, "kind": "reference",
                             "sample": f"{desc}; {reps_c} timed steps; residual threads={threads}, "
-                                      "tangent serial as in the reference"}
+                                      f"tangent serial as in the reference; host CPU: {cpu_model()}"}
         except Exception as exc:  # oracle library absent on this box
             cpu_baseline = {"value": None, "unit": UNIT, "cores": 0, "kind": "reference",
                             "sample": f"unavailable: {exc}"}
 
     if rank == 0:
+        cfgd = bench_config(hcfg, prob, pdt)
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": WORKLOAD, "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
-                       "l2": "256 MB buffer written between timed steps (not timed)",
-                       "elements": ne, "nodes": nn, "nnz_blocks": nnz, "modes": M, "time_points": N,
-                       "pseudo_dt": pdt},
-            "phases_ms_per_step": {k: float(step_ph_ms[i] / args.steps) for i, k in
-                                   enumerate(["residual", "res_hu", "res_elements", "res_finalize",
-                                              "tangent", "matvec", "jacobi", "gmres", "mass"])},
+            "config": cfgd,
+            "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
+            "nnz_blocks": nnz,
+            "phases_ms_per_step": phases,
             "roofline": roofline,
             "spmv": spmv,
             "newton_step": newton,
             "solve": solve,
             "cpu_baseline": cpu_baseline,
             "e2e": e2e,
+            "e2e_five_call": five,
             "clocks": clk.summary(),
             "gpu_launches": int(launches),
             "fp64_peak_tflops": fp64_peak,
@@ -756,6 +862,9 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--spmv-reps", type=int, default=100)
     ap.add_argument("--no-solve", dest="solve", action="store_false")
+    ap.add_argument("--no-newton", dest="newton", action="store_false")
+    ap.add_argument("--no-five-call", dest="five_call", action="store_false")
+    ap.add_argument("--headline-config", type=int, default=4, choices=[1, 4])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-solve", action="store_true", help="also time the reference's converged config-0 solve")
     ap.add_argument("--sweep4", action="store_true", help="config-4 operator sweep (separate run)")

@@ -75,6 +75,11 @@ const char* hbgpu_create_error(void);
 void* hbgpu_stream(hbgpu_ctx* ctx);
 int hbgpu_synchronize(hbgpu_ctx* ctx);
 
+/* Largest supported mode count (N = 63 time samples; BASELINE.json's largest is
+ * M = 24, the paper's N = 25).  hbgpu_set_basis rejects larger M with
+ * HBGPU_ERR_INVALID instead of failing at the first launch. */
+#define HBGPU_MAX_MODES 32
+
 /* SpectralBasis(M, T) (spectral.cpp:18-27) + SpectralOperators (H = E^-1 Omega E,
  * spectral.cpp:146-164,236-256), applied as a dense N x N matrix on device. */
 int hbgpu_set_basis(hbgpu_ctx* ctx, int modes, double period);
@@ -168,6 +173,13 @@ int hbgpu_set_resistance(hbgpu_ctx* ctx, int n, const int* patch, const double* 
 /* Copy of the context's current P values (BlockSparseMatrix::vals layout), e.g.
  * after hbgpu_assemble, which keeps P on the device. */
 int hbgpu_get_pvals(hbgpu_ctx* ctx, double* pvals);
+
+/* Block rows of the context's current P: for each listed node A (distinct or
+ * not), the segment vals[row_ptr[A]*8N .. row_ptr[A+1]*8N) appended to `out`
+ * in list order (the reference's BlockSparseMatrix::vals layout, 64-bit
+ * offsets).  Reads back a sample of P without copying all of it (P is 34.6 GB
+ * at BASELINE config 4, Nm = 24). */
+int hbgpu_get_pvals_rows(hbgpu_ctx* ctx, int nrows, const int* rows, double* out);
 
 /* Device pointers of the context's P values / mass / inverse diagonal. */
 double* hbgpu_pvals_dev(hbgpu_ctx* ctx);

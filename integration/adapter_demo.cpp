@@ -71,6 +71,26 @@ int main() {
     gpu::matvec(L, y, o_gpu);
     const double e_mv = rel(o_gpu, o_ref);
 
+    // in-place edits of host data the adapter has already mirrored on the
+    // device must be seen (content fingerprints, not pointer identity)
+    for (size_t k = 0; k < L.P.vals.size(); k += 3)
+        L.P.vals[k] *= 1.25;
+    for (auto& m : L.mass)
+        m *= 0.75;
+    L.matvec(y, o_ref);
+    gpu::matvec(L, y, o_gpu);
+    const double e_inplace_op = rel(o_gpu, o_ref);
+    BoundaryConditionSet bcs2 = in.bcs;
+    const auto r_gpu2a = gpu::assemble_residual(mesh, geoms, state, ops, in.props, bcs2, acfg);
+    for (auto& g : bcs2.dirichlet_g)
+        g *= 0.5;  // ramped Dirichlet data, same vector
+    const auto r_ref2 = assemble_residual(mesh, geoms, state, ops, in.props, bcs2, acfg, 1);
+    const auto r_gpu2 = gpu::assemble_residual(mesh, geoms, state, ops, in.props, bcs2, acfg);
+    const double e_inplace_g = rel(r_gpu2, r_ref2);
+    const double d_g = rel(r_gpu2a, r_ref2);  // the edit is visible in the residual
+    assemble_tangent(mesh, geoms, state, in.props, in.bcs, acfg, L.P);  // restore P
+    L.mass = assemble_mass(mesh, geoms, in.props.rho, *pattern);
+
     const auto pc_ref = jacobi_preconditioner(L);
     const auto pc_gpu = gpu::jacobi_preconditioner(L);
     const double e_jac = rel(pc_gpu.inv_diag, pc_ref.inv_diag);
@@ -112,7 +132,8 @@ int main() {
     const double e_time_u = rel(ts_gpu.cycle.u, ts_ref.cycle.u);
     const double e_time_p = rel(ts_gpu.cycle.p, ts_ref.cycle.p);
 
-    const bool ok = e_res < 1e-12 && e_tan < 1e-12 && e_mass < 1e-15 && e_mv < 1e-12 &&
+    const bool ok = e_inplace_op < 1e-12 && e_inplace_g < 1e-12 && d_g > 1e-10 &&
+                    e_res < 1e-12 && e_tan < 1e-12 && e_mass < 1e-15 && e_mv < 1e-12 &&
                     e_jac < 1e-15 && gmres_scaled <= 1e-8 * 1.0001 && s_ref.log.converged &&
                     s_gpu.log.converged && e_solve < 1e-8 && e_time_u < 1e-8 && e_time_p < 1e-8 &&
                     ts_gpu.total_steps == ts_ref.total_steps;
@@ -121,13 +142,14 @@ int main() {
         "\"matvec\": %.3e, \"jacobi\": %.3e, \"gmres_scaled_residual\": %.3e, \"gmres_iters\": %d, "
         "\"solve_state\": %.3e, \"newton_ref\": %zu, \"newton_gpu\": %zu, \"solve_ref_s\": %.3f, "
         "\"solve_gpu_s\": %.3f, \"time_u\": %.3e, \"time_p\": %.3e, \"time_newton_ref\": %d, "
-        "\"time_newton_gpu\": %d, \"time_ref_s\": %.3f, \"time_gpu_s\": %.3f, \"ok\": %s}\n",
+        "\"time_newton_gpu\": %d, \"time_ref_s\": %.3f, \"time_gpu_s\": %.3f, "
+        "\"inplace_operator\": %.3e, \"inplace_dirichlet\": %.3e, \"ok\": %s}\n",
         mesh.num_elements(), N, e_res, e_tan, e_mass, e_mv, e_jac, gmres_scaled, lin.iterations,
         e_solve, s_ref.log.entries.size(), s_gpu.log.entries.size(),
         std::chrono::duration<double>(t1 - t0).count(),
         std::chrono::duration<double>(t2 - t1).count(), e_time_u, e_time_p, ts_ref.total_newton_iters,
         ts_gpu.total_newton_iters, std::chrono::duration<double>(t4 - t3).count(),
-        std::chrono::duration<double>(t5 - t4).count(), ok ? "true" : "false");
+        std::chrono::duration<double>(t5 - t4).count(), e_inplace_op, e_inplace_g, ok ? "true" : "false");
     gpu::release(mesh);
     return ok ? 0 : 1;
 }

@@ -7,30 +7,102 @@
 #include "hbgpu.h"
 
 #include <cmath>
+#include <cstdint>
 #include <cstring>
 #include <limits>
 #include <map>
 #include <stdexcept>
 #include <string>
+#include <thread>
 
 namespace hbflow::gpu {
 
 namespace {
 
+// Content fingerprint of a host buffer: 64-bit multiply-rotate hash over
+// 8-byte words, computed in fixed chunks (several threads for large buffers)
+// and combined in chunk order, so it is deterministic.  The adapter skips a
+// host->device upload only when the buffer's address, size AND content hash
+// equal those of the copy already on the device: in-place edits, or a new
+// object at a freed one's address, are always re-uploaded.
+uint64_t hash_words(const uint64_t* w, size_t n, uint64_t seed) {
+    uint64_t h = seed ^ (n * 0x9e3779b97f4a7c15ull);
+    for (size_t i = 0; i < n; ++i) {
+        uint64_t k = w[i] * 0xff51afd7ed558ccdull;
+        k = (k << 31) | (k >> 33);
+        h = (h ^ k) * 0xc4ceb9fe1a85ec53ull;
+        h = (h << 27) | (h >> 37);
+    }
+    return h;
+}
+
+uint64_t hash_bytes(const void* data, size_t bytes) {
+    if (!data || bytes == 0)
+        return 0x1234567ull;
+    const size_t nw = bytes / 8;
+    const auto* w = static_cast<const uint64_t*>(data);
+    constexpr size_t kChunk = size_t(1) << 22;  // 32 MB of words per chunk
+    const size_t nchunk = (nw + kChunk - 1) / kChunk;
+    std::vector<uint64_t> part(nchunk > 0 ? nchunk : 1, 0);
+    const unsigned nthr = nchunk > 1 ? std::min<unsigned>(16, std::max(1u, std::thread::hardware_concurrency())) : 1;
+    auto work = [&](unsigned t) {
+        for (size_t c = t; c < nchunk; c += nthr)
+            part[c] = hash_words(w + c * kChunk, std::min(kChunk, nw - c * kChunk), c);
+    };
+    if (nthr > 1) {
+        std::vector<std::thread> th;
+        for (unsigned t = 0; t < nthr; ++t)
+            th.emplace_back(work, t);
+        for (auto& t : th)
+            t.join();
+    } else {
+        work(0);
+    }
+    uint64_t h = hash_words(part.data(), nchunk, bytes);
+    uint64_t tail = 0;
+    std::memcpy(&tail, static_cast<const char*>(data) + nw * 8, bytes - nw * 8);
+    return hash_words(&tail, 1, h);
+}
+
+struct Fingerprint {
+    const void* ptr = nullptr;
+    size_t bytes = 0;
+    uint64_t hash = 0;
+    bool valid = false;
+    static Fingerprint of(const void* p, size_t bytes) { return {p, bytes, hash_bytes(p, bytes), true}; }
+    bool matches(const void* p, size_t b) const {
+        return valid && p == ptr && b == bytes && hash_bytes(p, b) == hash;
+    }
+};
+
+// Identity of a Mesh's hot-path content: nodes, elements, Dirichlet flags and
+// boundary patches.  A cached context is reused only while it matches.
+uint64_t mesh_hash(const Mesh& mesh) {
+    uint64_t h = hash_bytes(mesh.nodes.data(), mesh.nodes.size() * sizeof(mesh.nodes[0]));
+    h ^= hash_bytes(mesh.elements.data(), mesh.elements.size() * sizeof(mesh.elements[0])) * 3;
+    h ^= hash_bytes(mesh.is_dirichlet_node.data(), mesh.is_dirichlet_node.size() * sizeof(mesh.is_dirichlet_node[0])) * 5;
+    for (const auto& p : mesh.patches) {
+        h = h * 0x100000001b3ull ^ uint64_t(p.kind == PatchKind::Dirichlet ? 1 : 2);
+        h ^= hash_bytes(p.facets.data(), p.facets.size() * sizeof(p.facets[0])) * 7;
+    }
+    return h;
+}
+
 struct Entry {
     hbgpu_ctx* ctx = nullptr;
+    uint64_t mesh_id = 0;
+    bool geometry_given = false;
     int modes = 0;
     double period = 0.0;
     double rho = -1.0, mu = -1.0;
-    const double* g_ptr = nullptr;
-    size_t g_size = 0;
+    Fingerprint g;                    // dirichlet_g last uploaded
     std::vector<int> neu_patch;
     std::vector<double> neu_h;
     double beta = -1.0;
     int tau = -1, backflow = -1;
     double pseudo_dt = -2.0, c1 = 0.0;
-    const double* p_src = nullptr;     // host P.vals mirrored on the device
-    const double* mass_src = nullptr;  // host mass mirrored on the device
+    Fingerprint p;                    // host P.vals whose content the device P holds
+    Fingerprint mass;                 // host mass whose content the device mass holds
 };
 
 std::map<const Mesh*, Entry>& cache() {
@@ -58,9 +130,15 @@ void check(hbgpu_ctx* c, int status) {
 
 Entry& entry(const Mesh& mesh, const std::vector<ElementGeometry>* geoms) {
     auto& m = cache();
+    const uint64_t id = mesh_hash(mesh);
     auto it = m.find(&mesh);
-    if (it != m.end())
-        return it->second;
+    if (it != m.end()) {
+        if (it->second.mesh_id == id)
+            return it->second;
+        // same address, different mesh (edited, or freed and reallocated)
+        hbgpu_destroy(it->second.ctx);
+        m.erase(it);
+    }
     static_assert(sizeof(ElementGeometry) == 22 * sizeof(double));
     static_assert(sizeof(std::array<int, 4>) == 4 * sizeof(int));
     std::vector<int> kinds, nf, facets;
@@ -95,6 +173,8 @@ Entry& entry(const Mesh& mesh, const std::vector<ElementGeometry>* geoms) {
         rethrow(st, hbgpu_create_error());
     Entry& e = m[&mesh];
     e.ctx = c;
+    e.mesh_id = id;
+    e.geometry_given = geoms != nullptr;
     return e;
 }
 
@@ -103,10 +183,10 @@ void set_basis(Entry& e, const SpectralBasis& b) {
         check(e.ctx, hbgpu_set_basis(e.ctx, b.modes, b.period));
         e.modes = b.modes;
         e.period = b.period;
-        e.g_ptr = nullptr;
+        e.g = Fingerprint{};
         e.neu_patch.clear();
         e.beta = -1.0;
-        e.p_src = e.mass_src = nullptr;
+        e.p = e.mass = Fingerprint{};
     }
 }
 
@@ -116,7 +196,7 @@ void set_physics(Entry& e, const FluidProperties& props, const BoundaryCondition
         check(e.ctx, hbgpu_set_fluid(e.ctx, props.rho, props.mu));
         e.rho = props.rho;
         e.mu = props.mu;
-        e.mass_src = nullptr;
+        e.mass = Fingerprint{};
     }
     const int N = 2 * e.modes - 1;
     std::vector<int> np;
@@ -128,11 +208,11 @@ void set_physics(Entry& e, const FluidProperties& props, const BoundaryCondition
             throw std::invalid_argument("Neumann data length does not match the basis");
     }
     const double* g = bcs.dirichlet_g.empty() ? nullptr : bcs.dirichlet_g.data();
-    if (g != e.g_ptr || bcs.dirichlet_g.size() != e.g_size || np != e.neu_patch || nh != e.neu_h ||
-        bcs.backflow_beta != e.beta) {
+    const size_t gbytes = bcs.dirichlet_g.size() * sizeof(double);
+    if (!e.g.matches(g, gbytes) || np != e.neu_patch || nh != e.neu_h || bcs.backflow_beta != e.beta) {
+        e.g = Fingerprint{};
         check(e.ctx, hbgpu_set_bcs(e.ctx, g, int(np.size()), np.data(), nh.data(), bcs.backflow_beta));
-        e.g_ptr = g;
-        e.g_size = bcs.dirichlet_g.size();
+        e.g = Fingerprint::of(g, gbytes);
         e.neu_patch = np;
         e.neu_h = nh;
         e.beta = bcs.backflow_beta;
@@ -153,13 +233,17 @@ void set_physics(Entry& e, const FluidProperties& props, const BoundaryCondition
 
 void sync_operator(Entry& e, const TangentOperator& L) {
     set_basis(e, L.ops->basis());
-    if (L.P.vals.data() != e.p_src) {
+    const size_t pbytes = L.P.vals.size() * sizeof(double);
+    if (!e.p.matches(L.P.vals.data(), pbytes)) {
+        e.p = Fingerprint{};
         check(e.ctx, hbgpu_set_pvals(e.ctx, L.P.vals.data()));
-        e.p_src = L.P.vals.data();
+        e.p = Fingerprint::of(L.P.vals.data(), pbytes);
     }
-    if (L.mass.data() != e.mass_src) {
+    const size_t mbytes = L.mass.size() * sizeof(double);
+    if (!e.mass.matches(L.mass.data(), mbytes)) {
+        e.mass = Fingerprint{};
         check(e.ctx, hbgpu_set_mass(e.ctx, L.mass.data()));
-        e.mass_src = L.mass.data();
+        e.mass = Fingerprint::of(L.mass.data(), mbytes);
     }
 }
 
@@ -185,8 +269,10 @@ void assemble_tangent(const Mesh& mesh, const std::vector<ElementGeometry>& geom
     Entry& e = entry(mesh, &geoms);
     set_basis(e, state.basis);
     set_physics(e, props, bcs, &cfg);
+    e.p = Fingerprint{};
     check(e.ctx, hbgpu_assemble_tangent(e.ctx, state.data.data(), P.vals.data()));
-    e.p_src = P.vals.data();  // the device copy is now current
+    // the device copy equals the host copy just written
+    e.p = Fingerprint::of(P.vals.data(), P.vals.size() * sizeof(double));
 }
 
 std::vector<double> assemble_mass(const Mesh& mesh, const std::vector<ElementGeometry>& geoms,
@@ -199,7 +285,11 @@ std::vector<double> assemble_mass(const Mesh& mesh, const std::vector<ElementGeo
         e.rho = rho;
     }
     std::vector<double> mass(size_t(pattern.nnz()));
+    e.mass = Fingerprint{};
     check(e.ctx, hbgpu_assemble_mass(e.ctx, mass.data()));
+    // the returned vector is moved into the caller's TangentOperator, so its
+    // buffer address survives; its content is checked again on use
+    e.mass = Fingerprint::of(mass.data(), mass.size() * sizeof(double));
     return mass;
 }
 
@@ -264,6 +354,8 @@ HbSolution solve_harmonic(const Mesh& mesh, const std::vector<ElementGeometry>& 
     hbgpu_solve_info info{};
     const int st = hbgpu_solve_harmonic(e.ctx, &sc, sol.state.data.data(), &info, cap, it.data(),
                                         res.data(), rel.data(), lin.data(), sec.data());
+    e.p = Fingerprint{};  // the solve replaced the device P (and assembled its own mass)
+    e.mass = Fingerprint{};
     for (int k = 0; k < info.entries; ++k)
         sol.log.entries.push_back({it[size_t(k)], res[size_t(k)], rel[size_t(k)], lin[size_t(k)],
                                    sec[size_t(k)]});
@@ -290,7 +382,7 @@ TimeSolution solve_time(const CaseInputs& inputs, const TimeSolverConfig& cfg) {
         nb.h.assign(1, nb.h.empty() ? 0.0 : nb.h[0]);
     b1.dirichlet_g.clear();
     set_physics(e, inputs.props, b1, nullptr);
-    e.g_ptr = nullptr;  // b1 is a temporary
+    e.g = Fingerprint{};  // b1 is a temporary
     e.neu_patch.clear();
     hbgpu_time_cfg tc{};
     tc.steps_per_cycle = cfg.steps_per_cycle;
@@ -323,7 +415,10 @@ TimeSolution solve_time(const CaseInputs& inputs, const TimeSolverConfig& cfg) {
     sol.cycle.u.assign(size_t(snaps) * n3, 0.0);
     sol.cycle.p.assign(size_t(snaps) * size_t(nn), 0.0);
     hbgpu_time_result res{};
-    check(e.ctx, hbgpu_solve_time(e.ctx, &tc, T, cb, &tr, sol.cycle.u.data(), sol.cycle.p.data(), &res));
+    const int st = hbgpu_solve_time(e.ctx, &tc, T, cb, &tr, sol.cycle.u.data(), sol.cycle.p.data(), &res);
+    e.p = Fingerprint{};  // the time solver overwrote the device P and mass
+    e.mass = Fingerprint{};
+    check(e.ctx, st);
     sol.cycle_change = res.cycle_change;
     sol.total_seconds = res.total_seconds;
     sol.total_steps = res.total_steps;

@@ -412,6 +412,9 @@ class Restated:
         _sig(L, "hbo_pattern", _i, [_i, _i, _vp, _vp, _vp])
         _sig(L, "hbo_residual", _i, [_vp, _vp, _vp])
         _sig(L, "hbo_tangent", _i, [_vp, _vp, _vp, _vp, _vp])
+        _sig(L, "hbo_residual_rows", _i, [_vp, _vp, _i, _vp, _vp])
+        _sig(L, "hbo_tangent_rows", _i, [_vp, _vp, _vp, _vp, _i, _vp, _vp])
+        _sig(L, "hbo_tangent_matvec_rows", _i, [_vp, _vp, _vp, _vp, _vp, _vp, _i, _vp, _vp])
         _sig(L, "hbo_mass", None, [_vp, _vp, _vp, _vp])
         _sig(L, "hbo_bsr_matvec", None, [_i, _i, _vp, _vp, _vp, _vp, _vp])
         _sig(L, "hbo_tangent_matvec", None, [_vp, _vp, _vp, _vp, _vp, _vp, _vp])
@@ -468,6 +471,43 @@ class Restated:
         if self.L.hbo_tangent(C.byref(self.p), _ptr(self.row_ptr), _ptr(self.col_idx), _ptr(s), _ptr(v)):
             raise ArithmeticError("singular stabilization parameter")
         return v
+
+    def _rows_status(self, st):
+        if st == -1:
+            raise ArithmeticError("singular stabilization parameter")
+        if st:
+            raise OracleError(f"row subset: status {st} (rows must be distinct and in range)")
+
+    def residual_rows(self, state, rows):
+        """Residual rows of the listed nodes, (len(rows), 4, N); bit-identical to
+        the corresponding rows of residual()."""
+        s = _f64(state)
+        rows = np.ascontiguousarray(rows, np.int32)
+        r = np.empty(len(rows) * 4 * self.N)
+        self._rows_status(self.L.hbo_residual_rows(C.byref(self.p), _ptr(s), len(rows), _ptr(rows), _ptr(r)))
+        return r.reshape(len(rows), 4, self.N)
+
+    def tangent_rows(self, state, rows):
+        """P block rows of the listed nodes: the segments
+        vals[row_ptr[A]*8N : row_ptr[A+1]*8N] concatenated in list order."""
+        s = _f64(state)
+        rows = np.ascontiguousarray(rows, np.int32)
+        tot = int(np.sum(self.row_ptr[rows + 1] - self.row_ptr[rows])) * 8 * self.N
+        v = np.empty(tot)
+        self._rows_status(self.L.hbo_tangent_rows(C.byref(self.p), _ptr(self.row_ptr), _ptr(self.col_idx),
+                                                  _ptr(s), len(rows), _ptr(rows), _ptr(v)))
+        return v
+
+    def matvec_rows(self, row_vals, mass, y, rows):
+        """TangentOperator::matvec rows of the listed nodes from their P
+        segments (tangent_rows layout), the full mass and the full y."""
+        rv, m, yy = _f64(row_vals), _f64(mass), _f64(y)
+        rows = np.ascontiguousarray(rows, np.int32)
+        o = np.empty(len(rows) * 4 * self.N)
+        self._rows_status(self.L.hbo_tangent_matvec_rows(C.byref(self.p), _ptr(self.row_ptr), _ptr(self.col_idx),
+                                                         _ptr(rv), _ptr(m), _ptr(yy), len(rows), _ptr(rows),
+                                                         _ptr(o)))
+        return o.reshape(len(rows), 4, self.N)
 
     def time_residual(self, u, udot, p, omega_hat):
         """time_solver.cpp:58-166 (u, udot node*3+i, p node) -> r node*4+c"""

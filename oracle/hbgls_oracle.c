@@ -396,17 +396,66 @@ int hbo_residual(const hbo_problem* p, const double* state, double* r) {
 
 /* ---------------------------------------------------------------- tangent */
 
-int hbo_tangent(const hbo_problem* p, const int* row_ptr, const int* col_idx,
-                const double* state, double* vals) {
-    const int N = p->N;
+/* element_tangent_p (assembly.cpp:265-374) of one element at one time sample:
+ * K[a][b], G[a][b][i], D[a][b][i], L[a][b] (assembly.hpp:101-110). */
+static int element_tangent_n(const hbo_problem* p, const double* g, const double u[4][3],
+                             double K[4][4], double G[4][4][3], double D[4][4][3],
+                             double L[4][4]) {
     const double rho = p->rho, mu = p->mu, nu = mu / rho;
     const int pseudo = p->pseudo_dt > 0.0 && isfinite(p->pseudo_dt);
     const double pc = pseudo ? p->pseudo_c1 * rho / p->pseudo_dt : 0.0;
+    const double V = GV(g), w = V / 4.0;
+    double gg[4][4];
+    for (int a = 0; a < 4; ++a)
+        for (int b = 0; b < 4; ++b) {
+            gg[a][b] = GN(g, a, 0) * GN(g, b, 0) + GN(g, a, 1) * GN(g, b, 1) +
+                       GN(g, a, 2) * GN(g, b, 2);
+            K[a][b] = mu * V * gg[a][b] + pc * (a == b ? V / 10.0 : V / 20.0);
+            L[a][b] = 0.0;
+            for (int i = 0; i < 3; ++i) {
+                G[a][b][i] = -GN(g, a, i) * V / 4.0;
+                D[a][b][i] = GN(g, b, i) * V / 4.0;
+            }
+        }
+    double tau_mean = 0.0;
+    if (p->tau_mode == 1) {
+        double um[3] = {0, 0, 0};
+        for (int a = 0; a < 4; ++a)
+            for (int i = 0; i < 3; ++i)
+                um[i] += 0.25 * u[a][i];
+        if (tau_of(g, um, nu, &tau_mean))
+            return -1;
+    }
+    for (int q = 0; q < 4; ++q) {
+        double uq[3] = {0, 0, 0}, adv[4];
+        for (int i = 0; i < 3; ++i)
+            for (int a = 0; a < 4; ++a)
+                uq[i] += tet_shape(q, a) * u[a][i];
+        double tau = tau_mean;
+        if (p->tau_mode == 0 && tau_of(g, uq, nu, &tau))
+            return -1;
+        for (int a = 0; a < 4; ++a)
+            adv[a] = uq[0] * GN(g, a, 0) + uq[1] * GN(g, a, 1) + uq[2] * GN(g, a, 2);
+        for (int a = 0; a < 4; ++a)
+            for (int b = 0; b < 4; ++b) {
+                K[a][b] += w * rho * (tet_shape(q, a) * adv[b] + adv[a] * tau * adv[b]);
+                L[a][b] += w * gg[a][b] * tau / rho;
+                for (int i = 0; i < 3; ++i) {
+                    G[a][b][i] += w * adv[a] * tau * GN(g, b, i);
+                    D[a][b][i] += w * GN(g, a, i) * tau * adv[b];
+                }
+            }
+    }
+    return 0;
+}
+
+int hbo_tangent(const hbo_problem* p, const int* row_ptr, const int* col_idx,
+                const double* state, double* vals) {
+    const int N = p->N;
     memset(vals, 0, sizeof(double) * (size_t)row_ptr[p->nn] * 8 * N);
     for (int e = 0; e < p->ne; ++e) {
         const int* cn = p->conn + 4 * e;
         const double* g = p->geom + 22 * (size_t)e;
-        const double V = GV(g), w = V / 4.0;
         int blk[4][4];
         for (int a = 0; a < 4; ++a)
             for (int b = 0; b < 4; ++b)
@@ -416,48 +465,9 @@ int hbo_tangent(const hbo_problem* p, const int* row_ptr, const int* col_idx,
             for (int a = 0; a < 4; ++a)
                 for (int i = 0; i < 3; ++i)
                     u[a][i] = state[((size_t)cn[a] * 4 + i) * N + n];
-            /* element_tangent_p (assembly.cpp:265-374) at sample n */
-            double K[4][4], G[4][4][3], D[4][4][3], L[4][4], gg[4][4];
-            for (int a = 0; a < 4; ++a)
-                for (int b = 0; b < 4; ++b) {
-                    gg[a][b] = GN(g, a, 0) * GN(g, b, 0) + GN(g, a, 1) * GN(g, b, 1) +
-                               GN(g, a, 2) * GN(g, b, 2);
-                    K[a][b] = mu * V * gg[a][b] + pc * (a == b ? V / 10.0 : V / 20.0);
-                    L[a][b] = 0.0;
-                    for (int i = 0; i < 3; ++i) {
-                        G[a][b][i] = -GN(g, a, i) * V / 4.0;
-                        D[a][b][i] = GN(g, b, i) * V / 4.0;
-                    }
-                }
-            double tau_mean = 0.0;
-            if (p->tau_mode == 1) {
-                double um[3] = {0, 0, 0};
-                for (int a = 0; a < 4; ++a)
-                    for (int i = 0; i < 3; ++i)
-                        um[i] += 0.25 * u[a][i];
-                if (tau_of(g, um, nu, &tau_mean))
-                    return -1;
-            }
-            for (int q = 0; q < 4; ++q) {
-                double uq[3] = {0, 0, 0}, adv[4];
-                for (int i = 0; i < 3; ++i)
-                    for (int a = 0; a < 4; ++a)
-                        uq[i] += tet_shape(q, a) * u[a][i];
-                double tau = tau_mean;
-                if (p->tau_mode == 0 && tau_of(g, uq, nu, &tau))
-                    return -1;
-                for (int a = 0; a < 4; ++a)
-                    adv[a] = uq[0] * GN(g, a, 0) + uq[1] * GN(g, a, 1) + uq[2] * GN(g, a, 2);
-                for (int a = 0; a < 4; ++a)
-                    for (int b = 0; b < 4; ++b) {
-                        K[a][b] += w * rho * (tet_shape(q, a) * adv[b] + adv[a] * tau * adv[b]);
-                        L[a][b] += w * gg[a][b] * tau / rho;
-                        for (int i = 0; i < 3; ++i) {
-                            G[a][b][i] += w * adv[a] * tau * GN(g, b, i);
-                            D[a][b][i] += w * GN(g, a, i) * tau * adv[b];
-                        }
-                    }
-            }
+            double K[4][4], G[4][4][3], D[4][4][3], L[4][4];
+            if (element_tangent_n(p, g, u, K, G, D, L))
+                return -1;
             /* masked scatter (assembly.cpp:574-610) */
             for (int a = 0; a < 4; ++a) {
                 const int afix = p->dirichlet[cn[a]] != 0;
@@ -927,4 +937,354 @@ void hbo_time_tangent(const hbo_problem* p, const int* row_ptr, const int* col_i
     for (int A = 0; A < p->nn; ++A)
         if (p->dirichlet[A])
             vals[8 * (size_t)hbo_find(row_ptr, col_idx, A, A)] = 1.0;
+}
+
+/* ---------------------------------------------------------------- row subsets
+ *
+ * The residual rows and P block rows of a given node list, computed with the
+ * same per-entry summation order as hbo_residual / hbo_tangent (element order,
+ * then facet order), so each returned entry is bit-identical to the full
+ * assembly's.  They exist so that parity can be checked on full-size meshes
+ * (millions of elements, P.vals beyond 2^31 doubles) in seconds. */
+
+/* Elements incident to each listed row, ascending: CSR (ptr[nrows+1], elem). */
+static int incident_elements(const hbo_problem* p, int nrows, const int* rows, int** ptr_out,
+                             int** elem_out) {
+    int* slot = malloc(sizeof(int) * (size_t)p->nn);
+    int* ptr = calloc((size_t)nrows + 1, sizeof(int));
+    if (!slot || !ptr) {
+        free(slot);
+        free(ptr);
+        return -1;
+    }
+    for (int A = 0; A < p->nn; ++A)
+        slot[A] = -1;
+    for (int k = 0; k < nrows; ++k) {
+        if (rows[k] < 0 || rows[k] >= p->nn || slot[rows[k]] >= 0) {
+            free(slot);
+            free(ptr);
+            return -2; /* out of range or repeated */
+        }
+        slot[rows[k]] = k;
+    }
+    for (int e = 0; e < p->ne; ++e)
+        for (int a = 0; a < 4; ++a) {
+            const int k = slot[p->conn[4 * e + a]];
+            if (k >= 0)
+                ptr[k + 1] += 1;
+        }
+    for (int k = 0; k < nrows; ++k)
+        ptr[k + 1] += ptr[k];
+    int* elem = malloc(sizeof(int) * (size_t)(ptr[nrows] > 0 ? ptr[nrows] : 1));
+    int* fill = malloc(sizeof(int) * (size_t)(nrows > 0 ? nrows : 1));
+    for (int k = 0; k < nrows; ++k)
+        fill[k] = ptr[k];
+    for (int e = 0; e < p->ne; ++e)
+        for (int a = 0; a < 4; ++a) {
+            const int k = slot[p->conn[4 * e + a]];
+            if (k >= 0)
+                elem[fill[k]++] = e;
+        }
+    free(fill);
+    free(slot);
+    *ptr_out = ptr;
+    *elem_out = elem;
+    return 0;
+}
+
+static int local_index(const int* cn, int A) {
+    for (int a = 0; a < 4; ++a)
+        if (cn[a] == A)
+            return a;
+    return -1;
+}
+
+int hbo_residual_rows(const hbo_problem* p, const double* state, int nrows, const int* rows,
+                      double* r) {
+    const int N = p->N;
+    if (N > 64)
+        return -3;
+    int *ptr, *elem;
+    const int st = incident_elements(p, nrows, rows, &ptr, &elem);
+    if (st)
+        return st;
+    double* s = malloc(sizeof(double) * 3 * (size_t)N);
+    double* hs = malloc(sizeof(double) * (size_t)N);
+    int status = 0;
+    for (int k = 0; k < nrows && !status; ++k) {
+        const int A = rows[k];
+        double* rA = r + (size_t)k * 4 * N;
+        memset(rA, 0, sizeof(double) * 4 * (size_t)N);
+        memset(s, 0, sizeof(double) * 3 * (size_t)N);
+        for (int t = ptr[k]; t < ptr[k + 1] && !status; ++t) {
+            const int e = elem[t];
+            const int* cn = p->conn + 4 * e;
+            const double* g = p->geom + 22 * (size_t)e;
+            const int la = local_index(cn, A);
+            /* nodal H*u of the element's nodes (assembly.cpp:453-463) */
+            double hu4[4][3][64];
+            for (int a = 0; a < 4; ++a)
+                for (int i = 0; i < 3; ++i)
+                    apply_h(N, p->H, state + ((size_t)cn[a] * 4 + i) * N, hu4[a][i]);
+            for (int n = 0; n < N; ++n) {
+                double u[4][3], pr[4], h4[4][3], rm[4][3] = {{0}}, rc[4] = {0}, sv[4][3] = {{0}};
+                for (int a = 0; a < 4; ++a) {
+                    for (int i = 0; i < 3; ++i) {
+                        u[a][i] = state[((size_t)cn[a] * 4 + i) * N + n];
+                        h4[a][i] = hu4[a][i][n];
+                    }
+                    pr[a] = state[((size_t)cn[a] * 4 + 3) * N + n];
+                }
+                if (element_residual_n(p, g, u, pr, h4, rm, rc, sv)) {
+                    status = -1;
+                    break;
+                }
+                for (int i = 0; i < 3; ++i) {
+                    rA[(size_t)i * N + n] += rm[la][i];
+                    s[(size_t)i * N + n] += sv[la][i];
+                }
+                rA[(size_t)3 * N + n] += rc[la];
+            }
+        }
+        if (status)
+            break;
+        /* r_m -= H s (assembly.cpp:523-535) */
+        for (int i = 0; i < 3; ++i) {
+            apply_h(N, p->H, s + (size_t)i * N, hs);
+            for (int n = 0; n < N; ++n)
+                rA[(size_t)i * N + n] -= hs[n];
+        }
+        /* Neumann traction + backflow of the facets touching A (assembly.cpp:376-413) */
+        for (int f = 0; f < p->nfac; ++f) {
+            const int* fac = p->fac + 3 * f;
+            int la = -1;
+            for (int a = 0; a < 3; ++a)
+                if (fac[a] == A)
+                    la = a;
+            if (la < 0)
+                continue;
+            const double* nv = p->fnormal + 3 * f;
+            const double* h = p->h + (size_t)p->fbc[f] * N;
+            const double w = p->farea[f] / 3.0;
+            for (int q = 0; q < 3; ++q)
+                for (int n = 0; n < N; ++n) {
+                    double uq[3] = {0, 0, 0};
+                    for (int a = 0; a < 3; ++a)
+                        for (int i = 0; i < 3; ++i)
+                            uq[i] += tri_shape(q, a) * state[((size_t)fac[a] * 4 + i) * N + n];
+                    const double un = uq[0] * nv[0] + uq[1] * nv[1] + uq[2] * nv[2];
+                    const double neg = un < 0.0 ? un : 0.0;
+                    for (int i = 0; i < 3; ++i)
+                        rA[(size_t)i * N + n] += w * tri_shape(q, la) *
+                                                 (-h[n] * nv[i] - 0.5 * p->rho * p->beta * neg * uq[i]);
+                }
+        }
+        /* resistance outlets (see hbgls_oracle.h) */
+        if (p->resistance) {
+            const int nk = neumann_entries(p);
+            for (int kk = 0; kk < nk; ++kk) {
+                const double R = p->resistance[kk];
+                if (R == 0.0)
+                    continue;
+                for (int n = 0; n < N; ++n) {
+                    const double RQ = R * entry_flux(p, kk, state, n, 0);
+                    for (int f = 0; f < p->nfac; ++f) {
+                        if (p->fbc[f] != kk)
+                            continue;
+                        const int* fac = p->fac + 3 * f;
+                        const double* nv = p->fnormal + 3 * f;
+                        const double w = p->farea[f] / 3.0;
+                        for (int q = 0; q < 3; ++q)
+                            for (int a = 0; a < 3; ++a) {
+                                if (fac[a] != A)
+                                    continue;
+                                for (int i = 0; i < 3; ++i)
+                                    rA[(size_t)i * N + n] += w * tri_shape(q, a) * RQ * nv[i];
+                            }
+                    }
+                }
+            }
+        }
+        if (p->dirichlet[A])
+            memset(rA, 0, sizeof(double) * 3 * (size_t)N);
+    }
+    free(s);
+    free(hs);
+    free(ptr);
+    free(elem);
+    return status;
+}
+
+int hbo_tangent_rows(const hbo_problem* p, const int* row_ptr, const int* col_idx,
+                     const double* state, int nrows, const int* rows, double* vals) {
+    const int N = p->N;
+    int *ptr, *elem;
+    const int st = incident_elements(p, nrows, rows, &ptr, &elem);
+    if (st)
+        return st;
+    size_t off = 0;
+    int status = 0;
+    for (int k = 0; k < nrows && !status; ++k) {
+        const int A = rows[k];
+        const int r0 = row_ptr[A], nb = row_ptr[A + 1] - r0;
+        double* vA = vals + off;
+        off += (size_t)nb * 8 * N;
+        memset(vA, 0, sizeof(double) * (size_t)nb * 8 * N);
+        const int afix = p->dirichlet[A] != 0;
+        for (int t = ptr[k]; t < ptr[k + 1] && !status; ++t) {
+            const int e = elem[t];
+            const int* cn = p->conn + 4 * e;
+            const double* g = p->geom + 22 * (size_t)e;
+            const int la = local_index(cn, A);
+            int blk[4];
+            for (int b = 0; b < 4; ++b)
+                blk[b] = hbo_find(row_ptr, col_idx, A, cn[b]) - r0;
+            for (int n = 0; n < N; ++n) {
+                double u[4][3];
+                for (int a = 0; a < 4; ++a)
+                    for (int i = 0; i < 3; ++i)
+                        u[a][i] = state[((size_t)cn[a] * 4 + i) * N + n];
+                double K[4][4], G[4][4][3], D[4][4][3], L[4][4];
+                if (element_tangent_n(p, g, u, K, G, D, L)) {
+                    status = -1;
+                    break;
+                }
+                for (int b = 0; b < 4; ++b) {
+                    const int bfix = p->dirichlet[cn[b]] != 0;
+                    double* v = vA + (size_t)blk[b] * 8 * N + n;
+                    if (!afix && !bfix)
+                        v[0] += K[la][b];
+                    for (int i = 0; i < 3; ++i) {
+                        if (!afix)
+                            v[(size_t)(1 + i) * N] += G[la][b][i];
+                        if (!bfix)
+                            v[(size_t)(4 + i) * N] += D[la][b][i];
+                    }
+                    v[(size_t)7 * N] += L[la][b];
+                }
+            }
+        }
+        if (status)
+            break;
+        if (p->backflow_in_tangent && !afix) {
+            /* frozen-coefficient backflow tangent (assembly.cpp:612-657), row A */
+            for (int f = 0; f < p->nfac; ++f) {
+                const int* fac = p->fac + 3 * f;
+                int la = -1;
+                for (int a = 0; a < 3; ++a)
+                    if (fac[a] == A)
+                        la = a;
+                if (la < 0)
+                    continue;
+                const double* nv = p->fnormal + 3 * f;
+                const double w = p->farea[f] / 3.0;
+                for (int q = 0; q < 3; ++q)
+                    for (int n = 0; n < N; ++n) {
+                        double uq[3] = {0, 0, 0};
+                        for (int a = 0; a < 3; ++a)
+                            for (int i = 0; i < 3; ++i)
+                                uq[i] += tri_shape(q, a) * state[((size_t)fac[a] * 4 + i) * N + n];
+                        const double un = uq[0] * nv[0] + uq[1] * nv[1] + uq[2] * nv[2];
+                        if (!(un < 0.0))
+                            continue;
+                        for (int b = 0; b < 3; ++b) {
+                            if (p->dirichlet[fac[b]])
+                                continue;
+                            const int kb = hbo_find(row_ptr, col_idx, A, fac[b]) - r0;
+                            const double c = w * tri_shape(q, la) * tri_shape(q, b) * 0.5 * p->rho *
+                                             p->beta;
+                            vA[(size_t)kb * 8 * N + n] -= c * un;
+                        }
+                    }
+            }
+        }
+        if (afix) {
+            /* identity on constrained velocity diagonals (assembly.cpp:659-665) */
+            const int kd = hbo_find(row_ptr, col_idx, A, A) - r0;
+            for (int n = 0; n < N; ++n)
+                vA[(size_t)kd * 8 * N + n] = 1.0;
+        }
+    }
+    free(ptr);
+    free(elem);
+    return status;
+}
+
+int hbo_tangent_matvec_rows(const hbo_problem* p, const int* row_ptr, const int* col_idx,
+                            const double* row_vals, const double* mass, const double* y, int nrows,
+                            const int* rows, double* out) {
+    const int N = p->N;
+    double* t = malloc(sizeof(double) * 3 * (size_t)N);
+    double* ht = malloc(sizeof(double) * (size_t)N);
+    size_t off = 0;
+    for (int r = 0; r < nrows; ++r) {
+        const int A = rows[r];
+        if (A < 0 || A >= p->nn) {
+            free(t);
+            free(ht);
+            return -2;
+        }
+        double* o = out + (size_t)r * 4 * N;
+        memset(o, 0, sizeof(double) * 4 * (size_t)N);
+        /* BlockSparseMatrix::matvec row A (linalg.cpp:41-76) */
+        for (int k = row_ptr[A]; k < row_ptr[A + 1]; ++k) {
+            const double* v = row_vals + off + (size_t)(k - row_ptr[A]) * 8 * N;
+            const double* yb = y + (size_t)col_idx[k] * 4 * N;
+            for (int n = 0; n < N; ++n) {
+                const double yp = yb[3 * N + n];
+                double op = v[7 * N + n] * yp;
+                for (int i = 0; i < 3; ++i) {
+                    o[i * N + n] += v[n] * yb[i * N + n] + v[(1 + i) * N + n] * yp;
+                    op += v[(4 + i) * N + n] * yb[i * N + n];
+                }
+                o[3 * N + n] += op;
+            }
+        }
+        off += (size_t)(row_ptr[A + 1] - row_ptr[A]) * 8 * N;
+        if (p->dirichlet[A])
+            continue;
+        /* H (x) mass part (linalg.cpp:84-127) */
+        memset(t, 0, sizeof(double) * 3 * (size_t)N);
+        for (int k = row_ptr[A]; k < row_ptr[A + 1]; ++k) {
+            const int B = col_idx[k];
+            if (p->dirichlet[B])
+                continue;
+            for (int j = 0; j < 3 * N; ++j)
+                t[j] += mass[k] * y[(size_t)B * 4 * N + j];
+        }
+        for (int i = 0; i < 3; ++i) {
+            apply_h(N, p->H, t + i * N, ht);
+            for (int n = 0; n < N; ++n)
+                o[(size_t)i * N + n] += ht[n];
+        }
+        /* resistance outlets, free rows and columns (see hbgls_oracle.h) */
+        if (p->resistance) {
+            const int nk = neumann_entries(p);
+            for (int kk = 0; kk < nk; ++kk) {
+                const double R = p->resistance[kk];
+                if (R == 0.0)
+                    continue;
+                for (int n = 0; n < N; ++n) {
+                    const double RQ = R * entry_flux(p, kk, y, n, 1);
+                    for (int f = 0; f < p->nfac; ++f) {
+                        if (p->fbc[f] != kk)
+                            continue;
+                        const int* fac = p->fac + 3 * f;
+                        const double* nv = p->fnormal + 3 * f;
+                        const double w = p->farea[f] / 3.0;
+                        for (int q = 0; q < 3; ++q)
+                            for (int a = 0; a < 3; ++a) {
+                                if (fac[a] != A)
+                                    continue;
+                                for (int i = 0; i < 3; ++i)
+                                    o[(size_t)i * N + n] += w * tri_shape(q, a) * RQ * nv[i];
+                            }
+                    }
+                }
+            }
+        }
+    }
+    free(t);
+    free(ht);
+    return 0;
 }

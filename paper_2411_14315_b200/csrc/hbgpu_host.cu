@@ -1312,6 +1312,12 @@ int hbgpu_set_basis(hbgpu_ctx* c, int modes, double period) {
         return fail(c, HBGPU_ERR_PARSE, "spectral basis requires at least one mode (M >= 1)");
     if (!(period > 0.0))
         return fail(c, HBGPU_ERR_PARSE, "spectral basis requires a positive period");
+    if (modes > HBGPU_MAX_MODES)
+        return fail(c, HBGPU_ERR_INVALID,
+                    "spectral basis: M = " + std::to_string(modes) + " exceeds the supported maximum " +
+                        std::to_string(HBGPU_MAX_MODES) + " (N = 2M-1 <= " +
+                        std::to_string(2 * HBGPU_MAX_MODES - 1) +
+                        " time samples; the dense H lives in shared memory)");
     c->M = modes;
     c->N = 2 * modes - 1;
     c->period = period;
@@ -1528,6 +1534,12 @@ int hbgpu_set_assembly_config(hbgpu_ctx* c, int tau_mode, double pseudo_dt, doub
 int hbgpu_set_bcs(hbgpu_ctx* c, const double* dirichlet_g, int n_neumann, const int* neumann_patch,
                   const double* neumann_h, double backflow_beta) {
     TRY(ensure_basis(c));
+    // validate everything before any context state changes
+    if (n_neumann < 0 || (n_neumann > 0 && (!neumann_patch || !neumann_h)))
+        return fail(c, HBGPU_ERR_INVALID, "set_bcs: bad Neumann arguments");
+    for (int k = 0; k < n_neumann; ++k)
+        if (neumann_patch[k] < 0 || neumann_patch[k] >= int(c->patches.size()))
+            return fail(c, HBGPU_ERR_INVALID, "Neumann entry references an unknown patch");
     const int N = c->N;
     const size_t gl = size_t(c->nn) * 3 * size_t(N);
     if (dirichlet_g)
@@ -1539,9 +1551,6 @@ int hbgpu_set_bcs(hbgpu_ctx* c, const double* dirichlet_g, int n_neumann, const 
     c->beta = backflow_beta;
     c->bc_patch.assign(neumann_patch, neumann_patch + n_neumann);
     c->h_h.assign(neumann_h, neumann_h + size_t(n_neumann) * size_t(N));
-    for (int k = 0; k < n_neumann; ++k)
-        if (neumann_patch[k] < 0 || neumann_patch[k] >= int(c->patches.size()))
-            return fail(c, HBGPU_ERR_INVALID, "Neumann entry references an unknown patch");
     // facet arrays over the Neumann list (assembly.cpp:537-539 order) and
     // per-node incidence lists in that order
     std::vector<int> fac, fbc;
@@ -1856,6 +1865,27 @@ int hbgpu_get_pvals(hbgpu_ctx* c, double* pvals) {
     return HBGPU_OK;
 }
 
+int hbgpu_get_pvals_rows(hbgpu_ctx* c, int nrows, const int* rows, double* out) {
+    if (!c->p_valid)
+        return fail(c, HBGPU_ERR_INVALID, "get_pvals_rows before assemble_tangent / set_pvals");
+    if (nrows < 0 || (nrows > 0 && (!rows || !out)))
+        return fail(c, HBGPU_ERR_INVALID, "get_pvals_rows: bad arguments");
+    CK(c, cudaStreamSynchronize(c->stream));
+    const size_t seg = 8 * size_t(c->N);
+    size_t off = 0;
+    for (int k = 0; k < nrows; ++k) {
+        const int A = rows[k];
+        if (A < 0 || A >= c->nn)
+            return fail(c, HBGPU_ERR_INVALID, "get_pvals_rows: node out of range");
+        const size_t r0 = size_t(c->row_ptr_h[size_t(A)]), r1 = size_t(c->row_ptr_h[size_t(A) + 1]);
+        CK(c, cudaMemcpyAsync(out + off, c->pvals.p + r0 * seg, sizeof(double) * (r1 - r0) * seg,
+                              cudaMemcpyDeviceToHost, c->stream));
+        off += (r1 - r0) * seg;
+    }
+    CK(c, cudaStreamSynchronize(c->stream));
+    return HBGPU_OK;
+}
+
 int hbgpu_matvec_dev(hbgpu_ctx* c, const double* d_y, double* d_out) {
     TRY(ensure_basis(c));
     return matvec_dev(c, d_y, d_out, nullptr, true);
@@ -1965,32 +1995,17 @@ int hbgpu_gmres(hbgpu_ctx* c, const double* rhs, const double* inv_diag, const h
 }
 
 // solve_harmonic (hb_solver.cpp:113-221)
-int hbgpu_solve_harmonic(hbgpu_ctx* c, const hbgpu_solver_cfg* cfg, double* state_out,
-                         hbgpu_solve_info* info, int cap, int* log_iter, double* log_res,
-                         double* log_rel, int* log_lin, double* log_sec) {
-    TRY(ensure_basis(c));
-    Timer total;
+// The Newton loop of solve_harmonic; every exit (including a failed CUDA call
+// or launch) returns through hbgpu_solve_harmonic, which fills the log/info
+// and the state as the reference's partial ConvergenceLog would be.
+extern "C++" {
+template <class LogFn>
+static int solve_harmonic_run(hbgpu_ctx* c, const hbgpu_solver_cfg* cfg, hbgpu_solve_info& inf,
+                              LogFn&& log) {
     const int N = c->N;
     const long n = long(c->state_len());
     cudaStream_t st = c->stream;
-    hbgpu_solve_info inf{};
-    auto log = [&](int iter, double res, double rel, int lin, double sec) {
-        if (inf.entries < cap) {
-            if (log_iter) log_iter[inf.entries] = iter;
-            if (log_res) log_res[inf.entries] = res;
-            if (log_rel) log_rel[inf.entries] = rel;
-            if (log_lin) log_lin[inf.entries] = lin;
-            if (log_sec) log_sec[inf.entries] = sec;
-            inf.entries += 1;
-        }
-    };
-    auto finish = [&](int code) {
-        inf.total_seconds = total.seconds();
-        if (info) *info = inf;
-        if (state_out)
-            cudaMemcpy(state_out, c->state.p, sizeof(double) * size_t(n), cudaMemcpyDeviceToHost);
-        return code;
-    };
+    auto finish = [](int code) { return code; };
 
     // rest + Dirichlet data + outlet pressure level (hb_solver.cpp:119-132,
     // assembly.cpp:415-441)
@@ -2044,8 +2059,10 @@ int hbgpu_solve_harmonic(hbgpu_ctx* c, const hbgpu_solver_cfg* cfg, double* stat
         return finish(fail(c, HBGPU_ERR_GEOMETRY, "CFL number needs a Dirichlet inlet patch with positive area"));
     inf.pseudo_dt = dt;
     inf.cfl = u_c * dt / c->h_c;
+    // a fresh AssemblyConfig per solve (hb_solver.cpp:140-146): pseudo_c1 = 1.5
     c->tau_mode = cfg->tau_mode;
     c->pseudo_dt = dt;
+    c->pseudo_c1 = 1.5;
     c->backflow_tangent = cfg->backflow_in_tangent;
 
     {
@@ -2114,6 +2131,46 @@ int hbgpu_solve_harmonic(hbgpu_ctx* c, const hbgpu_solver_cfg* cfg, double* stat
     }
     return finish(HBGPU_OK);
 }
+}  // extern "C++"
+
+int hbgpu_solve_harmonic(hbgpu_ctx* c, const hbgpu_solver_cfg* cfg, double* state_out,
+                         hbgpu_solve_info* info, int cap, int* log_iter, double* log_res,
+                         double* log_rel, int* log_lin, double* log_sec) {
+    TRY(ensure_basis(c));
+    if (!cfg)
+        return fail(c, HBGPU_ERR_INVALID, "solve_harmonic: null config");
+    Timer total;
+    hbgpu_solve_info inf{};
+    auto log = [&](int iter, double res, double rel, int lin, double sec) {
+        if (inf.entries < cap) {
+            if (log_iter) log_iter[inf.entries] = iter;
+            if (log_res) log_res[inf.entries] = res;
+            if (log_rel) log_rel[inf.entries] = rel;
+            if (log_lin) log_lin[inf.entries] = lin;
+            if (log_sec) log_sec[inf.entries] = sec;
+            inf.entries += 1;
+        }
+    };
+    // the solve owns its AssemblyConfig; the caller's is restored afterwards
+    const int tau0 = c->tau_mode, bf0 = c->backflow_tangent;
+    const double dt0 = c->pseudo_dt, c10 = c->pseudo_c1;
+    const int code = solve_harmonic_run(c, cfg, inf, log);
+    c->tau_mode = tau0;
+    c->backflow_tangent = bf0;
+    c->pseudo_dt = dt0;
+    c->pseudo_c1 = c10;
+    inf.total_seconds = total.seconds();
+    if (info)
+        *info = inf;
+    if (state_out) {
+        const cudaError_t e = cudaMemcpy(state_out, c->state.p, sizeof(double) * size_t(c->state_len()),
+                                         cudaMemcpyDeviceToHost);
+        if (e != cudaSuccess && code == HBGPU_OK)
+            return fail(c, HBGPU_ERR_CUDA, std::string("solve_harmonic state copy: ") + cudaGetErrorString(e));
+    }
+    return code;
+}
+
 
 }  // extern "C"
 

@@ -171,6 +171,7 @@ _assemble = _sig("hbgpu_assemble", C.c_int, [_vp, _vp, _vp])
 _tangent = _sig("hbgpu_assemble_tangent", C.c_int, [_vp, _vp, _vp])
 _mass = _sig("hbgpu_assemble_mass", C.c_int, [_vp, _vp])
 _set_pvals = _sig("hbgpu_set_pvals", C.c_int, [_vp, _vp])
+_set_mass = _sig("hbgpu_set_mass", C.c_int, [_vp, _vp])
 _matvec = _sig("hbgpu_matvec", C.c_int, [_vp, _vp, _vp])
 _bsr_matvec = _sig("hbgpu_bsr_matvec", C.c_int, [_vp, _vp, _vp])
 _jacobi = _sig("hbgpu_jacobi", C.c_int, [_vp, _vp, _ip])
@@ -184,6 +185,7 @@ _jacobi_dev = _sig("hbgpu_jacobi_dev", C.c_int, [_vp, _ip])
 _gmres_dev = _sig("hbgpu_gmres_dev", C.c_int, [_vp, _vp, C.POINTER(_KrylovCfg), _vp, C.POINTER(_KrylovRes), _vp, C.c_int])
 _pvals_dev = _sig("hbgpu_pvals_dev", _vp, [_vp])
 _get_pvals = _sig("hbgpu_get_pvals", C.c_int, [_vp, _vp])
+_get_pvals_rows = _sig("hbgpu_get_pvals_rows", C.c_int, [_vp, C.c_int, _vp, _vp])
 _set_resistance = _sig("hbgpu_set_resistance", C.c_int, [_vp, C.c_int, _vp, _vp])
 _time_residual = _sig("hbgpu_time_residual", C.c_int, [_vp, _vp, _vp, _vp, C.c_double, _vp])
 _time_tangent = _sig("hbgpu_time_tangent", C.c_int, [_vp, _vp, C.c_double, C.c_double, C.c_double, _vp])
@@ -402,6 +404,17 @@ class GpuContext:
         self._check(_get_pvals(self._h, _ptr(v)))
         return v
 
+    def pvals_rows(self, rows, row_ptr=None) -> np.ndarray:
+        """P block rows of the listed nodes, concatenated in list order
+        (hbgpu_get_pvals_rows): a sample of P without reading all of it."""
+        rows = np.ascontiguousarray(rows, np.int32)
+        if row_ptr is None:
+            row_ptr = self.pattern()[0]
+        tot = int(np.sum(row_ptr[rows + 1].astype(np.int64) - row_ptr[rows])) * 8 * self.N
+        v = np.empty(tot)
+        self._check(_get_pvals_rows(self._h, len(rows), _ptr(rows), _ptr(v)))
+        return v
+
     def set_resistance(self, resistance: dict):
         """{neumann patch index: R} resistance outlets (hbgpu_set_resistance)."""
         pk = np.array(list(resistance.keys()), np.int32)
@@ -462,6 +475,13 @@ class GpuContext:
         if p.size != self.nnz * 8 * self.N:
             raise ValueError("P values size mismatch")
         self._check(_set_pvals(self._h, _ptr(p)))
+
+    def set_mass(self, mass):
+        """Replace the device node-pair mass (TangentOperator::mass)."""
+        m = _f64(mass).reshape(-1)
+        if m.size != self.nnz:
+            raise ValueError("mass size mismatch")
+        self._check(_set_mass(self._h, _ptr(m)))
 
     def matvec(self, y) -> np.ndarray:
         v = self._vec_in(y)

@@ -616,3 +616,93 @@ def test_gmres_device_and_host_loops(gpu, monkeypatch, restart):
     assert rel(dev.x, host.x) < 1e-7
     n = min(len(dev.history), len(host.history))
     assert n > 1 and np.allclose(dev.history[:n], host.history[:n], rtol=1e-6, atol=1e-14)
+
+
+def test_gmres_stagnation_zero_operator(gpu):
+    """gmres_solve on a zero operator stagnates and returns the best iterate
+    with relative residual 1 (test_linalg.cpp:239-247, linalg.cpp:286-289):
+    P = 0 and mass = 0 through the C ABI, unit inverse diagonal."""
+    from paper_2411_14315_b200.hbgpu import KrylovConfig
+
+    prob = tube_problem(2, traction=False)
+    ctx = gpu_ctx(prob)
+    n, nnz, N = ctx.state_len, ctx.nnz, prob.N
+    ctx.set_pvals(np.zeros(nnz * 8 * N))
+    ctx.set_mass(np.zeros(nnz))
+    b = np.ones(n)
+    res = ctx.gmres(b, KrylovConfig(), inv_diag=np.ones(n))
+    assert res.status == 2
+    assert abs(res.relative_residual - 1.0) < 1e-12
+    assert not res.x.any()
+    orc = ob.Restated(prob)
+    ref = orc.gmres(np.zeros(nnz * 8 * N), np.zeros(nnz), b, np.ones(n))
+    assert ref["status"] == 2 and abs(ref["relative_residual"] - 1.0) < 1e-12
+
+
+def test_solve_divergence_errors(gpu):
+    """DivergenceError exactly where solve_harmonic throws it
+    (hb_solver.cpp:165-186): a residual ratio above divergence_ratio, and a
+    non-finite residual; the partial ConvergenceLog is kept."""
+    from paper_2411_14315_b200.hbgpu import DivergenceError, GpuContext, SolverConfig
+
+    prob = cases.config_problem(0, mesh=cases.meshgen.hex_cylinder(0.3, 1.0, 3, 3, 6))
+    ctx = GpuContext(prob.mesh)
+    ctx.set_basis(prob.modes, prob.period)
+    ctx.set_fluid(prob.rho, prob.mu)
+    ctx.set_bcs(prob.dirichlet_g, prob.neumann, prob.backflow_beta)
+    with pytest.raises(DivergenceError) as ei:
+        ctx.solve_harmonic(SolverConfig(divergence_ratio=0.5, max_newton_iters=3))
+    # iteration 0 has rel = 1 > 0.5: one log entry, then the throw
+    assert ei.value.partial_log_csv.count("\n") == 2
+    g = prob.dirichlet_g.copy()
+    g[np.flatnonzero(g)[:1]] = np.nan
+    ctx.set_bcs(g, prob.neumann, prob.backflow_beta)
+    with pytest.raises(DivergenceError, match="not finite"):
+        ctx.solve_harmonic(SolverConfig(max_newton_iters=3))
+    # the context's assembly config is untouched by the failed solves
+    ctx.set_bcs(prob.dirichlet_g, prob.neumann, prob.backflow_beta)
+    ctx.set_assembly_config(0, 0.3)
+    orc = ob.Restated(prob, tau_mode=0, pseudo_dt=0.3)
+    s = cases.random_state(prob.mesh.num_nodes, prob.N, 9)
+    assert rel(ctx.assemble_tangent(s), orc.tangent(s)) < TOL
+
+
+def test_solve_restores_assembly_config(gpu):
+    """solve_harmonic builds its own AssemblyConfig (pseudo_c1 = 1.5, the
+    solver's tau mode and pseudo-dt) and restores the caller's afterwards."""
+    from paper_2411_14315_b200.hbgpu import SolverConfig
+
+    prob = tube_problem(3, h=0.25, traction=False)
+    ctx = gpu_ctx(prob, 1, 0.7)
+    ctx.set_assembly_config(1, 0.7, 2.5, False)
+    ctx.solve_harmonic(SolverConfig(max_newton_iters=2))
+    orc = ob.Restated(prob, tau_mode=1, pseudo_dt=0.7, pseudo_c1=2.5)
+    s = cases.random_state(prob.mesh.num_nodes, prob.N, 19)
+    assert rel(ctx.assemble_tangent(s), orc.tangent(s)) < TOL
+
+
+def test_max_modes_and_bcs_validation(gpu):
+    """M = 32 (N = 63, the supported maximum) matches the oracle; M = 33 is
+    rejected by set_basis; set_bcs with a bad patch index leaves the
+    context's boundary data unchanged."""
+    from paper_2411_14315_b200 import meshgen
+
+    mesh = meshgen.cube_delaunay(1500, seed=21)
+    M = 32
+    N = 2 * M - 1
+    neu = [(k, np.full(N, 20.0)) for k, p in enumerate(mesh.patches) if p.kind == NEUMANN]
+    prob = Problem(mesh, M, 1.0, 1.06, 0.04, np.zeros(mesh.num_nodes * 3 * N), neu, 0.2)
+    ctx = gpu_ctx(prob, 0, 0.05)
+    orc = ob.Restated(prob, tau_mode=0, pseudo_dt=0.05)
+    s = cases.random_modes_state(mesh.num_nodes, M, 5)
+    r0 = ctx.assemble_residual(s)
+    assert rel(r0, orc.residual(s)) < TOL
+    p = ctx.assemble_tangent(s)
+    assert rel(p, orc.tangent(s)) < TOL
+    y = cases.random_state(mesh.num_nodes, N, 6)
+    assert rel(ctx.matvec(y), orc.matvec(p, orc.mass(), y)) < TOL
+    with pytest.raises(ValueError):
+        ctx.set_bcs(None, [(len(mesh.patches) + 1, np.zeros(N))], 0.2)
+    assert np.array_equal(ctx.assemble_residual(s), r0)
+    with pytest.raises(ValueError):
+        ctx.set_basis(33, 1.0)

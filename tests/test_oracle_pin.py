@@ -130,3 +130,47 @@ def test_resistance_restatement_is_consistent():
     d_l = o1.matvec(p, m, y) - o0.matvec(p, m, y)
     assert np.linalg.norm(d_l) > 0
     assert np.linalg.norm(d_r - d_l) <= 1e-10 * np.linalg.norm(d_l)
+
+
+@pytest.mark.parametrize("name", ["tube_m3_qp", "tube_m4_mean", "bifurcation_m3"])
+def test_row_subsets_equal_full_assembly(name):
+    """hbo_residual_rows / hbo_tangent_rows (the full-size parity checkers) give
+    exactly the rows of the full assembly: same per-entry summation order, so
+    bit-identical, including Dirichlet rows, boundary rows and the backflow
+    tangent."""
+    prob, d = load(name)
+    for bf in (False, True):
+        orc = ob.Restated(prob, tau_mode=int(d["tau_mode"]), pseudo_dt=d["pseudo_dt_eff"], backflow_tangent=bf)
+        s = d["state"]
+        nn, N = orc.nn, orc.N
+        rows = np.random.default_rng(3).permutation(nn)[: max(5, nn // 3)].astype(np.int32)
+        rows = np.concatenate([rows[rows != nn - 1], [nn - 1]]).astype(np.int32)
+        full_r = orc.residual(s).reshape(nn, 4, N)
+        assert np.array_equal(orc.residual_rows(s, rows), full_r[rows])
+        full_p = orc.tangent(s)
+        rp = orc.row_ptr
+        want = np.concatenate([full_p[rp[A] * 8 * N: rp[A + 1] * 8 * N] for A in rows])
+        assert np.array_equal(orc.tangent_rows(s, rows), want)
+        m = orc.mass()
+        y = d["y"]
+        full_mv = orc.matvec(full_p, m, y).reshape(nn, 4, N)
+        assert np.array_equal(orc.matvec_rows(want, m, y, rows), full_mv[rows])
+    with pytest.raises(ob.OracleError):
+        orc.residual_rows(s, np.array([0, 0], np.int32))
+
+
+def test_row_subsets_resistance():
+    """Row subsets with a resistance outlet equal the full restated residual."""
+    prob, d = load("tube_m3_qp")
+    outlet = [k for k, _ in prob.neumann][0]
+    orc = ob.Restated(prob, tau_mode=int(d["tau_mode"]), pseudo_dt=d["pseudo_dt_eff"],
+                      resistance={outlet: 1.1e4})
+    s = d["state"]
+    rows = np.arange(0, orc.nn, 3, dtype=np.int32)
+    assert np.array_equal(orc.residual_rows(s, rows), orc.residual(s).reshape(orc.nn, 4, orc.N)[rows])
+    p = orc.tangent(s)
+    m = orc.mass()
+    rp, N = orc.row_ptr, orc.N
+    seg = np.concatenate([p[rp[A] * 8 * N: rp[A + 1] * 8 * N] for A in rows])
+    assert np.array_equal(orc.matvec_rows(seg, m, d["y"], rows),
+                          orc.matvec(p, m, d["y"]).reshape(orc.nn, 4, N)[rows])
