@@ -80,14 +80,20 @@ int main() {
     L.matvec(y, o_ref);
     gpu::matvec(L, y, o_gpu);
     const double e_inplace_op = rel(o_gpu, o_ref);
+    // ramped Dirichlet data edited in place (same vector): dirichlet_g enters
+    // through install_dirichlet in solve_harmonic (assembly.cpp:429-441)
     BoundaryConditionSet bcs2 = in.bcs;
-    const auto r_gpu2a = gpu::assemble_residual(mesh, geoms, state, ops, in.props, bcs2, acfg);
+    SolverConfig ramp;
+    ramp.max_newton_iters = 2;
+    ramp.krylov.tolerance = 1e-12;
+    ramp.krylov.max_iters = 4000;
+    const auto r_gpu2a = gpu::solve_harmonic(mesh, geoms, in.basis, in.props, bcs2, ramp);
     for (auto& g : bcs2.dirichlet_g)
-        g *= 0.5;  // ramped Dirichlet data, same vector
-    const auto r_ref2 = assemble_residual(mesh, geoms, state, ops, in.props, bcs2, acfg, 1);
-    const auto r_gpu2 = gpu::assemble_residual(mesh, geoms, state, ops, in.props, bcs2, acfg);
-    const double e_inplace_g = rel(r_gpu2, r_ref2);
-    const double d_g = rel(r_gpu2a, r_ref2);  // the edit is visible in the residual
+        g *= 0.5;
+    const auto s_ref2 = solve_harmonic(mesh, geoms, in.basis, in.props, bcs2, ramp);
+    const auto s_gpu2 = gpu::solve_harmonic(mesh, geoms, in.basis, in.props, bcs2, ramp);
+    const double e_inplace_g = rel(s_gpu2.state.data, s_ref2.state.data);
+    const double d_g = rel(r_gpu2a.state.data, s_ref2.state.data);  // the edit is visible
     assemble_tangent(mesh, geoms, state, in.props, in.bcs, acfg, L.P);  // restore P
     L.mass = assemble_mass(mesh, geoms, in.props.rho, *pattern);
 
@@ -132,7 +138,7 @@ int main() {
     const double e_time_u = rel(ts_gpu.cycle.u, ts_ref.cycle.u);
     const double e_time_p = rel(ts_gpu.cycle.p, ts_ref.cycle.p);
 
-    const bool ok = e_inplace_op < 1e-12 && e_inplace_g < 1e-12 && d_g > 1e-10 &&
+    const bool ok = e_inplace_op < 1e-12 && e_inplace_g < 1e-8 && d_g > 1e-3 &&
                     e_res < 1e-12 && e_tan < 1e-12 && e_mass < 1e-15 && e_mv < 1e-12 &&
                     e_jac < 1e-15 && gmres_scaled <= 1e-8 * 1.0001 && s_ref.log.converged &&
                     s_gpu.log.converged && e_solve < 1e-8 && e_time_u < 1e-8 && e_time_p < 1e-8 &&
