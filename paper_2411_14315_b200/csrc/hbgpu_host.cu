@@ -1416,10 +1416,32 @@ int hbgpu_set_basis(hbgpu_ctx* c, int modes, double period) {
                         b.nt = N;
                     }
                 }
+                // tooling: HBGPU_TAN_NT caps the sample tile of every pipe bucket
+                if (const char* tn = std::getenv("HBGPU_TAN_NT")) {
+                    const int cap = std::max(1, std::atoi(tn));
+                    if (b.pipe && cap < N) {
+                        b.nt = cap;
+                        double bestw = 0.0;
+                        for (int w : widths) {
+                            const size_t sm = ps(b.nt);
+                            const int by_smem = int(size_t(228 * 1024) / (sm + 1024));
+                            const int by_regs = 65536 / (w * 128);
+                            const int ctas = std::min({32, by_smem, by_regs});
+                            if (ctas < 1)
+                                continue;
+                            const double it2 = double(b.max_inc) * b.nt;
+                            const double score = it2 / (std::ceil(it2 / w) * w) * std::min(1.0, ctas * (w / 32) / 24.0);
+                            if (score > bestw * 1.0001) {
+                                bestw = score;
+                                b.threads = w;
+                            }
+                        }
+                    }
+                }
                 // tooling: HBGPU_TAN_WIDTH forces the CTA width of every pipe bucket
                 if (const char* tw = std::getenv("HBGPU_TAN_WIDTH")) {
                     const int w = std::atoi(tw);
-                    if (b.pipe && std::find(widths, widths + 5, w) != widths + 5 && ps(N) <= size_t(227 * 1024))
+                    if (b.pipe && std::find(widths, widths + 5, w) != widths + 5 && ps(b.nt) <= size_t(227 * 1024))
                         b.threads = w;
                 }
                 if (!b.pipe) {
@@ -1964,7 +1986,10 @@ int hbgpu_profile_read(hbgpu_ctx* c, int nphase, double* ms, int* count) {
 long long hbgpu_kernel_launches(void) { return g_launches.load(); }
 
 int hbgpu_fp64_peak(double* tflops) {
-    const int blocks = 148 * 8, threads = 256, iters = 4096;
+    int dev = 0, nsm = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    const int blocks = nsm * 4, threads = 256, iters = 16384;
     double* d = nullptr;
     if (cudaMalloc(&d, sizeof(double)) != cudaSuccess)
         return HBGPU_ERR_CUDA;
@@ -1973,7 +1998,7 @@ int hbgpu_fp64_peak(double* tflops) {
     cudaFree(d);
     if (e != cudaSuccess)
         return HBGPU_ERR_CUDA;
-    *tflops = 2.0 * 8.0 * double(iters) * blocks * threads / (double(ms) * 1e-3) / 1e12;
+    *tflops = 2.0 * 16.0 * double(iters) * blocks * threads / (double(ms) * 1e-3) / 1e12;
     return HBGPU_OK;
 }
 

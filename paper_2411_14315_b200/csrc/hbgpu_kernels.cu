@@ -95,44 +95,91 @@ void launch_geometry(const double* xyz, const int4* conn, int ne, double* geom, 
 // out[(A*os + i*N) + n] = sum_m H[n][m] in[(A*is + i*N) + m], i < 3: the
 // batched pseudo-spectral derivative of every velocity series
 // (assembly.cpp:453-463; SpectralOperators::apply_many, spectral.cpp:185-227).
-__global__ void apply_h_series_kernel(const double* __restrict__ H, int N,
-                                      const double* __restrict__ in, int is,
-                                      double* __restrict__ out, int os, int nnodes) {
+// It is a small GEMM, OUT[3 nn x N] = X[3 nn x N] H^T[N x N], register-tiled:
+// a CTA takes 16 nodes (48 series); thread (g, j) computes series 4g..4g+3 at
+// samples j, j+16, ..., j+16(SPT-1): per m, 4 + SPT shared loads feed 4 SPT
+// FMAs (the per-(series, sample) dot product it replaces needed two loads
+// per FMA).  H^T and the series tile sit in shared memory; the tile is
+// loaded with coalesced reads of each node's contiguous 3N velocity values.
+constexpr int kHNodes = 16, kHSeries = 3 * kHNodes, kHThreads = (kHSeries / 4) * 16;
+template <int SPT>
+__global__ void __launch_bounds__(kHThreads) apply_h_tile_kernel(const double* __restrict__ H, int N,
+                                                                 const double* __restrict__ in, int is,
+                                                                 double* __restrict__ out, int os, int nnodes) {
     extern __shared__ double sh[];
-    double* sH = sh;
-    const int per = blockDim.x / N;
-    double* sx = sh + N * N;  // the CTA's `per` series, staged once (coalesced)
-    for (int k = threadIdx.x; k < N * N; k += blockDim.x)
-        sH[k] = H[k];
-    const int ls = threadIdx.x / N, n = threadIdx.x - ls * N;
-    const long s = (long)blockIdx.x * per + ls;
-    const bool valid = ls < per && s < 3L * nnodes;
-    if (valid) {
-        const long A = s / 3;
-        const int i = (int)(s - 3 * A);
-        sx[ls * N + n] = __ldg(in + A * is + (long)i * N + n);
+    constexpr int NP = 16 * SPT;       // padded sample count of H^T rows
+    double* Ht = sh;                   // [m][NP], Ht[m][n] = H[n][m], zero-padded
+    double* Xs = sh + N * NP;          // [series][N + 1]
+    const int XS = N + 1;
+    for (int k = threadIdx.x; k < N * NP; k += blockDim.x) {
+        const int m = k / NP, n = k - m * NP;
+        Ht[k] = n < N ? H[n * N + m] : 0.0;
+    }
+    const long A0 = (long)blockIdx.x * kHNodes;
+    const int nloc = (int)min((long)kHNodes, (long)nnodes - A0);
+    for (int k = threadIdx.x; k < nloc * 3 * N; k += blockDim.x) {
+        const int ln = k / (3 * N), rem = k - ln * 3 * N, i = rem / N, m = rem - i * N;
+        Xs[(ln * 3 + i) * XS + m] = __ldg(in + (A0 + ln) * is + rem);
     }
     __syncthreads();
-    if (!valid)
-        return;
-    const long A = s / 3;
-    const int i = (int)(s - 3 * A);
-    const double* h = sH + n * N;
-    const double* x = sx + ls * N;
-    double acc = 0.0;
-    for (int m = 0; m < N; ++m)
-        acc += h[m] * x[m];
-    out[A * os + (long)i * N + n] = acc;
+    const int g = threadIdx.x >> 4, j = threadIdx.x & 15;
+    double acc[4][SPT];
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+#pragma unroll
+        for (int k = 0; k < SPT; ++k)
+            acc[q][k] = 0.0;
+    const double* x = Xs + (4 * g) * XS;
+    const double* h = Ht + j;
+#pragma unroll 4
+    for (int m = 0; m < N; ++m) {
+        double xv[4], hv[SPT];
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+            xv[q] = x[q * XS + m];
+#pragma unroll
+        for (int k = 0; k < SPT; ++k)
+            hv[k] = h[m * NP + 16 * k];
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+#pragma unroll
+            for (int k = 0; k < SPT; ++k)
+                acc[q][k] = fma(hv[k], xv[q], acc[q][k]);
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const int sl = 4 * g + q, ln = sl / 3, i = sl - 3 * ln;
+        if (ln >= nloc)
+            continue;
+        double* o = out + (A0 + ln) * os + (long)i * N;
+#pragma unroll
+        for (int k = 0; k < SPT; ++k) {
+            const int n = j + 16 * k;
+            if (n < N)
+                o[n] = acc[q][k];
+        }
+    }
 }
 
 void launch_apply_h_series(const double* H, int N, const double* in, int in_node_stride,
                            double* out, int out_node_stride, int nnodes, cudaStream_t st) {
-    const int per = (N >= 256) ? 1 : 256 / N;
-    const long nser = 3L * nnodes;
-    const int blocks = (int)((nser + per - 1) / per);
+    if (nnodes <= 0)
+        return;
+    const int spt = (N + 15) / 16;
+    const int blocks = (nnodes + kHNodes - 1) / kHNodes;
+    const size_t smem = sizeof(double) * ((size_t)N * 16 * spt + (size_t)kHSeries * (N + 1));
+    static bool configured = false;  // N up to 63 needs ~57 KB (above the 48 KB default)
+    if (!configured) {
+        cudaFuncSetAttribute(apply_h_tile_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+        configured = true;
+    }
     note_launch();
-    apply_h_series_kernel<<<blocks, per * N, sizeof(double) * ((size_t)N * N + (size_t)per * N), st>>>(
-        H, N, in, in_node_stride, out, out_node_stride, nnodes);
+    switch (spt) {
+    case 1: apply_h_tile_kernel<1><<<blocks, kHThreads, smem, st>>>(H, N, in, in_node_stride, out, out_node_stride, nnodes); break;
+    case 2: apply_h_tile_kernel<2><<<blocks, kHThreads, smem, st>>>(H, N, in, in_node_stride, out, out_node_stride, nnodes); break;
+    case 3: apply_h_tile_kernel<3><<<blocks, kHThreads, smem, st>>>(H, N, in, in_node_stride, out, out_node_stride, nnodes); break;
+    default: apply_h_tile_kernel<4><<<blocks, kHThreads, smem, st>>>(H, N, in, in_node_stride, out, out_node_stride, nnodes); break;
+    }
 }
 
 // ---------------------------------------------------------------- residual
@@ -1037,22 +1084,24 @@ void launch_reduce_partials(const double* partial, int nv, double* out, int take
     reduce_partials_kernel<<<nv, kRedThreads, 0, st>>>(partial, out, take_sqrt, skip, nparts);
 }
 
-// DFMA throughput probe: 8 independent FMA chains per thread, enough CTAs
-// to fill every SM.  Used once by bench.py for the FP64 roofline peak (the
-// driver's MEASURED_PEAKS.json has HBM and bf16 only).
+// DFMA throughput probe: 16 independent FMA chains per thread, 32 warps per
+// SM, a few ms of work (shorter runs under-read the peak by ~10% from the
+// launch ramp).  Used by bench.py for the FP64 roofline peak (the driver's
+// MEASURED_PEAKS.json has HBM and bf16 only).
+constexpr int kPeakChains = 16;
 __global__ void fp64_peak_kernel(double* out, int iters, double a, double b) {
-    double x[8];
+    double x[kPeakChains];
 #pragma unroll
-    for (int k = 0; k < 8; ++k)
+    for (int k = 0; k < kPeakChains; ++k)
         x[k] = threadIdx.x * 1e-7 + k;
     for (int it = 0; it < iters; ++it) {
 #pragma unroll
-        for (int k = 0; k < 8; ++k)
+        for (int k = 0; k < kPeakChains; ++k)
             x[k] = fma(x[k], a, b);
     }
     double s = 0.0;
 #pragma unroll
-    for (int k = 0; k < 8; ++k)
+    for (int k = 0; k < kPeakChains; ++k)
         s += x[k];
     if (s == 12345.678)
         out[0] = s;

@@ -141,25 +141,41 @@ void launch_tangent_pack_refresh(unsigned char* pack, const int* pack_ptr, int n
 #endif
 constexpr int kRecStride = TAN_REC_STRIDE;
 
+// Sample pairs (P = 2): every phase-1 and phase-2 thread item covers a PAIR
+// of consecutive time samples.  The geometry record, the contribution record
+// and the index arithmetic are then loaded / computed once per two samples,
+// the two samples' tau chains are independent (ILP), and the summaries and
+// diagonal parts move as 16-byte double2 (sample stride padded to even).
+// Used for the compile-time N of 5..19: at config 1 (N = 19) 0.858 -> 0.821 ms.
+// At N = 47 the 512-thread CTA's items per row (ninc x 24 pairs vs ninc x 47)
+// quantise worse and pairs lose (31.6 -> 32.8 ms, config 4), so N >= 31 and the
+// generic kernel stay on single samples.
+__host__ __device__ constexpr int tan_pair(int NC) { return (NC >= 3 && NC <= 19) ? 2 : 1; }
+__host__ __device__ inline int tan_ntp(int NT, int P) { return (NT + P - 1) / P * P; }
+
 struct PipeSmem {
     int meta, su, tg, summ, rec, dpart, mbar, total;  // byte offsets
 };
-__host__ __device__ inline PipeSmem pipe_layout(int max_pack, int mi, int max_blk, int N, int NT) {
+__host__ __device__ inline PipeSmem pipe_layout(int max_pack, int mi, int max_blk, int N, int NT, int P) {
     PipeSmem L;
     const int dpmax = (mi + kTanPart - 1) / kTanPart;
+    const int NTp = tan_ntp(NT, P);
     L.meta = 0;                                                   // 2 x max_pack
     L.su = L.meta + 2 * pack_align16(max_pack);                   // [blk][4N]
     L.tg = L.su + max_blk * (4 * N + TAN_SU_PAD) * 8;             // [inc][20]
-    L.summ = L.tg + mi * kTGeo * 8;                               // [i][8][NT]
-    L.rec = L.summ + ((mi * 7 * (NT + TAN_SUMM_PAD) + 1) & ~1) * 8;  // [p][8]
-    L.dpart = L.rec + 4 * mi * kRecStride * 8;                    // [part][8][NT]
-    L.mbar = pack_align16(L.dpart + dpmax * 8 * NT * 8);          // 3 mbarriers
+    L.summ = L.tg + mi * kTGeo * 8;                               // [c][i][NTp]
+    L.rec = L.summ + ((mi * 7 * (NTp + TAN_SUMM_PAD) + 1) & ~1) * 8;  // [p][10]
+    L.dpart = L.rec + 4 * mi * kRecStride * 8;                    // [part][8][NTp]
+    L.mbar = pack_align16(L.dpart + dpmax * 8 * NTp * 8);         // 3 mbarriers
     L.total = L.mbar + 32;
     return L;
 }
 
+static bool pipe_nc_listed(int N);
 size_t tangent_pipe_smem(int max_pack, int max_inc, int max_blk, int N, int NT) {
-    return (size_t)pipe_layout(max_pack, max_inc, max_blk, N, NT).total;
+    // the compile-time-N kernel (whole series per CTA) may use sample pairs
+    const int P = (NT == N && pipe_nc_listed(N)) ? tan_pair(N) : 1;
+    return (size_t)pipe_layout(max_pack, max_inc, max_blk, N, NT, P).total;
 }
 
 // THREADS per CTA (32 ... 512) is chosen per valence bucket from the row's
@@ -167,27 +183,17 @@ size_t tangent_pipe_smem(int max_pack, int max_inc, int max_blk, int N, int NT) 
 // NC > 0: the time-sample count is the compile-time constant NC (and the
 // whole series is one tile), so every N-strided shared/global address folds
 // to an immediate offset; NC = 0 is the generic kernel.
-#ifndef TAN_SUMM_CMAJOR
-#define TAN_SUMM_CMAJOR 1
-#endif
-#ifndef TAN_P2_UNROLL
-#define TAN_P2_UNROLL 1
-#endif
-constexpr int kTanP2Unroll = TAN_P2_UNROLL;  // phase-2 contribution loop unroll (1: 0.899 ms, 2: 0.909, 4: 0.901 at config 1)
-// TAN_P1_PAIR=1 (two phase-1 items per iteration) measured slower at config 1
-// (0.909 -> 0.938 ms); off.
-#ifndef TAN_P1_PAIR
-#define TAN_P1_PAIR 0
-#endif
 template <int TAU, int THREADS, int NC>
 __global__ void __launch_bounds__(THREADS, 512 / THREADS) tangent_pipe_kernel(TangentArgs a, PipeArgs pa) {
+    constexpr int P = tan_pair(NC);
     extern __shared__ __align__(128) unsigned char smraw[];
     const int N = NC ? NC : a.N, NT = NC ? NC : a.NT;
     const int n0 = NC ? 0 : blockIdx.y * NT, nt = NC ? NC : min(NT, N - n0);
-    const PipeSmem Ls = pipe_layout(pa.max_pack, a.max_inc, a.max_blk, N, NT);
-    // summary layout: TAN_SUMM_CMAJOR = component-major [c][i][t] (item-contiguous
-    // stores in phase 1), else incidence-major [i][c][t]
-    const int SI = TAN_SUMM_CMAJOR ? NT + TAN_SUMM_PAD : 7 * NT, SC = TAN_SUMM_CMAJOR ? a.max_inc * SI : NT;
+    const int NTp = tan_ntp(NT, P);
+    const int nq = (nt + P - 1) / P;  // sample groups of this tile
+    const PipeSmem Ls = pipe_layout(pa.max_pack, a.max_inc, a.max_blk, N, NT, P);
+    // summaries, component-major [c][i][t]: the stores of one phase-1 pass are contiguous
+    const int SI = NTp + TAN_SUMM_PAD, SC = a.max_inc * SI;
     const int mpack = pack_align16(pa.max_pack);
     uint64_t* mbar = reinterpret_cast<uint64_t*>(smraw + Ls.mbar);  // [0..1] packs, [2] gathers
     double* summ = reinterpret_cast<double*>(smraw + Ls.summ);
@@ -197,7 +203,6 @@ __global__ void __launch_bounds__(THREADS, 512 / THREADS) tangent_pipe_kernel(Ta
     const double rho = a.rho, diffc = 3.0 * a.nu * a.nu, dAB = kQA - kQB;
     const double c1 = kQB * (1.0 + dAB), c2 = dAB * dAB;
     const double mu = a.mu, pc = a.pseudo_c;
-
     const int r0 = blockIdx.x, rs = gridDim.x, nrows = pa.nrows;
     if (threadIdx.x == 0) {
         for (int k = 0; k < 3; ++k)
@@ -239,8 +244,9 @@ __global__ void __launch_bounds__(THREADS, 512 / THREADS) tangent_pipe_kernel(Ta
         issue_gather(0);
     }
 
-    const int di = blockDim.x / nt, dt = blockDim.x - di * nt;
-    const int i_start = threadIdx.x / nt, t_start = threadIdx.x - i_start * nt;
+    // work items (x, q): x = incidence (phase 1) or slot (phase 2), q = sample group
+    const int dx = blockDim.x / nq, dq = blockDim.x - dx * nq;
+    const int x_start = threadIdx.x / nq, q_start = threadIdx.x - x_start * nq;
     // Diagonal block of the previous row: sum its parts in order, identity K on
     // Dirichlet rows (assembly.cpp:659-665).  Deferred into the next row's first
     // region so a row costs two barriers, not three.
@@ -254,7 +260,7 @@ __global__ void __launch_bounds__(THREADS, 512 / THREADS) tangent_pipe_kernel(Ta
             const int sl = it / nt, t = it - sl * nt, n = n0 + t;
             double v = 0.0;
             for (int p = 0; p < pd_parts; ++p)
-                v += dpart[((size_t)p * 8 + sl) * NT + t];
+                v += dpart[((size_t)p * 8 + sl) * NTp + t];
             if (sl == 0 && pd_fix)
                 v = 1.0;
             __stcs(a.pvals + (pd_blk * 8 + sl) * N + n, v);
@@ -300,11 +306,9 @@ __global__ void __launch_bounds__(THREADS, 512 / THREADS) tangent_pipe_kernel(Ta
             o[2] = make_double2(gb0, gb1);
             o[3] = make_double2(gb2, __longlong_as_double((long long)i * SI));
         }
-        // ---- phase 1: per (incidence, sample) summaries.  TAN_P1_PAIR: two
-        // items per iteration (independent dependency chains for the scheduler;
-        // the second one clamped and not stored past the end)
+        // ---- phase 1: per (incidence, sample group) summaries
         bool bad_acc = false;
-        auto p1item = [&](int i, int t, bool store) {
+        auto p1item = [&](int i, int t) {
             const double* gi = tg + i * kTGeo;
             const int2 ic = inc[i];
             const int la = (unsigned)ic.x >> 30;
@@ -321,91 +325,96 @@ __global__ void __launch_bounds__(THREADS, 512 / THREADS) tangent_pipe_kernel(Ta
                 const double q1 = fma(x12, v[2], x2.x * v[1]);
                 return fma(v[0], q0, fma(v[1], q1, fma(v[2], x3.x * v[2], diff)));
             };
-            const int n = n0 + t;
-            double u[4][3], usum[3] = {0.0, 0.0, 0.0};
+            int tt[P];
 #pragma unroll
-            for (int b = 0; b < 4; ++b) {
-                const double* sb = su + (size_t)((cols >> (8 * b)) & 0xFFu) * (4 * N + TAN_SU_PAD) + n;
+            for (int k2 = 0; k2 < P; ++k2)
+                tt[k2] = min(t + k2, nt - 1);  // the padded sample repeats the last one (not stored past N)
+            double u[P][4][3], usum[P][3];
 #pragma unroll
-                for (int c = 0; c < 3; ++c) {
-                    u[b][c] = sb[c * N];
-                    usum[c] += u[b][c];
+            for (int k2 = 0; k2 < P; ++k2) {
+                usum[k2][0] = usum[k2][1] = usum[k2][2] = 0.0;
+#pragma unroll
+                for (int b = 0; b < 4; ++b) {
+                    const double* sb =
+                        su + (size_t)((cols >> (8 * b)) & 0xFFu) * (4 * N + TAN_SU_PAD) + n0 + tt[k2];
+#pragma unroll
+                    for (int c = 0; c < 3; ++c) {
+                        u[k2][b][c] = sb[c * N];
+                        usum[k2][c] += u[k2][b][c];
+                    }
                 }
             }
-            double bu[3];
-#pragma unroll
-            for (int c = 0; c < 3; ++c)
-                bu[c] = kQB * usum[c];
             bool bad = false;
-            double tau_mean = 0.0;
-            if (TAU == 1) {
-                const double um[3] = {0.25 * usum[0], 0.25 * usum[1], 0.25 * usum[2]};
-                const double arg = quad(um);
-                bad = !(arg > 0.0);
-                tau_mean = tau_or_zero(arg, bad);
-            }
-            double tsum = 0.0, z[3] = {0.0, 0.0, 0.0}, kap[3] = {0.0, 0.0, 0.0};
+            double tau_mean[P];
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                double uq[3];
+            for (int k2 = 0; k2 < P; ++k2) {
+                tau_mean[k2] = 0.0;
+                if (TAU == 1) {
+                    const double um[3] = {0.25 * usum[k2][0], 0.25 * usum[k2][1], 0.25 * usum[k2][2]};
+                    const double arg = quad(um);
+                    const bool bm = !(arg > 0.0);
+                    bad |= bm;
+                    tau_mean[k2] = tau_or_zero(arg, bm);
+                }
+            }
+            double tsum[P], z[P][3], kap[P][3];
+#pragma unroll
+            for (int k2 = 0; k2 < P; ++k2) {
+                tsum[k2] = 0.0;
 #pragma unroll
                 for (int c = 0; c < 3; ++c)
-                    uq[c] = fma(dAB, u[q][c], bu[c]);
-                double tq = tau_mean;
-                if (TAU == 0) {
-                    const double arg = quad(uq);
-                    const bool bq = !(arg > 0.0);
-                    bad |= bq;
-                    tq = tau_or_zero(arg, bq);
-                }
-                const double tadv = tq * fma(uq[0], ga[0], fma(uq[1], ga[1], uq[2] * ga[2]));
-                tsum += tq;
+                    z[k2][c] = kap[k2][c] = 0.0;
+            }
 #pragma unroll
-                for (int c = 0; c < 3; ++c) {
-                    z[c] = fma(tq, uq[c], z[c]);
-                    kap[c] = fma(tadv, uq[c], kap[c]);
+            for (int q = 0; q < 4; ++q) {
+#pragma unroll
+                for (int k2 = 0; k2 < P; ++k2) {
+                    double uq[3];
+#pragma unroll
+                    for (int c = 0; c < 3; ++c)
+                        uq[c] = fma(dAB, u[k2][q][c], kQB * usum[k2][c]);
+                    double tq = tau_mean[k2];
+                    if (TAU == 0) {
+                        const double arg = quad(uq);
+                        const bool bq = !(arg > 0.0);
+                        bad |= bq;
+                        tq = tau_or_zero(arg, bq);
+                    }
+                    const double tadv = tq * fma(uq[0], ga[0], fma(uq[1], ga[1], uq[2] * ga[2]));
+                    tsum[k2] += tq;
+#pragma unroll
+                    for (int c = 0; c < 3; ++c) {
+                        z[k2][c] = fma(tq, uq[c], z[k2][c]);
+                        kap[k2][c] = fma(tadv, uq[c], kap[k2][c]);
+                    }
                 }
             }
             // + sum_q N_a(q) u_q = B usum + (A-B) u_{q=a} = c1 usum + c2 u_A (u_A: the row node)
-            {
-                const double* sA = su + (size_t)kdiag * (4 * N + TAN_SU_PAD) + n;
+            const double wr = w * rho, wo = w / rho;
+            double o[7][P];
 #pragma unroll
-                for (int c = 0; c < 3; ++c)
-                    kap[c] = fma(c1, usum[c], fma(c2, sA[c * N], kap[c]));
+            for (int k2 = 0; k2 < P; ++k2) {
+                const double* sA = su + (size_t)kdiag * (4 * N + TAN_SU_PAD) + n0 + tt[k2];
+#pragma unroll
+                for (int c = 0; c < 3; ++c) {
+                    o[c][k2] = wr * fma(c1, usum[k2][c], fma(c2, sA[c * N], kap[k2][c]));
+                    o[3 + c][k2] = w * z[k2][c];
+                }
+                o[6][k2] = wo * tsum[k2];
             }
             bad_acc |= bad;
-            if (!store)
-                return;
             double* so = summ + (size_t)i * SI + t;
-            const double wr = w * rho;
-            so[0] = wr * kap[0];
-            so[1 * SC] = wr * kap[1];
-            so[2 * SC] = wr * kap[2];
-            so[3 * SC] = w * z[0];
-            so[4 * SC] = w * z[1];
-            so[5 * SC] = w * z[2];
-            so[6 * SC] = (w / rho) * tsum;
-                };
-#if TAN_P1_PAIR
-        {
-            const int total = ninc * nt, step = blockDim.x;
-            int i = i_start, t = t_start;
-            for (int it = threadIdx.x; it < total; it += 2 * step) {
-                int t2 = t + dt, i2 = i + di + (t2 >= nt);
-                t2 -= (t2 >= nt ? nt : 0);
-                const bool v2 = it + step < total;
-                p1item(i, t, true);
-                p1item(v2 ? i2 : i, v2 ? t2 : t, v2);
-                t = t2 + dt;
-                i = i2 + di + (t >= nt);
-                t -= (t >= nt ? nt : 0);
+#pragma unroll
+            for (int c = 0; c < 7; ++c) {
+                if (P == 2)
+                    *reinterpret_cast<double2*>(so + c * SC) = make_double2(o[c][0], o[c][P - 1]);
+                else
+                    so[c * SC] = o[c][0];
             }
-        }
-#else
-        for (int it = threadIdx.x, i = i_start, t = t_start; it < ninc * nt;
-             it += blockDim.x, t += dt, i += di + (t >= nt), t -= (t >= nt ? nt : 0))
-            p1item(i, t, true);
-#endif
+        };
+        for (int it = threadIdx.x, i = x_start, q = q_start; it < ninc * nq;
+             it += blockDim.x, q += dq, i += dx + (q >= nq), q -= (q >= nq ? nq : 0))
+            p1item(i, P * q);
         if (bad_acc)
             atomicOr(a.flag, 1);
         __syncthreads();
@@ -414,71 +423,108 @@ __global__ void __launch_bounds__(THREADS, 512 / THREADS) tangent_pipe_kernel(Ta
             mbar_wait(mbar + (ms ^ 1), ((k + 1) >> 1) & 1);
             issue_gather(ms ^ 1);
         }
-        // ---- phase 2: per (slot, sample) register accumulation
-        for (int it = threadIdx.x, slot = i_start, t = t_start; it < nslots * nt;
-             it += blockDim.x, t += dt, slot += di + (t >= nt), t -= (t >= nt ? nt : 0)) {
-            const int n = n0 + t;
+        // ---- phase 2: per (slot, sample group) register accumulation
+        for (int it = threadIdx.x, slot = x_start, q = q_start; it < nslots * nq;
+             it += blockDim.x, q += dq, slot += dx + (q >= nq), q -= (q >= nq ? nq : 0)) {
+            const int t = P * q;
             const int4 info = sinfo[slot];
             const int j = info.z;
             const bool bfix = info.w != 0;
-            double K = 0.0, G0 = 0.0, G1 = 0.0, G2 = 0.0, D0 = 0.0, D1 = 0.0, D2 = 0.0, L = 0.0;
-#pragma unroll kTanP2Unroll
+            double K[P], G0[P], G1[P], G2[P], D0[P], D1[P], D2[P], L[P];
+#pragma unroll
+            for (int k2 = 0; k2 < P; ++k2)
+                K[k2] = G0[k2] = G1[k2] = G2[k2] = D0[k2] = D1[k2] = D2[k2] = L[k2] = 0.0;
             for (int p = info.x; p < info.y; ++p) {
                 const double2* rp = reinterpret_cast<const double2*>(rec + p * kRecStride);
                 const double2 ra = rp[0], rb = rp[1], rc = rp[2], rd = rp[3];
                 const double* sp = summ + __double_as_longlong(rd.y) + t;
                 const double gb0 = rc.x, gb1 = rc.y, gb2 = rd.x;
-                K = fma(sp[0], gb0, fma(sp[SC], gb1, fma(sp[2 * SC], gb2, K)));
-                // w alpha_a = (w z) . dN_a (phase 1 stores w z only: one shared
-                // load fewer per contribution; phase 2 is shared-memory bound)
-                const double z0 = sp[3 * SC], z1 = sp[4 * SC], z2 = sp[5 * SC];
-                const double al = fma(z0, ra.x, fma(z1, ra.y, z2 * rb.x));
-                G0 = fma(al, gb0, G0);
-                G1 = fma(al, gb1, G1);
-                G2 = fma(al, gb2, G2);
-                const double alb = fma(z0, gb0, fma(z1, gb1, z2 * gb2));
-                D0 = fma(ra.x, alb, D0);
-                D1 = fma(ra.y, alb, D1);
-                D2 = fma(rb.x, alb, D2);
-                L = fma(rb.y, sp[6 * SC], L);
+                double sv[7][P];
+#pragma unroll
+                for (int c = 0; c < 7; ++c) {
+                    if (P == 2) {
+                        const double2 v2 = *reinterpret_cast<const double2*>(sp + c * SC);
+                        sv[c][0] = v2.x;
+                        sv[c][P - 1] = v2.y;
+                    } else {
+                        sv[c][0] = sp[c * SC];
+                    }
+                }
+#pragma unroll
+                for (int k2 = 0; k2 < P; ++k2) {
+                    K[k2] = fma(sv[0][k2], gb0, fma(sv[1][k2], gb1, fma(sv[2][k2], gb2, K[k2])));
+                    // w alpha_a = (w z) . dN_a
+                    const double al = fma(sv[3][k2], ra.x, fma(sv[4][k2], ra.y, sv[5][k2] * rb.x));
+                    G0[k2] = fma(al, gb0, G0[k2]);
+                    G1[k2] = fma(al, gb1, G1[k2]);
+                    G2[k2] = fma(al, gb2, G2[k2]);
+                    const double alb = fma(sv[3][k2], gb0, fma(sv[4][k2], gb1, sv[5][k2] * gb2));
+                    D0[k2] = fma(ra.x, alb, D0[k2]);
+                    D1[k2] = fma(ra.y, alb, D1[k2]);
+                    D2[k2] = fma(rb.x, alb, D2[k2]);
+                    L[k2] = fma(rb.y, sv[6][k2], L[k2]);
+                }
             }
             if (slot >= dparts || slot == 0) {
                 const double2* bc = reinterpret_cast<const double2*>(blkc + j * 8);
                 const double2 b0 = bc[0], b1 = bc[1], b2 = bc[2], b3 = bc[3];
-                K += fma(mu, b0.x, pc * b0.y);
-                G0 += b1.x;
-                G1 += b1.y;
-                G2 += b2.x;
-                D0 += b2.y;
-                D1 += b3.x;
-                D2 += b3.y;
+                const double kc = fma(mu, b0.x, pc * b0.y);
+#pragma unroll
+                for (int k2 = 0; k2 < P; ++k2) {
+                    K[k2] += kc;
+                    G0[k2] += b1.x;
+                    G1[k2] += b1.y;
+                    G2[k2] += b2.x;
+                    D0[k2] += b2.y;
+                    D1[k2] += b3.x;
+                    D2[k2] += b3.y;
+                }
             }
-            if (afix || bfix)
-                K = 0.0;
-            if (afix)
-                G0 = G1 = G2 = 0.0;
-            if (bfix)
-                D0 = D1 = D2 = 0.0;
+#pragma unroll
+            for (int k2 = 0; k2 < P; ++k2) {
+                if (afix || bfix)
+                    K[k2] = 0.0;
+                if (afix)
+                    G0[k2] = G1[k2] = G2[k2] = 0.0;
+                if (bfix)
+                    D0[k2] = D1[k2] = D2[k2] = 0.0;
+            }
             if (slot >= dparts) {
-                double* out = a.pvals + ((long)(k0 + j) * 8) * N + n;
-                __stcs(out, K);
-                __stcs(out + N, G0);
-                __stcs(out + 2 * N, G1);
-                __stcs(out + 3 * N, G2);
-                __stcs(out + 4 * N, D0);
-                __stcs(out + 5 * N, D1);
-                __stcs(out + 6 * N, D2);
-                __stcs(out + 7 * N, L);
+#pragma unroll
+                for (int k2 = 0; k2 < P; ++k2) {
+                    if (t + k2 >= nt)
+                        break;
+                    double* out = a.pvals + ((long)(k0 + j) * 8) * N + n0 + t + k2;
+                    __stcs(out, K[k2]);
+                    __stcs(out + N, G0[k2]);
+                    __stcs(out + 2 * N, G1[k2]);
+                    __stcs(out + 3 * N, G2[k2]);
+                    __stcs(out + 4 * N, D0[k2]);
+                    __stcs(out + 5 * N, D1[k2]);
+                    __stcs(out + 6 * N, D2[k2]);
+                    __stcs(out + 7 * N, L[k2]);
+                }
             } else {
-                double* o = dpart + (size_t)slot * 8 * NT + t;
-                o[0] = K;
-                o[NT] = G0;
-                o[2 * NT] = G1;
-                o[3 * NT] = G2;
-                o[4 * NT] = D0;
-                o[5 * NT] = D1;
-                o[6 * NT] = D2;
-                o[7 * NT] = L;
+                double* o = dpart + (size_t)slot * 8 * NTp + t;
+                if (P == 2) {
+                    *reinterpret_cast<double2*>(o) = make_double2(K[0], K[P - 1]);
+                    *reinterpret_cast<double2*>(o + NTp) = make_double2(G0[0], G0[P - 1]);
+                    *reinterpret_cast<double2*>(o + 2 * NTp) = make_double2(G1[0], G1[P - 1]);
+                    *reinterpret_cast<double2*>(o + 3 * NTp) = make_double2(G2[0], G2[P - 1]);
+                    *reinterpret_cast<double2*>(o + 4 * NTp) = make_double2(D0[0], D0[P - 1]);
+                    *reinterpret_cast<double2*>(o + 5 * NTp) = make_double2(D1[0], D1[P - 1]);
+                    *reinterpret_cast<double2*>(o + 6 * NTp) = make_double2(D2[0], D2[P - 1]);
+                    *reinterpret_cast<double2*>(o + 7 * NTp) = make_double2(L[0], L[P - 1]);
+                } else {
+                    o[0] = K[0];
+                    o[NTp] = G0[0];
+                    o[2 * NTp] = G1[0];
+                    o[3 * NTp] = G2[0];
+                    o[4 * NTp] = D0[0];
+                    o[5 * NTp] = D1[0];
+                    o[6 * NTp] = D2[0];
+                    o[7 * NTp] = L[0];
+                }
             }
         }
         __syncthreads();
@@ -726,6 +772,12 @@ __global__ void __launch_bounds__(THREADS, 512 / THREADS) tangent_fused_kernel(T
 
 // Compile-time time-sample counts of the BASELINE configs (N = 2 Nm - 1).
 #define HBGPU_PIPE_NC_LIST(X) X(1) X(5) X(7) X(19) X(31) X(47)
+static bool pipe_nc_listed(int N) {
+#define HBGPU_NC_IS(n) if (N == n) return true;
+    HBGPU_PIPE_NC_LIST(HBGPU_NC_IS)
+#undef HBGPU_NC_IS
+    return false;
+}
 
 template <int T, int NC>
 static cudaError_t configure_pipe_tn(int b) {

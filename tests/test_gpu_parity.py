@@ -654,9 +654,11 @@ def test_solve_divergence_errors(gpu):
         ctx.solve_harmonic(SolverConfig(divergence_ratio=0.5, max_newton_iters=3))
     # iteration 0 has rel = 1 > 0.5: one log entry, then the throw
     assert ei.value.partial_log_csv.count("\n") == 2
-    g = prob.dirichlet_g.copy()
-    g[np.flatnonzero(g)[:1]] = np.nan
-    ctx.set_bcs(g, prob.neumann, prob.backflow_beta)
+    # a non-finite outlet traction: the residual is not finite while tau is
+    # (a NaN velocity would raise domain_error from compute_tau first, as in
+    # the reference, assembly.cpp:51-53)
+    bad = [(k, np.full(prob.N, np.nan)) for k, _ in prob.neumann]
+    ctx.set_bcs(prob.dirichlet_g, bad, prob.backflow_beta)
     with pytest.raises(DivergenceError, match="not finite"):
         ctx.solve_harmonic(SolverConfig(max_newton_iters=3))
     # the context's assembly config is untouched by the failed solves
