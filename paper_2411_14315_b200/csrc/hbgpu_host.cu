@@ -63,7 +63,29 @@ struct HostPatch {
 
 }  // namespace
 
+// Test / tooling switches, read ONCE when a context is created (never on a
+// hot call).  Defaults are the measured best; see DESIGN.md "Tooling switches".
+struct Tooling {
+    int res_tile = 0;           // HBGPU_RES_TILE: 1, 2 or 4 samples per residual tile (0 = auto)
+    bool tangent_rows = false;  // HBGPU_TANGENT_KERNEL=rows: the tiled row-kernel fallback
+    int tan_width = 0;          // HBGPU_TAN_WIDTH: force the tangent pipeline's CTA width
+    bool gmres_host = false;    // HBGPU_GMRES_HOST: host-driven GMRES step loop
+    int mv_lanes = 0;           // HBGPU_MV_LANES: 1 / 4 lanes per (row, sample) (0 = auto)
+    static Tooling from_env() {
+        Tooling t;
+        auto num = [](const char* k) { const char* v = std::getenv(k); return v ? std::atoi(v) : 0; };
+        t.res_tile = num("HBGPU_RES_TILE");
+        const char* tk = std::getenv("HBGPU_TANGENT_KERNEL");
+        t.tangent_rows = tk && std::strcmp(tk, "rows") == 0;
+        t.tan_width = num("HBGPU_TAN_WIDTH");
+        t.gmres_host = std::getenv("HBGPU_GMRES_HOST") != nullptr;
+        t.mv_lanes = num("HBGPU_MV_LANES");
+        return t;
+    }
+};
+
 struct hbgpu_ctx {
+    Tooling tool;
     int nn = 0, ne = 0;
     int M = 0, N = 0;
     double period = 1.0, omega = 0.0;
@@ -100,9 +122,6 @@ struct hbgpu_ctx {
         DBuf<int> pack_ptr;
         int max_pack = 0, grid = 0, threads = 128;
         bool pipe = false;
-        // fused assembly variant (tangent_fused_kernel)
-        size_t fsmem = 0;
-        int fgrid = 0;
     } tb[6];
     DBuf<double> blkc;        // per block: n-invariant tangent sums (8)
     DBuf<uint8_t> blk_order;  // per row: off-diagonal blocks by descending contribution count
@@ -110,11 +129,6 @@ struct hbgpu_ctx {
     DBuf<int> row_ptr, col_idx, diag_blk, inc_ptr;
     DBuf<int> mv_perm;  // L-matvec row order: by descending length within 4096-row windows
     DBuf<int4> mv_rows; // {A, row_ptr[A], row_ptr[A+1], 0} in that order
-    // fused assembly: element summaries written by the residual pass, read by the
-    // tangent rows (all pipe buckets hold whole series); disabled if not
-    bool fused_ok = false;
-    int summ_ns = 0;
-    DBuf<double> tsumm;
     // residual element chunks
     int nchunks = 0, max_nloc = 0, res_grid = 0, res_tile = 4;
     long npairs = 0;
@@ -340,8 +354,7 @@ static int upload_all(hbgpu_ctx* c, const hbgpu_mesh_desc* d) {
         for (int A = 0; A < nn; ++A)
             perm[size_t(A)] = A;
         const int* rp = c->row_ptr_h.data();
-        const char* pw = std::getenv("HBGPU_MV_WINDOW");  // tooling: window length
-        const int win = pw ? std::max(1, std::atoi(pw)) : 4096;
+        const int win = 4096;
         for (int w0 = 0; w0 < nn; w0 += win) {
             const int w1 = std::min(nn, w0 + win);
             std::stable_sort(perm.begin() + w0, perm.begin() + w1, [rp](int x, int y) {
@@ -602,7 +615,7 @@ static int rows_per_matvec_cta(int N) { return std::max(1, 256 / N); }
 
 // ---------------------------------------------------------------- operations
 
-static int residual_dev(hbgpu_ctx* c, const double* d_state, double* d_r, double* d_summ = nullptr) {
+static int residual_dev(hbgpu_ctx* c, const double* d_state, double* d_r) {
     const int N = c->N;
     cudaStream_t st = c->stream;
     const long p0 = prof_mark(c);
@@ -630,8 +643,6 @@ static int residual_dev(hbgpu_ctx* c, const double* d_state, double* d_r, double
     ca.nu = c->mu / c->rho;
     ca.tau_mode = c->tau_mode;
     ca.flag = c->flag.p;
-    ca.summ = d_summ;
-    ca.summ_ns = c->summ_ns;
     launch_residual_chunks(ca, c->res_grid, c->res_tile, st);
     const long p2 = prof_mark(c);
     launch_residual_nodes(c->H.p, N, c->nn, c->npart_ptr.p, c->npart.p, c->rpartial.p, c->dir.p,
@@ -748,17 +759,6 @@ static int mass_dev(hbgpu_ctx* c) {
     return check_launch(c);
 }
 
-// L-matvec kernel variant: bit 0 = rows in length-balanced order (mv_perm),
-// bit 1 = N == 1 rows split over 4 lanes, bits 2-3 = lanes per (row, sample)
-// for N > 1, bit 4 = 4 lanes automatically on small meshes, bit 6 = row records
-// {A, kb, ke} in one load.  Default 83 (config 4, 700k points: N = 1 0.277 ->
-// 0.189 ms, N = 7 1.398 -> 1.261 ms, N = 19 3.53 -> 3.22 ms; config 0: 26.7 ->
-// 14.9 us); HBGPU_MV_VARIANT overrides it (tooling).
-static int mv_variant() {
-    const char* e = std::getenv("HBGPU_MV_VARIANT");
-    return e ? std::atoi(e) : 83;
-}
-
 static int matvec_dev(hbgpu_ctx* c, const double* d_y, double* d_out, const double* d_scale,
                       bool with_c, const double* d_scale_out = nullptr, const int* d_skip = nullptr) {
     if (!c->p_valid)
@@ -781,7 +781,7 @@ static int matvec_dev(hbgpu_ctx* c, const double* d_y, double* d_out, const doub
     a.perm = c->mv_perm.p;
     a.rows = c->mv_rows.p;
     a.skip = d_skip;
-    a.variant = mv_variant();
+    a.lanes = c->tool.mv_lanes;
     a.nn = c->nn;
     a.N = c->N;
     a.rows_per_cta = rows_per_matvec_cta(c->N);
@@ -880,7 +880,7 @@ static int gmres_dev(hbgpu_ctx* c, const double* d_rhs, const double* d_inv,
     // HBGPU_GMRES_HOST=1 (or a restart too long for the Arnoldi kernel's shared
     // memory, m > ~700): the host-driven step loop, one synchronisation per
     // step; else the device-resident cycle
-    const bool devloop = std::getenv("HBGPU_GMRES_HOST") == nullptr && arnoldi_step_smem(m) <= 200 * 1024;
+    const bool devloop = !c->tool.gmres_host && arnoldi_step_smem(m) <= 200 * 1024;
     ArnoldiDev ad{};
     if (devloop) {
         const size_t hsz = size_t(m + 2) * size_t(m + 1);
@@ -960,7 +960,9 @@ static int gmres_dev(hbgpu_ctx* c, const double* d_rhs, const double* d_inv,
             // runs in arnoldi_step_kernel, so steps are enqueued in batches of
             // kBatch with no host round trip; the host polls the stop flag one
             // batch behind (steps enqueued past a stop return at once).
-            const int kBatch = std::getenv("HBGPU_GMRES_BATCH") ? std::max(1, std::atoi(std::getenv("HBGPU_GMRES_BATCH"))) : 8;
+            // steps per host poll: 4 / 8 / 16 / 32 measured equal on the config-0
+            // solve (0.677 / 0.670 / 0.670 / 0.675 s): the cycle is kernel-bound
+            constexpr int kBatch = 8;
             const int it0 = res->iterations;
             launch_arnoldi_init(ad, rnorm, it0, res->reorthogonalizations, c->red.p, st);
             launch_normalize(rsrc, c->red.p, V, n, st, c->scale.p, c->z.p);
@@ -1179,6 +1181,7 @@ hbgpu_ctx* hbgpu_create(const hbgpu_mesh_desc* d, int* status) {
         return nullptr;
     }
     auto* c = new hbgpu_ctx;
+    c->tool = Tooling::from_env();
     c->nn = d->num_nodes;
     c->ne = d->num_elements;
     c->conn_h.assign(d->conn, d->conn + 4 * size_t(c->ne));
@@ -1348,11 +1351,8 @@ int hbgpu_set_basis(hbgpu_ctx* c, int modes, double period) {
         CK(c, b->alloc(n));
     CK(c, c->hu.alloc(size_t(c->nn) * 3 * size_t(N)));
     c->res_tile = residual_tile(N);
-    if (const char* rt = std::getenv("HBGPU_RES_TILE")) {  // tooling: 1, 2 or 4 samples per tile
-        const int t = std::atoi(rt);
-        if (t == 1 || t == 2 || t == 4)
-            c->res_tile = t;
-    }
+    if (c->tool.res_tile == 1 || c->tool.res_tile == 2 || c->tool.res_tile == 4)
+        c->res_tile = c->tool.res_tile;
     CK(c, c->rpartial.alloc(size_t(c->npairs) * 7 * size_t((N + c->res_tile - 1) / c->res_tile) * c->res_tile));
     {
         const size_t rs = residual_smem_bytes(c->max_nloc, c->max_rpack, c->res_tile);
@@ -1385,8 +1385,7 @@ int hbgpu_set_basis(hbgpu_ctx* c, int modes, double period) {
         size_t mx = 0, mxp[5] = {0, 0, 0, 0, 0};
         int dev = 0, nsm = 0;
         // test knob: HBGPU_TANGENT_KERNEL=rows forces the row-kernel fallback
-        const char* tk = std::getenv("HBGPU_TANGENT_KERNEL");
-        const bool force_rows = tk && std::strcmp(tk, "rows") == 0;
+        const bool force_rows = c->tool.tangent_rows;
         CK(c, cudaGetDevice(&dev));
         CK(c, cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
         const int widths[5] = {32, 64, 128, 256, 512};
@@ -1416,31 +1415,9 @@ int hbgpu_set_basis(hbgpu_ctx* c, int modes, double period) {
                         b.nt = N;
                     }
                 }
-                // tooling: HBGPU_TAN_NT caps the sample tile of every pipe bucket
-                if (const char* tn = std::getenv("HBGPU_TAN_NT")) {
-                    const int cap = std::max(1, std::atoi(tn));
-                    if (b.pipe && cap < N) {
-                        b.nt = cap;
-                        double bestw = 0.0;
-                        for (int w : widths) {
-                            const size_t sm = ps(b.nt);
-                            const int by_smem = int(size_t(228 * 1024) / (sm + 1024));
-                            const int by_regs = 65536 / (w * 128);
-                            const int ctas = std::min({32, by_smem, by_regs});
-                            if (ctas < 1)
-                                continue;
-                            const double it2 = double(b.max_inc) * b.nt;
-                            const double score = it2 / (std::ceil(it2 / w) * w) * std::min(1.0, ctas * (w / 32) / 24.0);
-                            if (score > bestw * 1.0001) {
-                                bestw = score;
-                                b.threads = w;
-                            }
-                        }
-                    }
-                }
                 // tooling: HBGPU_TAN_WIDTH forces the CTA width of every pipe bucket
-                if (const char* tw = std::getenv("HBGPU_TAN_WIDTH")) {
-                    const int w = std::atoi(tw);
+                if (c->tool.tan_width) {
+                    const int w = c->tool.tan_width;
                     if (b.pipe && std::find(widths, widths + 5, w) != widths + 5 && ps(b.nt) <= size_t(227 * 1024))
                         b.threads = w;
                 }
@@ -1485,43 +1462,6 @@ int hbgpu_set_basis(hbgpu_ctx* c, int modes, double period) {
                 return fail(c, HBGPU_ERR_INVALID, "tangent pipeline does not fit on an SM");
             const int tiles = (N + b.nt - 1) / b.nt;
             b.grid = std::max(1, std::min(b.count, (nsm * per_sm + tiles - 1) / tiles));
-        }
-        // fused assembly: every bucket on the pipeline with whole series
-        c->summ_ns = N + (N & 1);
-        c->tsumm.release();
-        // opt-in (HBGPU_FUSED=1): measured at config 1, the residual pass grows
-        // 0.60 -> 0.82 ms with the summaries while the tangent rows drop 0.92 ->
-        // 0.74 ms (gather-latency bound), a net loss against the concurrent pair
-        c->fused_ok = std::getenv("HBGPU_FUSED") != nullptr;
-        size_t fx[5] = {0, 0, 0, 0, 0};
-        for (auto& b : c->tb) {
-            if (!b.count)
-                continue;
-            if (!b.pipe || b.nt != N) {
-                c->fused_ok = false;
-                continue;
-            }
-            b.fsmem = tangent_fused_smem(b.max_pack, b.max_inc, N, c->summ_ns);
-            if (b.fsmem > size_t(227 * 1024))
-                c->fused_ok = false;
-            const int w = int(std::find(widths, widths + 5, b.threads) - widths);
-            fx[w] = std::max(fx[w], b.fsmem);
-        }
-        if (c->fused_ok) {
-            for (int w = 0; w < 5; ++w)
-                if (fx[w])
-                    CK(c, configure_tangent_fused_smem(widths[w], fx[w]));
-            for (auto& b : c->tb) {
-                if (!b.count)
-                    continue;
-                int per_sm = 0;
-                CK(c, tangent_fused_occupancy(b.threads, &per_sm, b.fsmem));
-                if (per_sm < 1) {
-                    c->fused_ok = false;
-                    break;
-                }
-                b.fgrid = std::max(1, std::min(b.count, nsm * per_sm));
-            }
         }
     }
     // clear previous Neumann data sized for another N
@@ -1719,50 +1659,8 @@ int hbgpu_assemble_residual(hbgpu_ctx* c, const double* state, double* residual)
 // residual, so it overlaps the tangent.
 // Fused assembly: the residual pass also writes the tangent's element
 // summaries; the tangent rows then run without recomputing them.
-static int tangent_fused_dev(hbgpu_ctx* c, cudaStream_t st) {
-    TangentArgs a{};
-    a.tgeom = c->tgeom.p;
-    a.pvals = c->pvals.p;
-    a.N = c->N;
-    a.rho = c->rho;
-    a.mu = c->mu;
-    a.nu = c->mu / c->rho;
-    a.pseudo_c = std::isfinite(c->pseudo_dt) ? c->pseudo_c1 * c->rho / c->pseudo_dt : 0.0;
-    a.tau_mode = c->tau_mode;
-    a.flag = c->flag.p;
-    for (const auto& b : c->tb) {
-        if (!b.count)
-            continue;
-        a.max_inc = b.max_inc;
-        a.max_blk = b.max_blk;
-        a.NT = c->N;
-        PipeArgs pa;
-        pa.pack = b.pack.p;
-        pa.pack_ptr = b.pack_ptr.p;
-        pa.nrows = b.count;
-        pa.max_pack = b.max_pack;
-        pa.summ = c->tsumm.p;
-        pa.summ_ns = c->summ_ns;
-        launch_tangent_fused(a, pa, b.threads, b.fgrid, b.fsmem, st);
-    }
-    return check_launch(c);
-}
-
-static bool fused_ready(hbgpu_ctx* c) {
-    if (!c->fused_ok || c->backflow_tangent)
-        return false;
-    const size_t need = size_t(c->ne) * 16 * size_t(c->summ_ns);
-    if (c->tsumm.n < need && (c->tsumm.alloc(need) != cudaSuccess)) {
-        cudaGetLastError();
-        c->tsumm.release();
-        c->fused_ok = false;  // not enough memory: separate kernels from now on
-        return false;
-    }
-    return true;
-}
-
 static int assemble_both(hbgpu_ctx* c, const double* d_state, double* d_r, double* host_r = nullptr) {
-    if (host_r && !fused_ready(c)) {
+    if (host_r) {
         // host copy-back wanted: residual first, then the tangent on the second
         // stream while the residual travels back (concurrent kernels would finish
         // together and leave the copy exposed)
@@ -1780,26 +1678,7 @@ static int assemble_both(hbgpu_ctx* c, const double* d_state, double* d_r, doubl
         CK(c, cudaStreamWaitEvent(c->stream, c->ev_join, 0));
         return HBGPU_OK;
     }
-    if (fused_ready(c)) {
-        // residual (+ element summaries) on the main stream, then the tangent rows
-        // on the second stream; the residual's copy-back overlaps the tangent
-        const long p0 = prof_mark(c);
-        TRY(residual_dev(c, d_state, d_r, c->tsumm.p));
-        CK(c, cudaEventRecord(c->ev_fork, c->stream));
-        CK(c, cudaStreamWaitEvent(c->stream2, c->ev_fork, 0));
-        if (host_r)
-            CK(c, cudaMemcpyAsync(host_r, d_r, sizeof(double) * size_t(c->state_len()), cudaMemcpyDeviceToHost,
-                                  c->stream));
-        const long p1 = prof_mark(c);
-        TRY(tangent_fused_dev(c, c->stream2));
-        c->p_valid = true;
-        c->inv_valid = false;
-        CK(c, cudaEventRecord(c->ev_join, c->stream2));
-        CK(c, cudaStreamWaitEvent(c->stream, c->ev_join, 0));
-        prof_pair(c, kPhTangent, p1, prof_mark(c));
-        (void)p0;
-        return HBGPU_OK;
-    }
+    // residual and tangent concurrently on the context's two streams
     CK(c, cudaEventRecord(c->ev_fork, c->stream));
     CK(c, cudaStreamWaitEvent(c->stream2, c->ev_fork, 0));
     cudaStream_t main = c->stream;
@@ -1808,9 +1687,6 @@ static int assemble_both(hbgpu_ctx* c, const double* d_state, double* d_r, doubl
     c->stream = main;
     TRY(st);
     TRY(residual_dev(c, d_state, d_r));
-    if (host_r)
-        CK(c, cudaMemcpyAsync(host_r, d_r, sizeof(double) * size_t(c->state_len()), cudaMemcpyDeviceToHost,
-                              c->stream));
     CK(c, cudaEventRecord(c->ev_join, c->stream2));
     CK(c, cudaStreamWaitEvent(c->stream, c->ev_join, 0));
     return HBGPU_OK;

@@ -159,11 +159,6 @@ struct ResidualChunkArgs {
     double rho, mu, nu;
     int tau_mode;
     int* flag;
-    // fused assembly: per (element, sample) the tangent's element summaries
-    // (w rho kappa_a for a = 0..3, w z, w sum tau / rho: 16 series of summ_ns
-    // samples per element, summ[(e*16 + c)*summ_ns + n]); nullptr = off
-    double* summ;
-    int summ_ns;
 };
 
 struct TangentArgs {
@@ -199,9 +194,6 @@ struct PipeArgs {
     const int* pack_ptr;        // nrows + 1, in 16-byte units
     int nrows;
     int max_pack;               // bytes
-    // fused variant (tangent_fused_kernel): element summaries from the residual pass
-    const double* summ;
-    int summ_ns;                // padded sample stride of `summ` (even)
 };
 
 struct MatvecArgs {
@@ -220,7 +212,7 @@ struct MatvecArgs {
     const int* skip;          // optional device stop flag (GMRES steps past convergence)
     int nn, N, rows_per_cta;
     int with_c;
-    int variant;              // kernel variant (tooling: HBGPU_MV_VARIANT)
+    int lanes;                // lanes per (row, sample): 0 auto, 1 or 4 (tests)
 };
 
 struct BoundaryArgs {
@@ -278,12 +270,6 @@ void tangent_pack_write(unsigned char* dst, int A, int k0, int ninc, int nblk, i
 void launch_tangent_pack_refresh(unsigned char* pack, const int* pack_ptr, int nrows,
                                  const uint8_t* dir, const double* blkc, cudaStream_t st);
 size_t tangent_pipe_smem(int max_pack, int max_inc, int max_blk, int N, int NT);
-// fused assembly: the row pipeline fed by the residual pass's element summaries
-size_t tangent_fused_smem(int max_pack, int max_inc, int N, int NS);
-cudaError_t configure_tangent_fused_smem(int threads, size_t bytes);
-cudaError_t tangent_fused_occupancy(int threads, int* blocks_per_sm, size_t smem);
-void launch_tangent_fused(const TangentArgs& a, const PipeArgs& p, int threads, int grid_x, size_t smem,
-                          cudaStream_t st);
 cudaError_t configure_tangent_pipe_smem(int threads, size_t bytes);
 cudaError_t tangent_pipe_occupancy(int threads, int* blocks_per_sm, size_t smem);
 void launch_tangent_pipe(const TangentArgs& a, const PipeArgs& p, int threads, int grid_x, size_t smem,

@@ -328,96 +328,6 @@ __device__ __forceinline__ void element_residual_smem(const double* __restrict__
     }
 }
 
-// Fused assembly: the tangent's per-(element, sample) summaries, formed once
-// per element here instead of once per incident row in the tangent kernel
-// (where they cost four recomputations of tau per element).  For the element
-// (nodes a = 0..3) at one sample, with u_q = B usum + (A-B) u_q-node and
-// tau_q as in the residual (same branch-free rsqrt, same flags):
-//   T = sum_q tau_q u_q u_q^T (symmetric), z = sum_q tau_q u_q, ts = sum_q tau_q
-//   kappa_a = T dN_a + c1 usum + c2 u_a        (c1 = B(1+A-B), c2 = (A-B)^2)
-// stored as w rho kappa_a (a = 0..3), w z, (w/rho) ts — exactly the seven
-// values per incidence the tangent's phase 1 produces (hbgpu_tangent_pipe.cu),
-// algebraically identical to element_tangent_p's quadrature sums
-// (assembly.cpp:265-374).
-__device__ __forceinline__ void element_tangent_summary_smem(const double* __restrict__ gsm,
-                                                             const double* __restrict__ nd, int ndst,
-                                                             const int lc[4], int T, int t, double rho,
-                                                             double nu, int tau_mode, int* flag,
-                                                             double* __restrict__ out, int ns) {
-    const SmemRow g{gsm};
-    auto U = [&](int b, int c) { return lds(nd + lc[b] * ndst + c * T + t); };
-    const double V = g[12], w = 0.25 * V, dAB = kQA - kQB;
-    const double c1 = kQB * (1.0 + dAB), c2 = dAB * dAB;
-    const double diff = 3.0 * nu * nu * g[19];
-    auto quad = [&](const double v[3]) {
-        const double q0 = fma(2.0 * g[15], v[2], fma(2.0 * g[14], v[1], g[13] * v[0]));
-        const double q1 = fma(2.0 * g[17], v[2], g[16] * v[1]);
-        return fma(v[0], q0, fma(v[1], q1, fma(v[2], g[18] * v[2], diff)));
-    };
-    double usum[3] = {0.0, 0.0, 0.0};
-#pragma unroll
-    for (int b = 0; b < 4; ++b)
-#pragma unroll
-        for (int c = 0; c < 3; ++c)
-            usum[c] += U(b, c);
-    double bu[3];
-#pragma unroll
-    for (int c = 0; c < 3; ++c)
-        bu[c] = kQB * usum[c];
-    bool bad = false;
-    double tau_mean = 0.0;
-    if (tau_mode == 1) {
-        const double um[3] = {0.25 * usum[0], 0.25 * usum[1], 0.25 * usum[2]};
-        const double arg = quad(um);
-        bad = !(arg > 0.0);
-        tau_mean = tau_or_zero(arg, bad);
-    }
-    double T00 = 0.0, T01 = 0.0, T02 = 0.0, T11 = 0.0, T12 = 0.0, T22 = 0.0;
-    double z[3] = {0.0, 0.0, 0.0}, ts = 0.0;
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-        double uq[3];
-#pragma unroll
-        for (int c = 0; c < 3; ++c)
-            uq[c] = fma(dAB, U(q, c), bu[c]);
-        double tq = tau_mean;
-        if (tau_mode == 0) {
-            const double arg = quad(uq);
-            const bool bq = !(arg > 0.0);
-            bad |= bq;
-            tq = tau_or_zero(arg, bq);
-        }
-        ts += tq;
-        const double t0 = tq * uq[0], t1 = tq * uq[1], t2 = tq * uq[2];
-        z[0] += t0;
-        z[1] += t1;
-        z[2] += t2;
-        T00 = fma(t0, uq[0], T00);
-        T01 = fma(t0, uq[1], T01);
-        T02 = fma(t0, uq[2], T02);
-        T11 = fma(t1, uq[1], T11);
-        T12 = fma(t1, uq[2], T12);
-        T22 = fma(t2, uq[2], T22);
-    }
-    if (bad)
-        atomicOr(flag, 1);
-    const double wr = w * rho;
-#pragma unroll
-    for (int a = 0; a < 4; ++a) {
-        const double g0 = g[3 * a], g1 = g[3 * a + 1], g2 = g[3 * a + 2];
-        const double k0 = fma(T00, g0, fma(T01, g1, T02 * g2));
-        const double k1 = fma(T01, g0, fma(T11, g1, T12 * g2));
-        const double k2 = fma(T02, g0, fma(T12, g1, T22 * g2));
-        out[(3 * a) * ns] = wr * fma(c1, usum[0], fma(c2, U(a, 0), k0));
-        out[(3 * a + 1) * ns] = wr * fma(c1, usum[1], fma(c2, U(a, 1), k1));
-        out[(3 * a + 2) * ns] = wr * fma(c1, usum[2], fma(c2, U(a, 2), k2));
-    }
-    out[12 * ns] = w * z[0];
-    out[13 * ns] = w * z[1];
-    out[14 * ns] = w * z[2];
-    out[15 * ns] = (w / rho) * ts;
-}
-
 // Residual element pass as a persistent pipeline.  CTA b walks element
 // chunks b, b+G, ... and, per chunk, its time-sample tiles (T samples, residual_tile(N)).
 //  * The chunk's metadata ("chunk pack": local nodes, per-node slot lists,
@@ -500,7 +410,7 @@ size_t residual_smem_bytes(int max_nloc, int max_rpack, int T) {
 
 // T = time samples per tile (4; 1 when N is small, where a 4-sample tile would
 // leave most threads idle — the host picks it, residual_tile()).
-template <int T, bool SUMM>
+template <int T>
 __global__ void __launch_bounds__(kChunkElems * T, RES_MINB * 4 / T) residual_chunk_kernel(ResidualChunkArgs a) {
     extern __shared__ __align__(128) unsigned char smraw[];
     constexpr int CE = kChunkElems, ndst = 7 * T, es = 29 * T, nds = res_nd_stride(T);
@@ -621,11 +531,6 @@ __global__ void __launch_bounds__(kChunkElems * T, RES_MINB * 4 / T) residual_ch
                                        int(pkc >> 24)};
                     element_residual_smem(geo + el * kTGeo, nd, nds, lc, T, t, a.rho, a.mu, a.nu,
                                           a.tau_mode, a.flag, slots + el * es + t);
-                    if (SUMM)  // separate pass: inlining it into the residual's pass 2 spilled 248 B
-                        element_tangent_summary_smem(geo + el * kTGeo, nd, nds, lc, T, t, a.rho, a.nu, a.tau_mode,
-                                                     a.flag,
-                                                     a.summ + ((size_t)(ch * CE + el) * 16) * a.summ_ns + n0 + t,
-                                                     a.summ_ns);
                 }
             }
             __syncthreads();
@@ -659,41 +564,27 @@ int residual_tile(int N) {
     return 1;
 }
 
-template <bool SUMM>
-static void launch_res_t(const ResidualChunkArgs& a, int g, int T, size_t sm, cudaStream_t st) {
-    if (T == 4)
-        residual_chunk_kernel<4, SUMM><<<g, kChunkElems * 4, sm, st>>>(a);
-    else if (T == 2)
-        residual_chunk_kernel<2, SUMM><<<g, kChunkElems * 2, sm, st>>>(a);
-    else
-        residual_chunk_kernel<1, SUMM><<<g, kChunkElems, sm, st>>>(a);
-}
-
 void launch_residual_chunks(const ResidualChunkArgs& a, int grid, int T, cudaStream_t st) {
     if (a.nchunks <= 0)
         return;
     note_launch();
     const size_t sm = residual_smem_bytes(a.max_nloc, a.max_rpack, T);
     const int g = min(grid, a.nchunks);
-    if (a.summ)
-        launch_res_t<true>(a, g, T, sm, st);
-    else
-        launch_res_t<false>(a, g, T, sm, st);
-}
-
-template <bool SUMM>
-static cudaError_t configure_res_t(int b, int T) {
     if (T == 4)
-        return cudaFuncSetAttribute(residual_chunk_kernel<4, SUMM>, cudaFuncAttributeMaxDynamicSharedMemorySize, b);
-    if (T == 2)
-        return cudaFuncSetAttribute(residual_chunk_kernel<2, SUMM>, cudaFuncAttributeMaxDynamicSharedMemorySize, b);
-    return cudaFuncSetAttribute(residual_chunk_kernel<1, SUMM>, cudaFuncAttributeMaxDynamicSharedMemorySize, b);
+        residual_chunk_kernel<4><<<g, kChunkElems * 4, sm, st>>>(a);
+    else if (T == 2)
+        residual_chunk_kernel<2><<<g, kChunkElems * 2, sm, st>>>(a);
+    else
+        residual_chunk_kernel<1><<<g, kChunkElems, sm, st>>>(a);
 }
 
 cudaError_t configure_residual_smem(size_t bytes, int T) {
     const int b = int(bytes < 48 * 1024 ? 48 * 1024 : bytes);
-    const cudaError_t e = configure_res_t<false>(b, T);
-    return e != cudaSuccess ? e : configure_res_t<true>(b, T);
+    if (T == 4)
+        return cudaFuncSetAttribute(residual_chunk_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, b);
+    if (T == 2)
+        return cudaFuncSetAttribute(residual_chunk_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, b);
+    return cudaFuncSetAttribute(residual_chunk_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, b);
 }
 
 // Node pass: sums the node's chunk partials in chunk order, completes the
@@ -1127,9 +1018,9 @@ cudaError_t run_fp64_peak(int blocks, int threads, int iters, double* out, float
 namespace hbgpu {
 cudaError_t residual_occupancy(int* blocks_per_sm, size_t smem, int T) {
     if (T == 4)
-        return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, residual_chunk_kernel<4, false>, kChunkElems * 4, smem);
+        return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, residual_chunk_kernel<4>, kChunkElems * 4, smem);
     if (T == 2)
-        return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, residual_chunk_kernel<2, false>, kChunkElems * 2, smem);
-    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, residual_chunk_kernel<1, false>, kChunkElems, smem);
+        return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, residual_chunk_kernel<2>, kChunkElems * 2, smem);
+    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, residual_chunk_kernel<1>, kChunkElems, smem);
 }
 }  // namespace hbgpu

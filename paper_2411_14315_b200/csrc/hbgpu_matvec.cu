@@ -381,15 +381,11 @@ void launch_lmatvec(const MatvecArgs& a_in, cudaStream_t st) {
     if (a_in.nn <= 0)
         return;
     MatvecArgs a = a_in;
-    // variant bit 0: row order by length (perm); bit 1 (N == 1): G-lane rows;
-    // bit 6: {A, kb, ke} row records (one load instead of perm -> row_ptr)
-    if (!(a.variant & 1)) {
-        a.perm = nullptr;
-        a.rows = nullptr;
-    }
-    if (!(a.variant & 64))
-        a.rows = nullptr;
-    if (a.N == 1 && (a.variant & 2)) {
+    // Rows in the length-balanced order as {A, kb, ke} records.  N == 1: four
+    // lanes per row (config 4: 0.277 -> 0.189 ms).  N > 1: four lanes per
+    // (row, sample) when the (row, sample) threads alone cannot fill the GPU
+    // (config 0: 26.7 -> 18.5 us; on the large meshes the split costs 35-40%).
+    if (a.N == 1) {
         constexpr int G = 4;
         const int blocks = (int)(((long)a.nn * G + 255) / 256);
         note_launch();
@@ -399,18 +395,9 @@ void launch_lmatvec(const MatvecArgs& a_in, cudaStream_t st) {
             lmatvec_n1g_kernel<false, G><<<blocks, 256, 0, st>>>(a);
         return;
     }
-    // variant bits 2-3 (N > 1): log2 of the lanes per (row, sample); bit 4:
-    // 4 lanes when the (row, sample) threads alone cannot fill the GPU (config 0:
-    // 26.7 -> 18.5 us; on the large meshes the split costs 35-40%)
-    int lg = (a.variant >> 2) & 3;
-    if (lg == 0 && (a.variant & 16) && (long)a.nn * a.N < 65536)
-        lg = 2;
-    if (a.N > 1 && lg == 1)
-        return launch_lmatvec_g<2>(a, st);
-    if (a.N > 1 && lg == 2)
+    const bool split = a.lanes == 4 || (a.lanes == 0 && (long)a.nn * a.N < 65536);
+    if (split)
         return launch_lmatvec_g<4>(a, st);
-    if (a.N > 1 && lg == 3)
-        return launch_lmatvec_g<8>(a, st);
     const int blocks = (a.nn + a.rows_per_cta - 1) / a.rows_per_cta;
     const int threads = a.rows_per_cta * a.N;
     const size_t smem =

@@ -535,241 +535,6 @@ __global__ void __launch_bounds__(THREADS, 512 / THREADS) tangent_pipe_kernel(Ta
     diag_sum();
 }
 
-// ---------------------------------------------------------------- fused variant
-// Fused assembly (hbgpu_assemble with both outputs): the residual element pass
-// has already formed every element's summaries once (element_tangent_summary_smem,
-// hbgpu_kernels.cu), so the row pipeline skips phase 1 entirely: per incidence it
-// bulk-copies the element's w rho kappa_a (3 series, a = the row's local index)
-// and w z, (w/rho) sum tau (4 series) straight into the summary buffer that
-// phase 2 reads, next to the 160-byte geometry record (phase-2 records).  No
-// neighbour state records, no tau: one barrier for the records, one after phase
-// 2.  The summary buffer is single: the next row's copies are issued after phase
-// 2 (the other resident CTAs cover their latency).
-struct FusedSmem {
-    int meta, tg, summ, rec, dpart, mbar, total;  // byte offsets
-};
-__host__ __device__ inline FusedSmem fused_layout(int max_pack, int mi, int N, int NS) {
-    FusedSmem L;
-    const int dpmax = (mi + kTanPart - 1) / kTanPart;
-    L.meta = 0;                                       // 2 x max_pack
-    L.tg = L.meta + 2 * pack_align16(max_pack);       // [inc][20]
-    L.summ = L.tg + mi * kTGeo * 8;                   // [inc][7][NS]
-    L.rec = L.summ + mi * 7 * NS * 8;                 // [p][8]
-    L.dpart = L.rec + 4 * mi * 64;                    // [part][8][N]
-    L.mbar = pack_align16(L.dpart + dpmax * 8 * N * 8);
-    L.total = L.mbar + 32;
-    return L;
-}
-
-size_t tangent_fused_smem(int max_pack, int max_inc, int N, int NS) {
-    return (size_t)fused_layout(max_pack, max_inc, N, NS).total;
-}
-
-// L2 prefetch of the next row's records before phase 2: measured slower (0.737 ->
-// 0.784 ms at config 1: warp 0 waits for the next pack before its phase-2 work)
-#ifndef FUSED_PREFETCH
-#define FUSED_PREFETCH 0
-#endif
-template <int THREADS, int NC>
-__global__ void __launch_bounds__(THREADS, 512 / THREADS) tangent_fused_kernel(TangentArgs a, PipeArgs pa) {
-    extern __shared__ __align__(128) unsigned char smraw[];
-    const int N = NC ? NC : a.N, NS = pa.summ_ns;
-    const FusedSmem Ls = fused_layout(pa.max_pack, a.max_inc, N, NS);
-    const int mpack = pack_align16(pa.max_pack);
-    uint64_t* mbar = reinterpret_cast<uint64_t*>(smraw + Ls.mbar);  // [0..1] packs, [2] gathers
-    double* summ = reinterpret_cast<double*>(smraw + Ls.summ);
-    double* rec = reinterpret_cast<double*>(smraw + Ls.rec);
-    double* dpart = reinterpret_cast<double*>(smraw + Ls.dpart);
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const double mu = a.mu, pc = a.pseudo_c;
-    const int r0 = blockIdx.x, rs = gridDim.x, nrows = pa.nrows;
-    if (threadIdx.x == 0) {
-        for (int k = 0; k < 3; ++k)
-            mbar_init(mbar + k, 1);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncthreads();
-
-    auto issue_pack = [&](int r, int slot) {  // warp 0, lane 0
-        const int p0 = __ldg(pa.pack_ptr + r), p1 = __ldg(pa.pack_ptr + r + 1);
-        const uint32_t bytes = (uint32_t)(p1 - p0) * 16u;
-        mbar_expect_tx(mbar + slot, bytes);
-        bulk_g2s(smraw + Ls.meta + slot * mpack, pa.pack + (size_t)p0 * 16, bytes, mbar + slot);
-    };
-    auto issue_gather = [&](int slot) {  // warp 0, all lanes
-        const unsigned char* m = smraw + Ls.meta + slot * mpack;
-        const int* h = reinterpret_cast<const int*>(m);
-        const int ninc = h[1], nblk = h[2];
-        const PackSections s = pack_sections(ninc, nblk, h[5]);
-        const int2* inc = reinterpret_cast<const int2*>(m + s.inc);
-        double* tg = reinterpret_cast<double*>(smraw + Ls.tg);
-        if (lane == 0)
-            mbar_expect_tx(mbar + 2, (uint32_t)(ninc * (kTGeo * 8 + 7 * NS * 8)));
-        __syncwarp();
-        for (int i = lane; i < ninc; i += 32) {
-            const long e = inc[i].x & 0x3FFFFFFF;
-            const int la = (unsigned)inc[i].x >> 30;
-            bulk_g2s(tg + (size_t)i * kTGeo, a.tgeom + e * kTGeo, kTGeo * 8, mbar + 2);
-            const double* se = pa.summ + (e * 16) * NS;
-            double* sd = summ + (size_t)i * 7 * NS;
-            bulk_g2s(sd, se + 3 * la * NS, 3 * NS * 8, mbar + 2);
-            bulk_g2s(sd + 3 * NS, se + 12 * NS, 4 * NS * 8, mbar + 2);
-        }
-    };
-
-    if (warp == 0 && r0 < nrows) {
-        if (lane == 0)
-            issue_pack(r0, 0);
-        mbar_wait(mbar + 0, 0);
-        issue_gather(0);
-    }
-    const int di = blockDim.x / N, dt = blockDim.x - di * N;
-    const int i_start = threadIdx.x / N, t_start = threadIdx.x - i_start * N;
-    long pd_blk = -1;
-    int pd_parts = 0;
-    bool pd_fix = false;
-    auto diag_sum = [&]() {
-        if (pd_blk < 0)
-            return;
-        for (int it = threadIdx.x; it < 8 * N; it += blockDim.x) {
-            const int sl = it / N, t = it - sl * N;
-            double v = 0.0;
-            for (int p = 0; p < pd_parts; ++p)
-                v += dpart[((size_t)p * 8 + sl) * N + t];
-            if (sl == 0 && pd_fix)
-                v = 1.0;
-            __stcs(a.pvals + (pd_blk * 8 + sl) * N + t, v);
-        }
-    };
-    int k = 0;
-    for (int r = r0; r < nrows; r += rs, ++k) {
-        const int ms = k & 1;
-        const bool more = r + rs < nrows;
-        if (warp == 0 && lane == 0 && more)
-            issue_pack(r + rs, ms ^ 1);
-        mbar_wait(mbar + ms, (k >> 1) & 1);
-        mbar_wait(mbar + 2, k & 1);
-
-        const unsigned char* m = smraw + Ls.meta + ms * mpack;
-        const int* h = reinterpret_cast<const int*>(m);
-        const int ninc = h[1], nblk = h[2], kdiag = h[3], k0 = h[4], nslots = h[5], dparts = h[6];
-        const bool afix = h[7] != 0;
-        const PackSections s = pack_sections(ninc, nblk, nslots);
-        const int4* sinfo = reinterpret_cast<const int4*>(m + s.sinfo);
-        const int2* inc = reinterpret_cast<const int2*>(m + s.inc);
-        const uint16_t* cont = reinterpret_cast<const uint16_t*>(m + s.cont);
-        const double* blkc = reinterpret_cast<const double*>(m + s.blkc);
-        const double* tg = reinterpret_cast<const double*>(smraw + Ls.tg);
-
-        diag_sum();
-        // contribution records {dN_a (3), gg, dN_b (3), summary offset}
-        for (int p = threadIdx.x; p < 4 * ninc; p += blockDim.x) {
-            const int ent = cont[p];
-            const int i = ent >> 2, b = ent & 3;
-            const int la = (unsigned)inc[i].x >> 30;
-            const double* gi = tg + i * kTGeo;
-            const double ga0 = gi[3 * la], ga1 = gi[3 * la + 1], ga2 = gi[3 * la + 2];
-            const double gb0 = gi[3 * b], gb1 = gi[3 * b + 1], gb2 = gi[3 * b + 2];
-            double2* o = reinterpret_cast<double2*>(rec + p * 8);
-            o[0] = make_double2(ga0, ga1);
-            o[1] = make_double2(ga2, fma(ga0, gb0, fma(ga1, gb1, ga2 * gb2)));
-            o[2] = make_double2(gb0, gb1);
-            o[3] = make_double2(gb2, __longlong_as_double((long long)i * 7 * NS));
-        }
-        __syncthreads();
-        // the next row's records: L2 prefetch now, the shared-memory copies after
-        // phase 2 (they then come from L2)
-        if (FUSED_PREFETCH && warp == 0 && more) {
-            mbar_wait(mbar + (ms ^ 1), ((k + 1) >> 1) & 1);
-            const unsigned char* mn = smraw + Ls.meta + (ms ^ 1) * mpack;
-            const int* hn = reinterpret_cast<const int*>(mn);
-            const int ninc_n = hn[1];
-            const int2* incn = reinterpret_cast<const int2*>(mn + pack_sections(ninc_n, hn[2], hn[5]).inc);
-            for (int i = lane; i < ninc_n; i += 32) {
-                const long e = incn[i].x & 0x3FFFFFFF;
-                const int la = (unsigned)incn[i].x >> 30;
-                const double* se = pa.summ + (e * 16) * NS;
-                bulk_prefetch_l2(a.tgeom + e * kTGeo, kTGeo * 8);
-                bulk_prefetch_l2(se + 3 * la * NS, 3 * NS * 8);
-                bulk_prefetch_l2(se + 12 * NS, 4 * NS * 8);
-            }
-        }
-        // phase 2: per (slot, sample) register accumulation (as tangent_pipe_kernel)
-        for (int it = threadIdx.x, slot = i_start, t = t_start; it < nslots * N;
-             it += blockDim.x, t += dt, slot += di + (t >= N), t -= (t >= N ? N : 0)) {
-            const int4 info = sinfo[slot];
-            const int j = info.z;
-            const bool bfix = info.w != 0;
-            double K = 0.0, G0 = 0.0, G1 = 0.0, G2 = 0.0, D0 = 0.0, D1 = 0.0, D2 = 0.0, L = 0.0;
-#pragma unroll 2
-            for (int p = info.x; p < info.y; ++p) {
-                const double2* rp = reinterpret_cast<const double2*>(rec + p * 8);
-                const double2 ra = rp[0], rb = rp[1], rc = rp[2], rd = rp[3];
-                const double* sp = summ + __double_as_longlong(rd.y) + t;
-                const double gb0 = rc.x, gb1 = rc.y, gb2 = rd.x;
-                K = fma(sp[0], gb0, fma(sp[NS], gb1, fma(sp[2 * NS], gb2, K)));
-                const double z0 = sp[3 * NS], z1 = sp[4 * NS], z2 = sp[5 * NS];
-                const double al = fma(z0, ra.x, fma(z1, ra.y, z2 * rb.x));
-                G0 = fma(al, gb0, G0);
-                G1 = fma(al, gb1, G1);
-                G2 = fma(al, gb2, G2);
-                const double alb = fma(z0, gb0, fma(z1, gb1, z2 * gb2));
-                D0 = fma(ra.x, alb, D0);
-                D1 = fma(ra.y, alb, D1);
-                D2 = fma(rb.x, alb, D2);
-                L = fma(rb.y, sp[6 * NS], L);
-            }
-            if (slot >= dparts || slot == 0) {
-                const double2* bc = reinterpret_cast<const double2*>(blkc + j * 8);
-                const double2 b0 = bc[0], b1 = bc[1], b2 = bc[2], b3 = bc[3];
-                K += fma(mu, b0.x, pc * b0.y);
-                G0 += b1.x;
-                G1 += b1.y;
-                G2 += b2.x;
-                D0 += b2.y;
-                D1 += b3.x;
-                D2 += b3.y;
-            }
-            if (afix || bfix)
-                K = 0.0;
-            if (afix)
-                G0 = G1 = G2 = 0.0;
-            if (bfix)
-                D0 = D1 = D2 = 0.0;
-            if (slot >= dparts) {
-                double* out = a.pvals + ((long)(k0 + j) * 8) * N + t;
-                __stcs(out, K);
-                __stcs(out + N, G0);
-                __stcs(out + 2 * N, G1);
-                __stcs(out + 3 * N, G2);
-                __stcs(out + 4 * N, D0);
-                __stcs(out + 5 * N, D1);
-                __stcs(out + 6 * N, D2);
-                __stcs(out + 7 * N, L);
-            } else {
-                double* o = dpart + (size_t)slot * 8 * N + t;
-                o[0] = K;
-                o[N] = G0;
-                o[2 * N] = G1;
-                o[3 * N] = G2;
-                o[4 * N] = D0;
-                o[5 * N] = D1;
-                o[6 * N] = D2;
-                o[7 * N] = L;
-            }
-        }
-        __syncthreads();
-        if (warp == 0 && more) {
-            mbar_wait(mbar + (ms ^ 1), ((k + 1) >> 1) & 1);
-            issue_gather(ms ^ 1);
-        }
-        pd_blk = k0 + kdiag;
-        pd_parts = dparts;
-        pd_fix = afix;
-    }
-    diag_sum();
-}
-
 // Compile-time time-sample counts of the BASELINE configs (N = 2 Nm - 1).
 #define HBGPU_PIPE_NC_LIST(X) X(1) X(5) X(7) X(19) X(31) X(47)
 static bool pipe_nc_listed(int N) {
@@ -857,69 +622,6 @@ void launch_tangent_pipe(const TangentArgs& a, const PipeArgs& p, int threads, i
     case 256: launch_pipe_t<256>(a, p, grid, smem, st); break;
     case 512: launch_pipe_t<512>(a, p, grid, smem, st); break;
     default: launch_pipe_t<128>(a, p, grid, smem, st); break;
-    }
-}
-
-// fused-variant configuration / launch (same CTA widths and compile-time N list)
-template <int T>
-static cudaError_t configure_fused_t(size_t bytes) {
-    const int b = int(bytes < 48 * 1024 ? 48 * 1024 : bytes);
-    cudaError_t e = cudaFuncSetAttribute(tangent_fused_kernel<T, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, b);
-#define HBGPU_CFG_FNC(n)                                                                                 \
-    if (e == cudaSuccess)                                                                                \
-        e = cudaFuncSetAttribute(tangent_fused_kernel<T, n>, cudaFuncAttributeMaxDynamicSharedMemorySize, b);
-    HBGPU_PIPE_NC_LIST(HBGPU_CFG_FNC)
-#undef HBGPU_CFG_FNC
-    return e;
-}
-
-cudaError_t configure_tangent_fused_smem(int threads, size_t bytes) {
-    switch (threads) {
-    case 32: return configure_fused_t<32>(bytes);
-    case 64: return configure_fused_t<64>(bytes);
-    case 128: return configure_fused_t<128>(bytes);
-    case 256: return configure_fused_t<256>(bytes);
-    case 512: return configure_fused_t<512>(bytes);
-    default: return cudaErrorInvalidValue;
-    }
-}
-
-cudaError_t tangent_fused_occupancy(int threads, int* blocks_per_sm, size_t smem) {
-    switch (threads) {
-    case 32: return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, tangent_fused_kernel<32, 0>, 32, smem);
-    case 64: return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, tangent_fused_kernel<64, 0>, 64, smem);
-    case 128: return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, tangent_fused_kernel<128, 0>, 128, smem);
-    case 256: return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, tangent_fused_kernel<256, 0>, 256, smem);
-    case 512: return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, tangent_fused_kernel<512, 0>, 512, smem);
-    default: return cudaErrorInvalidValue;
-    }
-}
-
-template <int T>
-static void launch_fused_t(const TangentArgs& a, const PipeArgs& p, int grid, size_t smem, cudaStream_t st) {
-    switch (a.N) {
-#define HBGPU_LAUNCH_FNC(n)                                                  \
-    case n:                                                                  \
-        tangent_fused_kernel<T, n><<<grid, T, smem, st>>>(a, p);             \
-        return;
-        HBGPU_PIPE_NC_LIST(HBGPU_LAUNCH_FNC)
-#undef HBGPU_LAUNCH_FNC
-    default:
-        tangent_fused_kernel<T, 0><<<grid, T, smem, st>>>(a, p);
-    }
-}
-
-void launch_tangent_fused(const TangentArgs& a, const PipeArgs& p, int threads, int grid_x, size_t smem,
-                          cudaStream_t st) {
-    if (p.nrows <= 0)
-        return;
-    note_launch();
-    switch (threads) {
-    case 32: launch_fused_t<32>(a, p, grid_x, smem, st); break;
-    case 64: launch_fused_t<64>(a, p, grid_x, smem, st); break;
-    case 256: launch_fused_t<256>(a, p, grid_x, smem, st); break;
-    case 512: launch_fused_t<512>(a, p, grid_x, smem, st); break;
-    default: launch_fused_t<128>(a, p, grid_x, smem, st); break;
     }
 }
 
