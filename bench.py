@@ -802,6 +802,133 @@ def solve_config0(cpu_reference=False):
     return out
 
 
+def cpu_breadth(args):
+    """CPU-baseline breadth: the compiled reference on the
+    GPU box's host cores, next to the GPU figures of the same config in the
+    same run, for configs 0-4.  CPU calls run on a leading sub-mesh sized to a
+    time budget (stated); rates are per element / per byte so they compare
+    with the GPU's full-mesh rates.  Per config:
+      assemble_residual at threads = 1 and nproc, its two nodal H passes alone
+      (SpectralOperators::apply_many over 2 x 3 x nodes series), assemble_tangent
+      (serial by design), TangentOperator::matvec x10 at 1 and nproc threads
+      (GB/s of compulsory bytes), gmres_solve iterations at nproc threads
+      (bounded: per-iteration seconds), and for config 0 two Newton iterations
+      of solve_harmonic.  One JSON line per config."""
+    import torch
+
+    from oracle import bindings as ob
+    from paper_2411_14315_b200 import cases, hbgpu
+
+    nproc = os.cpu_count() or 1
+    cpu = cpu_model()
+    for cfg in [int(c) for c in args.cpu_breadth.split(",")]:
+        if cfg == 4:
+            prob, state, pdt = problem_and_state(4)
+        else:
+            prob = cases.config_problem(cfg)
+            state = cases.random_state(prob.mesh.num_nodes, prob.N, 1000 + cfg)
+            pdt = auto_pseudo_dt(prob)
+        mesh, M, N = prob.mesh, prob.modes, prob.N
+        ne, nn = mesh.num_elements, mesh.num_nodes
+        out = {"cpu_breadth": cfg, "elements": ne, "nodes": nn, "modes": M, "N": N, "host_cpu": cpu,
+               "nproc": nproc, "fftw": "O(N^2) DFT shim (libfftw3 absent)"}
+        # ---- GPU, full mesh
+        ctx = hbgpu.GpuContext(mesh)
+        ctx.set_basis(M, prob.period)
+        ctx.set_fluid(prob.rho, prob.mu)
+        ctx.set_bcs(prob.dirichlet_g, prob.neumann, prob.backflow_beta)
+        ctx.set_assembly_config(0, pdt)
+        stream = torch.cuda.ExternalStream(ctx.stream)
+        d_s = torch.from_numpy(state).cuda()
+        d_r = torch.empty_like(d_s)
+        for _ in range(2):
+            ctx.assemble_residual_dev(d_s.data_ptr(), d_r.data_ptr())
+            ctx.assemble_tangent_dev(d_s.data_ptr())
+        ctx.assemble_mass()
+        torch.cuda.synchronize()
+
+        def gtime(fn, reps=3):
+            ts = []
+            for _ in range(reps):
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                with torch.cuda.stream(stream):
+                    a.record(stream)
+                    fn()
+                    b.record(stream)
+                torch.cuda.synchronize()
+                ts.append(a.elapsed_time(b) * 1e-3)
+            return float(np.median(ts))
+
+        g_res = gtime(lambda: ctx.assemble_residual_dev(d_s.data_ptr(), d_r.data_ptr()))
+        g_tan = gtime(lambda: ctx.assemble_tangent_dev(d_s.data_ptr()))
+        y = torch.from_numpy(np.random.default_rng(5).uniform(-1, 1, nn * 4 * N)).cuda()
+        o = torch.empty_like(y)
+        g_mv = gtime(lambda: [ctx.matvec_dev(y.data_ptr(), o.data_ptr()) for _ in range(10)]) / 10
+        nnz = ctx.nnz
+        gi = 60
+        ctx.jacobi_dev()
+        ctx.gmres_dev(d_r.data_ptr(), o.data_ptr(), hbgpu.KrylovConfig(max_iters=1))
+        t0 = time.perf_counter()
+        it_g, _, _ = ctx.gmres_dev(d_r.data_ptr(), o.data_ptr(), hbgpu.KrylovConfig(max_iters=gi, tolerance=1e-30))
+        torch.cuda.synchronize()
+        g_gm = (time.perf_counter() - t0) / max(it_g, 1)
+        out["gpu"] = {"residual_s": g_res, "tangent_s": g_tan,
+                      "assembly_elements_modes_per_s": ne * M / (g_res + g_tan),
+                      "matvec_s": g_mv, "matvec_gbs": spmv_bytes(nnz, nn, N) / g_mv / 1e9,
+                      "gmres_s_per_iter": g_gm, "gmres_iters_timed": it_g}
+        ctx.close()
+        del d_s, d_r, y, o
+        torch.cuda.empty_cache()
+        # ---- CPU reference on a leading sub-mesh
+        budget = args.cpu_budget
+        rctx, ne_s, st, desc, full = cpu_reference_sample(prob, state, nproc, budget, pdt)
+        sub_nn = len(st) // (4 * N)
+
+        def ctime(fn, reps=2):
+            best = None
+            for _ in range(reps):
+                t0 = time.perf_counter()
+                fn()
+                t = time.perf_counter() - t0
+                best = t if best is None else min(best, t)
+            return best
+
+        c_res_n = ctime(lambda: rctx.residual(st, nproc))
+        c_res_1 = ctime(lambda: rctx.residual(st, 1), 1)
+        series = np.random.default_rng(3).uniform(-1, 1, 3 * sub_nn * N)
+        c_h = 2 * ctime(lambda: ob.ref_apply_h(M, prob.period, series), 1) if N > 1 else 0.0
+        c_tan = ctime(lambda: rctx.tangent(st), 1)
+        yv = np.random.default_rng(6).uniform(-1, 1, len(st))
+        c_mv_n = ctime(lambda: [rctx.matvec(yv, nproc) for _ in range(10)], 1) / 10
+        c_mv_1 = ctime(lambda: [rctx.matvec(yv, 1) for _ in range(3)], 1) / 3
+        inv, _ = rctx.jacobi()
+        ci = 20
+        t0 = time.perf_counter()
+        gres = rctx.gmres(rctx.residual(st, nproc), inv, max_iters=ci, tol=1e-30, threads=nproc)
+        c_gm = (time.perf_counter() - t0 - c_res_n) / max(gres["iterations"], 1)
+        sub_nnz = len(rctx.tangent(st)) // (8 * N)
+        mvb = spmv_bytes(sub_nnz, sub_nn, N)
+        out["cpu"] = {"sample": desc, "sample_elements": ne_s, "sample_nodes": sub_nn,
+                      "residual_s_threads_nproc": c_res_n, "residual_s_threads_1": c_res_1,
+                      "h_passes_s": c_h, "residual_without_h_s_threads_1": max(c_res_1 - c_h, 0.0),
+                      "tangent_s": c_tan,
+                      "assembly_elements_modes_per_s_nproc": ne_s * M / (c_res_n + c_tan),
+                      "assembly_elements_modes_per_s_1": ne_s * M / (c_res_1 + c_tan),
+                      "matvec_s_nproc": c_mv_n, "matvec_gbs_nproc": mvb / c_mv_n / 1e9,
+                      "matvec_s_1": c_mv_1, "matvec_gbs_1": mvb / c_mv_1 / 1e9,
+                      "gmres_s_per_iter_nproc": c_gm, "gmres_iters_timed": gres["iterations"],
+                      "note": "h_passes_s: the residual's nodal H*u and H*s passes through the reference's "
+                              "apply_many (1 thread); assemble_tangent and GMRES orthogonalisation are "
+                              "serial in the reference"}
+        per_el_gpu = ne * M / (g_res + g_tan)
+        out["gpu_over_cpu_assembly_nproc"] = per_el_gpu / out["cpu"]["assembly_elements_modes_per_s_nproc"]
+        if cfg == 0:
+            rc = ob.ref_context(prob)
+            sol = rc.solve(pseudo_dt=auto_pseudo_dt(prob) * 10.0, max_newton=2, threads=nproc)
+            out["cpu"]["solve_two_newton_iters_s"] = sol["total_seconds"]
+        print(json.dumps(out), flush=True)
+
+
 def time_solve(args):
     """The paper's comparison baseline: generalized-alpha
     time stepping (time_solver.cpp:269-485) of config 0 on the GPU with the
@@ -865,6 +992,8 @@ def main():
     ap.add_argument("--no-newton", dest="newton", action="store_false")
     ap.add_argument("--no-five-call", dest="five_call", action="store_false")
     ap.add_argument("--headline-config", type=int, default=4, choices=[1, 4])
+    ap.add_argument("--cpu-breadth", default=None, help="e.g. 0,1,2,3,4: CPU baseline breadth (separate run)")
+    ap.add_argument("--cpu-budget", type=float, default=4.0, help="seconds per CPU residual+tangent sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-solve", action="store_true", help="also time the reference's converged config-0 solve")
     ap.add_argument("--sweep4", action="store_true", help="config-4 operator sweep (separate run)")
@@ -875,6 +1004,9 @@ def main():
     args = ap.parse_args()
     if args.time_solve:
         time_solve(args)
+        return
+    if args.cpu_breadth:
+        cpu_breadth(args)
         return
     if args.sweep4:
         sweep_config4(args)
