@@ -150,6 +150,21 @@ int hbgpu_gmres(hbgpu_ctx* ctx, const double* rhs, const double* inv_diag,
                 const hbgpu_krylov_cfg* cfg, double* x, hbgpu_krylov_result* result,
                 double* history, int history_capacity);
 
+/* Host-side linear operator for hbgpu_gmres_apply: out = A y, n doubles each. */
+typedef void (*hbgpu_apply_fn)(void* user, const double* y, double* out);
+
+/* gmres_solve(const std::function<void(span<const double>, span<double>)>& apply,
+ * rhs, inv_diag, cfg) (linalg.hpp:107-109, linalg.cpp:167-293): the generic
+ * overload, with the operator supplied by the caller on the host.  The Krylov
+ * basis, Gram-Schmidt passes, Givens rotations and the restart / stagnation /
+ * iteration-cap logic run on the device as in hbgpu_gmres; each operator
+ * application copies the vector to the host, calls `apply`, and copies the
+ * result back.  n <= the context's state length.  Overwrites the context's
+ * Jacobi vector. */
+int hbgpu_gmres_apply(hbgpu_ctx* ctx, hbgpu_apply_fn apply, void* user, long long n, const double* rhs,
+                      const double* inv_diag, const hbgpu_krylov_cfg* cfg, double* x,
+                      hbgpu_krylov_result* result, double* history, int history_capacity);
+
 /* ---- device-resident fast path (device pointers, ctx stream) ----------- */
 int hbgpu_assemble_residual_dev(hbgpu_ctx* ctx, const double* d_state, double* d_residual);
 int hbgpu_assemble_tangent_dev(hbgpu_ctx* ctx, const double* d_state);

@@ -113,6 +113,27 @@ int main() {
     std::vector<double> zero(L.size(), 0.0);
     const double gmres_scaled = rel(sres, zero) / rel(sb, zero);
 
+    // the generic gmres_solve overload (linalg.hpp:107-109) with a lambda:
+    // the reference's zero-operator stagnation case (test_linalg.cpp:239-247)
+    // and the tangent operator as a lambda, against the reference's generic GMRES
+    const std::function<void(std::span<const double>, std::span<double>)> zero_op =
+        [](std::span<const double>, std::span<double> out) { std::fill(out.begin(), out.end(), 0.0); };
+    std::vector<double> b8(8, 1.0), ones8(8, 1.0);
+    const auto g_zero = gpu::gmres_solve(zero_op, b8, ones8, KrylovConfig{});
+    const bool zero_ok = g_zero.status == KrylovStatus::Stagnated && std::abs(g_zero.relative_residual - 1.0) < 1e-12;
+    const std::function<void(std::span<const double>, std::span<double>)> Lop =
+        [&L](std::span<const double> y, std::span<double> out) { L.matvec(y, out); };
+    KrylovConfig kc2;
+    kc2.tolerance = 1e-9;
+    kc2.restart = 60;
+    kc2.max_iters = 3000;
+    const auto g_lam = gpu::gmres_solve(Lop, r_ref, pc_ref.inv_diag, kc2);
+    const auto r_lam = gmres_solve(Lop, r_ref, pc_ref.inv_diag, kc2);
+    const double e_lambda = rel(g_lam.x, r_lam.x);
+    const bool lambda_ok = g_lam.status == KrylovStatus::Converged && r_lam.status == KrylovStatus::Converged &&
+                           e_lambda < 1e-6 &&
+                           std::abs(g_lam.iterations - r_lam.iterations) <= std::max(3, r_lam.iterations / 10);
+
     SolverConfig scfg;
     scfg.newton_tol_orders = 10.0;
     scfg.max_newton_iters = 300;
@@ -138,7 +159,7 @@ int main() {
     const double e_time_u = rel(ts_gpu.cycle.u, ts_ref.cycle.u);
     const double e_time_p = rel(ts_gpu.cycle.p, ts_ref.cycle.p);
 
-    const bool ok = e_inplace_op < 1e-12 && e_inplace_g < 1e-8 && d_g > 1e-3 &&
+    const bool ok = zero_ok && lambda_ok && e_inplace_op < 1e-12 && e_inplace_g < 1e-8 && d_g > 1e-3 &&
                     e_res < 1e-12 && e_tan < 1e-12 && e_mass < 1e-15 && e_mv < 1e-12 &&
                     e_jac < 1e-15 && gmres_scaled <= 1e-8 * 1.0001 && s_ref.log.converged &&
                     s_gpu.log.converged && e_solve < 1e-8 && e_time_u < 1e-8 && e_time_p < 1e-8 &&
@@ -149,13 +170,15 @@ int main() {
         "\"solve_state\": %.3e, \"newton_ref\": %zu, \"newton_gpu\": %zu, \"solve_ref_s\": %.3f, "
         "\"solve_gpu_s\": %.3f, \"time_u\": %.3e, \"time_p\": %.3e, \"time_newton_ref\": %d, "
         "\"time_newton_gpu\": %d, \"time_ref_s\": %.3f, \"time_gpu_s\": %.3f, "
-        "\"inplace_operator\": %.3e, \"inplace_dirichlet\": %.3e, \"ok\": %s}\n",
+        "\"inplace_operator\": %.3e, \"inplace_dirichlet\": %.3e, \"generic_gmres_zero_stagnated\": %s, "
+        "\"generic_gmres_lambda\": %.3e, \"generic_gmres_iters\": [%d, %d], \"ok\": %s}\n",
         mesh.num_elements(), N, e_res, e_tan, e_mass, e_mv, e_jac, gmres_scaled, lin.iterations,
         e_solve, s_ref.log.entries.size(), s_gpu.log.entries.size(),
         std::chrono::duration<double>(t1 - t0).count(),
         std::chrono::duration<double>(t2 - t1).count(), e_time_u, e_time_p, ts_ref.total_newton_iters,
         ts_gpu.total_newton_iters, std::chrono::duration<double>(t4 - t3).count(),
-        std::chrono::duration<double>(t5 - t4).count(), e_inplace_op, e_inplace_g, ok ? "true" : "false");
+        std::chrono::duration<double>(t5 - t4).count(), e_inplace_op, e_inplace_g, zero_ok ? "true" : "false",
+        e_lambda, g_lam.iterations, r_lam.iterations, ok ? "true" : "false");
     gpu::release(mesh);
     return ok ? 0 : 1;
 }

@@ -330,6 +330,70 @@ KrylovResult gmres_solve(const TangentOperator& L, std::span<const double> rhs,
     return res;
 }
 
+namespace {
+// Vector-only contexts for the generic GMRES overload: a node set without
+// elements (state length 4 x nodes at one time sample), one per vector length.
+std::map<size_t, hbgpu_ctx*>& vec_contexts() {
+    static std::map<size_t, hbgpu_ctx*> m;
+    return m;
+}
+
+hbgpu_ctx* vector_context(size_t n) {
+    auto& m = vec_contexts();
+    auto it = m.find(n);
+    if (it != m.end())
+        return it->second;
+    const int nodes = int((n + 3) / 4);
+    std::vector<double> xyz(size_t(nodes) * 3, 0.0);
+    std::vector<unsigned char> dir(size_t(nodes), 0);
+    int dummy_conn = 0;
+    hbgpu_mesh_desc d{};
+    d.num_nodes = nodes;
+    d.num_elements = 0;
+    d.xyz = xyz.data();
+    d.conn = &dummy_conn;
+    d.dirichlet = dir.data();
+    int st = 0;
+    hbgpu_ctx* c = hbgpu_create(&d, &st);
+    if (!c)
+        rethrow(st, hbgpu_create_error());
+    check(c, hbgpu_set_basis(c, 1, 1.0));
+    m[n] = c;
+    return c;
+}
+}  // namespace
+
+KrylovResult gmres_solve(const std::function<void(std::span<const double>, std::span<double>)>& apply,
+                         std::span<const double> rhs, std::span<const double> inv_diag,
+                         const KrylovConfig& cfg) {
+    if (rhs.size() != inv_diag.size() || rhs.empty())
+        throw std::invalid_argument("gmres_solve: size mismatch");
+    const size_t n = rhs.size();
+    hbgpu_ctx* c = vector_context(n);
+    struct Tramp {
+        const std::function<void(std::span<const double>, std::span<double>)>* fn;
+        size_t n;
+    } tr{&apply, n};
+    auto cb = [](void* user, const double* y, double* out) {
+        auto* t = static_cast<Tramp*>(user);
+        (*t->fn)(std::span<const double>(y, t->n), std::span<double>(out, t->n));
+    };
+    KrylovResult res;
+    res.x.resize(n);
+    res.history.resize(size_t(cfg.max_iters) + 2);
+    hbgpu_krylov_cfg kc{cfg.restart, cfg.max_iters, cfg.tolerance};
+    hbgpu_krylov_result kr{};
+    check(c, hbgpu_gmres_apply(c, cb, &tr, (long long)n, rhs.data(), inv_diag.data(), &kc, res.x.data(), &kr,
+                               res.history.data(), int(res.history.size())));
+    res.history.resize(size_t(kr.history_len));
+    res.iterations = kr.iterations;
+    res.relative_residual = kr.relative_residual;
+    res.status = kr.status == 0 ? KrylovStatus::Converged
+                 : kr.status == 1 ? KrylovStatus::MaxIterations
+                                  : KrylovStatus::Stagnated;
+    return res;
+}
+
 HbSolution solve_harmonic(const Mesh& mesh, const std::vector<ElementGeometry>& geoms,
                           const SpectralBasis& basis, const FluidProperties& props,
                           const BoundaryConditionSet& bcs, const SolverConfig& cfg) {

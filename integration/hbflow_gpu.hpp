@@ -22,6 +22,7 @@
 #include "hbflow/linalg.hpp"
 #include "hbflow/time_solver.hpp"
 
+#include <functional>
 #include <span>
 #include <vector>
 
@@ -49,6 +50,14 @@ JacobiPreconditioner jacobi_preconditioner(const TangentOperator& L);
 
 KrylovResult gmres_solve(const TangentOperator& L, std::span<const double> rhs,
                          const JacobiPreconditioner& pc, const KrylovConfig& cfg);
+
+/// The generic overload (linalg.hpp:107-109): any host operator.  The Krylov
+/// basis and its orthogonalisation live on the device; each application of
+/// `apply` goes through host buffers.  A vector-only device context is cached
+/// per vector length.
+KrylovResult gmres_solve(const std::function<void(std::span<const double>, std::span<double>)>& apply,
+                         std::span<const double> rhs, std::span<const double> inv_diag,
+                         const KrylovConfig& cfg);
 
 HbSolution solve_harmonic(const Mesh& mesh, const std::vector<ElementGeometry>& geoms,
                           const SpectralBasis& basis, const FluidProperties& props,

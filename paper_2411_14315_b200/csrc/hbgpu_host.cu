@@ -86,6 +86,12 @@ struct Tooling {
 
 struct hbgpu_ctx {
     Tooling tool;
+    // host operator of hbgpu_gmres_apply (gmres_solve(apply, ...), linalg.hpp:107-109):
+    // while set, GMRES applies it through host buffers instead of the L-matvec
+    hbgpu_apply_fn host_op = nullptr;
+    void* host_op_user = nullptr;
+    long host_n = 0;                   // vector length of the host operator
+    std::vector<double> host_in, host_out;
     int nn = 0, ne = 0;
     int M = 0, N = 0;
     double period = 1.0, omega = 0.0;
@@ -850,8 +856,20 @@ static int gmres_dev(hbgpu_ctx* c, const double* d_rhs, const double* d_inv,
                      const hbgpu_krylov_cfg* kc, double* d_x, hbgpu_krylov_result* res,
                      double* history, int hcap) {
     cudaStream_t st = c->stream;
-    const long n = long(c->state_len());
+    const long n = c->host_op ? c->host_n : long(c->state_len());
     const int m = std::max(1, kc->restart);
+    // the operator: out = [S] A in (S: the split Jacobi scaling, d_scale_out)
+    auto apply_op = [&](const double* d_in, double* d_out, const double* d_scale_out) -> int {
+        if (!c->host_op)
+            return matvec_dev(c, d_in, d_out, nullptr, true, d_scale_out);
+        CK(c, cudaMemcpyAsync(c->host_in.data(), d_in, sizeof(double) * size_t(n), cudaMemcpyDeviceToHost, st));
+        CK(c, cudaStreamSynchronize(st));
+        c->host_op(c->host_op_user, c->host_in.data(), c->host_out.data());
+        CK(c, cudaMemcpyAsync(d_out, c->host_out.data(), sizeof(double) * size_t(n), cudaMemcpyHostToDevice, st));
+        if (d_scale_out)
+            launch_mul(d_scale_out, d_out, d_out, n, st);
+        return check_launch(c);
+    };
     res->iterations = 0;
     res->relative_residual = 1.0;
     res->status = 0;
@@ -880,7 +898,7 @@ static int gmres_dev(hbgpu_ctx* c, const double* d_rhs, const double* d_inv,
     // HBGPU_GMRES_HOST=1 (or a restart too long for the Arnoldi kernel's shared
     // memory, m > ~700): the host-driven step loop, one synchronisation per
     // step; else the device-resident cycle
-    const bool devloop = !c->tool.gmres_host && arnoldi_step_smem(m) <= 200 * 1024;
+    const bool devloop = !c->tool.gmres_host && !c->host_op && arnoldi_step_smem(m) <= 200 * 1024;
     ArnoldiDev ad{};
     if (devloop) {
         const size_t hsz = size_t(m + 2) * size_t(m + 1);
@@ -1029,7 +1047,7 @@ static int gmres_dev(hbgpu_ctx* c, const double* d_rhs, const double* d_inv,
                 // last step of the cycle: only finalise column j-1
                 const bool last = (j == m) || (res->iterations + (j >= 1 ? 1 : 0) >= kc->max_iters);
                 if (!last)
-                    TRY(matvec_dev(c, c->z.p, c->w.p, nullptr, true, c->scale.p));  // w = S A S u_j
+                    TRY(apply_op(c->z.p, c->w.p, c->scale.p));  // w = S A S u_j
                 launch_dcgs_dots(V, n, j, u, last ? nullptr : c->w.p, n, c->partial.p, st);
                 const int rows = last ? j + 1 : 2 * j + 3;
                 launch_reduce_partials(c->partial.p, rows, c->red.p, 0, st);
@@ -1133,7 +1151,7 @@ static int gmres_dev(hbgpu_ctx* c, const double* d_rhs, const double* d_inv,
             launch_basis_combine(V, n, j, c->red.p, c->scale.p, d_x, n, st);
         }
         // recomputed scaled residual r = S (rhs - L x)
-        TRY(matvec_dev(c, d_x, c->w.p, nullptr, true));
+        TRY(apply_op(d_x, c->w.p, nullptr));
         launch_scaled_diff(c->scale.p, d_rhs, c->w.p, c->tmp.p, n, st);
         rsrc = c->tmp.p;
         TRY(dot_dev(c, c->tmp.p, c->tmp.p, n, &rnorm, true));
@@ -1875,6 +1893,28 @@ int hbgpu_fp64_peak(double* tflops) {
     if (e != cudaSuccess)
         return HBGPU_ERR_CUDA;
     *tflops = 2.0 * 16.0 * double(iters) * blocks * threads / (double(ms) * 1e-3) / 1e12;
+    return HBGPU_OK;
+}
+
+int hbgpu_gmres_apply(hbgpu_ctx* c, hbgpu_apply_fn apply, void* user, long long n, const double* rhs,
+                      const double* inv_diag, const hbgpu_krylov_cfg* cfg, double* x,
+                      hbgpu_krylov_result* result, double* history, int hcap) {
+    TRY(ensure_basis(c));
+    if (!apply || !rhs || !inv_diag || !cfg || !x || !result || n <= 0 || n > c->state_len())
+        return fail(c, HBGPU_ERR_INVALID, "gmres_apply: bad arguments (need 0 < n <= the context's state length)");
+    c->host_in.resize(size_t(n));
+    c->host_out.resize(size_t(n));
+    CK(c, cudaMemcpyAsync(c->inv.p, inv_diag, sizeof(double) * size_t(n), cudaMemcpyHostToDevice, c->stream));
+    CK(c, cudaMemcpyAsync(c->b.p, rhs, sizeof(double) * size_t(n), cudaMemcpyHostToDevice, c->stream));
+    c->host_op = apply;
+    c->host_op_user = user;
+    c->host_n = long(n);
+    const int st = gmres_dev(c, c->b.p, c->inv.p, cfg, c->x.p, result, history, hcap);
+    c->host_op = nullptr;
+    c->host_op_user = nullptr;
+    c->inv_valid = false;  // the context's Jacobi vector was overwritten
+    TRY(st);
+    CK(c, cudaMemcpy(x, c->x.p, sizeof(double) * size_t(n), cudaMemcpyDeviceToHost));
     return HBGPU_OK;
 }
 

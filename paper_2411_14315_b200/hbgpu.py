@@ -175,6 +175,9 @@ _set_mass = _sig("hbgpu_set_mass", C.c_int, [_vp, _vp])
 _matvec = _sig("hbgpu_matvec", C.c_int, [_vp, _vp, _vp])
 _bsr_matvec = _sig("hbgpu_bsr_matvec", C.c_int, [_vp, _vp, _vp])
 _jacobi = _sig("hbgpu_jacobi", C.c_int, [_vp, _vp, _ip])
+_APPLY_FN = C.CFUNCTYPE(None, C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_double))
+_gmres_apply = _sig("hbgpu_gmres_apply", C.c_int, [_vp, _APPLY_FN, _vp, C.c_longlong, _vp, _vp,
+                                                   C.POINTER(_KrylovCfg), _vp, C.POINTER(_KrylovRes), _vp, C.c_int])
 _gmres = _sig("hbgpu_gmres", C.c_int, [_vp, _vp, _vp, C.POINTER(_KrylovCfg), _vp, C.POINTER(_KrylovRes), _vp, C.c_int])
 _residual_dev = _sig("hbgpu_assemble_residual_dev", C.c_int, [_vp, _vp, _vp])
 _tangent_dev = _sig("hbgpu_assemble_tangent_dev", C.c_int, [_vp, _vp])
@@ -500,6 +503,31 @@ class GpuContext:
         deg = C.c_int(0)
         self._check(_jacobi(self._h, _ptr(inv), C.byref(deg)))
         return inv, deg.value
+
+    def gmres_apply(self, apply, rhs, inv_diag, cfg: KrylovConfig | None = None) -> KrylovResult:
+        """gmres_solve(apply, rhs, inv_diag, cfg) (linalg.hpp:107-109): the
+        generic overload with a host operator `apply(y) -> A y` (numpy arrays);
+        Krylov basis and orthogonalisation on the device."""
+        cfg = cfg or KrylovConfig()
+        b = _f64(rhs).reshape(-1)
+        inv = _f64(inv_diag).reshape(-1)
+        n = b.size
+        if inv.size != n:
+            raise ValueError("gmres_apply: size mismatch")
+
+        def cb(_user, y, out):
+            yv = np.ctypeslib.as_array(y, shape=(n,))
+            ov = np.ctypeslib.as_array(out, shape=(n,))
+            ov[:] = apply(yv.copy())
+
+        fn = _APPLY_FN(cb)
+        x = np.empty(n)
+        res = _KrylovRes()
+        hist = np.empty(cfg.max_iters + 2)
+        kc = _KrylovCfg(cfg.restart, cfg.max_iters, cfg.tolerance)
+        self._check(_gmres_apply(self._h, fn, None, n, _ptr(b), _ptr(inv), C.byref(kc), _ptr(x), C.byref(res),
+                                 _ptr(hist), len(hist)))
+        return KrylovResult(x, res.iterations, res.relative_residual, res.status, hist[: res.history_len].copy())
 
     def gmres(self, rhs, cfg: KrylovConfig | None = None, inv_diag=None) -> KrylovResult:
         cfg = cfg or KrylovConfig()

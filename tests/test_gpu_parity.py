@@ -660,3 +660,32 @@ def test_max_modes_and_bcs_validation(gpu):
     assert np.array_equal(ctx.assemble_residual(s), r0)
     with pytest.raises(ValueError):
         ctx.set_basis(33, 1.0)
+
+
+def test_gmres_generic_host_operator(gpu):
+    """The generic gmres_solve(apply, rhs, inv_diag, cfg) overload
+    (linalg.hpp:107-109) through hbgpu_gmres_apply: the zero operator of
+    test_linalg.cpp:239-247 (n = 8) stagnates with relative residual 1, and the
+    restated tangent operator as a host callback converges to the same
+    solution and iteration count as the device operator."""
+    from paper_2411_14315_b200.hbgpu import KrylovConfig
+
+    prob = tube_problem(3, h=0.25, traction=False)
+    ctx = gpu_ctx(prob, 0, 0.3)
+    res0 = ctx.gmres_apply(lambda y: np.zeros_like(y), np.ones(8), np.ones(8))
+    assert res0.status == 2 and abs(res0.relative_residual - 1.0) < 1e-12
+    orc = ob.Restated(prob, tau_mode=0, pseudo_dt=0.3)
+    s = cases.random_state(prob.mesh.num_nodes, prob.N, 61, 0.5)
+    p = ctx.assemble_tangent(s)
+    m = orc.mass()
+    inv, _ = ctx.jacobi()
+    b = cases.random_state(prob.mesh.num_nodes, prob.N, 62)
+    cfg = KrylovConfig(restart=60, max_iters=2000, tolerance=1e-9)
+    dev = ctx.gmres(b, cfg)
+    host = ctx.gmres_apply(lambda y: orc.matvec(p, m, y), b, inv, cfg)
+    assert dev.status == 0 and host.status == 0
+    assert abs(dev.iterations - host.iterations) <= 2
+    assert rel(host.x, dev.x) < 1e-6
+    scale = np.sqrt(np.abs(inv))
+    rr = np.linalg.norm(scale * (b - orc.matvec(p, m, host.x))) / np.linalg.norm(scale * b)
+    assert rr <= 1e-9 * 1.0001
