@@ -867,9 +867,12 @@ def cpu_breadth(args):
         nnz = ctx.nnz
         gi = 60
         ctx.jacobi_dev()
-        ctx.gmres_dev(d_r.data_ptr(), o.data_ptr(), hbgpu.KrylovConfig(max_iters=1))
+        # restart = the timed iterations: the default 200-vector basis alone would be
+        # 211 GB at config 4 (N = 47)
+        ctx.gmres_dev(d_r.data_ptr(), o.data_ptr(), hbgpu.KrylovConfig(restart=gi, max_iters=1))
         t0 = time.perf_counter()
-        it_g, _, _ = ctx.gmres_dev(d_r.data_ptr(), o.data_ptr(), hbgpu.KrylovConfig(max_iters=gi, tolerance=1e-30))
+        it_g, _, _ = ctx.gmres_dev(d_r.data_ptr(), o.data_ptr(),
+                                   hbgpu.KrylovConfig(restart=gi, max_iters=gi, tolerance=1e-30))
         torch.cuda.synchronize()
         g_gm = (time.perf_counter() - t0) / max(it_g, 1)
         out["gpu"] = {"residual_s": g_res, "tangent_s": g_tan,
@@ -904,7 +907,7 @@ def cpu_breadth(args):
         inv, _ = rctx.jacobi()
         ci = 20
         t0 = time.perf_counter()
-        gres = rctx.gmres(rctx.residual(st, nproc), inv, max_iters=ci, tol=1e-30, threads=nproc)
+        gres = rctx.gmres(rctx.residual(st, nproc), inv, restart=ci, max_iters=ci, tol=1e-30, threads=nproc)
         c_gm = (time.perf_counter() - t0 - c_res_n) / max(gres["iterations"], 1)
         sub_nnz = len(rctx.tangent(st)) // (8 * N)
         mvb = spmv_bytes(sub_nnz, sub_nn, N)

@@ -619,7 +619,10 @@ static int upload_all(hbgpu_ctx* c, const hbgpu_mesh_desc* d) {
     return HBGPU_OK;
 }
 
-static int rows_per_matvec_cta(int N) { return std::max(1, 256 / N); }
+#ifndef MV_CTA_THREADS
+#define MV_CTA_THREADS 256
+#endif
+static int rows_per_matvec_cta(int N) { return std::max(1, MV_CTA_THREADS / N); }
 
 // ---------------------------------------------------------------- operations
 

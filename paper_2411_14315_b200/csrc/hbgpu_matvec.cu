@@ -36,8 +36,14 @@ __device__ __forceinline__ double2 ldcs2(const double2* p) { return __ldcs(p); }
 // velocity series through shared memory for the dense H product.
 // N1: N == 1 (steady / time-stepping case): a block's 8 slots are 64 contiguous
 // bytes and y's 4 components 32 — loaded as 16-byte vectors (H is 0, no C part).
+#ifndef MV_CTA_THREADS
+#define MV_CTA_THREADS 256
+#endif
+#ifndef MV_UNROLL4
+#define MV_UNROLL4 0
+#endif
 template <bool SCALED, bool WITH_C, bool N1>
-__global__ void __launch_bounds__(256) lmatvec_kernel(MatvecArgs a) {
+__global__ void __launch_bounds__(MV_CTA_THREADS) lmatvec_kernel(MatvecArgs a) {
     if (a.skip && *a.skip)
         return;
     extern __shared__ double sh[];
@@ -109,6 +115,16 @@ __global__ void __launch_bounds__(256) lmatvec_kernel(MatvecArgs a) {
         // (loading the next blocks' column indices one iteration ahead measured
         // 25% slower on every mesh: more registers, fewer loads in flight)
         {
+#if MV_UNROLL4
+            for (; k + 3 < ke; k += 4) {
+                const int B0 = __ldg(a.col_idx + k), B1 = __ldg(a.col_idx + k + 1);
+                const int B2 = __ldg(a.col_idx + k + 2), B3 = __ldg(a.col_idx + k + 3);
+                block(k, B0);
+                block(k + 1, B1);
+                block(k + 2, B2);
+                block(k + 3, B3);
+            }
+#endif
             for (; k + 1 < ke; k += 2) {
                 block(k, __ldg(a.col_idx + k));
                 block(k + 1, __ldg(a.col_idx + k + 1));
