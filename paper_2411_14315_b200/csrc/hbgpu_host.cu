@@ -69,7 +69,6 @@ struct Tooling {
     int res_tile = 0;           // HBGPU_RES_TILE: 1, 2 or 4 samples per residual tile (0 = auto)
     bool tangent_rows = false;  // HBGPU_TANGENT_KERNEL=rows: the tiled row-kernel fallback
     int tan_width = 0;          // HBGPU_TAN_WIDTH: force the tangent pipeline's CTA width
-    int tan_nsub = 0;           // HBGPU_TAN_NSUB: force the sample sub-tiles per tangent row
     bool gmres_host = false;    // HBGPU_GMRES_HOST: host-driven GMRES step loop
     int mv_lanes = 0;           // HBGPU_MV_LANES: 1 / 4 lanes per (row, sample) (0 = auto)
     static Tooling from_env() {
@@ -79,7 +78,6 @@ struct Tooling {
         const char* tk = std::getenv("HBGPU_TANGENT_KERNEL");
         t.tangent_rows = tk && std::strcmp(tk, "rows") == 0;
         t.tan_width = num("HBGPU_TAN_WIDTH");
-        t.tan_nsub = num("HBGPU_TAN_NSUB");
         t.gmres_host = std::getenv("HBGPU_GMRES_HOST") != nullptr;
         t.mv_lanes = num("HBGPU_MV_LANES");
         return t;
@@ -128,7 +126,7 @@ struct hbgpu_ctx {
         // persistent row pipeline (used when its shared memory fits)
         DBuf<unsigned char> pack;
         DBuf<int> pack_ptr;
-        int max_pack = 0, grid = 0, threads = 128, nsub = 1;
+        int max_pack = 0, grid = 0, threads = 128;
         bool pipe = false;
     } tb[6];
     DBuf<double> blkc;        // per block: n-invariant tangent sums (8)
@@ -619,8 +617,11 @@ static int upload_all(hbgpu_ctx* c, const hbgpu_mesh_desc* d) {
     return HBGPU_OK;
 }
 
+// L-matvec CTA: MV_CTA_THREADS / N rows of N (row, sample) threads.  512:
+// config 4 (N = 47) 8.29 -> 7.89 ms, config 1 (N = 19) 0.211 -> 0.196 ms
+// against 256; 128 and a 4-block unroll were slower (profiles/r2i_kb_mv.jsonl)
 #ifndef MV_CTA_THREADS
-#define MV_CTA_THREADS 256
+#define MV_CTA_THREADS 512
 #endif
 static int rows_per_matvec_cta(int N) { return std::max(1, MV_CTA_THREADS / N); }
 
@@ -745,7 +746,6 @@ static int tangent_dev(hbgpu_ctx* c, const double* d_state) {
             pa.pack_ptr = b.pack_ptr.p;
             pa.nrows = b.count;
             pa.max_pack = b.max_pack;
-            pa.nsub = b.nsub;
             launch_tangent_pipe(a, pa, b.threads, b.grid, b.smem, c->stream);
         } else {
             launch_tangent_row(a, b.count, b.smem, c->stream);
@@ -1416,47 +1416,33 @@ int hbgpu_set_basis(hbgpu_ctx* c, int modes, double period) {
         for (auto& b : c->tb) {
             if (!b.count)
                 continue;
-            auto ps = [&](int nt, int nsub = 1) {
-                return tangent_pipe_smem(b.max_pack, b.max_inc, b.max_blk, N, nt, nsub);
-            };
+            auto ps = [&](int nt) { return tangent_pipe_smem(b.max_pack, b.max_inc, b.max_blk, N, nt); };
             b.pipe = false;
-            b.nsub = 1;
             if (TAN_PIPE && !force_rows) {
-                // (width, sub-tiles) scored by thread-slot use of a unit's items
-                // and resident warps; more than one resident CTA per SM is
-                // preferred (a CTA's phase barriers then stall only part of the
-                // SM).  Sub-tiles only for the compile-time-N kernel.
-                const int max_sub = tangent_pipe_nc(N) && N >= 31 ? 3 : 1;
+                const double items = double(b.max_inc) * N;
                 double best = 0.0;
-                for (int nsub = 1; nsub <= max_sub; ++nsub)
-                    for (int w : widths) {
-                        const size_t sm = ps(N, nsub);
-                        if (sm > size_t(227 * 1024))
-                            continue;
-                        const int by_smem = int(size_t(228 * 1024) / (sm + 1024));
-                        const int by_regs = 65536 / (w * 128);
-                        const int ctas = std::min({32, by_smem, by_regs});
-                        if (ctas < 1)
-                            continue;
-                        const double items = double(b.max_inc) * ((N + nsub - 1) / nsub);
-                        const double rounds = std::ceil(items / w);
-                        const double score = items / (rounds * w) * std::min(1.0, ctas * (w / 32) / 12.0) *
-                                             (ctas >= 2 ? 1.0 : 0.85) / (1.0 + 0.04 * (nsub - 1));
-                        if (score > best * 1.0001) {
-                            best = score;
-                            b.pipe = true;
-                            b.threads = w;
-                            b.nt = N;
-                            b.nsub = nsub;
-                        }
+                for (int w : widths) {
+                    const size_t sm = ps(N);
+                    if (sm > size_t(227 * 1024))
+                        continue;
+                    const int by_smem = int(size_t(228 * 1024) / (sm + 1024));
+                    const int by_regs = 65536 / (w * 128);
+                    const int ctas = std::min({32, by_smem, by_regs});
+                    if (ctas < 1)
+                        continue;
+                    const double rounds = std::ceil(items / w);
+                    const double score = items / (rounds * w) * std::min(1.0, ctas * (w / 32) / 12.0);
+                    if (score > best * 1.0001) {
+                        best = score;
+                        b.pipe = true;
+                        b.threads = w;
+                        b.nt = N;
                     }
-                // tooling: HBGPU_TAN_NSUB / HBGPU_TAN_WIDTH force the sub-tiles / CTA width
-                if (b.pipe && c->tool.tan_nsub >= 1 && c->tool.tan_nsub <= 4 && tangent_pipe_nc(N) &&
-                    ps(N, c->tool.tan_nsub) <= size_t(227 * 1024))
-                    b.nsub = c->tool.tan_nsub;
+                }
+                // tooling: HBGPU_TAN_WIDTH forces the CTA width of every pipe bucket
                 if (c->tool.tan_width) {
                     const int w = c->tool.tan_width;
-                    if (b.pipe && std::find(widths, widths + 5, w) != widths + 5 && ps(N, b.nsub) <= size_t(227 * 1024))
+                    if (b.pipe && std::find(widths, widths + 5, w) != widths + 5 && ps(b.nt) <= size_t(227 * 1024))
                         b.threads = w;
                 }
                 if (!b.pipe) {
@@ -1471,7 +1457,7 @@ int hbgpu_set_basis(hbgpu_ctx* c, int modes, double period) {
                 }
             }
             if (b.pipe) {
-                b.smem = ps(b.nt, b.nsub);
+                b.smem = ps(b.nt);
                 const int w = int(std::find(widths, widths + 5, b.threads) - widths);
                 mxp[w] = std::max(mxp[w], b.smem);
                 continue;
@@ -1925,11 +1911,13 @@ int hbgpu_gmres_apply(hbgpu_ctx* c, hbgpu_apply_fn apply, void* user, long long 
     c->host_in.resize(size_t(n));
     c->host_out.resize(size_t(n));
     CK(c, cudaMemcpyAsync(c->inv.p, inv_diag, sizeof(double) * size_t(n), cudaMemcpyHostToDevice, c->stream));
-    CK(c, cudaMemcpyAsync(c->b.p, rhs, sizeof(double) * size_t(n), cudaMemcpyHostToDevice, c->stream));
+    // rhs in its own buffer: gmres_dev overwrites c->b with the scaled rhs and
+    // reads the unscaled one again for the true residual of every cycle
+    CK(c, cudaMemcpyAsync(c->y.p, rhs, sizeof(double) * size_t(n), cudaMemcpyHostToDevice, c->stream));
     c->host_op = apply;
     c->host_op_user = user;
     c->host_n = long(n);
-    const int st = gmres_dev(c, c->b.p, c->inv.p, cfg, c->x.p, result, history, hcap);
+    const int st = gmres_dev(c, c->y.p, c->inv.p, cfg, c->x.p, result, history, hcap);
     c->host_op = nullptr;
     c->host_op_user = nullptr;
     c->inv_valid = false;  // the context's Jacobi vector was overwritten

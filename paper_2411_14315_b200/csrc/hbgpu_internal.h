@@ -193,7 +193,6 @@ struct PipeArgs {
     const unsigned char* pack;  // row packs, 16-byte aligned
     const int* pack_ptr;        // nrows + 1, in 16-byte units
     int nrows;
-    int nsub = 1;               // sample sub-tiles per row (compile-time-N kernel)
     int max_pack;               // bytes
 };
 
@@ -270,8 +269,7 @@ void tangent_pack_write(unsigned char* dst, int A, int k0, int ninc, int nblk, i
                         const uint8_t* order);
 void launch_tangent_pack_refresh(unsigned char* pack, const int* pack_ptr, int nrows,
                                  const uint8_t* dir, const double* blkc, cudaStream_t st);
-size_t tangent_pipe_smem(int max_pack, int max_inc, int max_blk, int N, int NT, int nsub = 1);
-bool tangent_pipe_nc(int N);
+size_t tangent_pipe_smem(int max_pack, int max_inc, int max_blk, int N, int NT);
 cudaError_t configure_tangent_pipe_smem(int threads, size_t bytes);
 cudaError_t tangent_pipe_occupancy(int threads, int* blocks_per_sm, size_t smem);
 void launch_tangent_pipe(const TangentArgs& a, const PipeArgs& p, int threads, int grid_x, size_t smem,

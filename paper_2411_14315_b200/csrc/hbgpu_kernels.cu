@@ -161,10 +161,79 @@ __global__ void __launch_bounds__(kHThreads) apply_h_tile_kernel(const double* _
     }
 }
 
+// The same product on the FP64 tensor cores (mma.sync.m8n8k4.f64, SASS DMMA):
+// a warp owns 8-series x 8-sample output tiles and walks m in steps of 4
+// (two shared loads per 256-FMA instruction); N is zero-padded to a multiple
+// of 8.  A CTA takes 32 nodes (96 series).  On B200 the DMMA and DFMA paths
+// share one FP64 throughput (tools/fp64_probe.cu: 37.2 / 37.1 TFLOP/s alone,
+// 35.3 together), so this only wins where the FFMA tile is bound by its
+// shared-memory operand traffic.
+constexpr int kHmNodes = 32, kHmSeries = 3 * kHmNodes, kHmThreads = 256;
+__device__ __forceinline__ void dmma_m8n8k4(double& c0, double& c1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                 : "+d"(c0), "+d"(c1)
+                 : "d"(a), "d"(b));
+}
+__global__ void __launch_bounds__(kHmThreads) apply_h_dmma_kernel(const double* __restrict__ H, int N,
+                                                                  const double* __restrict__ in, int is,
+                                                                  double* __restrict__ out, int os, int nnodes) {
+    extern __shared__ double sh[];
+    const int NP = (N + 7) & ~7, LS = NP + 4;  // padded sample count, smem row stride
+    double* Ht = sh;                           // [m][LS]: Ht[m][n] = H[n][m], zero-padded
+    double* Xs = sh + NP * LS;                 // [series][LS], zero-padded in m
+    for (int k = threadIdx.x; k < NP * NP; k += blockDim.x) {
+        const int m = k / NP, n = k - m * NP;
+        Ht[m * LS + n] = (m < N && n < N) ? H[n * N + m] : 0.0;
+    }
+    const long A0 = (long)blockIdx.x * kHmNodes;
+    const int nloc = (int)min((long)kHmNodes, (long)nnodes - A0);
+    for (int k = threadIdx.x; k < kHmSeries * NP; k += blockDim.x) {
+        const int sl = k / NP, m = k - sl * NP, ln = sl / 3, i = sl - 3 * ln;
+        Xs[sl * LS + m] = (ln < nloc && m < N) ? __ldg(in + (A0 + ln) * is + (long)i * N + m) : 0.0;
+    }
+    __syncthreads();
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int r = lane >> 2, q = lane & 3;
+    const int ntn = NP / 8, tiles = (kHmSeries / 8) * ntn;
+    for (int tile = warp; tile < tiles; tile += kHmThreads / 32) {
+        const int ts = tile / ntn, tn = tile - ts * ntn;
+        const double* xa = Xs + (ts * 8 + r) * LS + q;  // A[r][k] = X[s0 + r][k0 + q]
+        const double* hb = Ht + q * LS + tn * 8 + r;     // B[k][n] = Ht[k0 + q][n0 + r]
+        double c0 = 0.0, c1 = 0.0;
+        for (int k0 = 0; k0 < NP; k0 += 4)
+            dmma_m8n8k4(c0, c1, xa[k0], hb[k0 * LS]);
+        const int sl = ts * 8 + r, ln = sl / 3, i = sl - 3 * ln;
+        if (ln < nloc) {
+            double* o = out + (A0 + ln) * os + (long)i * N;
+            const int n = tn * 8 + 2 * q;
+            if (n < N)
+                o[n] = c0;
+            if (n + 1 < N)
+                o[n + 1] = c1;
+        }
+    }
+}
+
+#ifndef H_DMMA
+#define H_DMMA 0
+#endif
 void launch_apply_h_series(const double* H, int N, const double* in, int in_node_stride,
                            double* out, int out_node_stride, int nnodes, cudaStream_t st) {
     if (nnodes <= 0)
         return;
+    if (H_DMMA) {
+        const int NP = (N + 7) & ~7, LS = NP + 4;
+        const size_t smem = sizeof(double) * ((size_t)NP * LS + (size_t)kHmSeries * LS);
+        static bool cfg = false;
+        if (!cfg) {
+            cudaFuncSetAttribute(apply_h_dmma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+            cfg = true;
+        }
+        note_launch();
+        apply_h_dmma_kernel<<<(nnodes + kHmNodes - 1) / kHmNodes, kHmThreads, smem, st>>>(
+            H, N, in, in_node_stride, out, out_node_stride, nnodes);
+        return;
+    }
     const int spt = (N + 15) / 16;
     const int blocks = (nnodes + kHNodes - 1) / kHNodes;
     const size_t smem = sizeof(double) * ((size_t)N * 16 * spt + (size_t)kHSeries * (N + 1));

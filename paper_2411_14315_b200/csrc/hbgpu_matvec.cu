@@ -37,7 +37,7 @@ __device__ __forceinline__ double2 ldcs2(const double2* p) { return __ldcs(p); }
 // N1: N == 1 (steady / time-stepping case): a block's 8 slots are 64 contiguous
 // bytes and y's 4 components 32 — loaded as 16-byte vectors (H is 0, no C part).
 #ifndef MV_CTA_THREADS
-#define MV_CTA_THREADS 256
+#define MV_CTA_THREADS 512
 #endif
 #ifndef MV_UNROLL4
 #define MV_UNROLL4 0

@@ -172,13 +172,10 @@ __host__ __device__ inline PipeSmem pipe_layout(int max_pack, int mi, int max_bl
 }
 
 static bool pipe_nc_listed(int N);
-size_t tangent_pipe_smem(int max_pack, int max_inc, int max_blk, int N, int NT, int nsub) {
-    // the compile-time-N kernel (whole series per CTA, nsub sub-tiles) may use
-    // sample pairs; the generic kernel takes tiles of NT samples
-    const bool nc = NT == N && pipe_nc_listed(N);
-    const int P = nc ? tan_pair(N) : 1;
-    const int NTu = nc ? (N + nsub - 1) / nsub : NT;
-    return (size_t)pipe_layout(max_pack, max_inc, max_blk, N, NTu, P).total;
+size_t tangent_pipe_smem(int max_pack, int max_inc, int max_blk, int N, int NT) {
+    // the compile-time-N kernel (whole series per CTA) may use sample pairs
+    const int P = (NT == N && pipe_nc_listed(N)) ? tan_pair(N) : 1;
+    return (size_t)pipe_layout(max_pack, max_inc, max_blk, N, NT, P).total;
 }
 
 // THREADS per CTA (32 ... 512) is chosen per valence bucket from the row's
@@ -190,14 +187,10 @@ template <int TAU, int THREADS, int NC>
 __global__ void __launch_bounds__(THREADS, 512 / THREADS) tangent_pipe_kernel(TangentArgs a, PipeArgs pa) {
     constexpr int P = tan_pair(NC);
     extern __shared__ __align__(128) unsigned char smraw[];
-    const int N = NC ? NC : a.N;
-    // a row's samples are processed in nsub consecutive sub-tiles of NT samples
-    // (compile-time-N kernel: the whole series is gathered once per row, the
-    // summaries and diagonal parts only hold one sub-tile, so 2 CTAs fit an SM
-    // at N = 47); the generic kernel takes one tile per blockIdx.y instead
-    const int nsub = NC ? pa.nsub : 1;
-    const int NT = NC ? (N + nsub - 1) / nsub : a.NT;
+    const int N = NC ? NC : a.N, NT = NC ? NC : a.NT;
+    const int n0 = NC ? 0 : blockIdx.y * NT, nt = NC ? NC : min(NT, N - n0);
     const int NTp = tan_ntp(NT, P);
+    const int nq = (nt + P - 1) / P;  // sample groups of this tile
     const PipeSmem Ls = pipe_layout(pa.max_pack, a.max_inc, a.max_blk, N, NT, P);
     // summaries, component-major [c][i][t]: the stores of one phase-1 pass are contiguous
     const int SI = NTp + TAN_SUMM_PAD, SC = a.max_inc * SI;
@@ -251,17 +244,20 @@ __global__ void __launch_bounds__(THREADS, 512 / THREADS) tangent_pipe_kernel(Ta
         issue_gather(0);
     }
 
-    // Diagonal block of the previous unit (row, sub-tile): sum its parts in
-    // order, identity K on Dirichlet rows (assembly.cpp:659-665).  Deferred into
-    // the next unit's first region so a unit costs two barriers, not three.
+    // work items (x, q): x = incidence (phase 1) or slot (phase 2), q = sample group
+    const int dx = blockDim.x / nq, dq = blockDim.x - dx * nq;
+    const int x_start = threadIdx.x / nq, q_start = threadIdx.x - x_start * nq;
+    // Diagonal block of the previous row: sum its parts in order, identity K on
+    // Dirichlet rows (assembly.cpp:659-665).  Deferred into the next row's first
+    // region so a row costs two barriers, not three.
     long pd_blk = -1;
-    int pd_parts = 0, pd_n0 = 0, pd_nt = 0;
+    int pd_parts = 0;
     bool pd_fix = false;
     auto diag_sum = [&]() {
         if (pd_blk < 0)
             return;
-        for (int it = threadIdx.x; it < 8 * pd_nt; it += blockDim.x) {
-            const int sl = it / pd_nt, t = it - sl * pd_nt, n = pd_n0 + t;
+        for (int it = threadIdx.x; it < 8 * nt; it += blockDim.x) {
+            const int sl = it / nt, t = it - sl * nt, n = n0 + t;
             double v = 0.0;
             for (int p = 0; p < pd_parts; ++p)
                 v += dpart[((size_t)p * 8 + sl) * NTp + t];
@@ -272,9 +268,9 @@ __global__ void __launch_bounds__(THREADS, 512 / THREADS) tangent_pipe_kernel(Ta
     };
     int k = 0;
     for (int r = r0; r < nrows; r += rs, ++k) {
-        // Pipeline: the pack of row k+1 is fetched during the first phase 1 of
-        // row k, its gathers (into the single gather buffer, dead once the last
-        // phase 1 has read it) during the last phase 2 and the diagonal pass.
+        // Pipeline: the pack of row k+1 is fetched during phase 1 of row k, its
+        // gathers (into the single gather buffer, dead once phase 1 has read
+        // it) during phase 2 and the diagonal pass of row k.
         const int ms = k & 1;
         const bool more = r + rs < nrows;
         if (warp == 0 && lane == 0 && more)
@@ -294,15 +290,8 @@ __global__ void __launch_bounds__(THREADS, 512 / THREADS) tangent_pipe_kernel(Ta
         const double* su = reinterpret_cast<const double*>(smraw + Ls.su);
         const double* tg = reinterpret_cast<const double*>(smraw + Ls.tg);
 
-      for (int sub = 0; sub < nsub; ++sub) {
-        const int n0 = NC ? sub * NT : blockIdx.y * NT, nt = min(NT, N - n0);
-        const int nq = (nt + P - 1) / P;  // sample groups of this unit
-        // work items (x, q): x = incidence (phase 1) or slot (phase 2), q = sample group
-        const int dx = blockDim.x / nq, dq = blockDim.x - dx * nq;
-        const int x_start = threadIdx.x / nq, q_start = threadIdx.x - x_start * nq;
-        // ---- diagonal block of the previous unit (its parts are in dpart)
+        // ---- diagonal block of the previous row (its parts are in dpart)
         diag_sum();
-      if (sub == 0) {
         // ---- contribution records {dN_a (3), gg, dN_b (3), summary offset}
         for (int p = threadIdx.x; p < 4 * ninc; p += blockDim.x) {
             const int ent = cont[p];
@@ -317,7 +306,6 @@ __global__ void __launch_bounds__(THREADS, 512 / THREADS) tangent_pipe_kernel(Ta
             o[2] = make_double2(gb0, gb1);
             o[3] = make_double2(gb2, __longlong_as_double((long long)i * SI));
         }
-      }
         // ---- phase 1: per (incidence, sample group) summaries
         bool bad_acc = false;
         auto p1item = [&](int i, int t) {
@@ -431,7 +419,7 @@ __global__ void __launch_bounds__(THREADS, 512 / THREADS) tangent_pipe_kernel(Ta
             atomicOr(a.flag, 1);
         __syncthreads();
 
-        if (warp == 0 && more && sub == nsub - 1) {
+        if (warp == 0 && more) {
             mbar_wait(mbar + (ms ^ 1), ((k + 1) >> 1) & 1);
             issue_gather(ms ^ 1);
         }
@@ -543,9 +531,6 @@ __global__ void __launch_bounds__(THREADS, 512 / THREADS) tangent_pipe_kernel(Ta
         pd_blk = k0 + kdiag;
         pd_parts = dparts;
         pd_fix = afix;
-        pd_n0 = n0;
-        pd_nt = nt;
-      }
     }
     diag_sum();
 }
@@ -558,7 +543,6 @@ static bool pipe_nc_listed(int N) {
 #undef HBGPU_NC_IS
     return false;
 }
-bool tangent_pipe_nc(int N) { return pipe_nc_listed(N); }
 
 template <int T, int NC>
 static cudaError_t configure_pipe_tn(int b) {

@@ -173,25 +173,6 @@ def test_residual_tile_widths(gpu, monkeypatch, tile, modes):
     assert rel(ctx.assemble_residual(s), orc.residual(s)) < TOL
 
 
-@pytest.mark.parametrize("nsub", ["1", "2", "3"])
-@pytest.mark.parametrize("modes", [16, 24])
-def test_tangent_sample_subtiles(gpu, monkeypatch, modes, nsub):
-    """The tangent pipeline with a row's samples in 1, 2 or 3 sub-tiles
-    (HBGPU_TAN_NSUB, read at context creation) on a Delaunay cube at N = 31
-    and 47, including Dirichlet rows, against the restatement."""
-    from paper_2411_14315_b200 import meshgen
-
-    monkeypatch.setenv("HBGPU_TAN_NSUB", nsub)
-    mesh = meshgen.cube_delaunay(3000, seed=17)
-    N = 2 * modes - 1
-    neu = [(k, np.full(N, 5.0)) for k, p in enumerate(mesh.patches) if p.kind == NEUMANN]
-    prob = Problem(mesh, modes, 1.0, 1.06, 0.04, np.zeros(mesh.num_nodes * 3 * N), neu, 0.2)
-    ctx = gpu_ctx(prob, 0, 0.05)
-    orc = ob.Restated(prob, tau_mode=0, pseudo_dt=0.05)
-    s = cases.random_modes_state(mesh.num_nodes, modes, 23)
-    assert rel(ctx.assemble_tangent(s), orc.tangent(s)) < TOL
-
-
 @pytest.mark.parametrize("width", ["64", "256"])
 def test_tangent_pipe_widths(gpu, monkeypatch, width):
     """The persistent tangent pipeline at forced CTA widths (HBGPU_TAN_WIDTH)."""
