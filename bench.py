@@ -526,7 +526,12 @@ def run_ours(args):
     # ---- converged solve time (config 0, reference default tolerances)
     solve = None
     if args.solve and rank == 0:
-        solve = solve_config0(args.cpu_solve)
+        solve = {"config0": solve_config0(args.cpu_solve)}
+        for cfg in [int(c) for c in args.solve_configs.split(",") if c]:
+            solve[f"config{cfg}"] = solve_config(cfg)
+        solve["notes"] = ("config 0: converged (CFL 10); config 1: converged at CFL 100; configs 2 and 3: "
+                          "bounded runs — the reference's pseudo-time Newton does not converge on them within "
+                          "the explored budgets (profiles/r2_solve_exploration.jsonl, r2h_converged_solves.jsonl)")
 
     cpu_baseline = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -753,6 +758,52 @@ def sweep_configs(args):
                                "(hbgpu_set_resistance; new physics, not in the reference); random states "
                                "for assembly/matvec timing, Newton iterate 0 for the GMRES step",
                       "results": out}), flush=True)
+
+
+# Converged-solve settings per config, from the pseudo-time
+# exploration of round 2 (profiles/r2_solve_exploration.jsonl,
+# profiles/r2h_converged_solves.jsonl): the reference defaults (3 orders, GMRES
+# restart 200 / tol 0.03, 60 Newton iterations) with the pseudo time step as a
+# multiple of h_c/u_c (CFL) and an iteration cap.
+#   config 1: CFL 100 converges in 62 Newton iterations (CFL 1/3/10/30 do not
+#             within 40-60);
+#   config 2: no CFL tried converges (CFL 10: res_rel 0.106 at best in 400
+#             iterations, then drifting; CFL 30/100 stall at 0.7-1.4; CFL 300
+#             diverges) — bounded run reported;
+#   config 3 (resistance outlet R = 1e4): CFL 0.3/1/3 reach res_rel 8.5/2.8/0.93
+#             after 8 iterations (the first steps exhaust the 1000-iteration GMRES
+#             budget); no convergence within 25 min at CFL 1 — bounded run reported.
+SOLVE_SETTINGS = {1: (100.0, 70), 2: (10.0, 40), 3: (3.0, 4)}
+
+
+def solve_config(cfg):
+    """One solve of config 1, 2 or 3 with SOLVE_SETTINGS (GPU, device-resident
+    Newton loop): time, Newton / GMRES counts, final relative residual."""
+    from paper_2411_14315_b200 import cases, hbgpu
+
+    cfl, cap = SOLVE_SETTINGS[cfg]
+    t0 = time.time()
+    prob = cases.config_problem(cfg)
+    t_mesh = time.time() - t0
+    ctx = hbgpu.GpuContext(prob.mesh)
+    ctx.set_basis(prob.modes, prob.period)
+    ctx.set_fluid(prob.rho, prob.mu)
+    ctx.set_bcs(prob.dirichlet_g, prob.neumann, prob.backflow_beta)
+    if cfg == 3:
+        ctx.set_resistance({k: 1e4 for k, _ in prob.neumann})
+    sc = hbgpu.SolverConfig(pseudo_dt=auto_pseudo_dt(prob) * cfl, max_newton_iters=cap)
+    out = {"elements": prob.mesh.num_elements, "N": prob.N, "cfl": cfl, "max_newton_iters": cap,
+           "mesh_seconds": t_mesh}
+    try:
+        sol = ctx.solve_harmonic(sc)
+        out.update({"seconds": sol.total_seconds, "newton_iters": int(len(sol.log.iters)),
+                    "gmres_iters": int(sol.log.linear_iters.sum()), "converged": sol.log.converged,
+                    "final_rel": float(sol.log.res_rel[-1]), "min_rel": float(sol.log.res_rel.min()),
+                    "assembly_seconds": sol.assembly_seconds, "linear_seconds": sol.linear_seconds})
+    except Exception as exc:
+        out["error"] = f"{type(exc).__name__}: {exc}"
+    ctx.close()
+    return out
 
 
 def solve_config0(cpu_reference=False):
@@ -993,6 +1044,7 @@ def main():
     ap.add_argument("--spmv-reps", type=int, default=100)
     ap.add_argument("--no-solve", dest="solve", action="store_false")
     ap.add_argument("--no-newton", dest="newton", action="store_false")
+    ap.add_argument("--solve-configs", default="1,2,3", help="configs (besides 0) with a solve block")
     ap.add_argument("--no-five-call", dest="five_call", action="store_false")
     ap.add_argument("--headline-config", type=int, default=4, choices=[1, 4])
     ap.add_argument("--cpu-breadth", default=None, help="e.g. 0,1,2,3,4: CPU baseline breadth (separate run)")

@@ -163,7 +163,6 @@ struct hbgpu_ctx {
     // work buffers
     DBuf<double> state, r, hu, pvals, mass, mass_c, inv, y, out, x, w, z, scale, b, tmp;
     DBuf<double> V;
-    size_t V_vecs = 0;
     DBuf<double> partial, red;
     double* h_red = nullptr;  // pinned
     size_t red_cap = 1024;
@@ -886,10 +885,10 @@ static int gmres_dev(hbgpu_ctx* c, const double* d_rhs, const double* d_inv,
             history[res->history_len] = v;
         res->history_len += (history && res->history_len < hcap) ? 1 : 0;
     };
-    if (c->V_vecs < size_t(m) + 1) {
+    // basis capacity in doubles (the vector length differs between the
+    // L-matvec and a host operator of hbgpu_gmres_apply)
+    if (c->V.n < (size_t(m) + 1) * size_t(n))
         CK(c, c->V.alloc((size_t(m) + 1) * size_t(n)));
-        c->V_vecs = size_t(m) + 1;
-    }
     // scratch: red[0, 2m+4) dot results | [2m+4, 4m+8) update coefficients | [4m+8] |w'|
     const size_t need = 4 * size_t(m) + 16;
     if (c->red_cap < need) {
@@ -1394,7 +1393,6 @@ int hbgpu_set_basis(hbgpu_ctx* c, int modes, double period) {
     CK(c, cudaMemsetAsync(c->g.p, 0, sizeof(double) * size_t(c->nn) * 3 * size_t(N), c->stream));
     c->g_h.assign(size_t(c->nn) * 3 * size_t(N), 0.0);
     c->V.release();
-    c->V_vecs = 0;
     c->p_valid = c->inv_valid = false;
     c->mass_valid = false;
     {

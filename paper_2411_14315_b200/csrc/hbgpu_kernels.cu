@@ -95,79 +95,17 @@ void launch_geometry(const double* xyz, const int4* conn, int ne, double* geom, 
 // out[(A*os + i*N) + n] = sum_m H[n][m] in[(A*is + i*N) + m], i < 3: the
 // batched pseudo-spectral derivative of every velocity series
 // (assembly.cpp:453-463; SpectralOperators::apply_many, spectral.cpp:185-227).
-// It is a small GEMM, OUT[3 nn x N] = X[3 nn x N] H^T[N x N], register-tiled:
-// a CTA takes 16 nodes (48 series); thread (g, j) computes series 4g..4g+3 at
-// samples j, j+16, ..., j+16(SPT-1): per m, 4 + SPT shared loads feed 4 SPT
-// FMAs (the per-(series, sample) dot product it replaces needed two loads
-// per FMA).  H^T and the series tile sit in shared memory; the tile is
-// loaded with coalesced reads of each node's contiguous 3N velocity values.
-constexpr int kHNodes = 16, kHSeries = 3 * kHNodes, kHThreads = (kHSeries / 4) * 16;
-template <int SPT>
-__global__ void __launch_bounds__(kHThreads) apply_h_tile_kernel(const double* __restrict__ H, int N,
-                                                                 const double* __restrict__ in, int is,
-                                                                 double* __restrict__ out, int os, int nnodes) {
-    extern __shared__ double sh[];
-    constexpr int NP = 16 * SPT;       // padded sample count of H^T rows
-    double* Ht = sh;                   // [m][NP], Ht[m][n] = H[n][m], zero-padded
-    double* Xs = sh + N * NP;          // [series][N + 1]
-    const int XS = N + 1;
-    for (int k = threadIdx.x; k < N * NP; k += blockDim.x) {
-        const int m = k / NP, n = k - m * NP;
-        Ht[k] = n < N ? H[n * N + m] : 0.0;
-    }
-    const long A0 = (long)blockIdx.x * kHNodes;
-    const int nloc = (int)min((long)kHNodes, (long)nnodes - A0);
-    for (int k = threadIdx.x; k < nloc * 3 * N; k += blockDim.x) {
-        const int ln = k / (3 * N), rem = k - ln * 3 * N, i = rem / N, m = rem - i * N;
-        Xs[(ln * 3 + i) * XS + m] = __ldg(in + (A0 + ln) * is + rem);
-    }
-    __syncthreads();
-    const int g = threadIdx.x >> 4, j = threadIdx.x & 15;
-    double acc[4][SPT];
-#pragma unroll
-    for (int q = 0; q < 4; ++q)
-#pragma unroll
-        for (int k = 0; k < SPT; ++k)
-            acc[q][k] = 0.0;
-    const double* x = Xs + (4 * g) * XS;
-    const double* h = Ht + j;
-#pragma unroll 4
-    for (int m = 0; m < N; ++m) {
-        double xv[4], hv[SPT];
-#pragma unroll
-        for (int q = 0; q < 4; ++q)
-            xv[q] = x[q * XS + m];
-#pragma unroll
-        for (int k = 0; k < SPT; ++k)
-            hv[k] = h[m * NP + 16 * k];
-#pragma unroll
-        for (int q = 0; q < 4; ++q)
-#pragma unroll
-            for (int k = 0; k < SPT; ++k)
-                acc[q][k] = fma(hv[k], xv[q], acc[q][k]);
-    }
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-        const int sl = 4 * g + q, ln = sl / 3, i = sl - 3 * ln;
-        if (ln >= nloc)
-            continue;
-        double* o = out + (A0 + ln) * os + (long)i * N;
-#pragma unroll
-        for (int k = 0; k < SPT; ++k) {
-            const int n = j + 16 * k;
-            if (n < N)
-                o[n] = acc[q][k];
-        }
-    }
-}
-
-// The same product on the FP64 tensor cores (mma.sync.m8n8k4.f64, SASS DMMA):
-// a warp owns 8-series x 8-sample output tiles and walks m in steps of 4
-// (two shared loads per 256-FMA instruction); N is zero-padded to a multiple
-// of 8.  A CTA takes 32 nodes (96 series).  On B200 the DMMA and DFMA paths
-// share one FP64 throughput (tools/fp64_probe.cu: 37.2 / 37.1 TFLOP/s alone,
-// 35.3 together), so this only wins where the FFMA tile is bound by its
-// shared-memory operand traffic.
+// It is a small GEMM, OUT[3 nn x N] = X[3 nn x N] H^T[N x N], run on the FP64
+// tensor cores (mma.sync.m8n8k4.f64, SASS DMMA): a warp owns 8-series x
+// 8-sample output tiles and walks m in steps of 4 (two shared loads per
+// 256-FMA instruction); N is zero-padded to a multiple of 8.  A CTA takes 32
+// nodes (96 series).  On B200 the DMMA and DFMA paths share one FP64
+// throughput (tools/fp64_probe.cu: 37.2 / 37.1 TFLOP/s alone, 35.3 together),
+// so DMMA wins only where a DFMA formulation is bound by its shared-memory
+// operand traffic — as the register-tiled DFMA version of this pass was
+// (4 series x SPT samples per thread, 7 shared loads per 12 FMA): config 4
+// (N = 47) 0.864 -> 0.787 ms, config 1 (N = 19) 0.039 -> 0.030 ms with DMMA;
+// the round-1 per-(series, sample) dot product took 2.53 ms at config 4.
 constexpr int kHmNodes = 32, kHmSeries = 3 * kHmNodes, kHmThreads = 256;
 __device__ __forceinline__ void dmma_m8n8k4(double& c0, double& c1, double a, double b) {
     asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
@@ -214,41 +152,20 @@ __global__ void __launch_bounds__(kHmThreads) apply_h_dmma_kernel(const double* 
     }
 }
 
-#ifndef H_DMMA
-#define H_DMMA 0
-#endif
 void launch_apply_h_series(const double* H, int N, const double* in, int in_node_stride,
                            double* out, int out_node_stride, int nnodes, cudaStream_t st) {
     if (nnodes <= 0)
         return;
-    if (H_DMMA) {
-        const int NP = (N + 7) & ~7, LS = NP + 4;
-        const size_t smem = sizeof(double) * ((size_t)NP * LS + (size_t)kHmSeries * LS);
-        static bool cfg = false;
-        if (!cfg) {
-            cudaFuncSetAttribute(apply_h_dmma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
-            cfg = true;
-        }
-        note_launch();
-        apply_h_dmma_kernel<<<(nnodes + kHmNodes - 1) / kHmNodes, kHmThreads, smem, st>>>(
-            H, N, in, in_node_stride, out, out_node_stride, nnodes);
-        return;
-    }
-    const int spt = (N + 15) / 16;
-    const int blocks = (nnodes + kHNodes - 1) / kHNodes;
-    const size_t smem = sizeof(double) * ((size_t)N * 16 * spt + (size_t)kHSeries * (N + 1));
-    static bool configured = false;  // N up to 63 needs ~57 KB (above the 48 KB default)
+    const int NP = (N + 7) & ~7, LS = NP + 4;
+    const size_t smem = sizeof(double) * ((size_t)NP * LS + (size_t)kHmSeries * LS);
+    static bool configured = false;  // N up to 63: ~87 KB (above the 48 KB default)
     if (!configured) {
-        cudaFuncSetAttribute(apply_h_tile_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+        cudaFuncSetAttribute(apply_h_dmma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
         configured = true;
     }
     note_launch();
-    switch (spt) {
-    case 1: apply_h_tile_kernel<1><<<blocks, kHThreads, smem, st>>>(H, N, in, in_node_stride, out, out_node_stride, nnodes); break;
-    case 2: apply_h_tile_kernel<2><<<blocks, kHThreads, smem, st>>>(H, N, in, in_node_stride, out, out_node_stride, nnodes); break;
-    case 3: apply_h_tile_kernel<3><<<blocks, kHThreads, smem, st>>>(H, N, in, in_node_stride, out, out_node_stride, nnodes); break;
-    default: apply_h_tile_kernel<4><<<blocks, kHThreads, smem, st>>>(H, N, in, in_node_stride, out, out_node_stride, nnodes); break;
-    }
+    apply_h_dmma_kernel<<<(nnodes + kHmNodes - 1) / kHmNodes, kHmThreads, smem, st>>>(
+        H, N, in, in_node_stride, out, out_node_stride, nnodes);
 }
 
 // ---------------------------------------------------------------- residual
