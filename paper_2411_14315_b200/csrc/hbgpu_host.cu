@@ -68,7 +68,6 @@ struct HostPatch {
 struct Tooling {
     int res_tile = 0;           // HBGPU_RES_TILE: 1, 2 or 4 samples per residual tile (0 = auto)
     bool tangent_rows = false;  // HBGPU_TANGENT_KERNEL=rows: the tiled row-kernel fallback
-    bool tangent_pipe = false;  // HBGPU_TANGENT_KERNEL=pipe: the CTA-phase pipeline, not warp-split rows
     int tan_width = 0;          // HBGPU_TAN_WIDTH: force the tangent pipeline's CTA width
     bool gmres_host = false;    // HBGPU_GMRES_HOST: host-driven GMRES step loop
     int mv_lanes = 0;           // HBGPU_MV_LANES: 1 / 4 lanes per (row, sample) (0 = auto)
@@ -78,7 +77,6 @@ struct Tooling {
         t.res_tile = num("HBGPU_RES_TILE");
         const char* tk = std::getenv("HBGPU_TANGENT_KERNEL");
         t.tangent_rows = tk && std::strcmp(tk, "rows") == 0;
-        t.tangent_pipe = tk && std::strcmp(tk, "pipe") == 0;
         t.tan_width = num("HBGPU_TAN_WIDTH");
         t.gmres_host = std::getenv("HBGPU_GMRES_HOST") != nullptr;
         t.mv_lanes = num("HBGPU_MV_LANES");
@@ -130,12 +128,6 @@ struct hbgpu_ctx {
         DBuf<int> pack_ptr;
         int max_pack = 0, grid = 0, threads = 128;
         bool pipe = false;
-        // warp-split rows (hbgpu_tangent_ws.cu): contribution records per row
-        DBuf<long> rec_ptr;
-        DBuf<double> recs;
-        bool ws = false;
-        int ws_threads = 512, ws_grid = 0;
-        size_t ws_smem = 0;
     } tb[6];
     DBuf<double> blkc;        // per block: n-invariant tangent sums (8)
     DBuf<uint8_t> blk_order;  // per row: off-diagonal blocks by descending contribution count
@@ -522,14 +514,6 @@ static int upload_all(hbgpu_ctx* c, const hbgpu_mesh_desc* d) {
                                    c->col_idx_h.data() + k0, incl.data(),
                                    contrib.data() + cptr[size_t(k0)], rcptr.data(), order.data() + k0);
             }
-            // contribution records of the warp-split kernel: 4 x ninc per row
-            std::vector<long> rptr{0};
-            for (int A : brows[bk])
-                rptr.push_back(rptr.back() + 4L * (iptr[size_t(A) + 1] - iptr[size_t(A)]));
-            CK(c, c->tb[bk].rec_ptr.alloc(rptr.size()));
-            CK(c, cudaMemcpyAsync(c->tb[bk].rec_ptr.p, rptr.data(), sizeof(long) * rptr.size(),
-                                  cudaMemcpyHostToDevice, st));
-            CK(c, c->tb[bk].recs.alloc(size_t(rptr.back()) * 8));
             CK(c, c->tb[bk].pack.alloc(pk.size()));
             CK(c, c->tb[bk].pack_ptr.alloc(pptr.size()));
             CK(c, cudaMemcpyAsync(c->tb[bk].pack.p, pk.data(), pk.size(), cudaMemcpyHostToDevice, st));
@@ -547,10 +531,8 @@ static int upload_all(hbgpu_ctx* c, const hbgpu_mesh_desc* d) {
         CK(c, c->blkc.alloc(size_t(c->nnz) * 8));
         launch_tangent_blockconst(c->tgeom.p, c->row_ptr.p, c->inc_ptr.p, c->inc_rec.p,
                                   c->contrib_ptr.p, c->contrib.p, nn, c->blkc.p, st);
-        for (auto& b : c->tb) {
+        for (auto& b : c->tb)
             launch_tangent_pack_refresh(b.pack.p, b.pack_ptr.p, b.count, c->dir.p, c->blkc.p, st);
-            launch_tangent_recs(b.pack.p, b.pack_ptr.p, b.count, c->tgeom.p, b.rec_ptr.p, b.recs.p, st);
-        }
         TRY(check_launch(c));
         CK(c, cudaStreamSynchronize(st));
     }
@@ -763,10 +745,7 @@ static int tangent_dev(hbgpu_ctx* c, const double* d_state) {
             pa.pack_ptr = b.pack_ptr.p;
             pa.nrows = b.count;
             pa.max_pack = b.max_pack;
-            if (b.ws)
-                launch_tangent_ws(a, pa, b.recs.p, b.rec_ptr.p, b.ws_threads, b.ws_grid, b.ws_smem, c->stream);
-            else
-                launch_tangent_pipe(a, pa, b.threads, b.grid, b.smem, c->stream);
+            launch_tangent_pipe(a, pa, b.threads, b.grid, b.smem, c->stream);
         } else {
             launch_tangent_row(a, b.count, b.smem, c->stream);
         }
@@ -1327,8 +1306,6 @@ void hbgpu_destroy(hbgpu_ctx* c) {
         b.desc.release();
         b.pack.release();
         b.pack_ptr.release();
-        b.rec_ptr.release();
-        b.recs.release();
     }
     c->blkc.release();
     c->blk_order.release();
@@ -1507,41 +1484,6 @@ int hbgpu_set_basis(hbgpu_ctx* c, int modes, double period) {
                 return fail(c, HBGPU_ERR_INVALID, "tangent pipeline does not fit on an SM");
             const int tiles = (N + b.nt - 1) / b.nt;
             b.grid = std::max(1, std::min(b.count, (nsm * per_sm + tiles - 1) / tiles));
-        }
-        // warp-split rows for the compile-time-N buckets whose whole series
-        // fits: every warp owns ~3 time samples of the CTA's row (N / 3 warps,
-        // rounded to a power of two, 2..16)
-        size_t wsx[4] = {0, 0, 0, 0};
-        const int wsw[4] = {64, 128, 256, 512};
-        for (auto& b : c->tb) {
-            b.ws = false;
-            if (!b.count || !b.pipe || b.nt != N || !tangent_ws_supported(N) || c->tool.tangent_pipe ||
-                force_rows)
-                continue;
-            int W = 2;
-            while (W < 16 && double(W) * 1.5 < double(N) / 3.0)
-                W *= 2;
-            b.ws_threads = 32 * W;
-            b.ws_smem = tangent_ws_smem(b.max_pack, b.max_inc, b.max_blk, N);
-            if (b.ws_smem > size_t(227 * 1024))
-                continue;
-            b.ws = true;
-            const int wi = int(std::find(wsw, wsw + 4, b.ws_threads) - wsw);
-            wsx[wi] = std::max(wsx[wi], b.ws_smem);
-        }
-        for (int w = 0; w < 4; ++w)
-            if (wsx[w])
-                CK(c, configure_tangent_ws_smem(wsw[w], wsx[w]));
-        for (auto& b : c->tb) {
-            if (!b.ws)
-                continue;
-            int per_sm = 0;
-            CK(c, tangent_ws_occupancy(b.ws_threads, &per_sm, b.ws_smem));
-            if (per_sm < 1) {
-                b.ws = false;
-                continue;
-            }
-            b.ws_grid = std::max(1, std::min(b.count, nsm * per_sm));
         }
     }
     // clear previous Neumann data sized for another N

@@ -274,15 +274,6 @@ cudaError_t configure_tangent_pipe_smem(int threads, size_t bytes);
 cudaError_t tangent_pipe_occupancy(int threads, int* blocks_per_sm, size_t smem);
 void launch_tangent_pipe(const TangentArgs& a, const PipeArgs& p, int threads, int grid_x, size_t smem,
                          cudaStream_t st);
-// warp-split tangent rows (hbgpu_tangent_ws.cu)
-bool tangent_ws_supported(int N);
-size_t tangent_ws_smem(int max_pack, int max_inc, int max_blk, int N);
-cudaError_t configure_tangent_ws_smem(int threads, size_t bytes);
-cudaError_t tangent_ws_occupancy(int threads, int* blocks_per_sm, size_t smem);
-void launch_tangent_recs(const unsigned char* pack, const int* pack_ptr, int nrows, const double* tgeom,
-                         const long* rec_ptr, double* recs, cudaStream_t st);
-void launch_tangent_ws(const TangentArgs& a, const PipeArgs& p, const double* recs, const long* rec_ptr,
-                       int threads, int grid, size_t smem, cudaStream_t st);
 void launch_backflow_tangent(const BoundaryArgs& a, const int* row_ptr, const int* col_idx,
                              double* pvals, cudaStream_t st);
 void launch_lmatvec(const MatvecArgs& a, cudaStream_t st);

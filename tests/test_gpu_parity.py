@@ -173,34 +173,10 @@ def test_residual_tile_widths(gpu, monkeypatch, tile, modes):
     assert rel(ctx.assemble_residual(s), orc.residual(s)) < TOL
 
 
-@pytest.mark.parametrize("kernel", ["ws", "pipe"])
-@pytest.mark.parametrize("modes,tau", [(3, 0), (4, 1), (10, 0), (16, 0), (24, 0), (24, 1)])
-def test_tangent_warp_split_and_pipe(gpu, monkeypatch, kernel, modes, tau):
-    """Both tangent kernels of the compile-time-N buckets — warp-split rows
-    (default) and the CTA-phase pipeline (HBGPU_TANGENT_KERNEL=pipe, read at
-    context creation) — on a Delaunay cube (several valence buckets, Dirichlet
-    rows) at N = 5 ... 47 and both tau modes, against the restatement."""
-    from paper_2411_14315_b200 import meshgen
-
-    if kernel == "pipe":
-        monkeypatch.setenv("HBGPU_TANGENT_KERNEL", "pipe")
-    mesh = meshgen.cube_delaunay(2500, seed=29)
-    N = 2 * modes - 1
-    neu = [(k, np.full(N, 5.0)) for k, p in enumerate(mesh.patches) if p.kind == NEUMANN]
-    prob = Problem(mesh, modes, 1.0, 1.06, 0.04, np.zeros(mesh.num_nodes * 3 * N), neu, 0.2)
-    ctx = gpu_ctx(prob, tau, 0.05)
-    orc = ob.Restated(prob, tau_mode=tau, pseudo_dt=0.05)
-    s = cases.random_modes_state(mesh.num_nodes, modes, 23)
-    p1 = ctx.assemble_tangent(s)
-    assert rel(p1, orc.tangent(s)) < TOL
-    assert np.array_equal(p1, ctx.assemble_tangent(s))  # bitwise repeatable
-
-
 @pytest.mark.parametrize("width", ["64", "256"])
 def test_tangent_pipe_widths(gpu, monkeypatch, width):
     """The persistent tangent pipeline at forced CTA widths (HBGPU_TAN_WIDTH)."""
     monkeypatch.setenv("HBGPU_TAN_WIDTH", width)
-    monkeypatch.setenv("HBGPU_TANGENT_KERNEL", "pipe")
     prob = tube_problem(4)
     ctx = gpu_ctx(prob, 0, 0.3)
     orc = ob.Restated(prob, tau_mode=0, pseudo_dt=0.3)
