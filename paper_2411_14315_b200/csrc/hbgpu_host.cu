@@ -1344,6 +1344,8 @@ int hbgpu_set_basis(hbgpu_ctx* c, int modes, double period) {
                         std::to_string(HBGPU_MAX_MODES) + " (N = 2M-1 <= " +
                         std::to_string(2 * HBGPU_MAX_MODES - 1) +
                         " time samples; the dense H lives in shared memory)");
+    if ((unsigned long long)c->nn * 4ull * (unsigned long long)(2 * modes - 1) >= (1ull << 32))
+        return fail(c, HBGPU_ERR_INVALID, "state vector exceeds 2^32 doubles (32-bit element offsets in the gathers)");
     c->M = modes;
     c->N = 2 * modes - 1;
     c->period = period;

@@ -95,8 +95,21 @@ __device__ __forceinline__ double rsqrt_nr(double x) {
 // tau = arg^-1/2, or 0 when arg <= 0 / NaN (`bad`, flagged by the caller).
 // The argument is sanitised and the result masked by a multiply, so the
 // Newton iteration is always executed and never sits behind a branch.
+// TAU_UNCHECKED (default): a non-positive argument only happens on a degenerate
+// element; the caller raises the context's domain-error flag and every output of
+// that call is discarded by the host (the reference throws, assembly.cpp:64-66),
+// so the value returned for it is irrelevant and the sanitising select + masking
+// multiply (1 DMUL + 4 FSEL per quadrature point) are dropped.
+#ifndef TAU_UNCHECKED
+#define TAU_UNCHECKED 1
+#endif
 __device__ __forceinline__ double tau_or_zero(double arg, bool bad) {
+#if TAU_UNCHECKED
+    (void)bad;
+    return rsqrt_nr(arg);
+#else
     return rsqrt_nr(bad ? 1.0 : arg) * (bad ? 0.0 : 1.0);
+#endif
 }
 
 // mbarrier + bulk async copy (cp.async.bulk, the TMA engine's 1-D mode)

@@ -202,7 +202,7 @@ struct SmemRow {
 __device__ __forceinline__ void element_residual_smem(const double* __restrict__ gsm,
                                                       const double* __restrict__ nd, int ndst,
                                                       const int lc[4], int T, int t,
-                                                      double rho, double mu, double nu,
+                                                      double rho, double inv_rho, double mu, double nu,
                                                       int tau_mode, int* flag,
                                                       double* __restrict__ out) {
     // nd: node data [ln][c][t], c = u0 u1 u2 p hu0 hu1 hu2, node stride ndst
@@ -287,7 +287,8 @@ __device__ __forceinline__ void element_residual_smem(const double* __restrict__
     // pass 2, node a = quadrature point a: the q = a parts (conv_q, tl_q
     // recomputed from tau_a) plus the q-sum and Galerkin terms, each output
     // written once
-    const double muV = mu * V, moff = rho * V / 20.0, wr = w / rho;
+    // rho V / 20 and w / rho as multiplications (two FP64 divisions per (element, sample) otherwise)
+    const double muV = mu * V, moff = rho * V * 0.05, wr = w * inv_rho;
 #pragma unroll
     for (int a = 0; a < 4; ++a) {
         const double ga0 = g[3 * a], ga1 = g[3 * a + 1], ga2 = g[3 * a + 2];
@@ -371,6 +372,9 @@ void residual_pack_write(unsigned char* dst, int nloc, int ecount, int nb, const
 #ifndef RES_GATHER_LINEAR
 #define RES_GATHER_LINEAR 2
 #endif
+#ifndef RES_REDUCE_SPLIT
+#define RES_REDUCE_SPLIT 0
+#endif
 #ifndef RES_ND_PAD
 #define RES_ND_PAD 1
 #endif
@@ -409,6 +413,7 @@ __global__ void __launch_bounds__(kChunkElems * T, RES_MINB * 4 / T) residual_ch
     int ch = blockIdx.x;
     if (ch >= nch)
         return;
+    const double inv_rho = 1.0 / a.rho;
     if (threadIdx.x == 0) {
         mbar_init(mbar, 1);
         mbar_init(mbar + 1, 1);
@@ -437,8 +442,10 @@ __global__ void __launch_bounds__(kChunkElems * T, RES_MINB * 4 / T) residual_ch
         constexpr int P = (T % 2 == 0) ? 2 : 1, TG = T / P;
         for (int k = threadIdx.x; k < nloc * 7 * TG; k += blockDim.x) {
             const int ln = k / (7 * TG), rem = k - ln * 7 * TG, cc = rem / TG, t = P * (rem - cc * TG);
-            const long A = nodes[ln];
-            const double* src = cc < 4 ? a.state + (A * 4 + cc) * N + n0 : a.hu + (A * 3 + (cc - 4)) * N + n0;
+            // 32-bit element offsets (4 nn N < 2^32 is checked in hbgpu_set_basis)
+            const unsigned A = (unsigned)nodes[ln];
+            const double* src = cc < 4 ? a.state + ((A * 4u + (unsigned)cc) * (unsigned)N + (unsigned)n0)
+                                       : a.hu + ((A * 3u + (unsigned)(cc - 4)) * (unsigned)N + (unsigned)n0);
             double* dst = nd + ln * nds + cc * T + t;
 #pragma unroll
             for (int q = 0; q < P; ++q) {
@@ -515,14 +522,51 @@ __global__ void __launch_bounds__(kChunkElems * T, RES_MINB * 4 / T) residual_ch
                     const uint32_t pkc = lconn[el];
                     const int lc[4] = {int(pkc & 0xFF), int((pkc >> 8) & 0xFF), int((pkc >> 16) & 0xFF),
                                        int(pkc >> 24)};
-                    element_residual_smem(geo + el * kTGeo, nd, nds, lc, T, t, a.rho, a.mu, a.nu,
+                    element_residual_smem(geo + el * kTGeo, nd, nds, lc, T, t, a.rho, inv_rho, a.mu, a.nu,
                                           a.tau_mode, a.flag, slots + el * es + t);
                 }
             }
             __syncthreads();
             double* out = a.partial + ((long)tile * a.npairs + nb) * ndst;
+#if RES_REDUCE_SPLIT
+            // two threads per (chunk node, sample): outputs 0..3 and 4..6 (the per-sample
+            // mapping leaves 45% of the CTA idle in this pass); same summation order
+            {
+                const int half = nloc * T;
+                for (int k = threadIdx.x; k < 2 * half; k += blockDim.x) {
+                    const int hi = k >= half, kk = hi ? k - half : k;
+                    const int ln = kk / T, t = kk - ln * T;
+                    const int q1 = sptr[ln + 1];
+                    if (!hi) {
+                        double acc[4] = {0.0, 0.0, 0.0, 0.0};
+                        for (int q = sptr[ln]; q < q1; ++q) {
+                            const double* sp = slots + soff[q] * T + t;  // (el*29 + a*7) T
+#pragma unroll
+                            for (int cc = 0; cc < 4; ++cc)
+                                acc[cc] += sp[cc * T];
+                        }
+#pragma unroll
+                        for (int cc = 0; cc < 4; ++cc)
+                            out[(ln * 7 + cc) * T + t] = acc[cc];
+                    } else {
+                        double acc[3] = {0.0, 0.0, 0.0};
+                        for (int q = sptr[ln]; q < q1; ++q) {
+                            const double* sp = slots + soff[q] * T + 4 * T + t;
+#pragma unroll
+                            for (int cc = 0; cc < 3; ++cc)
+                                acc[cc] += sp[cc * T];
+                        }
+#pragma unroll
+                        for (int cc = 0; cc < 3; ++cc)
+                            out[(ln * 7 + 4 + cc) * T + t] = acc[cc];
+                    }
+                }
+            }
+#else
             // thread per (chunk node, sample): walk the node's slot offsets once,
-            // accumulating all 7 outputs
+            // accumulating all 7 outputs.  (One thread per (node, output, sample) — every
+            // thread busy, one 7x longer dependent chain each — measured slower: config 4
+            // element pass 22.2 -> 23.8 ms, profiles/r2r_kbench.log.)
             for (int k = threadIdx.x; k < nloc * T; k += blockDim.x) {
                 const int ln = k / T, t = k - ln * T;
                 double acc[7] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
@@ -537,6 +581,7 @@ __global__ void __launch_bounds__(kChunkElems * T, RES_MINB * 4 / T) residual_ch
                 for (int cc = 0; cc < 7; ++cc)
                     out[(ln * 7 + cc) * T + t] = acc[cc];
             }
+#endif
         }
     }
     cp_async_wait<0>();

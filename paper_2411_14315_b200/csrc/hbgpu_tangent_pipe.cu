@@ -140,6 +140,17 @@ void launch_tangent_pack_refresh(unsigned char* pack, const int* pack_ptr, int n
 #define TAN_REC_STRIDE 10
 #endif
 constexpr int kRecStride = TAN_REC_STRIDE;
+// gathers of the next row issued by every warp (a few bulk copies each)
+// instead of warp 0 alone, whose phase 2 then started late and held the
+// row's closing barrier (ncu r2p: warp 0 spent 36% of its time issuing copies)
+#ifndef TAN_GATHER_ALL
+#define TAN_GATHER_ALL 1
+#endif
+// the row node's velocity comes from the four gathered element nodes (local
+// slot 0 = the row node) instead of three more shared-memory loads
+#ifndef TAN_UA_REUSE
+#define TAN_UA_REUSE 1
+#endif
 
 // Sample pairs (P = 2): every phase-1 and phase-2 thread item covers a PAIR
 // of consecutive time samples.  The geometry record, the contribution record
@@ -151,6 +162,16 @@ constexpr int kRecStride = TAN_REC_STRIDE;
 // quantise worse and pairs lose (31.6 -> 32.8 ms, config 4), so N >= 31 and the
 // generic kernel stay on single samples.
 __host__ __device__ constexpr int tan_pair(int NC) { return (NC >= 3 && NC <= 19) ? 2 : 1; }
+// Phase-2 sample groups (single-sample kernels, NC >= 31): a phase-2 item is a
+// block slot and G2 samples t, t + Q, t + 2Q, ... (Q = ceil(N / G2)), so the
+// contribution record (4 x LDS.128, >= 2 wavefronts each even when broadcast) is
+// read once per G2 samples; consecutive lanes still take consecutive samples,
+// so summary loads and P stores stay contiguous per warp.  Phase 2 is bound by
+// shared-memory bandwidth (ncu r2p: 100% of the wavefront rate, FP64 pipe 31%).
+#ifndef TAN_G2
+#define TAN_G2 3
+#endif
+__host__ __device__ constexpr int tan_grp(int NC) { return (NC >= 31) ? TAN_G2 : 1; }
 __host__ __device__ inline int tan_ntp(int NT, int P) { return (NT + P - 1) / P * P; }
 
 struct PipeSmem {
@@ -186,6 +207,7 @@ size_t tangent_pipe_smem(int max_pack, int max_inc, int max_blk, int N, int NT) 
 template <int TAU, int THREADS, int NC>
 __global__ void __launch_bounds__(THREADS, 512 / THREADS) tangent_pipe_kernel(TangentArgs a, PipeArgs pa) {
     constexpr int P = tan_pair(NC);
+    constexpr bool UA = TAN_UA_REUSE && P == 1;  // (pairs: the six live doubles spill)
     extern __shared__ __align__(128) unsigned char smraw[];
     const int N = NC ? NC : a.N, NT = NC ? NC : a.NT;
     const int n0 = NC ? 0 : blockIdx.y * NT, nt = NC ? NC : min(NT, N - n0);
@@ -203,6 +225,7 @@ __global__ void __launch_bounds__(THREADS, 512 / THREADS) tangent_pipe_kernel(Ta
     const double rho = a.rho, diffc = 3.0 * a.nu * a.nu, dAB = kQA - kQB;
     const double c1 = kQB * (1.0 + dAB), c2 = dAB * dAB;
     const double mu = a.mu, pc = a.pseudo_c;
+    const double inv_rho = 1.0 / rho;  // once per thread (w / rho per item was a full FP64 division)
     const int r0 = blockIdx.x, rs = gridDim.x, nrows = pa.nrows;
     if (threadIdx.x == 0) {
         for (int k = 0; k < 3; ++k)
@@ -217,7 +240,11 @@ __global__ void __launch_bounds__(THREADS, 512 / THREADS) tangent_pipe_kernel(Ta
         mbar_expect_tx(mbar + slot, bytes);
         bulk_g2s(smraw + Ls.meta + slot * mpack, pa.pack + (size_t)p0 * 16, bytes, mbar + slot);
     };
-    auto issue_gather = [&](int slot) {  // warp 0, all lanes
+    // copies idx = first, first + stride, ... of the row in pack slot `slot`:
+    // idx < nblk the neighbour node's 4N state record, else an incidence's
+    // geometry record.  `expect` (one thread per row) arms the mbarrier with the
+    // row's byte count; its tx-count may run negative until then.
+    auto issue_gather = [&](int slot, int first, int stride, bool expect) {
         const unsigned char* m = smraw + Ls.meta + slot * mpack;
         const int* h = reinterpret_cast<const int*>(m);
         const int ninc = h[1], nblk = h[2];
@@ -226,14 +253,19 @@ __global__ void __launch_bounds__(THREADS, 512 / THREADS) tangent_pipe_kernel(Ta
         const int2* inc = reinterpret_cast<const int2*>(m + s.inc);
         double* su = reinterpret_cast<double*>(smraw + Ls.su);
         double* tg = reinterpret_cast<double*>(smraw + Ls.tg);
-        if (lane == 0)
+        if (expect)
             mbar_expect_tx(mbar + 2, (uint32_t)(nblk * 4 * N * 8 + ninc * kTGeo * 8));
         __syncwarp();
-        for (int j = lane; j < nblk; j += 32)
-            bulk_g2s(su + (size_t)j * (4 * N + TAN_SU_PAD), a.state + (size_t)cols[j] * 4 * N, 4 * N * 8, mbar + 2);
-        for (int i = lane; i < ninc; i += 32)
-            bulk_g2s(tg + (size_t)i * kTGeo, a.tgeom + (size_t)(inc[i].x & 0x3FFFFFFF) * kTGeo,
-                     kTGeo * 8, mbar + 2);
+        for (int idx = first; idx < nblk + ninc; idx += stride) {
+            if (idx < nblk) {
+                bulk_g2s(su + (size_t)idx * (4 * N + TAN_SU_PAD), a.state + (size_t)cols[idx] * 4 * N, 4 * N * 8,
+                         mbar + 2);
+            } else {
+                const int i = idx - nblk;
+                bulk_g2s(tg + (size_t)i * kTGeo, a.tgeom + (size_t)(inc[i].x & 0x3FFFFFFF) * kTGeo, kTGeo * 8,
+                         mbar + 2);
+            }
+        }
     };
 
     // prologue: pack and gathers of row 0
@@ -241,7 +273,7 @@ __global__ void __launch_bounds__(THREADS, 512 / THREADS) tangent_pipe_kernel(Ta
         if (lane == 0)
             issue_pack(r0, 0);
         mbar_wait(mbar + 0, 0);
-        issue_gather(0);
+        issue_gather(0, lane, 32, lane == 0);
     }
 
     // work items (x, q): x = incidence (phase 1) or slot (phase 2), q = sample group
@@ -335,8 +367,10 @@ __global__ void __launch_bounds__(THREADS, 512 / THREADS) tangent_pipe_kernel(Ta
                 usum[k2][0] = usum[k2][1] = usum[k2][2] = 0.0;
 #pragma unroll
                 for (int b = 0; b < 4; ++b) {
+                    // UA: slot 0 = the row node (the quadrature sums are symmetric)
+                    const int bb = UA ? ((la + b) & 3) : b;
                     const double* sb =
-                        su + (size_t)((cols >> (8 * b)) & 0xFFu) * (4 * N + TAN_SU_PAD) + n0 + tt[k2];
+                        su + (size_t)((cols >> (8 * bb)) & 0xFFu) * (4 * N + TAN_SU_PAD) + n0 + tt[k2];
 #pragma unroll
                     for (int c = 0; c < 3; ++c) {
                         u[k2][b][c] = sb[c * N];
@@ -390,14 +424,15 @@ __global__ void __launch_bounds__(THREADS, 512 / THREADS) tangent_pipe_kernel(Ta
                 }
             }
             // + sum_q N_a(q) u_q = B usum + (A-B) u_{q=a} = c1 usum + c2 u_A (u_A: the row node)
-            const double wr = w * rho, wo = w / rho;
+            const double wr = w * rho, wo = w * inv_rho;
             double o[7][P];
 #pragma unroll
             for (int k2 = 0; k2 < P; ++k2) {
                 const double* sA = su + (size_t)kdiag * (4 * N + TAN_SU_PAD) + n0 + tt[k2];
 #pragma unroll
                 for (int c = 0; c < 3; ++c) {
-                    o[c][k2] = wr * fma(c1, usum[k2][c], fma(c2, sA[c * N], kap[k2][c]));
+                    const double uA = UA ? u[k2][0][c] : sA[c * N];
+                    o[c][k2] = wr * fma(c1, usum[k2][c], fma(c2, uA, kap[k2][c]));
                     o[3 + c][k2] = w * z[k2][c];
                 }
                 o[6][k2] = wo * tsum[k2];
@@ -419,111 +454,215 @@ __global__ void __launch_bounds__(THREADS, 512 / THREADS) tangent_pipe_kernel(Ta
             atomicOr(a.flag, 1);
         __syncthreads();
 
+#if TAN_GATHER_ALL
+        if (more) {  // every warp issues a few of the next row's copies
+            mbar_wait(mbar + (ms ^ 1), ((k + 1) >> 1) & 1);
+            const int nw = blockDim.x >> 5;
+            issue_gather(ms ^ 1, lane * nw + warp, 32 * nw, threadIdx.x == 0);
+        }
+#else
         if (warp == 0 && more) {
             mbar_wait(mbar + (ms ^ 1), ((k + 1) >> 1) & 1);
-            issue_gather(ms ^ 1);
+            issue_gather(ms ^ 1, lane, 32, lane == 0);
         }
+#endif
         // ---- phase 2: per (slot, sample group) register accumulation
-        for (int it = threadIdx.x, slot = x_start, q = q_start; it < nslots * nq;
-             it += blockDim.x, q += dq, slot += dx + (q >= nq), q -= (q >= nq ? nq : 0)) {
-            const int t = P * q;
-            const int4 info = sinfo[slot];
-            const int j = info.z;
-            const bool bfix = info.w != 0;
-            double K[P], G0[P], G1[P], G2[P], D0[P], D1[P], D2[P], L[P];
+        if constexpr (P == 1) {
+            // item = (slot, q): samples q, q + Q2, ... (G2 of them); the contribution
+            // record is read once per item
+            constexpr int G2 = tan_grp(NC);
+            const int Q2 = (nt + G2 - 1) / G2;
+            const int dx2 = blockDim.x / Q2, dq2 = blockDim.x - dx2 * Q2;
+            int slot = threadIdx.x / Q2, q = threadIdx.x - slot * Q2;
+            for (int it = threadIdx.x; it < nslots * Q2;
+                 it += blockDim.x, q += dq2, slot += dx2 + (q >= Q2), q -= (q >= Q2 ? Q2 : 0)) {
+                const int4 info = sinfo[slot];
+                const int j = info.z;
+                const bool bfix = info.w != 0;
+                int tk[G2];
 #pragma unroll
-            for (int k2 = 0; k2 < P; ++k2)
-                K[k2] = G0[k2] = G1[k2] = G2[k2] = D0[k2] = D1[k2] = D2[k2] = L[k2] = 0.0;
-            for (int p = info.x; p < info.y; ++p) {
-                const double2* rp = reinterpret_cast<const double2*>(rec + p * kRecStride);
-                const double2 ra = rp[0], rb = rp[1], rc = rp[2], rd = rp[3];
-                const double* sp = summ + __double_as_longlong(rd.y) + t;
-                const double gb0 = rc.x, gb1 = rc.y, gb2 = rd.x;
-                double sv[7][P];
+                for (int g = 0; g < G2; ++g)
+                    tk[g] = min(q + g * Q2, nt - 1);  // a padded sample repeats the last one (not stored)
+                double K[G2], G0[G2], G1[G2], G2v[G2], D0[G2], D1[G2], D2[G2], L[G2];
 #pragma unroll
-                for (int c = 0; c < 7; ++c) {
-                    if (P == 2) {
-                        const double2 v2 = *reinterpret_cast<const double2*>(sp + c * SC);
-                        sv[c][0] = v2.x;
-                        sv[c][P - 1] = v2.y;
-                    } else {
-                        sv[c][0] = sp[c * SC];
+                for (int g = 0; g < G2; ++g)
+                    K[g] = G0[g] = G1[g] = G2v[g] = D0[g] = D1[g] = D2[g] = L[g] = 0.0;
+                for (int p = info.x; p < info.y; ++p) {
+                    const double2* rp = reinterpret_cast<const double2*>(rec + p * kRecStride);
+                    const double2 ra = rp[0], rb = rp[1], rc = rp[2], rd = rp[3];
+                    const double* sp = summ + __double_as_longlong(rd.y);
+                    const double gb0 = rc.x, gb1 = rc.y, gb2 = rd.x;
+#pragma unroll
+                    for (int g = 0; g < G2; ++g) {
+                        const double* sg = sp + tk[g];
+                        const double s0 = sg[0], s1 = sg[SC], s2 = sg[2 * SC], s3 = sg[3 * SC], s4 = sg[4 * SC],
+                                     s5 = sg[5 * SC], s6 = sg[6 * SC];
+                        K[g] = fma(s0, gb0, fma(s1, gb1, fma(s2, gb2, K[g])));
+                        const double al = fma(s3, ra.x, fma(s4, ra.y, s5 * rb.x));  // w alpha_a = (w z) . dN_a
+                        G0[g] = fma(al, gb0, G0[g]);
+                        G1[g] = fma(al, gb1, G1[g]);
+                        G2v[g] = fma(al, gb2, G2v[g]);
+                        const double alb = fma(s3, gb0, fma(s4, gb1, s5 * gb2));
+                        D0[g] = fma(ra.x, alb, D0[g]);
+                        D1[g] = fma(ra.y, alb, D1[g]);
+                        D2[g] = fma(rb.x, alb, D2[g]);
+                        L[g] = fma(rb.y, s6, L[g]);
+                    }
+                }
+                if (slot >= dparts || slot == 0) {
+                    const double2* bc = reinterpret_cast<const double2*>(blkc + j * 8);
+                    const double2 b0 = bc[0], b1 = bc[1], b2 = bc[2], b3 = bc[3];
+                    const double kc = fma(mu, b0.x, pc * b0.y);
+#pragma unroll
+                    for (int g = 0; g < G2; ++g) {
+                        K[g] += kc;
+                        G0[g] += b1.x;
+                        G1[g] += b1.y;
+                        G2v[g] += b2.x;
+                        D0[g] += b2.y;
+                        D1[g] += b3.x;
+                        D2[g] += b3.y;
                     }
                 }
 #pragma unroll
-                for (int k2 = 0; k2 < P; ++k2) {
-                    K[k2] = fma(sv[0][k2], gb0, fma(sv[1][k2], gb1, fma(sv[2][k2], gb2, K[k2])));
-                    // w alpha_a = (w z) . dN_a
-                    const double al = fma(sv[3][k2], ra.x, fma(sv[4][k2], ra.y, sv[5][k2] * rb.x));
-                    G0[k2] = fma(al, gb0, G0[k2]);
-                    G1[k2] = fma(al, gb1, G1[k2]);
-                    G2[k2] = fma(al, gb2, G2[k2]);
-                    const double alb = fma(sv[3][k2], gb0, fma(sv[4][k2], gb1, sv[5][k2] * gb2));
-                    D0[k2] = fma(ra.x, alb, D0[k2]);
-                    D1[k2] = fma(ra.y, alb, D1[k2]);
-                    D2[k2] = fma(rb.x, alb, D2[k2]);
-                    L[k2] = fma(rb.y, sv[6][k2], L[k2]);
+                for (int g = 0; g < G2; ++g) {
+                    if (afix || bfix)
+                        K[g] = 0.0;
+                    if (afix)
+                        G0[g] = G1[g] = G2v[g] = 0.0;
+                    if (bfix)
+                        D0[g] = D1[g] = D2[g] = 0.0;
                 }
-            }
-            if (slot >= dparts || slot == 0) {
-                const double2* bc = reinterpret_cast<const double2*>(blkc + j * 8);
-                const double2 b0 = bc[0], b1 = bc[1], b2 = bc[2], b3 = bc[3];
-                const double kc = fma(mu, b0.x, pc * b0.y);
 #pragma unroll
-                for (int k2 = 0; k2 < P; ++k2) {
-                    K[k2] += kc;
-                    G0[k2] += b1.x;
-                    G1[k2] += b1.y;
-                    G2[k2] += b2.x;
-                    D0[k2] += b2.y;
-                    D1[k2] += b3.x;
-                    D2[k2] += b3.y;
-                }
-            }
-#pragma unroll
-            for (int k2 = 0; k2 < P; ++k2) {
-                if (afix || bfix)
-                    K[k2] = 0.0;
-                if (afix)
-                    G0[k2] = G1[k2] = G2[k2] = 0.0;
-                if (bfix)
-                    D0[k2] = D1[k2] = D2[k2] = 0.0;
-            }
-            if (slot >= dparts) {
-#pragma unroll
-                for (int k2 = 0; k2 < P; ++k2) {
-                    if (t + k2 >= nt)
+                for (int g = 0; g < G2; ++g) {
+                    const int t = q + g * Q2;
+                    if (t >= nt)
                         break;
-                    double* out = a.pvals + ((long)(k0 + j) * 8) * N + n0 + t + k2;
-                    __stcs(out, K[k2]);
-                    __stcs(out + N, G0[k2]);
-                    __stcs(out + 2 * N, G1[k2]);
-                    __stcs(out + 3 * N, G2[k2]);
-                    __stcs(out + 4 * N, D0[k2]);
-                    __stcs(out + 5 * N, D1[k2]);
-                    __stcs(out + 6 * N, D2[k2]);
-                    __stcs(out + 7 * N, L[k2]);
+                    if (slot >= dparts) {
+                        double* out = a.pvals + ((long)(k0 + j) * 8) * N + n0 + t;
+                        __stcs(out, K[g]);
+                        __stcs(out + N, G0[g]);
+                        __stcs(out + 2 * N, G1[g]);
+                        __stcs(out + 3 * N, G2v[g]);
+                        __stcs(out + 4 * N, D0[g]);
+                        __stcs(out + 5 * N, D1[g]);
+                        __stcs(out + 6 * N, D2[g]);
+                        __stcs(out + 7 * N, L[g]);
+                    } else {
+                        double* o = dpart + (size_t)slot * 8 * NTp + t;
+                        o[0] = K[g];
+                        o[NTp] = G0[g];
+                        o[2 * NTp] = G1[g];
+                        o[3 * NTp] = G2v[g];
+                        o[4 * NTp] = D0[g];
+                        o[5 * NTp] = D1[g];
+                        o[6 * NTp] = D2[g];
+                        o[7 * NTp] = L[g];
+                    }
                 }
-            } else {
-                double* o = dpart + (size_t)slot * 8 * NTp + t;
-                if (P == 2) {
-                    *reinterpret_cast<double2*>(o) = make_double2(K[0], K[P - 1]);
-                    *reinterpret_cast<double2*>(o + NTp) = make_double2(G0[0], G0[P - 1]);
-                    *reinterpret_cast<double2*>(o + 2 * NTp) = make_double2(G1[0], G1[P - 1]);
-                    *reinterpret_cast<double2*>(o + 3 * NTp) = make_double2(G2[0], G2[P - 1]);
-                    *reinterpret_cast<double2*>(o + 4 * NTp) = make_double2(D0[0], D0[P - 1]);
-                    *reinterpret_cast<double2*>(o + 5 * NTp) = make_double2(D1[0], D1[P - 1]);
-                    *reinterpret_cast<double2*>(o + 6 * NTp) = make_double2(D2[0], D2[P - 1]);
-                    *reinterpret_cast<double2*>(o + 7 * NTp) = make_double2(L[0], L[P - 1]);
+            }
+        } else {
+            for (int it = threadIdx.x, slot = x_start, q = q_start; it < nslots * nq;
+                 it += blockDim.x, q += dq, slot += dx + (q >= nq), q -= (q >= nq ? nq : 0)) {
+                const int t = P * q;
+                const int4 info = sinfo[slot];
+                const int j = info.z;
+                const bool bfix = info.w != 0;
+                double K[P], G0[P], G1[P], G2[P], D0[P], D1[P], D2[P], L[P];
+    #pragma unroll
+                for (int k2 = 0; k2 < P; ++k2)
+                    K[k2] = G0[k2] = G1[k2] = G2[k2] = D0[k2] = D1[k2] = D2[k2] = L[k2] = 0.0;
+                for (int p = info.x; p < info.y; ++p) {
+                    const double2* rp = reinterpret_cast<const double2*>(rec + p * kRecStride);
+                    const double2 ra = rp[0], rb = rp[1], rc = rp[2], rd = rp[3];
+                    const double* sp = summ + __double_as_longlong(rd.y) + t;
+                    const double gb0 = rc.x, gb1 = rc.y, gb2 = rd.x;
+                    double sv[7][P];
+    #pragma unroll
+                    for (int c = 0; c < 7; ++c) {
+                        if (P == 2) {
+                            const double2 v2 = *reinterpret_cast<const double2*>(sp + c * SC);
+                            sv[c][0] = v2.x;
+                            sv[c][P - 1] = v2.y;
+                        } else {
+                            sv[c][0] = sp[c * SC];
+                        }
+                    }
+    #pragma unroll
+                    for (int k2 = 0; k2 < P; ++k2) {
+                        K[k2] = fma(sv[0][k2], gb0, fma(sv[1][k2], gb1, fma(sv[2][k2], gb2, K[k2])));
+                        // w alpha_a = (w z) . dN_a
+                        const double al = fma(sv[3][k2], ra.x, fma(sv[4][k2], ra.y, sv[5][k2] * rb.x));
+                        G0[k2] = fma(al, gb0, G0[k2]);
+                        G1[k2] = fma(al, gb1, G1[k2]);
+                        G2[k2] = fma(al, gb2, G2[k2]);
+                        const double alb = fma(sv[3][k2], gb0, fma(sv[4][k2], gb1, sv[5][k2] * gb2));
+                        D0[k2] = fma(ra.x, alb, D0[k2]);
+                        D1[k2] = fma(ra.y, alb, D1[k2]);
+                        D2[k2] = fma(rb.x, alb, D2[k2]);
+                        L[k2] = fma(rb.y, sv[6][k2], L[k2]);
+                    }
+                }
+                if (slot >= dparts || slot == 0) {
+                    const double2* bc = reinterpret_cast<const double2*>(blkc + j * 8);
+                    const double2 b0 = bc[0], b1 = bc[1], b2 = bc[2], b3 = bc[3];
+                    const double kc = fma(mu, b0.x, pc * b0.y);
+    #pragma unroll
+                    for (int k2 = 0; k2 < P; ++k2) {
+                        K[k2] += kc;
+                        G0[k2] += b1.x;
+                        G1[k2] += b1.y;
+                        G2[k2] += b2.x;
+                        D0[k2] += b2.y;
+                        D1[k2] += b3.x;
+                        D2[k2] += b3.y;
+                    }
+                }
+    #pragma unroll
+                for (int k2 = 0; k2 < P; ++k2) {
+                    if (afix || bfix)
+                        K[k2] = 0.0;
+                    if (afix)
+                        G0[k2] = G1[k2] = G2[k2] = 0.0;
+                    if (bfix)
+                        D0[k2] = D1[k2] = D2[k2] = 0.0;
+                }
+                if (slot >= dparts) {
+    #pragma unroll
+                    for (int k2 = 0; k2 < P; ++k2) {
+                        if (t + k2 >= nt)
+                            break;
+                        double* out = a.pvals + ((long)(k0 + j) * 8) * N + n0 + t + k2;
+                        __stcs(out, K[k2]);
+                        __stcs(out + N, G0[k2]);
+                        __stcs(out + 2 * N, G1[k2]);
+                        __stcs(out + 3 * N, G2[k2]);
+                        __stcs(out + 4 * N, D0[k2]);
+                        __stcs(out + 5 * N, D1[k2]);
+                        __stcs(out + 6 * N, D2[k2]);
+                        __stcs(out + 7 * N, L[k2]);
+                    }
                 } else {
-                    o[0] = K[0];
-                    o[NTp] = G0[0];
-                    o[2 * NTp] = G1[0];
-                    o[3 * NTp] = G2[0];
-                    o[4 * NTp] = D0[0];
-                    o[5 * NTp] = D1[0];
-                    o[6 * NTp] = D2[0];
-                    o[7 * NTp] = L[0];
+                    double* o = dpart + (size_t)slot * 8 * NTp + t;
+                    if (P == 2) {
+                        *reinterpret_cast<double2*>(o) = make_double2(K[0], K[P - 1]);
+                        *reinterpret_cast<double2*>(o + NTp) = make_double2(G0[0], G0[P - 1]);
+                        *reinterpret_cast<double2*>(o + 2 * NTp) = make_double2(G1[0], G1[P - 1]);
+                        *reinterpret_cast<double2*>(o + 3 * NTp) = make_double2(G2[0], G2[P - 1]);
+                        *reinterpret_cast<double2*>(o + 4 * NTp) = make_double2(D0[0], D0[P - 1]);
+                        *reinterpret_cast<double2*>(o + 5 * NTp) = make_double2(D1[0], D1[P - 1]);
+                        *reinterpret_cast<double2*>(o + 6 * NTp) = make_double2(D2[0], D2[P - 1]);
+                        *reinterpret_cast<double2*>(o + 7 * NTp) = make_double2(L[0], L[P - 1]);
+                    } else {
+                        o[0] = K[0];
+                        o[NTp] = G0[0];
+                        o[2 * NTp] = G1[0];
+                        o[3 * NTp] = G2[0];
+                        o[4 * NTp] = D0[0];
+                        o[5 * NTp] = D1[0];
+                        o[6 * NTp] = D2[0];
+                        o[7 * NTp] = L[0];
+                    }
                 }
             }
         }

@@ -116,6 +116,14 @@ def run_one(which, points, reps):
         # parity of this build against the first library's outputs is checked by the caller
         r = d_r.cpu().numpy()
         np.save(f"/tmp/kbench_out_{w}_{os.path.basename(hbgpu.LIB_PATH)}_r.npy", r[: 4 * N * 2000])
+        # a spread of P block rows (first, last and a stride through the mesh); compared with the
+        # first library's by the caller
+        nn = prob.mesh.num_nodes
+        rows = np.unique(np.concatenate([np.arange(0, nn, max(1, nn // 1500)), np.arange(nn - 50, nn)])).astype(np.int32)
+        ctx.assemble_tangent_dev(d_s.data_ptr())
+        torch.cuda.synchronize()
+        pr = ctx.pvals_rows(rows)
+        np.save(f"/tmp/kbench_out_{w}_{os.path.basename(hbgpu.LIB_PATH)}_p.npy", pr)
         ctx.close()
         del d_s, d_r
         torch.cuda.empty_cache()
@@ -134,12 +142,24 @@ def main():
         run_one(args.which, args.points, args.reps)
         return
     make_problems(args.which, args.points)
+    first = None
     for lib in args.libs.split(","):
         env = dict(os.environ, HBGPU_LIB=os.path.abspath(lib))
         out = subprocess.run([sys.executable, __file__, "--child", "--which", args.which, "--points",
                               str(args.points), "--reps", str(args.reps)], env=env, capture_output=True,
                              text=True)
         print(out.stdout.strip() or out.stderr[-2000:], flush=True)
+        import numpy as np
+        base = os.path.basename(os.path.abspath(lib))
+        first = first or base
+        for w in args.which.split(","):
+            for kind in ("r", "p"):
+                try:
+                    x = np.load(f"/tmp/kbench_out_{w}_{base}_{kind}.npy")
+                    y = np.load(f"/tmp/kbench_out_{w}_{first}_{kind}.npy")
+                    print(f"  parity {w} {kind}: rel diff vs {first} = {np.linalg.norm(x - y) / np.linalg.norm(y):.2e}", flush=True)
+                except Exception as e:  # noqa: BLE001
+                    print(f"  parity {w} {kind}: {e}", flush=True)
 
 
 if __name__ == "__main__":
