@@ -367,16 +367,18 @@ void residual_pack_write(unsigned char* dst, int nloc, int ecount, int nb, const
     memcpy(dst + s.lconn, lconn, sizeof(uint32_t) * (size_t)ecount);
 }
 
-// shared-memory node-record stride of the residual tiles: 7T doubles, padded
-// to 7T + 1 for T = 4 so the 8 node records a warp reads start on spread banks
+// shared-memory node-record stride of the residual tiles: 7T doubles, unpadded.  A
+// warp's nodal load is eight 32-byte runs (8 elements x 4 samples); with the stride
+// 28 doubles = 24 words (mod 32) every run starts on an 8-bank boundary, so two runs
+// either coincide in their banks or do not touch (25% of node pairs conflict).  The
+// round-1 pad to 7T + 1 put consecutive nodes 6 banks apart, where 44% of the pairs
+// overlap partially: config 4 element pass 22.24 -> 21.60 ms without it
+// (profiles/r2w_kbench.log; ncu r2p: 4.13 wavefronts per nodal load against 2 ideal).
 #ifndef RES_GATHER_LINEAR
 #define RES_GATHER_LINEAR 2
 #endif
-#ifndef RES_REDUCE_SPLIT
-#define RES_REDUCE_SPLIT 0
-#endif
 #ifndef RES_ND_PAD
-#define RES_ND_PAD 1
+#define RES_ND_PAD 0
 #endif
 __host__ __device__ constexpr int res_nd_stride(int T) { return 7 * T + ((T == 4 && RES_ND_PAD) ? 1 : 0); }
 
@@ -528,45 +530,12 @@ __global__ void __launch_bounds__(kChunkElems * T, RES_MINB * 4 / T) residual_ch
             }
             __syncthreads();
             double* out = a.partial + ((long)tile * a.npairs + nb) * ndst;
-#if RES_REDUCE_SPLIT
-            // two threads per (chunk node, sample): outputs 0..3 and 4..6 (the per-sample
-            // mapping leaves 45% of the CTA idle in this pass); same summation order
-            {
-                const int half = nloc * T;
-                for (int k = threadIdx.x; k < 2 * half; k += blockDim.x) {
-                    const int hi = k >= half, kk = hi ? k - half : k;
-                    const int ln = kk / T, t = kk - ln * T;
-                    const int q1 = sptr[ln + 1];
-                    if (!hi) {
-                        double acc[4] = {0.0, 0.0, 0.0, 0.0};
-                        for (int q = sptr[ln]; q < q1; ++q) {
-                            const double* sp = slots + soff[q] * T + t;  // (el*29 + a*7) T
-#pragma unroll
-                            for (int cc = 0; cc < 4; ++cc)
-                                acc[cc] += sp[cc * T];
-                        }
-#pragma unroll
-                        for (int cc = 0; cc < 4; ++cc)
-                            out[(ln * 7 + cc) * T + t] = acc[cc];
-                    } else {
-                        double acc[3] = {0.0, 0.0, 0.0};
-                        for (int q = sptr[ln]; q < q1; ++q) {
-                            const double* sp = slots + soff[q] * T + 4 * T + t;
-#pragma unroll
-                            for (int cc = 0; cc < 3; ++cc)
-                                acc[cc] += sp[cc * T];
-                        }
-#pragma unroll
-                        for (int cc = 0; cc < 3; ++cc)
-                            out[(ln * 7 + 4 + cc) * T + t] = acc[cc];
-                    }
-                }
-            }
-#else
             // thread per (chunk node, sample): walk the node's slot offsets once,
-            // accumulating all 7 outputs.  (One thread per (node, output, sample) — every
-            // thread busy, one 7x longer dependent chain each — measured slower: config 4
-            // element pass 22.2 -> 23.8 ms, profiles/r2r_kbench.log.)
+            // accumulating all 7 outputs.  This pass runs at the shared-memory wavefront
+            // rate (ncu r2p: 94%); spreading it over more threads was slower both ways
+            // tried at config 4: one thread per (node, output, sample), one 7x longer
+            // dependent chain each, 22.2 -> 23.8 ms; two threads per (node, sample) with
+            // 4 + 3 outputs 22.2 -> 23.8 ms (profiles/r2r_kbench.log, r2w_kbench.log)
             for (int k = threadIdx.x; k < nloc * T; k += blockDim.x) {
                 const int ln = k / T, t = k - ln * T;
                 double acc[7] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
@@ -581,7 +550,6 @@ __global__ void __launch_bounds__(kChunkElems * T, RES_MINB * 4 / T) residual_ch
                 for (int cc = 0; cc < 7; ++cc)
                     out[(ln * 7 + cc) * T + t] = acc[cc];
             }
-#endif
         }
     }
     cp_async_wait<0>();

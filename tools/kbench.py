@@ -88,9 +88,9 @@ def run_one(which, points, reps):
 
         L.hbgpu_profile_enable(ctx.handle, 1)
         t_res = timed(lambda: ctx.assemble_residual_dev(d_s.data_ptr(), d_r.data_ptr()))
-        ms = np.zeros(9)
-        cnt = np.zeros(9, np.int32)
-        L.hbgpu_profile_read(ctx.handle, 9, ms.ctypes.data, cnt.ctypes.data)
+        ms = np.zeros(14)
+        cnt = np.zeros(14, np.int32)
+        L.hbgpu_profile_read(ctx.handle, 14, ms.ctypes.data, cnt.ctypes.data)
         L.hbgpu_profile_enable(ctx.handle, 0)
         t_tan = timed(lambda: ctx.assemble_tangent_dev(d_s.data_ptr()))
         t_both = timed(lambda: ctx.assemble_dev(d_s.data_ptr(), d_r.data_ptr()))
@@ -109,7 +109,7 @@ def run_one(which, points, reps):
         ne, N = prob.mesh.num_elements, prob.N
         res[w] = {"elements": ne, "N": N, "residual_ms": t_res, "tangent_ms": t_tan, "step_ms": t_both,
                   "res_elem_ms": float(ms[2] / max(cnt[2], 1)), "res_hu_ms": float(ms[1] / max(cnt[1], 1)),
-                  "res_final_ms": float(ms[3] / max(cnt[3], 1)),
+                  "res_final_ms": float(ms[3] / max(cnt[3], 1)), "tau_ms": float(ms[13] / max(cnt[13], 1)),
                   "res_tflops": CANON_RES * ne * N / (t_res * 1e-3) / 1e12,
                   "tan_tflops": CANON_TAN * ne * N / (t_tan * 1e-3) / 1e12,
                   "matvec_ms": t_mv, "matvec_gbs": mvb / (t_mv * 1e-3) / 1e9}
