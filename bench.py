@@ -746,6 +746,9 @@ def sweep_configs(args):
             "residual_tflops": CANON_RES_FLOP * ne * N / (t_res * 1e-3) / 1e12,
             "tangent_tflops": CANON_TAN_FLOP * ne * N / (t_tan * 1e-3) / 1e12,
             "matvec_ms": t_mv, "matvec_gbs": mvb / (t_mv * 1e-3) / 1e9, "matvec_frac_hbm": mvb / (t_mv * 1e-3) / 1e9 / hbm,
+            # the 100 back-to-back calls re-read P and y: below the 126 MB L2 the figure is an
+            # L2-resident rate, not an HBM one
+            "matvec_l2_resident": bool(mvb < 126e6),
             "newton_iter0": {"ms": t_newton, "gmres_iters": g_it, "gmres_relres": g_rr,
                              "gmres_status": g_st, "gmres_ms": float(ph_ms[7]), "matvec_ms": float(ph_ms[5])},
         })

@@ -59,11 +59,26 @@ constexpr int kTanPart = 8;
 // caller's select (which would cost a BSSY/BRA pair per quadrature point).
 #ifdef __CUDACC__
 #ifndef RSQRT_NEWTON
-#define RSQRT_NEWTON 2
+#define RSQRT_NEWTON 3
 #endif
 __device__ __forceinline__ double rsqrt_nr(double x) {
     double y;
-#if RSQRT_NEWTON == 1
+#if RSQRT_NEWTON == 3
+    // one cubic (Halley) step from the 2^-22 hardware seed: e = 1 - x y0^2,
+    // y = y0 (1 + e (1/2 + 3/8 e)); relative error ~ e^3 < 2^-60 (5 FP64
+    // instructions, against 7 for two Newton steps)
+    asm volatile(
+        "{\n\t.reg .f64 t, e, p, y0;\n\t"
+        "rsqrt.approx.ftz.f64 y0, %1;\n\t"
+        "mul.rn.f64 t, %1, y0;\n\t"
+        "neg.f64 t, t;\n\t"
+        "fma.rn.f64 e, t, y0, 0d3FF0000000000000;\n\t"
+        "fma.rn.f64 p, e, 0d3FD8000000000000, 0d3FE0000000000000;\n\t"
+        "mul.rn.f64 p, p, e;\n\t"
+        "fma.rn.f64 %0, y0, p, y0;\n\t}"
+        : "=d"(y)
+        : "d"(x));
+#elif RSQRT_NEWTON == 1
     asm volatile(
         "{\n\t.reg .f64 h, t, e, y0;\n\t"
         "rsqrt.approx.ftz.f64 y0, %1;\n\t"

@@ -161,7 +161,13 @@ constexpr int kRecStride = TAN_REC_STRIDE;
 // At N = 47 the 512-thread CTA's items per row (ninc x 24 pairs vs ninc x 47)
 // quantise worse and pairs lose (31.6 -> 32.8 ms, config 4), so N >= 31 and the
 // generic kernel stay on single samples.
-__host__ __device__ constexpr int tan_pair(int NC) { return (NC >= 3 && NC <= 19) ? 2 : 1; }
+#ifndef TAN_PAIR_MAXN
+#define TAN_PAIR_MAXN 19
+#endif
+#ifndef TAN_GRP_MINN
+#define TAN_GRP_MINN 31
+#endif
+__host__ __device__ constexpr int tan_pair(int NC) { return (NC >= 3 && NC <= TAN_PAIR_MAXN) ? 2 : 1; }
 // Phase-2 sample groups (single-sample kernels, NC >= 31): a phase-2 item is a
 // block slot and G2 samples t, t + Q, t + 2Q, ... (Q = ceil(N / G2)), so the
 // contribution record (4 x LDS.128, >= 2 wavefronts each even when broadcast) is
@@ -171,7 +177,7 @@ __host__ __device__ constexpr int tan_pair(int NC) { return (NC >= 3 && NC <= 19
 #ifndef TAN_G2
 #define TAN_G2 3
 #endif
-__host__ __device__ constexpr int tan_grp(int NC) { return (NC >= 31) ? TAN_G2 : 1; }
+__host__ __device__ constexpr int tan_grp(int NC) { return (NC >= TAN_GRP_MINN) ? TAN_G2 : 1; }
 __host__ __device__ inline int tan_ntp(int NT, int P) { return (NT + P - 1) / P * P; }
 
 struct PipeSmem {
