@@ -437,6 +437,8 @@ def run_ours(args):
         "unit": "TFLOP/s", "frac": dk["tflops"] / fp64_peak if fp64_peak > 0 else None,
         "frac_nominal": dk["tflops"] / nominal_peak, "nominal_peak": nominal_peak,
         "traffic": traffic.get(dom),
+        # what ncu shows to limit the kernel (profiles/, static: taken from the committed captures)
+        "ncu": (traffic.get("ncu") or {}).get("tangent rows" if dom == "tangent" else "residual_chunk_kernel"),
         "algorithmic": f"{CANON_TAN_FLOP if dom.startswith('tangent') else CANON_RES_FLOP} FP64 "
                        f"FLOP per (element, sample) x {ne}x{N}",
         "timing": "kernel alone, CUDA events on its stream, L2 flushed, mean of 5",
