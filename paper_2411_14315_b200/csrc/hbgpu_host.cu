@@ -71,6 +71,7 @@ struct Tooling {
     int tan_width = 0;          // HBGPU_TAN_WIDTH: force the tangent pipeline's CTA width
     bool gmres_host = false;    // HBGPU_GMRES_HOST: host-driven GMRES step loop
     int mv_lanes = 0;           // HBGPU_MV_LANES: 1 / 4 lanes per (row, sample) (0 = auto)
+    std::string solve_progress; // HBGPU_SOLVE_PROGRESS=path: one line per Newton iteration (long solves)
     static Tooling from_env() {
         Tooling t;
         auto num = [](const char* k) { const char* v = std::getenv(k); return v ? std::atoi(v) : 0; };
@@ -80,6 +81,8 @@ struct Tooling {
         t.tan_width = num("HBGPU_TAN_WIDTH");
         t.gmres_host = std::getenv("HBGPU_GMRES_HOST") != nullptr;
         t.mv_lanes = num("HBGPU_MV_LANES");
+        if (const char* sp = std::getenv("HBGPU_SOLVE_PROGRESS"))
+            t.solve_progress = sp;
         return t;
     }
 };
@@ -2091,6 +2094,12 @@ int hbgpu_solve_harmonic(hbgpu_ctx* c, const hbgpu_solver_cfg* cfg, double* stat
     Timer total;
     hbgpu_solve_info inf{};
     auto log = [&](int iter, double res, double rel, int lin, double sec) {
+        if (!c->tool.solve_progress.empty()) {  // tooling: the ConvergenceLog rows as they are produced
+            if (FILE* f = std::fopen(c->tool.solve_progress.c_str(), "a")) {
+                std::fprintf(f, "%d,%.17g,%.17g,%d,%.6f\n", iter, res, rel, lin, sec);
+                std::fclose(f);
+            }
+        }
         if (inf.entries < cap) {
             if (log_iter) log_iter[inf.entries] = iter;
             if (log_res) log_res[inf.entries] = res;
