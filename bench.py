@@ -533,7 +533,10 @@ def run_ours(args):
             solve[f"config{cfg}"] = solve_config(cfg)
         solve["notes"] = ("config 0: converged (CFL 10); config 1: converged at CFL 100; configs 2 and 3: "
                           "bounded runs — the reference's pseudo-time Newton does not converge on them within "
-                          "the explored budgets (profiles/r2_solve_exploration.jsonl, r2h_converged_solves.jsonl)")
+                          "the explored budgets (profiles/r2_solve_exploration.jsonl, r2h_converged_solves.jsonl); "
+                          "config 3 does converge, slowly, once the GMRES cap is 4000: res_rel 8.7e-3 after 19 Newton "
+                          "iterations / 1434 s at CFL 100, monotone, ~80 iterations / 1.6 h extrapolated to 3 orders "
+                          "(profiles/r3h_config3_cfl100_progress.csv)")
 
     cpu_baseline = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -778,6 +781,12 @@ def sweep_configs(args):
 #   config 3 (resistance outlet R = 1e4): CFL 0.3/1/3 reach res_rel 8.5/2.8/0.93
 #             after 8 iterations (the first steps exhaust the 1000-iteration GMRES
 #             budget); no convergence within 25 min at CFL 1 — bounded run reported.
+#             With the GMRES cap raised to 4000 (every step then uses all 4000, 72 s per
+#             Newton iteration) the residual falls monotonically: CFL 10 1.25e-2 after 39
+#             iterations (x0.92 per iteration, 2779 s), CFL 30 2.2e-2 after 19, CFL 100
+#             8.7e-3 after 19 (1434 s; x0.965 per iteration in the tail) — about 80
+#             iterations / 1.6 h to 3 orders (profiles/r3f_*, r3h_*: HBGPU_SOLVE_PROGRESS
+#             histories); too long for the default bench run.
 SOLVE_SETTINGS = {1: (100.0, 70), 2: (10.0, 40), 3: (3.0, 4)}
 
 
