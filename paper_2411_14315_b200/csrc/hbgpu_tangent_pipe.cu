@@ -148,6 +148,11 @@ constexpr int kRecStride = TAN_REC_STRIDE;
 #endif
 // the row node's velocity comes from the four gathered element nodes (local
 // slot 0 = the row node) instead of three more shared-memory loads
+// phase-1 items of the single-sample kernels mapped with 16-lane-aligned sample groups per
+// incidence (lanes past the last sample idle), so a half-warp never straddles incidences
+#ifndef TAN_P1_ALIGN
+#define TAN_P1_ALIGN 1
+#endif
 #ifndef TAN_UA_REUSE
 #define TAN_UA_REUSE 1
 #endif
@@ -174,10 +179,16 @@ __host__ __device__ constexpr int tan_pair(int NC) { return (NC >= 3 && NC <= TA
 // read once per G2 samples; consecutive lanes still take consecutive samples,
 // so summary loads and P stores stay contiguous per warp.  Phase 2 is bound by
 // shared-memory bandwidth (ncu r2p: 100% of the wavefront rate, FP64 pipe 31%).
+// G2 = ceil(N / 16): 16 lanes per slot, so a warp is exactly two slots (record loads are
+// two broadcasts, summary loads two 128-byte runs).  Config-4 tangent at N = 31: G2 = 1 /
+// 2 / 3 / 4 -> 21.0 / 18.2 / 22.0 / 22.2 ms (profiles/r3i_kbench_n31.log); at N = 47:
+// 31.6 (G2 = 1) / 29.3 / 27.5 / 33.6 ms (r2q).  TAN_G2 > 0 forces a value (A/B builds).
 #ifndef TAN_G2
-#define TAN_G2 3
+#define TAN_G2 0
 #endif
-__host__ __device__ constexpr int tan_grp(int NC) { return (NC >= TAN_GRP_MINN) ? TAN_G2 : 1; }
+__host__ __device__ constexpr int tan_grp(int NC) {
+    return (NC >= TAN_GRP_MINN) ? (TAN_G2 > 0 ? TAN_G2 : (NC + 15) / 16) : 1;
+}
 __host__ __device__ inline int tan_ntp(int NT, int P) { return (NT + P - 1) / P * P; }
 
 struct PipeSmem {
@@ -453,9 +464,18 @@ __global__ void __launch_bounds__(THREADS, 512 / THREADS) tangent_pipe_kernel(Ta
                     so[c * SC] = o[c][0];
             }
         };
-        for (int it = threadIdx.x, i = x_start, q = q_start; it < ninc * nq;
-             it += blockDim.x, q += dq, i += dx + (q >= nq), q -= (q >= nq ? nq : 0))
-            p1item(i, P * q);
+        if constexpr (TAN_P1_ALIGN && P == 1 && NC >= TAN_GRP_MINN) {  // (N = 1: 16x the loop trips)
+            const int nqa = (nq + 15) & ~15;
+            for (int it = threadIdx.x; it < ninc * nqa; it += blockDim.x) {
+                const int i = it / nqa, q = it - i * nqa;
+                if (q < nq)
+                    p1item(i, q);
+            }
+        } else {
+            for (int it = threadIdx.x, i = x_start, q = q_start; it < ninc * nq;
+                 it += blockDim.x, q += dq, i += dx + (q >= nq), q -= (q >= nq ? nq : 0))
+                p1item(i, P * q);
+        }
         if (bad_acc)
             atomicOr(a.flag, 1);
         __syncthreads();
